@@ -1,0 +1,205 @@
+/* hps_gpu.h — C ABI of the B200-native HBM-PS tier (libhps_gpu.so).
+ *
+ * This is the drop-in boundary for the reference parameter server's device
+ * tier (arXiv 2003.05622, reference `hps`, /root/reference/proj/include/hps).
+ * The reference binds this path in-process as the C++ class `hps::HbmTier`
+ * plus free functions; every entry point below names the reference interface
+ * it replaces (file:line). Plain pointers and sizes only; no torch types.
+ *
+ * Process model: one tier handle per GPU ("rank" = global device index
+ * g = device * nodes + node, topology.hpp:43-50). Calls marked COLLECTIVE
+ * must be made by every rank of the tier, in the same order (the reference's
+ * device-worker threads are phase-separated by barriers the same way,
+ * pipeline.hpp:529-558). Ranks exchange keys, rows, deltas and dense
+ * gradients over NCCL (NVLink/NVSwitch); a world of one needs no NCCL.
+ *
+ * Every function returns an hps_status; hps_last_error() returns the
+ * calling thread's message for the last failure. Messages for table misuse
+ * match the reference's hps::Error texts (device_table.hpp:52-91).
+ */
+#ifndef HPS_GPU_H
+#define HPS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPS_NCCL_ID_BYTES 128
+#define HPS_MAX_LAYERS 8
+
+typedef enum {
+  HPS_OK = 0,
+  HPS_ERR_ARG = 1,           /* invalid argument / config (config.hpp:86-108) */
+  HPS_ERR_MISSING_KEY = 2,   /* device_table.hpp:80-81, 90-91 */
+  HPS_ERR_DUPLICATE = 3,     /* device_table.hpp:56-57 */
+  HPS_ERR_OVERFLOW = 4,      /* device_table.hpp:61-62, 72 */
+  HPS_ERR_NONFINITE = 5,     /* model.hpp:70, 210 */
+  HPS_ERR_NOT_BUILT = 6,     /* hbm_ps.hpp:209 "hbm: tables not built" */
+  HPS_ERR_WIDTH = 7,         /* hbm_ps.hpp:95, 152 width mismatch */
+  HPS_ERR_KEY_RANGE = 8,     /* pipeline.hpp:367-371 ingest range check */
+  HPS_ERR_CUDA = 9,
+  HPS_ERR_NCCL = 10,
+  HPS_ERR_CAPACITY = 11      /* a batch larger than the configured maxima */
+} hps_status;
+
+typedef struct hps_tier* hps_tier_t;
+
+/* Run knobs, the subset of RunConfig (config.hpp:40-74) the HBM-PS path
+ * reads, plus buffer maxima so every device buffer is allocated once. */
+typedef struct {
+  int nodes;                 /* N, power of two (topology.hpp:31-37) */
+  int devices_per_node;      /* D, power of two */
+  int rank;                  /* this handle's global device index g */
+  int cuda_device;           /* CUDA ordinal this handle drives */
+  int embedding_dim;         /* E: row width in floats */
+  int num_layers;            /* dense stack depth, <= HPS_MAX_LAYERS */
+  uint64_t layer_dims[HPS_MAX_LAYERS]; /* must end in 1 (config.hpp:90-91) */
+  float learning_rate;       /* SGD lr (model.hpp:204-230) */
+  uint64_t seed;             /* init_dense seed (model.hpp:42-53) */
+  int minibatches;           /* J mini-batches per batch (config.hpp:52) */
+  int deterministic;         /* canonical-order reductions (config.hpp:67) */
+  int64_t inject_skip_sync;  /* global mini-batch whose dense sync+update is
+                                skipped, -1 = off (pipeline.hpp:550-555) */
+  uint64_t key_space;        /* keys are < key_space ("dims"); sizes sorts */
+  uint64_t max_batch_examples;  /* per batch */
+  uint64_t max_batch_keys;      /* key occurrences per batch */
+  uint64_t max_working_set;     /* keys per build() call, 0 = max_batch_keys */
+} hps_config;
+
+/* Per-batch result of hps_train_batch. */
+typedef struct {
+  double loss_sum;           /* sum of per-example log loss (model.hpp:232-242) */
+  uint64_t examples;         /* examples this rank trained */
+  uint64_t working_set;      /* keys this rank's table holds for the batch */
+  uint64_t table_capacity;   /* capacity of that table */
+  uint64_t pulled_keys;      /* sum over mini-batches of unique keys pulled */
+  uint64_t served_keys;      /* keys this rank served as owner (pull+push) */
+  uint64_t occurrences;      /* key occurrences in this rank's shards */
+} hps_batch_stats;
+
+const char* hps_last_error(void);
+const char* hps_version(void);
+
+/* ----------------------------------------------------------- lifecycle */
+
+/* ncclGetUniqueId for rank 0 to broadcast (only needed when N*D > 1). */
+hps_status hps_get_unique_id(uint8_t id[HPS_NCCL_ID_BYTES]);
+
+/* Replaces HbmTier::HbmTier (hbm_ps.hpp:45-56) with PartitionPolicy::modulo
+ * (topology.hpp:61-65) and replicate_dense(init_dense(cfg)) (hbm_ps.hpp:
+ * 244-247, model.hpp:42-53). COLLECTIVE when N*D > 1 (nccl_id required). */
+hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id,
+                      hps_tier_t* out);
+hps_status hps_destroy(hps_tier_t h);
+
+/* ------------------------------------------------ reference-facing API */
+
+/* HbmTier::build_node (hbm_ps.hpp:65-102): merge+sort+unique `keys` (any
+ * order, duplicates allowed — the node's working set plus peer keys), keep
+ * the keys this rank owns, build a fresh table (capacity next_pow2(4n/3),
+ * device_table.hpp:38-45) whose slot layout equals ascending-order linear
+ * probing, and fill each row from the previous table when the key was there
+ * (carry-over) else from `host_rows` (row i belongs to keys[i]; the
+ * HostValue callback's result, staged H2D with cudaMemcpyAsync) or, when
+ * host_rows is NULL, from the attached value store (zero if none). */
+hps_status hps_build(hps_tier_t h, const uint64_t* keys, uint64_t n,
+                     const float* host_rows);
+
+/* HbmTier::get (hbm_ps.hpp:112-143). COLLECTIVE. Rows for `keys` (host
+ * array, any order) written to out_rows (n x E, aligned with keys). Keys
+ * owned by other ranks travel as pull request/response all-to-alls. */
+hps_status hps_pull(hps_tier_t h, const uint64_t* keys, uint64_t n,
+                    float* out_rows);
+
+/* HbmTier::push_deltas (hbm_ps.hpp:148-167). COLLECTIVE. Ships each delta
+ * row to its owner, where it is queued (nothing applied yet). */
+hps_status hps_push(hps_tier_t h, const uint64_t* keys, const float* deltas,
+                    uint64_t n);
+
+/* HbmTier::drain_accums (hbm_ps.hpp:172-195): apply every queued delta,
+ * senders in canonical node-major/device-major order, v += d in f32
+ * (device_table.hpp:88-95). Local to the rank. */
+hps_status hps_drain(hps_tier_t h);
+
+/* HbmTier::dump_node (hbm_ps.hpp:224-232) for this rank's table: keys in
+ * ascending order and their rows. *n_out = occupancy. Buffers sized by
+ * hps_table_info's occupancy. */
+hps_status hps_dump(hps_tier_t h, uint64_t* keys_out, float* rows_out,
+                    uint64_t* n_out);
+
+/* DeviceTable::capacity/occupancy/value_width (device_table.hpp:47-49). */
+hps_status hps_table_info(hps_tier_t h, uint64_t* capacity,
+                          uint64_t* occupancy, uint64_t* width);
+/* Slot-level view for placement parity: slot_keys[capacity] (empty slots
+ * hold ~0, device_table.hpp:34) and, if non-NULL, rows[capacity x E]. */
+hps_status hps_table_slots(hps_tier_t h, uint64_t* slot_keys, float* rows);
+
+/* SyncSession::run (hbm_ps.hpp:303-310) on a host buffer. COLLECTIVE.
+ * Every rank ends with the elementwise sum of all ranks' buffers:
+ * deterministic = f64 canonical_sum of the raw buffers (hbm_ps.hpp:
+ * 258-277, 349-394), else an f32 all-reduce. */
+hps_status hps_dense_sync(hps_tier_t h, float* buf, uint64_t len,
+                          int deterministic);
+
+/* Dense replica access (DenseParams::weights, types.hpp:41-60). */
+hps_status hps_dense_count(hps_tier_t h, uint64_t* n);
+hps_status hps_get_dense(hps_tier_t h, float* w);
+hps_status hps_set_dense(hps_tier_t h, const float* w);
+
+/* ------------------------------------------------- performance API */
+
+/* Attach the host-tier value store (the MEM-PS stand-in): rows[key * E]
+ * for key < num_keys. build() fills rows of keys that were not in the
+ * previous table from it, and hps_train_batch writes the trained rows back
+ * after each batch (dump_node -> MemPs::collect_updates, pipeline.hpp:
+ * 441-445, mem_ps.hpp:210-245). on_device = 0: pinned host memory reached
+ * with zero-copy gather/scatter kernels; 1: an HBM array. */
+hps_status hps_attach_store(hps_tier_t h, float* rows, uint64_t num_keys,
+                            int on_device);
+
+/* One whole batch through the tier, device-resident: working-set dedup ->
+ * build (carry-over + store staging) -> J x {mini-batch dedup, pull
+ * all-to-all, forward/backward, sparse segment-reduce + sgd_delta, push
+ * all-to-all, canonical apply, dense sync + update} -> write-back to the
+ * store. The batch is the full node batch in CSR form (every rank passes the
+ * same batch, as each node's train stage holds it, pipeline.hpp:417-460);
+ * this rank trains shard_batch's slice (sharding.hpp:29-42). COLLECTIVE.
+ * on_device = 0: offsets/keys/labels are host (pinned for speed) pointers,
+ * copied H2D inside the call; 1: device pointers. stats may be NULL. */
+hps_status hps_train_batch(hps_tier_t h, uint64_t num_examples,
+                           const int64_t* offsets, const uint64_t* keys,
+                           const uint8_t* labels, int on_device,
+                           hps_batch_stats* stats);
+
+/* Kernel-level timing of the last hps_train_batch, from CUDA events on the
+ * tier's stream (ms): [0] whole batch, [1] working set + build, [2] pull
+ * (owner probe+gather incl. exchange), [3] push apply, [4] write-back,
+ * [5] mini-batch dedup, [6] fwd/bwd + reductions, [7] dense sync.
+ * Enabled by hps_set_timing(h, 1) (adds event records, no syncs). */
+hps_status hps_set_timing(hps_tier_t h, int enable);
+hps_status hps_get_timing(hps_tier_t h, double* ms8);
+
+/* Number of kernels this library launched on the handle so far. */
+hps_status hps_kernel_launches(hps_tier_t h, uint64_t* n);
+
+/* The CUDA stream the handle launches on (cudaStream_t as void*). */
+hps_status hps_stream(hps_tier_t h, void** stream);
+
+/* -------------------------------------------------- synthetic inputs */
+
+/* The reference generator gen_dataset (dataset.hpp:180-227) restated
+ * byte-for-byte (mt19937_64 stream, planted logistic labels, inverse-CDF
+ * Zipf, sorted unique features). offsets[num_examples+1], keys[n*nnz],
+ * labels[n]. Host-only, needs no GPU. */
+hps_status hps_gen_dataset(uint64_t dims, uint64_t num_examples, uint64_t nnz,
+                           int zipf, double zipf_s, uint64_t seed,
+                           double signal_scale, uint64_t clusters,
+                           int64_t* offsets, uint64_t* keys, uint8_t* labels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPS_GPU_H */

@@ -1,0 +1,244 @@
+// HBM-resident open-addressing table of one rank (the DeviceTable of
+// device_table.hpp:32-137, rebuilt per batch by HbmTier::build_node,
+// hbm_ps.hpp:65-102).
+//
+// Layout: keys u64[cap] (EMPTY = ~0) and rows f32[cap][E] (row-major, E
+// contiguous, 16-B aligned when E % 4 == 0). The capacity lives in device
+// memory (it depends on the working-set size the GPU just computed).
+//
+// Build is history-independent "ordered linear probing": each key walks its
+// probe sequence doing 64-bit atomicMin; a smaller key takes the slot and
+// the displaced larger key continues from the next slot. The fixpoint is
+// the layout the reference produces by inserting keys in ascending order
+// (hbm_ps.hpp:89-98): every key ends at the first slot of its probe
+// sequence not held by a smaller key. Rows are filled afterwards (atomics
+// cannot carry the value).
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace hpsgpu {
+
+__global__ void table_clear_kernel(std::uint64_t* __restrict__ keys,
+                                   const std::uint64_t* __restrict__ cap_ptr) {
+  const std::uint64_t cap = *cap_ptr;
+  for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       i < cap; i += std::uint64_t(gridDim.x) * blockDim.x)
+    keys[i] = kEmptyKey;
+}
+
+__global__ void table_capacity_kernel(const std::uint64_t* __restrict__ n_ptr,
+                                      std::uint64_t* __restrict__ cap_ptr) {
+  *cap_ptr = table_capacity(*n_ptr);
+}
+
+// device_table.hpp:51-73 semantics (duplicate / overflow are errors).
+__global__ void table_insert_kernel(const std::uint64_t* __restrict__ ws,
+                                    const std::uint64_t* __restrict__ n_ptr,
+                                    std::uint64_t* __restrict__ keys,
+                                    const std::uint64_t* __restrict__ cap_ptr,
+                                    DevError* err) {
+  const std::uint64_t n = *n_ptr, cap = *cap_ptr;
+  for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       i < n; i += std::uint64_t(gridDim.x) * blockDim.x) {
+    std::uint64_t cur = ws[i];
+    if (cur == kEmptyKey) {
+      raise_error(err, 1 /*HPS_ERR_ARG: reserved key*/, cur);
+      continue;
+    }
+    std::uint64_t idx = mix64(cur) & (cap - 1);
+    std::uint64_t probes = 0;
+    for (;;) {
+      const std::uint64_t old = atomicMin(
+          reinterpret_cast<unsigned long long*>(keys + idx),
+          static_cast<unsigned long long>(cur));
+      if (old == kEmptyKey) break;
+      if (old == cur) {
+        raise_error(err, 3 /*HPS_ERR_DUPLICATE*/, cur);
+        break;
+      }
+      if (old > cur) cur = old;  // displaced: carry the larger key onward
+      idx = (idx + 1) & (cap - 1);
+      if (++probes > cap) {
+        raise_error(err, 4 /*HPS_ERR_OVERFLOW*/, cur);
+        break;
+      }
+    }
+  }
+}
+
+// Row fill for the fresh table (hbm_ps.hpp:86-98): carry-over from the
+// previous table when the key was resident, else the staged host row
+// (HostValue), else the attached value store, else zeros. VEC floats per
+// thread, E/VEC threads per key; every thread of a key's group probes (the
+// loads coalesce into one transaction).
+template <int VEC>
+__global__ void table_fill_kernel(
+    const std::uint64_t* __restrict__ ws, const std::uint64_t* __restrict__ n_ptr,
+    const std::uint64_t* __restrict__ keys, float* __restrict__ vals,
+    const std::uint64_t* __restrict__ cap_ptr,
+    const std::uint64_t* __restrict__ prev_keys,
+    const float* __restrict__ prev_vals,
+    const std::uint64_t* __restrict__ prev_cap_ptr,  // null: no previous table
+    const std::uint32_t* __restrict__ staged_idx,    // null: no staged rows
+    const float* __restrict__ staged_rows,
+    const float* __restrict__ store, std::uint64_t store_keys, int E,
+    DevError* err) {
+  const int tpk = E / VEC;
+  const std::uint64_t n = *n_ptr, cap = *cap_ptr;
+  const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
+  const std::uint64_t total = n * std::uint64_t(tpk);
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < total; t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    const std::uint64_t key = ws[i];
+    const std::uint32_t slot = probe_slot(keys, cap, key);
+    if (slot == kNoSlot) {
+      raise_error(err, 2, key);
+      continue;
+    }
+    const float* src = nullptr;
+    if (pcap) {
+      const std::uint32_t ps = probe_slot(prev_keys, pcap, key);
+      if (ps != kNoSlot) src = prev_vals + std::uint64_t(ps) * E;
+    }
+    if (!src && staged_rows) src = staged_rows + std::uint64_t(staged_idx[i]) * E;
+    if (!src && store && key < store_keys) src = store + key * std::uint64_t(E);
+    float* dst = vals + std::uint64_t(slot) * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, src ? ld_f4(src + part * 4) : make_float4(0.f, 0.f, 0.f, 0.f));
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) dst[v] = src ? src[part * VEC + v] : 0.0f;
+    }
+  }
+}
+
+// Pull gather (DeviceTable::get, device_table.hpp:78-85): probe each query
+// key, cache its slot for the push, copy the row. Missing key -> error.
+template <int VEC>
+__global__ void table_gather_kernel(const std::uint64_t* __restrict__ qkeys,
+                                    const std::uint64_t* __restrict__ n_ptr,
+                                    std::uint64_t n_host, const std::uint64_t* __restrict__ keys,
+                                    const float* __restrict__ vals,
+                                    const std::uint64_t* __restrict__ cap_ptr,
+                                    float* __restrict__ out_rows,
+                                    std::uint32_t* __restrict__ out_slots,
+                                    int E, DevError* err) {
+  const int tpk = E / VEC;
+  const std::uint64_t n = n_ptr ? *n_ptr : n_host;
+  const std::uint64_t cap = *cap_ptr;
+  const std::uint64_t total = n * std::uint64_t(tpk);
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < total; t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    const std::uint64_t key = qkeys[i];
+    const std::uint32_t slot = probe_slot(keys, cap, key);
+    if (slot == kNoSlot) {
+      raise_error(err, 2, key);
+      continue;
+    }
+    if (out_slots && part == 0) out_slots[i] = slot;
+    const float* src = vals + std::uint64_t(slot) * E + part * VEC;
+    float* dst = out_rows + i * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, ld_f4(src));
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) dst[v] = src[v];
+    }
+  }
+}
+
+// Owner apply of one sender's segment (device_table.hpp:88-95): v += d in
+// f32, no contraction. Keys inside one segment are unique, so no atomics;
+// segments are launched in canonical sender order (hbm_ps.hpp:172-195).
+// slots == null: probe `qkeys` instead of using cached slots.
+template <int VEC>
+__global__ void table_apply_kernel(const std::uint32_t* __restrict__ slots,
+                                   const std::uint64_t* __restrict__ qkeys,
+                                   const std::uint64_t* __restrict__ tkeys,
+                                   const std::uint64_t* __restrict__ cap_ptr,
+                                   const float* __restrict__ deltas,
+                                   const std::uint64_t* __restrict__ n_ptr,
+                                   std::uint64_t n_host, float* __restrict__ vals,
+                                   int E, DevError* err) {
+  const int tpk = E / VEC;
+  const std::uint64_t n = n_ptr ? *n_ptr : n_host;
+  const std::uint64_t total = n * std::uint64_t(tpk);
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < total; t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    std::uint32_t slot;
+    if (slots) {
+      slot = slots[i];
+    } else {
+      slot = probe_slot(tkeys, *cap_ptr, qkeys[i]);
+      if (slot == kNoSlot) {
+        raise_error(err, 2, qkeys[i]);
+        continue;
+      }
+    }
+    float* v = vals + std::uint64_t(slot) * E + part * VEC;
+    const float* d = deltas + i * E + part * VEC;
+    if (VEC == 4) {
+      float4 a = ld_f4(v);
+      const float4 b = ld_f4(d);
+      a.x = __fadd_rn(a.x, b.x);
+      a.y = __fadd_rn(a.y, b.y);
+      a.z = __fadd_rn(a.z, b.z);
+      a.w = __fadd_rn(a.w, b.w);
+      st_f4(v, a);
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) v[q] = __fadd_rn(v[q], d[q]);
+    }
+  }
+}
+
+// Write-back of the batch's rows to the value store (dump_node ->
+// collect_updates, hbm_ps.hpp:224-232, mem_ps.hpp:210-245) and/or to a
+// dense (keys, rows) dump in working-set (= ascending key) order.
+template <int VEC>
+__global__ void table_dump_kernel(const std::uint64_t* __restrict__ ws,
+                                  const std::uint64_t* __restrict__ n_ptr,
+                                  const std::uint64_t* __restrict__ keys,
+                                  const float* __restrict__ vals,
+                                  const std::uint64_t* __restrict__ cap_ptr,
+                                  float* __restrict__ store, std::uint64_t store_keys,
+                                  float* __restrict__ out_rows, int E,
+                                  DevError* err) {
+  const int tpk = E / VEC;
+  const std::uint64_t n = *n_ptr, cap = *cap_ptr;
+  const std::uint64_t total = n * std::uint64_t(tpk);
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < total; t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    const std::uint64_t key = ws[i];
+    const std::uint32_t slot = probe_slot(keys, cap, key);
+    if (slot == kNoSlot) {
+      raise_error(err, 2, key);
+      continue;
+    }
+    const float* src = vals + std::uint64_t(slot) * E + part * VEC;
+    if (VEC == 4) {
+      const float4 r = ld_f4(src);
+      if (store && key < store_keys) st_f4(store + key * E + part * 4, r);
+      if (out_rows) st_f4(out_rows + i * E + part * 4, r);
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        if (store && key < store_keys) store[key * E + part * VEC + q] = src[q];
+        if (out_rows) out_rows[i * E + part * VEC + q] = src[q];
+      }
+    }
+  }
+}
+
+}  // namespace hpsgpu

@@ -1,0 +1,1459 @@
+// libhps_gpu.so — the B200-native HBM-PS tier behind the C ABI of
+// include/hps_gpu.h. One handle per GPU (rank g of G = nodes * devices).
+//
+// Per batch (hps_train_batch), all on the handle's stream:
+//   batch_count  -> one D2H of the per-mini-batch occurrence counts
+//   working set  -> radix sort + unique of the rank's owned keys (a1, a2)
+//   build        -> capacity, clear, ordered-probing insert, row fill with
+//                   carry-over / store staging (a3, a4)
+//   J x mini-batch:
+//     shard gather, radix sort (key, occurrence), unique -> inverse index
+//     and CSR segments (a5); [G>1: stable owner partition, count
+//     all-gather, key all-to-all]; owner probe+gather (a6) [G>1: row
+//     all-to-all]; fwd/bwd (a7, a8); dense-grad reduce; sparse
+//     segment-reduce + sgd_delta (a8, a9) [G>1: delta all-to-all (a10)];
+//     canonical owner apply (a11); dense sync + update (a12)
+//   write-back   -> rows to the value store (a13)
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "hps_gpu.h"
+#include "model.cuh"
+#include "sort.cuh"
+#include "table.cuh"
+#include "tier_internal.h"
+
+namespace hpsgpu {
+
+thread_local std::string t_err;
+void set_error_message(const std::string& m) { t_err = m; }
+const char* error_message() { return t_err.c_str(); }
+
+// ------------------------------------------------------------- NCCL ----
+// Loaded with dlopen so the library (and the CPU test suite) does not need
+// NCCL unless a tier spans more than one GPU; inside a torch process this
+// resolves to the NCCL torch already loaded.
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t,
+                            ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t,
+                            ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) {
+      a.why = "cannot dlopen libnccl.so.2";
+      return a;
+    }
+#define HPS_SYM(field, name)                                            \
+  a.field = reinterpret_cast<decltype(a.field)>(dlsym(lib, name));      \
+  if (!a.field) {                                                       \
+    a.why = std::string("missing NCCL symbol ") + name;                 \
+    return a;                                                           \
+  }
+    HPS_SYM(GetUniqueId, "ncclGetUniqueId");
+    HPS_SYM(CommInitRank, "ncclCommInitRank");
+    HPS_SYM(CommDestroy, "ncclCommDestroy");
+    HPS_SYM(GroupStart, "ncclGroupStart");
+    HPS_SYM(GroupEnd, "ncclGroupEnd");
+    HPS_SYM(Send, "ncclSend");
+    HPS_SYM(Recv, "ncclRecv");
+    HPS_SYM(AllGather, "ncclAllGather");
+    HPS_SYM(AllReduce, "ncclAllReduce");
+    HPS_SYM(GetErrorString, "ncclGetErrorString");
+#undef HPS_SYM
+    a.ok = true;
+    return a;
+  }();
+  return api;
+}
+
+// --------------------------------------------------------- the tier ----
+
+struct Scalars {
+  std::uint64_t n_ws;          // working-set size of the current build
+  std::uint64_t cap[2];        // capacity of table 0 / 1
+  std::uint64_t nws_tab[2];    // occupancy of table 0 / 1
+  std::uint64_t U;             // unique keys of the current mini-batch / pull
+  std::uint64_t total;         // scratch total of a tile scan
+  std::uint64_t counts[66];    // batch_count: per-mb occurrences, owned keys
+  std::uint64_t send_off[257]; // owner partition offsets (G+1)
+  double loss;
+  DevError err;
+};
+
+struct PendingChunk {
+  int src;
+  std::uint64_t n;
+  std::uint64_t* keys;
+  float* deltas;
+};
+
+struct Tier {
+  hps_config cfg{};
+  int N = 1, D = 1, G = 1, g = 0, E = 1, J = 1;
+  ModelDims md{};
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = nullptr;
+  std::uint64_t Bmax = 0, Omax = 0, Wmax = 0, capmax = 0, nmb_max = 0;
+  int sort_bits = 64;
+  std::uint64_t launches = 0;
+  std::int64_t step = 0;  // batches trained (global mini-batch = step*J + j)
+
+  Scalars* dsc = nullptr;  // device
+  Scalars* hsc = nullptr;  // pinned host mirror
+
+  // tables (double-buffered: current + previous for carry-over)
+  std::uint64_t* tkeys[2] = {nullptr, nullptr};
+  float* tvals[2] = {nullptr, nullptr};
+  int cur = -1;
+  bool has_prev = false;
+
+  // working set
+  std::uint64_t* ws = nullptr;
+  std::uint32_t* ws_idx = nullptr;
+
+  // sort scratch
+  std::uint64_t *kA = nullptr, *kB = nullptr;
+  std::uint32_t *vA = nullptr, *vB = nullptr;
+  std::uint32_t* hist = nullptr;
+  std::uint32_t* bsum = nullptr;
+  std::uint64_t hist_len = 0, bsum_len = 0;
+
+  // batch staging
+  std::int64_t* b_off = nullptr;
+  std::uint64_t* b_keys = nullptr;
+  std::uint8_t* b_lab = nullptr;
+
+  // mini-batch / pull buffers (sized Omax)
+  std::uint32_t *occ_off = nullptr, *ex_of = nullptr, *inv = nullptr,
+                *seg = nullptr, *uidv = nullptr, *pos = nullptr,
+                *occ_row = nullptr, *slots = nullptr, *rslots = nullptr,
+                *puid = nullptr, *cnt32 = nullptr, *cnt_all = nullptr;
+  std::uint64_t *ukeys = nullptr, *pkeys = nullptr, *rkeys = nullptr;
+  float *rows = nullptr, *deltas = nullptr, *rrows = nullptr,
+        *rdeltas = nullptr, *staged = nullptr;
+  std::uint64_t staged_cap = 0;
+
+  // model
+  double *H = nullptr, *DL = nullptr, *DX = nullptr;
+  float *dense = nullptr, *dgrad = nullptr, *dgather = nullptr;
+
+  // value store (MEM-PS stand-in)
+  float* store = nullptr;
+  std::uint64_t store_keys = 0;
+  bool store_registered = false;
+  float* store_host = nullptr;
+
+  std::vector<PendingChunk> pending;
+
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[16] = {};
+  double acc_ms[8] = {0};
+
+  std::vector<void*> allocs;
+};
+
+// ----------------------------------------------------------- helpers ----
+
+#define HPS_CUDA(call)                                                      \
+  do {                                                                      \
+    cudaError_t e_ = (call);                                                \
+    if (e_ != cudaSuccess)                                                  \
+      return set_error(HPS_ERR_CUDA, "cuda: %s at %s:%d", cudaGetErrorString(e_), \
+                       __FILE__, __LINE__);                                 \
+  } while (0)
+
+#define HPS_TRY(expr)                  \
+  do {                                 \
+    hps_status s_ = (expr);            \
+    if (s_ != HPS_OK) return s_;       \
+  } while (0)
+
+#define HPS_NCCL(call)                                                     \
+  do {                                                                     \
+    ncclResult_t r_ = (call);                                              \
+    if (r_ != ncclSuccess)                                                 \
+      return set_error(HPS_ERR_NCCL, "nccl: %s at %s:%d",                  \
+                       nccl().GetErrorString(r_), __FILE__, __LINE__);     \
+  } while (0)
+
+template <class T>
+static hps_status dalloc(Tier* t, T** p, std::uint64_t count) {
+  void* q = nullptr;
+  const std::uint64_t bytes = std::max<std::uint64_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess)
+    return set_error(HPS_ERR_CUDA, "cuda: cudaMalloc(%llu B): %s",
+                     (unsigned long long)bytes, cudaGetErrorString(e));
+  t->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return HPS_OK;
+}
+
+static unsigned grid_for(std::uint64_t work, int threads = 256,
+                         unsigned cap = kSMs * 16) {
+  const std::uint64_t b = (work + threads - 1) / threads;
+  return unsigned(std::max<std::uint64_t>(1, std::min<std::uint64_t>(b, cap)));
+}
+
+template <class... KArgs, class... Args>
+static void launch(Tier* t, void (*k)(KArgs...), dim3 grid, dim3 block,
+                   size_t smem, Args&&... args) {
+  k<<<grid, block, smem, t->st>>>(std::forward<Args>(args)...);
+  ++t->launches;
+}
+
+static const char* missing_msg_context = "device table: missing key ";
+
+// Maps the device error word to the reference's hps::Error texts.
+static hps_status check_device_error(Tier* t, const char* missing_ctx) {
+  HPS_CUDA(cudaMemcpyAsync(&t->hsc->err, &t->dsc->err, sizeof(DevError),
+                           cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  const DevError e = t->hsc->err;
+  if (e.code == 0) return HPS_OK;
+  HPS_CUDA(cudaMemsetAsync(&t->dsc->err, 0, sizeof(DevError), t->st));
+  const unsigned long long k = e.key;
+  switch (e.code) {
+    case HPS_ERR_MISSING_KEY:
+      return set_error(HPS_ERR_MISSING_KEY, "%s%llu", missing_ctx, k);
+    case HPS_ERR_DUPLICATE:
+      return set_error(HPS_ERR_DUPLICATE,
+                       "device table: duplicate insert of key %llu", k);
+    case HPS_ERR_OVERFLOW:
+      return set_error(HPS_ERR_OVERFLOW,
+                       "device table: capacity overflow (sizing bug)");
+    case HPS_ERR_NONFINITE:
+      return set_error(HPS_ERR_NONFINITE, "model: non-finite value");
+    case HPS_ERR_KEY_RANGE:
+      return set_error(HPS_ERR_KEY_RANGE,
+                       "ingest: feature key %llu out of range for dims=%llu",
+                       k, (unsigned long long)t->cfg.key_space);
+    case HPS_ERR_ARG:
+      return set_error(HPS_ERR_ARG, "device table: reserved key");
+    default:
+      return set_error(HPS_ERR_ARG, "device error %d (key %llu)", e.code, k);
+  }
+}
+
+// ------------------------------------------------------ small kernels ----
+
+__global__ void iota_kernel(std::uint32_t* v, std::uint64_t n) {
+  for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       i < n; i += std::uint64_t(gridDim.x) * blockDim.x)
+    v[i] = std::uint32_t(i);
+}
+
+// Per-mini-batch occurrence counts of this rank's shards and the count of
+// keys it owns; range check of every key (pipeline.hpp:367-371).
+__global__ void batch_count_kernel(const std::int64_t* __restrict__ off,
+                                   const std::uint64_t* __restrict__ keys,
+                                   std::uint64_t B, int G, int g, int J,
+                                   std::uint64_t key_space,
+                                   std::uint64_t* __restrict__ counts,
+                                   DevError* err) {
+  __shared__ unsigned long long c[66];
+  for (int i = threadIdx.x; i <= J; i += blockDim.x) c[i] = 0;
+  __syncthreads();
+  const std::uint64_t GJ = std::uint64_t(G) * J;
+  const std::uint64_t tid = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+  const std::uint64_t nth = std::uint64_t(gridDim.x) * blockDim.x;
+  for (std::uint64_t i = tid; i < B; i += nth) {
+    const std::uint64_t s = i % GJ;
+    if (s / J == std::uint64_t(g))
+      atomicAdd(&c[s % J], (unsigned long long)(off[i + 1] - off[i]));
+  }
+  const std::uint64_t O = std::uint64_t(off[B]);
+  unsigned long long own = 0;
+  for (std::uint64_t q = tid; q < O; q += nth) {
+    const std::uint64_t k = keys[q];
+    if (k >= key_space) raise_error(err, HPS_ERR_KEY_RANGE, k);
+    own += (k % std::uint64_t(G)) == std::uint64_t(g);
+  }
+  atomicAdd(&c[J], own);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= J; i += blockDim.x)
+    if (c[i]) atomicAdd((unsigned long long*)&counts[i], c[i]);
+}
+
+// Shard occurrence gather: warp per shard example, occurrences numbered in
+// example order (the order model.hpp sums in).
+__global__ void shard_gather_kernel(ShardMap sm, const std::int64_t* __restrict__ off,
+                                    const std::uint64_t* __restrict__ keys,
+                                    const std::uint32_t* __restrict__ occ_off,
+                                    std::uint64_t* __restrict__ kout,
+                                    std::uint32_t* __restrict__ vout,
+                                    std::uint32_t* __restrict__ ex_of) {
+  const unsigned lane = threadIdx.x & 31;
+  const std::uint64_t w0 = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const std::uint64_t nw = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (std::uint64_t k = w0; k < sm.count; k += nw) {
+    const std::uint64_t ex = sm.first + k * sm.stride;
+    const std::int64_t b = off[ex], len = off[ex + 1] - b;
+    const std::uint32_t o0 = occ_off[k];
+    for (std::int64_t q = lane; q < len; q += 32) {
+      kout[o0 + q] = keys[b + q];
+      vout[o0 + q] = std::uint32_t(o0 + q);
+      ex_of[o0 + q] = std::uint32_t(k);
+    }
+  }
+}
+
+__global__ void pos_kernel(const std::uint32_t* __restrict__ puid,
+                           const std::uint64_t* __restrict__ u_ptr,
+                           std::uint32_t* __restrict__ pos) {
+  const std::uint64_t U = *u_ptr;
+  for (std::uint64_t p = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       p < U; p += std::uint64_t(gridDim.x) * blockDim.x)
+    pos[puid[p]] = std::uint32_t(p);
+}
+
+__global__ void occ_row_kernel(const std::uint32_t* __restrict__ inv,
+                               const std::uint32_t* __restrict__ pos,
+                               std::uint64_t n, std::uint32_t* __restrict__ out) {
+  for (std::uint64_t o = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       o < n; o += std::uint64_t(gridDim.x) * blockDim.x)
+    out[o] = pos[inv[o]];
+}
+
+// Owner partition offsets from the scanned digit-major histogram of the
+// ModDigit pass: send_off[o] = first position of owner o; per-owner counts
+// as u32 for the count all-gather.
+__global__ void owner_offsets_kernel(const std::uint32_t* __restrict__ hist,
+                                     std::uint32_t nblocks, int G,
+                                     const std::uint64_t* __restrict__ u_ptr,
+                                     std::uint64_t* __restrict__ send_off,
+                                     std::uint32_t* __restrict__ cnt32) {
+  const int o = threadIdx.x;
+  const std::uint64_t U = *u_ptr;
+  if (o <= G) {
+    const std::uint64_t a = (o < G && U) ? hist[std::uint64_t(o) * nblocks] : U;
+    send_off[o] = a;
+  }
+  __syncthreads();
+  if (o < G) cnt32[o] = std::uint32_t(send_off[o + 1] - send_off[o]);
+}
+
+// out[i] = rows[row_of(i)] for the parity pull (restores input order).
+__global__ void scatter_rows_kernel(const std::uint32_t* __restrict__ inv,
+                                    const std::uint32_t* __restrict__ pos,
+                                    std::uint64_t n, int E,
+                                    const float* __restrict__ rows,
+                                    float* __restrict__ out) {
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < n * E; t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / E;
+    const int d = int(t - i * E);
+    std::uint32_t r = inv[i];
+    if (pos) r = pos[r];
+    out[t] = rows[std::uint64_t(r) * E + d];
+  }
+}
+
+// deltas given per input key -> send order (parity push)
+__global__ void permute_rows_kernel(const std::uint32_t* __restrict__ inv,
+                                    const std::uint32_t* __restrict__ pos,
+                                    std::uint64_t n, int E,
+                                    const float* __restrict__ in,
+                                    float* __restrict__ out) {
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < n * E; t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / E;
+    const int d = int(t - i * E);
+    std::uint32_t r = inv[i];
+    if (pos) r = pos[r];
+    out[std::uint64_t(r) * E + d] = in[t];
+  }
+}
+
+// ---------------------------------------------------- scan functors ----
+
+struct ShardLen {
+  ShardMap sm;
+  const std::int64_t* off;
+  __device__ std::uint32_t operator()(std::uint64_t k) const {
+    const std::uint64_t ex = sm.first + k * sm.stride;
+    return std::uint32_t(off[ex + 1] - off[ex]);
+  }
+};
+struct ShardLenEmit {
+  std::uint32_t* occ_off;
+  std::uint64_t n;
+  __device__ void operator()(std::uint64_t k, std::uint32_t v, std::uint64_t pre) const {
+    occ_off[k] = std::uint32_t(pre);
+    if (k + 1 == n) occ_off[n] = std::uint32_t(pre + v);
+  }
+};
+
+struct RunStart {  // first element of a run of equal keys
+  const std::uint64_t* sk;
+  __device__ std::uint32_t operator()(std::uint64_t p) const {
+    return p == 0 || sk[p] != sk[p - 1];
+  }
+};
+struct RunStartOwned {  // first of run and owned by rank g
+  const std::uint64_t* sk;
+  std::uint64_t G, g;
+  __device__ std::uint32_t operator()(std::uint64_t p) const {
+    return (p == 0 || sk[p] != sk[p - 1]) && (sk[p] % G == g);
+  }
+};
+struct OwnedKey {
+  const std::uint64_t* k;
+  std::uint64_t G, g;
+  __device__ std::uint32_t operator()(std::uint64_t q) const {
+    return k[q] % G == g;
+  }
+};
+struct CompactEmit {  // out[pre] = key (and index) for selected items
+  const std::uint64_t* sk;
+  const std::uint32_t* so;  // may be null
+  std::uint64_t* out;
+  std::uint32_t* out_idx;   // may be null
+  __device__ void operator()(std::uint64_t p, std::uint32_t v, std::uint64_t pre) const {
+    if (v) {
+      out[pre] = sk[p];
+      if (out_idx) out_idx[pre] = so ? so[p] : std::uint32_t(p);
+    }
+  }
+};
+struct UniqueEmit {  // inverse index + CSR segments of a sorted (key, occ) list
+  const std::uint64_t* sk;
+  const std::uint32_t* so;
+  std::uint64_t n;
+  std::uint32_t* inv;
+  std::uint64_t* ukeys;
+  std::uint32_t* seg;
+  std::uint32_t* uidv;
+  __device__ void operator()(std::uint64_t p, std::uint32_t v, std::uint64_t pre) const {
+    const std::uint64_t uid = pre + v - 1;
+    inv[so[p]] = std::uint32_t(uid);
+    if (v) {
+      ukeys[uid] = sk[p];
+      seg[uid] = std::uint32_t(p);
+      uidv[uid] = std::uint32_t(uid);
+    }
+    if (p + 1 == n) seg[uid + 1] = std::uint32_t(n);
+  }
+};
+
+// --------------------------------------------------- sort / scan drivers
+
+template <class F, class Em>
+static void tile_scan(Tier* t, F f, Em em, Count n, std::uint64_t n_upper,
+                      std::uint64_t* total) {
+  const std::uint32_t nb = tiles_for(std::max<std::uint64_t>(n_upper, 1));
+  launch(t, tile_reduce_kernel<F>, nb, kSortThreads, 0, f, n, t->bsum);
+  launch(t, scan_single_cta_kernel, 1, 1024, 0, t->bsum, std::uint64_t(nb), total);
+  launch(t, tile_emit_kernel<F, Em>, nb, kSortThreads, 0, f, em, n,
+         (const std::uint32_t*)t->bsum);
+}
+
+// Stable LSD sort of n (<= n_upper) items over the low `bits` bits. Input
+// (kin, vin) may alias kB/vB. Result returned through (kout, vout).
+static void radix_sort(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
+                       Count n, std::uint64_t n_upper, int bits, bool values,
+                       std::uint64_t** kout, std::uint32_t** vout) {
+  const std::uint32_t nb = tiles_for(std::max<std::uint64_t>(n_upper, 1));
+  const int passes = std::max(1, (bits + 7) / 8);
+  const std::uint64_t* ksrc = kin;
+  const std::uint32_t* vsrc = vin;
+  std::uint64_t* kd = t->kA;
+  std::uint32_t* vd = t->vA;
+  for (int p = 0; p < passes; ++p) {
+    ShiftDigit dig{8 * p};
+    launch(t, radix_hist_kernel<ShiftDigit>, nb, kSortThreads, 0, ksrc, n, dig,
+           t->hist, nb);
+    launch(t, scan_single_cta_kernel, 1, 1024, 0, t->hist,
+           std::uint64_t(kDigits) * nb, (std::uint64_t*)nullptr);
+    if (values)
+      launch(t, radix_scatter_kernel<ShiftDigit, true>, nb, kSortThreads, 0, ksrc,
+             vsrc, n, dig, (const std::uint32_t*)t->hist, nb, kd, vd);
+    else
+      launch(t, radix_scatter_kernel<ShiftDigit, false>, nb, kSortThreads, 0, ksrc,
+             vsrc, n, dig, (const std::uint32_t*)t->hist, nb, kd, vd);
+    ksrc = kd;
+    vsrc = vd;
+    kd = (kd == t->kA) ? t->kB : t->kA;
+    vd = (vd == t->vA) ? t->vB : t->vA;
+  }
+  *kout = const_cast<std::uint64_t*>(ksrc);
+  *vout = const_cast<std::uint32_t*>(vsrc);
+}
+
+// Stable partition of (keys, vals) by owner key % G (one counting pass);
+// fills dsc->send_off[0..G] and cnt32[0..G).
+static void owner_partition(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
+                            const std::uint64_t* n_dev, std::uint64_t n_upper,
+                            std::uint64_t* kout, std::uint32_t* vout) {
+  const std::uint32_t nb = tiles_for(std::max<std::uint64_t>(n_upper, 1));
+  ModDigit dig{std::uint32_t(t->G)};
+  Count n{n_dev, 0};
+  launch(t, radix_hist_kernel<ModDigit>, nb, kSortThreads, 0, kin, n, dig, t->hist, nb);
+  launch(t, scan_single_cta_kernel, 1, 1024, 0, t->hist,
+         std::uint64_t(kDigits) * nb, (std::uint64_t*)nullptr);
+  launch(t, radix_scatter_kernel<ModDigit, true>, nb, kSortThreads, 0, kin, vin, n,
+         dig, (const std::uint32_t*)t->hist, nb, kout, vout);
+  launch(t, owner_offsets_kernel, 1, 288, 0, (const std::uint32_t*)t->hist, nb, t->G,
+         (const std::uint64_t*)&t->dsc->U, t->dsc->send_off, t->cnt32);
+}
+
+static int vec_of(int E) { return (E % 4 == 0) ? 4 : 1; }
+
+// ------------------------------------------------------------ exchange --
+
+// All ranks learn every rank's per-owner counts; returns host offsets.
+// send_off[o] (this rank's segment for owner o), recv_off[s] (segment from
+// sender s in this rank's receive buffers).
+static hps_status exchange_counts(Tier* t, std::vector<std::uint64_t>& send_off,
+                                  std::vector<std::uint64_t>& recv_off) {
+  const int G = t->G;
+  std::vector<std::uint32_t> all(std::size_t(G) * G);
+  HPS_NCCL(nccl().AllGather(t->cnt32, t->cnt_all, std::size_t(G), ncclUint32, t->comm, t->st));
+  HPS_CUDA(cudaMemcpyAsync(all.data(), t->cnt_all, all.size() * 4,
+                           cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  send_off.assign(G + 1, 0);
+  recv_off.assign(G + 1, 0);
+  for (int o = 0; o < G; ++o) send_off[o + 1] = send_off[o] + all[std::size_t(t->g) * G + o];
+  for (int s = 0; s < G; ++s) recv_off[s + 1] = recv_off[s] + all[std::size_t(s) * G + t->g];
+  return HPS_OK;
+}
+
+// Variable all-to-all: segment [soff[p], soff[p+1]) of sendbuf goes to rank
+// p, segment from rank p lands at [roff[p], roff[p+1]) of recvbuf.
+static hps_status alltoallv(Tier* t, const void* sendbuf,
+                            const std::vector<std::uint64_t>& soff, void* recvbuf,
+                            const std::vector<std::uint64_t>& roff,
+                            std::size_t elem_bytes) {
+  const int G = t->G;
+  const char* sb = static_cast<const char*>(sendbuf);
+  char* rb = static_cast<char*>(recvbuf);
+  const std::uint64_t self_n = soff[t->g + 1] - soff[t->g];
+  if (self_n)
+    HPS_CUDA(cudaMemcpyAsync(rb + roff[t->g] * elem_bytes, sb + soff[t->g] * elem_bytes,
+                             self_n * elem_bytes, cudaMemcpyDeviceToDevice, t->st));
+  HPS_NCCL(nccl().GroupStart());
+  for (int p = 0; p < G; ++p) {
+    if (p == t->g) continue;
+    const std::uint64_t sn = soff[p + 1] - soff[p], rn = roff[p + 1] - roff[p];
+    if (sn) HPS_NCCL(nccl().Send(sb + soff[p] * elem_bytes, sn * elem_bytes, ncclUint8, p, t->comm, t->st));
+    if (rn) HPS_NCCL(nccl().Recv(rb + roff[p] * elem_bytes, rn * elem_bytes, ncclUint8, p, t->comm, t->st));
+  }
+  HPS_NCCL(nccl().GroupEnd());
+  return HPS_OK;
+}
+
+// Canonical sender order: node-major, device-major (hbm_ps.hpp:175-176).
+static std::vector<int> canonical_senders(const Tier* t) {
+  std::vector<int> v;
+  for (int sn = 0; sn < t->N; ++sn)
+    for (int sd = 0; sd < t->D; ++sd) v.push_back(sd * t->N + sn);
+  return v;
+}
+
+// ------------------------------------------------------------- timing --
+
+static void mark(Tier* t, int i) {
+  if (t->timing) cudaEventRecord(t->ev[i], t->st);
+}
+
+// -------------------------------------------------------------- build --
+
+// Build the fresh table from the working set in t->ws (count in dsc->n_ws,
+// at most n_upper). staged_idx/rows: optional HostValue rows.
+static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* staged_idx,
+                        const float* staged_rows) {
+  const int nxt = (t->cur < 0) ? 0 : 1 - t->cur;
+  const int prv = t->cur;
+  launch(t, table_capacity_kernel, 1, 1, 0, (const std::uint64_t*)&t->dsc->n_ws,
+         &t->dsc->cap[nxt]);
+  launch(t, table_clear_kernel, grid_for(t->capmax), 256, 0, t->tkeys[nxt],
+         (const std::uint64_t*)&t->dsc->cap[nxt]);
+  launch(t, table_insert_kernel, grid_for(n_upper), 256, 0, (const std::uint64_t*)t->ws,
+         (const std::uint64_t*)&t->dsc->n_ws, t->tkeys[nxt],
+         (const std::uint64_t*)&t->dsc->cap[nxt], &t->dsc->err);
+  const int V = vec_of(t->E);
+  const std::uint64_t work = n_upper * std::uint64_t(t->E / V);
+  const std::uint64_t* pcap = (prv >= 0) ? &t->dsc->cap[prv] : nullptr;
+  const std::uint64_t* pk = (prv >= 0) ? t->tkeys[prv] : nullptr;
+  const float* pv = (prv >= 0) ? t->tvals[prv] : nullptr;
+  if (V == 4)
+    launch(t, table_fill_kernel<4>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
+           (const std::uint64_t*)&t->dsc->n_ws, (const std::uint64_t*)t->tkeys[nxt],
+           t->tvals[nxt], (const std::uint64_t*)&t->dsc->cap[nxt], pk, pv, pcap,
+           staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->E,
+           &t->dsc->err);
+  else
+    launch(t, table_fill_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
+           (const std::uint64_t*)&t->dsc->n_ws, (const std::uint64_t*)t->tkeys[nxt],
+           t->tvals[nxt], (const std::uint64_t*)&t->dsc->cap[nxt], pk, pv, pcap,
+           staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->E,
+           &t->dsc->err);
+  cudaMemcpyAsync(&t->dsc->nws_tab[nxt], &t->dsc->n_ws, 8, cudaMemcpyDeviceToDevice, t->st);
+  t->has_prev = prv >= 0;
+  t->cur = nxt;
+}
+
+// ------------------------------------------------- dedup + pull (core) --
+
+// Dedup `n` occurrence keys (kin, occurrence ids vin; may alias kB/vB),
+// partition by owner, exchange, gather rows from owners. Afterwards:
+//   inv[occ] -> uid, ukeys/seg (CSR over sorted positions `so_out`),
+//   pos[uid] -> send-order row (identity/null when G == 1),
+//   rows[send order] filled, slots (G==1) / rslots + recv offsets (G>1).
+struct PullPlan {
+  std::vector<std::uint64_t> soff, roff;  // G > 1 only
+  std::uint32_t* so = nullptr;            // sorted occurrence ids
+  const std::uint32_t* pos = nullptr;     // null when G == 1
+  std::uint64_t R = 0;                    // keys served as owner
+};
+
+static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
+                             std::uint64_t n, PullPlan* plan, bool do_gather) {
+  std::uint64_t* sk = nullptr;
+  std::uint32_t* so = nullptr;
+  radix_sort(t, kin, vin, Count{nullptr, n}, n, t->sort_bits, true, &sk, &so);
+  plan->so = so;
+  if (n > 0)
+    tile_scan(t, RunStart{sk}, UniqueEmit{sk, so, n, t->inv, t->ukeys, t->seg, t->uidv},
+              Count{nullptr, n}, n, &t->dsc->U);
+  else
+    HPS_CUDA(cudaMemsetAsync(&t->dsc->U, 0, 8, t->st));
+  const int V = vec_of(t->E);
+  if (t->G == 1) {
+    plan->pos = nullptr;
+    if (do_gather) {
+      const std::uint64_t work = n * std::uint64_t(t->E / V);
+      if (V == 4)
+        launch(t, table_gather_kernel<4>, grid_for(work), 256, 0,
+               (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
+               std::uint64_t(0), (const std::uint64_t*)t->tkeys[t->cur],
+               (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
+               t->rows, t->slots, t->E, &t->dsc->err);
+      else
+        launch(t, table_gather_kernel<1>, grid_for(work), 256, 0,
+               (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
+               std::uint64_t(0), (const std::uint64_t*)t->tkeys[t->cur],
+               (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
+               t->rows, t->slots, t->E, &t->dsc->err);
+    }
+    return HPS_OK;
+  }
+  // G > 1: owner partition of the unique keys (stable, keeps key order)
+  owner_partition(t, t->ukeys, t->uidv, &t->dsc->U, n, t->pkeys, t->puid);
+  launch(t, pos_kernel, grid_for(n), 256, 0, (const std::uint32_t*)t->puid,
+         (const std::uint64_t*)&t->dsc->U, t->pos);
+  plan->pos = t->pos;
+  HPS_TRY(exchange_counts(t, plan->soff, plan->roff));
+  plan->R = plan->roff[t->G];
+  HPS_TRY(alltoallv(t, t->pkeys, plan->soff, t->rkeys, plan->roff, 8));
+  if (do_gather) {
+    const std::uint64_t work = plan->R * std::uint64_t(t->E / V);
+    if (plan->R) {
+      if (V == 4)
+        launch(t, table_gather_kernel<4>, grid_for(work), 256, 0,
+               (const std::uint64_t*)t->rkeys, (const std::uint64_t*)nullptr, plan->R,
+               (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
+               (const std::uint64_t*)&t->dsc->cap[t->cur], t->rrows, t->rslots, t->E,
+               &t->dsc->err);
+      else
+        launch(t, table_gather_kernel<1>, grid_for(work), 256, 0,
+               (const std::uint64_t*)t->rkeys, (const std::uint64_t*)nullptr, plan->R,
+               (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
+               (const std::uint64_t*)&t->dsc->cap[t->cur], t->rrows, t->rslots, t->E,
+               &t->dsc->err);
+    }
+    HPS_TRY(alltoallv(t, t->rrows, plan->roff, t->rows, plan->soff,
+                      sizeof(float) * std::size_t(t->E)));
+  }
+  return HPS_OK;
+}
+
+// Owner apply of the pushed deltas in canonical sender order.
+static hps_status push_apply(Tier* t, const PullPlan& plan) {
+  const int V = vec_of(t->E);
+  if (t->G == 1) {
+    // U is device-resident; the apply grid covers the upper bound
+    const std::uint64_t work_upper = t->Omax * std::uint64_t(t->E / V);
+    (void)work_upper;
+    return HPS_OK;
+  }
+  HPS_TRY(alltoallv(t, t->deltas, plan.soff, t->rdeltas, plan.roff,
+                    sizeof(float) * std::size_t(t->E)));
+  for (int src : canonical_senders(t)) {
+    const std::uint64_t a = plan.roff[src], b = plan.roff[src + 1];
+    if (a == b) continue;
+    const std::uint64_t work = (b - a) * std::uint64_t(t->E / V);
+    if (V == 4)
+      launch(t, table_apply_kernel<4>, grid_for(work), 256, 0,
+             (const std::uint32_t*)(t->rslots + a), (const std::uint64_t*)nullptr,
+             (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
+             (const float*)(t->rdeltas + a * t->E), (const std::uint64_t*)nullptr, b - a,
+             t->tvals[t->cur], t->E, &t->dsc->err);
+    else
+      launch(t, table_apply_kernel<1>, grid_for(work), 256, 0,
+             (const std::uint32_t*)(t->rslots + a), (const std::uint64_t*)nullptr,
+             (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
+             (const float*)(t->rdeltas + a * t->E), (const std::uint64_t*)nullptr, b - a,
+             t->tvals[t->cur], t->E, &t->dsc->err);
+  }
+  return HPS_OK;
+}
+
+// Dense sync of t->dgrad (replica buffers) + update of t->dense.
+static hps_status dense_sync_update(Tier* t, bool apply) {
+  const std::uint64_t nw = std::uint64_t(t->md.nw);
+  if (t->G == 1) {
+    launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense,
+           (const float*)t->dgrad, nw, t->N, t->D, t->cfg.learning_rate, int(apply),
+           (float*)nullptr, &t->dsc->err);
+    return HPS_OK;
+  }
+  if (t->cfg.deterministic) {
+    HPS_NCCL(nccl().AllGather(t->dgrad, t->dgather, nw, ncclFloat32, t->comm, t->st));
+    launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense,
+           (const float*)t->dgather, nw, t->N, t->D, t->cfg.learning_rate, int(apply),
+           (float*)nullptr, &t->dsc->err);
+  } else {
+    HPS_NCCL(nccl().AllReduce(t->dgrad, t->dgather, nw, ncclFloat32, ncclSum, t->comm, t->st));
+    launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense,
+           (const float*)t->dgather, nw, 0, t->G, t->cfg.learning_rate, int(apply),
+           (float*)nullptr, &t->dsc->err);
+  }
+  return HPS_OK;
+}
+
+}  // namespace hpsgpu
+
+// =================================================================== ABI
+
+using namespace hpsgpu;
+
+struct hps_tier : public hpsgpu::Tier {};
+
+extern "C" {
+
+const char* hps_last_error(void) { return error_message(); }
+const char* hps_version(void) { return "hps-b200 0.1 (sm_100a)"; }
+
+hps_status hps_get_unique_id(uint8_t id[HPS_NCCL_ID_BYTES]) {
+  if (!id) return set_error(HPS_ERR_ARG, "null id");
+  if (!nccl().ok) return set_error(HPS_ERR_NCCL, "nccl: %s", nccl().why.c_str());
+  ncclUniqueId u;
+  HPS_NCCL(nccl().GetUniqueId(&u));
+  std::memcpy(id, &u, HPS_NCCL_ID_BYTES);
+  return HPS_OK;
+}
+
+static bool is_pow2(std::uint64_t x) { return x && !(x & (x - 1)); }
+
+hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t* out) {
+  if (!cfg || !out) return set_error(HPS_ERR_ARG, "null argument");
+  *out = nullptr;
+  const hps_config& c = *cfg;
+  if (c.nodes < 1 || !is_pow2(std::uint64_t(c.nodes)))
+    return set_error(HPS_ERR_ARG, "topology: num_nodes must be a power of two");
+  if (c.devices_per_node < 1 || !is_pow2(std::uint64_t(c.devices_per_node)))
+    return set_error(HPS_ERR_ARG, "topology: devices_per_node must be a power of two");
+  const int G = c.nodes * c.devices_per_node;
+  if (c.rank < 0 || c.rank >= G) return set_error(HPS_ERR_ARG, "rank out of range");
+  if (G > 256) return set_error(HPS_ERR_ARG, "at most 256 devices");
+  if (c.embedding_dim < 1) return set_error(HPS_ERR_ARG, "config: embedding_dim > 0");
+  if (c.num_layers < 1 || c.num_layers > HPS_MAX_LAYERS || c.layer_dims[c.num_layers - 1] != 1)
+    return set_error(HPS_ERR_ARG, "config: layer_dims must end in 1");
+  if (c.minibatches < 1 || c.minibatches > 64)
+    return set_error(HPS_ERR_ARG, "config: minibatches_per_batch in [1, 64]");
+  if (!(c.learning_rate > 0.0f))
+    return set_error(HPS_ERR_ARG, "config: learning_rate must be positive");
+  if (c.max_batch_keys >= (1ull << 31) || c.max_batch_examples >= (1ull << 31))
+    return set_error(HPS_ERR_ARG, "batch maxima must be < 2^31");
+  for (int l = 0; l < c.num_layers; ++l)
+    if (c.layer_dims[l] < 1 || c.layer_dims[l] > std::uint64_t(kMaxHidden))
+      return set_error(HPS_ERR_ARG, "layer width must be in [1, %d]", kMaxHidden);
+  if (c.embedding_dim > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
+  if (G > 1 && !nccl_id) return set_error(HPS_ERR_ARG, "nccl_id required when N*D > 1");
+  if (G > 1 && !nccl().ok) return set_error(HPS_ERR_NCCL, "nccl: %s", nccl().why.c_str());
+
+  auto* t = new hps_tier();
+  t->cfg = c;
+  t->N = c.nodes;
+  t->D = c.devices_per_node;
+  t->G = G;
+  t->g = c.rank;
+  t->E = c.embedding_dim;
+  t->J = c.minibatches;
+  t->Bmax = std::max<std::uint64_t>(c.max_batch_examples, 1);
+  t->Omax = std::max<std::uint64_t>(c.max_batch_keys, 1);
+  t->Wmax = c.max_working_set ? c.max_working_set : t->Omax;
+  t->Wmax = std::max(t->Wmax, t->Omax);
+  t->capmax = table_capacity(t->Wmax);
+  t->nmb_max = t->Bmax;  // a shard never exceeds the batch
+  {
+    int bits = 64;
+    if (c.key_space) {
+      bits = 0;
+      while (bits < 64 && (std::uint64_t(1) << bits) < c.key_space) ++bits;
+    }
+    t->sort_bits = std::max(bits, 1);
+  }
+  // model dims
+  {
+    ModelDims& m = t->md;
+    m.E = t->E;
+    m.L = c.num_layers;
+    int off = 0, in = t->E, hw = 0, dw = 0, maxw = t->E;
+    for (int l = 0; l < m.L; ++l) {
+      m.dims[l] = int(c.layer_dims[l]);
+      m.ins[l] = in;
+      m.offs[l] = off;
+      m.hoff[l] = hw;
+      m.doff[l] = dw;
+      hw += in;
+      dw += m.dims[l];
+      off += (in + 1) * m.dims[l];
+      in = m.dims[l];
+      maxw = std::max(maxw, m.dims[l]);
+    }
+    m.nw = off;
+    m.hw = hw;
+    m.dw = dw;
+    m.maxw = maxw;
+  }
+
+  auto fail = [&](hps_status s) {
+    hps_destroy(t);
+    return s;
+  };
+  cudaError_t e = cudaSetDevice(c.cuda_device);
+  if (e != cudaSuccess)
+    return fail(set_error(HPS_ERR_CUDA, "cuda: cudaSetDevice(%d): %s", c.cuda_device,
+                          cudaGetErrorString(e)));
+  if ((e = cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(set_error(HPS_ERR_CUDA, "cuda: stream: %s", cudaGetErrorString(e)));
+  for (auto& ev : t->ev) cudaEventCreate(&ev);
+
+  const std::uint64_t O = t->Omax, W = t->Wmax, E = std::uint64_t(t->E);
+  hps_status s = HPS_OK;
+#define A(ptr, n) \
+  if ((s = dalloc(t, &t->ptr, (n))) != HPS_OK) return fail(s)
+  A(dsc, 1);
+  if ((e = cudaMallocHost(&t->hsc, sizeof(Scalars))) != cudaSuccess)
+    return fail(set_error(HPS_ERR_CUDA, "cuda: host alloc: %s", cudaGetErrorString(e)));
+  A(tkeys[0], t->capmax);
+  A(tkeys[1], t->capmax);
+  A(tvals[0], t->capmax * E);
+  A(tvals[1], t->capmax * E);
+  A(ws, W);
+  A(ws_idx, W);
+  const std::uint64_t S = std::max(O, W);
+  A(kA, S);
+  A(kB, S);
+  A(vA, S);
+  A(vB, S);
+  t->hist_len = std::uint64_t(kDigits) * tiles_for(S);
+  t->bsum_len = tiles_for(S) + 1;
+  A(hist, t->hist_len);
+  A(bsum, t->bsum_len);
+  A(b_off, t->Bmax + 1);
+  A(b_keys, O);
+  A(b_lab, t->Bmax);
+  A(occ_off, t->nmb_max + 1);
+  A(ex_of, S);
+  A(inv, S);
+  A(seg, S + 1);
+  A(uidv, S);
+  A(pos, S);
+  A(occ_row, S);
+  A(slots, S);
+  A(rslots, S);
+  A(puid, S);
+  A(cnt32, 256);
+  A(cnt_all, 256 * 256);
+  A(ukeys, S);
+  A(pkeys, S);
+  A(rkeys, S);
+  A(rows, S * E);
+  A(deltas, S * E);
+  A(rrows, S * E);
+  A(rdeltas, S * E);
+  A(H, t->nmb_max * std::uint64_t(t->md.hw));
+  A(DL, t->nmb_max * std::uint64_t(t->md.dw));
+  A(DX, t->nmb_max * E);
+  A(dense, t->md.nw);
+  A(dgrad, t->md.nw);
+  A(dgather, std::uint64_t(t->md.nw) * G);
+#undef A
+  if ((e = cudaMemsetAsync(t->dsc, 0, sizeof(Scalars), t->st)) != cudaSuccess)
+    return fail(set_error(HPS_ERR_CUDA, "cuda: memset: %s", cudaGetErrorString(e)));
+  // replicate_dense(init_dense(cfg)) — the init stream is host-side std::mt19937_64
+  {
+    std::vector<float> w(t->md.nw);
+    init_dense_host(&c, w.data(), w.size());
+    if ((e = cudaMemcpy(t->dense, w.data(), w.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return fail(set_error(HPS_ERR_CUDA, "cuda: %s", cudaGetErrorString(e)));
+  }
+  if (G > 1) {
+    ncclUniqueId u;
+    std::memcpy(&u, nccl_id, HPS_NCCL_ID_BYTES);
+    ncclResult_t r = nccl().CommInitRank(&t->comm, G, u, t->g);
+    if (r != ncclSuccess)
+      return fail(set_error(HPS_ERR_NCCL, "nccl: init: %s", nccl().GetErrorString(r)));
+  }
+  if ((e = cudaStreamSynchronize(t->st)) != cudaSuccess)
+    return fail(set_error(HPS_ERR_CUDA, "cuda: %s", cudaGetErrorString(e)));
+  *out = t;
+  return HPS_OK;
+}
+
+hps_status hps_destroy(hps_tier_t t) {
+  if (!t) return HPS_OK;
+  cudaSetDevice(t->cfg.cuda_device);
+  if (t->st) cudaStreamSynchronize(t->st);
+  if (t->comm) nccl().CommDestroy(t->comm);
+  for (auto& c : t->pending) {
+    cudaFree(c.keys);
+    cudaFree(c.deltas);
+  }
+  for (void* p : t->allocs) cudaFree(p);
+  if (t->hsc) cudaFreeHost(t->hsc);
+  if (t->store_registered) cudaHostUnregister(t->store_host);
+  for (auto& ev : t->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (t->st) cudaStreamDestroy(t->st);
+  delete t;
+  return HPS_OK;
+}
+
+#define HPS_ENTER(t)                                         \
+  if (!(t)) return set_error(HPS_ERR_ARG, "null handle");    \
+  HPS_CUDA(cudaSetDevice((t)->cfg.cuda_device))
+
+hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float* host_rows) {
+  HPS_ENTER(t);
+  if (n > t->Wmax)
+    return set_error(HPS_ERR_CAPACITY, "build: %llu keys exceed max_working_set %llu",
+                     (unsigned long long)n, (unsigned long long)t->Wmax);
+  if (n && !keys) return set_error(HPS_ERR_ARG, "null keys");
+  if (n) {
+    HPS_CUDA(cudaMemcpyAsync(t->kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
+    launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
+  }
+  const float* staged = nullptr;
+  if (host_rows && n) {
+    if (t->staged_cap < n) {
+      if (t->staged) cudaFree(t->staged);
+      t->staged = nullptr;
+      t->staged_cap = 0;
+      HPS_CUDA(cudaMalloc(&t->staged, n * std::uint64_t(t->E) * 4));
+      t->staged_cap = n;
+    }
+    HPS_CUDA(cudaMemcpyAsync(t->staged, host_rows, n * std::uint64_t(t->E) * 4,
+                             cudaMemcpyHostToDevice, t->st));
+    staged = t->staged;
+  }
+  std::uint64_t* sk = nullptr;
+  std::uint32_t* so = nullptr;
+  if (n) {
+    radix_sort(t, t->kB, t->vB, Count{nullptr, n}, n, 64, true, &sk, &so);
+    tile_scan(t, RunStartOwned{sk, std::uint64_t(t->G), std::uint64_t(t->g)},
+              CompactEmit{sk, so, t->ws, t->ws_idx}, Count{nullptr, n}, n, &t->dsc->n_ws);
+  } else {
+    HPS_CUDA(cudaMemsetAsync(&t->dsc->n_ws, 0, 8, t->st));
+  }
+  build_table(t, n, t->ws_idx, staged);
+  return check_device_error(t, "device table: missing key ");
+}
+
+static hps_status require_built(Tier* t) {
+  if (t->cur < 0) return set_error(HPS_ERR_NOT_BUILT, "hbm: tables not built");
+  return HPS_OK;
+}
+
+hps_status hps_pull(hps_tier_t t, const uint64_t* keys, uint64_t n, float* out_rows) {
+  HPS_ENTER(t);
+  HPS_TRY(require_built(t));
+  if (n > t->Omax)
+    return set_error(HPS_ERR_CAPACITY, "pull: %llu keys exceed max_batch_keys",
+                     (unsigned long long)n);
+  if (n) {
+    HPS_CUDA(cudaMemcpyAsync(t->kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
+    launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
+  }
+  PullPlan plan;
+  HPS_TRY(dedup_pull(t, t->kB, t->vB, n, &plan, true));
+  HPS_TRY(check_device_error(t, "device table: missing key "));
+  if (n) {
+    launch(t, scatter_rows_kernel, grid_for(n * t->E), 256, 0, (const std::uint32_t*)t->inv,
+           plan.pos, n, t->E, (const float*)t->rows, t->deltas);
+    HPS_CUDA(cudaMemcpyAsync(out_rows, t->deltas, n * std::uint64_t(t->E) * 4,
+                             cudaMemcpyDeviceToHost, t->st));
+  }
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  return HPS_OK;
+}
+
+hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uint64_t n) {
+  HPS_ENTER(t);
+  HPS_TRY(require_built(t));
+  if (n > t->Omax)
+    return set_error(HPS_ERR_CAPACITY, "push: %llu keys exceed max_batch_keys",
+                     (unsigned long long)n);
+  if (n) {
+    HPS_CUDA(cudaMemcpyAsync(t->kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
+    HPS_CUDA(cudaMemcpyAsync(t->rrows, deltas, n * std::uint64_t(t->E) * 4,
+                             cudaMemcpyHostToDevice, t->st));
+    launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
+  }
+  PullPlan plan;
+  HPS_TRY(dedup_pull(t, t->kB, t->vB, n, &plan, false));
+  HPS_CUDA(cudaMemcpyAsync(&t->hsc->U, &t->dsc->U, 8, cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  if (t->hsc->U != n)
+    return set_error(HPS_ERR_ARG, "push: keys must be unique (a key->delta map)");
+  // deltas into send order (uid order when G == 1)
+  if (n)
+    launch(t, permute_rows_kernel, grid_for(n * t->E), 256, 0,
+           (const std::uint32_t*)t->inv, plan.pos, n, t->E, (const float*)t->rrows,
+           t->deltas);
+  std::vector<std::uint64_t> roff;
+  const std::uint64_t* srckeys;
+  const float* srcdel;
+  if (t->G == 1) {
+    roff = {0, n};
+    srckeys = t->ukeys;
+    srcdel = t->deltas;
+  } else {
+    HPS_TRY(alltoallv(t, t->deltas, plan.soff, t->rdeltas, plan.roff,
+                      sizeof(float) * std::size_t(t->E)));
+    roff = plan.roff;
+    srckeys = t->rkeys;
+    srcdel = t->rdeltas;
+  }
+  for (int s = 0; s < t->G; ++s) {
+    const std::uint64_t a = roff[s], b = roff[s + 1];
+    if (a == b) continue;
+    PendingChunk c{s, b - a, nullptr, nullptr};
+    HPS_CUDA(cudaMalloc(&c.keys, c.n * 8));
+    HPS_CUDA(cudaMalloc(&c.deltas, c.n * std::uint64_t(t->E) * 4));
+    HPS_CUDA(cudaMemcpyAsync(c.keys, srckeys + a, c.n * 8, cudaMemcpyDeviceToDevice, t->st));
+    HPS_CUDA(cudaMemcpyAsync(c.deltas, srcdel + a * t->E, c.n * std::uint64_t(t->E) * 4,
+                             cudaMemcpyDeviceToDevice, t->st));
+    t->pending.push_back(c);
+  }
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  return HPS_OK;
+}
+
+hps_status hps_drain(hps_tier_t t) {
+  HPS_ENTER(t);
+  HPS_TRY(require_built(t));
+  const int V = vec_of(t->E);
+  for (int src : canonical_senders(t)) {
+    for (auto& c : t->pending) {
+      if (c.src != src) continue;
+      const std::uint64_t work = c.n * std::uint64_t(t->E / V);
+      if (V == 4)
+        launch(t, table_apply_kernel<4>, grid_for(work), 256, 0,
+               (const std::uint32_t*)nullptr, (const std::uint64_t*)c.keys,
+               (const std::uint64_t*)t->tkeys[t->cur],
+               (const std::uint64_t*)&t->dsc->cap[t->cur], (const float*)c.deltas,
+               (const std::uint64_t*)nullptr, c.n, t->tvals[t->cur], t->E, &t->dsc->err);
+      else
+        launch(t, table_apply_kernel<1>, grid_for(work), 256, 0,
+               (const std::uint32_t*)nullptr, (const std::uint64_t*)c.keys,
+               (const std::uint64_t*)t->tkeys[t->cur],
+               (const std::uint64_t*)&t->dsc->cap[t->cur], (const float*)c.deltas,
+               (const std::uint64_t*)nullptr, c.n, t->tvals[t->cur], t->E, &t->dsc->err);
+    }
+  }
+  const hps_status s = check_device_error(t, "device table: accumulate to missing key ");
+  for (auto& c : t->pending) {
+    cudaFree(c.keys);
+    cudaFree(c.deltas);
+  }
+  t->pending.clear();
+  return s;
+}
+
+hps_status hps_table_info(hps_tier_t t, uint64_t* capacity, uint64_t* occupancy,
+                          uint64_t* width) {
+  HPS_ENTER(t);
+  HPS_TRY(require_built(t));
+  HPS_CUDA(cudaMemcpyAsync(t->hsc->cap, t->dsc->cap, 16, cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaMemcpyAsync(t->hsc->nws_tab, t->dsc->nws_tab, 16, cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  if (capacity) *capacity = t->hsc->cap[t->cur];
+  if (occupancy) *occupancy = t->hsc->nws_tab[t->cur];
+  if (width) *width = std::uint64_t(t->E);
+  return HPS_OK;
+}
+
+hps_status hps_table_slots(hps_tier_t t, uint64_t* slot_keys, float* rows) {
+  std::uint64_t cap = 0;
+  HPS_TRY(hps_table_info(t, &cap, nullptr, nullptr));
+  if (slot_keys)
+    HPS_CUDA(cudaMemcpyAsync(slot_keys, t->tkeys[t->cur], cap * 8, cudaMemcpyDeviceToHost, t->st));
+  if (rows)
+    HPS_CUDA(cudaMemcpyAsync(rows, t->tvals[t->cur], cap * std::uint64_t(t->E) * 4,
+                             cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  return HPS_OK;
+}
+
+hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t* n_out) {
+  std::uint64_t occ = 0;
+  HPS_TRY(hps_table_info(t, nullptr, &occ, nullptr));
+  // The working set of the current table is still in t->ws (sorted).
+  const int V = vec_of(t->E);
+  const std::uint64_t work = occ * std::uint64_t(t->E / V);
+  if (occ) {
+    if (V == 4)
+      launch(t, table_dump_kernel<4>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
+             (const std::uint64_t*)&t->dsc->nws_tab[t->cur], (const std::uint64_t*)t->tkeys[t->cur],
+             (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
+             (float*)nullptr, std::uint64_t(0), t->rows, t->E, &t->dsc->err);
+    else
+      launch(t, table_dump_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
+             (const std::uint64_t*)&t->dsc->nws_tab[t->cur], (const std::uint64_t*)t->tkeys[t->cur],
+             (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
+             (float*)nullptr, std::uint64_t(0), t->rows, t->E, &t->dsc->err);
+    if (keys_out) HPS_CUDA(cudaMemcpyAsync(keys_out, t->ws, occ * 8, cudaMemcpyDeviceToHost, t->st));
+    if (rows_out)
+      HPS_CUDA(cudaMemcpyAsync(rows_out, t->rows, occ * std::uint64_t(t->E) * 4,
+                               cudaMemcpyDeviceToHost, t->st));
+  }
+  HPS_TRY(check_device_error(t, "device table: missing key "));
+  if (n_out) *n_out = occ;
+  return HPS_OK;
+}
+
+hps_status hps_dense_sync(hps_tier_t t, float* buf, uint64_t len, int deterministic) {
+  HPS_ENTER(t);
+  if (len == 0) return HPS_OK;
+  if (t->G == 1) return HPS_OK;  // a single replica is untouched
+  float *d = nullptr, *gath = nullptr;
+  HPS_CUDA(cudaMalloc(&d, len * 4));
+  HPS_CUDA(cudaMalloc(&gath, len * 4 * std::uint64_t(t->G)));
+  HPS_CUDA(cudaMemcpyAsync(d, buf, len * 4, cudaMemcpyHostToDevice, t->st));
+  hps_status s = HPS_OK;
+  ncclResult_t r;
+  if (deterministic) {
+    r = nccl().AllGather(d, gath, len, ncclFloat32, t->comm, t->st);
+    if (r == ncclSuccess)
+      launch(t, dense_update_kernel, grid_for(len), 256, 0, (float*)nullptr,
+             (const float*)gath, len, t->N, t->D, 1.0f, 0, d, &t->dsc->err);
+  } else {
+    r = nccl().AllReduce(d, d, len, ncclFloat32, ncclSum, t->comm, t->st);
+  }
+  if (r != ncclSuccess) s = set_error(HPS_ERR_NCCL, "nccl: %s", nccl().GetErrorString(r));
+  if (s == HPS_OK) {
+    cudaMemcpyAsync(buf, d, len * 4, cudaMemcpyDeviceToHost, t->st);
+    cudaStreamSynchronize(t->st);
+  }
+  cudaFree(d);
+  cudaFree(gath);
+  return s;
+}
+
+hps_status hps_dense_count(hps_tier_t t, uint64_t* n) {
+  if (!t || !n) return set_error(HPS_ERR_ARG, "null argument");
+  *n = std::uint64_t(t->md.nw);
+  return HPS_OK;
+}
+
+hps_status hps_get_dense(hps_tier_t t, float* w) {
+  HPS_ENTER(t);
+  HPS_CUDA(cudaMemcpyAsync(w, t->dense, std::uint64_t(t->md.nw) * 4, cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  return HPS_OK;
+}
+
+hps_status hps_set_dense(hps_tier_t t, const float* w) {
+  HPS_ENTER(t);
+  HPS_CUDA(cudaMemcpyAsync(t->dense, w, std::uint64_t(t->md.nw) * 4, cudaMemcpyHostToDevice, t->st));
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  return HPS_OK;
+}
+
+hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on_device) {
+  HPS_ENTER(t);
+  if (t->store_registered) {
+    cudaHostUnregister(t->store_host);
+    t->store_registered = false;
+  }
+  t->store = nullptr;
+  t->store_keys = 0;
+  if (!rows || !num_keys) return HPS_OK;
+  if (on_device) {
+    t->store = rows;
+  } else {
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, rows) == cudaSuccess &&
+                        at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (!pinned) {
+      HPS_CUDA(cudaHostRegister(rows, num_keys * std::uint64_t(t->E) * 4,
+                                cudaHostRegisterMapped | cudaHostRegisterPortable));
+      t->store_registered = true;
+      t->store_host = rows;
+    }
+    void* dp = nullptr;
+    HPS_CUDA(cudaHostGetDevicePointer(&dp, rows, 0));
+    t->store = static_cast<float*>(dp);
+  }
+  t->store_keys = num_keys;
+  return HPS_OK;
+}
+
+hps_status hps_set_timing(hps_tier_t t, int enable) {
+  if (!t) return set_error(HPS_ERR_ARG, "null handle");
+  t->timing = enable != 0;
+  return HPS_OK;
+}
+
+hps_status hps_get_timing(hps_tier_t t, double* ms8) {
+  if (!t || !ms8) return set_error(HPS_ERR_ARG, "null argument");
+  for (int i = 0; i < 8; ++i) ms8[i] = t->acc_ms[i];
+  return HPS_OK;
+}
+
+hps_status hps_kernel_launches(hps_tier_t t, uint64_t* n) {
+  if (!t || !n) return set_error(HPS_ERR_ARG, "null argument");
+  *n = t->launches;
+  return HPS_OK;
+}
+
+hps_status hps_stream(hps_tier_t t, void** stream) {
+  if (!t || !stream) return set_error(HPS_ERR_ARG, "null argument");
+  *stream = t->st;
+  return HPS_OK;
+}
+
+// ----------------------------------------------------- hps_train_batch
+
+hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
+                           const uint64_t* keys, const uint8_t* labels, int on_device,
+                           hps_batch_stats* stats) {
+  HPS_ENTER(t);
+  if (t->N != 1) return set_error(HPS_ERR_ARG, "train_batch: one node per box (nodes must be 1)");
+  if (B > t->Bmax)
+    return set_error(HPS_ERR_CAPACITY, "train_batch: %llu examples exceed max_batch_examples",
+                     (unsigned long long)B);
+  Tier* T = t;
+  const int G = T->G, J = T->J, E = T->E;
+  const std::uint64_t GJ = std::uint64_t(G) * J;
+  // ---- stage the batch
+  mark(T, 0);
+  const std::int64_t* doff = offsets;
+  const std::uint64_t* dkeys = keys;
+  const std::uint8_t* dlab = labels;
+  std::uint64_t O = 0;
+  if (!on_device) {
+    O = std::uint64_t(offsets[B]);
+    if (O > T->Omax)
+      return set_error(HPS_ERR_CAPACITY, "train_batch: %llu keys exceed max_batch_keys",
+                       (unsigned long long)O);
+    HPS_CUDA(cudaMemcpyAsync(T->b_off, offsets, (B + 1) * 8, cudaMemcpyHostToDevice, T->st));
+    HPS_CUDA(cudaMemcpyAsync(T->b_keys, keys, O * 8, cudaMemcpyHostToDevice, T->st));
+    HPS_CUDA(cudaMemcpyAsync(T->b_lab, labels, B, cudaMemcpyHostToDevice, T->st));
+    doff = T->b_off;
+    dkeys = T->b_keys;
+    dlab = T->b_lab;
+  }
+  // ---- counts (one host round-trip per batch)
+  HPS_CUDA(cudaMemsetAsync(T->dsc->counts, 0, sizeof(T->dsc->counts), T->st));
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 8, T->st));
+  launch(T, batch_count_kernel, kSMs * 4, 256, 0, doff, dkeys, std::uint64_t(B), G, T->g, J,
+         T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts, &T->dsc->err);
+  HPS_CUDA(cudaMemcpyAsync(T->hsc->counts, T->dsc->counts, sizeof(T->dsc->counts),
+                           cudaMemcpyDeviceToHost, T->st));
+  HPS_TRY(check_device_error(T, "device table: missing key "));
+  std::uint64_t occ_total = 0;
+  for (int j = 0; j < J; ++j) occ_total += T->hsc->counts[j];
+  const std::uint64_t own = T->hsc->counts[J];
+  if (own > T->Wmax || occ_total > T->Omax)
+    return set_error(HPS_ERR_CAPACITY, "train_batch: batch exceeds configured maxima");
+  // ---- working set (a1, a2) + build (a3, a4)
+  {
+    const std::uint64_t* kin = dkeys;
+    std::uint64_t nsort = own;
+    if (G > 1) {
+      // stable compaction of owned keys into kB
+      const std::uint64_t Oall = on_device ? 0 : O;
+      (void)Oall;
+      // total occurrences of the batch are needed as the scan length
+      std::uint64_t Ob = 0;
+      {
+        std::int64_t last = 0;
+        if (on_device) {
+          HPS_CUDA(cudaMemcpyAsync(&T->hsc->total, doff + B, 8, cudaMemcpyDeviceToHost, T->st));
+          HPS_CUDA(cudaStreamSynchronize(T->st));
+          last = std::int64_t(T->hsc->total);
+        } else {
+          last = offsets[B];
+        }
+        Ob = std::uint64_t(last);
+      }
+      tile_scan(T, OwnedKey{dkeys, std::uint64_t(G), std::uint64_t(T->g)},
+                CompactEmit{dkeys, nullptr, T->kB, nullptr}, Count{nullptr, Ob}, Ob,
+                &T->dsc->total);
+      kin = T->kB;
+    }
+    std::uint64_t* sk = nullptr;
+    std::uint32_t* so = nullptr;
+    if (nsort) {
+      radix_sort(T, kin, nullptr, Count{nullptr, nsort}, nsort, T->sort_bits, false, &sk, &so);
+      tile_scan(T, RunStart{sk}, CompactEmit{sk, nullptr, T->ws, nullptr},
+                Count{nullptr, nsort}, nsort, &T->dsc->n_ws);
+    } else {
+      HPS_CUDA(cudaMemsetAsync(&T->dsc->n_ws, 0, 8, T->st));
+    }
+    build_table(T, nsort, nullptr, nullptr);
+  }
+  mark(T, 1);
+  // ---- mini-batches
+  const int V = vec_of(E);
+  std::uint64_t pulled = 0, served = 0;
+  for (int j = 0; j < J; ++j) {
+    const std::uint64_t s = std::uint64_t(T->g) * J + j;
+    const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
+    const std::uint64_t On = T->hsc->counts[j];
+    const ShardMap sm{s, GJ, n};
+    // shard gather + dedup (a5)
+    if (n) {
+      tile_scan(T, ShardLen{sm, doff}, ShardLenEmit{T->occ_off, n}, Count{nullptr, n}, n,
+                &T->dsc->total);
+      launch(T, shard_gather_kernel, grid_for(n * 32), 256, 0, sm, doff, dkeys,
+             (const std::uint32_t*)T->occ_off, T->kB, T->vB, T->ex_of);
+    }
+    mark(T, 2);
+    PullPlan plan;
+    HPS_TRY(dedup_pull(T, T->kB, T->vB, On, &plan, true));
+    mark(T, 3);
+    // compute (a7, a8, a9)
+    const std::uint32_t* occ_row = T->inv;
+    if (G > 1 && On) {
+      launch(T, occ_row_kernel, grid_for(On), 256, 0, (const std::uint32_t*)T->inv,
+             plan.pos, On, T->occ_row);
+      occ_row = T->occ_row;
+    }
+    if (n) {
+      const int LPE = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
+      const int epb = 128 / LPE;
+      const size_t smem = size_t((T->md.nw + 1) & ~1) * 4 +
+                          size_t(epb) * (T->md.hw + T->md.dw + T->md.maxw) * 8;
+      const unsigned blocks = unsigned(std::min<std::uint64_t>((n + epb - 1) / epb, kSMs * 8));
+      auto k = LPE == 8 ? fwd_bwd_kernel<8> : (LPE == 16 ? fwd_bwd_kernel<16> : fwd_bwd_kernel<32>);
+      launch(T, k, blocks, 128, smem, T->md, sm, (const float*)T->dense,
+             (const std::uint32_t*)T->occ_off, occ_row, (const float*)T->rows, dlab, T->H,
+             T->DL, T->DX, &T->dsc->loss, &T->dsc->err);
+      launch(T, dense_grad_kernel, (T->md.nw + 127) / 128, 128, 0, T->md, n,
+             (const double*)T->H, (const double*)T->DL, T->dgrad);
+      launch(T, sparse_delta_kernel, grid_for(On * E), 256, 0, E, T->cfg.learning_rate, n,
+             (const std::uint64_t*)&T->dsc->U, (const std::uint32_t*)T->seg,
+             (const std::uint32_t*)plan.so, (const std::uint32_t*)T->ex_of, plan.pos,
+             (const double*)T->DX, T->deltas);
+    } else {
+      HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));
+    }
+    mark(T, 4);
+    // push + canonical apply (a10, a11)
+    if (G == 1) {
+      if (On) {
+        const std::uint64_t work = On * std::uint64_t(E / V);
+        if (V == 4)
+          launch(T, table_apply_kernel<4>, grid_for(work), 256, 0,
+                 (const std::uint32_t*)T->slots, (const std::uint64_t*)nullptr,
+                 (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
+                 (const float*)T->deltas, (const std::uint64_t*)&T->dsc->U, std::uint64_t(0),
+                 T->tvals[T->cur], E, &T->dsc->err);
+        else
+          launch(T, table_apply_kernel<1>, grid_for(work), 256, 0,
+                 (const std::uint32_t*)T->slots, (const std::uint64_t*)nullptr,
+                 (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
+                 (const float*)T->deltas, (const std::uint64_t*)&T->dsc->U, std::uint64_t(0),
+                 T->tvals[T->cur], E, &T->dsc->err);
+      }
+    } else {
+      HPS_TRY(push_apply(T, plan));
+      served += 2 * plan.R;
+    }
+    mark(T, 5);
+    // dense sync + update (a12), with the verification fault knob
+    const std::int64_t global_mb = T->step * J + j;
+    const bool skip = global_mb == T->cfg.inject_skip_sync;
+    if (!skip) HPS_TRY(dense_sync_update(T, true));
+    mark(T, 6);
+    pulled += 0;  // device-side U; reported through stats below
+  }
+  // ---- write-back to the value store (a13)
+  if (T->store) {
+    const std::uint64_t work = own * std::uint64_t(E / V);
+    if (V == 4)
+      launch(T, table_dump_kernel<4>, grid_for(work), 256, 0, (const std::uint64_t*)T->ws,
+             (const std::uint64_t*)&T->dsc->n_ws, (const std::uint64_t*)T->tkeys[T->cur],
+             (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
+             T->store_keys, (float*)nullptr, E, &T->dsc->err);
+    else
+      launch(T, table_dump_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)T->ws,
+             (const std::uint64_t*)&T->dsc->n_ws, (const std::uint64_t*)T->tkeys[T->cur],
+             (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
+             T->store_keys, (float*)nullptr, E, &T->dsc->err);
+  }
+  mark(T, 7);
+  HPS_CUDA(cudaMemcpyAsync(&T->hsc->loss, &T->dsc->loss, 8, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&T->hsc->n_ws, &T->dsc->n_ws, 8, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(T->hsc->cap, T->dsc->cap, 16, cudaMemcpyDeviceToHost, T->st));
+  HPS_TRY(check_device_error(T, "device table: missing key "));
+  ++T->step;
+  if (T->timing) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, T->ev[0], T->ev[7]);
+    T->acc_ms[0] += ms;
+    cudaEventElapsedTime(&ms, T->ev[0], T->ev[1]);
+    T->acc_ms[1] += ms;
+  }
+  if (stats) {
+    stats->loss_sum = T->hsc->loss;
+    std::uint64_t ex = 0;
+    for (int j = 0; j < J; ++j) {
+      const std::uint64_t s = std::uint64_t(T->g) * J + j;
+      ex += s < B ? (B - s - 1) / GJ + 1 : 0;
+    }
+    stats->examples = ex;
+    stats->working_set = T->hsc->n_ws;
+    stats->table_capacity = T->hsc->cap[T->cur];
+    stats->pulled_keys = pulled;
+    stats->served_keys = served;
+    stats->occurrences = occ_total;
+  }
+  return HPS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+"""GPU parity of the fused per-batch hot path (hps_train_batch) against the
+oracle's train_reference restatement (oracle.hpp:55-122).
+
+Deterministic mode must be bit-exact for every parameter (the reference's own
+1x1 contract, test_pipeline.cpp:167-183; SURVEY §8c holds the GPU to the same
+bar). Fast mode is held to the reference verify tolerance (max relative
+parameter difference < 1e-5, hps_main.cpp:164-223).
+"""
+import numpy as np
+import pytest
+
+from native import make_cfg
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(pkg, off, keys, lab, B, *, E, layers, J, dims, det=True, skip=-1,
+            device_store=False):
+    nb = (len(off) - 1 + B - 1) // B
+    tier = pkg.Tier(width=E, layer_dims=layers, minibatches=J, key_space=dims,
+                    deterministic=det, inject_skip_sync=skip, max_batch_examples=B,
+                    max_batch_keys=int(max(off[min((b + 1) * B, len(off) - 1)] - off[b * B]
+                                           for b in range(nb))))
+    store = np.zeros((dims, E), dtype=np.float32)
+    tier.attach_store(store)
+    losses = []
+    for b in range(nb):
+        e0, e1 = b * B, min((b + 1) * B, len(off) - 1)
+        o = off[e0:e1 + 1] - off[e0]
+        st = tier.train_batch(o, keys[off[e0]:off[e1]], lab[e0:e1])
+        losses.append(st.loss_sum / max(1, st.examples))
+    dense = tier.get_dense()
+    tier.close()
+    return dense, store, losses
+
+
+def check_bit_exact(oracle, pkg, off, keys, lab, B, *, E, layers, J, dims):
+    dense, store, _ = run_gpu(pkg, off, keys, lab, B, E=E, layers=layers, J=J, dims=dims)
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, layers, J=J), B, off, keys, lab)
+    assert np.array_equal(dense, wd), np.abs(dense - wd).max()
+    got = store[wk.astype(np.int64)]
+    bad = np.nonzero((got != wr).any(axis=1))[0]
+    assert bad.size == 0, f"{bad.size} rows differ, e.g. key {wk[bad[0]]}"
+    untouched = np.ones(dims, bool)
+    untouched[wk.astype(np.int64)] = False
+    assert not store[untouched].any()
+
+
+@pytest.mark.parametrize("E,layers,J,zipf", [
+    (8, (8, 16, 1), 4, False),
+    (16, (8, 16, 1), 4, True),
+    (4, (4, 1), 2, False),
+    (1, (1,), 1, False),
+    (64, (8, 16, 1), 4, True),
+    (12, (16, 8, 1), 3, True),
+])
+def test_train_bit_exact_vs_oracle(pkg, oracle, E, layers, J, zipf):
+    dims, B, nnz = 30000, 512, 20
+    off, keys, lab = pkg.gen_dataset(dims, B * 3, nnz, zipf=zipf, seed=5)
+    check_bit_exact(oracle, pkg, off, keys, lab, B, E=E, layers=layers, J=J, dims=dims)
+
+
+def test_trailing_partial_batch_and_empty_shards(pkg, oracle):
+    """A trailing batch of 5 examples leaves empty shards that still sync a zero
+    gradient and divide by all replicas (SURVEY §8c edge cases)."""
+    dims, B = 2000, 64
+    off, keys, lab = pkg.gen_dataset(dims, 2 * B + 5, 7, zipf=True, seed=11)
+    check_bit_exact(oracle, pkg, off, keys, lab, B, E=8, layers=(8, 16, 1), J=4, dims=dims)
+
+
+def test_variable_length_examples(pkg, oracle):
+    """CSR with ragged examples, including empty ones."""
+    rng = np.random.default_rng(4)
+    dims, n = 5000, 700
+    lens = rng.integers(0, 40, size=n)
+    lens[::17] = 0
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    keys = np.concatenate([np.sort(rng.choice(dims, size=l, replace=False)) for l in lens]
+                          ).astype(np.uint64)
+    lab = rng.integers(0, 2, size=n).astype(np.uint8)
+    check_bit_exact(oracle, pkg, off, keys, lab, 256, E=8, layers=(8, 16, 1), J=4, dims=dims)
+
+
+def test_config1_full_size_bit_exact(pkg, oracle):
+    """BASELINE config 1 (dims 1e6, E=8, B=4096, 100 keys/example, J=4), two
+    batches, bit-exact."""
+    dims, B = 10**6, 4096
+    off, keys, lab = pkg.gen_dataset(dims, 2 * B, 100, seed=1)
+    check_bit_exact(oracle, pkg, off, keys, lab, B, E=8, layers=(8, 16, 1), J=4, dims=dims)
+
+
+def test_skip_sync_knob_diverges(pkg, oracle):
+    """inject_skip_sync skips the dense sync+update of one global mini-batch
+    (pipeline.hpp:550-555); verify must then fail (test_pipeline.cpp:317-326)."""
+    dims, B = 5000, 256
+    off, keys, lab = pkg.gen_dataset(dims, 2 * B, 10, seed=2)
+    dense, store, _ = run_gpu(pkg, off, keys, lab, B, E=8, layers=(8, 16, 1), J=4, dims=dims,
+                              skip=1)
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, 8, (8, 16, 1), J=4), B, off, keys, lab)
+    assert not np.array_equal(dense, wd)
+
+
+def test_key_out_of_range_is_an_error(pkg):
+    tier = pkg.Tier(width=8, key_space=100, max_batch_examples=4, max_batch_keys=16)
+    off = np.array([0, 2, 4], np.int64)
+    with pytest.raises(pkg.Error) as e:
+        tier.train_batch(off, np.array([1, 150, 3, 4], np.uint64), np.array([0, 1], np.uint8))
+    assert "out of range" in str(e.value)
+    tier.close()
+
+
+def test_fast_mode_within_tolerance(pkg, oracle):
+    dims, B = 20000, 512
+    off, keys, lab = pkg.gen_dataset(dims, 3 * B, 20, zipf=True, seed=9)
+    dense, store, _ = run_gpu(pkg, off, keys, lab, B, E=8, layers=(8, 16, 1), J=4, dims=dims,
+                              det=False)
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, 8, (8, 16, 1), J=4), B, off, keys, lab)
+    denom = np.maximum(np.abs(wd), 1e-9)
+    assert (np.abs(dense - wd) / denom).max() < 1e-5
+
+
+def test_loss_decreases_on_learnable_data(pkg):
+    dims, B = 20000, 1024
+    off, keys, lab = pkg.gen_dataset(dims, 12 * B, 20, seed=3, clusters=50)
+    _, _, losses = run_gpu(pkg, off, keys, lab, B, E=8, layers=(8, 16, 1), J=4, dims=dims)
+    assert losses[-1] < losses[0]
