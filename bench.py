@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""Benchmark of the HBM-PS hot path (one JSON line on rank 0).
+
+A step is one batch of the BASELINE workload through the tier: working-set
+dedup -> table build (carry-over + value-store staging) -> J mini-batches of
+{dedup, pull, fwd/bwd, segment-reduce, push, canonical apply, dense sync} ->
+write-back. Workload (config.workload): BASELINE.json configs[1] ("c2"):
+10M-key space, E=16, batch 16384, Zipf(1.0) keys, 100 keys/example, 3-layer
+MLP {8,16,1}, J=4; at N GPUs the same batch is sharded over the N ranks
+(strong scaling, as the reference shards a node's batch over its devices).
+
+  value : examples/s with the batch pool and the value store resident in HBM
+  e2e   : the same through the C ABI with HOST buffers: pinned batch H2D,
+          rows staged from / written back to a pinned host value store
+          (zero-copy), loss D2H — all inside the timed region.
+
+Timing: CUDA events on the tier's own stream around every step, L2 flushed
+(256 MiB write) between steps outside the events, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train examples/sec at 1/2/4/8 B200; pull+push keys/sec and HBM GB/s vs roofline"
+UNIT = "examples/s"
+
+CONFIGS = {
+    "c1": dict(dims=10**6, E=8, B=4096, nnz=100, zipf=False, J=4, layers=(8, 16, 1),
+               text="c1: 1M-key table, E=8, batch 4096, ~100 uniform keys/example, "
+                    "MLP {8,16,1}, J=4"),
+    "c2": dict(dims=10**7, E=16, B=16384, nnz=100, zipf=True, J=4, layers=(8, 16, 1),
+               text="c2: 10M-key table, E=16, batch 16384, Zipf(1.0) keys, 100 keys/example, "
+                    "MLP {8,16,1}, J=4"),
+    "c3": dict(dims=10**8, E=64, B=65536, nnz=100, zipf=False, J=4, layers=(8, 16, 1),
+               text="c3 (SGD, no Adagrad yet): 100M-key table, E=64, batch 65536, "
+                    "100 uniform keys/example, MLP {8,16,1}, J=4"),
+}
+
+L2_FLUSH_BYTES = 256 << 20
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- clocks --
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- reference --
+
+def host_threads() -> int:
+    n = os.cpu_count() or 1
+    p = 1
+    while p * 2 <= min(n, 64):
+        p *= 2
+    return p
+
+
+def run_reference_hot_path(cfgname, steps, warmup, threads, budget_s=60.0):
+    """The reference's own HBM-PS hot path (oracle/_ref, the unmodified
+    headers): one std::thread per simulated device running the device-worker
+    loop (pipeline.hpp:504-566). Returns (examples/s, seconds, batches run)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from native import RefHotPath, RefLib, make_cfg
+
+    c = CONFIGS[cfgname]
+    ref = RefLib()
+    pool = max(1, min(steps + warmup, 4))
+    off, keys, lab = ref.gen_dataset(c["dims"], pool * c["B"], c["nnz"], c["zipf"])
+    cfg = make_cfg(1, threads, c["E"], c["layers"], J=c["J"], det=True)
+    hp = RefHotPath(ref, cfg, c["B"], off, keys, lab)
+    if warmup:
+        hp.run(0, warmup)
+    # bounded sample: full batches until `steps` are done or ~budget_s elapsed
+    ms, done = 0.0, 0
+    while done < steps and (done < 2 or ms < budget_s * 1e3):
+        ms += hp.run(warmup + done, 1)
+        done += 1
+    hp.close()
+    return done * c["B"] / (ms / 1e3), ms / 1e3, done
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    c = CONFIGS[args.config]
+    threads = host_threads()
+    value, secs, done = run_reference_hot_path(args.config, args.steps, min(args.warmup, 1),
+                                               threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs * 1e3 / done, "steps_timed": done, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 params / f64 math",
+        "data": "synthetic (reference gen_dataset, seed 1)",
+        "config": {"workload": c["text"], "dims": c["dims"], "E": c["E"], "batch": c["B"],
+                   "nnz": c["nnz"], "zipf": c["zipf"], "J": c["J"],
+                   "layers": list(c["layers"])},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{done} batches x {c['B']} examples (of {args.steps} "
+                                   f"requested; stops after ~60 s) after 1 warm-up batch, "
+                                   f"{threads} simulated devices (one std::thread each), "
+                                   f"deterministic sync"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- ours --
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2003_05622_b200 as pkg
+
+    c = CONFIGS[args.config]
+    dims, E, B, nnz, J = c["dims"], c["E"], c["B"], c["nnz"], c["J"]
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+
+    # batch pool (identical on every rank: the node's batch stream)
+    P = args.pool
+    off, keys, lab = pkg.gen_dataset(dims, P * B, nnz, zipf=c["zipf"], seed=1)
+    batches = []
+    for b in range(P):
+        o = (off[b * B:(b + 1) * B + 1] - off[b * B]).astype(np.int64)
+        batches.append((o, keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B]))
+    max_keys = max(int(b[0][-1]) for b in batches)
+
+    nccl_id = None
+    if world > 1:
+        obj = [pkg.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    tier = pkg.Tier(nodes=1, devices=world, rank=rank, cuda_device=local_rank, width=E,
+                    layer_dims=c["layers"], minibatches=J, deterministic=args.det,
+                    key_space=dims, max_batch_examples=B, max_batch_keys=max_keys,
+                    nccl_id=nccl_id)
+    stream = torch.cuda.ExternalStream(tier.stream(), device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed_steps(step_fn, n_steps, first):
+        """Returns (sum of per-step event ms, per-step stats list)."""
+        total = 0.0
+        stats = []
+        for i in range(n_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st = step_fn((first + i) % P)
+            e1.record(stream)
+            e1.synchronize()
+            total += e0.elapsed_time(e1)
+            stats.append(st)
+        return total, stats
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---------------- device-resident (value) ----------------
+    dbatches = []
+    for o, k, l in batches:
+        dbatches.append((torch.from_numpy(o).to(dev), torch.from_numpy(k.view(np.int64)).to(dev),
+                         torch.from_numpy(l).to(dev)))
+    dstore = torch.zeros((dims, E), dtype=torch.float32, device=dev)
+    tier.attach_store(dstore.data_ptr(), on_device=True, num_keys=dims)
+
+    def dev_step(b):
+        o, k, l = dbatches[b]
+        return tier.train_batch((o.data_ptr(), B), k.data_ptr(), l.data_ptr(), on_device=True)
+
+    for i in range(args.warmup):
+        dev_step(i % P)
+    barrier()
+    tier.set_timing(True)
+    tier.reset_timing()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    launches0 = tier.kernel_launches()
+    barrier()
+    dev_ms, dev_stats = timed_steps(dev_step, args.steps, args.warmup)
+    barrier()
+    launches = tier.kernel_launches() - launches0
+    clk = clocks.stop()
+    phases = tier.timing()
+    tier.set_timing(False)
+    dev_ms_max = max_over_ranks(dev_ms)
+    value = args.steps * B / (dev_ms_max / 1e3)
+
+    # per-rank work counters over the timed steps
+    pulled = sum(s.pulled_keys for s in dev_stats)
+    ws = sum(s.working_set for s in dev_stats)
+    occ = sum(s.occurrences for s in dev_stats)
+    carried = sum(s.carried_rows for s in dev_stats)
+    loss = sum(s.loss_sum for s in dev_stats) / max(1, sum(s.examples for s in dev_stats))
+
+    # ---------------- end to end through the C ABI, host buffers (e2e) -------
+    e2e = None
+    if not args.no_e2e:
+        hstore_t = torch.zeros((dims, E), dtype=torch.float32).pin_memory()
+        hstore = hstore_t.numpy()
+        tier.attach_store(hstore)
+        hbatches = []
+        for o, k, l in batches:
+            hbatches.append(tuple(torch.from_numpy(x).pin_memory().numpy()
+                                  for x in (o, k.view(np.int64), l)))
+
+        def host_step(b):
+            o, k, l = hbatches[b]
+            return tier.train_batch(o, k.view(np.uint64), l, on_device=False)
+
+        for i in range(args.warmup):
+            host_step(i % P)
+        barrier()
+        e2e_ms, e2e_stats = timed_steps(host_step, args.steps, args.warmup)
+        barrier()
+        e2e_ms_max = max_over_ranks(e2e_ms)
+        h2d = sum(8 * (b[0].size) + 8 * b[1].size + b[2].size for b in
+                  (hbatches[(args.warmup + i) % P] for i in range(args.steps))) / args.steps
+        h2d += sum((s.working_set - s.carried_rows) * E * 4 for s in e2e_stats) / args.steps
+        d2h = sum(s.working_set * E * 4 + 24 for s in e2e_stats) / args.steps
+        e2e = {"value": args.steps * B / (e2e_ms_max / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(sum_over_ranks(h2d)),
+               "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
+               "ms_per_step": e2e_ms_max / args.steps,
+               "path": "hps_train_batch(on_device=0): pinned batch H2D + zero-copy staging "
+                       "from/to a pinned host value store + loss D2H"}
+        tier.attach_store(None)
+        del hstore_t
+
+    # ---------------- roofline of the dominant kernel -----------------------
+    peak, peak_kind = load_peaks()
+    K = args.steps
+    per_key_pull = 8 + 8 + 4 * E + 4 * E   # key + slot probe + row read + row write
+    per_key_apply = 4 + 12 * E             # slot + delta read + row read + row write
+    per_key_build = 8 + 8 + 4 * E + 4 * E
+    phase_bytes = {
+        "pull": pulled * per_key_pull,
+        "apply": pulled * per_key_apply,
+        "build": ws * per_key_build + occ / J * 0,  # table part only
+        "writeback": ws * per_key_pull,
+        "dedup": 12 * occ + 8 * pulled,
+    }
+    rl = {}
+    for name, nbytes in phase_bytes.items():
+        ms = phases.get(name, 0.0)
+        if ms > 0:
+            gbs = nbytes / (ms / 1e3) / 1e9
+            rl[name] = {"ms_per_step": ms / K, "algorithmic_bytes_per_step": nbytes / K,
+                        "achieved_gbs": gbs, "frac": gbs / peak}
+    dominant = os.environ.get("HPS_ROOFLINE_KERNEL", "pull")
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get(args.config, {}).get(dominant)
+        except Exception:
+            traffic = None
+    dom = rl.get(dominant, {})
+    roofline = {"bound": "hbm", "kernel": {"pull": "table_gather_kernel<4>",
+                                           "apply": "table_apply_kernel<4>"}.get(dominant, dominant),
+                "achieved": dom.get("achieved_gbs"), "peak": peak, "unit": "GB/s",
+                "frac": dom.get("frac"), "traffic": traffic, "peak_kind": peak_kind,
+                "bytes_model": {"pull": "U*(8+8+8E)", "apply": "U*(4+12E)"}.get(dominant),
+                "phases": rl}
+
+    # ---------------- CPU baseline (reference hot path, rank 0, N=1) ---------
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = host_threads()
+        try:
+            v, secs, _ = run_reference_hot_path(args.config, 2, 1, threads)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"2 batches x {B} examples of {args.config} after 1 warm-up "
+                             f"batch; reference HbmTier device-worker loop, {threads} "
+                             f"simulated devices (std::threads), flat-map host store",
+                   "seconds": secs}
+        except Exception as ex:  # the reference library is prebuilt here
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    all_launch = int(sum_over_ranks(launches))
+    pull_keys_s = sum_over_ranks(pulled) / (dev_ms_max / 1e3)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 params / f64 math",
+            "data": "synthetic (reference gen_dataset stream, seed 1; random-init dense)",
+            "config": {"workload": c["text"], "dims": dims, "E": E, "global_batch": B,
+                       "nnz": nnz, "zipf": c["zipf"], "J": J, "layers": list(c["layers"]),
+                       "parallelism": f"key-sharded x{world}", "batch_pool": P,
+                       "deterministic": bool(args.det),
+                       "l2": "flushed between steps (256 MiB write, outside the events)"},
+            "e2e": e2e,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": all_launch,
+            "pull_keys_per_s": pull_keys_s,
+            "push_keys_per_s": pull_keys_s,
+            "phase_ms_per_step": {k: v / K for k, v in phases.items()},
+            "train_loss": loss,
+            "carried_rows_per_step": carried / K,
+            "working_set_per_step": ws / K,
+        }
+        print(json.dumps(line), flush=True)
+    tier.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--pool", type=int, default=8, help="distinct batches cycled")
+    ap.add_argument("--det", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -78,7 +78,24 @@ typedef struct {
   uint64_t pulled_keys;      /* sum over mini-batches of unique keys pulled */
   uint64_t served_keys;      /* keys this rank served as owner (pull+push) */
   uint64_t occurrences;      /* key occurrences in this rank's shards */
+  uint64_t carried_rows;     /* build rows taken from the previous table */
 } hps_batch_stats;
+
+/* Phase slots of hps_get_timing (ms accumulated over hps_train_batch calls,
+ * measured with CUDA events on the tier's stream). */
+#define HPS_TIMING_SLOTS 10
+enum {
+  HPS_T_TOTAL = 0,     /* whole batch */
+  HPS_T_STAGE = 1,     /* H2D of the batch + per-shard counts (one D2H) */
+  HPS_T_BUILD = 2,     /* working-set dedup + table build (a1-a4) */
+  HPS_T_DEDUP = 3,     /* mini-batch dedup + owner partition (a5) */
+  HPS_T_PULL = 4,      /* owner probe + row gather (+ all-to-alls) (a6) */
+  HPS_T_FWDBWD = 5,    /* forward/backward (a7, a8) */
+  HPS_T_GRADS = 6,     /* dense-grad reduce + sparse segment-reduce (a8, a9) */
+  HPS_T_APPLY = 7,     /* push exchange + canonical owner apply (a10, a11) */
+  HPS_T_DENSE = 8,     /* dense sync + update (a12) */
+  HPS_T_WRITEBACK = 9  /* rows back to the value store (a13) */
+};
 
 const char* hps_last_error(void);
 const char* hps_version(void);
@@ -174,13 +191,12 @@ hps_status hps_train_batch(hps_tier_t h, uint64_t num_examples,
                            const uint8_t* labels, int on_device,
                            hps_batch_stats* stats);
 
-/* Kernel-level timing of the last hps_train_batch, from CUDA events on the
- * tier's stream (ms): [0] whole batch, [1] working set + build, [2] pull
- * (owner probe+gather incl. exchange), [3] push apply, [4] write-back,
- * [5] mini-batch dedup, [6] fwd/bwd + reductions, [7] dense sync.
- * Enabled by hps_set_timing(h, 1) (adds event records, no syncs). */
+/* Per-phase device time of hps_train_batch (HPS_T_* slots, ms, accumulated
+ * until hps_reset_timing). Enabled by hps_set_timing(h, 1): adds event
+ * records on the tier stream, no extra host synchronisation. */
 hps_status hps_set_timing(hps_tier_t h, int enable);
-hps_status hps_get_timing(hps_tier_t h, double* ms8);
+hps_status hps_get_timing(hps_tier_t h, double* ms /* HPS_TIMING_SLOTS */);
+hps_status hps_reset_timing(hps_tier_t h);
 
 /* Number of kernels this library launched on the handle so far. */
 hps_status hps_kernel_launches(hps_tier_t h, uint64_t* n);

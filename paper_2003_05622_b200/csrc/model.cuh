@@ -164,57 +164,235 @@ __global__ void __launch_bounds__(128)
   if (sub == 0 && loss_acc != 0.0) atomicAdd(loss, loss_acc);
 }
 
-// Dense gradient of the shard: one thread per weight, examples in order,
-// then *1/n and the f32 cast (model.hpp:189-193).
-__global__ void dense_grad_kernel(ModelDims md, std::uint64_t n,
-                                  const double* __restrict__ H,
-                                  const double* __restrict__ DL,
-                                  float* __restrict__ grad) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= md.nw) return;
-  int l = md.L - 1;
-  while (w < md.offs[l]) --l;
-  const int in = md.ins[l], out = md.dims[l], rel = w - md.offs[l];
-  const bool bias = rel >= in * out;
-  const int o = bias ? rel - in * out : rel / in;
-  const int i = bias ? 0 : rel % in;
-  const double* dl = DL + md.doff[l] + o;
-  const double* h = H + md.hoff[l] + i;
-  double acc = 0.0;
-  if (bias) {
-    for (std::uint64_t k = 0; k < n; ++k) acc = __dadd_rn(acc, dl[k * md.dw]);
-  } else {
-    for (std::uint64_t k = 0; k < n; ++k)
-      acc = __dadd_rn(acc, __dmul_rn(dl[k * md.dw], h[k * md.hw]));
-  }
-  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-  grad[w] = __double2float_rn(__dmul_rn(acc, inv_n));
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Sparse gradient segment-reduce + sgd_delta (model.hpp:182-200, 226-230):
-// thread per (unique key, dim); the key's CSR segment lists its
-// occurrences in example order. Writes -(lr * g) into the push buffer row
-// of the key (its position in the owner-partitioned send order).
-__global__ void sparse_delta_kernel(int E, float lr, std::uint64_t n,
-                                    const std::uint64_t* __restrict__ u_ptr,
-                                    const std::uint32_t* __restrict__ seg,
-                                    const std::uint32_t* __restrict__ sorted_occ,
-                                    const std::uint32_t* __restrict__ ex_of_occ,
-                                    const std::uint32_t* __restrict__ pos,  // null: identity
-                                    const double* __restrict__ DX,
-                                    float* __restrict__ out) {
+// Dense gradient of the shard: one thread per weight walks the examples in
+// order (model.hpp:161-175), then *1/n and the f32 cast (model.hpp:189-193).
+// The per-example H/DL records (contiguous per chunk of examples) stream
+// through a kGradStages-deep cp.async ring in shared memory, so the loads of
+// the next chunks overlap each thread's sequential f64 chain.
+constexpr int kGradStages = 4;
+constexpr int kGradThreads = 256;
+
+inline int grad_chunk(const ModelDims& md) {
+  int ch = 64;
+  while (ch > 8 && size_t(kGradStages) * ch * (md.hw + md.dw) * 8 > 200 * 1024) ch >>= 1;
+  return ch;
+}
+inline size_t dense_grad_smem(const ModelDims& md) {
+  return size_t(kGradStages) * grad_chunk(md) * (md.hw + md.dw) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(kGradThreads)
+    dense_grad_kernel(ModelDims md, std::uint64_t n, int chunk,
+                      const double* __restrict__ H, const double* __restrict__ DL,
+                      float* __restrict__ grad) {
+  extern __shared__ double sm[];
+  const int rec = md.hw + md.dw;
+  const int w = blockIdx.x * kGradThreads + threadIdx.x;
+  const bool live = w < md.nw;
+  int hi = 0, di = 0;
+  bool bias = false;
+  if (live) {
+    int l = md.L - 1;
+    while (w < md.offs[l]) --l;
+    const int in = md.ins[l], out = md.dims[l], rel = w - md.offs[l];
+    bias = rel >= in * out;
+    const int o = bias ? rel - in * out : rel / in;
+    di = md.doff[l] + o;
+    hi = md.hoff[l] + (bias ? 0 : rel % in);
+  }
+  const std::uint64_t nchunks = (n + chunk - 1) / chunk;
+  auto issue = [&](std::uint64_t c) {
+    if (c < nchunks) {
+      double* sH = sm + (c % kGradStages) * std::size_t(chunk) * rec;
+      double* sD = sH + std::size_t(chunk) * md.hw;
+      const std::uint64_t k0 = c * chunk;
+      const int cnt = int(n - k0 < std::uint64_t(chunk) ? n - k0 : chunk);
+      const double* gH = H + k0 * md.hw;
+      const double* gD = DL + k0 * md.dw;
+      for (int t = threadIdx.x; t < cnt * md.hw; t += kGradThreads) cp_async8(sH + t, gH + t);
+      for (int t = threadIdx.x; t < cnt * md.dw; t += kGradThreads) cp_async8(sD + t, gD + t);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < kGradStages - 1; ++s) issue(s);
+  double acc = 0.0;
+  for (std::uint64_t c = 0; c < nchunks; ++c) {
+    issue(c + kGradStages - 1);
+    cp_async_wait<kGradStages - 1>();
+    __syncthreads();
+    if (live) {
+      const double* sH = sm + (c % kGradStages) * std::size_t(chunk) * rec;
+      const double* sD = sH + std::size_t(chunk) * md.hw;
+      const std::uint64_t k0 = c * chunk;
+      const int cnt = int(n - k0 < std::uint64_t(chunk) ? n - k0 : chunk);
+      if (bias) {
+#pragma unroll 8
+        for (int k = 0; k < cnt; ++k) acc = __dadd_rn(acc, sD[k * md.dw + di]);
+      } else {
+#pragma unroll 8
+        for (int k = 0; k < cnt; ++k)
+          acc = __dadd_rn(acc, __dmul_rn(sD[k * md.dw + di], sH[k * md.hw + hi]));
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  if (live) {
+    const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+    grad[w] = __double2float_rn(__dmul_rn(acc, inv_n));
+  }
+}
+
+// Sparse gradient segment-reduce + sgd_delta (model.hpp:182-200, 226-230).
+// Per unique key u: sum over its occurrences, in example order, of the
+// example's dL/dx (the CSR segment [seg[u], seg[u+1]) of the stably sorted
+// occurrences; exs[p] = shard example of sorted occurrence p), *1/n, f32,
+// then -(lr * g) into the push row of the key (pos[u], its position in the
+// owner-partitioned send order; identity when pos is null).
+//
+// Short segments (<= kLongSeg): LPK lanes per key; each round the group loads
+// up to 8 example ids, every lane issues its 8 independent DX loads into
+// registers, then adds them in order. Longer segments (hot Zipf keys: up to
+// the whole shard) are queued for sparse_delta_long_kernel.
+constexpr int kLongSeg = 64;
+constexpr int kStageDepth = 8;
+
+__device__ __forceinline__ void write_delta(float* out, std::uint64_t row, int E, int d,
+                                            double acc, double inv_n, float lr) {
+  const float g = __double2float_rn(__dmul_rn(acc, inv_n));
+  out[row * E + d] = -__fmul_rn(lr, g);
+}
+
+template <int LPK, int kDPL>
+__global__ void __launch_bounds__(256)
+    sparse_delta_kernel(int E, float lr, std::uint64_t n,
+                        const std::uint64_t* __restrict__ u_ptr,
+                        const std::uint32_t* __restrict__ seg,
+                        const std::uint32_t* __restrict__ exs,
+                        const std::uint32_t* __restrict__ pos,
+                        const double* __restrict__ DX, float* __restrict__ out,
+                        unsigned long long* __restrict__ pulled,
+                        std::uint32_t* __restrict__ long_list,
+                        unsigned long long* __restrict__ n_long) {
   const std::uint64_t U = *u_ptr;
+  if (pulled && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(pulled, (unsigned long long)U);
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
-       t < U * E; t += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint64_t u = t / E;
-    const int d = int(t - u * E);
+  const int sub = threadIdx.x % LPK;
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned gmask =
+      LPK == 32 ? 0xFFFFFFFFu : (((1u << LPK) - 1u) << (lane / LPK * LPK));
+  constexpr int SD = LPK < kStageDepth ? LPK : kStageDepth;  // ids come from SD lanes
+  const std::uint64_t groups = (std::uint64_t(gridDim.x) * blockDim.x) / LPK;
+  for (std::uint64_t u = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) / LPK; u < U;
+       u += groups) {
+    const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
+    if (p1 - p0 > std::uint32_t(kLongSeg)) {
+      if (sub == 0) long_list[atomicAdd(n_long, 1ull)] = std::uint32_t(u);
+      continue;
+    }
+    double acc[kDPL];
+#pragma unroll
+    for (int q = 0; q < kDPL; ++q) acc[q] = 0.0;
+    for (std::uint32_t c = p0; c < p1; c += SD) {
+      const int len = int(p1 - c < std::uint32_t(SD) ? p1 - c : SD);
+      const std::uint32_t my_ex = sub < len ? exs[c + sub] : 0u;
+      double v[SD][kDPL];
+#pragma unroll
+      for (int r = 0; r < SD; ++r) {
+        const std::uint64_t ex = __shfl_sync(gmask, my_ex, r, LPK);
+        const double* row = DX + ex * std::uint64_t(E);
+#pragma unroll
+        for (int q = 0; q < kDPL; ++q) {
+          const int d = sub + q * LPK;
+          v[r][q] = (r < len && d < E) ? row[d] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < SD; ++r)
+        if (r < len) {
+#pragma unroll
+          for (int q = 0; q < kDPL; ++q) acc[q] = __dadd_rn(acc[q], v[r][q]);
+        }
+    }
+    const std::uint64_t orow = pos ? pos[u] : u;
+#pragma unroll
+    for (int q = 0; q < kDPL; ++q) {
+      const int d = sub + q * LPK;
+      if (d < E) write_delta(out, orow, E, d, acc[q], inv_n, lr);
+    }
+  }
+}
+
+// Long segments: one CTA per key. All threads stream the segment's DX rows
+// through a double-buffered cp.async ring ([chunk][E] doubles); the first E
+// threads run the sequential f64 sums from shared memory.
+constexpr int kLongThreads = 256;
+
+inline int long_chunk(int E) {
+  int ch = 512;
+  while (ch > 32 && size_t(2) * ch * E * 8 > 160 * 1024) ch >>= 1;
+  return ch;
+}
+
+__global__ void __launch_bounds__(kLongThreads)
+    sparse_delta_long_kernel(int E, float lr, std::uint64_t n, int chunk,
+                             const std::uint32_t* __restrict__ long_list,
+                             const unsigned long long* __restrict__ n_long,
+                             const std::uint32_t* __restrict__ seg,
+                             const std::uint32_t* __restrict__ exs,
+                             const std::uint32_t* __restrict__ pos,
+                             const double* __restrict__ DX, float* __restrict__ out) {
+  extern __shared__ double sm[];
+  const unsigned long long NL = *n_long;
+  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  for (unsigned long long li = blockIdx.x; li < NL; li += gridDim.x) {
+    const std::uint32_t u = long_list[li];
+    const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
+    const std::uint32_t nch = (p1 - p0 + chunk - 1) / chunk;
+    auto issue = [&](std::uint32_t c) {
+      if (c < nch) {
+        double* buf = sm + std::size_t(c & 1) * chunk * E;
+        const std::uint32_t b = p0 + c * chunk;
+        const int cnt = int(p1 - b < std::uint32_t(chunk) ? p1 - b : chunk);
+        for (int t = threadIdx.x; t < cnt * E; t += kLongThreads) {
+          const int r = t / E, d = t - r * E;
+          cp_async8(buf + t, DX + std::uint64_t(exs[b + r]) * E + d);
+        }
+      }
+      cp_async_commit();
+    };
+    issue(0);
     double acc = 0.0;
-    for (std::uint32_t p = seg[u], pe = seg[u + 1]; p < pe; ++p)
-      acc = __dadd_rn(acc, DX[std::uint64_t(ex_of_occ[sorted_occ[p]]) * E + d]);
-    const float g = __double2float_rn(__dmul_rn(acc, inv_n));
-    const std::uint64_t row = pos ? pos[u] : u;
-    out[row * E + d] = -__fmul_rn(lr, g);
+    for (std::uint32_t c = 0; c < nch; ++c) {
+      issue(c + 1);
+      cp_async_wait<1>();
+      __syncthreads();
+      if (int(threadIdx.x) < E) {
+        const double* buf = sm + std::size_t(c & 1) * chunk * E;
+        const std::uint32_t b = p0 + c * chunk;
+        const int cnt = int(p1 - b < std::uint32_t(chunk) ? p1 - b : chunk);
+#pragma unroll 8
+        for (int r = 0; r < cnt; ++r) acc = __dadd_rn(acc, buf[r * E + threadIdx.x]);
+      }
+      __syncthreads();
+    }
+    cp_async_wait<0>();
+    if (int(threadIdx.x) < E)
+      write_delta(out, pos ? pos[u] : u, E, threadIdx.x, acc, inv_n, lr);
+    __syncthreads();
   }
 }
 

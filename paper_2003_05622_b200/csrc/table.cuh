@@ -85,7 +85,7 @@ __global__ void table_fill_kernel(
     const std::uint32_t* __restrict__ staged_idx,    // null: no staged rows
     const float* __restrict__ staged_rows,
     const float* __restrict__ store, std::uint64_t store_keys, int E,
-    DevError* err) {
+    unsigned long long* carried, DevError* err) {
   const int tpk = E / VEC;
   const std::uint64_t n = *n_ptr, cap = *cap_ptr;
   const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
@@ -104,6 +104,11 @@ __global__ void table_fill_kernel(
     if (pcap) {
       const std::uint32_t ps = probe_slot(prev_keys, pcap, key);
       if (ps != kNoSlot) src = prev_vals + std::uint64_t(ps) * E;
+    }
+    if (carried) {  // warp-aggregated count of carry-over rows
+      const unsigned hit = __ballot_sync(__activemask(), src != nullptr && part == 0);
+      if (hit && (threadIdx.x & 31) == unsigned(__ffs(__activemask()) - 1))
+        atomicAdd(carried, (unsigned long long)__popc(hit));
     }
     if (!src && staged_rows) src = staged_rows + std::uint64_t(staged_idx[i]) * E;
     if (!src && store && key < store_keys) src = store + key * std::uint64_t(E);

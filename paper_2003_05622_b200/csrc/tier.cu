@@ -102,6 +102,10 @@ struct Scalars {
   std::uint64_t counts[66];    // batch_count: per-mb occurrences, owned keys
   std::uint64_t send_off[257]; // owner partition offsets (G+1)
   double loss;
+  unsigned long long pulled;   // sum over mini-batches of unique keys pulled
+  unsigned long long carried;  // rows filled from the previous table
+  unsigned long long n_long;   // long CSR segments queued this mini-batch
+  int err_any;                 // error code max-reduced over ranks
   DevError err;
 };
 
@@ -152,7 +156,8 @@ struct Tier {
   std::uint32_t *occ_off = nullptr, *ex_of = nullptr, *inv = nullptr,
                 *seg = nullptr, *uidv = nullptr, *pos = nullptr,
                 *occ_row = nullptr, *slots = nullptr, *rslots = nullptr,
-                *puid = nullptr, *cnt32 = nullptr, *cnt_all = nullptr;
+                *puid = nullptr, *cnt32 = nullptr, *cnt_all = nullptr, *exs = nullptr,
+                *long_list = nullptr;
   std::uint64_t *ukeys = nullptr, *pkeys = nullptr, *rkeys = nullptr;
   float *rows = nullptr, *deltas = nullptr, *rrows = nullptr,
         *rdeltas = nullptr, *staged = nullptr;
@@ -170,10 +175,11 @@ struct Tier {
 
   std::vector<PendingChunk> pending;
 
-  // timing
+  // timing: events recorded at phase boundaries on the tier stream
   bool timing = false;
-  cudaEvent_t ev[16] = {};
-  double acc_ms[8] = {0};
+  std::vector<cudaEvent_t> evpool;
+  std::vector<int> ev_phase;
+  double acc_ms[HPS_TIMING_SLOTS] = {0};
 
   std::vector<void*> allocs;
 };
@@ -230,12 +236,29 @@ static void launch(Tier* t, void (*k)(KArgs...), dim3 grid, dim3 block,
 
 static const char* missing_msg_context = "device table: missing key ";
 
-// Maps the device error word to the reference's hps::Error texts.
-static hps_status check_device_error(Tier* t, const char* missing_ctx) {
+// Maps the device error word to the reference's hps::Error texts. With
+// collective = true (calls every rank makes in lockstep) the error code is
+// max-reduced over ranks first, so an owner-side failure (e.g. a missing key
+// requested by a peer) makes every rank raise instead of diverging.
+static hps_status check_device_error(Tier* t, const char* missing_ctx,
+                                     bool collective = false) {
+  if (collective && t->G > 1) {
+    HPS_CUDA(cudaMemcpyAsync(&t->dsc->err_any, &t->dsc->err.code, sizeof(int),
+                             cudaMemcpyDeviceToDevice, t->st));
+    ncclResult_t r = nccl().AllReduce(&t->dsc->err_any, &t->dsc->err_any, 1, ncclInt32, ncclMax,
+                                      t->comm, t->st);
+    if (r != ncclSuccess)
+      return set_error(HPS_ERR_NCCL, "nccl: %s", nccl().GetErrorString(r));
+    HPS_CUDA(cudaMemcpyAsync(&t->hsc->err_any, &t->dsc->err_any, sizeof(int),
+                             cudaMemcpyDeviceToHost, t->st));
+  }
   HPS_CUDA(cudaMemcpyAsync(&t->hsc->err, &t->dsc->err, sizeof(DevError),
                            cudaMemcpyDeviceToHost, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
   const DevError e = t->hsc->err;
+  if (e.code == 0 && collective && t->G > 1 && t->hsc->err_any != 0)
+    return set_error(hps_status(t->hsc->err_any),
+                     "hbm: a peer rank failed this collective (status %d)", t->hsc->err_any);
   if (e.code == 0) return HPS_OK;
   HPS_CUDA(cudaMemsetAsync(&t->dsc->err, 0, sizeof(DevError), t->st));
   const unsigned long long k = e.key;
@@ -450,9 +473,13 @@ struct UniqueEmit {  // inverse index + CSR segments of a sorted (key, occ) list
   std::uint64_t* ukeys;
   std::uint32_t* seg;
   std::uint32_t* uidv;
+  const std::uint32_t* ex_of;  // occurrence -> shard example (null: none)
+  std::uint32_t* exs;          // sorted position -> shard example
   __device__ void operator()(std::uint64_t p, std::uint32_t v, std::uint64_t pre) const {
     const std::uint64_t uid = pre + v - 1;
-    inv[so[p]] = std::uint32_t(uid);
+    const std::uint32_t occ = so[p];
+    inv[occ] = std::uint32_t(uid);
+    if (ex_of) exs[p] = ex_of[occ];
     if (v) {
       ukeys[uid] = sk[p];
       seg[uid] = std::uint32_t(p);
@@ -579,8 +606,36 @@ static std::vector<int> canonical_senders(const Tier* t) {
 
 // ------------------------------------------------------------- timing --
 
-static void mark(Tier* t, int i) {
-  if (t->timing) cudaEventRecord(t->ev[i], t->st);
+// Records the end of `phase` (the start of the next one).
+static void mark(Tier* t, int phase) {
+  if (!t->timing) return;
+  const std::size_t i = t->ev_phase.size();
+  if (i == t->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    t->evpool.push_back(e);
+  }
+  cudaEventRecord(t->evpool[i], t->st);
+  t->ev_phase.push_back(phase);
+}
+
+static void timing_begin(Tier* t) {
+  t->ev_phase.clear();
+  mark(t, -1);
+}
+
+// After the stream is idle: fold the recorded phases into acc_ms.
+static void timing_end(Tier* t) {
+  if (!t->timing || t->ev_phase.size() < 2) return;
+  for (std::size_t i = 1; i < t->ev_phase.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t->evpool[i - 1], t->evpool[i]);
+    const int p = t->ev_phase[i];
+    if (p > 0 && p < HPS_TIMING_SLOTS) t->acc_ms[p] += ms;
+  }
+  float tot = 0;
+  cudaEventElapsedTime(&tot, t->evpool[0], t->evpool[t->ev_phase.size() - 1]);
+  t->acc_ms[0] += tot;
 }
 
 // -------------------------------------------------------------- build --
@@ -608,13 +663,13 @@ static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* sta
            (const std::uint64_t*)&t->dsc->n_ws, (const std::uint64_t*)t->tkeys[nxt],
            t->tvals[nxt], (const std::uint64_t*)&t->dsc->cap[nxt], pk, pv, pcap,
            staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->E,
-           &t->dsc->err);
+           &t->dsc->carried, &t->dsc->err);
   else
     launch(t, table_fill_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
            (const std::uint64_t*)&t->dsc->n_ws, (const std::uint64_t*)t->tkeys[nxt],
            t->tvals[nxt], (const std::uint64_t*)&t->dsc->cap[nxt], pk, pv, pcap,
            staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->E,
-           &t->dsc->err);
+           &t->dsc->carried, &t->dsc->err);
   cudaMemcpyAsync(&t->dsc->nws_tab[nxt], &t->dsc->n_ws, 8, cudaMemcpyDeviceToDevice, t->st);
   t->has_prev = prv >= 0;
   t->cur = nxt;
@@ -635,18 +690,22 @@ struct PullPlan {
 };
 
 static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
-                             std::uint64_t n, PullPlan* plan, bool do_gather) {
+                             std::uint64_t n, PullPlan* plan, bool do_gather,
+                             bool with_examples = false) {
   std::uint64_t* sk = nullptr;
   std::uint32_t* so = nullptr;
   radix_sort(t, kin, vin, Count{nullptr, n}, n, t->sort_bits, true, &sk, &so);
   plan->so = so;
   if (n > 0)
-    tile_scan(t, RunStart{sk}, UniqueEmit{sk, so, n, t->inv, t->ukeys, t->seg, t->uidv},
+    tile_scan(t, RunStart{sk},
+              UniqueEmit{sk, so, n, t->inv, t->ukeys, t->seg, t->uidv,
+                         with_examples ? t->ex_of : nullptr, t->exs},
               Count{nullptr, n}, n, &t->dsc->U);
   else
     HPS_CUDA(cudaMemsetAsync(&t->dsc->U, 0, 8, t->st));
   const int V = vec_of(t->E);
   if (t->G == 1) {
+    mark(t, HPS_T_DEDUP);
     plan->pos = nullptr;
     if (do_gather) {
       const std::uint64_t work = n * std::uint64_t(t->E / V);
@@ -662,6 +721,7 @@ static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint3
                std::uint64_t(0), (const std::uint64_t*)t->tkeys[t->cur],
                (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
                t->rows, t->slots, t->E, &t->dsc->err);
+      mark(t, HPS_T_PULL);
     }
     return HPS_OK;
   }
@@ -671,6 +731,7 @@ static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint3
          (const std::uint64_t*)&t->dsc->U, t->pos);
   plan->pos = t->pos;
   HPS_TRY(exchange_counts(t, plan->soff, plan->roff));
+  mark(t, HPS_T_DEDUP);
   plan->R = plan->roff[t->G];
   HPS_TRY(alltoallv(t, t->pkeys, plan->soff, t->rkeys, plan->roff, 8));
   if (do_gather) {
@@ -691,6 +752,7 @@ static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint3
     }
     HPS_TRY(alltoallv(t, t->rrows, plan->roff, t->rows, plan->soff,
                       sizeof(float) * std::size_t(t->E)));
+    mark(t, HPS_T_PULL);
   }
   return HPS_OK;
 }
@@ -746,6 +808,41 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
            (const float*)t->dgather, nw, 0, t->G, t->cfg.learning_rate, int(apply),
            (float*)nullptr, &t->dsc->err);
   }
+  return HPS_OK;
+}
+
+// Sparse segment-reduce launches: LPK lanes per short segment (pow2 >= E,
+// 4..32), then one CTA per long segment.
+static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint32_t* pos,
+                                      std::uint64_t u_upper) {
+  const int E = t->E;
+  if (E > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
+  int lpk = 4;
+  while (lpk < E && lpk < 32) lpk <<= 1;
+  const std::uint64_t threads = std::max<std::uint64_t>(u_upper, 1) * lpk;
+  const unsigned grid = grid_for(threads, 256, kSMs * 32);
+  const float lr = t->cfg.learning_rate;
+  const std::uint64_t* U = &t->dsc->U;
+  const std::uint32_t* seg = t->seg;
+  const std::uint32_t* exs = t->exs;
+  const double* DX = t->DX;
+  unsigned long long* pulled = &t->dsc->pulled;
+  unsigned long long* nl = &t->dsc->n_long;
+  HPS_CUDA(cudaMemsetAsync(nl, 0, 8, t->st));
+#define HPS_SD(L, Q)                                                                    \
+  launch(t, sparse_delta_kernel<L, Q>, grid, 256, 0, E, lr, n, U, seg, exs, pos, DX,    \
+         t->deltas, pulled, t->long_list, nl)
+  if (lpk == 4) HPS_SD(4, 1);
+  else if (lpk == 8) HPS_SD(8, 1);
+  else if (lpk == 16) HPS_SD(16, 1);
+  else if (E <= 32) HPS_SD(32, 1);
+  else if (E <= 64) HPS_SD(32, 2);
+  else HPS_SD(32, 8);
+#undef HPS_SD
+  const int ch = long_chunk(E);
+  launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, size_t(2) * ch * E * 8, E, lr, n,
+         ch, (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos,
+         DX, t->deltas);
   return HPS_OK;
 }
 
@@ -856,8 +953,22 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
                           cudaGetErrorString(e)));
   if ((e = cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking)) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: stream: %s", cudaGetErrorString(e)));
-  for (auto& ev : t->ev) cudaEventCreate(&ev);
 
+  {
+    // dynamic shared memory of the model kernels (per-example scratch, streamed records)
+    const int big = 200 * 1024;
+    const size_t need_grad = dense_grad_smem(t->md);
+    const size_t need_fwd = size_t((t->md.nw + 1) & ~1) * 4 +
+                            size_t(16) * (t->md.hw + t->md.dw + t->md.maxw) * 8;
+    if (need_grad > size_t(big) || need_fwd > size_t(big))
+      return fail(set_error(HPS_ERR_ARG, "dense model too large for the fused kernels"));
+    cudaFuncSetAttribute(dense_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(sparse_delta_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         big);
+    cudaFuncSetAttribute(fwd_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(fwd_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(fwd_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  }
   const std::uint64_t O = t->Omax, W = t->Wmax, E = std::uint64_t(t->E);
   hps_status s = HPS_OK;
 #define A(ptr, n) \
@@ -893,6 +1004,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(slots, S);
   A(rslots, S);
   A(puid, S);
+  A(exs, S);
+  A(long_list, S);
   A(cnt32, 256);
   A(cnt_all, 256 * 256);
   A(ukeys, S);
@@ -943,8 +1056,7 @@ hps_status hps_destroy(hps_tier_t t) {
   for (void* p : t->allocs) cudaFree(p);
   if (t->hsc) cudaFreeHost(t->hsc);
   if (t->store_registered) cudaHostUnregister(t->store_host);
-  for (auto& ev : t->ev)
-    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : t->evpool) cudaEventDestroy(ev);
   if (t->st) cudaStreamDestroy(t->st);
   delete t;
   return HPS_OK;
@@ -1007,7 +1119,7 @@ hps_status hps_pull(hps_tier_t t, const uint64_t* keys, uint64_t n, float* out_r
   }
   PullPlan plan;
   HPS_TRY(dedup_pull(t, t->kB, t->vB, n, &plan, true));
-  HPS_TRY(check_device_error(t, "device table: missing key "));
+  HPS_TRY(check_device_error(t, "device table: missing key ", true));
   if (n) {
     launch(t, scatter_rows_kernel, grid_for(n * t->E), 256, 0, (const std::uint32_t*)t->inv,
            plan.pos, n, t->E, (const float*)t->rows, t->deltas);
@@ -1237,9 +1349,15 @@ hps_status hps_set_timing(hps_tier_t t, int enable) {
   return HPS_OK;
 }
 
-hps_status hps_get_timing(hps_tier_t t, double* ms8) {
-  if (!t || !ms8) return set_error(HPS_ERR_ARG, "null argument");
-  for (int i = 0; i < 8; ++i) ms8[i] = t->acc_ms[i];
+hps_status hps_get_timing(hps_tier_t t, double* ms) {
+  if (!t || !ms) return set_error(HPS_ERR_ARG, "null argument");
+  for (int i = 0; i < HPS_TIMING_SLOTS; ++i) ms[i] = t->acc_ms[i];
+  return HPS_OK;
+}
+
+hps_status hps_reset_timing(hps_tier_t t) {
+  if (!t) return set_error(HPS_ERR_ARG, "null handle");
+  for (double& v : t->acc_ms) v = 0;
   return HPS_OK;
 }
 
@@ -1269,7 +1387,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   const int G = T->G, J = T->J, E = T->E;
   const std::uint64_t GJ = std::uint64_t(G) * J;
   // ---- stage the batch
-  mark(T, 0);
+  timing_begin(T);
   const std::int64_t* doff = offsets;
   const std::uint64_t* dkeys = keys;
   const std::uint8_t* dlab = labels;
@@ -1288,15 +1406,16 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   }
   // ---- counts (one host round-trip per batch)
   HPS_CUDA(cudaMemsetAsync(T->dsc->counts, 0, sizeof(T->dsc->counts), T->st));
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 8, T->st));
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 8 * 3, T->st));  // loss, pulled, carried
   launch(T, batch_count_kernel, kSMs * 4, 256, 0, doff, dkeys, std::uint64_t(B), G, T->g, J,
          T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts, &T->dsc->err);
   HPS_CUDA(cudaMemcpyAsync(T->hsc->counts, T->dsc->counts, sizeof(T->dsc->counts),
                            cudaMemcpyDeviceToHost, T->st));
-  HPS_TRY(check_device_error(T, "device table: missing key "));
+  HPS_TRY(check_device_error(T, "device table: missing key ", true));
   std::uint64_t occ_total = 0;
   for (int j = 0; j < J; ++j) occ_total += T->hsc->counts[j];
   const std::uint64_t own = T->hsc->counts[J];
+  mark(T, HPS_T_STAGE);
   if (own > T->Wmax || occ_total > T->Omax)
     return set_error(HPS_ERR_CAPACITY, "train_batch: batch exceeds configured maxima");
   // ---- working set (a1, a2) + build (a3, a4)
@@ -1336,10 +1455,10 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
     }
     build_table(T, nsort, nullptr, nullptr);
   }
-  mark(T, 1);
+  mark(T, HPS_T_BUILD);
   // ---- mini-batches
   const int V = vec_of(E);
-  std::uint64_t pulled = 0, served = 0;
+  std::uint64_t served = 0;
   for (int j = 0; j < J; ++j) {
     const std::uint64_t s = std::uint64_t(T->g) * J + j;
     const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
@@ -1352,10 +1471,8 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
       launch(T, shard_gather_kernel, grid_for(n * 32), 256, 0, sm, doff, dkeys,
              (const std::uint32_t*)T->occ_off, T->kB, T->vB, T->ex_of);
     }
-    mark(T, 2);
     PullPlan plan;
-    HPS_TRY(dedup_pull(T, T->kB, T->vB, On, &plan, true));
-    mark(T, 3);
+    HPS_TRY(dedup_pull(T, T->kB, T->vB, On, &plan, true, true));
     // compute (a7, a8, a9)
     const std::uint32_t* occ_row = T->inv;
     if (G > 1 && On) {
@@ -1373,16 +1490,15 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
       launch(T, k, blocks, 128, smem, T->md, sm, (const float*)T->dense,
              (const std::uint32_t*)T->occ_off, occ_row, (const float*)T->rows, dlab, T->H,
              T->DL, T->DX, &T->dsc->loss, &T->dsc->err);
-      launch(T, dense_grad_kernel, (T->md.nw + 127) / 128, 128, 0, T->md, n,
+      mark(T, HPS_T_FWDBWD);
+      launch(T, dense_grad_kernel, (T->md.nw + kGradThreads - 1) / kGradThreads,
+             kGradThreads, dense_grad_smem(T->md), T->md, n, grad_chunk(T->md),
              (const double*)T->H, (const double*)T->DL, T->dgrad);
-      launch(T, sparse_delta_kernel, grid_for(On * E), 256, 0, E, T->cfg.learning_rate, n,
-             (const std::uint64_t*)&T->dsc->U, (const std::uint32_t*)T->seg,
-             (const std::uint32_t*)plan.so, (const std::uint32_t*)T->ex_of, plan.pos,
-             (const double*)T->DX, T->deltas);
+      HPS_TRY(launch_sparse_delta(T, n, plan.pos, On));
     } else {
       HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));
     }
-    mark(T, 4);
+    mark(T, HPS_T_GRADS);
     // push + canonical apply (a10, a11)
     if (G == 1) {
       if (On) {
@@ -1404,13 +1520,12 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
       HPS_TRY(push_apply(T, plan));
       served += 2 * plan.R;
     }
-    mark(T, 5);
+    mark(T, HPS_T_APPLY);
     // dense sync + update (a12), with the verification fault knob
     const std::int64_t global_mb = T->step * J + j;
     const bool skip = global_mb == T->cfg.inject_skip_sync;
     if (!skip) HPS_TRY(dense_sync_update(T, true));
-    mark(T, 6);
-    pulled += 0;  // device-side U; reported through stats below
+    mark(T, HPS_T_DENSE);
   }
   // ---- write-back to the value store (a13)
   if (T->store) {
@@ -1426,19 +1541,13 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
              (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
              T->store_keys, (float*)nullptr, E, &T->dsc->err);
   }
-  mark(T, 7);
-  HPS_CUDA(cudaMemcpyAsync(&T->hsc->loss, &T->dsc->loss, 8, cudaMemcpyDeviceToHost, T->st));
+  mark(T, HPS_T_WRITEBACK);
+  HPS_CUDA(cudaMemcpyAsync(&T->hsc->loss, &T->dsc->loss, 8 * 3, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&T->hsc->n_ws, &T->dsc->n_ws, 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(T->hsc->cap, T->dsc->cap, 16, cudaMemcpyDeviceToHost, T->st));
-  HPS_TRY(check_device_error(T, "device table: missing key "));
+  HPS_TRY(check_device_error(T, "device table: missing key ", true));
   ++T->step;
-  if (T->timing) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, T->ev[0], T->ev[7]);
-    T->acc_ms[0] += ms;
-    cudaEventElapsedTime(&ms, T->ev[0], T->ev[1]);
-    T->acc_ms[1] += ms;
-  }
+  timing_end(T);
   if (stats) {
     stats->loss_sum = T->hsc->loss;
     std::uint64_t ex = 0;
@@ -1449,7 +1558,8 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
     stats->examples = ex;
     stats->working_set = T->hsc->n_ws;
     stats->table_capacity = T->hsc->cap[T->cur];
-    stats->pulled_keys = pulled;
+    stats->pulled_keys = T->hsc->pulled;
+    stats->carried_rows = T->hsc->carried;
     stats->served_keys = served;
     stats->occurrences = occ_total;
   }

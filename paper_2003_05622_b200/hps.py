@@ -72,7 +72,11 @@ class HpsBatchStats(ctypes.Structure):
         ("pulled_keys", ctypes.c_uint64),
         ("served_keys", ctypes.c_uint64),
         ("occurrences", ctypes.c_uint64),
+        ("carried_rows", ctypes.c_uint64),
     ]
+
+TIMING_SLOTS = ["total", "stage", "build", "dedup", "pull", "fwdbwd", "grads", "apply",
+                "dense", "writeback"]
 
 
 # Every symbol include/hps_gpu.h declares, with its ctypes signature.
@@ -101,6 +105,7 @@ _SIGS = {
                          ctypes.POINTER(HpsBatchStats)], ctypes.c_int),
     "hps_set_timing": ([_P, ctypes.c_int], ctypes.c_int),
     "hps_get_timing": ([_P, _P], ctypes.c_int),
+    "hps_reset_timing": ([_P], ctypes.c_int),
     "hps_kernel_launches": ([_P, _U64P], ctypes.c_int),
     "hps_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "hps_gen_dataset": ([_U64, _U64, _U64, ctypes.c_int, ctypes.c_double, _U64,
@@ -313,7 +318,10 @@ class Tier:
     def attach_store(self, rows, on_device: bool = False, num_keys: Optional[int] = None):
         """rows: host numpy float32 [num_keys, E] (kept alive here) or a device
         pointer (int) with num_keys."""
-        if on_device:
+        if rows is None:
+            _check(lib().hps_attach_store(self._h, None, 0, 0))
+            self._store = None
+        elif on_device:
             _check(lib().hps_attach_store(self._h, ctypes.c_void_p(int(rows)), int(num_keys), 1))
             self._store = rows
         else:
@@ -340,10 +348,13 @@ class Tier:
     def set_timing(self, on: bool) -> None:
         _check(lib().hps_set_timing(self._h, int(on)))
 
-    def timing(self) -> List[float]:
-        buf = (ctypes.c_double * 8)()
+    def timing(self) -> Dict[str, float]:
+        buf = (ctypes.c_double * len(TIMING_SLOTS))()
         _check(lib().hps_get_timing(self._h, buf))
-        return list(buf)
+        return dict(zip(TIMING_SLOTS, buf))
+
+    def reset_timing(self) -> None:
+        _check(lib().hps_reset_timing(self._h))
 
     def kernel_launches(self) -> int:
         n = ctypes.c_uint64()
