@@ -176,29 +176,69 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// ---- TMA bulk copy + mbarrier helpers (sm_90+/sm_100a async proxy) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         std::uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 // Dense gradient of the shard: one thread per weight walks the examples in
 // order (model.hpp:161-175), then *1/n and the f32 cast (model.hpp:189-193).
-// The per-example H/DL records (contiguous per chunk of examples) stream
-// through a kGradStages-deep cp.async ring in shared memory, so the loads of
-// the next chunks overlap each thread's sequential f64 chain.
+// 128 threads = one warp per SM sub-partition, so each weight's f64 chain
+// issues at the DADD latency. The per-example H/DL records (contiguous per
+// chunk of examples) arrive through a kGradStages-deep ring of TMA bulk
+// copies (one elected thread, mbarrier completion), off the consumers' issue
+// slots. H/DL are padded by 2 doubles so chunk sizes round up to 16 B.
 constexpr int kGradStages = 4;
-constexpr int kGradThreads = 256;
+constexpr int kGradThreads = 128;
 
 inline int grad_chunk(const ModelDims& md) {
   int ch = 64;
-  while (ch > 8 && size_t(kGradStages) * ch * (md.hw + md.dw) * 8 > 200 * 1024) ch >>= 1;
+  while (ch > 8 && size_t(kGradStages) * ch * (md.hw + md.dw) * 8 + 64 > 200 * 1024) ch >>= 1;
   return ch;
 }
 inline size_t dense_grad_smem(const ModelDims& md) {
-  return size_t(kGradStages) * grad_chunk(md) * (md.hw + md.dw) * sizeof(double);
+  return size_t(kGradStages) * grad_chunk(md) * (md.hw + md.dw) * sizeof(double) + 64;
 }
 
 __global__ void __launch_bounds__(kGradThreads)
     dense_grad_kernel(ModelDims md, std::uint64_t n, int chunk,
                       const double* __restrict__ H, const double* __restrict__ DL,
                       float* __restrict__ grad) {
-  extern __shared__ double sm[];
-  const int rec = md.hw + md.dw;
+  extern __shared__ __align__(128) double sm[];
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sm);  // kGradStages barriers
+  double* ring = sm + 8;                                          // 64 B header
+  const int hw = md.hw, dw = md.dw;
+  const std::size_t stage_elems = std::size_t(chunk) * (hw + dw);
   const int w = blockIdx.x * kGradThreads + threadIdx.x;
   const bool live = w < md.nw;
   int hi = 0, di = 0;
@@ -213,43 +253,44 @@ __global__ void __launch_bounds__(kGradThreads)
     hi = md.hoff[l] + (bias ? 0 : rel % in);
   }
   const std::uint64_t nchunks = (n + chunk - 1) / chunk;
-  auto issue = [&](std::uint64_t c) {
-    if (c < nchunks) {
-      double* sH = sm + (c % kGradStages) * std::size_t(chunk) * rec;
-      double* sD = sH + std::size_t(chunk) * md.hw;
-      const std::uint64_t k0 = c * chunk;
-      const int cnt = int(n - k0 < std::uint64_t(chunk) ? n - k0 : chunk);
-      const double* gH = H + k0 * md.hw;
-      const double* gD = DL + k0 * md.dw;
-      for (int t = threadIdx.x; t < cnt * md.hw; t += kGradThreads) cp_async8(sH + t, gH + t);
-      for (int t = threadIdx.x; t < cnt * md.dw; t += kGradThreads) cp_async8(sD + t, gD + t);
-    }
-    cp_async_commit();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kGradStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](std::uint64_t c) {  // thread 0 only
+    double* sH = ring + (c % kGradStages) * stage_elems;
+    double* sD = sH + std::size_t(chunk) * hw;
+    const std::uint64_t k0 = c * chunk;
+    const unsigned cnt = unsigned(n - k0 < std::uint64_t(chunk) ? n - k0 : chunk);
+    const unsigned bh = (cnt * hw * 8u + 15u) & ~15u, bd = (cnt * dw * 8u + 15u) & ~15u;
+    std::uint64_t* bar = &full[c % kGradStages];
+    mbar_expect_tx(bar, bh + bd);
+    bulk_g2s(sH, H + k0 * hw, bh, bar);
+    bulk_g2s(sD, DL + k0 * dw, bd, bar);
   };
-#pragma unroll
-  for (int s = 0; s < kGradStages - 1; ++s) issue(s);
+  if (threadIdx.x == 0)
+    for (std::uint64_t c = 0; c < nchunks && c < std::uint64_t(kGradStages); ++c) issue(c);
   double acc = 0.0;
   for (std::uint64_t c = 0; c < nchunks; ++c) {
-    issue(c + kGradStages - 1);
-    cp_async_wait<kGradStages - 1>();
-    __syncthreads();
+    mbar_wait(&full[c % kGradStages], unsigned((c / kGradStages) & 1));
     if (live) {
-      const double* sH = sm + (c % kGradStages) * std::size_t(chunk) * rec;
-      const double* sD = sH + std::size_t(chunk) * md.hw;
+      const double* sH = ring + (c % kGradStages) * stage_elems + hi;
+      const double* sD = ring + (c % kGradStages) * stage_elems + std::size_t(chunk) * hw + di;
       const std::uint64_t k0 = c * chunk;
       const int cnt = int(n - k0 < std::uint64_t(chunk) ? n - k0 : chunk);
       if (bias) {
 #pragma unroll 8
-        for (int k = 0; k < cnt; ++k) acc = __dadd_rn(acc, sD[k * md.dw + di]);
+        for (int k = 0; k < cnt; ++k, sD += dw) acc = __dadd_rn(acc, *sD);
       } else {
 #pragma unroll 8
-        for (int k = 0; k < cnt; ++k)
-          acc = __dadd_rn(acc, __dmul_rn(sD[k * md.dw + di], sH[k * md.hw + hi]));
+        for (int k = 0; k < cnt; ++k, sD += dw, sH += hw)
+          acc = __dadd_rn(acc, __dmul_rn(*sD, *sH));
       }
     }
-    __syncthreads();
+    __syncthreads();  // every consumer is done with this stage
+    if (threadIdx.x == 0 && c + kGradStages < nchunks) issue(c + kGradStages);
   }
-  cp_async_wait<0>();
   if (live) {
     const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
     grad[w] = __double2float_rn(__dmul_rn(acc, inv_n));
@@ -336,9 +377,11 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Long segments: one CTA per key. All threads stream the segment's DX rows
-// through a double-buffered cp.async ring ([chunk][E] doubles); the first E
-// threads run the sequential f64 sums from shared memory.
+// Long segments: one CTA per key. Warps that own no dimension (and do not
+// share sub-partition 0 with warp 0) gather the segment's DX rows into a
+// double-buffered shared ring with 16-B cp.async; thread d < E runs the
+// sequential f64 sum of dimension d from shared memory, alone on its issue
+// slot, so the chain proceeds at the DADD latency.
 constexpr int kLongThreads = 256;
 
 inline int long_chunk(int E) {
@@ -355,21 +398,42 @@ __global__ void __launch_bounds__(kLongThreads)
                              const std::uint32_t* __restrict__ exs,
                              const std::uint32_t* __restrict__ pos,
                              const double* __restrict__ DX, float* __restrict__ out) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   const unsigned long long NL = *n_long;
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  const int warp = threadIdx.x >> 5;
+  const int cw = (E + 31) / 32;  // consumer warps 0..cw-1
+  // producers: warps >= cw that do not share a sub-partition with a consumer
+  const bool producer = warp >= cw && (warp % 4) >= cw;
+  int prank = 0, nprod = 0;
+  for (int w = 0; w < kLongThreads / 32; ++w) {
+    const bool pw = w >= cw && (w % 4) >= cw;
+    if (pw) {
+      if (w < warp) prank += 32;
+      nprod += 32;
+    }
+  }
+  prank += threadIdx.x & 31;
+  const bool even = (E & 1) == 0;
+  const int pieces_per_row = even ? E / 2 : E;  // 16-B or 8-B pieces
   for (unsigned long long li = blockIdx.x; li < NL; li += gridDim.x) {
     const std::uint32_t u = long_list[li];
     const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
     const std::uint32_t nch = (p1 - p0 + chunk - 1) / chunk;
     auto issue = [&](std::uint32_t c) {
-      if (c < nch) {
+      if (producer && c < nch) {
         double* buf = sm + std::size_t(c & 1) * chunk * E;
         const std::uint32_t b = p0 + c * chunk;
         const int cnt = int(p1 - b < std::uint32_t(chunk) ? p1 - b : chunk);
-        for (int t = threadIdx.x; t < cnt * E; t += kLongThreads) {
-          const int r = t / E, d = t - r * E;
-          cp_async8(buf + t, DX + std::uint64_t(exs[b + r]) * E + d);
+        for (int t = prank; t < cnt * pieces_per_row; t += nprod) {
+          const int r = t / pieces_per_row, q = t - r * pieces_per_row;
+          const double* src = DX + std::uint64_t(exs[b + r]) * E;
+          if (even) {
+            const unsigned s = smem_u32(buf + r * E + 2 * q);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src + 2 * q));
+          } else {
+            cp_async8(buf + r * E + q, src + q);
+          }
         }
       }
       cp_async_commit();
@@ -381,11 +445,11 @@ __global__ void __launch_bounds__(kLongThreads)
       cp_async_wait<1>();
       __syncthreads();
       if (int(threadIdx.x) < E) {
-        const double* buf = sm + std::size_t(c & 1) * chunk * E;
+        const double* buf = sm + std::size_t(c & 1) * chunk * E + threadIdx.x;
         const std::uint32_t b = p0 + c * chunk;
         const int cnt = int(p1 - b < std::uint32_t(chunk) ? p1 - b : chunk);
 #pragma unroll 8
-        for (int r = 0; r < cnt; ++r) acc = __dadd_rn(acc, buf[r * E + threadIdx.x]);
+        for (int r = 0; r < cnt; ++r, buf += E) acc = __dadd_rn(acc, *buf);
       }
       __syncthreads();
     }

@@ -1,15 +1,21 @@
-// Stable LSD radix sort and tile scans whose element counts live in device
-// memory, so a whole batch can run without host round-trips.
+// Stable LSD radix sort and prefix scans whose element counts may live in
+// device memory, so a whole batch runs without host round-trips.
 //
-// Used for the working-set dedup (mem_ps.hpp:101-108, hbm_ps.hpp:69-74),
-// the mini-batch dedup + inverse index (pipeline.hpp:523-528) and the stable
-// partition of unique keys by owner (hbm_ps.hpp:75-79, 116-121). Keys are
-// u64 but only their significant bits (< key_space) are sorted.
+// Used for the working-set dedup (mem_ps.hpp:101-108, hbm_ps.hpp:69-74), the
+// mini-batch dedup + inverse index (pipeline.hpp:523-528) and the stable
+// owner partition of unique keys (hbm_ps.hpp:75-79, 116-121). Keys are u64;
+// only their significant bits (< key_space) are sorted.
 //
-// Tile = 256 threads x 16 items. A pass is histogram -> single-CTA
-// exclusive scan of the digit-major [digit][tile] counts -> stable scatter,
-// ranked inside each warp with __match_any_sync (warps own contiguous
-// 512-item sub-tiles, so warp order is input order).
+// Onesweep structure (8-bit digits):
+//   * one histogram kernel counts the digits of every pass up front;
+//   * one kernel per pass: a CTA takes the next tile ticket, ranks its tile
+//     stably (warps own contiguous sub-tiles; __match_any_sync ranks within
+//     a warp), publishes its per-digit count, resolves its exclusive prefix
+//     per digit by decoupled look-back over the preceding tiles, and
+//     scatters. Tickets are handed out in launch order, so a tile only ever
+//     waits on tiles that are already running.
+// Status words are 64-bit [epoch:32 | flag:2 | count:30]; every launch uses a
+// fresh epoch, so the status arrays never need clearing.
 #pragma once
 
 #include <cstdint>
@@ -19,18 +25,32 @@
 namespace hpsgpu {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 2048
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kWarpTile = kSortTile / kSortWarps;      // 512
+constexpr int kWarpTile = kSortTile / kSortWarps;      // 256
 constexpr int kDigits = 256;
+constexpr int kMaxPasses = 8;
 
-// An element count that is either known on the host or produced on the
-// device by an earlier kernel (read at kernel start, no host round-trip).
+constexpr std::uint64_t kFlagAgg = 1ull << 30;
+constexpr std::uint64_t kFlagInc = 2ull << 30;
+constexpr std::uint64_t kCountMask = (1ull << 30) - 1;
+
+// An element count known on the host or produced on the device by an
+// earlier kernel (read at kernel start, no host round-trip).
 struct Count {
   const std::uint64_t* p;
   std::uint64_t v;
   __device__ __forceinline__ std::uint64_t get() const { return p ? *p : v; }
+};
+
+// Look-back context of one launch: ticket counter, the host-tracked number of
+// tickets handed out before this launch, the launch's epoch, status words.
+struct LookBack {
+  unsigned long long* ticket;
+  std::uint64_t base;
+  std::uint32_t epoch;
+  std::uint64_t* status;
 };
 
 struct ShiftDigit {
@@ -48,89 +68,103 @@ struct ModDigit {
   }
 };
 
-template <class Digit>
-__global__ void __launch_bounds__(kSortThreads)
-    radix_hist_kernel(const std::uint64_t* __restrict__ keys,
-                      Count cnt_n, Digit dig,
-                      std::uint32_t* __restrict__ hist, std::uint32_t nblocks) {
-  __shared__ std::uint32_t cnt[kDigits];
-  const std::uint64_t n = cnt_n.get();
-  cnt[threadIdx.x] = 0;
-  __syncthreads();
-  const std::uint64_t base = std::uint64_t(blockIdx.x) * kSortTile;
-  const unsigned lane = threadIdx.x & 31;
-#pragma unroll 4
-  for (int it = 0; it < kSortItems; ++it) {
-    const std::uint64_t idx = base + std::uint64_t(it) * kSortThreads + threadIdx.x;
-    const bool valid = idx < n;
-    const std::uint32_t d = valid ? dig(keys[idx]) : kDigits;
-    // warp-aggregated increments: one smem atomic per distinct digit
-    const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
-    if (valid && lane == unsigned(__ffs(peers) - 1))
-      atomicAdd(&cnt[d], unsigned(__popc(peers)));
-  }
-  __syncthreads();
-  hist[std::uint64_t(threadIdx.x) * nblocks + blockIdx.x] = cnt[threadIdx.x];
+__device__ __forceinline__ std::uint64_t ld_status(const std::uint64_t* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+__device__ __forceinline__ void st_status(std::uint64_t* p, std::uint64_t v) {
+  *reinterpret_cast<volatile unsigned long long*>(p) = v;
+}
+__device__ __forceinline__ std::uint64_t status_word(std::uint32_t epoch, std::uint64_t flag,
+                                                     std::uint64_t count) {
+  return (std::uint64_t(epoch) << 32) | flag | count;
 }
 
-// Exclusive scan of data[0..m) in place by one CTA of 1024 threads; the
-// grand total goes to *total if non-null.
-__global__ void __launch_bounds__(1024)
-    scan_single_cta_kernel(std::uint32_t* __restrict__ data, std::uint64_t m,
-                           std::uint64_t* __restrict__ total) {
-  __shared__ std::uint32_t warp_sums[32];
-  const std::uint64_t per = (m + 1023) / 1024;
-  const std::uint64_t beg = per * threadIdx.x;
-  const std::uint64_t end = beg + per < m ? beg + per : m;
-  std::uint32_t s = 0;
-  for (std::uint64_t i = beg; i < end; ++i) s += data[i];
-  // block exclusive scan of s
+// Exclusive prefix of `tile` for one lane (digit) by decoupled look-back.
+__device__ __forceinline__ std::uint64_t look_back(const LookBack& lb, std::uint64_t tile,
+                                                   int stride, int lane_idx) {
+  std::uint64_t excl = 0;
+  std::int64_t j = std::int64_t(tile) - 1;
+  while (j >= 0) {
+    const std::uint64_t w = ld_status(lb.status + std::uint64_t(j) * stride + lane_idx);
+    if (std::uint32_t(w >> 32) != lb.epoch || (w & (kFlagAgg | kFlagInc)) == 0) continue;
+    excl += w & kCountMask;
+    if (w & kFlagInc) break;
+    --j;
+  }
+  return excl;
+}
+
+// ------------------------------------------------------------ histogram --
+
+// Digit counts of every pass: hist[p * 256 + d] (p < passes), plus the count
+// of a ModDigit when passes == 0 (mod_G > 0).
+__global__ void __launch_bounds__(kSortThreads)
+    onesweep_hist_kernel(const std::uint64_t* __restrict__ keys, Count cnt_n, int passes,
+                         std::uint32_t mod_G, std::uint32_t* __restrict__ hist) {
+  __shared__ std::uint32_t h[kMaxPasses * kDigits];
+  const int np = passes ? passes : 1;
+  for (int i = threadIdx.x; i < np * kDigits; i += kSortThreads) h[i] = 0;
+  __syncthreads();
+  const std::uint64_t n = cnt_n.get();
+  const unsigned lane = threadIdx.x & 31;
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * kSortThreads;
+  for (std::uint64_t base = std::uint64_t(blockIdx.x) * kSortThreads; base < n; base += stride) {
+    const std::uint64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const std::uint64_t k = valid ? keys[i] : 0;
+    for (int p = 0; p < np; ++p) {
+      const std::uint32_t d = !valid ? kDigits
+                                     : (passes ? std::uint32_t(k >> (8 * p)) & 0xFFu
+                                               : std::uint32_t(k % mod_G));
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+      if (valid && lane == unsigned(__ffs(peers) - 1))
+        atomicAdd(&h[p * kDigits + d], unsigned(__popc(peers)));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < np * kDigits; i += kSortThreads)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// In-place exclusive scan of each pass's 256 counts (one CTA per pass).
+__global__ void __launch_bounds__(kDigits) onesweep_scan_kernel(std::uint32_t* __restrict__ hist) {
+  __shared__ std::uint32_t ws[kDigits / 32];
+  std::uint32_t* h = hist + blockIdx.x * kDigits;
+  const std::uint32_t v = h[threadIdx.x];
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  std::uint32_t x = s;
+  std::uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
     if (lane >= unsigned(o)) x += y;
   }
-  if (lane == 31) warp_sums[warp] = x;
+  if (lane == 31) ws[warp] = x;
   __syncthreads();
-  if (warp == 0) {
-    std::uint32_t w = warp_sums[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
-      if (lane >= unsigned(o)) w += y;
-    }
-    warp_sums[lane] = w;  // inclusive
-  }
-  __syncthreads();
-  std::uint32_t run = x - s + (warp ? warp_sums[warp - 1] : 0u);
-  for (std::uint64_t i = beg; i < end; ++i) {
-    const std::uint32_t v = data[i];
-    data[i] = run;
-    run += v;
-  }
-  if (total && threadIdx.x == 1023) *total = run;
+  std::uint32_t pre = 0;
+  for (unsigned w = 0; w < warp; ++w) pre += ws[w];
+  h[threadIdx.x] = pre + x - v;
 }
+
+// ------------------------------------------------------------ one pass --
 
 template <class Digit, bool kValues>
 __global__ void __launch_bounds__(kSortThreads)
-    radix_scatter_kernel(const std::uint64_t* __restrict__ kin,
-                         const std::uint32_t* __restrict__ vin,
-                         Count cnt_n, Digit dig,
-                         const std::uint32_t* __restrict__ hist_scanned,
-                         std::uint32_t nblocks, std::uint64_t* __restrict__ kout,
-                         std::uint32_t* __restrict__ vout) {
+    onesweep_pass_kernel(const std::uint64_t* __restrict__ kin,
+                         const std::uint32_t* __restrict__ vin, Count cnt_n, Digit dig,
+                         const std::uint32_t* __restrict__ digit_base, LookBack lb,
+                         std::uint64_t* __restrict__ kout, std::uint32_t* __restrict__ vout) {
   __shared__ std::uint32_t wcnt[kSortWarps][kDigits];
   __shared__ std::uint32_t gbase[kDigits];
-  const std::uint64_t n = cnt_n.get();
-  const std::uint64_t base = std::uint64_t(blockIdx.x) * kSortTile;
-  if (base >= n) return;
+  __shared__ std::uint64_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(lb.ticket, 1ull) - lb.base;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int i = 0; i < kDigits / 32; ++i) wcnt[warp][lane + 32 * i] = 0;
-  gbase[threadIdx.x] = hist_scanned[std::uint64_t(threadIdx.x) * nblocks + blockIdx.x];
-  __syncwarp();
+  __syncthreads();
+  const std::uint64_t tile = s_tile;
+  const std::uint64_t n = cnt_n.get();
+  const std::uint64_t base = tile * kSortTile;
+  if (base >= n) return;  // trailing tiles of an upper-bound grid: nobody waits on them
   const unsigned lt = lanemask_lt();
   const std::uint64_t wbase = base + std::uint64_t(warp) * kWarpTile;
   std::uint64_t k[kSortItems];
@@ -147,19 +181,28 @@ __global__ void __launch_bounds__(kSortThreads)
     const std::uint32_t prior = valid ? wcnt[warp][d] : 0u;
     r[it] = prior + unsigned(__popc(peers & lt));
     __syncwarp();
-    if (valid && lane == unsigned(__ffs(peers) - 1))
-      wcnt[warp][d] = prior + unsigned(__popc(peers));
+    if (valid && lane == unsigned(__ffs(peers) - 1)) wcnt[warp][d] = prior + unsigned(__popc(peers));
     __syncwarp();
   }
   __syncthreads();
   {
-    const unsigned d = threadIdx.x;
+    const unsigned d = threadIdx.x;  // one thread per digit
     std::uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kSortWarps; ++w) {
       const std::uint32_t c = wcnt[w][d];
       wcnt[w][d] = run;
       run += c;
+    }
+    std::uint64_t* my = lb.status + tile * kDigits + d;
+    if (tile == 0) {
+      st_status(my, status_word(lb.epoch, kFlagInc, run));
+      gbase[d] = digit_base[d];
+    } else {
+      st_status(my, status_word(lb.epoch, kFlagAgg, run));
+      const std::uint64_t excl = look_back(lb, tile, kDigits, d);
+      st_status(my, status_word(lb.epoch, kFlagInc, excl + run));
+      gbase[d] = digit_base[d] + std::uint32_t(excl);
     }
   }
   __syncthreads();
@@ -175,49 +218,37 @@ __global__ void __launch_bounds__(kSortThreads)
   }
 }
 
-// ---- three-kernel tile scan with a device-side element count -----------
+// ---------------------------------------------------------- tile scan ----
 //
-// F  : __device__ std::uint32_t operator()(std::uint64_t i) const — item value
-// Em : __device__ void operator()(std::uint64_t i, std::uint32_t v,
-//                                  std::uint64_t exclusive_prefix) const
+// Single-pass exclusive scan with decoupled look-back.
+//   F  : __device__ std::uint32_t operator()(std::uint64_t i) const — item value
+//   Em : __device__ void operator()(std::uint64_t i, std::uint32_t v,
+//                                    std::uint64_t exclusive_prefix) const
+// The grand total goes to *total (written by the tile holding item n-1).
 
-template <class F>
-__global__ void __launch_bounds__(kSortThreads)
-    tile_reduce_kernel(F f, Count cnt_n,
-                       std::uint32_t* __restrict__ bsum) {
-  __shared__ std::uint32_t ws[kSortWarps];
-  const std::uint64_t n = cnt_n.get();
-  const std::uint64_t base = std::uint64_t(blockIdx.x) * kSortTile;
-  std::uint32_t s = 0;
-  for (int it = 0; it < kSortItems; ++it) {
-    const std::uint64_t idx = base + std::uint64_t(it) * kSortThreads + threadIdx.x;
-    if (idx < n) s += f(idx);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    std::uint32_t t = 0;
-    for (int w = 0; w < kSortWarps; ++w) t += ws[w];
-    bsum[blockIdx.x] = t;
-  }
-}
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kSortThreads * kScanItems;  // 4096
 
 template <class F, class Em>
 __global__ void __launch_bounds__(kSortThreads)
-    tile_emit_kernel(F f, Em em, Count cnt_n,
-                     const std::uint32_t* __restrict__ bsum_scanned) {
+    scan_lookback_kernel(F f, Em em, Count cnt_n, LookBack lb, std::uint64_t* __restrict__ total) {
   __shared__ std::uint32_t ws[kSortWarps];
+  __shared__ std::uint64_t s_tile, s_pre;
+  if (threadIdx.x == 0) s_tile = atomicAdd(lb.ticket, 1ull) - lb.base;
+  __syncthreads();
+  const std::uint64_t tile = s_tile;
   const std::uint64_t n = cnt_n.get();
-  const std::uint64_t base = std::uint64_t(blockIdx.x) * kSortTile;
-  if (base >= n) return;
+  const std::uint64_t base = tile * kScanTile;
+  if (base >= n) {
+    if (tile == 0 && total) *total = 0;
+    return;
+  }
   // blocked arrangement: thread t owns items base + t*16 .. +15
-  const std::uint64_t tb = base + std::uint64_t(threadIdx.x) * kSortItems;
-  std::uint32_t vals[kSortItems];
+  const std::uint64_t tb = base + std::uint64_t(threadIdx.x) * kScanItems;
+  std::uint32_t vals[kScanItems];
   std::uint32_t s = 0;
 #pragma unroll
-  for (int it = 0; it < kSortItems; ++it) {
+  for (int it = 0; it < kScanItems; ++it) {
     const std::uint64_t idx = tb + it;
     vals[it] = idx < n ? f(idx) : 0u;
     s += vals[it];
@@ -231,19 +262,38 @@ __global__ void __launch_bounds__(kSortThreads)
   }
   if (lane == 31) ws[warp] = x;
   __syncthreads();
+  if (threadIdx.x == 0) {
+    std::uint32_t agg = 0;
+    for (int w = 0; w < kSortWarps; ++w) agg += ws[w];
+    std::uint64_t* my = lb.status + tile;
+    std::uint64_t pre = 0;
+    if (tile == 0) {
+      st_status(my, status_word(lb.epoch, kFlagInc, agg));
+    } else {
+      st_status(my, status_word(lb.epoch, kFlagAgg, agg));
+      pre = look_back(lb, tile, 1, 0);
+      st_status(my, status_word(lb.epoch, kFlagInc, pre + agg));
+    }
+    s_pre = pre;
+    if (total && base + kScanTile >= n) *total = pre + agg;
+  }
+  __syncthreads();
   std::uint32_t wpre = 0;
   for (unsigned w = 0; w < warp; ++w) wpre += ws[w];
-  std::uint64_t run = std::uint64_t(bsum_scanned[blockIdx.x]) + wpre + (x - s);
+  std::uint64_t run = s_pre + wpre + (x - s);
 #pragma unroll
-  for (int it = 0; it < kSortItems; ++it) {
+  for (int it = 0; it < kScanItems; ++it) {
     const std::uint64_t idx = tb + it;
     if (idx < n) em(idx, vals[it], run);
     run += vals[it];
   }
 }
 
-inline std::uint32_t tiles_for(std::uint64_t n) {
+inline std::uint32_t sort_tiles(std::uint64_t n) {
   return std::uint32_t((n + kSortTile - 1) / kSortTile);
+}
+inline std::uint32_t scan_tiles(std::uint64_t n) {
+  return std::uint32_t((n + kScanTile - 1) / kScanTile);
 }
 
 }  // namespace hpsgpu

@@ -121,6 +121,8 @@ struct Tier {
   int N = 1, D = 1, G = 1, g = 0, E = 1, J = 1;
   ModelDims md{};
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;           // side stream: dense-grad overlaps sparse reduce
+  cudaEvent_t fork = nullptr, join = nullptr;
   ncclComm_t comm = nullptr;
   std::uint64_t Bmax = 0, Omax = 0, Wmax = 0, capmax = 0, nmb_max = 0;
   int sort_bits = 64;
@@ -143,9 +145,11 @@ struct Tier {
   // sort scratch
   std::uint64_t *kA = nullptr, *kB = nullptr;
   std::uint32_t *vA = nullptr, *vB = nullptr;
-  std::uint32_t* hist = nullptr;
-  std::uint32_t* bsum = nullptr;
-  std::uint64_t hist_len = 0, bsum_len = 0;
+  std::uint32_t* ghist = nullptr;          // [kMaxPasses][256] digit bases
+  std::uint64_t* status = nullptr;         // look-back status words
+  unsigned long long* ticket = nullptr;    // look-back tile tickets
+  std::uint64_t tickets = 0;               // tickets handed out so far (host view)
+  std::uint32_t epoch = 0;                 // per-launch status epoch
 
   // batch staging
   std::int64_t* b_off = nullptr;
@@ -231,6 +235,13 @@ template <class... KArgs, class... Args>
 static void launch(Tier* t, void (*k)(KArgs...), dim3 grid, dim3 block,
                    size_t smem, Args&&... args) {
   k<<<grid, block, smem, t->st>>>(std::forward<Args>(args)...);
+  ++t->launches;
+}
+
+template <class... KArgs, class... Args>
+static void launch_on(Tier* t, cudaStream_t s, void (*k)(KArgs...), dim3 grid, dim3 block,
+                      size_t smem, Args&&... args) {
+  k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
   ++t->launches;
 }
 
@@ -364,20 +375,16 @@ __global__ void occ_row_kernel(const std::uint32_t* __restrict__ inv,
     out[o] = pos[inv[o]];
 }
 
-// Owner partition offsets from the scanned digit-major histogram of the
-// ModDigit pass: send_off[o] = first position of owner o; per-owner counts
-// as u32 for the count all-gather.
-__global__ void owner_offsets_kernel(const std::uint32_t* __restrict__ hist,
-                                     std::uint32_t nblocks, int G,
+// Owner partition offsets from the exclusive-scanned owner histogram of
+// the ModDigit pass: send_off[o] = first position of owner o, send_off[G] =
+// U; per-owner counts as u32 for the count all-gather.
+__global__ void owner_offsets_kernel(const std::uint32_t* __restrict__ base, int G,
                                      const std::uint64_t* __restrict__ u_ptr,
                                      std::uint64_t* __restrict__ send_off,
                                      std::uint32_t* __restrict__ cnt32) {
   const int o = threadIdx.x;
   const std::uint64_t U = *u_ptr;
-  if (o <= G) {
-    const std::uint64_t a = (o < G && U) ? hist[std::uint64_t(o) * nblocks] : U;
-    send_off[o] = a;
-  }
+  if (o <= G) send_off[o] = o < G ? base[o] : U;
   __syncthreads();
   if (o < G) cnt32[o] = std::uint32_t(send_off[o + 1] - send_off[o]);
 }
@@ -491,14 +498,31 @@ struct UniqueEmit {  // inverse index + CSR segments of a sorted (key, occ) list
 
 // --------------------------------------------------- sort / scan drivers
 
+static LookBack next_lookback(Tier* t, std::uint32_t grid) {
+  LookBack lb{t->ticket, t->tickets, ++t->epoch, t->status};
+  if (lb.epoch == 0) lb.epoch = ++t->epoch;  // 0 marks "never written"
+  t->tickets += grid;
+  return lb;
+}
+
 template <class F, class Em>
 static void tile_scan(Tier* t, F f, Em em, Count n, std::uint64_t n_upper,
                       std::uint64_t* total) {
-  const std::uint32_t nb = tiles_for(std::max<std::uint64_t>(n_upper, 1));
-  launch(t, tile_reduce_kernel<F>, nb, kSortThreads, 0, f, n, t->bsum);
-  launch(t, scan_single_cta_kernel, 1, 1024, 0, t->bsum, std::uint64_t(nb), total);
-  launch(t, tile_emit_kernel<F, Em>, nb, kSortThreads, 0, f, em, n,
-         (const std::uint32_t*)t->bsum);
+  const std::uint32_t nb = std::max<std::uint32_t>(1, scan_tiles(n_upper));
+  launch(t, scan_lookback_kernel<F, Em>, nb, kSortThreads, 0, f, em, n, next_lookback(t, nb),
+         total);
+}
+
+// Digit histogram(s) + exclusive scan into t->ghist (passes > 0: 8-bit
+// digits of each pass; passes == 0: owner buckets key % mod_G).
+static void sort_histogram(Tier* t, const std::uint64_t* kin, Count n, std::uint64_t n_upper,
+                           int passes, std::uint32_t mod_G) {
+  const int np = passes ? passes : 1;
+  cudaMemsetAsync(t->ghist, 0, std::size_t(np) * kDigits * 4, t->st);
+  const unsigned hb = unsigned(std::max<std::uint64_t>(
+      1, std::min<std::uint64_t>((n_upper + kSortThreads - 1) / kSortThreads, kSMs * 4)));
+  launch(t, onesweep_hist_kernel, hb, kSortThreads, 0, kin, n, passes, mod_G, t->ghist);
+  launch(t, onesweep_scan_kernel, np, kDigits, 0, t->ghist);
 }
 
 // Stable LSD sort of n (<= n_upper) items over the low `bits` bits. Input
@@ -506,24 +530,22 @@ static void tile_scan(Tier* t, F f, Em em, Count n, std::uint64_t n_upper,
 static void radix_sort(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
                        Count n, std::uint64_t n_upper, int bits, bool values,
                        std::uint64_t** kout, std::uint32_t** vout) {
-  const std::uint32_t nb = tiles_for(std::max<std::uint64_t>(n_upper, 1));
-  const int passes = std::max(1, (bits + 7) / 8);
+  const std::uint32_t nb = std::max<std::uint32_t>(1, sort_tiles(n_upper));
+  const int passes = std::min(kMaxPasses, std::max(1, (bits + 7) / 8));
+  sort_histogram(t, kin, n, n_upper, passes, 0);
   const std::uint64_t* ksrc = kin;
   const std::uint32_t* vsrc = vin;
   std::uint64_t* kd = t->kA;
   std::uint32_t* vd = t->vA;
   for (int p = 0; p < passes; ++p) {
-    ShiftDigit dig{8 * p};
-    launch(t, radix_hist_kernel<ShiftDigit>, nb, kSortThreads, 0, ksrc, n, dig,
-           t->hist, nb);
-    launch(t, scan_single_cta_kernel, 1, 1024, 0, t->hist,
-           std::uint64_t(kDigits) * nb, (std::uint64_t*)nullptr);
+    const ShiftDigit dig{8 * p};
+    const std::uint32_t* db = t->ghist + p * kDigits;
     if (values)
-      launch(t, radix_scatter_kernel<ShiftDigit, true>, nb, kSortThreads, 0, ksrc,
-             vsrc, n, dig, (const std::uint32_t*)t->hist, nb, kd, vd);
+      launch(t, onesweep_pass_kernel<ShiftDigit, true>, nb, kSortThreads, 0, ksrc, vsrc, n, dig,
+             db, next_lookback(t, nb), kd, vd);
     else
-      launch(t, radix_scatter_kernel<ShiftDigit, false>, nb, kSortThreads, 0, ksrc,
-             vsrc, n, dig, (const std::uint32_t*)t->hist, nb, kd, vd);
+      launch(t, onesweep_pass_kernel<ShiftDigit, false>, nb, kSortThreads, 0, ksrc, vsrc, n, dig,
+             db, next_lookback(t, nb), kd, vd);
     ksrc = kd;
     vsrc = vd;
     kd = (kd == t->kA) ? t->kB : t->kA;
@@ -538,15 +560,13 @@ static void radix_sort(Tier* t, const std::uint64_t* kin, const std::uint32_t* v
 static void owner_partition(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
                             const std::uint64_t* n_dev, std::uint64_t n_upper,
                             std::uint64_t* kout, std::uint32_t* vout) {
-  const std::uint32_t nb = tiles_for(std::max<std::uint64_t>(n_upper, 1));
-  ModDigit dig{std::uint32_t(t->G)};
-  Count n{n_dev, 0};
-  launch(t, radix_hist_kernel<ModDigit>, nb, kSortThreads, 0, kin, n, dig, t->hist, nb);
-  launch(t, scan_single_cta_kernel, 1, 1024, 0, t->hist,
-         std::uint64_t(kDigits) * nb, (std::uint64_t*)nullptr);
-  launch(t, radix_scatter_kernel<ModDigit, true>, nb, kSortThreads, 0, kin, vin, n,
-         dig, (const std::uint32_t*)t->hist, nb, kout, vout);
-  launch(t, owner_offsets_kernel, 1, 288, 0, (const std::uint32_t*)t->hist, nb, t->G,
+  const std::uint32_t nb = std::max<std::uint32_t>(1, sort_tiles(n_upper));
+  const Count n{n_dev, 0};
+  sort_histogram(t, kin, n, n_upper, 0, std::uint32_t(t->G));
+  launch(t, onesweep_pass_kernel<ModDigit, true>, nb, kSortThreads, 0, kin, vin, n,
+         ModDigit{std::uint32_t(t->G)}, (const std::uint32_t*)t->ghist, next_lookback(t, nb), kout,
+         vout);
+  launch(t, owner_offsets_kernel, 1, 288, 0, (const std::uint32_t*)t->ghist, t->G,
          (const std::uint64_t*)&t->dsc->U, t->dsc->send_off, t->cnt32);
 }
 
@@ -951,7 +971,10 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (e != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: cudaSetDevice(%d): %s", c.cuda_device,
                           cudaGetErrorString(e)));
-  if ((e = cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking)) != cudaSuccess)
+  if ((e = cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&t->st2, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&t->fork, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&t->join, cudaEventDisableTiming)) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: stream: %s", cudaGetErrorString(e)));
 
   {
@@ -987,10 +1010,9 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(kB, S);
   A(vA, S);
   A(vB, S);
-  t->hist_len = std::uint64_t(kDigits) * tiles_for(S);
-  t->bsum_len = tiles_for(S) + 1;
-  A(hist, t->hist_len);
-  A(bsum, t->bsum_len);
+  A(ghist, std::uint64_t(kMaxPasses) * kDigits);
+  A(status, std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1);
+  A(ticket, 1);
   A(b_off, t->Bmax + 1);
   A(b_keys, O);
   A(b_lab, t->Bmax);
@@ -1015,13 +1037,17 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(deltas, S * E);
   A(rrows, S * E);
   A(rdeltas, S * E);
-  A(H, t->nmb_max * std::uint64_t(t->md.hw));
-  A(DL, t->nmb_max * std::uint64_t(t->md.dw));
+  A(H, t->nmb_max * std::uint64_t(t->md.hw) + 2);   // +2: 16-B rounded bulk copies
+  A(DL, t->nmb_max * std::uint64_t(t->md.dw) + 2);
   A(DX, t->nmb_max * E);
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
   A(dgather, std::uint64_t(t->md.nw) * G);
 #undef A
+  cudaMemsetAsync(t->ticket, 0, 8, t->st);
+  cudaMemsetAsync(t->status, 0,
+                  (std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1) * 8,
+                  t->st);
   if ((e = cudaMemsetAsync(t->dsc, 0, sizeof(Scalars), t->st)) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: memset: %s", cudaGetErrorString(e)));
   // replicate_dense(init_dense(cfg)) — the init stream is host-side std::mt19937_64
@@ -1057,6 +1083,9 @@ hps_status hps_destroy(hps_tier_t t) {
   if (t->hsc) cudaFreeHost(t->hsc);
   if (t->store_registered) cudaHostUnregister(t->store_host);
   for (auto& ev : t->evpool) cudaEventDestroy(ev);
+  if (t->fork) cudaEventDestroy(t->fork);
+  if (t->join) cudaEventDestroy(t->join);
+  if (t->st2) cudaStreamDestroy(t->st2);
   if (t->st) cudaStreamDestroy(t->st);
   delete t;
   return HPS_OK;
@@ -1491,10 +1520,15 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
              (const std::uint32_t*)T->occ_off, occ_row, (const float*)T->rows, dlab, T->H,
              T->DL, T->DX, &T->dsc->loss, &T->dsc->err);
       mark(T, HPS_T_FWDBWD);
-      launch(T, dense_grad_kernel, (T->md.nw + kGradThreads - 1) / kGradThreads,
-             kGradThreads, dense_grad_smem(T->md), T->md, n, grad_chunk(T->md),
-             (const double*)T->H, (const double*)T->DL, T->dgrad);
+      // dense-grad reduce on the side stream, overlapping the sparse reduce
+      HPS_CUDA(cudaEventRecord(T->fork, T->st));
+      HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
+      launch_on(T, T->st2, dense_grad_kernel, (T->md.nw + kGradThreads - 1) / kGradThreads,
+                kGradThreads, dense_grad_smem(T->md), T->md, n, grad_chunk(T->md),
+                (const double*)T->H, (const double*)T->DL, T->dgrad);
+      HPS_CUDA(cudaEventRecord(T->join, T->st2));
       HPS_TRY(launch_sparse_delta(T, n, plan.pos, On));
+      HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
     } else {
       HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));
     }
