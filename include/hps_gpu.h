@@ -79,6 +79,8 @@ typedef struct {
   uint64_t served_keys;      /* keys this rank served as owner (pull+push) */
   uint64_t occurrences;      /* key occurrences in this rank's shards */
   uint64_t carried_rows;     /* build rows taken from the previous table */
+  uint64_t exact_fallbacks;  /* certified parallel sums that had to be redone
+                                in the exact sequential order */
 } hps_batch_stats;
 
 /* Phase slots of hps_get_timing (ms accumulated over hps_train_batch calls,

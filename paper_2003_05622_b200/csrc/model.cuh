@@ -82,13 +82,27 @@ __global__ void __launch_bounds__(128)
     const std::uint64_t k = k0 + slot;
     const bool active = k < sm.count;
     // --- embed_sum: x[d] = sum over features in order
+    // (the group's lanes load LPE row ids at once, every lane then issues its
+    // LPE independent row loads before the in-order f64 chain)
     if (active) {
       const std::uint32_t o0 = occ_off[k], o1 = occ_off[k + 1];
-      for (int d = sub; d < E; d += LPE) {
+      for (int d0 = 0; d0 < E; d0 += LPE) {
+        const int d = d0 + sub;
         double acc = 0.0;
-        for (std::uint32_t o = o0; o < o1; ++o)
-          acc = __dadd_rn(acc, double(rows[std::uint64_t(occ_row[o]) * E + d]));
-        hrec[d] = acc;
+        for (std::uint32_t c = o0; c < o1; c += LPE) {
+          const int len = int(o1 - c < std::uint32_t(LPE) ? o1 - c : LPE);
+          const std::uint32_t my_row = sub < len ? occ_row[c + sub] : 0u;
+          float v[LPE];
+#pragma unroll
+          for (int r = 0; r < LPE; ++r) {
+            const std::uint32_t rid = __shfl_sync(gmask, my_row, r, LPE);
+            v[r] = (r < len && d < E) ? rows[std::uint64_t(rid) * E + d] : 0.0f;
+          }
+#pragma unroll
+          for (int r = 0; r < LPE; ++r)
+            if (r < len) acc = __dadd_rn(acc, double(v[r]));
+        }
+        if (d < E) hrec[d] = acc;
       }
     }
     __syncwarp();
@@ -211,91 +225,207 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
   } while (!ok);
 }
 
-// Dense gradient of the shard: one thread per weight walks the examples in
-// order (model.hpp:161-175), then *1/n and the f32 cast (model.hpp:189-193).
-// 128 threads = one warp per SM sub-partition, so each weight's f64 chain
-// issues at the DADD latency. The per-example H/DL records (contiguous per
-// chunk of examples) arrive through a kGradStages-deep ring of TMA bulk
-// copies (one elected thread, mbarrier completion), off the consumers' issue
-// slots. H/DL are padded by 2 doubles so chunk sizes round up to 16 B.
-constexpr int kGradStages = 4;
-constexpr int kGradThreads = 128;
+// ---- certified parallel summation -----------------------------------
+//
+// The reference sums n terms x_1..x_n in a fixed sequential order in f64 and
+// keeps only g = f32(fl(S * inv_n)) (model.hpp:189-200). With s_k the exact
+// prefix sums, recursive summation satisfies (Higham, Accuracy and Stability,
+// eq. 4.3 and its a-posteriori form)
+//   |S_seq - s_n| <= u/(1-u) * sum_{k>=2} |s^_k|,
+//   |s^_k| <= |s_k| + gamma_n * A,          A = sum |x_i|,  u = 2^-53.
+// The kernels compute, slice-parallel and exactly reproducibly:
+//   * S  = s_n by Neumaier compensated summation of the slices and of their
+//     (sum, compensation) pairs (error <= 2u|S| + 2((n+m+slices+8) u)^2 A),
+//   * B >= sum_k |t_k|, t_k = offset_slice + in-slice prefix (|t_k - s_k| <=
+//     2u|t_k| + (m + slices + 4) u A),
+// so S_seq lies within S +- delta,
+//   delta = 1.02 * (u B + 2u|S| + 2 (n + m + slices + 8)^2 u^2 A).
+// fl(. * inv_n) and the f32 cast are monotone: when both interval ends give
+// the same f32 bit pattern, that IS the sequential result. Otherwise (rare)
+// the caller recomputes the exact in-order chain.
+constexpr double kUnitRoundoff = 1.1102230246251565e-16;  // 2^-53
+#ifdef HPS_DEBUG_CERT
+__device__ int g_dbg_count = 0;
+#endif
 
-inline int grad_chunk(const ModelDims& md) {
-  int ch = 64;
-  while (ch > 8 && size_t(kGradStages) * ch * (md.hw + md.dw) * 8 + 64 > 200 * 1024) ch >>= 1;
-  return ch;
+// Neumaier (improved Kahan-Babuska) accumulator: the running sum's chain is
+// one DADD per term; the exact rounding error of each addition goes to c.
+struct DD {
+  double hi, lo;  // running sum, accumulated compensation
+};
+__device__ __forceinline__ DD dd_add(DD a, double x) {
+  const double t = __dadd_rn(a.hi, x);
+  const double e = fabs(a.hi) >= fabs(x) ? __dadd_rn(__dsub_rn(a.hi, t), x)
+                                         : __dadd_rn(__dsub_rn(x, t), a.hi);
+  return DD{t, __dadd_rn(a.lo, e)};
 }
-inline size_t dense_grad_smem(const ModelDims& md) {
-  return size_t(kGradStages) * grad_chunk(md) * (md.hw + md.dw) * sizeof(double) + 64;
+__device__ __forceinline__ DD dd_add(DD a, DD b) { return dd_add(dd_add(a, b.hi), b.lo); }
+__device__ __forceinline__ double dd_value(DD a) { return __dadd_rn(a.hi, a.lo); }
+
+__device__ __forceinline__ bool certify_f32(double S, double B, double A, std::uint64_t n,
+                                            std::uint64_t m_plus_slices, double inv_n, float* g) {
+  const double u = kUnitRoundoff;
+  const double t = double(n + m_plus_slices + 8);
+  const double second = __dmul_ru(__dmul_ru(2.0 * t, t), __dmul_ru(__dmul_ru(u, u), A));
+  const double first = __dadd_ru(__dmul_ru(u, B), __dmul_ru(2.0 * u, fabs(S)));
+  const double bound = __dmul_ru(1.02, __dadd_ru(first, second));
+  if (bound == 0.0) {  // every term is zero: S (+0 from a +0 start) is exact
+    *g = __double2float_rn(__dmul_rn(S, inv_n));
+    return true;
+  }
+  const double lo = __dsub_rd(S, bound), hi = __dadd_ru(S, bound);
+  const float glo = __double2float_rn(__dmul_rn(lo, inv_n));
+  const float ghi = __double2float_rn(__dmul_rn(hi, inv_n));
+  *g = glo;
+#ifdef HPS_DEBUG_CERT
+  if (__float_as_uint(glo) != __float_as_uint(ghi)) {
+    __shared__ int dbg_once;
+    if (atomicAdd(&g_dbg_count, 1) < 24)
+      printf("cert fail: S=%.17g B=%.6g A=%.6g n=%llu bound=%.6g glo=%.9g ghi=%.9g\n", S, B, A,
+             (unsigned long long)n, bound, glo, ghi);
+    (void)dbg_once;
+  }
+#endif
+  return __float_as_uint(glo) == __float_as_uint(ghi);
 }
 
-__global__ void __launch_bounds__(kGradThreads)
-    dense_grad_kernel(ModelDims md, std::uint64_t n, int chunk,
-                      const double* __restrict__ H, const double* __restrict__ DL,
-                      float* __restrict__ grad) {
-  extern __shared__ __align__(128) double sm[];
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(sm);  // kGradStages barriers
-  double* ring = sm + 8;                                          // 64 B header
-  const int hw = md.hw, dw = md.dw;
-  const std::size_t stage_elems = std::size_t(chunk) * (hw + dw);
-  const int w = blockIdx.x * kGradThreads + threadIdx.x;
+// Exact in-order f64 sum of buf[0..cnt) from shared memory, continuing acc.
+__device__ __forceinline__ double chain_sum(const double* buf, int cnt, double acc) {
+  constexpr int kGroup = 16;
+  int r = 0;
+  for (; r + kGroup <= cnt; r += kGroup) {
+    double v[kGroup];
+#pragma unroll
+    for (int j = 0; j < kGroup; ++j) v[j] = buf[r + j];
+#pragma unroll
+    for (int j = 0; j < kGroup; ++j) acc = __dadd_rn(acc, v[j]);
+  }
+  for (; r < cnt; ++r) acc = __dadd_rn(acc, buf[r]);
+  return acc;
+}
+
+constexpr int kFallbackChunk = 2048;  // doubles staged per round (16 KB)
+
+// Dense gradient of the shard (model.hpp:161-175, 189-193), two launches over
+// grid (weight groups of 32, kDGSlices example slices):
+//   p1: per (weight, slice) the double-double total T and sum|p| A;
+//   p2: per (weight, slice) the running prefixes from the slice's offset
+//       (sum of earlier T) -> B; the last CTA of a weight group combines the
+//       slices, certifies, and recomputes uncertified weights in the exact
+//       order (the warp stages the products, lane 0 chains them).
+constexpr int kDGSlices = 32;
+
+struct WeightRef {
+  int hi, di;
+  bool bias;
+};
+__device__ __forceinline__ WeightRef weight_ref(const ModelDims& md, int w) {
+  int l = md.L - 1;
+  while (w < md.offs[l]) --l;
+  const int in = md.ins[l], out = md.dims[l], rel = w - md.offs[l];
+  const bool bias = rel >= in * out;
+  const int o = bias ? rel - in * out : rel / in;
+  return WeightRef{md.hoff[l] + (bias ? 0 : rel % in), md.doff[l] + o, bias};
+}
+__device__ __forceinline__ double weight_term(const ModelDims& md, const double* H,
+                                              const double* DL, WeightRef r, std::uint64_t k) {
+  const double d = DL[k * md.dw + r.di];
+  return r.bias ? d : __dmul_rn(d, H[k * md.hw + r.hi]);
+}
+
+__global__ void __launch_bounds__(32)
+    dense_grad_p1_kernel(ModelDims md, std::uint64_t n, const double* __restrict__ H,
+                         const double* __restrict__ DL, double* __restrict__ part) {
+  const int w = blockIdx.x * 32 + threadIdx.x;
+  if (w >= md.nw) return;
+  const WeightRef r = weight_ref(md, w);
+  const std::uint64_t per = (n + kDGSlices - 1) / kDGSlices;
+  const std::uint64_t k0 = blockIdx.y * per, k1 = k0 + per < n ? k0 + per : n;
+  DD t{0.0, 0.0};
+  double a = 0.0;
+#pragma unroll 4
+  for (std::uint64_t k = k0; k < k1; ++k) {
+    const double x = weight_term(md, H, DL, r, k);
+    t = dd_add(t, x);
+    a = __dadd_ru(a, fabs(x));
+  }
+  double* slot = part + (std::uint64_t(w) * kDGSlices + blockIdx.y) * 4;
+  slot[0] = t.hi;
+  slot[1] = t.lo;
+  slot[2] = a;
+}
+
+__global__ void __launch_bounds__(32)
+    dense_grad_p2_kernel(ModelDims md, std::uint64_t n, const double* __restrict__ H,
+                         const double* __restrict__ DL, double* __restrict__ part,
+                         unsigned* __restrict__ done, float* __restrict__ grad,
+                         unsigned long long* __restrict__ fallbacks) {
+  __shared__ double stage[kFallbackChunk];
+  const int w = blockIdx.x * 32 + threadIdx.x;
   const bool live = w < md.nw;
-  int hi = 0, di = 0;
-  bool bias = false;
+  const WeightRef r = live ? weight_ref(md, w) : WeightRef{0, 0, false};
+  const std::uint64_t per = (n + kDGSlices - 1) / kDGSlices;
   if (live) {
-    int l = md.L - 1;
-    while (w < md.offs[l]) --l;
-    const int in = md.ins[l], out = md.dims[l], rel = w - md.offs[l];
-    bias = rel >= in * out;
-    const int o = bias ? rel - in * out : rel / in;
-    di = md.doff[l] + o;
-    hi = md.hoff[l] + (bias ? 0 : rel % in);
-  }
-  const std::uint64_t nchunks = (n + chunk - 1) / chunk;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kGradStages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto issue = [&](std::uint64_t c) {  // thread 0 only
-    double* sH = ring + (c % kGradStages) * stage_elems;
-    double* sD = sH + std::size_t(chunk) * hw;
-    const std::uint64_t k0 = c * chunk;
-    const unsigned cnt = unsigned(n - k0 < std::uint64_t(chunk) ? n - k0 : chunk);
-    const unsigned bh = (cnt * hw * 8u + 15u) & ~15u, bd = (cnt * dw * 8u + 15u) & ~15u;
-    std::uint64_t* bar = &full[c % kGradStages];
-    mbar_expect_tx(bar, bh + bd);
-    bulk_g2s(sH, H + k0 * hw, bh, bar);
-    bulk_g2s(sD, DL + k0 * dw, bd, bar);
-  };
-  if (threadIdx.x == 0)
-    for (std::uint64_t c = 0; c < nchunks && c < std::uint64_t(kGradStages); ++c) issue(c);
-  double acc = 0.0;
-  for (std::uint64_t c = 0; c < nchunks; ++c) {
-    mbar_wait(&full[c % kGradStages], unsigned((c / kGradStages) & 1));
-    if (live) {
-      const double* sH = ring + (c % kGradStages) * stage_elems + hi;
-      const double* sD = ring + (c % kGradStages) * stage_elems + std::size_t(chunk) * hw + di;
-      const std::uint64_t k0 = c * chunk;
-      const int cnt = int(n - k0 < std::uint64_t(chunk) ? n - k0 : chunk);
-      if (bias) {
-#pragma unroll 8
-        for (int k = 0; k < cnt; ++k, sD += dw) acc = __dadd_rn(acc, *sD);
-      } else {
-#pragma unroll 8
-        for (int k = 0; k < cnt; ++k, sD += dw, sH += hw)
-          acc = __dadd_rn(acc, __dmul_rn(*sD, *sH));
-      }
+    const double* base = part + std::uint64_t(w) * kDGSlices * 4;
+    DD off{0.0, 0.0};
+    for (unsigned s = 0; s < blockIdx.y; ++s) off = dd_add(off, DD{base[s * 4], base[s * 4 + 1]});
+    const double o = dd_value(off);
+    const std::uint64_t k0 = blockIdx.y * per, k1 = k0 + per < n ? k0 + per : n;
+    double l = 0.0, b = 0.0;
+#pragma unroll 4
+    for (std::uint64_t k = k0; k < k1; ++k) {
+      l = __dadd_rn(l, weight_term(md, H, DL, r, k));
+      b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
     }
-    __syncthreads();  // every consumer is done with this stage
-    if (threadIdx.x == 0 && c + kGradStages < nchunks) issue(c + kGradStages);
+    part[(std::uint64_t(w) * kDGSlices + blockIdx.y) * 4 + 3] = b;
   }
+  __threadfence();
+  unsigned last = 0;
+  if (threadIdx.x == 0) last = atomicAdd(&done[blockIdx.x], 1u) == kDGSlices - 1;
+  last = __shfl_sync(0xFFFFFFFFu, last, 0);
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) done[blockIdx.x] = 0;  // ready for the next launch
+  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  float g = 0.0f;
+  bool ok = true;
   if (live) {
-    const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-    grad[w] = __double2float_rn(__dmul_rn(acc, inv_n));
+    DD S{0.0, 0.0};
+    double A = 0.0, B = 0.0;
+    const double* base = part + std::uint64_t(w) * kDGSlices * 4;
+    for (int s = 0; s < kDGSlices; ++s) {
+      S = dd_add(S, DD{__ldcg(base + s * 4), __ldcg(base + s * 4 + 1)});
+      A = __dadd_ru(A, __ldcg(base + s * 4 + 2));
+      B = __dadd_ru(B, __ldcg(base + s * 4 + 3));
+    }
+    ok = certify_f32(dd_value(S), B, A, n, per + kDGSlices, inv_n, &g);
   }
+  unsigned todo = __ballot_sync(0xFFFFFFFFu, !ok);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    WeightRef sr;
+    sr.hi = __shfl_sync(0xFFFFFFFFu, r.hi, src);
+    sr.di = __shfl_sync(0xFFFFFFFFu, r.di, src);
+    sr.bias = __shfl_sync(0xFFFFFFFFu, r.bias, src);
+    double acc = 0.0;
+    for (std::uint64_t c0 = 0; c0 < n; c0 += kFallbackChunk) {
+      const int cnt = int(n - c0 < kFallbackChunk ? n - c0 : kFallbackChunk);
+      for (int j = threadIdx.x; j < cnt; j += 32) stage[j] = weight_term(md, H, DL, sr, c0 + j);
+      __syncwarp();
+      if (threadIdx.x == 0) acc = chain_sum(stage, cnt, acc);
+      __syncwarp();
+    }
+    acc = __shfl_sync(0xFFFFFFFFu, acc, 0);
+    if (int(threadIdx.x) == src) {
+      g = __double2float_rn(__dmul_rn(acc, inv_n));
+      if (fallbacks) atomicAdd(fallbacks, 1ull);
+    }
+  }
+  if (live) grad[w] = g;
 }
+
+inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw + 31) / 32); }
 
 // Sparse gradient segment-reduce + sgd_delta (model.hpp:182-200, 226-230).
 // Per unique key u: sum over its occurrences, in example order, of the
@@ -308,7 +438,7 @@ __global__ void __launch_bounds__(kGradThreads)
 // up to 8 example ids, every lane issues its 8 independent DX loads into
 // registers, then adds them in order. Longer segments (hot Zipf keys: up to
 // the whole shard) are queued for sparse_delta_long_kernel.
-constexpr int kLongSeg = 64;
+constexpr int kLongSeg = 32;
 constexpr int kStageDepth = 8;
 
 __device__ __forceinline__ void write_delta(float* out, std::uint64_t row, int E, int d,
@@ -377,85 +507,111 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Long segments: one CTA per key. Warps that own no dimension (and do not
-// share sub-partition 0 with warp 0) gather the segment's DX rows into a
-// double-buffered shared ring with 16-B cp.async; thread d < E runs the
-// sequential f64 sum of dimension d from shared memory, alone on its issue
-// slot, so the chain proceeds at the DADD latency.
-constexpr int kLongThreads = 256;
-
-inline int long_chunk(int E) {
-  int ch = 512;
-  while (ch > 32 && size_t(2) * ch * E * 8 > 160 * 1024) ch >>= 1;
-  return ch;
-}
+// Long segments (hot keys): one CTA per key, in chunks of kLongChunk
+// occurrences whose example ids are staged in shared memory (one coalesced
+// pass). Thread (slice s, dim d) first sums dimension d over its slice of the
+// chunk (Neumaier, plus sum|x|); with the running total of earlier chunks and
+// slices as offset it then re-walks its slice accumulating the running-prefix
+// magnitudes B. Thread d combines and certifies (certify_f32); uncertified
+// dimensions are recomputed in the exact order (the CTA stages the values in
+// shared memory, one thread chains them).
+constexpr int kLongThreads = 512;
+constexpr int kLongChunk = 2048;
 
 __global__ void __launch_bounds__(kLongThreads)
-    sparse_delta_long_kernel(int E, float lr, std::uint64_t n, int chunk,
+    sparse_delta_long_kernel(int E, float lr, std::uint64_t n,
                              const std::uint32_t* __restrict__ long_list,
                              const unsigned long long* __restrict__ n_long,
                              const std::uint32_t* __restrict__ seg,
                              const std::uint32_t* __restrict__ exs,
                              const std::uint32_t* __restrict__ pos,
-                             const double* __restrict__ DX, float* __restrict__ out) {
-  extern __shared__ __align__(16) double sm[];
+                             const double* __restrict__ DX, float* __restrict__ out,
+                             unsigned long long* __restrict__ fallbacks) {
+  __shared__ double th[kLongThreads], tl[kLongThreads], ta[kLongThreads], tb[kLongThreads];
+  __shared__ std::uint32_t sex[kLongChunk];
+  __shared__ double stage[kFallbackChunk];
+  __shared__ bool bad[kLongThreads];
   const unsigned long long NL = *n_long;
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-  const int warp = threadIdx.x >> 5;
-  const int cw = (E + 31) / 32;  // consumer warps 0..cw-1
-  // producers: warps >= cw that do not share a sub-partition with a consumer
-  const bool producer = warp >= cw && (warp % 4) >= cw;
-  int prank = 0, nprod = 0;
-  for (int w = 0; w < kLongThreads / 32; ++w) {
-    const bool pw = w >= cw && (w % 4) >= cw;
-    if (pw) {
-      if (w < warp) prank += 32;
-      nprod += 32;
-    }
-  }
-  prank += threadIdx.x & 31;
-  const bool even = (E & 1) == 0;
-  const int pieces_per_row = even ? E / 2 : E;  // 16-B or 8-B pieces
+  const int slices = kLongThreads / E;  // E <= 512
+  const int s = threadIdx.x / E, d = threadIdx.x - s * E;
+  const bool worker = s < slices;
   for (unsigned long long li = blockIdx.x; li < NL; li += gridDim.x) {
     const std::uint32_t u = long_list[li];
     const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
-    const std::uint32_t nch = (p1 - p0 + chunk - 1) / chunk;
-    auto issue = [&](std::uint32_t c) {
-      if (producer && c < nch) {
-        double* buf = sm + std::size_t(c & 1) * chunk * E;
-        const std::uint32_t b = p0 + c * chunk;
-        const int cnt = int(p1 - b < std::uint32_t(chunk) ? p1 - b : chunk);
-        for (int t = prank; t < cnt * pieces_per_row; t += nprod) {
-          const int r = t / pieces_per_row, q = t - r * pieces_per_row;
-          const double* src = DX + std::uint64_t(exs[b + r]) * E;
-          if (even) {
-            const unsigned s = smem_u32(buf + r * E + 2 * q);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src + 2 * q));
-          } else {
-            cp_async8(buf + r * E + q, src + q);
+    DD run{0.0, 0.0};     // total of the chunks done (thread d < E keeps it)
+    DD S{0.0, 0.0};
+    double A = 0.0, B = 0.0;
+    for (std::uint32_t c0 = p0; c0 < p1; c0 += kLongChunk) {
+      const int cnt = int(p1 - c0 < std::uint32_t(kLongChunk) ? p1 - c0 : kLongChunk);
+      for (int j = threadIdx.x; j < cnt; j += kLongThreads) sex[j] = exs[c0 + j];
+      __syncthreads();
+      const int per = (cnt + slices - 1) / slices;
+      const int a0 = s * per, a1 = a0 + int(per) < cnt ? a0 + int(per) : cnt;
+      if (worker) {
+        DD t{0.0, 0.0};
+        double asum = 0.0;
+#pragma unroll 16
+        for (int p = a0; p < a1; ++p) {
+          const double x = DX[std::uint64_t(sex[p]) * E + d];
+          t = dd_add(t, x);
+          asum = __dadd_ru(asum, fabs(x));
+        }
+        th[threadIdx.x] = t.hi;
+        tl[threadIdx.x] = t.lo;
+        ta[threadIdx.x] = asum;
+      }
+      __syncthreads();
+      if (worker) {
+        DD off{0.0, 0.0};
+        for (int q = 0; q < s; ++q) off = dd_add(off, DD{th[q * E + d], tl[q * E + d]});
+        const double o = __dadd_rn(dd_value(run), dd_value(off));
+        double l = 0.0, b = 0.0;
+#pragma unroll 16
+        for (int p = a0; p < a1; ++p) {
+          l = __dadd_rn(l, DX[std::uint64_t(sex[p]) * E + d]);
+          b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
+        }
+        tb[threadIdx.x] = b;
+      }
+      __syncthreads();
+      if (worker) {
+        // every worker of dim d folds this chunk into its copy of the running
+        // state, in slice order (identical across the dim's workers)
+        for (int q = 0; q < slices; ++q) {
+          const DD tq{th[q * E + d], tl[q * E + d]};
+          run = dd_add(run, tq);
+          if (s == 0) {
+            S = dd_add(S, tq);
+            A = __dadd_ru(A, ta[q * E + d]);
+            B = __dadd_ru(B, tb[q * E + d]);
           }
         }
       }
-      cp_async_commit();
-    };
-    issue(0);
-    double acc = 0.0;
-    for (std::uint32_t c = 0; c < nch; ++c) {
-      issue(c + 1);
-      cp_async_wait<1>();
-      __syncthreads();
-      if (int(threadIdx.x) < E) {
-        const double* buf = sm + std::size_t(c & 1) * chunk * E + threadIdx.x;
-        const std::uint32_t b = p0 + c * chunk;
-        const int cnt = int(p1 - b < std::uint32_t(chunk) ? p1 - b : chunk);
-#pragma unroll 8
-        for (int r = 0; r < cnt; ++r, buf += E) acc = __dadd_rn(acc, *buf);
-      }
       __syncthreads();
     }
-    cp_async_wait<0>();
+    float g = 0.0f;
     if (int(threadIdx.x) < E)
-      write_delta(out, pos ? pos[u] : u, E, threadIdx.x, acc, inv_n, lr);
+      bad[threadIdx.x] = !certify_f32(dd_value(S), B, A, p1 - p0, (p1 - p0) + slices, inv_n, &g);
+    __syncthreads();
+    for (int dd = 0; dd < E; ++dd) {
+      if (!bad[dd]) continue;
+      double acc = 0.0;
+      for (std::uint32_t c0 = p0; c0 < p1; c0 += kFallbackChunk) {
+        const int cnt = int(p1 - c0 < kFallbackChunk ? p1 - c0 : kFallbackChunk);
+        for (int j = threadIdx.x; j < cnt; j += kLongThreads)
+          stage[j] = DX[std::uint64_t(exs[c0 + j]) * E + dd];
+        __syncthreads();
+        if (int(threadIdx.x) == dd) acc = chain_sum(stage, cnt, acc);
+        __syncthreads();
+      }
+      if (int(threadIdx.x) == dd) {
+        g = __double2float_rn(__dmul_rn(acc, inv_n));
+        if (fallbacks) atomicAdd(fallbacks, 1ull);
+      }
+    }
+    if (int(threadIdx.x) < E)
+      out[std::uint64_t(pos ? pos[u] : u) * E + threadIdx.x] = -__fmul_rn(lr, g);
     __syncthreads();
   }
 }

@@ -106,6 +106,7 @@ struct Scalars {
   unsigned long long carried;  // rows filled from the previous table
   unsigned long long n_long;   // long CSR segments queued this mini-batch
   int err_any;                 // error code max-reduced over ranks
+  unsigned long long fallbacks;  // certified sums that needed the exact chain
   DevError err;
 };
 
@@ -168,7 +169,8 @@ struct Tier {
   std::uint64_t staged_cap = 0;
 
   // model
-  double *H = nullptr, *DL = nullptr, *DX = nullptr;
+  double *H = nullptr, *DL = nullptr, *DX = nullptr, *dpart = nullptr;
+  unsigned* dg_done = nullptr;
   float *dense = nullptr, *dgrad = nullptr, *dgather = nullptr;
 
   // value store (MEM-PS stand-in)
@@ -245,7 +247,6 @@ static void launch_on(Tier* t, cudaStream_t s, void (*k)(KArgs...), dim3 grid, d
   ++t->launches;
 }
 
-static const char* missing_msg_context = "device table: missing key ";
 
 // Maps the device error word to the reference's hps::Error texts. With
 // collective = true (calls every rank makes in lockstep) the error code is
@@ -859,10 +860,9 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   else if (E <= 64) HPS_SD(32, 2);
   else HPS_SD(32, 8);
 #undef HPS_SD
-  const int ch = long_chunk(E);
-  launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, size_t(2) * ch * E * 8, E, lr, n,
-         ch, (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos,
-         DX, t->deltas);
+  launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, 0, E, lr, n,
+         (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos, DX,
+         t->deltas, &t->dsc->fallbacks);
   return HPS_OK;
 }
 
@@ -980,14 +980,12 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   {
     // dynamic shared memory of the model kernels (per-example scratch, streamed records)
     const int big = 200 * 1024;
-    const size_t need_grad = dense_grad_smem(t->md);
+    const size_t need_grad = 0;
     const size_t need_fwd = size_t((t->md.nw + 1) & ~1) * 4 +
                             size_t(16) * (t->md.hw + t->md.dw + t->md.maxw) * 8;
     if (need_grad > size_t(big) || need_fwd > size_t(big))
       return fail(set_error(HPS_ERR_ARG, "dense model too large for the fused kernels"));
-    cudaFuncSetAttribute(dense_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(sparse_delta_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         big);
+
     cudaFuncSetAttribute(fwd_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -1040,11 +1038,14 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(H, t->nmb_max * std::uint64_t(t->md.hw) + 2);   // +2: 16-B rounded bulk copies
   A(DL, t->nmb_max * std::uint64_t(t->md.dw) + 2);
   A(DX, t->nmb_max * E);
+  A(dpart, std::uint64_t(t->md.nw) * kDGSlices * 4);
+  A(dg_done, dense_grad_groups(t->md));
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
   A(dgather, std::uint64_t(t->md.nw) * G);
 #undef A
   cudaMemsetAsync(t->ticket, 0, 8, t->st);
+  cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
   cudaMemsetAsync(t->status, 0,
                   (std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1) * 8,
                   t->st);
@@ -1436,6 +1437,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   // ---- counts (one host round-trip per batch)
   HPS_CUDA(cudaMemsetAsync(T->dsc->counts, 0, sizeof(T->dsc->counts), T->st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 8 * 3, T->st));  // loss, pulled, carried
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 8, T->st));
   launch(T, batch_count_kernel, kSMs * 4, 256, 0, doff, dkeys, std::uint64_t(B), G, T->g, J,
          T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts, &T->dsc->err);
   HPS_CUDA(cudaMemcpyAsync(T->hsc->counts, T->dsc->counts, sizeof(T->dsc->counts),
@@ -1523,9 +1525,11 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
       // dense-grad reduce on the side stream, overlapping the sparse reduce
       HPS_CUDA(cudaEventRecord(T->fork, T->st));
       HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
-      launch_on(T, T->st2, dense_grad_kernel, (T->md.nw + kGradThreads - 1) / kGradThreads,
-                kGradThreads, dense_grad_smem(T->md), T->md, n, grad_chunk(T->md),
-                (const double*)T->H, (const double*)T->DL, T->dgrad);
+      launch_on(T, T->st2, dense_grad_p1_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
+                0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart);
+      launch_on(T, T->st2, dense_grad_p2_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
+                0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart, T->dg_done,
+                T->dgrad, &T->dsc->fallbacks);
       HPS_CUDA(cudaEventRecord(T->join, T->st2));
       HPS_TRY(launch_sparse_delta(T, n, plan.pos, On));
       HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
@@ -1577,6 +1581,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   }
   mark(T, HPS_T_WRITEBACK);
   HPS_CUDA(cudaMemcpyAsync(&T->hsc->loss, &T->dsc->loss, 8 * 3, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&T->hsc->fallbacks, &T->dsc->fallbacks, 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&T->hsc->n_ws, &T->dsc->n_ws, 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(T->hsc->cap, T->dsc->cap, 16, cudaMemcpyDeviceToHost, T->st));
   HPS_TRY(check_device_error(T, "device table: missing key ", true));
@@ -1594,6 +1599,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
     stats->table_capacity = T->hsc->cap[T->cur];
     stats->pulled_keys = T->hsc->pulled;
     stats->carried_rows = T->hsc->carried;
+    stats->exact_fallbacks = T->hsc->fallbacks;
     stats->served_keys = served;
     stats->occurrences = occ_total;
   }

@@ -73,6 +73,7 @@ class HpsBatchStats(ctypes.Structure):
         ("served_keys", ctypes.c_uint64),
         ("occurrences", ctypes.c_uint64),
         ("carried_rows", ctypes.c_uint64),
+        ("exact_fallbacks", ctypes.c_uint64),
     ]
 
 TIMING_SLOTS = ["total", "stage", "build", "dedup", "pull", "fwdbwd", "grads", "apply",

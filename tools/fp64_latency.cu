@@ -35,7 +35,7 @@ __global__ void chain_smem(double* out, long long* cyc, int n) {
   long long t1 = clock64();
   out[threadIdx.x] = a; if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
-int main() {
+int lat_main() {
   double* d; float* f; long long* c; long long h;
   cudaMalloc(&d, 8192); cudaMalloc(&f, 64); cudaMalloc(&c, 8);
   const int n = 1 << 16;
@@ -53,3 +53,57 @@ int main() {
   }
   return 0;
 }
+// (appended) DADD throughput: 8 independent chains per thread, full occupancy
+__global__ void dadd_tput(double* out, int n) {
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3 + j;
+  const double b = 1e-9;
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = __dadd_rn(a[j], b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void fadd_tput(float* out, int n) {
+  float a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = threadIdx.x * 1e-3f + j;
+  const float b = 1e-9f;
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = __fadd_rn(a[j], b);
+  }
+  float s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s += a[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+int tput_main() {
+  double* d; float* f;
+  cudaMalloc(&d, 148 * 8 * 1024 * 8);
+  cudaMalloc(&f, 148 * 8 * 1024 * 4);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  const int n = 4096;
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEventRecord(a);
+    dadd_tput<<<148 * 8, 256>>>(d, n);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    const double ops = 148.0 * 8 * 256 * n * 8;
+    if (rep) printf("DADD throughput: %.2f Tops/s = %.1f lanes/clk/SM @1.965GHz\n", ops / ms / 1e9,
+                    ops / (ms * 1e-3) / 148 / 1.965e9);
+    cudaEventRecord(a);
+    fadd_tput<<<148 * 8, 256>>>(f, n);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep) printf("FADD throughput: %.2f Tops/s = %.1f lanes/clk/SM @1.965GHz\n", ops / ms / 1e9,
+                    ops / (ms * 1e-3) / 148 / 1.965e9);
+  }
+  return 0;
+}
+int main() { lat_main(); return tput_main(); }
