@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "50", "-i", str(self.index)],
+                 "-lms", "20", "-i", str(self.index)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -176,7 +176,7 @@ def reference_arm(args, rank):
                                    f"deterministic sync"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------- ours --
@@ -399,14 +399,26 @@ def run_ours(args, rank, world, local_rank):
             "carried_rows_per_step": carried / K,
             "working_set_per_step": ws / K,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     tier.close()
 
 
+_JSON_FD = None
+
+
+def emit(line: dict) -> None:
+    """Print the one JSON line on the real stdout (library/NCCL banners are
+    routed to stderr for the whole run)."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # anything else written to stdout goes to stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))

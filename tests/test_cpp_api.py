@@ -1,0 +1,18 @@
+"""GPU: the C++ host-side mirror of the reference API (include/hps_gpu/hbm_tier.hpp)
+driven by a compiled C++ test (tests/cpp/test_hbm_tier.cpp)."""
+import os
+import subprocess
+
+import pytest
+
+BIN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "test_hbm_tier")
+
+pytestmark = pytest.mark.gpu
+
+
+def test_cpp_hbm_tier_parity():
+    if not os.path.exists(BIN):
+        pytest.fail("tests/cpp/test_hbm_tier not built (run __graft_entry__.build())")
+    p = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert " 0 failed" in p.stdout
