@@ -1,0 +1,224 @@
+// In-kernel NVLink/NVSwitch all-to-all between the ranks of one box.
+//
+// Every rank exports one HBM window through CUDA IPC (or, for ranks living in
+// one process, plain peer pointers):
+//   keys   u64 [G][slot]     pull requests from each source rank
+//   hdr    u64 [G][2]        per source: {count, source's send offset}
+//   deltas f32 [G][slot][E]  pushed deltas, same order as the keys
+//   dense  f32 [G][nw]       dense-gradient replicas for the canonical sum
+//   flags  u64 [G][kPhases]  arrival flags per source and phase
+// plus the requester-side row buffer, written directly by the owners.
+//
+// A phase is: writer kernel (P2P stores straight into the peers' windows) ->
+// its last CTA fences at system scope and raises flags[me][phase] = epoch in
+// every peer -> the consumer's wait kernel spins (bounded) until every
+// source's flag reached the epoch. Windows are reused every mini-batch; the
+// phase order (keys -> rows -> deltas -> dense) guarantees a window is never
+// overwritten before its owner consumed it.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace hpsgpu {
+
+constexpr int kMaxRanks = 8;
+enum P2PPhase { kPhKeys = 0, kPhRows = 1, kPhDeltas = 2, kPhDense = 3, kPhases = 4 };
+
+struct PeerWindows {
+  std::uint64_t* keys[kMaxRanks];    // peer's keys window base
+  std::uint64_t* hdr[kMaxRanks];     // peer's header base
+  float* deltas[kMaxRanks];          // peer's delta window base
+  float* dense[kMaxRanks];           // peer's dense window base
+  float* rows[kMaxRanks];            // peer's requester row buffer
+  std::uint64_t* flags[kMaxRanks];   // peer's flag array
+};
+
+__device__ __forceinline__ void st_release_sys(std::uint64_t* p, std::uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) {
+  std::uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Called by every CTA after its P2P stores; the last CTA to finish raises
+// this rank's flag for `phase` in every peer.
+__device__ __forceinline__ void signal_peers(const PeerWindows& pw, int G, int me, int phase,
+                                             std::uint64_t epoch, unsigned* done_ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned prev = atomicAdd(done_ctr, 1u);
+    if (prev == gridDim.x * gridDim.y - 1) {
+      *done_ctr = 0;
+      __threadfence_system();
+      for (int p = 0; p < G; ++p) st_release_sys(pw.flags[p] + me * kPhases + phase, epoch);
+    }
+  }
+}
+
+// Waits until every source raised `phase` to `epoch` in this rank's flags.
+__global__ void p2p_wait_kernel(const std::uint64_t* __restrict__ my_flags, int G, int phase,
+                                std::uint64_t epoch, DevError* err) {
+  if (threadIdx.x >= unsigned(G)) return;
+  const std::uint64_t* f = my_flags + threadIdx.x * kPhases + phase;
+  long long spins = 0;
+  while (ld_acquire_sys(f) < epoch) {
+    if (++spins > (1ll << 27)) {  // ~10 s: a peer died; fail instead of hanging
+      raise_error(err, 10 /*HPS_ERR_NCCL*/, std::uint64_t(threadIdx.x));
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+
+// Requester -> owners: every unique key (owner-partitioned, positions p in
+// send order) goes to its owner's keys window, region `me`; one thread per
+// key. Thread 0 also writes the {count, send offset} headers.
+__global__ void p2p_send_keys_kernel(PeerWindows pw, int G, int me, std::uint64_t slot,
+                                     const std::uint64_t* __restrict__ pkeys,
+                                     const std::uint64_t* __restrict__ u_ptr,
+                                     const std::uint64_t* __restrict__ send_off,
+                                     std::uint64_t epoch, unsigned* done_ctr) {
+  const std::uint64_t U = *u_ptr;
+  if (blockIdx.x == 0 && threadIdx.x < unsigned(G)) {
+    const int o = threadIdx.x;
+    std::uint64_t* h = pw.hdr[o] + me * 2;
+    h[0] = send_off[o + 1] - send_off[o];
+    h[1] = send_off[o];
+  }
+  for (std::uint64_t p = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; p < U;
+       p += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t k = pkeys[p];
+    const int o = int(k % std::uint64_t(G));
+    pw.keys[o][me * slot + (p - send_off[o])] = k;
+  }
+  signal_peers(pw, G, me, kPhKeys, epoch, done_ctr);
+}
+
+// Owner: for every source s and request i (G <= 8 segments, decoded from the
+// headers): probe, cache the slot, store the row straight into requester s's
+// row buffer at its send position. VEC floats per thread.
+template <int VEC>
+__global__ void p2p_serve_rows_kernel(PeerWindows pw, int G, int me, std::uint64_t slot,
+                                      const std::uint64_t* __restrict__ my_keys,
+                                      const std::uint64_t* __restrict__ my_hdr,
+                                      const std::uint64_t* __restrict__ tkeys,
+                                      const float* __restrict__ tvals,
+                                      const std::uint64_t* __restrict__ cap_ptr,
+                                      std::uint32_t* __restrict__ rslots, int E,
+                                      std::uint64_t epoch, unsigned* done_ctr,
+                                      unsigned long long* served, DevError* err) {
+  const int tpk = E / VEC;
+  const std::uint64_t cap = *cap_ptr;
+  std::uint64_t cnt[kMaxRanks], base[kMaxRanks];
+  std::uint64_t total = 0;
+  for (int s = 0; s < G; ++s) {
+    cnt[s] = my_hdr[s * 2];
+    base[s] = total;
+    total += cnt[s];
+  }
+  if (served && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(served, total);
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < total * tpk; t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t r = t / tpk;
+    const int part = int(t - r * tpk);
+    int s = 0;
+    while (s + 1 < G && r >= base[s + 1]) ++s;
+    const std::uint64_t i = r - base[s];
+    const std::uint64_t key = my_keys[s * slot + i];
+    const std::uint32_t sl = probe_slot(tkeys, cap, key);
+    if (sl == kNoSlot) {
+      raise_error(err, 2, key);
+      continue;
+    }
+    if (part == 0) rslots[s * slot + i] = sl;
+    const float* src = tvals + std::uint64_t(sl) * E + part * VEC;
+    float* dst = pw.rows[s] + (my_hdr[s * 2 + 1] + i) * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, ld_f4(src));
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) dst[q] = src[q];
+    }
+  }
+  signal_peers(pw, G, me, kPhRows, epoch, done_ctr);
+}
+
+// Requester -> owners: delta rows (send order) into the owner's deltas
+// window, region `me`, at the request's index.
+template <int VEC>
+__global__ void p2p_send_deltas_kernel(PeerWindows pw, int G, int me, std::uint64_t slot,
+                                       const std::uint64_t* __restrict__ pkeys,
+                                       const std::uint64_t* __restrict__ u_ptr,
+                                       const std::uint64_t* __restrict__ send_off,
+                                       const float* __restrict__ deltas, int E,
+                                       std::uint64_t epoch, unsigned* done_ctr) {
+  const int tpk = E / VEC;
+  const std::uint64_t U = *u_ptr;
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < U * tpk;
+       t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t p = t / tpk;
+    const int part = int(t - p * tpk);
+    const int o = int(pkeys[p] % std::uint64_t(G));
+    const float* src = deltas + p * E + part * VEC;
+    float* dst = pw.deltas[o] + (me * slot + (p - send_off[o])) * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, ld_f4(src));
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) dst[q] = src[q];
+    }
+  }
+  signal_peers(pw, G, me, kPhDeltas, epoch, done_ctr);
+}
+
+// Owner apply of every source's deltas in canonical sender order (one pass
+// per source inside the kernel would race across keys shared between
+// sources, so the host launches one grid per source, in order).
+template <int VEC>
+__global__ void p2p_apply_kernel(const std::uint64_t* __restrict__ my_hdr, int s,
+                                 std::uint64_t slot, const std::uint32_t* __restrict__ rslots,
+                                 const float* __restrict__ my_deltas, float* __restrict__ tvals,
+                                 int E) {
+  const int tpk = E / VEC;
+  const std::uint64_t n = my_hdr[s * 2];
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < n * tpk;
+       t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    float* v = tvals + std::uint64_t(rslots[s * slot + i]) * E + part * VEC;
+    const float* d = my_deltas + (s * slot + i) * E + part * VEC;
+    if (VEC == 4) {
+      float4 a = ld_f4(v);
+      const float4 b = ld_f4(d);
+      a.x = __fadd_rn(a.x, b.x);
+      a.y = __fadd_rn(a.y, b.y);
+      a.z = __fadd_rn(a.z, b.z);
+      a.w = __fadd_rn(a.w, b.w);
+      st_f4(v, a);
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) v[q] = __fadd_rn(v[q], d[q]);
+    }
+  }
+}
+
+// Dense replica all-gather: this rank's gradient into every peer's dense
+// window, region `me`.
+__global__ void p2p_send_dense_kernel(PeerWindows pw, int G, int me, std::uint64_t nw,
+                                      const float* __restrict__ grad, std::uint64_t epoch,
+                                      unsigned* done_ctr) {
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < nw * G;
+       t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const int p = int(t / nw);
+    const std::uint64_t i = t - std::uint64_t(p) * nw;
+    pw.dense[p][me * nw + i] = grad[i];
+  }
+  signal_peers(pw, G, me, kPhDense, epoch, done_ctr);
+}
+
+}  // namespace hpsgpu

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstring>
@@ -26,6 +27,7 @@
 #include "common.cuh"
 #include "hps_gpu.h"
 #include "model.cuh"
+#include "p2p.cuh"
 #include "sort.cuh"
 #include "table.cuh"
 #include "tier_internal.h"
@@ -107,6 +109,7 @@ struct Scalars {
   unsigned long long n_long;   // long CSR segments queued this mini-batch
   int err_any;                 // error code max-reduced over ranks
   unsigned long long fallbacks;  // certified sums that needed the exact chain
+  unsigned long long served;     // keys this rank served as owner (G > 1)
   DevError err;
 };
 
@@ -160,18 +163,17 @@ struct Tier {
   // mini-batch / pull buffers (sized Omax)
   std::uint32_t *occ_off = nullptr, *ex_of = nullptr, *inv = nullptr,
                 *seg = nullptr, *uidv = nullptr, *pos = nullptr,
-                *occ_row = nullptr, *slots = nullptr, *rslots = nullptr,
+                *occ_row = nullptr, *slots = nullptr,
                 *puid = nullptr, *cnt32 = nullptr, *cnt_all = nullptr, *exs = nullptr,
                 *long_list = nullptr;
-  std::uint64_t *ukeys = nullptr, *pkeys = nullptr, *rkeys = nullptr;
-  float *rows = nullptr, *deltas = nullptr, *rrows = nullptr,
-        *rdeltas = nullptr, *staged = nullptr;
+  std::uint64_t *ukeys = nullptr, *pkeys = nullptr;
+  float *rows = nullptr, *deltas = nullptr, *hstage = nullptr, *staged = nullptr;
   std::uint64_t staged_cap = 0;
 
   // model
   double *H = nullptr, *DL = nullptr, *DX = nullptr, *dpart = nullptr;
   unsigned* dg_done = nullptr;
-  float *dense = nullptr, *dgrad = nullptr, *dgather = nullptr;
+  float *dense = nullptr, *dgrad = nullptr;
 
   // value store (MEM-PS stand-in)
   float* store = nullptr;
@@ -180,6 +182,28 @@ struct Tier {
   float* store_host = nullptr;
 
   std::vector<PendingChunk> pending;
+
+  // in-kernel NVLink all-to-all (G > 1): this rank's exported window and the
+  // peers' windows (p2p.cuh)
+  // Windows are double-buffered by round parity (epoch & 1) so a fast rank
+  // never overwrites a region a slower peer is still reading.
+  PeerWindows pwp[2]{};
+  PeerWindows pw{};                  // the current round's set
+  std::uint64_t slot = 0;            // per-source region capacity (keys)
+  std::uint64_t* w_keys_p[2] = {};   // [G][slot]
+  std::uint64_t* w_hdr_p[2] = {};    // [G][2]
+  float* w_deltas_p[2] = {};         // [G][slot][E]
+  float* w_dense_p[2] = {};          // [G][nw]
+  std::uint64_t* w_keys = nullptr;
+  std::uint64_t* w_hdr = nullptr;
+  float* w_deltas = nullptr;
+  float* w_dense = nullptr;
+  std::uint64_t* w_flags = nullptr;  // [G][kPhases] (monotonic epochs)
+  std::uint32_t* w_rslots = nullptr; // [G][slot] cached owner slots (local)
+  unsigned* done_ctr = nullptr;
+  std::uint64_t p2p_epoch = 0;
+  void* win_base = nullptr;
+  std::vector<void*> ipc_opened;
 
   // timing: events recorded at phase boundaries on the tier stream
   bool timing = false;
@@ -575,46 +599,21 @@ static int vec_of(int E) { return (E % 4 == 0) ? 4 : 1; }
 
 // ------------------------------------------------------------ exchange --
 
-// All ranks learn every rank's per-owner counts; returns host offsets.
-// send_off[o] (this rank's segment for owner o), recv_off[s] (segment from
-// sender s in this rank's receive buffers).
-static hps_status exchange_counts(Tier* t, std::vector<std::uint64_t>& send_off,
-                                  std::vector<std::uint64_t>& recv_off) {
-  const int G = t->G;
-  std::vector<std::uint32_t> all(std::size_t(G) * G);
-  HPS_NCCL(nccl().AllGather(t->cnt32, t->cnt_all, std::size_t(G), ncclUint32, t->comm, t->st));
-  HPS_CUDA(cudaMemcpyAsync(all.data(), t->cnt_all, all.size() * 4,
-                           cudaMemcpyDeviceToHost, t->st));
-  HPS_CUDA(cudaStreamSynchronize(t->st));
-  send_off.assign(G + 1, 0);
-  recv_off.assign(G + 1, 0);
-  for (int o = 0; o < G; ++o) send_off[o + 1] = send_off[o] + all[std::size_t(t->g) * G + o];
-  for (int s = 0; s < G; ++s) recv_off[s + 1] = recv_off[s] + all[std::size_t(s) * G + t->g];
-  return HPS_OK;
+// One exchange round (a mini-batch, or one collective API call): every
+// phase of the round is tagged with the same epoch on all ranks.
+static void begin_round(Tier* t) {
+  ++t->p2p_epoch;
+  const int par = int(t->p2p_epoch & 1);
+  t->pw = t->pwp[par];
+  t->w_keys = t->w_keys_p[par];
+  t->w_hdr = t->w_hdr_p[par];
+  t->w_deltas = t->w_deltas_p[par];
+  t->w_dense = t->w_dense_p[par];
 }
 
-// Variable all-to-all: segment [soff[p], soff[p+1]) of sendbuf goes to rank
-// p, segment from rank p lands at [roff[p], roff[p+1]) of recvbuf.
-static hps_status alltoallv(Tier* t, const void* sendbuf,
-                            const std::vector<std::uint64_t>& soff, void* recvbuf,
-                            const std::vector<std::uint64_t>& roff,
-                            std::size_t elem_bytes) {
-  const int G = t->G;
-  const char* sb = static_cast<const char*>(sendbuf);
-  char* rb = static_cast<char*>(recvbuf);
-  const std::uint64_t self_n = soff[t->g + 1] - soff[t->g];
-  if (self_n)
-    HPS_CUDA(cudaMemcpyAsync(rb + roff[t->g] * elem_bytes, sb + soff[t->g] * elem_bytes,
-                             self_n * elem_bytes, cudaMemcpyDeviceToDevice, t->st));
-  HPS_NCCL(nccl().GroupStart());
-  for (int p = 0; p < G; ++p) {
-    if (p == t->g) continue;
-    const std::uint64_t sn = soff[p + 1] - soff[p], rn = roff[p + 1] - roff[p];
-    if (sn) HPS_NCCL(nccl().Send(sb + soff[p] * elem_bytes, sn * elem_bytes, ncclUint8, p, t->comm, t->st));
-    if (rn) HPS_NCCL(nccl().Recv(rb + roff[p] * elem_bytes, rn * elem_bytes, ncclUint8, p, t->comm, t->st));
-  }
-  HPS_NCCL(nccl().GroupEnd());
-  return HPS_OK;
+static void p2p_wait(Tier* t, int phase) {
+  launch(t, p2p_wait_kernel, 1, 32, 0, (const std::uint64_t*)t->w_flags, t->G, phase,
+         t->p2p_epoch, &t->dsc->err);
 }
 
 // Canonical sender order: node-major, device-major (hbm_ps.hpp:175-176).
@@ -746,65 +745,63 @@ static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint3
     }
     return HPS_OK;
   }
-  // G > 1: owner partition of the unique keys (stable, keeps key order)
+  // G > 1: owner partition of the unique keys (stable, keeps key order),
+  // then the keys go straight into the owners' windows over NVLink
   owner_partition(t, t->ukeys, t->uidv, &t->dsc->U, n, t->pkeys, t->puid);
   launch(t, pos_kernel, grid_for(n), 256, 0, (const std::uint32_t*)t->puid,
          (const std::uint64_t*)&t->dsc->U, t->pos);
   plan->pos = t->pos;
-  HPS_TRY(exchange_counts(t, plan->soff, plan->roff));
+  launch(t, p2p_send_keys_kernel, grid_for(n), 256, 0, t->pw, t->G, t->g, t->slot,
+         (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
+         (const std::uint64_t*)t->dsc->send_off, t->p2p_epoch, t->done_ctr);
+  p2p_wait(t, kPhKeys);
   mark(t, HPS_T_DEDUP);
-  plan->R = plan->roff[t->G];
-  HPS_TRY(alltoallv(t, t->pkeys, plan->soff, t->rkeys, plan->roff, 8));
   if (do_gather) {
-    const std::uint64_t work = plan->R * std::uint64_t(t->E / V);
-    if (plan->R) {
-      if (V == 4)
-        launch(t, table_gather_kernel<4>, grid_for(work), 256, 0,
-               (const std::uint64_t*)t->rkeys, (const std::uint64_t*)nullptr, plan->R,
-               (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
-               (const std::uint64_t*)&t->dsc->cap[t->cur], t->rrows, t->rslots, t->E,
-               &t->dsc->err);
-      else
-        launch(t, table_gather_kernel<1>, grid_for(work), 256, 0,
-               (const std::uint64_t*)t->rkeys, (const std::uint64_t*)nullptr, plan->R,
-               (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
-               (const std::uint64_t*)&t->dsc->cap[t->cur], t->rrows, t->rslots, t->E,
-               &t->dsc->err);
-    }
-    HPS_TRY(alltoallv(t, t->rrows, plan->roff, t->rows, plan->soff,
-                      sizeof(float) * std::size_t(t->E)));
+    const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
+    if (V == 4)
+      launch(t, p2p_serve_rows_kernel<4>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+             (const std::uint64_t*)t->w_keys, (const std::uint64_t*)t->w_hdr,
+             (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
+             (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->p2p_epoch,
+             t->done_ctr, &t->dsc->served, &t->dsc->err);
+    else
+      launch(t, p2p_serve_rows_kernel<1>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+             (const std::uint64_t*)t->w_keys, (const std::uint64_t*)t->w_hdr,
+             (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
+             (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->p2p_epoch,
+             t->done_ctr, &t->dsc->served, &t->dsc->err);
+    p2p_wait(t, kPhRows);
     mark(t, HPS_T_PULL);
   }
   return HPS_OK;
 }
 
-// Owner apply of the pushed deltas in canonical sender order.
-static hps_status push_apply(Tier* t, const PullPlan& plan) {
+// Owner apply of the pushed deltas in canonical sender order (G > 1): the
+// delta rows go straight into the owners' windows; each owner applies the
+// sources' segments in (node, device) order with the slots cached at pull.
+static hps_status push_apply(Tier* t) {
   const int V = vec_of(t->E);
-  if (t->G == 1) {
-    // U is device-resident; the apply grid covers the upper bound
-    const std::uint64_t work_upper = t->Omax * std::uint64_t(t->E / V);
-    (void)work_upper;
-    return HPS_OK;
-  }
-  HPS_TRY(alltoallv(t, t->deltas, plan.soff, t->rdeltas, plan.roff,
-                    sizeof(float) * std::size_t(t->E)));
+  const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
+  if (V == 4)
+    launch(t, p2p_send_deltas_kernel<4>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+           (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
+           (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->p2p_epoch,
+           t->done_ctr);
+  else
+    launch(t, p2p_send_deltas_kernel<1>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+           (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
+           (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->p2p_epoch,
+           t->done_ctr);
+  p2p_wait(t, kPhDeltas);
   for (int src : canonical_senders(t)) {
-    const std::uint64_t a = plan.roff[src], b = plan.roff[src + 1];
-    if (a == b) continue;
-    const std::uint64_t work = (b - a) * std::uint64_t(t->E / V);
     if (V == 4)
-      launch(t, table_apply_kernel<4>, grid_for(work), 256, 0,
-             (const std::uint32_t*)(t->rslots + a), (const std::uint64_t*)nullptr,
-             (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
-             (const float*)(t->rdeltas + a * t->E), (const std::uint64_t*)nullptr, b - a,
-             t->tvals[t->cur], t->E, &t->dsc->err);
+      launch(t, p2p_apply_kernel<4>, grid_for(t->slot * std::uint64_t(t->E / V)), 256, 0,
+             (const std::uint64_t*)t->w_hdr, src, t->slot, (const std::uint32_t*)t->w_rslots,
+             (const float*)t->w_deltas, t->tvals[t->cur], t->E);
     else
-      launch(t, table_apply_kernel<1>, grid_for(work), 256, 0,
-             (const std::uint32_t*)(t->rslots + a), (const std::uint64_t*)nullptr,
-             (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
-             (const float*)(t->rdeltas + a * t->E), (const std::uint64_t*)nullptr, b - a,
-             t->tvals[t->cur], t->E, &t->dsc->err);
+      launch(t, p2p_apply_kernel<1>, grid_for(t->slot * std::uint64_t(t->E / V)), 256, 0,
+             (const std::uint64_t*)t->w_hdr, src, t->slot, (const std::uint32_t*)t->w_rslots,
+             (const float*)t->w_deltas, t->tvals[t->cur], t->E);
   }
   return HPS_OK;
 }
@@ -818,17 +815,13 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
            (float*)nullptr, &t->dsc->err);
     return HPS_OK;
   }
-  if (t->cfg.deterministic) {
-    HPS_NCCL(nccl().AllGather(t->dgrad, t->dgather, nw, ncclFloat32, t->comm, t->st));
-    launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense,
-           (const float*)t->dgather, nw, t->N, t->D, t->cfg.learning_rate, int(apply),
-           (float*)nullptr, &t->dsc->err);
-  } else {
-    HPS_NCCL(nccl().AllReduce(t->dgrad, t->dgather, nw, ncclFloat32, ncclSum, t->comm, t->st));
-    launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense,
-           (const float*)t->dgather, nw, 0, t->G, t->cfg.learning_rate, int(apply),
-           (float*)nullptr, &t->dsc->err);
-  }
+  // replicas all-gathered over NVLink, then the canonical f64 sum (det and
+  // fast modes alike: the canonical order costs nothing extra here)
+  launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->pw, t->G, t->g, nw,
+         (const float*)t->dgrad, t->p2p_epoch, t->done_ctr);
+  p2p_wait(t, kPhDense);
+  launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense, (const float*)t->w_dense, nw,
+         t->N, t->D, t->cfg.learning_rate, int(apply), (float*)nullptr, &t->dsc->err);
   return HPS_OK;
 }
 
@@ -863,6 +856,95 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, 0, E, lr, n,
          (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos, DX,
          t->deltas, &t->dsc->fallbacks);
+  return HPS_OK;
+}
+
+// Exported window of this rank + the peers' windows (p2p.cuh). Ranks in
+// other processes are mapped through CUDA IPC handles; ranks in this process
+// through peer access. The window descriptors are all-gathered with NCCL.
+static hps_status setup_p2p(Tier* t, std::uint64_t S) {
+  const int G = t->G;
+  if (G > kMaxRanks) return set_error(HPS_ERR_ARG, "at most %d GPUs per tier", kMaxRanks);
+  const std::uint64_t E = std::uint64_t(t->E), nw = std::uint64_t(t->md.nw);
+  t->slot = t->Omax;
+  auto al = [](std::uint64_t b) { return (b + 255) & ~std::uint64_t(255); };
+  const std::uint64_t o_flags = 0;
+  const std::uint64_t o_rows = o_flags + al(G * kPhases * 8);
+  const std::uint64_t o_par = o_rows + al(S * E * 4);  // two parity copies follow
+  const std::uint64_t p_keys = 0;
+  const std::uint64_t p_hdr = p_keys + al(G * t->slot * 8);
+  const std::uint64_t p_deltas = p_hdr + al(G * 2 * 8);
+  const std::uint64_t p_dense = p_deltas + al(G * t->slot * E * 4);
+  const std::uint64_t par_bytes = p_dense + al(G * nw * 4);
+  const std::uint64_t total = o_par + 2 * par_bytes;
+  HPS_CUDA(cudaMalloc(&t->win_base, total));
+  t->allocs.push_back(t->win_base);
+  HPS_CUDA(cudaMemset(t->win_base, 0, total));
+  char* b = static_cast<char*>(t->win_base);
+  t->w_flags = reinterpret_cast<std::uint64_t*>(b + o_flags);
+  t->rows = reinterpret_cast<float*>(b + o_rows);
+  for (int par = 0; par < 2; ++par) {
+    char* pb = b + o_par + par * par_bytes;
+    t->w_keys_p[par] = reinterpret_cast<std::uint64_t*>(pb + p_keys);
+    t->w_hdr_p[par] = reinterpret_cast<std::uint64_t*>(pb + p_hdr);
+    t->w_deltas_p[par] = reinterpret_cast<float*>(pb + p_deltas);
+    t->w_dense_p[par] = reinterpret_cast<float*>(pb + p_dense);
+  }
+  HPS_TRY(dalloc(t, &t->w_rslots, G * t->slot));
+  HPS_TRY(dalloc(t, &t->done_ctr, 1));
+  HPS_CUDA(cudaMemset(t->done_ctr, 0, 4));
+  struct Info {
+    cudaIpcMemHandle_t h;
+    std::uint64_t base;
+    std::int32_t pid, dev;
+  };
+  Info mine{};
+  HPS_CUDA(cudaIpcGetMemHandle(&mine.h, t->win_base));
+  mine.base = reinterpret_cast<std::uint64_t>(t->win_base);
+  mine.pid = std::int32_t(getpid());
+  mine.dev = t->cfg.cuda_device;
+  std::vector<Info> all(G);
+  char* dinfo = nullptr;
+  HPS_CUDA(cudaMalloc(&dinfo, sizeof(Info) * (G + 1)));
+  HPS_CUDA(cudaMemcpy(dinfo, &mine, sizeof(Info), cudaMemcpyHostToDevice));
+  ncclResult_t r = nccl().AllGather(dinfo, dinfo + sizeof(Info), sizeof(Info), ncclUint8, t->comm,
+                                    t->st);
+  if (r != ncclSuccess) {
+    cudaFree(dinfo);
+    return set_error(HPS_ERR_NCCL, "nccl: window exchange: %s", nccl().GetErrorString(r));
+  }
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  HPS_CUDA(cudaMemcpy(all.data(), dinfo + sizeof(Info), sizeof(Info) * G, cudaMemcpyDeviceToHost));
+  cudaFree(dinfo);
+  for (int p = 0; p < G; ++p) {
+    char* base = nullptr;
+    if (p == t->g) {
+      base = b;
+    } else if (all[p].pid == mine.pid) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(all[p].dev, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return set_error(HPS_ERR_CUDA, "cuda: peer access %d->%d: %s", mine.dev, all[p].dev,
+                         cudaGetErrorString(e));
+      cudaGetLastError();
+      base = reinterpret_cast<char*>(all[p].base);
+    } else {
+      void* q = nullptr;
+      HPS_CUDA(cudaIpcOpenMemHandle(&q, all[p].h, cudaIpcMemLazyEnablePeerAccess));
+      t->ipc_opened.push_back(q);
+      base = static_cast<char*>(q);
+    }
+    for (int par = 0; par < 2; ++par) {
+      char* pb = base + o_par + par * par_bytes;
+      PeerWindows& w = t->pwp[par];
+      w.keys[p] = reinterpret_cast<std::uint64_t*>(pb + p_keys);
+      w.hdr[p] = reinterpret_cast<std::uint64_t*>(pb + p_hdr);
+      w.deltas[p] = reinterpret_cast<float*>(pb + p_deltas);
+      w.dense[p] = reinterpret_cast<float*>(pb + p_dense);
+      w.flags[p] = reinterpret_cast<std::uint64_t*>(base + o_flags);
+      w.rows[p] = reinterpret_cast<float*>(base + o_rows);
+    }
+  }
+  begin_round(t);  // epoch 1 (flags start at 0)
   return HPS_OK;
 }
 
@@ -1022,7 +1104,6 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(pos, S);
   A(occ_row, S);
   A(slots, S);
-  A(rslots, S);
   A(puid, S);
   A(exs, S);
   A(long_list, S);
@@ -1030,11 +1111,9 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(cnt_all, 256 * 256);
   A(ukeys, S);
   A(pkeys, S);
-  A(rkeys, S);
-  A(rows, S * E);
+  if (G == 1) A(rows, S * E);  // G > 1: inside the exported window (peers write it)
   A(deltas, S * E);
-  A(rrows, S * E);
-  A(rdeltas, S * E);
+  A(hstage, S * E);
   A(H, t->nmb_max * std::uint64_t(t->md.hw) + 2);   // +2: 16-B rounded bulk copies
   A(DL, t->nmb_max * std::uint64_t(t->md.dw) + 2);
   A(DX, t->nmb_max * E);
@@ -1042,7 +1121,6 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(dg_done, dense_grad_groups(t->md));
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
-  A(dgather, std::uint64_t(t->md.nw) * G);
 #undef A
   cudaMemsetAsync(t->ticket, 0, 8, t->st);
   cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
@@ -1064,6 +1142,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     ncclResult_t r = nccl().CommInitRank(&t->comm, G, u, t->g);
     if (r != ncclSuccess)
       return fail(set_error(HPS_ERR_NCCL, "nccl: init: %s", nccl().GetErrorString(r)));
+    if ((s = setup_p2p(t, S)) != HPS_OK) return fail(s);
   }
   if ((e = cudaStreamSynchronize(t->st)) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: %s", cudaGetErrorString(e)));
@@ -1080,6 +1159,7 @@ hps_status hps_destroy(hps_tier_t t) {
     cudaFree(c.keys);
     cudaFree(c.deltas);
   }
+  for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : t->allocs) cudaFree(p);
   if (t->hsc) cudaFreeHost(t->hsc);
   if (t->store_registered) cudaHostUnregister(t->store_host);
@@ -1148,6 +1228,7 @@ hps_status hps_pull(hps_tier_t t, const uint64_t* keys, uint64_t n, float* out_r
     launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
   }
   PullPlan plan;
+  begin_round(t);
   HPS_TRY(dedup_pull(t, t->kB, t->vB, n, &plan, true));
   HPS_TRY(check_device_error(t, "device table: missing key ", true));
   if (n) {
@@ -1168,43 +1249,59 @@ hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uin
                      (unsigned long long)n);
   if (n) {
     HPS_CUDA(cudaMemcpyAsync(t->kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
-    HPS_CUDA(cudaMemcpyAsync(t->rrows, deltas, n * std::uint64_t(t->E) * 4,
+    HPS_CUDA(cudaMemcpyAsync(t->hstage, deltas, n * std::uint64_t(t->E) * 4,
                              cudaMemcpyHostToDevice, t->st));
     launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
   }
   PullPlan plan;
+  begin_round(t);
   HPS_TRY(dedup_pull(t, t->kB, t->vB, n, &plan, false));
   HPS_CUDA(cudaMemcpyAsync(&t->hsc->U, &t->dsc->U, 8, cudaMemcpyDeviceToHost, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
-  if (t->hsc->U != n)
-    return set_error(HPS_ERR_ARG, "push: keys must be unique (a key->delta map)");
-  // deltas into send order (uid order when G == 1)
-  if (n)
-    launch(t, permute_rows_kernel, grid_for(n * t->E), 256, 0,
-           (const std::uint32_t*)t->inv, plan.pos, n, t->E, (const float*)t->rrows,
-           t->deltas);
-  std::vector<std::uint64_t> roff;
-  const std::uint64_t* srckeys;
-  const float* srcdel;
+  // a duplicate key is reported only after the collective completes, so no
+  // rank is left waiting on a peer that bailed out
+  const bool dup = t->hsc->U != n;
+  if (n)  // deltas into send order (uid order when G == 1)
+    launch(t, permute_rows_kernel, grid_for(n * t->E), 256, 0, (const std::uint32_t*)t->inv,
+           plan.pos, n, t->E, (const float*)t->hstage, t->deltas);
+  std::vector<std::uint64_t> cnt(t->G, 0);
+  std::vector<const std::uint64_t*> srckeys(t->G);
+  std::vector<const float*> srcdel(t->G);
   if (t->G == 1) {
-    roff = {0, n};
-    srckeys = t->ukeys;
-    srcdel = t->deltas;
+    cnt[0] = t->hsc->U;
+    srckeys[0] = t->ukeys;
+    srcdel[0] = t->deltas;
   } else {
-    HPS_TRY(alltoallv(t, t->deltas, plan.soff, t->rdeltas, plan.roff,
-                      sizeof(float) * std::size_t(t->E)));
-    roff = plan.roff;
-    srckeys = t->rkeys;
-    srcdel = t->rdeltas;
+    const int V = vec_of(t->E);
+    const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
+    if (V == 4)
+      launch(t, p2p_send_deltas_kernel<4>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+             (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
+             (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E,
+             t->p2p_epoch, t->done_ctr);
+    else
+      launch(t, p2p_send_deltas_kernel<1>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+             (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
+             (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E,
+             t->p2p_epoch, t->done_ctr);
+    p2p_wait(t, kPhDeltas);
+    std::vector<std::uint64_t> hdr(2 * t->G);
+    HPS_CUDA(cudaMemcpyAsync(hdr.data(), t->w_hdr, hdr.size() * 8, cudaMemcpyDeviceToHost, t->st));
+    HPS_TRY(check_device_error(t, "device table: missing key ", true));
+    for (int s = 0; s < t->G; ++s) {
+      cnt[s] = hdr[2 * s];
+      srckeys[s] = t->w_keys + s * t->slot;
+      srcdel[s] = t->w_deltas + s * t->slot * t->E;
+    }
   }
+  if (dup) return set_error(HPS_ERR_ARG, "push: keys must be unique (a key->delta map)");
   for (int s = 0; s < t->G; ++s) {
-    const std::uint64_t a = roff[s], b = roff[s + 1];
-    if (a == b) continue;
-    PendingChunk c{s, b - a, nullptr, nullptr};
+    if (!cnt[s]) continue;
+    PendingChunk c{s, cnt[s], nullptr, nullptr};
     HPS_CUDA(cudaMalloc(&c.keys, c.n * 8));
     HPS_CUDA(cudaMalloc(&c.deltas, c.n * std::uint64_t(t->E) * 4));
-    HPS_CUDA(cudaMemcpyAsync(c.keys, srckeys + a, c.n * 8, cudaMemcpyDeviceToDevice, t->st));
-    HPS_CUDA(cudaMemcpyAsync(c.deltas, srcdel + a * t->E, c.n * std::uint64_t(t->E) * 4,
+    HPS_CUDA(cudaMemcpyAsync(c.keys, srckeys[s], c.n * 8, cudaMemcpyDeviceToDevice, t->st));
+    HPS_CUDA(cudaMemcpyAsync(c.deltas, srcdel[s], c.n * std::uint64_t(t->E) * 4,
                              cudaMemcpyDeviceToDevice, t->st));
     t->pending.push_back(c);
   }
@@ -1297,30 +1394,23 @@ hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t*
 
 hps_status hps_dense_sync(hps_tier_t t, float* buf, uint64_t len, int deterministic) {
   HPS_ENTER(t);
-  if (len == 0) return HPS_OK;
-  if (t->G == 1) return HPS_OK;  // a single replica is untouched
-  float *d = nullptr, *gath = nullptr;
-  HPS_CUDA(cudaMalloc(&d, len * 4));
-  HPS_CUDA(cudaMalloc(&gath, len * 4 * std::uint64_t(t->G)));
-  HPS_CUDA(cudaMemcpyAsync(d, buf, len * 4, cudaMemcpyHostToDevice, t->st));
-  hps_status s = HPS_OK;
-  ncclResult_t r;
-  if (deterministic) {
-    r = nccl().AllGather(d, gath, len, ncclFloat32, t->comm, t->st);
-    if (r == ncclSuccess)
-      launch(t, dense_update_kernel, grid_for(len), 256, 0, (float*)nullptr,
-             (const float*)gath, len, t->N, t->D, 1.0f, 0, d, &t->dsc->err);
-  } else {
-    r = nccl().AllReduce(d, d, len, ncclFloat32, ncclSum, t->comm, t->st);
+  (void)deterministic;  // the canonical f64 sum serves both modes
+  if (len == 0 || t->G == 1) return HPS_OK;  // a single replica is untouched
+  const std::uint64_t nw = std::uint64_t(t->md.nw);
+  float* sum = t->hstage;
+  for (std::uint64_t c0 = 0; c0 < len; c0 += nw) {  // window-sized rounds
+    const std::uint64_t L = std::min(nw, len - c0);
+    HPS_CUDA(cudaMemsetAsync(t->dgrad, 0, nw * 4, t->st));
+    HPS_CUDA(cudaMemcpyAsync(t->dgrad, buf + c0, L * 4, cudaMemcpyHostToDevice, t->st));
+    begin_round(t);
+    launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->pw, t->G, t->g, nw,
+           (const float*)t->dgrad, t->p2p_epoch, t->done_ctr);
+    p2p_wait(t, kPhDense);
+    launch(t, dense_update_kernel, grid_for(nw), 256, 0, (float*)nullptr,
+           (const float*)t->w_dense, nw, t->N, t->D, 1.0f, 0, sum, &t->dsc->err);
+    HPS_CUDA(cudaMemcpyAsync(buf + c0, sum, L * 4, cudaMemcpyDeviceToHost, t->st));
   }
-  if (r != ncclSuccess) s = set_error(HPS_ERR_NCCL, "nccl: %s", nccl().GetErrorString(r));
-  if (s == HPS_OK) {
-    cudaMemcpyAsync(buf, d, len * 4, cudaMemcpyDeviceToHost, t->st);
-    cudaStreamSynchronize(t->st);
-  }
-  cudaFree(d);
-  cudaFree(gath);
-  return s;
+  return check_device_error(t, "device table: missing key ", true);
 }
 
 hps_status hps_dense_count(hps_tier_t t, uint64_t* n) {
@@ -1437,7 +1527,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   // ---- counts (one host round-trip per batch)
   HPS_CUDA(cudaMemsetAsync(T->dsc->counts, 0, sizeof(T->dsc->counts), T->st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 8 * 3, T->st));  // loss, pulled, carried
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 8, T->st));
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 16, T->st));  // fallbacks, served
   launch(T, batch_count_kernel, kSMs * 4, 256, 0, doff, dkeys, std::uint64_t(B), G, T->g, J,
          T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts, &T->dsc->err);
   HPS_CUDA(cudaMemcpyAsync(T->hsc->counts, T->dsc->counts, sizeof(T->dsc->counts),
@@ -1489,7 +1579,6 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   mark(T, HPS_T_BUILD);
   // ---- mini-batches
   const int V = vec_of(E);
-  std::uint64_t served = 0;
   for (int j = 0; j < J; ++j) {
     const std::uint64_t s = std::uint64_t(T->g) * J + j;
     const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
@@ -1503,6 +1592,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
              (const std::uint32_t*)T->occ_off, T->kB, T->vB, T->ex_of);
     }
     PullPlan plan;
+    if (G > 1) begin_round(T);
     HPS_TRY(dedup_pull(T, T->kB, T->vB, On, &plan, true, true));
     // compute (a7, a8, a9)
     const std::uint32_t* occ_row = T->inv;
@@ -1555,8 +1645,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
                  T->tvals[T->cur], E, &T->dsc->err);
       }
     } else {
-      HPS_TRY(push_apply(T, plan));
-      served += 2 * plan.R;
+      HPS_TRY(push_apply(T));
     }
     mark(T, HPS_T_APPLY);
     // dense sync + update (a12), with the verification fault knob
@@ -1581,7 +1670,8 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   }
   mark(T, HPS_T_WRITEBACK);
   HPS_CUDA(cudaMemcpyAsync(&T->hsc->loss, &T->dsc->loss, 8 * 3, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&T->hsc->fallbacks, &T->dsc->fallbacks, 8, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&T->hsc->fallbacks, &T->dsc->fallbacks, 16, cudaMemcpyDeviceToHost,
+                           T->st));
   HPS_CUDA(cudaMemcpyAsync(&T->hsc->n_ws, &T->dsc->n_ws, 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(T->hsc->cap, T->dsc->cap, 16, cudaMemcpyDeviceToHost, T->st));
   HPS_TRY(check_device_error(T, "device table: missing key ", true));
@@ -1600,7 +1690,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
     stats->pulled_keys = T->hsc->pulled;
     stats->carried_rows = T->hsc->carried;
     stats->exact_fallbacks = T->hsc->fallbacks;
-    stats->served_keys = served;
+    stats->served_keys = T->hsc->served;
     stats->occurrences = occ_total;
   }
   return HPS_OK;
