@@ -200,7 +200,12 @@ hps_status hps_set_timing(hps_tier_t h, int enable);
 hps_status hps_get_timing(hps_tier_t h, double* ms /* HPS_TIMING_SLOTS */);
 hps_status hps_reset_timing(hps_tier_t h);
 
-/* Number of kernels this library launched on the handle so far. */
+/* hps_train_batch captures its device-side body into a CUDA graph per
+ * batch shape and replays it (default on); 0 = launch kernel by kernel. */
+hps_status hps_set_graphs(hps_tier_t h, int enable);
+
+/* Number of kernels this library launched on the handle so far (a graph
+ * replay counts the kernels it contains). */
 hps_status hps_kernel_launches(hps_tier_t h, uint64_t* n);
 
 /* The CUDA stream the handle launches on (cudaStream_t as void*). */

@@ -624,7 +624,9 @@ __global__ void dense_update_kernel(float* __restrict__ w,
                                     const float* __restrict__ bufs,
                                     std::uint64_t len, int nodes, int devices,
                                     float lr, int apply, float* __restrict__ sum_out,
-                                    DevError* err) {
+                                    DevError* err, const float* bufs_odd = nullptr,
+                                    const unsigned long long* round = nullptr) {
+  if (round && (*round & 1)) bufs = bufs_odd;  // P2P window parity of this round
   for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        i < len; i += std::uint64_t(gridDim.x) * blockDim.x) {
     float s;

@@ -35,6 +35,18 @@ struct PeerWindows {
   std::uint64_t* flags[kMaxRanks];   // peer's flag array
 };
 
+// Both parity copies of every rank's windows plus the device-resident round
+// counter: kernels pick the parity from the counter, so a captured CUDA graph
+// stays valid across replays (nothing round-dependent is baked into it).
+struct P2PCtx {
+  PeerWindows par[2];
+  const unsigned long long* epoch;
+  __device__ __forceinline__ std::uint64_t round() const { return *epoch; }
+  __device__ __forceinline__ const PeerWindows& cur(std::uint64_t e) const { return par[e & 1]; }
+};
+
+__global__ void epoch_inc_kernel(unsigned long long* epoch) { *epoch += 1; }
+
 __device__ __forceinline__ void st_release_sys(std::uint64_t* p, std::uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
 }
@@ -60,11 +72,12 @@ __device__ __forceinline__ void signal_peers(const PeerWindows& pw, int G, int m
   }
 }
 
-// Waits until every source raised `phase` to `epoch` in this rank's flags.
-__global__ void p2p_wait_kernel(const std::uint64_t* __restrict__ my_flags, int G, int phase,
-                                std::uint64_t epoch, DevError* err) {
+// Waits until every source raised `phase` to the current round in this
+// rank's flags.
+__global__ void p2p_wait_kernel(P2PCtx ctx, int G, int me, int phase, DevError* err) {
   if (threadIdx.x >= unsigned(G)) return;
-  const std::uint64_t* f = my_flags + threadIdx.x * kPhases + phase;
+  const std::uint64_t epoch = ctx.round();
+  const std::uint64_t* f = ctx.par[0].flags[me] + threadIdx.x * kPhases + phase;
   long long spins = 0;
   while (ld_acquire_sys(f) < epoch) {
     if (++spins > (1ll << 27)) {  // ~10 s: a peer died; fail instead of hanging
@@ -78,11 +91,13 @@ __global__ void p2p_wait_kernel(const std::uint64_t* __restrict__ my_flags, int 
 // Requester -> owners: every unique key (owner-partitioned, positions p in
 // send order) goes to its owner's keys window, region `me`; one thread per
 // key. Thread 0 also writes the {count, send offset} headers.
-__global__ void p2p_send_keys_kernel(PeerWindows pw, int G, int me, std::uint64_t slot,
+__global__ void p2p_send_keys_kernel(P2PCtx ctx, int G, int me, std::uint64_t slot,
                                      const std::uint64_t* __restrict__ pkeys,
                                      const std::uint64_t* __restrict__ u_ptr,
                                      const std::uint64_t* __restrict__ send_off,
-                                     std::uint64_t epoch, unsigned* done_ctr) {
+                                     unsigned* done_ctr) {
+  const std::uint64_t epoch = ctx.round();
+  const PeerWindows& pw = ctx.cur(epoch);
   const std::uint64_t U = *u_ptr;
   if (blockIdx.x == 0 && threadIdx.x < unsigned(G)) {
     const int o = threadIdx.x;
@@ -103,15 +118,17 @@ __global__ void p2p_send_keys_kernel(PeerWindows pw, int G, int me, std::uint64_
 // headers): probe, cache the slot, store the row straight into requester s's
 // row buffer at its send position. VEC floats per thread.
 template <int VEC>
-__global__ void p2p_serve_rows_kernel(PeerWindows pw, int G, int me, std::uint64_t slot,
-                                      const std::uint64_t* __restrict__ my_keys,
-                                      const std::uint64_t* __restrict__ my_hdr,
+__global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t slot,
                                       const std::uint64_t* __restrict__ tkeys,
                                       const float* __restrict__ tvals,
                                       const std::uint64_t* __restrict__ cap_ptr,
                                       std::uint32_t* __restrict__ rslots, int E,
-                                      std::uint64_t epoch, unsigned* done_ctr,
-                                      unsigned long long* served, DevError* err) {
+                                      unsigned* done_ctr, unsigned long long* served,
+                                      DevError* err) {
+  const std::uint64_t epoch = ctx.round();
+  const PeerWindows& pw = ctx.cur(epoch);
+  const std::uint64_t* my_keys = pw.keys[me];
+  const std::uint64_t* my_hdr = pw.hdr[me];
   const int tpk = E / VEC;
   const std::uint64_t cap = *cap_ptr;
   std::uint64_t cnt[kMaxRanks], base[kMaxRanks];
@@ -151,12 +168,14 @@ __global__ void p2p_serve_rows_kernel(PeerWindows pw, int G, int me, std::uint64
 // Requester -> owners: delta rows (send order) into the owner's deltas
 // window, region `me`, at the request's index.
 template <int VEC>
-__global__ void p2p_send_deltas_kernel(PeerWindows pw, int G, int me, std::uint64_t slot,
+__global__ void p2p_send_deltas_kernel(P2PCtx ctx, int G, int me, std::uint64_t slot,
                                        const std::uint64_t* __restrict__ pkeys,
                                        const std::uint64_t* __restrict__ u_ptr,
                                        const std::uint64_t* __restrict__ send_off,
                                        const float* __restrict__ deltas, int E,
-                                       std::uint64_t epoch, unsigned* done_ctr) {
+                                       unsigned* done_ctr) {
+  const std::uint64_t epoch = ctx.round();
+  const PeerWindows& pw = ctx.cur(epoch);
   const int tpk = E / VEC;
   const std::uint64_t U = *u_ptr;
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < U * tpk;
@@ -180,10 +199,12 @@ __global__ void p2p_send_deltas_kernel(PeerWindows pw, int G, int me, std::uint6
 // per source inside the kernel would race across keys shared between
 // sources, so the host launches one grid per source, in order).
 template <int VEC>
-__global__ void p2p_apply_kernel(const std::uint64_t* __restrict__ my_hdr, int s,
-                                 std::uint64_t slot, const std::uint32_t* __restrict__ rslots,
-                                 const float* __restrict__ my_deltas, float* __restrict__ tvals,
-                                 int E) {
+__global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
+                                 const std::uint32_t* __restrict__ rslots,
+                                 float* __restrict__ tvals, int E) {
+  const PeerWindows& pw = ctx.cur(ctx.round());
+  const std::uint64_t* my_hdr = pw.hdr[me];
+  const float* my_deltas = pw.deltas[me];
   const int tpk = E / VEC;
   const std::uint64_t n = my_hdr[s * 2];
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < n * tpk;
@@ -209,9 +230,10 @@ __global__ void p2p_apply_kernel(const std::uint64_t* __restrict__ my_hdr, int s
 
 // Dense replica all-gather: this rank's gradient into every peer's dense
 // window, region `me`.
-__global__ void p2p_send_dense_kernel(PeerWindows pw, int G, int me, std::uint64_t nw,
-                                      const float* __restrict__ grad, std::uint64_t epoch,
-                                      unsigned* done_ctr) {
+__global__ void p2p_send_dense_kernel(P2PCtx ctx, int G, int me, std::uint64_t nw,
+                                      const float* __restrict__ grad, unsigned* done_ctr) {
+  const std::uint64_t epoch = ctx.round();
+  const PeerWindows& pw = ctx.cur(epoch);
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < nw * G;
        t += std::uint64_t(gridDim.x) * blockDim.x) {
     const int p = int(t / nw);
@@ -221,4 +243,11 @@ __global__ void p2p_send_dense_kernel(PeerWindows pw, int G, int me, std::uint64
   signal_peers(pw, G, me, kPhDense, epoch, done_ctr);
 }
 
+}  // namespace hpsgpu
+
+namespace hpsgpu {
+// The dense replicas this rank received in the current round's parity.
+__device__ __forceinline__ const float* dense_window(const P2PCtx& ctx, int me) {
+  return ctx.cur(ctx.round()).dense[me];
+}
 }  // namespace hpsgpu

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -108,9 +109,24 @@ struct Scalars {
   unsigned long long carried;  // rows filled from the previous table
   unsigned long long n_long;   // long CSR segments queued this mini-batch
   int err_any;                 // error code max-reduced over ranks
+  unsigned long long epoch;    // P2P exchange round (parity selects the windows)
   unsigned long long fallbacks;  // certified sums that needed the exact chain
   unsigned long long served;     // keys this rank served as owner (G > 1)
   DevError err;
+};
+
+struct BatchShape {
+  std::uint64_t B = 0;
+  std::uint64_t own_bound = 0, batch_bound = 0;
+  std::uint64_t mb_bound[64] = {};
+};
+
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  std::uint64_t launches = 0;
+  std::vector<int> ev_phase;
+  int cur_after = -1;
+  bool prev_after = false;
 };
 
 struct PendingChunk {
@@ -187,17 +203,14 @@ struct Tier {
   // peers' windows (p2p.cuh)
   // Windows are double-buffered by round parity (epoch & 1) so a fast rank
   // never overwrites a region a slower peer is still reading.
-  PeerWindows pwp[2]{};
-  PeerWindows pw{};                  // the current round's set
+  // The round counter lives in device memory (Scalars::epoch); kernels pick
+  // the parity themselves, so captured graphs stay valid across replays.
+  P2PCtx ctx{};
   std::uint64_t slot = 0;            // per-source region capacity (keys)
-  std::uint64_t* w_keys_p[2] = {};   // [G][slot]
+  std::uint64_t* w_keys_p[2] = {};   // this rank's windows, per parity: [G][slot]
   std::uint64_t* w_hdr_p[2] = {};    // [G][2]
   float* w_deltas_p[2] = {};         // [G][slot][E]
   float* w_dense_p[2] = {};          // [G][nw]
-  std::uint64_t* w_keys = nullptr;
-  std::uint64_t* w_hdr = nullptr;
-  float* w_deltas = nullptr;
-  float* w_dense = nullptr;
   std::uint64_t* w_flags = nullptr;  // [G][kPhases] (monotonic epochs)
   std::uint32_t* w_rslots = nullptr; // [G][slot] cached owner slots (local)
   unsigned* done_ctr = nullptr;
@@ -212,6 +225,10 @@ struct Tier {
   double acc_ms[HPS_TIMING_SLOTS] = {0};
 
   std::vector<void*> allocs;
+
+  // captured per-batch graphs (hps_train_batch), keyed by the batch shape
+  bool use_graphs = true;
+  std::map<std::vector<std::uint64_t>, GraphEntry> graphs;
 };
 
 // ----------------------------------------------------------- helpers ----
@@ -348,6 +365,7 @@ __global__ void batch_count_kernel(const std::int64_t* __restrict__ off,
       atomicAdd(&c[s % J], (unsigned long long)(off[i + 1] - off[i]));
   }
   const std::uint64_t O = std::uint64_t(off[B]);
+  if (tid == 0) counts[J + 1] = O;  // the batch's key occurrences
   unsigned long long own = 0;
   for (std::uint64_t q = tid; q < O; q += nth) {
     const std::uint64_t k = keys[q];
@@ -394,7 +412,8 @@ __global__ void pos_kernel(const std::uint32_t* __restrict__ puid,
 
 __global__ void occ_row_kernel(const std::uint32_t* __restrict__ inv,
                                const std::uint32_t* __restrict__ pos,
-                               std::uint64_t n, std::uint32_t* __restrict__ out) {
+                               Count cn, std::uint32_t* __restrict__ out) {
+  const std::uint64_t n = cn.get();
   for (std::uint64_t o = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        o < n; o += std::uint64_t(gridDim.x) * blockDim.x)
     out[o] = pos[inv[o]];
@@ -500,7 +519,7 @@ struct CompactEmit {  // out[pre] = key (and index) for selected items
 struct UniqueEmit {  // inverse index + CSR segments of a sorted (key, occ) list
   const std::uint64_t* sk;
   const std::uint32_t* so;
-  std::uint64_t n;
+  Count n;
   std::uint32_t* inv;
   std::uint64_t* ukeys;
   std::uint32_t* seg;
@@ -517,7 +536,8 @@ struct UniqueEmit {  // inverse index + CSR segments of a sorted (key, occ) list
       seg[uid] = std::uint32_t(p);
       uidv[uid] = std::uint32_t(uid);
     }
-    if (p + 1 == n) seg[uid + 1] = std::uint32_t(n);
+    const std::uint64_t nn = n.get();
+    if (p + 1 == nn) seg[uid + 1] = std::uint32_t(nn);
   }
 };
 
@@ -602,18 +622,12 @@ static int vec_of(int E) { return (E % 4 == 0) ? 4 : 1; }
 // One exchange round (a mini-batch, or one collective API call): every
 // phase of the round is tagged with the same epoch on all ranks.
 static void begin_round(Tier* t) {
-  ++t->p2p_epoch;
-  const int par = int(t->p2p_epoch & 1);
-  t->pw = t->pwp[par];
-  t->w_keys = t->w_keys_p[par];
-  t->w_hdr = t->w_hdr_p[par];
-  t->w_deltas = t->w_deltas_p[par];
-  t->w_dense = t->w_dense_p[par];
+  ++t->p2p_epoch;  // host mirror (same sequence on every rank)
+  launch(t, epoch_inc_kernel, 1, 1, 0, &t->dsc->epoch);
 }
 
 static void p2p_wait(Tier* t, int phase) {
-  launch(t, p2p_wait_kernel, 1, 32, 0, (const std::uint64_t*)t->w_flags, t->G, phase,
-         t->p2p_epoch, &t->dsc->err);
+  launch(t, p2p_wait_kernel, 1, 32, 0, t->ctx, t->G, t->g, phase, &t->dsc->err);
 }
 
 // Canonical sender order: node-major, device-major (hbm_ps.hpp:175-176).
@@ -635,7 +649,11 @@ static void mark(Tier* t, int phase) {
     cudaEventCreate(&e);
     t->evpool.push_back(e);
   }
-  cudaEventRecord(t->evpool[i], t->st);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(t->st, &cs);
+  // inside a capture the record must become an external event node
+  cudaEventRecordWithFlags(t->evpool[i], t->st,
+                           cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0);
   t->ev_phase.push_back(phase);
 }
 
@@ -710,19 +728,17 @@ struct PullPlan {
 };
 
 static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
-                             std::uint64_t n, PullPlan* plan, bool do_gather,
+                             Count cn, std::uint64_t n, PullPlan* plan, bool do_gather,
                              bool with_examples = false) {
+  // cn: the occurrence count (host or device); n: its host upper bound
   std::uint64_t* sk = nullptr;
   std::uint32_t* so = nullptr;
-  radix_sort(t, kin, vin, Count{nullptr, n}, n, t->sort_bits, true, &sk, &so);
+  radix_sort(t, kin, vin, cn, n, t->sort_bits, true, &sk, &so);
   plan->so = so;
-  if (n > 0)
-    tile_scan(t, RunStart{sk},
-              UniqueEmit{sk, so, n, t->inv, t->ukeys, t->seg, t->uidv,
-                         with_examples ? t->ex_of : nullptr, t->exs},
-              Count{nullptr, n}, n, &t->dsc->U);
-  else
-    HPS_CUDA(cudaMemsetAsync(&t->dsc->U, 0, 8, t->st));
+  tile_scan(t, RunStart{sk},
+            UniqueEmit{sk, so, cn, t->inv, t->ukeys, t->seg, t->uidv,
+                       with_examples ? t->ex_of : nullptr, t->exs},
+            cn, n, &t->dsc->U);
   const int V = vec_of(t->E);
   if (t->G == 1) {
     mark(t, HPS_T_DEDUP);
@@ -751,25 +767,23 @@ static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint3
   launch(t, pos_kernel, grid_for(n), 256, 0, (const std::uint32_t*)t->puid,
          (const std::uint64_t*)&t->dsc->U, t->pos);
   plan->pos = t->pos;
-  launch(t, p2p_send_keys_kernel, grid_for(n), 256, 0, t->pw, t->G, t->g, t->slot,
+  launch(t, p2p_send_keys_kernel, grid_for(n), 256, 0, t->ctx, t->G, t->g, t->slot,
          (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-         (const std::uint64_t*)t->dsc->send_off, t->p2p_epoch, t->done_ctr);
+         (const std::uint64_t*)t->dsc->send_off, t->done_ctr);
   p2p_wait(t, kPhKeys);
   mark(t, HPS_T_DEDUP);
   if (do_gather) {
     const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
     if (V == 4)
-      launch(t, p2p_serve_rows_kernel<4>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
-             (const std::uint64_t*)t->w_keys, (const std::uint64_t*)t->w_hdr,
+      launch(t, p2p_serve_rows_kernel<4>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
              (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
-             (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->p2p_epoch,
-             t->done_ctr, &t->dsc->served, &t->dsc->err);
+             (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->done_ctr,
+             &t->dsc->served, &t->dsc->err);
     else
-      launch(t, p2p_serve_rows_kernel<1>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
-             (const std::uint64_t*)t->w_keys, (const std::uint64_t*)t->w_hdr,
+      launch(t, p2p_serve_rows_kernel<1>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
              (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
-             (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->p2p_epoch,
-             t->done_ctr, &t->dsc->served, &t->dsc->err);
+             (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->done_ctr,
+             &t->dsc->served, &t->dsc->err);
     p2p_wait(t, kPhRows);
     mark(t, HPS_T_PULL);
   }
@@ -783,25 +797,23 @@ static hps_status push_apply(Tier* t) {
   const int V = vec_of(t->E);
   const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
   if (V == 4)
-    launch(t, p2p_send_deltas_kernel<4>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+    launch(t, p2p_send_deltas_kernel<4>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
            (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-           (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->p2p_epoch,
-           t->done_ctr);
+           (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->done_ctr);
   else
-    launch(t, p2p_send_deltas_kernel<1>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+    launch(t, p2p_send_deltas_kernel<1>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
            (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-           (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->p2p_epoch,
-           t->done_ctr);
+           (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->done_ctr);
   p2p_wait(t, kPhDeltas);
   for (int src : canonical_senders(t)) {
     if (V == 4)
       launch(t, p2p_apply_kernel<4>, grid_for(t->slot * std::uint64_t(t->E / V)), 256, 0,
-             (const std::uint64_t*)t->w_hdr, src, t->slot, (const std::uint32_t*)t->w_rslots,
-             (const float*)t->w_deltas, t->tvals[t->cur], t->E);
+             t->ctx, t->g, src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur],
+             t->E);
     else
       launch(t, p2p_apply_kernel<1>, grid_for(t->slot * std::uint64_t(t->E / V)), 256, 0,
-             (const std::uint64_t*)t->w_hdr, src, t->slot, (const std::uint32_t*)t->w_rslots,
-             (const float*)t->w_deltas, t->tvals[t->cur], t->E);
+             t->ctx, t->g, src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur],
+             t->E);
   }
   return HPS_OK;
 }
@@ -812,16 +824,18 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
   if (t->G == 1) {
     launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense,
            (const float*)t->dgrad, nw, t->N, t->D, t->cfg.learning_rate, int(apply),
-           (float*)nullptr, &t->dsc->err);
+           (float*)nullptr, &t->dsc->err, (const float*)nullptr,
+           (const unsigned long long*)nullptr);
     return HPS_OK;
   }
   // replicas all-gathered over NVLink, then the canonical f64 sum (det and
   // fast modes alike: the canonical order costs nothing extra here)
-  launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->pw, t->G, t->g, nw,
-         (const float*)t->dgrad, t->p2p_epoch, t->done_ctr);
+  launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->ctx, t->G, t->g, nw,
+         (const float*)t->dgrad, t->done_ctr);
   p2p_wait(t, kPhDense);
-  launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense, (const float*)t->w_dense, nw,
-         t->N, t->D, t->cfg.learning_rate, int(apply), (float*)nullptr, &t->dsc->err);
+  launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense, (const float*)t->w_dense_p[0],
+         nw, t->N, t->D, t->cfg.learning_rate, int(apply), (float*)nullptr, &t->dsc->err,
+         (const float*)t->w_dense_p[1], (const unsigned long long*)&t->dsc->epoch);
   return HPS_OK;
 }
 
@@ -935,7 +949,7 @@ static hps_status setup_p2p(Tier* t, std::uint64_t S) {
     }
     for (int par = 0; par < 2; ++par) {
       char* pb = base + o_par + par * par_bytes;
-      PeerWindows& w = t->pwp[par];
+      PeerWindows& w = t->ctx.par[par];
       w.keys[p] = reinterpret_cast<std::uint64_t*>(pb + p_keys);
       w.hdr[p] = reinterpret_cast<std::uint64_t*>(pb + p_hdr);
       w.deltas[p] = reinterpret_cast<float*>(pb + p_deltas);
@@ -944,7 +958,188 @@ static hps_status setup_p2p(Tier* t, std::uint64_t S) {
       w.rows[p] = reinterpret_cast<float*>(base + o_rows);
     }
   }
-  begin_round(t);  // epoch 1 (flags start at 0)
+  t->ctx.epoch = &t->dsc->epoch;
+  begin_round(t);  // round 1 (flags start at 0)
+  return HPS_OK;
+}
+
+// ------------------------------------------------- the per-batch body --
+
+inline std::uint64_t shape_bound(std::uint64_t x) {
+  std::uint64_t p = 4096;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// Everything of hps_train_batch after the count round-trip. Enqueue-only (no
+// host synchronisation, no host-read device values, round counter on the
+// device), so it can be captured into a CUDA graph and replayed. skip_mb:
+// mini-batch of this batch whose dense sync+update is skipped, -1 = none.
+static hps_status enqueue_batch_body(Tier* T, const BatchShape& sh, int skip_mb) {
+  const int G = T->G, J = T->J, E = T->E;
+  const std::uint64_t B = sh.B, GJ = std::uint64_t(G) * J;
+  const std::int64_t* doff = T->b_off;
+  const std::uint64_t* dkeys = T->b_keys;
+  const std::uint8_t* dlab = T->b_lab;
+  const Count own_n{&T->dsc->counts[J], 0};
+  // ---- working set (a1, a2) + build (a3, a4)
+  {
+    const std::uint64_t* kin = dkeys;
+    if (G > 1) {  // stable compaction of the owned keys into kB
+      tile_scan(T, OwnedKey{dkeys, std::uint64_t(G), std::uint64_t(T->g)},
+                CompactEmit{dkeys, nullptr, T->kB, nullptr},
+                Count{reinterpret_cast<const std::uint64_t*>(doff + B), 0}, sh.batch_bound,
+                &T->dsc->total);
+      kin = T->kB;
+    }
+    std::uint64_t* sk = nullptr;
+    std::uint32_t* so = nullptr;
+    radix_sort(T, kin, nullptr, own_n, sh.own_bound, T->sort_bits, false, &sk, &so);
+    tile_scan(T, RunStart{sk}, CompactEmit{sk, nullptr, T->ws, nullptr}, own_n, sh.own_bound,
+              &T->dsc->n_ws);
+    build_table(T, sh.own_bound, nullptr, nullptr);
+  }
+  mark(T, HPS_T_BUILD);
+  // ---- mini-batches
+  const int V = vec_of(E);
+  for (int j = 0; j < J; ++j) {
+    const std::uint64_t s = std::uint64_t(T->g) * J + j;
+    const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
+    const Count on_n{&T->dsc->counts[j], 0};
+    const std::uint64_t ob = sh.mb_bound[j];
+    const ShardMap sm{s, GJ, n};
+    // shard gather + dedup (a5)
+    if (n) {
+      tile_scan(T, ShardLen{sm, doff}, ShardLenEmit{T->occ_off, n}, Count{nullptr, n}, n,
+                &T->dsc->total);
+      launch(T, shard_gather_kernel, grid_for(n * 32), 256, 0, sm, doff, dkeys,
+             (const std::uint32_t*)T->occ_off, T->kB, T->vB, T->ex_of);
+    }
+    PullPlan plan;
+    if (G > 1) begin_round(T);
+    HPS_TRY(dedup_pull(T, T->kB, T->vB, on_n, ob, &plan, true, true));
+    // compute (a7, a8, a9)
+    const std::uint32_t* occ_row = T->inv;
+    if (G > 1) {
+      launch(T, occ_row_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)T->inv, plan.pos,
+             on_n, T->occ_row);
+      occ_row = T->occ_row;
+    }
+    if (n) {
+      const int LPE = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
+      const int epb = 128 / LPE;
+      const size_t smem = size_t((T->md.nw + 1) & ~1) * 4 +
+                          size_t(epb) * (T->md.hw + T->md.dw + T->md.maxw) * 8;
+      const unsigned blocks = unsigned(std::min<std::uint64_t>((n + epb - 1) / epb, kSMs * 8));
+      auto k = LPE == 8 ? fwd_bwd_kernel<8> : (LPE == 16 ? fwd_bwd_kernel<16> : fwd_bwd_kernel<32>);
+      launch(T, k, blocks, 128, smem, T->md, sm, (const float*)T->dense,
+             (const std::uint32_t*)T->occ_off, occ_row, (const float*)T->rows, dlab, T->H,
+             T->DL, T->DX, &T->dsc->loss, &T->dsc->err);
+      mark(T, HPS_T_FWDBWD);
+      // dense-grad reduce on the side stream, overlapping the sparse reduce
+      HPS_CUDA(cudaEventRecord(T->fork, T->st));
+      HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
+      launch_on(T, T->st2, dense_grad_p1_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
+                0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart);
+      launch_on(T, T->st2, dense_grad_p2_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
+                0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart, T->dg_done,
+                T->dgrad, &T->dsc->fallbacks);
+      HPS_CUDA(cudaEventRecord(T->join, T->st2));
+      HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob));
+      HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
+    } else {
+      HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));
+    }
+    mark(T, HPS_T_GRADS);
+    // push + canonical apply (a10, a11)
+    if (G == 1) {
+      const std::uint64_t work = ob * std::uint64_t(E / V);
+      if (V == 4)
+        launch(T, table_apply_kernel<4>, grid_for(work), 256, 0, (const std::uint32_t*)T->slots,
+               (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
+               (const std::uint64_t*)nullptr, (const float*)T->deltas,
+               (const std::uint64_t*)&T->dsc->U, std::uint64_t(0), T->tvals[T->cur], E,
+               &T->dsc->err);
+      else
+        launch(T, table_apply_kernel<1>, grid_for(work), 256, 0, (const std::uint32_t*)T->slots,
+               (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
+               (const std::uint64_t*)nullptr, (const float*)T->deltas,
+               (const std::uint64_t*)&T->dsc->U, std::uint64_t(0), T->tvals[T->cur], E,
+               &T->dsc->err);
+    } else {
+      HPS_TRY(push_apply(T));
+    }
+    mark(T, HPS_T_APPLY);
+    // dense sync + update (a12), with the verification fault knob
+    if (j != skip_mb) HPS_TRY(dense_sync_update(T, true));
+    mark(T, HPS_T_DENSE);
+  }
+  // ---- write-back to the value store (a13)
+  if (T->store) {
+    const std::uint64_t work = sh.own_bound * std::uint64_t(E / V);
+    if (V == 4)
+      launch(T, table_dump_kernel<4>, grid_for(work), 256, 0, (const std::uint64_t*)T->ws,
+             (const std::uint64_t*)&T->dsc->n_ws, (const std::uint64_t*)T->tkeys[T->cur],
+             (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
+             T->store_keys, (float*)nullptr, E, &T->dsc->err);
+    else
+      launch(T, table_dump_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)T->ws,
+             (const std::uint64_t*)&T->dsc->n_ws, (const std::uint64_t*)T->tkeys[T->cur],
+             (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
+             T->store_keys, (float*)nullptr, E, &T->dsc->err);
+  }
+  mark(T, HPS_T_WRITEBACK);
+  return HPS_OK;
+}
+
+// Capture the body once per shape (and table parity, store, timing), then
+// replay: the whole batch becomes one cudaGraphLaunch.
+static hps_status run_body_graph(Tier* T, const BatchShape& sh) {
+  std::vector<std::uint64_t> key = {sh.B, sh.own_bound, sh.batch_bound,
+                                    std::uint64_t(T->cur + 1), std::uint64_t(T->has_prev),
+                                    reinterpret_cast<std::uint64_t>(T->store), T->store_keys,
+                                    std::uint64_t(T->timing)};
+  for (int j = 0; j < T->J; ++j) key.push_back(sh.mb_bound[j]);
+  auto it = T->graphs.find(key);
+  const int cur_before = T->cur;
+  const bool prev_before = T->has_prev;
+  if (it == T->graphs.end()) {
+    if (T->graphs.size() >= 16) {  // bounded cache
+      cudaGraphExecDestroy(T->graphs.begin()->second.exec);
+      T->graphs.erase(T->graphs.begin());
+    }
+    GraphEntry ge;
+    const std::uint64_t l0 = T->launches;
+    const std::size_t ev0 = T->ev_phase.size();
+    HPS_CUDA(cudaStreamBeginCapture(T->st, cudaStreamCaptureModeThreadLocal));
+    const hps_status s = enqueue_batch_body(T, sh, -1);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(T->st, &g);
+    if (s != HPS_OK) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    if (ce != cudaSuccess)
+      return set_error(HPS_ERR_CUDA, "cuda: graph capture: %s", cudaGetErrorString(ce));
+    const cudaError_t ie = cudaGraphInstantiate(&ge.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess)
+      return set_error(HPS_ERR_CUDA, "cuda: graph instantiate: %s", cudaGetErrorString(ie));
+    ge.launches = T->launches - l0;
+    ge.ev_phase.assign(T->ev_phase.begin() + ev0, T->ev_phase.end());
+    ge.cur_after = T->cur;
+    ge.prev_after = T->has_prev;
+    T->launches = l0;  // counted per replay below
+    T->ev_phase.resize(ev0);
+    T->cur = cur_before;
+    T->has_prev = prev_before;
+    it = T->graphs.emplace(key, std::move(ge)).first;
+  }
+  HPS_CUDA(cudaGraphLaunch(it->second.exec, T->st));
+  T->launches += it->second.launches;
+  T->ev_phase.insert(T->ev_phase.end(), it->second.ev_phase.begin(), it->second.ev_phase.end());
+  T->cur = it->second.cur_after;
+  T->has_prev = it->second.prev_after;
   return HPS_OK;
 }
 
@@ -1159,6 +1354,7 @@ hps_status hps_destroy(hps_tier_t t) {
     cudaFree(c.keys);
     cudaFree(c.deltas);
   }
+  for (auto& kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
   for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : t->allocs) cudaFree(p);
   if (t->hsc) cudaFreeHost(t->hsc);
@@ -1229,7 +1425,7 @@ hps_status hps_pull(hps_tier_t t, const uint64_t* keys, uint64_t n, float* out_r
   }
   PullPlan plan;
   begin_round(t);
-  HPS_TRY(dedup_pull(t, t->kB, t->vB, n, &plan, true));
+  HPS_TRY(dedup_pull(t, t->kB, t->vB, Count{nullptr, n}, n, &plan, true));
   HPS_TRY(check_device_error(t, "device table: missing key ", true));
   if (n) {
     launch(t, scatter_rows_kernel, grid_for(n * t->E), 256, 0, (const std::uint32_t*)t->inv,
@@ -1255,7 +1451,7 @@ hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uin
   }
   PullPlan plan;
   begin_round(t);
-  HPS_TRY(dedup_pull(t, t->kB, t->vB, n, &plan, false));
+  HPS_TRY(dedup_pull(t, t->kB, t->vB, Count{nullptr, n}, n, &plan, false));
   HPS_CUDA(cudaMemcpyAsync(&t->hsc->U, &t->dsc->U, 8, cudaMemcpyDeviceToHost, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
   // a duplicate key is reported only after the collective completes, so no
@@ -1275,23 +1471,23 @@ hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uin
     const int V = vec_of(t->E);
     const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
     if (V == 4)
-      launch(t, p2p_send_deltas_kernel<4>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+      launch(t, p2p_send_deltas_kernel<4>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
              (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-             (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E,
-             t->p2p_epoch, t->done_ctr);
+             (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->done_ctr);
     else
-      launch(t, p2p_send_deltas_kernel<1>, grid_for(work), 256, 0, t->pw, t->G, t->g, t->slot,
+      launch(t, p2p_send_deltas_kernel<1>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
              (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-             (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E,
-             t->p2p_epoch, t->done_ctr);
+             (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->done_ctr);
     p2p_wait(t, kPhDeltas);
+    const int par = int(t->p2p_epoch & 1);
     std::vector<std::uint64_t> hdr(2 * t->G);
-    HPS_CUDA(cudaMemcpyAsync(hdr.data(), t->w_hdr, hdr.size() * 8, cudaMemcpyDeviceToHost, t->st));
+    HPS_CUDA(cudaMemcpyAsync(hdr.data(), t->w_hdr_p[par], hdr.size() * 8, cudaMemcpyDeviceToHost,
+                             t->st));
     HPS_TRY(check_device_error(t, "device table: missing key ", true));
     for (int s = 0; s < t->G; ++s) {
       cnt[s] = hdr[2 * s];
-      srckeys[s] = t->w_keys + s * t->slot;
-      srcdel[s] = t->w_deltas + s * t->slot * t->E;
+      srckeys[s] = t->w_keys_p[par] + s * t->slot;
+      srcdel[s] = t->w_deltas_p[par] + s * t->slot * t->E;
     }
   }
   if (dup) return set_error(HPS_ERR_ARG, "push: keys must be unique (a key->delta map)");
@@ -1403,11 +1599,12 @@ hps_status hps_dense_sync(hps_tier_t t, float* buf, uint64_t len, int determinis
     HPS_CUDA(cudaMemsetAsync(t->dgrad, 0, nw * 4, t->st));
     HPS_CUDA(cudaMemcpyAsync(t->dgrad, buf + c0, L * 4, cudaMemcpyHostToDevice, t->st));
     begin_round(t);
-    launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->pw, t->G, t->g, nw,
-           (const float*)t->dgrad, t->p2p_epoch, t->done_ctr);
+    launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->ctx, t->G, t->g, nw,
+           (const float*)t->dgrad, t->done_ctr);
     p2p_wait(t, kPhDense);
     launch(t, dense_update_kernel, grid_for(nw), 256, 0, (float*)nullptr,
-           (const float*)t->w_dense, nw, t->N, t->D, 1.0f, 0, sum, &t->dsc->err);
+           (const float*)t->w_dense_p[0], nw, t->N, t->D, 1.0f, 0, sum, &t->dsc->err,
+           (const float*)t->w_dense_p[1], (const unsigned long long*)&t->dsc->epoch);
     HPS_CUDA(cudaMemcpyAsync(buf + c0, sum, L * 4, cudaMemcpyDeviceToHost, t->st));
   }
   return check_device_error(t, "device table: missing key ", true);
@@ -1435,6 +1632,8 @@ hps_status hps_set_dense(hps_tier_t t, const float* w) {
 
 hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on_device) {
   HPS_ENTER(t);
+  for (auto& kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
+  t->graphs.clear();
   if (t->store_registered) {
     cudaHostUnregister(t->store_host);
     t->store_registered = false;
@@ -1504,31 +1703,37 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
     return set_error(HPS_ERR_CAPACITY, "train_batch: %llu examples exceed max_batch_examples",
                      (unsigned long long)B);
   Tier* T = t;
-  const int G = T->G, J = T->J, E = T->E;
+  const int G = T->G, J = T->J;
   const std::uint64_t GJ = std::uint64_t(G) * J;
-  // ---- stage the batch
+  // ---- stage the batch into the tier's own buffers (so captured graphs
+  // never depend on caller pointers)
   timing_begin(T);
-  const std::int64_t* doff = offsets;
-  const std::uint64_t* dkeys = keys;
-  const std::uint8_t* dlab = labels;
-  std::uint64_t O = 0;
-  if (!on_device) {
-    O = std::uint64_t(offsets[B]);
+  if (on_device) {
+    std::int64_t last = 0;
+    HPS_CUDA(cudaMemcpyAsync(T->b_off, offsets, (B + 1) * 8, cudaMemcpyDeviceToDevice, T->st));
+    HPS_CUDA(cudaMemcpyAsync(&last, offsets + B, 8, cudaMemcpyDeviceToHost, T->st));
+    HPS_CUDA(cudaStreamSynchronize(T->st));
+    if (std::uint64_t(last) > T->Omax)
+      return set_error(HPS_ERR_CAPACITY, "train_batch: %llu keys exceed max_batch_keys",
+                       (unsigned long long)last);
+    HPS_CUDA(cudaMemcpyAsync(T->b_keys, keys, std::uint64_t(last) * 8, cudaMemcpyDeviceToDevice,
+                             T->st));
+    HPS_CUDA(cudaMemcpyAsync(T->b_lab, labels, B, cudaMemcpyDeviceToDevice, T->st));
+  } else {
+    const std::uint64_t O = std::uint64_t(offsets[B]);
     if (O > T->Omax)
       return set_error(HPS_ERR_CAPACITY, "train_batch: %llu keys exceed max_batch_keys",
                        (unsigned long long)O);
     HPS_CUDA(cudaMemcpyAsync(T->b_off, offsets, (B + 1) * 8, cudaMemcpyHostToDevice, T->st));
     HPS_CUDA(cudaMemcpyAsync(T->b_keys, keys, O * 8, cudaMemcpyHostToDevice, T->st));
     HPS_CUDA(cudaMemcpyAsync(T->b_lab, labels, B, cudaMemcpyHostToDevice, T->st));
-    doff = T->b_off;
-    dkeys = T->b_keys;
-    dlab = T->b_lab;
   }
   // ---- counts (one host round-trip per batch)
   HPS_CUDA(cudaMemsetAsync(T->dsc->counts, 0, sizeof(T->dsc->counts), T->st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 8 * 3, T->st));  // loss, pulled, carried
   HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 16, T->st));  // fallbacks, served
-  launch(T, batch_count_kernel, kSMs * 4, 256, 0, doff, dkeys, std::uint64_t(B), G, T->g, J,
+  launch(T, batch_count_kernel, kSMs * 4, 256, 0, (const std::int64_t*)T->b_off,
+         (const std::uint64_t*)T->b_keys, std::uint64_t(B), G, T->g, J,
          T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts, &T->dsc->err);
   HPS_CUDA(cudaMemcpyAsync(T->hsc->counts, T->dsc->counts, sizeof(T->dsc->counts),
                            cudaMemcpyDeviceToHost, T->st));
@@ -1539,136 +1744,21 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   mark(T, HPS_T_STAGE);
   if (own > T->Wmax || occ_total > T->Omax)
     return set_error(HPS_ERR_CAPACITY, "train_batch: batch exceeds configured maxima");
-  // ---- working set (a1, a2) + build (a3, a4)
-  {
-    const std::uint64_t* kin = dkeys;
-    std::uint64_t nsort = own;
-    if (G > 1) {
-      // stable compaction of owned keys into kB
-      const std::uint64_t Oall = on_device ? 0 : O;
-      (void)Oall;
-      // total occurrences of the batch are needed as the scan length
-      std::uint64_t Ob = 0;
-      {
-        std::int64_t last = 0;
-        if (on_device) {
-          HPS_CUDA(cudaMemcpyAsync(&T->hsc->total, doff + B, 8, cudaMemcpyDeviceToHost, T->st));
-          HPS_CUDA(cudaStreamSynchronize(T->st));
-          last = std::int64_t(T->hsc->total);
-        } else {
-          last = offsets[B];
-        }
-        Ob = std::uint64_t(last);
-      }
-      tile_scan(T, OwnedKey{dkeys, std::uint64_t(G), std::uint64_t(T->g)},
-                CompactEmit{dkeys, nullptr, T->kB, nullptr}, Count{nullptr, Ob}, Ob,
-                &T->dsc->total);
-      kin = T->kB;
-    }
-    std::uint64_t* sk = nullptr;
-    std::uint32_t* so = nullptr;
-    if (nsort) {
-      radix_sort(T, kin, nullptr, Count{nullptr, nsort}, nsort, T->sort_bits, false, &sk, &so);
-      tile_scan(T, RunStart{sk}, CompactEmit{sk, nullptr, T->ws, nullptr},
-                Count{nullptr, nsort}, nsort, &T->dsc->n_ws);
-    } else {
-      HPS_CUDA(cudaMemsetAsync(&T->dsc->n_ws, 0, 8, T->st));
-    }
-    build_table(T, nsort, nullptr, nullptr);
+  // ---- the device-side body: launch-only, sized by power-of-two upper bounds
+  // of the counts, so one captured CUDA graph serves every batch of a shape
+  BatchShape sh;
+  sh.B = B;
+  sh.own_bound = shape_bound(own);
+  sh.batch_bound = shape_bound(std::uint64_t(T->hsc->counts[J + 1]));
+  for (int j = 0; j < J; ++j) sh.mb_bound[j] = shape_bound(T->hsc->counts[j]);
+  const std::int64_t first_mb = T->step * J;
+  const bool skip_in_batch = T->cfg.inject_skip_sync >= first_mb &&
+                             T->cfg.inject_skip_sync < first_mb + J;
+  if (T->use_graphs && !skip_in_batch) {
+    HPS_TRY(run_body_graph(T, sh));
+  } else {
+    HPS_TRY(enqueue_batch_body(T, sh, skip_in_batch ? int(T->cfg.inject_skip_sync - first_mb) : -1));
   }
-  mark(T, HPS_T_BUILD);
-  // ---- mini-batches
-  const int V = vec_of(E);
-  for (int j = 0; j < J; ++j) {
-    const std::uint64_t s = std::uint64_t(T->g) * J + j;
-    const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
-    const std::uint64_t On = T->hsc->counts[j];
-    const ShardMap sm{s, GJ, n};
-    // shard gather + dedup (a5)
-    if (n) {
-      tile_scan(T, ShardLen{sm, doff}, ShardLenEmit{T->occ_off, n}, Count{nullptr, n}, n,
-                &T->dsc->total);
-      launch(T, shard_gather_kernel, grid_for(n * 32), 256, 0, sm, doff, dkeys,
-             (const std::uint32_t*)T->occ_off, T->kB, T->vB, T->ex_of);
-    }
-    PullPlan plan;
-    if (G > 1) begin_round(T);
-    HPS_TRY(dedup_pull(T, T->kB, T->vB, On, &plan, true, true));
-    // compute (a7, a8, a9)
-    const std::uint32_t* occ_row = T->inv;
-    if (G > 1 && On) {
-      launch(T, occ_row_kernel, grid_for(On), 256, 0, (const std::uint32_t*)T->inv,
-             plan.pos, On, T->occ_row);
-      occ_row = T->occ_row;
-    }
-    if (n) {
-      const int LPE = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
-      const int epb = 128 / LPE;
-      const size_t smem = size_t((T->md.nw + 1) & ~1) * 4 +
-                          size_t(epb) * (T->md.hw + T->md.dw + T->md.maxw) * 8;
-      const unsigned blocks = unsigned(std::min<std::uint64_t>((n + epb - 1) / epb, kSMs * 8));
-      auto k = LPE == 8 ? fwd_bwd_kernel<8> : (LPE == 16 ? fwd_bwd_kernel<16> : fwd_bwd_kernel<32>);
-      launch(T, k, blocks, 128, smem, T->md, sm, (const float*)T->dense,
-             (const std::uint32_t*)T->occ_off, occ_row, (const float*)T->rows, dlab, T->H,
-             T->DL, T->DX, &T->dsc->loss, &T->dsc->err);
-      mark(T, HPS_T_FWDBWD);
-      // dense-grad reduce on the side stream, overlapping the sparse reduce
-      HPS_CUDA(cudaEventRecord(T->fork, T->st));
-      HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
-      launch_on(T, T->st2, dense_grad_p1_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
-                0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart);
-      launch_on(T, T->st2, dense_grad_p2_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
-                0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart, T->dg_done,
-                T->dgrad, &T->dsc->fallbacks);
-      HPS_CUDA(cudaEventRecord(T->join, T->st2));
-      HPS_TRY(launch_sparse_delta(T, n, plan.pos, On));
-      HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
-    } else {
-      HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));
-    }
-    mark(T, HPS_T_GRADS);
-    // push + canonical apply (a10, a11)
-    if (G == 1) {
-      if (On) {
-        const std::uint64_t work = On * std::uint64_t(E / V);
-        if (V == 4)
-          launch(T, table_apply_kernel<4>, grid_for(work), 256, 0,
-                 (const std::uint32_t*)T->slots, (const std::uint64_t*)nullptr,
-                 (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
-                 (const float*)T->deltas, (const std::uint64_t*)&T->dsc->U, std::uint64_t(0),
-                 T->tvals[T->cur], E, &T->dsc->err);
-        else
-          launch(T, table_apply_kernel<1>, grid_for(work), 256, 0,
-                 (const std::uint32_t*)T->slots, (const std::uint64_t*)nullptr,
-                 (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
-                 (const float*)T->deltas, (const std::uint64_t*)&T->dsc->U, std::uint64_t(0),
-                 T->tvals[T->cur], E, &T->dsc->err);
-      }
-    } else {
-      HPS_TRY(push_apply(T));
-    }
-    mark(T, HPS_T_APPLY);
-    // dense sync + update (a12), with the verification fault knob
-    const std::int64_t global_mb = T->step * J + j;
-    const bool skip = global_mb == T->cfg.inject_skip_sync;
-    if (!skip) HPS_TRY(dense_sync_update(T, true));
-    mark(T, HPS_T_DENSE);
-  }
-  // ---- write-back to the value store (a13)
-  if (T->store) {
-    const std::uint64_t work = own * std::uint64_t(E / V);
-    if (V == 4)
-      launch(T, table_dump_kernel<4>, grid_for(work), 256, 0, (const std::uint64_t*)T->ws,
-             (const std::uint64_t*)&T->dsc->n_ws, (const std::uint64_t*)T->tkeys[T->cur],
-             (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
-             T->store_keys, (float*)nullptr, E, &T->dsc->err);
-    else
-      launch(T, table_dump_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)T->ws,
-             (const std::uint64_t*)&T->dsc->n_ws, (const std::uint64_t*)T->tkeys[T->cur],
-             (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
-             T->store_keys, (float*)nullptr, E, &T->dsc->err);
-  }
-  mark(T, HPS_T_WRITEBACK);
   HPS_CUDA(cudaMemcpyAsync(&T->hsc->loss, &T->dsc->loss, 8 * 3, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&T->hsc->fallbacks, &T->dsc->fallbacks, 16, cudaMemcpyDeviceToHost,
                            T->st));
@@ -1693,6 +1783,12 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
     stats->served_keys = T->hsc->served;
     stats->occurrences = occ_total;
   }
+  return HPS_OK;
+}
+
+hps_status hps_set_graphs(hps_tier_t t, int enable) {
+  if (!t) return set_error(HPS_ERR_ARG, "null handle");
+  t->use_graphs = enable != 0;
   return HPS_OK;
 }
 

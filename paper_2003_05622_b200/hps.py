@@ -108,6 +108,7 @@ _SIGS = {
     "hps_get_timing": ([_P, _P], ctypes.c_int),
     "hps_reset_timing": ([_P], ctypes.c_int),
     "hps_kernel_launches": ([_P, _U64P], ctypes.c_int),
+    "hps_set_graphs": ([_P, ctypes.c_int], ctypes.c_int),
     "hps_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "hps_gen_dataset": ([_U64, _U64, _U64, ctypes.c_int, ctypes.c_double, _U64,
                          ctypes.c_double, _U64, _P, _P, _P], ctypes.c_int),
@@ -356,6 +357,9 @@ class Tier:
 
     def reset_timing(self) -> None:
         _check(lib().hps_reset_timing(self._h))
+
+    def set_graphs(self, on: bool) -> None:
+        _check(lib().hps_set_graphs(self._h, int(on)))
 
     def kernel_launches(self) -> int:
         n = ctypes.c_uint64()
