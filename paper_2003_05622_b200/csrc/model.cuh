@@ -439,6 +439,7 @@ inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw 
 // registers, then adds them in order. Longer segments (hot Zipf keys: up to
 // the whole shard) are queued for sparse_delta_long_kernel.
 constexpr int kLongSeg = 32;
+constexpr int kBigChunk = 512;  // segments longer than this are split over CTAs
 constexpr int kStageDepth = 8;
 
 __device__ __forceinline__ void write_delta(float* out, std::uint64_t row, int E, int d,
@@ -457,7 +458,9 @@ __global__ void __launch_bounds__(256)
                         const double* __restrict__ DX, float* __restrict__ out,
                         unsigned long long* __restrict__ pulled,
                         std::uint32_t* __restrict__ long_list,
-                        unsigned long long* __restrict__ n_long) {
+                        unsigned long long* __restrict__ n_long,
+                        std::uint32_t* __restrict__ big_list,
+                        unsigned long long* __restrict__ n_big) {
   const std::uint64_t U = *u_ptr;
   if (pulled && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(pulled, (unsigned long long)U);
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
@@ -471,7 +474,12 @@ __global__ void __launch_bounds__(256)
        u += groups) {
     const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
     if (p1 - p0 > std::uint32_t(kLongSeg)) {
-      if (sub == 0) long_list[atomicAdd(n_long, 1ull)] = std::uint32_t(u);
+      if (sub == 0) {
+        if (p1 - p0 > std::uint32_t(kBigChunk))
+          big_list[atomicAdd(n_big, 1ull)] = std::uint32_t(u);
+        else
+          long_list[atomicAdd(n_long, 1ull)] = std::uint32_t(u);
+      }
       continue;
     }
     double acc[kDPL];
@@ -515,8 +523,8 @@ __global__ void __launch_bounds__(256)
 // magnitudes B. Thread d combines and certifies (certify_f32); uncertified
 // dimensions are recomputed in the exact order (the CTA stages the values in
 // shared memory, one thread chains them).
-constexpr int kLongThreads = 512;
-constexpr int kLongChunk = 2048;
+constexpr int kLongThreads = 256;
+constexpr int kLongChunk = kBigChunk;
 
 __global__ void __launch_bounds__(kLongThreads)
     sparse_delta_long_kernel(int E, float lr, std::uint64_t n,
@@ -600,6 +608,217 @@ __global__ void __launch_bounds__(kLongThreads)
       for (std::uint32_t c0 = p0; c0 < p1; c0 += kFallbackChunk) {
         const int cnt = int(p1 - c0 < kFallbackChunk ? p1 - c0 : kFallbackChunk);
         for (int j = threadIdx.x; j < cnt; j += kLongThreads)
+          stage[j] = DX[std::uint64_t(exs[c0 + j]) * E + dd];
+        __syncthreads();
+        if (int(threadIdx.x) == dd) acc = chain_sum(stage, cnt, acc);
+        __syncthreads();
+      }
+      if (int(threadIdx.x) == dd) {
+        g = __double2float_rn(__dmul_rn(acc, inv_n));
+        if (fallbacks) atomicAdd(fallbacks, 1ull);
+      }
+    }
+    if (int(threadIdx.x) < E)
+      out[std::uint64_t(pos ? pos[u] : u) * E + threadIdx.x] = -__fmul_rn(lr, g);
+    __syncthreads();
+  }
+}
+
+// ---- big segments (> kBigChunk occurrences): split over CTAs -------------
+//
+// Work item w = (big key, chunk of kBigChunk occurrences). big_plan: prefix
+// of the per-key chunk counts. p1: per (item, slice, dim) Neumaier total and
+// sum|x|. p2: the item's offset is the total of the key's earlier chunks and
+// slices; the slice is re-walked for B; the key's last CTA combines all
+// chunks, certifies (certify_f32) and, rarely, recomputes the exact chain.
+constexpr int kBigThreads = 256;
+struct BigPart {
+  double hi, lo, a, b;
+};
+struct ChunkSum {  // one chunk of one dimension: total (Neumaier), sum|x|, B bound
+  double hi, lo, a, b;
+};
+
+__global__ void big_plan_kernel(const std::uint32_t* __restrict__ big_list,
+                                const unsigned long long* __restrict__ n_big,
+                                const std::uint32_t* __restrict__ seg,
+                                std::uint32_t* __restrict__ chunk_off,
+                                unsigned long long* __restrict__ n_items) {
+  __shared__ std::uint32_t ws[32];
+  const std::uint64_t NB = *n_big;
+  std::uint32_t carry = 0;
+  for (std::uint64_t b0 = 0; b0 < NB; b0 += blockDim.x) {
+    const std::uint64_t i = b0 + threadIdx.x;
+    std::uint32_t v = 0;
+    if (i < NB) {
+      const std::uint32_t u = big_list[i];
+      v = (seg[u + 1] - seg[u] + kBigChunk - 1) / kBigChunk;
+    }
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    std::uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= unsigned(o)) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    std::uint32_t pre = carry;
+    for (unsigned w = 0; w < warp; ++w) pre += ws[w];
+    if (i < NB) chunk_off[i] = pre + x - v;
+    std::uint32_t tot = 0;
+    for (unsigned w = 0; w < blockDim.x / 32; ++w) tot += ws[w];
+    __syncthreads();
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    chunk_off[NB] = carry;
+    *n_items = carry;
+  }
+}
+
+__device__ __forceinline__ void big_item(const std::uint32_t* chunk_off, std::uint64_t NB,
+                                         std::uint64_t w, std::uint32_t* key_idx,
+                                         std::uint32_t* chunk) {
+  std::uint64_t lo = 0, hi = NB;  // last key with chunk_off <= w
+  while (hi - lo > 1) {
+    const std::uint64_t mid = (lo + hi) / 2;
+    if (chunk_off[mid] <= w) lo = mid; else hi = mid;
+  }
+  *key_idx = std::uint32_t(lo);
+  *chunk = std::uint32_t(w - chunk_off[lo]);
+}
+
+__global__ void __launch_bounds__(kBigThreads)
+    big_p1_kernel(int E, const std::uint32_t* __restrict__ big_list,
+                  const unsigned long long* __restrict__ n_big,
+                  const std::uint32_t* __restrict__ chunk_off,
+                  const unsigned long long* __restrict__ n_items,
+                  const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
+                  const double* __restrict__ DX, BigPart* __restrict__ part,
+                  ChunkSum* __restrict__ chunk_tot) {
+  __shared__ double sh[kBigThreads], sl[kBigThreads], sa[kBigThreads];
+  const int slices = kBigThreads / E;
+  const int s = threadIdx.x / E, d = threadIdx.x - s * E;
+  const std::uint64_t NB = *n_big, W = *n_items;
+  for (std::uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    std::uint32_t ki, c;
+    big_item(chunk_off, NB, w, &ki, &c);
+    if (s < slices) {
+      const std::uint32_t u = big_list[ki];
+      const std::uint32_t c0 = seg[u] + c * kBigChunk;
+      const std::uint32_t c1 = min(seg[u + 1], c0 + kBigChunk);
+      const std::uint32_t per = (c1 - c0 + slices - 1) / slices;
+      const std::uint32_t a0 = c0 + s * per, a1 = min(c1, a0 + per);
+      DD t{0.0, 0.0};
+      double asum = 0.0;
+#pragma unroll 8
+      for (std::uint32_t p = a0; p < a1; ++p) {
+        const double x = DX[std::uint64_t(exs[p]) * E + d];
+        t = dd_add(t, x);
+        asum = __dadd_ru(asum, fabs(x));
+      }
+      part[w * kBigThreads + threadIdx.x] = BigPart{t.hi, t.lo, asum, 0.0};
+      sh[threadIdx.x] = t.hi;
+      sl[threadIdx.x] = t.lo;
+      sa[threadIdx.x] = asum;
+    }
+    __syncthreads();
+    if (int(threadIdx.x) < E) {  // the chunk's total per dimension, slices in order
+      DD ct{0.0, 0.0};
+      double ca = 0.0;
+      for (int q = 0; q < slices; ++q) {
+        ct = dd_add(ct, DD{sh[q * E + threadIdx.x], sl[q * E + threadIdx.x]});
+        ca = __dadd_ru(ca, sa[q * E + threadIdx.x]);
+      }
+      chunk_tot[w * E + threadIdx.x] = ChunkSum{ct.hi, ct.lo, ca, 0.0};
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kBigThreads)
+    big_p2_kernel(int E, float lr, std::uint64_t n, const std::uint32_t* __restrict__ big_list,
+                  const unsigned long long* __restrict__ n_big,
+                  const std::uint32_t* __restrict__ chunk_off,
+                  const unsigned long long* __restrict__ n_items,
+                  const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
+                  const std::uint32_t* __restrict__ pos, const double* __restrict__ DX,
+                  BigPart* __restrict__ part, ChunkSum* __restrict__ chunk_tot,
+                  unsigned* __restrict__ key_done, float* __restrict__ out,
+                  unsigned long long* __restrict__ fallbacks) {
+  __shared__ double stage[kFallbackChunk];
+  __shared__ double sb[kBigThreads];
+  __shared__ bool bad[kBigThreads];
+  __shared__ unsigned s_last;
+  const int slices = kBigThreads / E;
+  const int s = threadIdx.x / E, d = threadIdx.x - s * E;
+  const bool worker = s < slices;
+  const std::uint64_t NB = *n_big, W = *n_items;
+  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  for (std::uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    std::uint32_t ki, c;
+    big_item(chunk_off, NB, w, &ki, &c);
+    const std::uint32_t u = big_list[ki];
+    const std::uint32_t k0 = seg[u], k1 = seg[u + 1];
+    const std::uint32_t nch = chunk_off[ki + 1] - chunk_off[ki];
+    const std::uint64_t w0 = chunk_off[ki];  // the key's first item
+    if (worker) {
+      DD off{0.0, 0.0};  // earlier chunks' totals, then this chunk's earlier slices
+      for (std::uint32_t cc = 0; cc < c; ++cc) {
+        const ChunkSum& ct = chunk_tot[(w0 + cc) * E + d];
+        off = dd_add(off, DD{ct.hi, ct.lo});
+      }
+      for (int q = 0; q < s; ++q) {
+        const BigPart& bp = part[w * kBigThreads + q * E + d];
+        off = dd_add(off, DD{bp.hi, bp.lo});
+      }
+      const double o = dd_value(off);
+      const std::uint32_t c0 = k0 + c * kBigChunk, c1 = min(k1, c0 + kBigChunk);
+      const std::uint32_t per = (c1 - c0 + slices - 1) / slices;
+      const std::uint32_t a0 = c0 + s * per, a1 = min(c1, a0 + per);
+      double l = 0.0, b = 0.0;
+#pragma unroll 8
+      for (std::uint32_t p = a0; p < a1; ++p) {
+        l = __dadd_rn(l, DX[std::uint64_t(exs[p]) * E + d]);
+        b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
+      }
+      sb[threadIdx.x] = b;
+    }
+    __syncthreads();
+    if (int(threadIdx.x) < E) {  // this chunk's B bound per dimension
+      double cb = 0.0;
+      for (int q = 0; q < slices; ++q) cb = __dadd_ru(cb, sb[q * E + threadIdx.x]);
+      chunk_tot[w * E + threadIdx.x].b = cb;
+    }
+    // the key's last CTA certifies
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&key_done[ki], 1u) == nch - 1;
+    __syncthreads();
+    if (!s_last) continue;
+    __threadfence();
+    float g = 0.0f;
+    if (int(threadIdx.x) < E) {
+      DD S{0.0, 0.0};
+      double A = 0.0, B = 0.0;
+      for (std::uint32_t cc = 0; cc < nch; ++cc) {
+        const double* bp = reinterpret_cast<const double*>(&chunk_tot[(w0 + cc) * E + threadIdx.x]);
+        S = dd_add(S, DD{__ldcg(bp), __ldcg(bp + 1)});
+        A = __dadd_ru(A, __ldcg(bp + 2));
+        B = __dadd_ru(B, __ldcg(bp + 3));
+      }
+      bad[threadIdx.x] = !certify_f32(dd_value(S), B, A, k1 - k0, (k1 - k0) + slices + nch,
+                                      inv_n, &g);
+    }
+    if (threadIdx.x == 0) key_done[ki] = 0;  // ready for the next launch
+    __syncthreads();
+    for (int dd = 0; dd < E; ++dd) {
+      if (!bad[dd]) continue;
+      double acc = 0.0;
+      for (std::uint32_t c0 = k0; c0 < k1; c0 += kFallbackChunk) {
+        const int cnt = int(k1 - c0 < kFallbackChunk ? k1 - c0 : kFallbackChunk);
+        for (int j = threadIdx.x; j < cnt; j += kBigThreads)
           stage[j] = DX[std::uint64_t(exs[c0 + j]) * E + dd];
         __syncthreads();
         if (int(threadIdx.x) == dd) acc = chain_sum(stage, cnt, acc);

@@ -80,16 +80,27 @@ __device__ __forceinline__ std::uint64_t status_word(std::uint32_t epoch, std::u
 }
 
 // Exclusive prefix of `tile` for one lane (digit) by decoupled look-back.
+// Eight predecessors' status words are loaded per step (independent loads),
+// then consumed newest-first until an inclusive prefix ends the walk; a
+// not-yet-published predecessor is re-polled from where the walk stopped.
 __device__ __forceinline__ std::uint64_t look_back(const LookBack& lb, std::uint64_t tile,
                                                    int stride, int lane_idx) {
+  constexpr int kAhead = 8;
   std::uint64_t excl = 0;
   std::int64_t j = std::int64_t(tile) - 1;
   while (j >= 0) {
-    const std::uint64_t w = ld_status(lb.status + std::uint64_t(j) * stride + lane_idx);
-    if (std::uint32_t(w >> 32) != lb.epoch || (w & (kFlagAgg | kFlagInc)) == 0) continue;
-    excl += w & kCountMask;
-    if (w & kFlagInc) break;
-    --j;
+    std::uint64_t w[kAhead];
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q)
+      w[q] = (j - q >= 0) ? ld_status(lb.status + std::uint64_t(j - q) * stride + lane_idx) : 0;
+    int q = 0;
+    for (; q < kAhead && j - q >= 0; ++q) {
+      const std::uint64_t x = w[q];
+      if (std::uint32_t(x >> 32) != lb.epoch || (x & (kFlagAgg | kFlagInc)) == 0) break;
+      excl += x & kCountMask;
+      if (x & kFlagInc) return excl;
+    }
+    j -= q;  // consumed q aggregates; re-poll the first unready one (if any)
   }
   return excl;
 }

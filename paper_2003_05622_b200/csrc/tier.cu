@@ -107,7 +107,9 @@ struct Scalars {
   double loss;
   unsigned long long pulled;   // sum over mini-batches of unique keys pulled
   unsigned long long carried;  // rows filled from the previous table
-  unsigned long long n_long;   // long CSR segments queued this mini-batch
+  unsigned long long n_long;   // medium CSR segments queued this mini-batch
+  unsigned long long n_big;    // big segments (split over CTAs)
+  unsigned long long n_items;  // their (key, chunk) work items
   int err_any;                 // error code max-reduced over ranks
   unsigned long long epoch;    // P2P exchange round (parity selects the windows)
   unsigned long long fallbacks;  // certified sums that needed the exact chain
@@ -181,7 +183,10 @@ struct Tier {
                 *seg = nullptr, *uidv = nullptr, *pos = nullptr,
                 *occ_row = nullptr, *slots = nullptr,
                 *puid = nullptr, *cnt32 = nullptr, *cnt_all = nullptr, *exs = nullptr,
-                *long_list = nullptr;
+                *long_list = nullptr, *big_list = nullptr, *chunk_off = nullptr,
+                *key_done = nullptr;
+  BigPart* big_part = nullptr;
+  ChunkSum* chunk_tot = nullptr;
   std::uint64_t *ukeys = nullptr, *pkeys = nullptr;
   float *rows = nullptr, *deltas = nullptr, *hstage = nullptr, *staged = nullptr;
   std::uint64_t staged_cap = 0;
@@ -856,10 +861,11 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   const double* DX = t->DX;
   unsigned long long* pulled = &t->dsc->pulled;
   unsigned long long* nl = &t->dsc->n_long;
-  HPS_CUDA(cudaMemsetAsync(nl, 0, 8, t->st));
+  unsigned long long* nb = &t->dsc->n_big;
+  HPS_CUDA(cudaMemsetAsync(nl, 0, 16, t->st));  // n_long, n_big
 #define HPS_SD(L, Q)                                                                    \
   launch(t, sparse_delta_kernel<L, Q>, grid, 256, 0, E, lr, n, U, seg, exs, pos, DX,    \
-         t->deltas, pulled, t->long_list, nl)
+         t->deltas, pulled, t->long_list, nl, t->big_list, nb)
   if (lpk == 4) HPS_SD(4, 1);
   else if (lpk == 8) HPS_SD(8, 1);
   else if (lpk == 16) HPS_SD(16, 1);
@@ -870,6 +876,16 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, 0, E, lr, n,
          (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos, DX,
          t->deltas, &t->dsc->fallbacks);
+  // big segments: plan (key, chunk) items, then the two passes over CTAs
+  launch(t, big_plan_kernel, 1, 256, 0, (const std::uint32_t*)t->big_list,
+         (const unsigned long long*)nb, seg, t->chunk_off, &t->dsc->n_items);
+  launch(t, big_p1_kernel, kSMs * 4, kBigThreads, 0, E, (const std::uint32_t*)t->big_list,
+         (const unsigned long long*)nb, (const std::uint32_t*)t->chunk_off,
+         (const unsigned long long*)&t->dsc->n_items, seg, exs, DX, t->big_part, t->chunk_tot);
+  launch(t, big_p2_kernel, kSMs * 4, kBigThreads, 0, E, lr, n, (const std::uint32_t*)t->big_list,
+         (const unsigned long long*)nb, (const std::uint32_t*)t->chunk_off,
+         (const unsigned long long*)&t->dsc->n_items, seg, exs, pos, DX, t->big_part,
+         t->chunk_tot, t->key_done, t->deltas, &t->dsc->fallbacks);
   return HPS_OK;
 }
 
@@ -1302,6 +1318,11 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(puid, S);
   A(exs, S);
   A(long_list, S);
+  A(big_list, S / kBigChunk + 2);
+  A(chunk_off, S / kBigChunk + 3);
+  A(key_done, S / kBigChunk + 2);
+  A(big_part, (2 * S / kBigChunk + 2) * std::uint64_t(kBigThreads));
+  A(chunk_tot, (2 * S / kBigChunk + 2) * E);
   A(cnt32, 256);
   A(cnt_all, 256 * 256);
   A(ukeys, S);
@@ -1319,6 +1340,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
 #undef A
   cudaMemsetAsync(t->ticket, 0, 8, t->st);
   cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
+  cudaMemsetAsync(t->key_done, 0, (S / kBigChunk + 2) * 4, t->st);
   cudaMemsetAsync(t->status, 0,
                   (std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1) * 8,
                   t->st);

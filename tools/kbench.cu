@@ -107,26 +107,60 @@ int main() {
     seg.push_back(std::uint32_t(exs.size()));
     list.push_back(k);
   }
-  std::uint32_t *dseg, *dexs, *dlist;
-  unsigned long long* dnl;
+  std::uint32_t *dseg, *dexs, *dlist, *dbig, *dchunk, *dkd;
+  unsigned long long *dnl, *dnb, *dni;
+  BigPart* dpart;
+  ChunkSum* dct;
+  std::vector<std::uint32_t> med, bigl;
+  for (int k = 0; k < nkeys; ++k) (seg[k + 1] - seg[k] > std::uint32_t(kBigChunk) ? bigl : med).push_back(k);
   CK(cudaMalloc(&dseg, seg.size() * 4));
   CK(cudaMalloc(&dexs, exs.size() * 4));
-  CK(cudaMalloc(&dlist, list.size() * 4));
+  CK(cudaMalloc(&dlist, nkeys * 4));
+  CK(cudaMalloc(&dbig, nkeys * 4));
+  CK(cudaMalloc(&dchunk, (nkeys + 1) * 4));
+  CK(cudaMalloc(&dkd, nkeys * 4));
+  CK(cudaMalloc(&dpart, 4096 * kBigThreads * sizeof(BigPart)));
+  CK(cudaMalloc(&dct, 4096 * 16 * sizeof(ChunkSum)));
   CK(cudaMalloc(&dnl, 8));
+  CK(cudaMalloc(&dnb, 8));
+  CK(cudaMalloc(&dni, 8));
   CK(cudaMalloc(&out, nkeys * 16 * 4));
-  unsigned long long nl = list.size();
+  CK(cudaMemset(dkd, 0, nkeys * 4));
+  unsigned long long nm = med.size(), nbg = bigl.size();
   CK(cudaMemcpy(dseg, seg.data(), seg.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dexs, exs.data(), exs.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(dlist, list.data(), list.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(dnl, &nl, 8, cudaMemcpyHostToDevice));
-  t = time_ms([&] {
+  CK(cudaMemcpy(dlist, med.data(), med.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dbig, bigl.data(), bigl.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dnl, &nm, 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dnb, &nbg, 8, cudaMemcpyHostToDevice));
+  auto run_long = [&] {
     sparse_delta_long_kernel<<<kSMs * 2, kLongThreads>>>(16, 0.05f, n, dlist, dnl, dseg, dexs,
                                                         nullptr, DX, out, fb);
-  });
+    big_plan_kernel<<<1, 256>>>(dbig, dnb, dseg, dchunk, dni);
+    big_p1_kernel<<<kSMs * 4, kBigThreads>>>(16, dbig, dnb, dchunk, dni, dseg, dexs, DX, dpart, dct);
+    big_p2_kernel<<<kSMs * 4, kBigThreads>>>(16, 0.05f, n, dbig, dnb, dchunk, dni, dseg, dexs,
+                                            nullptr, DX, dpart, dct, dkd, out, fb);
+  };
+  {
+    const float tm = time_ms([&] {
+      sparse_delta_long_kernel<<<kSMs * 2, kLongThreads>>>(16, 0.05f, n, dlist, dnl, dseg, dexs,
+                                                          nullptr, DX, out, fb);
+    });
+    const float tp = time_ms([&] { big_plan_kernel<<<1, 256>>>(dbig, dnb, dseg, dchunk, dni); });
+    const float t1 = time_ms([&] {
+      big_p1_kernel<<<kSMs * 4, kBigThreads>>>(16, dbig, dnb, dchunk, dni, dseg, dexs, DX, dpart, dct);
+    });
+    const float t2 = time_ms([&] {
+      big_p2_kernel<<<kSMs * 4, kBigThreads>>>(16, 0.05f, n, dbig, dnb, dchunk, dni, dseg, dexs,
+                                              nullptr, DX, dpart, dct, dkd, out, fb);
+    });
+    printf("  medium %.2f us, big plan %.2f us, big p1 %.2f us, big p2 %.2f us\n", tm * 1e3,
+           tp * 1e3, t1 * 1e3, t2 * 1e3);
+  }
+  t = time_ms(run_long);
   CK(cudaGetLastError());
-  printf("sparse_delta_long_kernel %d keys, %zu occurrences (max seg %u): %.2f us "
-         "(%.1f cycles/elem of the longest)\n",
-         nkeys, exs.size(), seg[1] - seg[0], t * 1e3, t * 1e-3 * 1.965e9 / (seg[1] - seg[0]));
+  printf("long-segment reduce (%zu medium + %zu big keys, %zu occurrences, max seg %u): %.2f us\n",
+         med.size(), bigl.size(), exs.size(), seg[1] - seg[0], t * 1e3);
   // forward/backward of the shard (embed-sum of 100 rows per example + MLP)
   {
     const std::uint32_t nnz = 100, nrows = 150000;
