@@ -20,6 +20,7 @@
 #include <cstdint>
 
 #include "common.cuh"
+#include "sort.cuh"
 
 namespace hpsgpu {
 
@@ -28,6 +29,7 @@ enum P2PPhase { kPhKeys = 0, kPhRows = 1, kPhDeltas = 2, kPhDense = 3, kPhases =
 
 struct PeerWindows {
   std::uint64_t* keys[kMaxRanks];    // peer's keys window base
+  std::uint32_t* uids[kMaxRanks];    // requester-side uid of each requested key
   std::uint64_t* hdr[kMaxRanks];     // peer's header base
   float* deltas[kMaxRanks];          // peer's delta window base
   float* dense[kMaxRanks];           // peer's dense window base
@@ -88,28 +90,106 @@ __global__ void p2p_wait_kernel(P2PCtx ctx, int G, int me, int phase, DevError* 
   }
 }
 
-// Requester -> owners: every unique key (owner-partitioned, positions p in
-// send order) goes to its owner's keys window, region `me`; one thread per
-// key. Thread 0 also writes the {count, send offset} headers.
+// Owner ranks of the sorted unique keys: orank[u] = number of earlier unique
+// keys with the same owner (key % G), i.e. the key's index in its owner's
+// request region; otot[o] = keys per owner. One decoupled look-back pass
+// (G <= 8 counters per tile). Thread 0 of tile 0 also opens the exchange
+// round (device round counter) and clears the segment queues of the sparse
+// reduce, saving two graph nodes.
+constexpr int kRankThreads = 256;
+constexpr int kRankItems = 8;
+constexpr int kRankTile = kRankThreads * kRankItems;
+
+__global__ void __launch_bounds__(kRankThreads)
+    owner_rank_kernel(const std::uint64_t* __restrict__ ukeys,
+                      const std::uint64_t* __restrict__ u_ptr, int G, LookBack lb,
+                      std::uint32_t* __restrict__ orank, std::uint64_t* __restrict__ otot,
+                      unsigned long long* epoch, unsigned long long* clear2) {
+  __shared__ std::uint32_t wcnt[kRankThreads / 32][kMaxRanks];
+  __shared__ std::uint32_t base[kMaxRanks];
+  __shared__ std::uint64_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(lb.ticket, 1ull) - lb.base;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane < kMaxRanks) wcnt[warp][lane] = 0;
+  __syncthreads();
+  const std::uint64_t tile = s_tile;
+  const std::uint64_t U = *u_ptr;
+  if (tile == 0 && threadIdx.x == 0) {
+    *epoch += 1;
+    clear2[0] = 0;
+    clear2[1] = 0;
+  }
+  const std::uint64_t b0 = tile * kRankTile;
+  if (b0 >= U && !(tile == 0)) return;
+  const unsigned lt = lanemask_lt();
+  const std::uint64_t wb = b0 + std::uint64_t(warp) * (kRankTile / (kRankThreads / 32));
+  std::uint32_t r[kRankItems], dg[kRankItems];
+#pragma unroll
+  for (int it = 0; it < kRankItems; ++it) {
+    const std::uint64_t idx = wb + std::uint64_t(it) * 32 + lane;
+    const bool valid = idx < U;
+    const std::uint32_t d = valid ? std::uint32_t(ukeys[idx] % std::uint64_t(G)) : kMaxRanks;
+    dg[it] = d;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+    const std::uint32_t prior = valid ? wcnt[warp][d] : 0u;
+    r[it] = prior + unsigned(__popc(peers & lt));
+    __syncwarp();
+    if (valid && lane == unsigned(__ffs(peers) - 1)) wcnt[warp][d] = prior + unsigned(__popc(peers));
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x < unsigned(G)) {
+    const int d = threadIdx.x;
+    std::uint32_t run = 0;
+    for (int w = 0; w < kRankThreads / 32; ++w) {
+      const std::uint32_t c = wcnt[w][d];
+      wcnt[w][d] = run;
+      run += c;
+    }
+    std::uint64_t* my = lb.status + tile * kMaxRanks + d;
+    std::uint64_t excl = 0;
+    const std::uint32_t ep = lb.epoch();
+    if (tile == 0) {
+      st_status(my, status_word(ep, kFlagInc, run));
+    } else {
+      st_status(my, status_word(ep, kFlagAgg, run));
+      excl = look_back(lb, ep, tile, kMaxRanks, d);
+      st_status(my, status_word(ep, kFlagInc, excl + run));
+    }
+    base[d] = std::uint32_t(excl);
+    if (b0 + kRankTile >= U) otot[d] = excl + run;  // the last tile knows the totals
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kRankItems; ++it) {
+    const std::uint64_t idx = wb + std::uint64_t(it) * 32 + lane;
+    if (idx < U) orank[idx] = base[dg[it]] + wcnt[warp][dg[it]] + r[it];
+  }
+}
+
+// Requester -> owners: every unique key u goes to its owner's keys window,
+// region `me`, at its owner rank, with u (the requester's row index).
+// Thread o < G of block 0 writes the per-owner request counts.
 __global__ void p2p_send_keys_kernel(P2PCtx ctx, int G, int me, std::uint64_t slot,
-                                     const std::uint64_t* __restrict__ pkeys,
+                                     const std::uint64_t* __restrict__ ukeys,
                                      const std::uint64_t* __restrict__ u_ptr,
-                                     const std::uint64_t* __restrict__ send_off,
+                                     const std::uint32_t* __restrict__ orank,
+                                     const std::uint64_t* __restrict__ otot,
                                      unsigned* done_ctr) {
   const std::uint64_t epoch = ctx.round();
   const PeerWindows& pw = ctx.cur(epoch);
   const std::uint64_t U = *u_ptr;
   if (blockIdx.x == 0 && threadIdx.x < unsigned(G)) {
     const int o = threadIdx.x;
-    std::uint64_t* h = pw.hdr[o] + me * 2;
-    h[0] = send_off[o + 1] - send_off[o];
-    h[1] = send_off[o];
+    pw.hdr[o][me * 2] = U ? otot[o] : 0;
   }
-  for (std::uint64_t p = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; p < U;
-       p += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint64_t k = pkeys[p];
+  for (std::uint64_t u = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; u < U;
+       u += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t k = ukeys[u];
     const int o = int(k % std::uint64_t(G));
-    pw.keys[o][me * slot + (p - send_off[o])] = k;
+    const std::uint64_t at = me * slot + orank[u];
+    pw.keys[o][at] = k;
+    pw.uids[o][at] = std::uint32_t(u);
   }
   signal_peers(pw, G, me, kPhKeys, epoch, done_ctr);
 }
@@ -128,6 +208,7 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
   const std::uint64_t epoch = ctx.round();
   const PeerWindows& pw = ctx.cur(epoch);
   const std::uint64_t* my_keys = pw.keys[me];
+  const std::uint32_t* my_uids = pw.uids[me];
   const std::uint64_t* my_hdr = pw.hdr[me];
   const int tpk = E / VEC;
   const std::uint64_t cap = *cap_ptr;
@@ -154,7 +235,7 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
     }
     if (part == 0) rslots[s * slot + i] = sl;
     const float* src = tvals + std::uint64_t(sl) * E + part * VEC;
-    float* dst = pw.rows[s] + (my_hdr[s * 2 + 1] + i) * E + part * VEC;
+    float* dst = pw.rows[s] + std::uint64_t(my_uids[s * slot + i]) * E + part * VEC;
     if (VEC == 4) {
       st_f4(dst, ld_f4(src));
     } else {
@@ -169,9 +250,9 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
 // window, region `me`, at the request's index.
 template <int VEC>
 __global__ void p2p_send_deltas_kernel(P2PCtx ctx, int G, int me, std::uint64_t slot,
-                                       const std::uint64_t* __restrict__ pkeys,
+                                       const std::uint64_t* __restrict__ ukeys,
                                        const std::uint64_t* __restrict__ u_ptr,
-                                       const std::uint64_t* __restrict__ send_off,
+                                       const std::uint32_t* __restrict__ orank,
                                        const float* __restrict__ deltas, int E,
                                        unsigned* done_ctr) {
   const std::uint64_t epoch = ctx.round();
@@ -180,11 +261,11 @@ __global__ void p2p_send_deltas_kernel(P2PCtx ctx, int G, int me, std::uint64_t 
   const std::uint64_t U = *u_ptr;
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < U * tpk;
        t += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint64_t p = t / tpk;
-    const int part = int(t - p * tpk);
-    const int o = int(pkeys[p] % std::uint64_t(G));
-    const float* src = deltas + p * E + part * VEC;
-    float* dst = pw.deltas[o] + (me * slot + (p - send_off[o])) * E + part * VEC;
+    const std::uint64_t u = t / tpk;
+    const int part = int(t - u * tpk);
+    const int o = int(ukeys[u] % std::uint64_t(G));
+    const float* src = deltas + u * E + part * VEC;
+    float* dst = pw.deltas[o] + (me * slot + orank[u]) * E + part * VEC;
     if (VEC == 4) {
       st_f4(dst, ld_f4(src));
     } else {
@@ -195,9 +276,9 @@ __global__ void p2p_send_deltas_kernel(P2PCtx ctx, int G, int me, std::uint64_t 
   signal_peers(pw, G, me, kPhDeltas, epoch, done_ctr);
 }
 
-// Owner apply of every source's deltas in canonical sender order (one pass
-// per source inside the kernel would race across keys shared between
-// sources, so the host launches one grid per source, in order).
+// Owner apply of one source's deltas; sources are applied in canonical
+// sender order (keys shared between sources would race inside one grid, so
+// the host enqueues one small grid per source, in order).
 template <int VEC>
 __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
                                  const std::uint32_t* __restrict__ rslots,
@@ -224,6 +305,47 @@ __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
     } else {
 #pragma unroll
       for (int q = 0; q < VEC; ++q) v[q] = __fadd_rn(v[q], d[q]);
+    }
+  }
+}
+
+// Wait for every source's dense replica, then the canonical f64 sum, /G
+// and the SGD update (hbm_ps.hpp:258-277, 249-256, model.hpp:205-212) in the
+// same launch. One CTA.
+__global__ void p2p_dense_update_kernel(P2PCtx ctx, int G, int me, int nodes, int devices,
+                                        std::uint64_t nw, float* __restrict__ w, float lr,
+                                        int apply, float* __restrict__ sum_out, DevError* err) {
+  __shared__ int ok;
+  const std::uint64_t epoch = ctx.round();
+  if (threadIdx.x == 0) ok = 1;
+  __syncthreads();
+  if (threadIdx.x < unsigned(G)) {
+    const std::uint64_t* f = ctx.par[0].flags[me] + threadIdx.x * kPhases + kPhDense;
+    long long spins = 0;
+    while (ld_acquire_sys(f) < epoch) {
+      if (++spins > (1ll << 27)) {
+        raise_error(err, 10, std::uint64_t(threadIdx.x));
+        ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  if (!ok) return;
+  const float* bufs = ctx.cur(epoch).dense[me];
+  for (std::uint64_t i = threadIdx.x; i < nw; i += blockDim.x) {
+    double acc = 0.0;
+    for (int nn = 0; nn < nodes; ++nn)
+      for (int d = 0; d < devices; ++d)
+        acc = __dadd_rn(acc, double(bufs[std::uint64_t(d * nodes + nn) * nw + i]));
+    const float s = __double2float_rn(acc);
+    if (sum_out) sum_out[i] = s;
+    if (apply) {
+      const float g = __fdiv_rn(s, float(nodes * devices));
+      const float nwv = __fsub_rn(w[i], __fmul_rn(lr, g));
+      if (!isfinite(nwv)) raise_error(err, 5, i);
+      w[i] = nwv;
     }
   }
 }

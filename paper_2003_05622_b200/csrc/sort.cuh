@@ -14,8 +14,12 @@
 //     per digit by decoupled look-back over the preceding tiles, and
 //     scatters. Tickets are handed out in launch order, so a tile only ever
 //     waits on tiles that are already running.
-// Status words are 64-bit [epoch:32 | flag:2 | count:30]; every launch uses a
-// fresh epoch, so the status arrays never need clearing.
+// Status words are 64-bit [epoch:32 | flag:2 | count:30]. A launch's epoch is
+// (device context counter << 12) | launch index within the context, and the
+// tile ticket counter is reset at the start of every context (a batch body or
+// one API call): nothing baked into a launch depends on earlier launches, so
+// a captured CUDA graph replays correctly, and the status arrays never need
+// clearing (the host clears them once per 2^20 contexts, before a wrap).
 #pragma once
 
 #include <cstdint>
@@ -47,10 +51,12 @@ struct Count {
 // Look-back context of one launch: ticket counter, the host-tracked number of
 // tickets handed out before this launch, the launch's epoch, status words.
 struct LookBack {
-  unsigned long long* ticket;
-  std::uint64_t base;
-  std::uint32_t epoch;
+  unsigned long long* ticket;   // reset at the start of every context
+  std::uint64_t base;           // tickets handed out earlier in this context
+  std::uint32_t local;          // launch index within the context (< 4096)
   std::uint64_t* status;
+  const std::uint32_t* context; // device context counter
+  __device__ __forceinline__ std::uint32_t epoch() const { return (*context << 12) | local; }
 };
 
 struct ShiftDigit {
@@ -83,8 +89,8 @@ __device__ __forceinline__ std::uint64_t status_word(std::uint32_t epoch, std::u
 // Eight predecessors' status words are loaded per step (independent loads),
 // then consumed newest-first until an inclusive prefix ends the walk; a
 // not-yet-published predecessor is re-polled from where the walk stopped.
-__device__ __forceinline__ std::uint64_t look_back(const LookBack& lb, std::uint64_t tile,
-                                                   int stride, int lane_idx) {
+__device__ __forceinline__ std::uint64_t look_back(const LookBack& lb, std::uint32_t epoch,
+                                                   std::uint64_t tile, int stride, int lane_idx) {
   constexpr int kAhead = 8;
   std::uint64_t excl = 0;
   std::int64_t j = std::int64_t(tile) - 1;
@@ -96,7 +102,7 @@ __device__ __forceinline__ std::uint64_t look_back(const LookBack& lb, std::uint
     int q = 0;
     for (; q < kAhead && j - q >= 0; ++q) {
       const std::uint64_t x = w[q];
-      if (std::uint32_t(x >> 32) != lb.epoch || (x & (kFlagAgg | kFlagInc)) == 0) break;
+      if (std::uint32_t(x >> 32) != epoch || (x & (kFlagAgg | kFlagInc)) == 0) break;
       excl += x & kCountMask;
       if (x & kFlagInc) return excl;
     }
@@ -206,13 +212,14 @@ __global__ void __launch_bounds__(kSortThreads)
       run += c;
     }
     std::uint64_t* my = lb.status + tile * kDigits + d;
+    const std::uint32_t ep = lb.epoch();
     if (tile == 0) {
-      st_status(my, status_word(lb.epoch, kFlagInc, run));
+      st_status(my, status_word(ep, kFlagInc, run));
       gbase[d] = digit_base[d];
     } else {
-      st_status(my, status_word(lb.epoch, kFlagAgg, run));
-      const std::uint64_t excl = look_back(lb, tile, kDigits, d);
-      st_status(my, status_word(lb.epoch, kFlagInc, excl + run));
+      st_status(my, status_word(ep, kFlagAgg, run));
+      const std::uint64_t excl = look_back(lb, ep, tile, kDigits, d);
+      st_status(my, status_word(ep, kFlagInc, excl + run));
       gbase[d] = digit_base[d] + std::uint32_t(excl);
     }
   }
@@ -278,12 +285,13 @@ __global__ void __launch_bounds__(kSortThreads)
     for (int w = 0; w < kSortWarps; ++w) agg += ws[w];
     std::uint64_t* my = lb.status + tile;
     std::uint64_t pre = 0;
+    const std::uint32_t ep = lb.epoch();
     if (tile == 0) {
-      st_status(my, status_word(lb.epoch, kFlagInc, agg));
+      st_status(my, status_word(ep, kFlagInc, agg));
     } else {
-      st_status(my, status_word(lb.epoch, kFlagAgg, agg));
-      pre = look_back(lb, tile, 1, 0);
-      st_status(my, status_word(lb.epoch, kFlagInc, pre + agg));
+      st_status(my, status_word(ep, kFlagAgg, agg));
+      pre = look_back(lb, ep, tile, 1, 0);
+      st_status(my, status_word(ep, kFlagInc, pre + agg));
     }
     s_pre = pre;
     if (total && base + kScanTile >= n) *total = pre + agg;

@@ -103,7 +103,6 @@ struct Scalars {
   std::uint64_t U;             // unique keys of the current mini-batch / pull
   std::uint64_t total;         // scratch total of a tile scan
   std::uint64_t counts[66];    // batch_count: per-mb occurrences, owned keys
-  std::uint64_t send_off[257]; // owner partition offsets (G+1)
   double loss;
   unsigned long long pulled;   // sum over mini-batches of unique keys pulled
   unsigned long long carried;  // rows filled from the previous table
@@ -112,6 +111,8 @@ struct Scalars {
   unsigned long long n_items;  // their (key, chunk) work items
   int err_any;                 // error code max-reduced over ranks
   unsigned long long epoch;    // P2P exchange round (parity selects the windows)
+  std::uint32_t lb_context;    // look-back context counter (sort.cuh)
+  std::uint32_t pad0;
   unsigned long long fallbacks;  // certified sums that needed the exact chain
   unsigned long long served;     // keys this rank served as owner (G > 1)
   DevError err;
@@ -170,8 +171,10 @@ struct Tier {
   std::uint32_t* ghist = nullptr;          // [kMaxPasses][256] digit bases
   std::uint64_t* status = nullptr;         // look-back status words
   unsigned long long* ticket = nullptr;    // look-back tile tickets
-  std::uint64_t tickets = 0;               // tickets handed out so far (host view)
-  std::uint32_t epoch = 0;                 // per-launch status epoch
+  std::uint64_t tickets = 0;               // tickets handed out in this context
+  std::uint32_t lb_local = 0;              // launches in this context
+  std::uint64_t lb_contexts = 0;           // contexts opened (host mirror)
+  std::uint64_t status_words = 0;
 
   // batch staging
   std::int64_t* b_off = nullptr;
@@ -181,13 +184,15 @@ struct Tier {
   // mini-batch / pull buffers (sized Omax)
   std::uint32_t *occ_off = nullptr, *ex_of = nullptr, *inv = nullptr,
                 *seg = nullptr, *uidv = nullptr, *pos = nullptr,
-                *occ_row = nullptr, *slots = nullptr,
-                *puid = nullptr, *cnt32 = nullptr, *cnt_all = nullptr, *exs = nullptr,
+                *slots = nullptr,
+                *exs = nullptr,
                 *long_list = nullptr, *big_list = nullptr, *chunk_off = nullptr,
+                *orank = nullptr,
                 *key_done = nullptr;
   BigPart* big_part = nullptr;
   ChunkSum* chunk_tot = nullptr;
-  std::uint64_t *ukeys = nullptr, *pkeys = nullptr;
+  std::uint64_t* otot = nullptr;
+  std::uint64_t* ukeys = nullptr;
   float *rows = nullptr, *deltas = nullptr, *hstage = nullptr, *staged = nullptr;
   std::uint64_t staged_cap = 0;
 
@@ -406,38 +411,6 @@ __global__ void shard_gather_kernel(ShardMap sm, const std::int64_t* __restrict_
   }
 }
 
-__global__ void pos_kernel(const std::uint32_t* __restrict__ puid,
-                           const std::uint64_t* __restrict__ u_ptr,
-                           std::uint32_t* __restrict__ pos) {
-  const std::uint64_t U = *u_ptr;
-  for (std::uint64_t p = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
-       p < U; p += std::uint64_t(gridDim.x) * blockDim.x)
-    pos[puid[p]] = std::uint32_t(p);
-}
-
-__global__ void occ_row_kernel(const std::uint32_t* __restrict__ inv,
-                               const std::uint32_t* __restrict__ pos,
-                               Count cn, std::uint32_t* __restrict__ out) {
-  const std::uint64_t n = cn.get();
-  for (std::uint64_t o = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
-       o < n; o += std::uint64_t(gridDim.x) * blockDim.x)
-    out[o] = pos[inv[o]];
-}
-
-// Owner partition offsets from the exclusive-scanned owner histogram of
-// the ModDigit pass: send_off[o] = first position of owner o, send_off[G] =
-// U; per-owner counts as u32 for the count all-gather.
-__global__ void owner_offsets_kernel(const std::uint32_t* __restrict__ base, int G,
-                                     const std::uint64_t* __restrict__ u_ptr,
-                                     std::uint64_t* __restrict__ send_off,
-                                     std::uint32_t* __restrict__ cnt32) {
-  const int o = threadIdx.x;
-  const std::uint64_t U = *u_ptr;
-  if (o <= G) send_off[o] = o < G ? base[o] : U;
-  __syncthreads();
-  if (o < G) cnt32[o] = std::uint32_t(send_off[o + 1] - send_off[o]);
-}
-
 // out[i] = rows[row_of(i)] for the parity pull (restores input order).
 __global__ void scatter_rows_kernel(const std::uint32_t* __restrict__ inv,
                                     const std::uint32_t* __restrict__ pos,
@@ -548,9 +521,25 @@ struct UniqueEmit {  // inverse index + CSR segments of a sorted (key, occ) list
 
 // --------------------------------------------------- sort / scan drivers
 
+__global__ void context_open_kernel(std::uint32_t* context, unsigned long long* ticket) {
+  *context += 1;
+  *ticket = 0;
+}
+
+// Opens a look-back context (the start of a batch body or of an API call):
+// resets the device ticket counter and advances the device context counter,
+// so the launches that follow bake only context-relative values.
+static void open_lookback_context(Tier* t) {
+  if ((t->lb_contexts + 1) % (1u << 20) == 0)  // before the 20-bit wrap
+    cudaMemsetAsync(t->status, 0, t->status_words * 8, t->st);
+  ++t->lb_contexts;
+  launch(t, context_open_kernel, 1, 1, 0, &t->dsc->lb_context, t->ticket);
+  t->tickets = 0;
+  t->lb_local = 0;
+}
+
 static LookBack next_lookback(Tier* t, std::uint32_t grid) {
-  LookBack lb{t->ticket, t->tickets, ++t->epoch, t->status};
-  if (lb.epoch == 0) lb.epoch = ++t->epoch;  // 0 marks "never written"
+  LookBack lb{t->ticket, t->tickets, ++t->lb_local, t->status, &t->dsc->lb_context};
   t->tickets += grid;
   return lb;
 }
@@ -605,30 +594,17 @@ static void radix_sort(Tier* t, const std::uint64_t* kin, const std::uint32_t* v
   *vout = const_cast<std::uint32_t*>(vsrc);
 }
 
-// Stable partition of (keys, vals) by owner key % G (one counting pass);
-// fills dsc->send_off[0..G] and cnt32[0..G).
-static void owner_partition(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
-                            const std::uint64_t* n_dev, std::uint64_t n_upper,
-                            std::uint64_t* kout, std::uint32_t* vout) {
-  const std::uint32_t nb = std::max<std::uint32_t>(1, sort_tiles(n_upper));
-  const Count n{n_dev, 0};
-  sort_histogram(t, kin, n, n_upper, 0, std::uint32_t(t->G));
-  launch(t, onesweep_pass_kernel<ModDigit, true>, nb, kSortThreads, 0, kin, vin, n,
-         ModDigit{std::uint32_t(t->G)}, (const std::uint32_t*)t->ghist, next_lookback(t, nb), kout,
-         vout);
-  launch(t, owner_offsets_kernel, 1, 288, 0, (const std::uint32_t*)t->ghist, t->G,
-         (const std::uint64_t*)&t->dsc->U, t->dsc->send_off, t->cnt32);
-}
-
 static int vec_of(int E) { return (E % 4 == 0) ? 4 : 1; }
 
 // ------------------------------------------------------------ exchange --
 
 // One exchange round (a mini-batch, or one collective API call): every
 // phase of the round is tagged with the same epoch on all ranks.
-static void begin_round(Tier* t) {
+// device_counter = false: the round's first kernel (owner_rank_kernel)
+// increments the device counter itself.
+static void begin_round(Tier* t, bool device_counter = true) {
   ++t->p2p_epoch;  // host mirror (same sequence on every rank)
-  launch(t, epoch_inc_kernel, 1, 1, 0, &t->dsc->epoch);
+  if (device_counter) launch(t, epoch_inc_kernel, 1, 1, 0, &t->dsc->epoch);
 }
 
 static void p2p_wait(Tier* t, int phase) {
@@ -766,26 +742,31 @@ static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint3
     }
     return HPS_OK;
   }
-  // G > 1: owner partition of the unique keys (stable, keeps key order),
-  // then the keys go straight into the owners' windows over NVLink
-  owner_partition(t, t->ukeys, t->uidv, &t->dsc->U, n, t->pkeys, t->puid);
-  launch(t, pos_kernel, grid_for(n), 256, 0, (const std::uint32_t*)t->puid,
-         (const std::uint64_t*)&t->dsc->U, t->pos);
-  plan->pos = t->pos;
-  launch(t, p2p_send_keys_kernel, grid_for(n), 256, 0, t->ctx, t->G, t->g, t->slot,
-         (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-         (const std::uint64_t*)t->dsc->send_off, t->done_ctr);
+  // G > 1: each unique key's rank among the keys of its owner (one look-back
+  // pass that also opens the exchange round), then (key, uid) pairs go
+  // straight into the owners' windows over NVLink; rows come back in uid order
+  plan->pos = nullptr;
+  {
+    const std::uint32_t nb = std::max<std::uint32_t>(
+        1, std::uint32_t((n + kRankTile - 1) / kRankTile));
+    launch(t, owner_rank_kernel, nb, kRankThreads, 0, (const std::uint64_t*)t->ukeys,
+           (const std::uint64_t*)&t->dsc->U, t->G, next_lookback(t, nb), t->orank, t->otot,
+           &t->dsc->epoch, &t->dsc->n_long);
+  }
+  launch(t, p2p_send_keys_kernel, grid_for(n, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
+         (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
+         (const std::uint32_t*)t->orank, (const std::uint64_t*)t->otot, t->done_ctr);
   p2p_wait(t, kPhKeys);
   mark(t, HPS_T_DEDUP);
   if (do_gather) {
     const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
     if (V == 4)
-      launch(t, p2p_serve_rows_kernel<4>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
+      launch(t, p2p_serve_rows_kernel<4>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
              (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
              (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->done_ctr,
              &t->dsc->served, &t->dsc->err);
     else
-      launch(t, p2p_serve_rows_kernel<1>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
+      launch(t, p2p_serve_rows_kernel<1>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
              (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
              (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->done_ctr,
              &t->dsc->served, &t->dsc->err);
@@ -802,21 +783,21 @@ static hps_status push_apply(Tier* t) {
   const int V = vec_of(t->E);
   const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
   if (V == 4)
-    launch(t, p2p_send_deltas_kernel<4>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
-           (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-           (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->done_ctr);
+    launch(t, p2p_send_deltas_kernel<4>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G,
+           t->g, t->slot, (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
+           (const std::uint32_t*)t->orank, (const float*)t->deltas, t->E, t->done_ctr);
   else
-    launch(t, p2p_send_deltas_kernel<1>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
-           (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-           (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->done_ctr);
+    launch(t, p2p_send_deltas_kernel<1>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G,
+           t->g, t->slot, (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
+           (const std::uint32_t*)t->orank, (const float*)t->deltas, t->E, t->done_ctr);
   p2p_wait(t, kPhDeltas);
   for (int src : canonical_senders(t)) {
     if (V == 4)
-      launch(t, p2p_apply_kernel<4>, grid_for(t->slot * std::uint64_t(t->E / V)), 256, 0,
+      launch(t, p2p_apply_kernel<4>, grid_for(t->slot * std::uint64_t(t->E / V), 256, kSMs * 2), 256, 0,
              t->ctx, t->g, src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur],
              t->E);
     else
-      launch(t, p2p_apply_kernel<1>, grid_for(t->slot * std::uint64_t(t->E / V)), 256, 0,
+      launch(t, p2p_apply_kernel<1>, grid_for(t->slot * std::uint64_t(t->E / V), 256, kSMs * 2), 256, 0,
              t->ctx, t->g, src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur],
              t->E);
   }
@@ -837,10 +818,8 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
   // fast modes alike: the canonical order costs nothing extra here)
   launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->ctx, t->G, t->g, nw,
          (const float*)t->dgrad, t->done_ctr);
-  p2p_wait(t, kPhDense);
-  launch(t, dense_update_kernel, grid_for(nw), 256, 0, t->dense, (const float*)t->w_dense_p[0],
-         nw, t->N, t->D, t->cfg.learning_rate, int(apply), (float*)nullptr, &t->dsc->err,
-         (const float*)t->w_dense_p[1], (const unsigned long long*)&t->dsc->epoch);
+  launch(t, p2p_dense_update_kernel, 1, 256, 0, t->ctx, t->G, t->g, t->N, t->D, nw, t->dense,
+         t->cfg.learning_rate, int(apply), (float*)nullptr, &t->dsc->err);
   return HPS_OK;
 }
 
@@ -862,7 +841,7 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   unsigned long long* pulled = &t->dsc->pulled;
   unsigned long long* nl = &t->dsc->n_long;
   unsigned long long* nb = &t->dsc->n_big;
-  HPS_CUDA(cudaMemsetAsync(nl, 0, 16, t->st));  // n_long, n_big
+  if (t->G == 1) HPS_CUDA(cudaMemsetAsync(nl, 0, 16, t->st));  // G > 1: owner_rank_kernel
 #define HPS_SD(L, Q)                                                                    \
   launch(t, sparse_delta_kernel<L, Q>, grid, 256, 0, E, lr, n, U, seg, exs, pos, DX,    \
          t->deltas, pulled, t->long_list, nl, t->big_list, nb)
@@ -902,7 +881,8 @@ static hps_status setup_p2p(Tier* t, std::uint64_t S) {
   const std::uint64_t o_rows = o_flags + al(G * kPhases * 8);
   const std::uint64_t o_par = o_rows + al(S * E * 4);  // two parity copies follow
   const std::uint64_t p_keys = 0;
-  const std::uint64_t p_hdr = p_keys + al(G * t->slot * 8);
+  const std::uint64_t p_uids = p_keys + al(G * t->slot * 8);
+  const std::uint64_t p_hdr = p_uids + al(G * t->slot * 4);
   const std::uint64_t p_deltas = p_hdr + al(G * 2 * 8);
   const std::uint64_t p_dense = p_deltas + al(G * t->slot * E * 4);
   const std::uint64_t par_bytes = p_dense + al(G * nw * 4);
@@ -967,6 +947,7 @@ static hps_status setup_p2p(Tier* t, std::uint64_t S) {
       char* pb = base + o_par + par * par_bytes;
       PeerWindows& w = t->ctx.par[par];
       w.keys[p] = reinterpret_cast<std::uint64_t*>(pb + p_keys);
+      w.uids[p] = reinterpret_cast<std::uint32_t*>(pb + p_uids);
       w.hdr[p] = reinterpret_cast<std::uint64_t*>(pb + p_hdr);
       w.deltas[p] = reinterpret_cast<float*>(pb + p_deltas);
       w.dense[p] = reinterpret_cast<float*>(pb + p_dense);
@@ -998,6 +979,8 @@ static hps_status enqueue_batch_body(Tier* T, const BatchShape& sh, int skip_mb)
   const std::uint64_t* dkeys = T->b_keys;
   const std::uint8_t* dlab = T->b_lab;
   const Count own_n{&T->dsc->counts[J], 0};
+  // (the caller opened the look-back context: ticket counter reset, device
+  // context counter advanced — eagerly, so captured graphs replay correctly)
   // ---- working set (a1, a2) + build (a3, a4)
   {
     const std::uint64_t* kin = dkeys;
@@ -1032,15 +1015,10 @@ static hps_status enqueue_batch_body(Tier* T, const BatchShape& sh, int skip_mb)
              (const std::uint32_t*)T->occ_off, T->kB, T->vB, T->ex_of);
     }
     PullPlan plan;
-    if (G > 1) begin_round(T);
+    if (G > 1) begin_round(T, false);
     HPS_TRY(dedup_pull(T, T->kB, T->vB, on_n, ob, &plan, true, true));
-    // compute (a7, a8, a9)
+    // compute (a7, a8, a9); rows are in uid order at every G
     const std::uint32_t* occ_row = T->inv;
-    if (G > 1) {
-      launch(T, occ_row_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)T->inv, plan.pos,
-             on_n, T->occ_row);
-      occ_row = T->occ_row;
-    }
     if (n) {
       const int LPE = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
       const int epb = 128 / LPE;
@@ -1302,7 +1280,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(vA, S);
   A(vB, S);
   A(ghist, std::uint64_t(kMaxPasses) * kDigits);
-  A(status, std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1);
+  t->status_words = std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1;
+  A(status, t->status_words);
   A(ticket, 1);
   A(b_off, t->Bmax + 1);
   A(b_keys, O);
@@ -1313,20 +1292,17 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(seg, S + 1);
   A(uidv, S);
   A(pos, S);
-  A(occ_row, S);
   A(slots, S);
-  A(puid, S);
   A(exs, S);
+  A(orank, S);
+  A(otot, kMaxRanks);
   A(long_list, S);
   A(big_list, S / kBigChunk + 2);
   A(chunk_off, S / kBigChunk + 3);
   A(key_done, S / kBigChunk + 2);
   A(big_part, (2 * S / kBigChunk + 2) * std::uint64_t(kBigThreads));
   A(chunk_tot, (2 * S / kBigChunk + 2) * E);
-  A(cnt32, 256);
-  A(cnt_all, 256 * 256);
   A(ukeys, S);
-  A(pkeys, S);
   if (G == 1) A(rows, S * E);  // G > 1: inside the exported window (peers write it)
   A(deltas, S * E);
   A(hstage, S * E);
@@ -1419,6 +1395,7 @@ hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float
   }
   std::uint64_t* sk = nullptr;
   std::uint32_t* so = nullptr;
+  open_lookback_context(t);
   if (n) {
     radix_sort(t, t->kB, t->vB, Count{nullptr, n}, n, 64, true, &sk, &so);
     tile_scan(t, RunStartOwned{sk, std::uint64_t(t->G), std::uint64_t(t->g)},
@@ -1446,7 +1423,8 @@ hps_status hps_pull(hps_tier_t t, const uint64_t* keys, uint64_t n, float* out_r
     launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
   }
   PullPlan plan;
-  begin_round(t);
+  open_lookback_context(t);
+  if (t->G > 1) begin_round(t, false);
   HPS_TRY(dedup_pull(t, t->kB, t->vB, Count{nullptr, n}, n, &plan, true));
   HPS_TRY(check_device_error(t, "device table: missing key ", true));
   if (n) {
@@ -1472,7 +1450,8 @@ hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uin
     launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
   }
   PullPlan plan;
-  begin_round(t);
+  open_lookback_context(t);
+  if (t->G > 1) begin_round(t, false);
   HPS_TRY(dedup_pull(t, t->kB, t->vB, Count{nullptr, n}, n, &plan, false));
   HPS_CUDA(cudaMemcpyAsync(&t->hsc->U, &t->dsc->U, 8, cudaMemcpyDeviceToHost, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
@@ -1493,13 +1472,13 @@ hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uin
     const int V = vec_of(t->E);
     const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
     if (V == 4)
-      launch(t, p2p_send_deltas_kernel<4>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
-             (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-             (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->done_ctr);
+      launch(t, p2p_send_deltas_kernel<4>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G,
+             t->g, t->slot, (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
+             (const std::uint32_t*)t->orank, (const float*)t->deltas, t->E, t->done_ctr);
     else
-      launch(t, p2p_send_deltas_kernel<1>, grid_for(work), 256, 0, t->ctx, t->G, t->g, t->slot,
-             (const std::uint64_t*)t->pkeys, (const std::uint64_t*)&t->dsc->U,
-             (const std::uint64_t*)t->dsc->send_off, (const float*)t->deltas, t->E, t->done_ctr);
+      launch(t, p2p_send_deltas_kernel<1>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G,
+             t->g, t->slot, (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
+             (const std::uint32_t*)t->orank, (const float*)t->deltas, t->E, t->done_ctr);
     p2p_wait(t, kPhDeltas);
     const int par = int(t->p2p_epoch & 1);
     std::vector<std::uint64_t> hdr(2 * t->G);
@@ -1623,10 +1602,8 @@ hps_status hps_dense_sync(hps_tier_t t, float* buf, uint64_t len, int determinis
     begin_round(t);
     launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->ctx, t->G, t->g, nw,
            (const float*)t->dgrad, t->done_ctr);
-    p2p_wait(t, kPhDense);
-    launch(t, dense_update_kernel, grid_for(nw), 256, 0, (float*)nullptr,
-           (const float*)t->w_dense_p[0], nw, t->N, t->D, 1.0f, 0, sum, &t->dsc->err,
-           (const float*)t->w_dense_p[1], (const unsigned long long*)&t->dsc->epoch);
+    launch(t, p2p_dense_update_kernel, 1, 256, 0, t->ctx, t->G, t->g, t->N, t->D, nw,
+           (float*)nullptr, 1.0f, 0, sum, &t->dsc->err);
     HPS_CUDA(cudaMemcpyAsync(buf + c0, sum, L * 4, cudaMemcpyDeviceToHost, t->st));
   }
   return check_device_error(t, "device table: missing key ", true);
@@ -1776,6 +1753,7 @@ hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
   const std::int64_t first_mb = T->step * J;
   const bool skip_in_batch = T->cfg.inject_skip_sync >= first_mb &&
                              T->cfg.inject_skip_sync < first_mb + J;
+  open_lookback_context(T);  // eager, before capture or replay
   if (T->use_graphs && !skip_in_batch) {
     HPS_TRY(run_body_graph(T, sh));
   } else {

@@ -158,6 +158,9 @@ def main():
     results["train_e4_j2"] = case_train(world, rank, oracle, 4, (4, 1), 2, True, 3000, 64, 4, 9)
     results["train_fast"] = case_train(world, rank, oracle, 8, (8, 16, 1), 4, True, 20000, 512,
                                        3, 20, det=False)
+    # many same-shape batches: captured-graph replays across both table parities
+    results["train_replays"] = case_train(world, rank, oracle, 16, (8, 16, 1), 4, True, 50000,
+                                          1024, 9, 30)
     flags = torch.tensor([int(v) for v in results.values()], device="cuda")
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:

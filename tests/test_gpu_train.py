@@ -125,3 +125,27 @@ def test_loss_decreases_on_learnable_data(pkg):
     off, keys, lab = pkg.gen_dataset(dims, 12 * B, 20, seed=3, clusters=50)
     _, _, losses = run_gpu(pkg, off, keys, lab, B, E=8, layers=(8, 16, 1), J=4, dims=dims)
     assert losses[-1] < losses[0]
+
+
+def test_graph_replays_bit_exact(pkg, oracle):
+    """Same-shape batches make hps_train_batch replay its captured CUDA graph
+    (both table parities); every replay must still be bit-exact, and equal to
+    the kernel-by-kernel (non-graph) execution."""
+    dims, B, nnz, nb = 20000, 512, 20, 9
+    off, keys, lab = pkg.gen_dataset(dims, B * nb, nnz, zipf=True, seed=21)
+    outs = []
+    for graphs in (True, False):
+        tier = pkg.Tier(width=8, layer_dims=(8, 16, 1), minibatches=4, key_space=dims,
+                        max_batch_examples=B, max_batch_keys=B * nnz)
+        tier.set_graphs(graphs)
+        store = np.zeros((dims, 8), dtype=np.float32)
+        tier.attach_store(store)
+        for b in range(nb):
+            tier.train_batch(off[b * B:(b + 1) * B + 1] - off[b * B],
+                             keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B])
+        outs.append((tier.get_dense(), store))
+        tier.close()
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, 8, (8, 16, 1), J=4), B, off, keys, lab)
+    for dense, store in outs:
+        assert np.array_equal(dense, wd)
+        assert np.array_equal(store[wk.astype(np.int64)], wr)
