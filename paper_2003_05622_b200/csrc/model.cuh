@@ -448,10 +448,11 @@ __device__ __forceinline__ void write_delta(float* out, std::uint64_t row, int E
   out[row * E + d] = -__fmul_rn(lr, g);
 }
 
-template <int LPK, int kDPL>
+// Short segments, exact: one thread per (unique key, dim) sums the key's
+// occurrences in example order (4 independent loads per step, the adds in
+// order). Longer segments are queued for the chunked CTA path.
 __global__ void __launch_bounds__(256)
-    sparse_delta_kernel(int E, float lr, std::uint64_t n,
-                        const std::uint64_t* __restrict__ u_ptr,
+    sparse_short_kernel(int E, float lr, std::uint64_t n, const std::uint64_t* __restrict__ u_ptr,
                         const std::uint32_t* __restrict__ seg,
                         const std::uint32_t* __restrict__ exs,
                         const std::uint32_t* __restrict__ pos,
@@ -460,58 +461,35 @@ __global__ void __launch_bounds__(256)
                         std::uint32_t* __restrict__ long_list,
                         unsigned long long* __restrict__ n_long,
                         std::uint32_t* __restrict__ big_list,
-                        unsigned long long* __restrict__ n_big) {
+                        unsigned long long* __restrict__ n_big, std::uint32_t medium_max) {
   const std::uint64_t U = *u_ptr;
   if (pulled && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(pulled, (unsigned long long)U);
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-  const int sub = threadIdx.x % LPK;
-  const unsigned lane = threadIdx.x & 31;
-  const unsigned gmask =
-      LPK == 32 ? 0xFFFFFFFFu : (((1u << LPK) - 1u) << (lane / LPK * LPK));
-  constexpr int SD = LPK < kStageDepth ? LPK : kStageDepth;  // ids come from SD lanes
-  const std::uint64_t groups = (std::uint64_t(gridDim.x) * blockDim.x) / LPK;
-  for (std::uint64_t u = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) / LPK; u < U;
-       u += groups) {
+  const std::uint64_t total = U * std::uint64_t(E);
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t u = t / std::uint64_t(E);
+    const int d = int(t - u * E);
     const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
     if (p1 - p0 > std::uint32_t(kLongSeg)) {
-      if (sub == 0) {
-        if (p1 - p0 > std::uint32_t(kBigChunk))
+      if (d == 0) {
+        if (p1 - p0 > medium_max)
           big_list[atomicAdd(n_big, 1ull)] = std::uint32_t(u);
         else
           long_list[atomicAdd(n_long, 1ull)] = std::uint32_t(u);
       }
       continue;
     }
-    double acc[kDPL];
-#pragma unroll
-    for (int q = 0; q < kDPL; ++q) acc[q] = 0.0;
-    for (std::uint32_t c = p0; c < p1; c += SD) {
-      const int len = int(p1 - c < std::uint32_t(SD) ? p1 - c : SD);
-      const std::uint32_t my_ex = sub < len ? exs[c + sub] : 0u;
-      double v[SD][kDPL];
-#pragma unroll
-      for (int r = 0; r < SD; ++r) {
-        const std::uint64_t ex = __shfl_sync(gmask, my_ex, r, LPK);
-        const double* row = DX + ex * std::uint64_t(E);
-#pragma unroll
-        for (int q = 0; q < kDPL; ++q) {
-          const int d = sub + q * LPK;
-          v[r][q] = (r < len && d < E) ? row[d] : 0.0;
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < SD; ++r)
-        if (r < len) {
-#pragma unroll
-          for (int q = 0; q < kDPL; ++q) acc[q] = __dadd_rn(acc[q], v[r][q]);
-        }
+    double acc = 0.0;
+    std::uint32_t p = p0;
+    for (; p + 4 <= p1; p += 4) {
+      const std::uint32_t e0 = exs[p], e1 = exs[p + 1], e2 = exs[p + 2], e3 = exs[p + 3];
+      const double x0 = DX[std::uint64_t(e0) * E + d], x1 = DX[std::uint64_t(e1) * E + d];
+      const double x2 = DX[std::uint64_t(e2) * E + d], x3 = DX[std::uint64_t(e3) * E + d];
+      acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, x0), x1), x2), x3);
     }
-    const std::uint64_t orow = pos ? pos[u] : u;
-#pragma unroll
-    for (int q = 0; q < kDPL; ++q) {
-      const int d = sub + q * LPK;
-      if (d < E) write_delta(out, orow, E, d, acc[q], inv_n, lr);
-    }
+    for (; p < p1; ++p) acc = __dadd_rn(acc, DX[std::uint64_t(exs[p]) * E + d]);
+    write_delta(out, pos ? pos[u] : u, E, d, acc, inv_n, lr);
   }
 }
 
@@ -639,7 +617,7 @@ struct ChunkSum {  // one chunk of one dimension: total (Neumaier), sum|x|, B bo
   double hi, lo, a, b;
 };
 
-__global__ void big_plan_kernel(const std::uint32_t* __restrict__ big_list,
+__global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big_list,
                                 const unsigned long long* __restrict__ n_big,
                                 const std::uint32_t* __restrict__ seg,
                                 std::uint32_t* __restrict__ chunk_off,
@@ -652,7 +630,7 @@ __global__ void big_plan_kernel(const std::uint32_t* __restrict__ big_list,
     std::uint32_t v = 0;
     if (i < NB) {
       const std::uint32_t u = big_list[i];
-      v = (seg[u + 1] - seg[u] + kBigChunk - 1) / kBigChunk;
+      v = (seg[u + 1] - seg[u] + chunk - 1) / chunk;
     }
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     std::uint32_t x = v;
@@ -690,7 +668,7 @@ __device__ __forceinline__ void big_item(const std::uint32_t* chunk_off, std::ui
 }
 
 __global__ void __launch_bounds__(kBigThreads)
-    big_p1_kernel(int E, const std::uint32_t* __restrict__ big_list,
+    big_p1_kernel(int E, int chunk, const std::uint32_t* __restrict__ big_list,
                   const unsigned long long* __restrict__ n_big,
                   const std::uint32_t* __restrict__ chunk_off,
                   const unsigned long long* __restrict__ n_items,
@@ -706,8 +684,8 @@ __global__ void __launch_bounds__(kBigThreads)
     big_item(chunk_off, NB, w, &ki, &c);
     if (s < slices) {
       const std::uint32_t u = big_list[ki];
-      const std::uint32_t c0 = seg[u] + c * kBigChunk;
-      const std::uint32_t c1 = min(seg[u + 1], c0 + kBigChunk);
+      const std::uint32_t c0 = seg[u] + c * chunk;
+      const std::uint32_t c1 = min(seg[u + 1], c0 + chunk);
       const std::uint32_t per = (c1 - c0 + slices - 1) / slices;
       const std::uint32_t a0 = c0 + s * per, a1 = min(c1, a0 + per);
       DD t{0.0, 0.0};
@@ -738,7 +716,8 @@ __global__ void __launch_bounds__(kBigThreads)
 }
 
 __global__ void __launch_bounds__(kBigThreads)
-    big_p2_kernel(int E, float lr, std::uint64_t n, const std::uint32_t* __restrict__ big_list,
+    big_p2_kernel(int E, int chunk, float lr, std::uint64_t n,
+                  const std::uint32_t* __restrict__ big_list,
                   const unsigned long long* __restrict__ n_big,
                   const std::uint32_t* __restrict__ chunk_off,
                   const unsigned long long* __restrict__ n_items,
@@ -774,7 +753,7 @@ __global__ void __launch_bounds__(kBigThreads)
         off = dd_add(off, DD{bp.hi, bp.lo});
       }
       const double o = dd_value(off);
-      const std::uint32_t c0 = k0 + c * kBigChunk, c1 = min(k1, c0 + kBigChunk);
+      const std::uint32_t c0 = k0 + c * chunk, c1 = min(k1, c0 + chunk);
       const std::uint32_t per = (c1 - c0 + slices - 1) / slices;
       const std::uint32_t a0 = c0 + s * per, a1 = min(c1, a0 + per);
       double l = 0.0, b = 0.0;

@@ -69,6 +69,211 @@ __global__ void table_insert_kernel(const std::uint64_t* __restrict__ ws,
   }
 }
 
+// ---- sort-free build from the raw batch keys (hps_train_batch) ---------
+//
+// 1. ws_count_kernel: exact count of the distinct owned keys through a
+//    scratch hash set (atomicCAS; the capacity of the real table, hence its
+//    layout, depends on that count).
+// 2. table_insert_dedup_kernel: ordered linear probing of every owned
+//    occurrence; a thread that meets its own key stops. Ordered probing is
+//    history-independent for sets, so the layout equals ascending insertion
+//    of the sorted unique keys (hbm_ps.hpp:69-98) without sorting them.
+// 3. rows are filled / written back by scanning the table's slots.
+
+__global__ void ws_count_kernel(const std::uint64_t* __restrict__ keys,
+                                const std::int64_t* __restrict__ o_ptr, std::uint64_t G,
+                                std::uint64_t g, std::uint64_t* __restrict__ set,
+                                std::uint64_t set_mask, unsigned long long* __restrict__ n_ws) {
+  const std::uint64_t O = std::uint64_t(*o_ptr);
+  unsigned long long mine = 0;
+  for (std::uint64_t q = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; q < O;
+       q += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t k = keys[q];
+    if (k % G != g) continue;
+    std::uint64_t idx = mix64(k) & set_mask;
+    for (;;) {
+      const unsigned long long old =
+          atomicCAS(reinterpret_cast<unsigned long long*>(set + idx), kEmptyKey, k);
+      if (old == kEmptyKey) {
+        ++mine;
+        break;
+      }
+      if (old == k) break;
+      idx = (idx + 1) & set_mask;
+    }
+  }
+  // warp-aggregated count
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(n_ws, mine);
+}
+
+__global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys,
+                                          const std::int64_t* __restrict__ o_ptr,
+                                          std::uint64_t G, std::uint64_t g,
+                                          std::uint64_t* __restrict__ tkeys,
+                                          const std::uint64_t* __restrict__ cap_ptr,
+                                          DevError* err) {
+  const std::uint64_t O = std::uint64_t(*o_ptr), cap = *cap_ptr;
+  for (std::uint64_t q = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; q < O;
+       q += std::uint64_t(gridDim.x) * blockDim.x) {
+    std::uint64_t cur = keys[q];
+    if (cur % G != g) continue;
+    if (cur == kEmptyKey) {
+      raise_error(err, 1, cur);
+      continue;
+    }
+    std::uint64_t idx = mix64(cur) & (cap - 1);
+    for (std::uint64_t probes = 0;; ++probes) {
+      const std::uint64_t old = atomicMin(reinterpret_cast<unsigned long long*>(tkeys + idx),
+                                          static_cast<unsigned long long>(cur));
+      if (old == kEmptyKey || old == cur) break;  // placed / already present
+      if (old > cur) cur = old;                   // displaced: carry the larger key
+      idx = (idx + 1) & (cap - 1);
+      if (probes > cap) {
+        raise_error(err, 4, cur);
+        break;
+      }
+    }
+  }
+}
+
+// Row fill over the table's slots (hbm_ps.hpp:86-98): carry-over from the
+// previous table, else the attached value store, else zeros.
+template <int VEC>
+__global__ void table_fill_slots_kernel(const std::uint64_t* __restrict__ keys,
+                                        float* __restrict__ vals,
+                                        const std::uint64_t* __restrict__ cap_ptr,
+                                        const std::uint64_t* __restrict__ prev_keys,
+                                        const float* __restrict__ prev_vals,
+                                        const std::uint64_t* __restrict__ prev_cap_ptr,
+                                        const float* __restrict__ store,
+                                        std::uint64_t store_keys, int E,
+                                        unsigned long long* carried) {
+  const int tpk = E / VEC;
+  const std::uint64_t cap = *cap_ptr;
+  const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < cap * std::uint64_t(tpk); t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t slot = t / tpk;
+    const int part = int(t - slot * tpk);
+    const std::uint64_t key = keys[slot];
+    const bool live = key != kEmptyKey;
+    const float* src = nullptr;
+    if (live && pcap) {
+      const std::uint32_t ps = probe_slot(prev_keys, pcap, key);
+      if (ps != kNoSlot) src = prev_vals + std::uint64_t(ps) * E;
+    }
+    if (carried) {
+      const unsigned hit = __ballot_sync(__activemask(), src != nullptr && part == 0);
+      if (hit && (threadIdx.x & 31) == unsigned(__ffs(__activemask()) - 1))
+        atomicAdd(carried, (unsigned long long)__popc(hit));
+    }
+    if (!live) continue;
+    if (!src && store && key < store_keys) src = store + key * std::uint64_t(E);
+    float* dst = vals + slot * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, src ? ld_f4(src + part * 4) : make_float4(0.f, 0.f, 0.f, 0.f));
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) dst[v] = src ? src[part * VEC + v] : 0.0f;
+    }
+  }
+}
+
+// Write-back of every live row to the value store, over the slots.
+template <int VEC>
+__global__ void table_writeback_slots_kernel(const std::uint64_t* __restrict__ keys,
+                                             const float* __restrict__ vals,
+                                             const std::uint64_t* __restrict__ cap_ptr,
+                                             float* __restrict__ store, std::uint64_t store_keys,
+                                             int E) {
+  const int tpk = E / VEC;
+  const std::uint64_t cap = *cap_ptr;
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < cap * std::uint64_t(tpk); t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t slot = t / tpk;
+    const int part = int(t - slot * tpk);
+    const std::uint64_t key = keys[slot];
+    if (key == kEmptyKey || key >= store_keys) continue;
+    const float* src = vals + slot * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(store + key * E + part * 4, ld_f4(src));
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) store[key * E + part * VEC + q] = src[q];
+    }
+  }
+}
+
+// Row fill in ascending key order with known slots (ws[i], wslot[i]): the
+// value-store accesses run through adjacent rows, which keeps zero-copy
+// PCIe reads of a host-resident store efficient.
+template <int VEC>
+__global__ void table_fill_sorted_kernel(const std::uint64_t* __restrict__ ws,
+                                         const std::uint32_t* __restrict__ wslot,
+                                         const std::uint64_t* __restrict__ n_ptr,
+                                         float* __restrict__ vals,
+                                         const std::uint64_t* __restrict__ prev_keys,
+                                         const float* __restrict__ prev_vals,
+                                         const std::uint64_t* __restrict__ prev_cap_ptr,
+                                         const float* __restrict__ store,
+                                         std::uint64_t store_keys, int E,
+                                         unsigned long long* carried) {
+  const int tpk = E / VEC;
+  const std::uint64_t n = *n_ptr;
+  const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < n * std::uint64_t(tpk); t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    const std::uint64_t key = ws[i];
+    const float* src = nullptr;
+    if (pcap) {
+      const std::uint32_t ps = probe_slot(prev_keys, pcap, key);
+      if (ps != kNoSlot) src = prev_vals + std::uint64_t(ps) * E;
+    }
+    if (carried) {
+      const unsigned hit = __ballot_sync(__activemask(), src != nullptr && part == 0);
+      if (hit && (threadIdx.x & 31) == unsigned(__ffs(__activemask()) - 1))
+        atomicAdd(carried, (unsigned long long)__popc(hit));
+    }
+    if (!src && store && key < store_keys) src = store + key * std::uint64_t(E);
+    float* dst = vals + std::uint64_t(wslot[i]) * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, src ? ld_f4(src + part * 4) : make_float4(0.f, 0.f, 0.f, 0.f));
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) dst[v] = src ? src[part * VEC + v] : 0.0f;
+    }
+  }
+}
+
+// Write-back in ascending key order with known slots.
+template <int VEC>
+__global__ void table_writeback_sorted_kernel(const std::uint64_t* __restrict__ ws,
+                                              const std::uint32_t* __restrict__ wslot,
+                                              const std::uint64_t* __restrict__ n_ptr,
+                                              const float* __restrict__ vals,
+                                              float* __restrict__ store, std::uint64_t store_keys,
+                                              int E) {
+  const int tpk = E / VEC;
+  const std::uint64_t n = *n_ptr;
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+       t < n * std::uint64_t(tpk); t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    const std::uint64_t key = ws[i];
+    if (key >= store_keys) continue;
+    const float* src = vals + std::uint64_t(wslot[i]) * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(store + key * E + part * 4, ld_f4(src));
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) store[key * E + part * VEC + q] = src[q];
+    }
+  }
+}
+
 // Row fill for the fresh table (hbm_ps.hpp:86-98): carry-over from the
 // previous table when the key was resident, else the staged host row
 // (HostValue), else the attached value store, else zeros. VEC floats per

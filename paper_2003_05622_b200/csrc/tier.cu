@@ -162,8 +162,11 @@ struct Tier {
   bool has_prev = false;
 
   // working set
-  std::uint64_t* ws = nullptr;
+  std::uint64_t* ws = nullptr;       // sorted keys of the current table (when ws_sorted)
   std::uint32_t* ws_idx = nullptr;
+  bool ws_sorted = true;
+  std::uint64_t* wsset = nullptr;    // scratch hash set of the sort-free build
+  std::uint64_t wsset_cap = 0;
 
   // sort scratch
   std::uint64_t *kA = nullptr, *kB = nullptr;
@@ -494,6 +497,11 @@ struct CompactEmit {  // out[pre] = key (and index) for selected items
     }
   }
 };
+struct LiveSlot {
+  const std::uint64_t* keys;
+  __device__ std::uint32_t operator()(std::uint64_t i) const { return keys[i] != kEmptyKey; }
+};
+
 struct UniqueEmit {  // inverse index + CSR segments of a sorted (key, occ) list
   const std::uint64_t* sk;
   const std::uint32_t* so;
@@ -823,16 +831,18 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
   return HPS_OK;
 }
 
+// Segment-length routing of the sparse reduce: <= kLongSeg in-order by a
+// sub-warp, (kLongSeg, kMediumMax] one CTA per key, longer ones split into
+// kBigChunkRun-occurrence chunks over CTAs.
+constexpr int kMediumMax = kLongSeg;  // medium path off: chunks serve every long key
+constexpr int kBigChunkRun = 256;
+
 // Sparse segment-reduce launches: LPK lanes per short segment (pow2 >= E,
 // 4..32), then one CTA per long segment.
 static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint32_t* pos,
                                       std::uint64_t u_upper) {
   const int E = t->E;
   if (E > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
-  int lpk = 4;
-  while (lpk < E && lpk < 32) lpk <<= 1;
-  const std::uint64_t threads = std::max<std::uint64_t>(u_upper, 1) * lpk;
-  const unsigned grid = grid_for(threads, 256, kSMs * 32);
   const float lr = t->cfg.learning_rate;
   const std::uint64_t* U = &t->dsc->U;
   const std::uint32_t* seg = t->seg;
@@ -842,26 +852,22 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   unsigned long long* nl = &t->dsc->n_long;
   unsigned long long* nb = &t->dsc->n_big;
   if (t->G == 1) HPS_CUDA(cudaMemsetAsync(nl, 0, 16, t->st));  // G > 1: owner_rank_kernel
-#define HPS_SD(L, Q)                                                                    \
-  launch(t, sparse_delta_kernel<L, Q>, grid, 256, 0, E, lr, n, U, seg, exs, pos, DX,    \
-         t->deltas, pulled, t->long_list, nl, t->big_list, nb)
-  if (lpk == 4) HPS_SD(4, 1);
-  else if (lpk == 8) HPS_SD(8, 1);
-  else if (lpk == 16) HPS_SD(16, 1);
-  else if (E <= 32) HPS_SD(32, 1);
-  else if (E <= 64) HPS_SD(32, 2);
-  else HPS_SD(32, 8);
-#undef HPS_SD
-  launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, 0, E, lr, n,
-         (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos, DX,
-         t->deltas, &t->dsc->fallbacks);
+launch(t, sparse_short_kernel, grid_for(std::max<std::uint64_t>(u_upper, 1) * E, 256, kSMs * 32),
+         256, 0, E, lr, n, U, seg, exs, pos, DX, t->deltas, pulled, t->long_list, nl, t->big_list,
+         nb, std::uint32_t(kMediumMax));
+  if (kMediumMax > kLongSeg)
+    launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, 0, E, lr, n,
+           (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos, DX,
+           t->deltas, &t->dsc->fallbacks);
   // big segments: plan (key, chunk) items, then the two passes over CTAs
-  launch(t, big_plan_kernel, 1, 256, 0, (const std::uint32_t*)t->big_list,
+  launch(t, big_plan_kernel, 1, 256, 0, kBigChunkRun, (const std::uint32_t*)t->big_list,
          (const unsigned long long*)nb, seg, t->chunk_off, &t->dsc->n_items);
-  launch(t, big_p1_kernel, kSMs * 4, kBigThreads, 0, E, (const std::uint32_t*)t->big_list,
+  launch(t, big_p1_kernel, kSMs * 4, kBigThreads, 0, E, kBigChunkRun,
+         (const std::uint32_t*)t->big_list,
          (const unsigned long long*)nb, (const std::uint32_t*)t->chunk_off,
          (const unsigned long long*)&t->dsc->n_items, seg, exs, DX, t->big_part, t->chunk_tot);
-  launch(t, big_p2_kernel, kSMs * 4, kBigThreads, 0, E, lr, n, (const std::uint32_t*)t->big_list,
+  launch(t, big_p2_kernel, kSMs * 4, kBigThreads, 0, E, kBigChunkRun, lr, n,
+         (const std::uint32_t*)t->big_list,
          (const unsigned long long*)nb, (const std::uint32_t*)t->chunk_off,
          (const unsigned long long*)&t->dsc->n_items, seg, exs, pos, DX, t->big_part,
          t->chunk_tot, t->key_done, t->deltas, &t->dsc->fallbacks);
@@ -981,22 +987,59 @@ static hps_status enqueue_batch_body(Tier* T, const BatchShape& sh, int skip_mb)
   const Count own_n{&T->dsc->counts[J], 0};
   // (the caller opened the look-back context: ticket counter reset, device
   // context counter advanced — eagerly, so captured graphs replay correctly)
-  // ---- working set (a1, a2) + build (a3, a4)
+  // ---- working set (a1, a2) + build (a3, a4), sort-free: exact distinct
+  // count through a scratch set (it fixes the capacity), then ordered probing
+  // of the raw owned occurrences (duplicates stop on their own key), then the
+  // rows by slot scan (carry-over, else the value store)
   {
-    const std::uint64_t* kin = dkeys;
-    if (G > 1) {  // stable compaction of the owned keys into kB
-      tile_scan(T, OwnedKey{dkeys, std::uint64_t(G), std::uint64_t(T->g)},
-                CompactEmit{dkeys, nullptr, T->kB, nullptr},
-                Count{reinterpret_cast<const std::uint64_t*>(doff + B), 0}, sh.batch_bound,
-                &T->dsc->total);
-      kin = T->kB;
-    }
+    const int nxt = (T->cur < 0) ? 0 : 1 - T->cur;
+    const int prv = T->cur;
+    const std::int64_t* o_ptr = doff + B;
+    std::uint64_t setcap = 1;
+    while (setcap < 2 * sh.own_bound) setcap <<= 1;
+    setcap = std::min(setcap, T->wsset_cap);
+    HPS_CUDA(cudaMemsetAsync(T->wsset, 0xFF, setcap * 8, T->st));
+    HPS_CUDA(cudaMemsetAsync(&T->dsc->n_ws, 0, 8, T->st));
+    const unsigned gk = grid_for(sh.batch_bound, 256, kSMs * 8);
+    launch(T, ws_count_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G), std::uint64_t(T->g),
+           T->wsset, setcap - 1, (unsigned long long*)&T->dsc->n_ws);
+    launch(T, table_capacity_kernel, 1, 1, 0, (const std::uint64_t*)&T->dsc->n_ws,
+           &T->dsc->cap[nxt]);
+    const std::uint64_t cap_bound = table_capacity(sh.own_bound);
+    launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[nxt],
+           (const std::uint64_t*)&T->dsc->cap[nxt]);
+    launch(T, table_insert_dedup_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G),
+           std::uint64_t(T->g), T->tkeys[nxt], (const std::uint64_t*)&T->dsc->cap[nxt],
+           &T->dsc->err);
+    // the distinct keys with their slots, ascending: compact the live slots,
+    // sort them (n_ws items, ~3x fewer than the occurrences)
+    tile_scan(T, LiveSlot{T->tkeys[nxt]}, CompactEmit{T->tkeys[nxt], nullptr, T->kB, T->vB},
+              Count{&T->dsc->cap[nxt], 0}, cap_bound, &T->dsc->total);
     std::uint64_t* sk = nullptr;
     std::uint32_t* so = nullptr;
-    radix_sort(T, kin, nullptr, own_n, sh.own_bound, T->sort_bits, false, &sk, &so);
-    tile_scan(T, RunStart{sk}, CompactEmit{sk, nullptr, T->ws, nullptr}, own_n, sh.own_bound,
-              &T->dsc->n_ws);
-    build_table(T, sh.own_bound, nullptr, nullptr);
+    radix_sort(T, T->kB, T->vB, Count{&T->dsc->n_ws, 0}, sh.own_bound, T->sort_bits, true, &sk,
+               &so);
+    const std::uint64_t wcopy = std::min(sh.own_bound, T->Wmax);  // bound, within the buffers
+    HPS_CUDA(cudaMemcpyAsync(T->ws, sk, wcopy * 8, cudaMemcpyDeviceToDevice, T->st));
+    HPS_CUDA(cudaMemcpyAsync(T->ws_idx, so, wcopy * 4, cudaMemcpyDeviceToDevice, T->st));
+    const std::uint64_t* pcap = (prv >= 0) ? &T->dsc->cap[prv] : nullptr;
+    const std::uint64_t* pk = (prv >= 0) ? T->tkeys[prv] : nullptr;
+    const float* pv = (prv >= 0) ? T->tvals[prv] : nullptr;
+    const int V = vec_of(E);
+    const unsigned gf = grid_for(sh.own_bound * std::uint64_t(E / V));
+    if (V == 4)
+      launch(T, table_fill_sorted_kernel<4>, gf, 256, 0, (const std::uint64_t*)T->ws,
+             (const std::uint32_t*)T->ws_idx, (const std::uint64_t*)&T->dsc->n_ws, T->tvals[nxt],
+             pk, pv, pcap, (const float*)T->store, T->store_keys, E, &T->dsc->carried);
+    else
+      launch(T, table_fill_sorted_kernel<1>, gf, 256, 0, (const std::uint64_t*)T->ws,
+             (const std::uint32_t*)T->ws_idx, (const std::uint64_t*)&T->dsc->n_ws, T->tvals[nxt],
+             pk, pv, pcap, (const float*)T->store, T->store_keys, E, &T->dsc->carried);
+    HPS_CUDA(cudaMemcpyAsync(&T->dsc->nws_tab[nxt], &T->dsc->n_ws, 8, cudaMemcpyDeviceToDevice,
+                             T->st));
+    T->has_prev = prv >= 0;
+    T->cur = nxt;
+    T->ws_sorted = true;
   }
   mark(T, HPS_T_BUILD);
   // ---- mini-batches
@@ -1068,19 +1111,17 @@ static hps_status enqueue_batch_body(Tier* T, const BatchShape& sh, int skip_mb)
     if (j != skip_mb) HPS_TRY(dense_sync_update(T, true));
     mark(T, HPS_T_DENSE);
   }
-  // ---- write-back to the value store (a13)
+  // ---- write-back to the value store (a13), over the table's slots
   if (T->store) {
-    const std::uint64_t work = sh.own_bound * std::uint64_t(E / V);
+    const unsigned gw = grid_for(sh.own_bound * std::uint64_t(E / V));
     if (V == 4)
-      launch(T, table_dump_kernel<4>, grid_for(work), 256, 0, (const std::uint64_t*)T->ws,
-             (const std::uint64_t*)&T->dsc->n_ws, (const std::uint64_t*)T->tkeys[T->cur],
-             (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
-             T->store_keys, (float*)nullptr, E, &T->dsc->err);
+      launch(T, table_writeback_sorted_kernel<4>, gw, 256, 0, (const std::uint64_t*)T->ws,
+             (const std::uint32_t*)T->ws_idx, (const std::uint64_t*)&T->dsc->n_ws,
+             (const float*)T->tvals[T->cur], T->store, T->store_keys, E);
     else
-      launch(T, table_dump_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)T->ws,
-             (const std::uint64_t*)&T->dsc->n_ws, (const std::uint64_t*)T->tkeys[T->cur],
-             (const float*)T->tvals[T->cur], (const std::uint64_t*)&T->dsc->cap[T->cur], T->store,
-             T->store_keys, (float*)nullptr, E, &T->dsc->err);
+      launch(T, table_writeback_sorted_kernel<1>, gw, 256, 0, (const std::uint64_t*)T->ws,
+             (const std::uint32_t*)T->ws_idx, (const std::uint64_t*)&T->dsc->n_ws,
+             (const float*)T->tvals[T->cur], T->store, T->store_keys, E);
   }
   mark(T, HPS_T_WRITEBACK);
   return HPS_OK;
@@ -1274,6 +1315,9 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(tvals[1], t->capmax * E);
   A(ws, W);
   A(ws_idx, W);
+  t->wsset_cap = 1;
+  while (t->wsset_cap < 2 * std::max(O, W)) t->wsset_cap <<= 1;
+  A(wsset, t->wsset_cap);
   const std::uint64_t S = std::max(O, W);
   A(kA, S);
   A(kB, S);
@@ -1297,11 +1341,11 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(orank, S);
   A(otot, kMaxRanks);
   A(long_list, S);
-  A(big_list, S / kBigChunk + 2);
-  A(chunk_off, S / kBigChunk + 3);
-  A(key_done, S / kBigChunk + 2);
-  A(big_part, (2 * S / kBigChunk + 2) * std::uint64_t(kBigThreads));
-  A(chunk_tot, (2 * S / kBigChunk + 2) * E);
+  A(big_list, S / (kLongSeg + 1) + 2);
+  A(chunk_off, S / (kLongSeg + 1) + 3);
+  A(key_done, S / (kLongSeg + 1) + 2);
+  A(big_part, (S / kBigChunkRun + S / (kLongSeg + 1) + 2) * std::uint64_t(kBigThreads));
+  A(chunk_tot, (S / kBigChunkRun + S / (kLongSeg + 1) + 2) * E);
   A(ukeys, S);
   if (G == 1) A(rows, S * E);  // G > 1: inside the exported window (peers write it)
   A(deltas, S * E);
@@ -1316,7 +1360,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
 #undef A
   cudaMemsetAsync(t->ticket, 0, 8, t->st);
   cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
-  cudaMemsetAsync(t->key_done, 0, (S / kBigChunk + 2) * 4, t->st);
+  cudaMemsetAsync(t->key_done, 0, (S / (kLongSeg + 1) + 2) * 4, t->st);
   cudaMemsetAsync(t->status, 0,
                   (std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1) * 8,
                   t->st);
@@ -1404,6 +1448,7 @@ hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float
     HPS_CUDA(cudaMemsetAsync(&t->dsc->n_ws, 0, 8, t->st));
   }
   build_table(t, n, t->ws_idx, staged);
+  t->ws_sorted = true;
   return check_device_error(t, "device table: missing key ");
 }
 
@@ -1562,9 +1607,21 @@ hps_status hps_table_slots(hps_tier_t t, uint64_t* slot_keys, float* rows) {
   return HPS_OK;
 }
 
+
 hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t* n_out) {
-  std::uint64_t occ = 0;
-  HPS_TRY(hps_table_info(t, nullptr, &occ, nullptr));
+  std::uint64_t occ = 0, cap = 0;
+  HPS_TRY(hps_table_info(t, &cap, &occ, nullptr));
+  if (!t->ws_sorted) {  // after hps_train_batch: the sorted key list from the table itself
+    open_lookback_context(t);
+    tile_scan(t, LiveSlot{t->tkeys[t->cur]},
+              CompactEmit{t->tkeys[t->cur], nullptr, t->kB, nullptr}, Count{nullptr, cap}, cap,
+              &t->dsc->total);
+    std::uint64_t* sk = nullptr;
+    std::uint32_t* so = nullptr;
+    radix_sort(t, t->kB, nullptr, Count{nullptr, occ}, occ, t->sort_bits, false, &sk, &so);
+    HPS_CUDA(cudaMemcpyAsync(t->ws, sk, occ * 8, cudaMemcpyDeviceToDevice, t->st));
+    t->ws_sorted = true;
+  }
   // The working set of the current table is still in t->ws (sorted).
   const int V = vec_of(t->E);
   const std::uint64_t work = occ * std::uint64_t(t->E / V);

@@ -149,3 +149,25 @@ def test_graph_replays_bit_exact(pkg, oracle):
     for dense, store in outs:
         assert np.array_equal(dense, wd)
         assert np.array_equal(store[wk.astype(np.int64)], wr)
+
+
+def test_dump_after_sort_free_build(pkg, oracle):
+    """hps_train_batch builds its table without sorting the working set; the
+    reference dump_node contract (every key of the batch, ascending, with its
+    row, hbm_ps.hpp:224-232) must still hold."""
+    dims, B, nnz = 20000, 512, 20
+    off, keys, lab = pkg.gen_dataset(dims, 2 * B, nnz, zipf=True, seed=8)
+    tier = pkg.Tier(width=8, layer_dims=(8, 16, 1), minibatches=4, key_space=dims,
+                    max_batch_examples=B, max_batch_keys=B * nnz)
+    store = np.zeros((dims, 8), dtype=np.float32)
+    tier.attach_store(store)
+    for b in range(2):
+        tier.train_batch(off[b * B:(b + 1) * B + 1] - off[b * B],
+                         keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B])
+    dk, dr = tier.dump()
+    want = np.unique(keys[off[B]:off[2 * B]])
+    assert np.array_equal(dk, want)
+    assert np.array_equal(dr, store[want.astype(np.int64)])
+    slots = tier.table_slots()
+    assert np.array_equal(slots, oracle.table_build(want))  # layout == ascending insert
+    tier.close()
