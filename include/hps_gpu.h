@@ -81,6 +81,9 @@ typedef struct {
   uint64_t carried_rows;     /* build rows taken from the previous table */
   uint64_t exact_fallbacks;  /* certified parallel sums that had to be redone
                                 in the exact sequential order */
+  uint64_t store_rows;       /* build rows read from the attached value store
+                                (the rest: carried, the table two builds back
+                                while its write-back drains, or zeros) */
 } hps_batch_stats;
 
 /* Phase slots of hps_get_timing (ms accumulated over hps_train_batch calls,
@@ -175,9 +178,18 @@ hps_status hps_set_dense(hps_tier_t h, const float* w);
  * previous table from it, and hps_train_batch writes the trained rows back
  * after each batch (dump_node -> MemPs::collect_updates, pipeline.hpp:
  * 441-445, mem_ps.hpp:210-245). on_device = 0: pinned host memory reached
- * with zero-copy gather/scatter kernels; 1: an HBM array. */
+ * with zero-copy gather/scatter kernels; 1: an HBM array. Flushes pending
+ * write-backs to the previously attached store first. */
 hps_status hps_attach_store(hps_tier_t h, float* rows, uint64_t num_keys,
                             int on_device);
+
+/* The write-back of batch b runs asynchronously, overlapping batch b+1 (the
+ * reference's collect stage runs beside the next train step, pipeline.hpp:
+ * 462-474); batch b+2's build waits for it, as prepare of step+2 waits for
+ * collect of step (mem_ps.hpp freshness rule). hps_flush blocks until every
+ * pending write-back has reached the store; after it (or hps_attach_store /
+ * hps_destroy) the store holds every trained row. */
+hps_status hps_flush(hps_tier_t h);
 
 /* One whole batch through the tier, device-resident: working-set dedup ->
  * build (carry-over + store staging) -> J x {mini-batch dedup, pull
@@ -193,9 +205,26 @@ hps_status hps_train_batch(hps_tier_t h, uint64_t num_examples,
                            const uint8_t* labels, int on_device,
                            hps_batch_stats* stats);
 
+/* The same batch, pipelined (the reference Trainer's bounded stage queues,
+ * pipeline.hpp:42-60 and 305-315): hps_submit_batch stages the batch (H2D +
+ * counts; the host blocks only on that round-trip), enqueues its table build
+ * beside the previous batch's body, its body and its write-back, and returns.
+ * hps_wait_batch returns the results of the oldest submitted batch not yet
+ * waited for, in submission order. At most three batches are in flight (a
+ * fourth submit first completes the oldest; its result stays queued). The caller's
+ * buffers may be reused as soon as hps_submit_batch returns. Results are
+ * bit-identical to hps_train_batch on the same batches. COLLECTIVE. Every
+ * other entry point completes all in-flight batches first. */
+hps_status hps_submit_batch(hps_tier_t h, uint64_t num_examples,
+                            const int64_t* offsets, const uint64_t* keys,
+                            const uint8_t* labels, int on_device);
+hps_status hps_wait_batch(hps_tier_t h, hps_batch_stats* stats);
+
 /* Per-phase device time of hps_train_batch (HPS_T_* slots, ms, accumulated
  * until hps_reset_timing). Enabled by hps_set_timing(h, 1): adds event
- * records on the tier stream, no extra host synchronisation. */
+ * records on the pipeline's streams and runs one batch at a time, so every
+ * phase is timed without overlap (BUILD = table build + carry-over;
+ * WRITEBACK = the deferred write-back; TOTAL = stage start to body end). */
 hps_status hps_set_timing(hps_tier_t h, int enable);
 hps_status hps_get_timing(hps_tier_t h, double* ms /* HPS_TIMING_SLOTS */);
 hps_status hps_reset_timing(hps_tier_t h);

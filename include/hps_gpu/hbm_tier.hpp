@@ -273,9 +273,22 @@ class HbmTier {
     check(hps_train_batch(h_, num_examples, offsets, keys, labels, on_device ? 1 : 0, &st));
     return st;
   }
+  // pipelined train_batch: submit returns once the batch is staged and
+  // enqueued; wait returns results in submission order
+  void submit_batch(std::uint64_t num_examples, const std::int64_t* offsets,
+                    const ParamKey* keys, const std::uint8_t* labels, bool on_device = false) {
+    check(hps_submit_batch(h_, num_examples, offsets, keys, labels, on_device ? 1 : 0));
+  }
+  hps_batch_stats wait_batch() {
+    hps_batch_stats st{};
+    check(hps_wait_batch(h_, &st));
+    return st;
+  }
   void attach_store(float* rows, std::uint64_t num_keys, bool on_device) {
     check(hps_attach_store(h_, rows, num_keys, on_device ? 1 : 0));
   }
+  // collect stage barrier: deferred write-backs have reached the store
+  void flush() { check(hps_flush(h_)); }
   std::vector<float> dense() const {
     std::uint64_t n = 0;
     check(hps_dense_count(h_, &n));

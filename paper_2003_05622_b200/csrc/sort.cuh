@@ -99,14 +99,27 @@ __device__ __forceinline__ std::uint64_t look_back(const LookBack& lb, std::uint
 #pragma unroll
     for (int q = 0; q < kAhead; ++q)
       w[q] = (j - q >= 0) ? ld_status(lb.status + std::uint64_t(j - q) * stride + lane_idx) : 0;
-    int q = 0;
-    for (; q < kAhead && j - q >= 0; ++q) {
-      const std::uint64_t x = w[q];
-      if (std::uint32_t(x >> 32) != epoch || (x & (kFlagAgg | kFlagInc)) == 0) break;
-      excl += x & kCountMask;
-      if (x & kFlagInc) return excl;
+    // consume newest-first (fully unrolled: w stays in registers)
+    int consumed = 0;
+    bool stop = false, done = false;
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) {
+      if (!stop) {
+        const std::uint64_t x = w[q];
+        if (j - q < 0 || std::uint32_t(x >> 32) != epoch || (x & (kFlagAgg | kFlagInc)) == 0) {
+          stop = true;
+        } else {
+          excl += x & kCountMask;
+          ++consumed;
+          if (x & kFlagInc) {
+            done = true;
+            stop = true;
+          }
+        }
+      }
     }
-    j -= q;  // consumed q aggregates; re-poll the first unready one (if any)
+    if (done) return excl;
+    j -= consumed;  // re-poll the first unready predecessor (if any)
   }
   return excl;
 }

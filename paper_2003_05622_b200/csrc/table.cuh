@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -78,7 +79,9 @@ __global__ void table_insert_kernel(const std::uint64_t* __restrict__ ws,
 //    occurrence; a thread that meets its own key stops. Ordered probing is
 //    history-independent for sets, so the layout equals ascending insertion
 //    of the sorted unique keys (hbm_ps.hpp:69-98) without sorting them.
-// 3. rows are filled / written back by scanning the table's slots.
+// 3. the live slots are compacted and sorted by key; rows are then filled in
+//    key order (table_prefetch_probe / store_gather / table_carry) and
+//    written back in key order (table_writeback_sorted).
 
 __global__ void ws_count_kernel(const std::uint64_t* __restrict__ keys,
                                 const std::int64_t* __restrict__ o_ptr, std::uint64_t G,
@@ -92,6 +95,13 @@ __global__ void ws_count_kernel(const std::uint64_t* __restrict__ keys,
     if (k % G != g) continue;
     std::uint64_t idx = mix64(k) & set_mask;
     for (;;) {
+      // read first: hot keys are already present, no atomic (and no contention)
+      const std::uint64_t seen = *reinterpret_cast<volatile const std::uint64_t*>(set + idx);
+      if (seen == k) break;
+      if (seen != kEmptyKey) {
+        idx = (idx + 1) & set_mask;
+        continue;
+      }
       const unsigned long long old =
           atomicCAS(reinterpret_cast<unsigned long long*>(set + idx), kEmptyKey, k);
       if (old == kEmptyKey) {
@@ -124,6 +134,19 @@ __global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys
     }
     std::uint64_t idx = mix64(cur) & (cap - 1);
     for (std::uint64_t probes = 0;; ++probes) {
+      // slots only ever decrease: a read that shows cur (present) or a smaller
+      // key (advance) decides exactly what the atomic would; hot keys then
+      // cost plain cached loads instead of serialised atomics
+      const std::uint64_t seen = *reinterpret_cast<volatile const std::uint64_t*>(tkeys + idx);
+      if (seen == cur) break;
+      if (seen < cur) {
+        idx = (idx + 1) & (cap - 1);
+        if (probes > cap) {
+          raise_error(err, 4, cur);
+          break;
+        }
+        continue;
+      }
       const std::uint64_t old = atomicMin(reinterpret_cast<unsigned long long*>(tkeys + idx),
                                           static_cast<unsigned long long>(cur));
       if (old == kEmptyKey || old == cur) break;  // placed / already present
@@ -137,142 +160,166 @@ __global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys
   }
 }
 
-// Row fill over the table's slots (hbm_ps.hpp:86-98): carry-over from the
-// previous table, else the attached value store, else zeros.
-template <int VEC>
-__global__ void table_fill_slots_kernel(const std::uint64_t* __restrict__ keys,
-                                        float* __restrict__ vals,
-                                        const std::uint64_t* __restrict__ cap_ptr,
-                                        const std::uint64_t* __restrict__ prev_keys,
-                                        const float* __restrict__ prev_vals,
-                                        const std::uint64_t* __restrict__ prev_cap_ptr,
-                                        const float* __restrict__ store,
-                                        std::uint64_t store_keys, int E,
-                                        unsigned long long* carried) {
-  const int tpk = E / VEC;
-  const std::uint64_t cap = *cap_ptr;
-  const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
-  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
-       t < cap * std::uint64_t(tpk); t += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint64_t slot = t / tpk;
-    const int part = int(t - slot * tpk);
-    const std::uint64_t key = keys[slot];
-    const bool live = key != kEmptyKey;
-    const float* src = nullptr;
-    if (live && pcap) {
-      const std::uint32_t ps = probe_slot(prev_keys, pcap, key);
-      if (ps != kNoSlot) src = prev_vals + std::uint64_t(ps) * E;
-    }
-    if (carried) {
-      const unsigned hit = __ballot_sync(__activemask(), src != nullptr && part == 0);
-      if (hit && (threadIdx.x & 31) == unsigned(__ffs(__activemask()) - 1))
-        atomicAdd(carried, (unsigned long long)__popc(hit));
-    }
-    if (!live) continue;
-    if (!src && store && key < store_keys) src = store + key * std::uint64_t(E);
-    float* dst = vals + slot * E + part * VEC;
-    if (VEC == 4) {
-      st_f4(dst, src ? ld_f4(src + part * 4) : make_float4(0.f, 0.f, 0.f, 0.f));
-    } else {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) dst[v] = src ? src[part * VEC + v] : 0.0f;
-    }
-  }
-}
-
-// Write-back of every live row to the value store, over the slots.
-template <int VEC>
-__global__ void table_writeback_slots_kernel(const std::uint64_t* __restrict__ keys,
-                                             const float* __restrict__ vals,
-                                             const std::uint64_t* __restrict__ cap_ptr,
-                                             float* __restrict__ store, std::uint64_t store_keys,
-                                             int E) {
-  const int tpk = E / VEC;
-  const std::uint64_t cap = *cap_ptr;
-  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
-       t < cap * std::uint64_t(tpk); t += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint64_t slot = t / tpk;
-    const int part = int(t - slot * tpk);
-    const std::uint64_t key = keys[slot];
-    if (key == kEmptyKey || key >= store_keys) continue;
-    const float* src = vals + slot * E + part * VEC;
-    if (VEC == 4) {
-      st_f4(store + key * E + part * 4, ld_f4(src));
-    } else {
-#pragma unroll
-      for (int q = 0; q < VEC; ++q) store[key * E + part * VEC + q] = src[q];
-    }
-  }
-}
-
-// Row fill in ascending key order with known slots (ws[i], wslot[i]): the
-// value-store accesses run through adjacent rows, which keeps zero-copy
-// PCIe reads of a host-resident store efficient.
-template <int VEC>
-__global__ void table_fill_sorted_kernel(const std::uint64_t* __restrict__ ws,
-                                         const std::uint32_t* __restrict__ wslot,
-                                         const std::uint64_t* __restrict__ n_ptr,
-                                         float* __restrict__ vals,
-                                         const std::uint64_t* __restrict__ prev_keys,
-                                         const float* __restrict__ prev_vals,
-                                         const std::uint64_t* __restrict__ prev_cap_ptr,
-                                         const float* __restrict__ store,
-                                         std::uint64_t store_keys, int E,
-                                         unsigned long long* carried) {
-  const int tpk = E / VEC;
+// Pipelined build, prep half (runs beside the previous batch's body), in two
+// kernels so that PCIe latency never sits behind HBM probes:
+// table_prefetch_probe_kernel (full grid, HBM only), one thread per
+// working-set entry i (sorted key ws[i], slot wslot[i] in the fresh table):
+// csrc[i] = the key's slot in the previous table (copied by
+// table_carry_kernel once the previous batch is done, hbm_ps.hpp:86-98), else
+// the row comes from the table two builds back when that holds the key (its
+// final rows are exactly what its write-back puts into the store, and the
+// previous batch never touched the key), else the key joins the store list
+// (warp-contiguous, so in key order within a warp), else the row is zeros.
+__global__ void table_prefetch_probe_kernel(
+    const std::uint64_t* __restrict__ ws, const std::uint32_t* __restrict__ wslot,
+    const std::uint64_t* __restrict__ n_ptr, float* __restrict__ vals,
+    std::uint32_t* __restrict__ csrc, const std::uint64_t* __restrict__ prev_keys,
+    const std::uint64_t* __restrict__ prev_cap_ptr, const std::uint64_t* __restrict__ old_keys,
+    const float* __restrict__ old_vals, const std::uint64_t* __restrict__ old_cap_ptr,
+    bool from_store, std::uint64_t store_keys, int E, std::uint64_t* __restrict__ need_key,
+    std::uint32_t* __restrict__ need_slot, unsigned long long* __restrict__ n_need,
+    unsigned long long* carried) {
   const std::uint64_t n = *n_ptr;
   const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
+  const std::uint64_t ocap = old_cap_ptr ? *old_cap_ptr : 0;
+  const unsigned lane = threadIdx.x & 31;
+  unsigned long long n_car = 0;
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  // warp-uniform trip count (the ballots below need the whole warp)
+  for (std::uint64_t base = blockIdx.x * std::uint64_t(blockDim.x) + (threadIdx.x & ~31u);
+       base < n; base += stride) {
+    const std::uint64_t i = base + lane;
+    const bool live = i < n;
+    const std::uint64_t key = live ? ws[i] : 0;
+    const std::uint32_t slot = live ? wslot[i] : 0;
+    std::uint32_t ps = kNoSlot;
+    if (live && pcap) ps = probe_slot(prev_keys, pcap, key);
+    if (live) csrc[i] = ps;
+    bool need = false;
+    if (live && ps == kNoSlot) {
+      const std::uint32_t os = ocap ? probe_slot(old_keys, ocap, key) : kNoSlot;
+      float* dst = vals + std::uint64_t(slot) * E;
+      if (os != kNoSlot) {
+        const float* src = old_vals + std::uint64_t(os) * E;
+        for (int d = 0; d < E; ++d) dst[d] = src[d];
+      } else if (from_store && key < store_keys) {
+        need = true;
+      } else {
+        for (int d = 0; d < E; ++d) dst[d] = 0.0f;
+      }
+    }
+    n_car += (live && ps != kNoSlot);
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, need);
+    if (m) {
+      unsigned long long at = 0;
+      if (lane == 0) at = atomicAdd(n_need, (unsigned long long)__popc(m));
+      at = __shfl_sync(0xFFFFFFFFu, at, 0);
+      if (need) {
+        const unsigned r = __popc(m & ((1u << lane) - 1u));
+        need_key[at + r] = key;
+        need_slot[at + r] = slot;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) n_car += __shfl_xor_sync(0xFFFFFFFFu, n_car, o);
+  if (lane == 0 && n_car) atomicAdd(carried, n_car);
+}
+
+// The store rows of the list: a streaming gather (zero-copy over PCIe for a
+// host store), ILP independent loads per thread before their stores so a few
+// CTAs keep the link busy.
+template <int VEC, int ILP>
+__global__ void store_gather_kernel(const std::uint64_t* __restrict__ need_key,
+                                    const std::uint32_t* __restrict__ need_slot,
+                                    const unsigned long long* __restrict__ n_need,
+                                    const float* __restrict__ store, float* __restrict__ vals,
+                                    int E) {
+  using V = typename std::conditional<VEC == 4, float4, float>::type;
+  const int tpk = E / VEC;
+  const std::uint64_t total = std::uint64_t(*n_need) * tpk;
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  for (std::uint64_t t0 = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t0 < total;
+       t0 += stride * ILP) {
+    V v[ILP];
+    std::uint64_t dst[ILP];
+#pragma unroll
+    for (int u = 0; u < ILP; ++u) {
+      const std::uint64_t t = t0 + u * stride;
+      if (t < total) {
+        const std::uint64_t i = t / tpk;
+        const int part = int(t - i * tpk);
+        v[u] = reinterpret_cast<const V*>(store + need_key[i] * E)[part];
+        dst[u] = std::uint64_t(need_slot[i]) * E + std::uint64_t(part) * VEC;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < ILP; ++u)
+      if (t0 + u * stride < total) *reinterpret_cast<V*>(vals + dst[u]) = v[u];
+  }
+}
+
+// Pipelined build, body half: the carried rows, after the previous batch.
+template <int VEC>
+__global__ void table_carry_kernel(const std::uint32_t* __restrict__ csrc,
+                                   const std::uint32_t* __restrict__ wslot,
+                                   const std::uint64_t* __restrict__ n_ptr,
+                                   const float* __restrict__ prev_vals, float* __restrict__ vals,
+                                   int E) {
+  const int tpk = E / VEC;
+  const std::uint64_t n = *n_ptr;
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        t < n * std::uint64_t(tpk); t += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint64_t i = t / tpk;
+    const std::uint32_t ps = csrc[i];
+    if (ps == kNoSlot) continue;
     const int part = int(t - i * tpk);
-    const std::uint64_t key = ws[i];
-    const float* src = nullptr;
-    if (pcap) {
-      const std::uint32_t ps = probe_slot(prev_keys, pcap, key);
-      if (ps != kNoSlot) src = prev_vals + std::uint64_t(ps) * E;
-    }
-    if (carried) {
-      const unsigned hit = __ballot_sync(__activemask(), src != nullptr && part == 0);
-      if (hit && (threadIdx.x & 31) == unsigned(__ffs(__activemask()) - 1))
-        atomicAdd(carried, (unsigned long long)__popc(hit));
-    }
-    if (!src && store && key < store_keys) src = store + key * std::uint64_t(E);
+    const float* src = prev_vals + std::uint64_t(ps) * E + part * VEC;
     float* dst = vals + std::uint64_t(wslot[i]) * E + part * VEC;
     if (VEC == 4) {
-      st_f4(dst, src ? ld_f4(src + part * 4) : make_float4(0.f, 0.f, 0.f, 0.f));
+      st_f4(dst, ld_f4(src));
     } else {
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) dst[v] = src ? src[part * VEC + v] : 0.0f;
+      for (int v = 0; v < VEC; ++v) dst[v] = src[v];
     }
   }
 }
 
-// Write-back in ascending key order with known slots.
-template <int VEC>
+
+// Write-back in ascending key order with known slots; ILP independent row
+// loads per thread before their (posted, zero-copy for a host store) stores.
+template <int VEC, int ILP>
 __global__ void table_writeback_sorted_kernel(const std::uint64_t* __restrict__ ws,
                                               const std::uint32_t* __restrict__ wslot,
                                               const std::uint64_t* __restrict__ n_ptr,
                                               const float* __restrict__ vals,
                                               float* __restrict__ store, std::uint64_t store_keys,
                                               int E) {
+  using V = typename std::conditional<VEC == 4, float4, float>::type;
   const int tpk = E / VEC;
-  const std::uint64_t n = *n_ptr;
-  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
-       t < n * std::uint64_t(tpk); t += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint64_t i = t / tpk;
-    const int part = int(t - i * tpk);
-    const std::uint64_t key = ws[i];
-    if (key >= store_keys) continue;
-    const float* src = vals + std::uint64_t(wslot[i]) * E + part * VEC;
-    if (VEC == 4) {
-      st_f4(store + key * E + part * 4, ld_f4(src));
-    } else {
+  const std::uint64_t total = *n_ptr * std::uint64_t(tpk);
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  for (std::uint64_t t0 = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t0 < total;
+       t0 += stride * ILP) {
+    V v[ILP];
+    std::uint64_t key[ILP];
 #pragma unroll
-      for (int q = 0; q < VEC; ++q) store[key * E + part * VEC + q] = src[q];
+    for (int u = 0; u < ILP; ++u) {
+      const std::uint64_t t = t0 + u * stride;
+      key[u] = ~std::uint64_t(0);
+      if (t < total) {
+        const std::uint64_t i = t / tpk;
+        const int part = int(t - i * tpk);
+        key[u] = ws[i] * E + std::uint64_t(part) * VEC;
+        if (ws[i] >= store_keys) key[u] = ~std::uint64_t(0);
+        v[u] = reinterpret_cast<const V*>(vals + std::uint64_t(wslot[i]) * E)[part];
+      }
     }
+#pragma unroll
+    for (int u = 0; u < ILP; ++u)
+      if (key[u] != ~std::uint64_t(0)) *reinterpret_cast<V*>(store + key[u]) = v[u];
   }
 }
+
 
 // Row fill for the fresh table (hbm_ps.hpp:86-98): carry-over from the
 // previous table when the key was resident, else the staged host row

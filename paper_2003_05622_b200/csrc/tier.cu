@@ -20,7 +20,10 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <string>
 #include <vector>
@@ -96,13 +99,17 @@ static NcclApi& nccl() {
 
 // --------------------------------------------------------- the tier ----
 
+constexpr int kTables = 3;  // current, previous (carry-over), the one before (store proxy)
+constexpr int kSlots = 3;   // staging slots = batches in flight
+
 struct Scalars {
   std::uint64_t n_ws;          // working-set size of the current build
-  std::uint64_t cap[2];        // capacity of table 0 / 1
-  std::uint64_t nws_tab[2];    // occupancy of table 0 / 1
+  std::uint64_t cap[kTables];      // capacity of each table
+  std::uint64_t nws_tab[kTables];  // occupancy of each table
+  unsigned long long carried_tab[kTables];  // rows carried over when the table was built
+  unsigned long long stored_tab[kTables];   // rows read from the value store for it
   std::uint64_t U;             // unique keys of the current mini-batch / pull
-  std::uint64_t total;         // scratch total of a tile scan
-  std::uint64_t counts[66];    // batch_count: per-mb occurrences, owned keys
+  std::uint64_t counts[kSlots][66]; // batch_count per staging slot: per-mb occurrences, owned keys
   double loss;
   unsigned long long pulled;   // sum over mini-batches of unique keys pulled
   unsigned long long carried;  // rows filled from the previous table
@@ -111,8 +118,8 @@ struct Scalars {
   unsigned long long n_items;  // their (key, chunk) work items
   int err_any;                 // error code max-reduced over ranks
   unsigned long long epoch;    // P2P exchange round (parity selects the windows)
-  std::uint32_t lb_context;    // look-back context counter (sort.cuh)
-  std::uint32_t pad0;
+  std::uint32_t pad0, pad1;
+  std::int64_t total_unused;   // host side: offsets[B] of a device batch
   unsigned long long fallbacks;  // certified sums that needed the exact chain
   unsigned long long served;     // keys this rank served as owner (G > 1)
   DevError err;
@@ -124,12 +131,56 @@ struct BatchShape {
   std::uint64_t mb_bound[64] = {};
 };
 
+// Which buffers one in-flight batch uses (hps_submit_batch).
+struct BatchPlan {
+  std::uint64_t id = 0;  // submission index
+  std::uint64_t B = 0;
+  int sp = 0;         // staging slot (double-buffered batch + counts)
+  int tb = 0;         // its table
+  int tp = -1;        // previous table (carry-over), -1 = none
+  int tq = -1;        // table two builds back, usable as a store proxy, -1 = none
+  std::int64_t step = 0;
+  std::uint64_t occ_total = 0;
+  int skip_mb = -1;
+};
+
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   std::uint64_t launches = 0;
-  std::vector<int> ev_phase;
-  int cur_after = -1;
-  bool prev_after = false;
+  std::uint64_t epochs = 0;  // exchange rounds the body opens (host mirror)
+  std::vector<int> ev_phase, ev_lane;
+};
+
+// A stream with its own sort / scan scratch and look-back state, so the
+// build of batch b+1 (prep lane) and the body of batch b (main lane) can run
+// concurrently.
+struct LaneDev {
+  std::uint64_t total;      // scratch total of a tile scan
+  std::uint32_t context;    // look-back context counter (sort.cuh)
+  std::uint32_t pad;
+};
+struct Lane {
+  cudaStream_t st = nullptr;
+  std::uint64_t *kA = nullptr, *kB = nullptr;
+  std::uint32_t *vA = nullptr, *vB = nullptr;
+  std::uint32_t* ghist = nullptr;          // [kMaxPasses][256] digit bases
+  std::uint64_t* status = nullptr;         // look-back status words
+  unsigned long long* ticket = nullptr;    // look-back tile tickets
+  LaneDev* d = nullptr;
+  std::uint64_t tickets = 0;               // tickets handed out in this context
+  std::uint32_t lb_local = 0;              // launches in this context
+  std::uint64_t lb_contexts = 0;           // contexts opened (host mirror)
+  std::uint64_t status_words = 0;
+};
+
+// Per-batch results read back at hps_wait_batch (pinned).
+struct BatchOut {
+  double loss;
+  unsigned long long pulled;
+  unsigned long long fallbacks, served;
+  unsigned long long carried, stored;
+  std::uint64_t n_ws, cap;
+  DevError err;
 };
 
 struct PendingChunk {
@@ -143,9 +194,33 @@ struct Tier {
   hps_config cfg{};
   int N = 1, D = 1, G = 1, g = 0, E = 1, J = 1;
   ModelDims md{};
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr;            // == lane[0].st: bodies and the parity API
   cudaStream_t st2 = nullptr;           // side stream: dense-grad overlaps sparse reduce
   cudaEvent_t fork = nullptr, join = nullptr;
+  Lane lane[2];                         // 0: main (body), 1: prep (build of the next batch)
+  Lane* L = &lane[0];                   // the lane launch() enqueues on
+  // The batch pipeline (the reference's 4-stage pipeline, pipeline.hpp:230-
+  // 500, as streams): stage (H2D + counts, st_stage) -> prep (working set,
+  // table build, store prefetch; lane 1) -> body (carry + J mini-batches;
+  // lane 0) -> write-back (st_wb, the collect stage, pipeline.hpp:462-474).
+  // Batch b+1 is staged and prepared while batch b trains; b's write-back
+  // overlaps b+1.
+  cudaStream_t st_stage = nullptr, st_wb = nullptr;
+  cudaEvent_t ev_staged = nullptr, ev_prep = nullptr;
+  cudaEvent_t ev_body_tab[kTables] = {}, ev_body_sp[kSlots] = {}, ev_wb[kTables] = {};
+  cudaEvent_t ev_wbt[kTables][2] = {};  // write-back timing pairs
+  bool body_pending[kTables] = {}, sp_pending[kSlots] = {}, wb_pending[kTables] = {},
+       wb_timed[kTables] = {};
+  bool tab_wb[kTables] = {};            // table's final rows go to the current store
+  std::deque<BatchPlan> inflight;       // submitted, not yet completed (<= kSlots)
+  struct Done {
+    std::uint64_t id;
+    hps_status st;
+    std::string msg;
+    hps_batch_stats stats;
+  };
+  std::deque<Done> done;                // completed, not yet returned
+  std::uint64_t submitted = 0;
   ncclComm_t comm = nullptr;
   std::uint64_t Bmax = 0, Omax = 0, Wmax = 0, capmax = 0, nmb_max = 0;
   int sort_bits = 64;
@@ -155,34 +230,27 @@ struct Tier {
   Scalars* dsc = nullptr;  // device
   Scalars* hsc = nullptr;  // pinned host mirror
 
-  // tables (double-buffered: current + previous for carry-over)
-  std::uint64_t* tkeys[2] = {nullptr, nullptr};
-  float* tvals[2] = {nullptr, nullptr};
-  int cur = -1;
-  bool has_prev = false;
+  // tables (triple-buffered: current, previous for carry-over, and the one
+  // before, whose rows stand in for the store while its write-back drains)
+  std::uint64_t* tkeys[kTables] = {};
+  float* tvals[kTables] = {};
+  int cur = -1, prev = -1;
 
   // working set
   std::uint64_t* ws = nullptr;       // sorted keys of the current table (when ws_sorted)
-  std::uint32_t* ws_idx = nullptr;
+  std::uint32_t* ws_idx = nullptr;   // (ws / ws_idx point into wsb / wsib of the table)
+  std::uint64_t* wsb[kTables] = {};
+  std::uint32_t* wsib[kTables] = {};
+  std::uint32_t* csrc[kTables] = {};  // carry source slot per working-set entry
   bool ws_sorted = true;
   std::uint64_t* wsset = nullptr;    // scratch hash set of the sort-free build
   std::uint64_t wsset_cap = 0;
 
-  // sort scratch
-  std::uint64_t *kA = nullptr, *kB = nullptr;
-  std::uint32_t *vA = nullptr, *vB = nullptr;
-  std::uint32_t* ghist = nullptr;          // [kMaxPasses][256] digit bases
-  std::uint64_t* status = nullptr;         // look-back status words
-  unsigned long long* ticket = nullptr;    // look-back tile tickets
-  std::uint64_t tickets = 0;               // tickets handed out in this context
-  std::uint32_t lb_local = 0;              // launches in this context
-  std::uint64_t lb_contexts = 0;           // contexts opened (host mirror)
-  std::uint64_t status_words = 0;
-
-  // batch staging
-  std::int64_t* b_off = nullptr;
-  std::uint64_t* b_keys = nullptr;
-  std::uint8_t* b_lab = nullptr;
+  // batch staging (double-buffered)
+  std::int64_t* b_off[kSlots] = {};
+  std::uint64_t* b_keys[kSlots] = {};
+  std::uint8_t* b_lab[kSlots] = {};
+  BatchOut* hout = nullptr;          // pinned, [kSlots] by staging slot
 
   // mini-batch / pull buffers (sized Omax)
   std::uint32_t *occ_off = nullptr, *ex_of = nullptr, *inv = nullptr,
@@ -207,6 +275,20 @@ struct Tier {
   // value store (MEM-PS stand-in)
   float* store = nullptr;
   std::uint64_t store_keys = 0;
+  bool store_on_host = false;
+  // zero-copy kernels on a host store run on a few SMs only: a PCIe access
+  // stalls the memory pipeline of the SM issuing it for everyone on that SM
+  unsigned pf_ctas = 8, wb_ctas = 4;
+  // HPS_TRACE=1: timed events at the pipeline's stage boundaries, printed
+  // per batch to stderr at completion (diagnostics)
+  bool trace = false;
+  bool priorities = true;
+  int zc_threads = 1024;  // CTA size of the zero-copy kernels
+  cudaEvent_t tr_base = nullptr;
+  cudaEvent_t tr[kSlots][6] = {};   // by staging slot: stage0 stage1 prep0 prep1 body0 body1
+  cudaEvent_t trw[4][2] = {};  // write-back start/end by batch id % 4
+  std::uint64_t* need_key = nullptr;   // store rows of the build in flight
+  std::uint32_t* need_slot = nullptr;
   bool store_registered = false;
   float* store_host = nullptr;
 
@@ -231,10 +313,10 @@ struct Tier {
   void* win_base = nullptr;
   std::vector<void*> ipc_opened;
 
-  // timing: events recorded at phase boundaries on the tier stream
+  // timing: events recorded at phase boundaries on the lanes' streams
   bool timing = false;
   std::vector<cudaEvent_t> evpool;
-  std::vector<int> ev_phase;
+  std::vector<int> ev_phase, ev_lane;  // lane: 0 main, 1 prep, 2 stage
   double acc_ms[HPS_TIMING_SLOTS] = {0};
 
   std::vector<void*> allocs;
@@ -290,7 +372,7 @@ static unsigned grid_for(std::uint64_t work, int threads = 256,
 template <class... KArgs, class... Args>
 static void launch(Tier* t, void (*k)(KArgs...), dim3 grid, dim3 block,
                    size_t smem, Args&&... args) {
-  k<<<grid, block, smem, t->st>>>(std::forward<Args>(args)...);
+  k<<<grid, block, smem, t->L->st>>>(std::forward<Args>(args)...);
   ++t->launches;
 }
 
@@ -306,27 +388,35 @@ static void launch_on(Tier* t, cudaStream_t s, void (*k)(KArgs...), dim3 grid, d
 // collective = true (calls every rank makes in lockstep) the error code is
 // max-reduced over ranks first, so an owner-side failure (e.g. a missing key
 // requested by a peer) makes every rank raise instead of diverging.
+static hps_status device_error_status(Tier* t, const DevError& e, const char* missing_ctx);
+
 static hps_status check_device_error(Tier* t, const char* missing_ctx,
-                                     bool collective = false) {
+                                     bool collective = false, cudaStream_t s = nullptr) {
+  if (!s) s = t->st;
   if (collective && t->G > 1) {
     HPS_CUDA(cudaMemcpyAsync(&t->dsc->err_any, &t->dsc->err.code, sizeof(int),
-                             cudaMemcpyDeviceToDevice, t->st));
+                             cudaMemcpyDeviceToDevice, s));
     ncclResult_t r = nccl().AllReduce(&t->dsc->err_any, &t->dsc->err_any, 1, ncclInt32, ncclMax,
-                                      t->comm, t->st);
+                                      t->comm, s);
     if (r != ncclSuccess)
       return set_error(HPS_ERR_NCCL, "nccl: %s", nccl().GetErrorString(r));
     HPS_CUDA(cudaMemcpyAsync(&t->hsc->err_any, &t->dsc->err_any, sizeof(int),
-                             cudaMemcpyDeviceToHost, t->st));
+                             cudaMemcpyDeviceToHost, s));
   }
   HPS_CUDA(cudaMemcpyAsync(&t->hsc->err, &t->dsc->err, sizeof(DevError),
-                           cudaMemcpyDeviceToHost, t->st));
-  HPS_CUDA(cudaStreamSynchronize(t->st));
+                           cudaMemcpyDeviceToHost, s));
+  HPS_CUDA(cudaStreamSynchronize(s));
   const DevError e = t->hsc->err;
   if (e.code == 0 && collective && t->G > 1 && t->hsc->err_any != 0)
     return set_error(hps_status(t->hsc->err_any),
                      "hbm: a peer rank failed this collective (status %d)", t->hsc->err_any);
   if (e.code == 0) return HPS_OK;
-  HPS_CUDA(cudaMemsetAsync(&t->dsc->err, 0, sizeof(DevError), t->st));
+  HPS_CUDA(cudaMemsetAsync(&t->dsc->err, 0, sizeof(DevError), s));
+  return device_error_status(t, e, missing_ctx);
+}
+
+static hps_status device_error_status(Tier* t, const DevError& e, const char* missing_ctx) {
+  if (e.code == 0) return HPS_OK;
   const unsigned long long k = e.key;
   switch (e.code) {
     case HPS_ERR_MISSING_KEY:
@@ -538,17 +628,19 @@ __global__ void context_open_kernel(std::uint32_t* context, unsigned long long* 
 // resets the device ticket counter and advances the device context counter,
 // so the launches that follow bake only context-relative values.
 static void open_lookback_context(Tier* t) {
-  if ((t->lb_contexts + 1) % (1u << 20) == 0)  // before the 20-bit wrap
-    cudaMemsetAsync(t->status, 0, t->status_words * 8, t->st);
-  ++t->lb_contexts;
-  launch(t, context_open_kernel, 1, 1, 0, &t->dsc->lb_context, t->ticket);
-  t->tickets = 0;
-  t->lb_local = 0;
+  Lane& l = *t->L;
+  if ((l.lb_contexts + 1) % (1u << 20) == 0)  // before the 20-bit wrap
+    cudaMemsetAsync(l.status, 0, l.status_words * 8, l.st);
+  ++l.lb_contexts;
+  launch(t, context_open_kernel, 1, 1, 0, &l.d->context, l.ticket);
+  l.tickets = 0;
+  l.lb_local = 0;
 }
 
 static LookBack next_lookback(Tier* t, std::uint32_t grid) {
-  LookBack lb{t->ticket, t->tickets, ++t->lb_local, t->status, &t->dsc->lb_context};
-  t->tickets += grid;
+  Lane& l = *t->L;
+  LookBack lb{l.ticket, l.tickets, ++l.lb_local, l.status, &l.d->context};
+  l.tickets += grid;
   return lb;
 }
 
@@ -565,11 +657,11 @@ static void tile_scan(Tier* t, F f, Em em, Count n, std::uint64_t n_upper,
 static void sort_histogram(Tier* t, const std::uint64_t* kin, Count n, std::uint64_t n_upper,
                            int passes, std::uint32_t mod_G) {
   const int np = passes ? passes : 1;
-  cudaMemsetAsync(t->ghist, 0, std::size_t(np) * kDigits * 4, t->st);
+  cudaMemsetAsync(t->L->ghist, 0, std::size_t(np) * kDigits * 4, t->L->st);
   const unsigned hb = unsigned(std::max<std::uint64_t>(
       1, std::min<std::uint64_t>((n_upper + kSortThreads - 1) / kSortThreads, kSMs * 4)));
-  launch(t, onesweep_hist_kernel, hb, kSortThreads, 0, kin, n, passes, mod_G, t->ghist);
-  launch(t, onesweep_scan_kernel, np, kDigits, 0, t->ghist);
+  launch(t, onesweep_hist_kernel, hb, kSortThreads, 0, kin, n, passes, mod_G, t->L->ghist);
+  launch(t, onesweep_scan_kernel, np, kDigits, 0, t->L->ghist);
 }
 
 // Stable LSD sort of n (<= n_upper) items over the low `bits` bits. Input
@@ -582,11 +674,12 @@ static void radix_sort(Tier* t, const std::uint64_t* kin, const std::uint32_t* v
   sort_histogram(t, kin, n, n_upper, passes, 0);
   const std::uint64_t* ksrc = kin;
   const std::uint32_t* vsrc = vin;
-  std::uint64_t* kd = t->kA;
-  std::uint32_t* vd = t->vA;
+  Lane& l = *t->L;
+  std::uint64_t* kd = l.kA;
+  std::uint32_t* vd = l.vA;
   for (int p = 0; p < passes; ++p) {
     const ShiftDigit dig{8 * p};
-    const std::uint32_t* db = t->ghist + p * kDigits;
+    const std::uint32_t* db = l.ghist + p * kDigits;
     if (values)
       launch(t, onesweep_pass_kernel<ShiftDigit, true>, nb, kSortThreads, 0, ksrc, vsrc, n, dig,
              db, next_lookback(t, nb), kd, vd);
@@ -595,8 +688,8 @@ static void radix_sort(Tier* t, const std::uint64_t* kin, const std::uint32_t* v
              db, next_lookback(t, nb), kd, vd);
     ksrc = kd;
     vsrc = vd;
-    kd = (kd == t->kA) ? t->kB : t->kA;
-    vd = (vd == t->vA) ? t->vB : t->vA;
+    kd = (kd == l.kA) ? l.kB : l.kA;
+    vd = (vd == l.vA) ? l.vB : l.vA;
   }
   *kout = const_cast<std::uint64_t*>(ksrc);
   *vout = const_cast<std::uint32_t*>(vsrc);
@@ -638,27 +731,48 @@ static void mark(Tier* t, int phase) {
     cudaEventCreate(&e);
     t->evpool.push_back(e);
   }
+  const int lane = t->L == &t->lane[1] ? 1 : 0;
+  cudaStream_t s = t->L->st;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(t->st, &cs);
+  cudaStreamIsCapturing(s, &cs);
   // inside a capture the record must become an external event node
-  cudaEventRecordWithFlags(t->evpool[i], t->st,
+  cudaEventRecordWithFlags(t->evpool[i], s,
                            cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0);
   t->ev_phase.push_back(phase);
+  t->ev_lane.push_back(lane);
+}
+
+// A phase boundary on the staging stream (lane 2).
+static void mark_stage(Tier* t, int phase) {
+  if (!t->timing) return;
+  Lane* l = t->L;
+  Lane tmp;
+  tmp.st = t->st_stage;
+  t->L = &tmp;
+  mark(t, phase);
+  t->L = l;
+  t->ev_lane.back() = 2;
 }
 
 static void timing_begin(Tier* t) {
   t->ev_phase.clear();
-  mark(t, -1);
+  t->ev_lane.clear();
 }
 
-// After the stream is idle: fold the recorded phases into acc_ms.
+// After the batch is done: fold the recorded phases into acc_ms. A phase is
+// the time between consecutive marks of the same lane; TOTAL spans the first
+// mark to the last.
 static void timing_end(Tier* t) {
   if (!t->timing || t->ev_phase.size() < 2) return;
-  for (std::size_t i = 1; i < t->ev_phase.size(); ++i) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, t->evpool[i - 1], t->evpool[i]);
-    const int p = t->ev_phase[i];
-    if (p > 0 && p < HPS_TIMING_SLOTS) t->acc_ms[p] += ms;
+  int last[3] = {-1, -1, -1};
+  for (std::size_t i = 0; i < t->ev_phase.size(); ++i) {
+    const int ln = t->ev_lane[i], p = t->ev_phase[i];
+    if (last[ln] >= 0 && p > 0 && p < HPS_TIMING_SLOTS) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, t->evpool[last[ln]], t->evpool[i]);
+      t->acc_ms[p] += ms;
+    }
+    last[ln] = int(i);
   }
   float tot = 0;
   cudaEventElapsedTime(&tot, t->evpool[0], t->evpool[t->ev_phase.size() - 1]);
@@ -669,9 +783,11 @@ static void timing_end(Tier* t) {
 
 // Build the fresh table from the working set in t->ws (count in dsc->n_ws,
 // at most n_upper). staged_idx/rows: optional HostValue rows.
+static int next_table(const Tier* t) { return t->cur < 0 ? 0 : (t->cur + 1) % kTables; }
+
 static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* staged_idx,
                         const float* staged_rows) {
-  const int nxt = (t->cur < 0) ? 0 : 1 - t->cur;
+  const int nxt = next_table(t);
   const int prv = t->cur;
   launch(t, table_capacity_kernel, 1, 1, 0, (const std::uint64_t*)&t->dsc->n_ws,
          &t->dsc->cap[nxt]);
@@ -698,8 +814,9 @@ static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* sta
            staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->E,
            &t->dsc->carried, &t->dsc->err);
   cudaMemcpyAsync(&t->dsc->nws_tab[nxt], &t->dsc->n_ws, 8, cudaMemcpyDeviceToDevice, t->st);
-  t->has_prev = prv >= 0;
+  t->prev = prv;
   t->cur = nxt;
+  t->tab_wb[nxt] = false;  // not a train-batch table: never a store proxy
 }
 
 // ------------------------------------------------- dedup + pull (core) --
@@ -974,72 +1091,100 @@ inline std::uint64_t shape_bound(std::uint64_t x) {
   return p;
 }
 
-// Everything of hps_train_batch after the count round-trip. Enqueue-only (no
-// host synchronisation, no host-read device values, round counter on the
-// device), so it can be captured into a CUDA graph and replayed. skip_mb:
-// mini-batch of this batch whose dense sync+update is skipped, -1 = none.
-static hps_status enqueue_batch_body(Tier* T, const BatchShape& sh, int skip_mb) {
+// Prep of one batch (lane 1, beside the previous batch's body): the sort-free
+// build of its table. Exact distinct count through a scratch set (it fixes
+// the capacity, hence the layout), ordered probing of the raw owned
+// occurrences (duplicates stop on their own key; ordered probing is
+// history-independent, so the layout equals ascending insertion,
+// hbm_ps.hpp:69-98), the distinct keys with their slots in ascending key
+// order (compact + sort), then every row that is not a carry-over: from the
+// table two builds back when it holds the key, else the value store.
+// Enqueue-only (capturable).
+static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& bp) {
+  const int G = T->G, E = T->E, tb = bp.tb;
+  Lane& l = *T->L;
+  const std::uint64_t* dkeys = T->b_keys[bp.sp];
+  const std::int64_t* o_ptr = T->b_off[bp.sp] + sh.B;
+  std::uint64_t* nws = &T->dsc->nws_tab[tb];
+  std::uint64_t* cap = &T->dsc->cap[tb];
+  mark(T, -1);
+  std::uint64_t setcap = 1;
+  while (setcap < 2 * sh.own_bound) setcap <<= 1;
+  setcap = std::min(setcap, T->wsset_cap);
+  HPS_CUDA(cudaMemsetAsync(T->wsset, 0xFF, setcap * 8, l.st));
+  HPS_CUDA(cudaMemsetAsync(nws, 0, 8, l.st));
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->carried_tab[tb], 0, 8, l.st));
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->stored_tab[tb], 0, 8, l.st));
+  const unsigned gk = grid_for(sh.batch_bound, 256, kSMs * 8);
+  launch(T, ws_count_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G), std::uint64_t(T->g),
+         T->wsset, setcap - 1, (unsigned long long*)nws);
+  launch(T, table_capacity_kernel, 1, 1, 0, (const std::uint64_t*)nws, cap);
+  const std::uint64_t cap_bound = table_capacity(sh.own_bound);
+  launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[tb],
+         (const std::uint64_t*)cap);
+  launch(T, table_insert_dedup_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G),
+         std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap, &T->dsc->err);
+  // the distinct keys with their slots, ascending: compact the live slots,
+  // sort them (n_ws items, ~3x fewer than the occurrences)
+  tile_scan(T, LiveSlot{T->tkeys[tb]}, CompactEmit{T->tkeys[tb], nullptr, l.kB, l.vB},
+            Count{cap, 0}, cap_bound, &l.d->total);
+  std::uint64_t* sk = nullptr;
+  std::uint32_t* so = nullptr;
+  radix_sort(T, l.kB, l.vB, Count{nws, 0}, sh.own_bound, T->sort_bits, true, &sk, &so);
+  const std::uint64_t wcopy = std::min(sh.own_bound, T->Wmax);  // bound, within the buffers
+  HPS_CUDA(cudaMemcpyAsync(T->wsb[tb], sk, wcopy * 8, cudaMemcpyDeviceToDevice, l.st));
+  HPS_CUDA(cudaMemcpyAsync(T->wsib[tb], so, wcopy * 4, cudaMemcpyDeviceToDevice, l.st));
+  // rows: carry flags + table-two-back copies + the store list (HBM, full
+  // grid), then the store rows (zero-copy over PCIe for a host store: a few
+  // CTAs with independent loads in flight saturate the link, and leave the
+  // other SMs to the running body)
+  const int tp = bp.tp, tq = bp.tq;
+  const std::uint64_t* pk = tp >= 0 ? T->tkeys[tp] : nullptr;
+  const std::uint64_t* pc = tp >= 0 ? &T->dsc->cap[tp] : nullptr;
+  const std::uint64_t* qk = tq >= 0 ? T->tkeys[tq] : nullptr;
+  const float* qv = tq >= 0 ? T->tvals[tq] : nullptr;
+  const std::uint64_t* qc = tq >= 0 ? &T->dsc->cap[tq] : nullptr;
+  launch(T, table_prefetch_probe_kernel, grid_for(sh.own_bound), 256, 0,
+         (const std::uint64_t*)T->wsb[tb], (const std::uint32_t*)T->wsib[tb],
+         (const std::uint64_t*)nws, T->tvals[tb], T->csrc[tb], pk, pc, qk, qv, qc,
+         T->store != nullptr, T->store_keys, E, T->need_key, T->need_slot,
+         &T->dsc->stored_tab[tb], &T->dsc->carried_tab[tb]);
+  if (T->store) {
+    const int V = vec_of(E);
+    const std::uint64_t work = sh.own_bound * std::uint64_t(E / V);
+    const unsigned gg = T->store_on_host ? T->pf_ctas : grid_for(work, 256 * 4);
+    const int tpb = T->store_on_host ? T->zc_threads : 256;
+    auto k = V == 4 ? store_gather_kernel<4, 4> : store_gather_kernel<1, 4>;
+    launch(T, k, gg, tpb, 0, (const std::uint64_t*)T->need_key,
+           (const std::uint32_t*)T->need_slot,
+           (const unsigned long long*)&T->dsc->stored_tab[tb], (const float*)T->store,
+           T->tvals[tb], E);
+  }
+  mark(T, HPS_T_BUILD);
+  return HPS_OK;
+}
+
+// The body of one batch (lane 0): carried rows from the previous table, then
+// J x {shard gather, dedup, pull, fwd/bwd, sparse reduce, push + canonical
+// apply, dense sync + update}. Enqueue-only (no host synchronisation, no
+// host-read device values, round counter on the device), so it can be
+// captured into a CUDA graph and replayed.
+static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& bp) {
   const int G = T->G, J = T->J, E = T->E;
   const std::uint64_t B = sh.B, GJ = std::uint64_t(G) * J;
-  const std::int64_t* doff = T->b_off;
-  const std::uint64_t* dkeys = T->b_keys;
-  const std::uint8_t* dlab = T->b_lab;
-  const Count own_n{&T->dsc->counts[J], 0};
-  // (the caller opened the look-back context: ticket counter reset, device
-  // context counter advanced — eagerly, so captured graphs replay correctly)
-  // ---- working set (a1, a2) + build (a3, a4), sort-free: exact distinct
-  // count through a scratch set (it fixes the capacity), then ordered probing
-  // of the raw owned occurrences (duplicates stop on their own key), then the
-  // rows by slot scan (carry-over, else the value store)
-  {
-    const int nxt = (T->cur < 0) ? 0 : 1 - T->cur;
-    const int prv = T->cur;
-    const std::int64_t* o_ptr = doff + B;
-    std::uint64_t setcap = 1;
-    while (setcap < 2 * sh.own_bound) setcap <<= 1;
-    setcap = std::min(setcap, T->wsset_cap);
-    HPS_CUDA(cudaMemsetAsync(T->wsset, 0xFF, setcap * 8, T->st));
-    HPS_CUDA(cudaMemsetAsync(&T->dsc->n_ws, 0, 8, T->st));
-    const unsigned gk = grid_for(sh.batch_bound, 256, kSMs * 8);
-    launch(T, ws_count_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G), std::uint64_t(T->g),
-           T->wsset, setcap - 1, (unsigned long long*)&T->dsc->n_ws);
-    launch(T, table_capacity_kernel, 1, 1, 0, (const std::uint64_t*)&T->dsc->n_ws,
-           &T->dsc->cap[nxt]);
-    const std::uint64_t cap_bound = table_capacity(sh.own_bound);
-    launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[nxt],
-           (const std::uint64_t*)&T->dsc->cap[nxt]);
-    launch(T, table_insert_dedup_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G),
-           std::uint64_t(T->g), T->tkeys[nxt], (const std::uint64_t*)&T->dsc->cap[nxt],
-           &T->dsc->err);
-    // the distinct keys with their slots, ascending: compact the live slots,
-    // sort them (n_ws items, ~3x fewer than the occurrences)
-    tile_scan(T, LiveSlot{T->tkeys[nxt]}, CompactEmit{T->tkeys[nxt], nullptr, T->kB, T->vB},
-              Count{&T->dsc->cap[nxt], 0}, cap_bound, &T->dsc->total);
-    std::uint64_t* sk = nullptr;
-    std::uint32_t* so = nullptr;
-    radix_sort(T, T->kB, T->vB, Count{&T->dsc->n_ws, 0}, sh.own_bound, T->sort_bits, true, &sk,
-               &so);
-    const std::uint64_t wcopy = std::min(sh.own_bound, T->Wmax);  // bound, within the buffers
-    HPS_CUDA(cudaMemcpyAsync(T->ws, sk, wcopy * 8, cudaMemcpyDeviceToDevice, T->st));
-    HPS_CUDA(cudaMemcpyAsync(T->ws_idx, so, wcopy * 4, cudaMemcpyDeviceToDevice, T->st));
-    const std::uint64_t* pcap = (prv >= 0) ? &T->dsc->cap[prv] : nullptr;
-    const std::uint64_t* pk = (prv >= 0) ? T->tkeys[prv] : nullptr;
-    const float* pv = (prv >= 0) ? T->tvals[prv] : nullptr;
+  const std::int64_t* doff = T->b_off[bp.sp];
+  const std::uint64_t* dkeys = T->b_keys[bp.sp];
+  const std::uint8_t* dlab = T->b_lab[bp.sp];
+  mark(T, -1);
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 16, T->st));       // loss, pulled
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 16, T->st));  // fallbacks, served
+  if (bp.tp >= 0) {
     const int V = vec_of(E);
-    const unsigned gf = grid_for(sh.own_bound * std::uint64_t(E / V));
-    if (V == 4)
-      launch(T, table_fill_sorted_kernel<4>, gf, 256, 0, (const std::uint64_t*)T->ws,
-             (const std::uint32_t*)T->ws_idx, (const std::uint64_t*)&T->dsc->n_ws, T->tvals[nxt],
-             pk, pv, pcap, (const float*)T->store, T->store_keys, E, &T->dsc->carried);
-    else
-      launch(T, table_fill_sorted_kernel<1>, gf, 256, 0, (const std::uint64_t*)T->ws,
-             (const std::uint32_t*)T->ws_idx, (const std::uint64_t*)&T->dsc->n_ws, T->tvals[nxt],
-             pk, pv, pcap, (const float*)T->store, T->store_keys, E, &T->dsc->carried);
-    HPS_CUDA(cudaMemcpyAsync(&T->dsc->nws_tab[nxt], &T->dsc->n_ws, 8, cudaMemcpyDeviceToDevice,
-                             T->st));
-    T->has_prev = prv >= 0;
-    T->cur = nxt;
-    T->ws_sorted = true;
+    const unsigned gc = grid_for(sh.own_bound * std::uint64_t(E / V));
+    auto k = V == 4 ? table_carry_kernel<4> : table_carry_kernel<1>;
+    launch(T, k, gc, 256, 0, (const std::uint32_t*)T->csrc[bp.tb],
+           (const std::uint32_t*)T->wsib[bp.tb], (const std::uint64_t*)&T->dsc->nws_tab[bp.tb],
+           (const float*)T->tvals[bp.tp], T->tvals[bp.tb], E);
   }
   mark(T, HPS_T_BUILD);
   // ---- mini-batches
@@ -1047,19 +1192,19 @@ static hps_status enqueue_batch_body(Tier* T, const BatchShape& sh, int skip_mb)
   for (int j = 0; j < J; ++j) {
     const std::uint64_t s = std::uint64_t(T->g) * J + j;
     const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
-    const Count on_n{&T->dsc->counts[j], 0};
+    const Count on_n{&T->dsc->counts[bp.sp][j], 0};
     const std::uint64_t ob = sh.mb_bound[j];
     const ShardMap sm{s, GJ, n};
     // shard gather + dedup (a5)
     if (n) {
       tile_scan(T, ShardLen{sm, doff}, ShardLenEmit{T->occ_off, n}, Count{nullptr, n}, n,
-                &T->dsc->total);
+                &T->L->d->total);
       launch(T, shard_gather_kernel, grid_for(n * 32), 256, 0, sm, doff, dkeys,
-             (const std::uint32_t*)T->occ_off, T->kB, T->vB, T->ex_of);
+             (const std::uint32_t*)T->occ_off, T->L->kB, T->L->vB, T->ex_of);
     }
     PullPlan plan;
     if (G > 1) begin_round(T, false);
-    HPS_TRY(dedup_pull(T, T->kB, T->vB, on_n, ob, &plan, true, true));
+    HPS_TRY(dedup_pull(T, T->L->kB, T->L->vB, on_n, ob, &plan, true, true));
     // compute (a7, a8, a9); rows are in uid order at every G
     const std::uint32_t* occ_row = T->inv;
     if (n) {
@@ -1108,73 +1253,307 @@ static hps_status enqueue_batch_body(Tier* T, const BatchShape& sh, int skip_mb)
     }
     mark(T, HPS_T_APPLY);
     // dense sync + update (a12), with the verification fault knob
-    if (j != skip_mb) HPS_TRY(dense_sync_update(T, true));
+    if (j != bp.skip_mb) HPS_TRY(dense_sync_update(T, true));
     mark(T, HPS_T_DENSE);
   }
-  // ---- write-back to the value store (a13), over the table's slots
-  if (T->store) {
-    const unsigned gw = grid_for(sh.own_bound * std::uint64_t(E / V));
-    if (V == 4)
-      launch(T, table_writeback_sorted_kernel<4>, gw, 256, 0, (const std::uint64_t*)T->ws,
-             (const std::uint32_t*)T->ws_idx, (const std::uint64_t*)&T->dsc->n_ws,
-             (const float*)T->tvals[T->cur], T->store, T->store_keys, E);
-    else
-      launch(T, table_writeback_sorted_kernel<1>, gw, 256, 0, (const std::uint64_t*)T->ws,
-             (const std::uint32_t*)T->ws_idx, (const std::uint64_t*)&T->dsc->n_ws,
-             (const float*)T->tvals[T->cur], T->store, T->store_keys, E);
-  }
-  mark(T, HPS_T_WRITEBACK);
   return HPS_OK;
 }
 
-// Capture the body once per shape (and table parity, store, timing), then
-// replay: the whole batch becomes one cudaGraphLaunch.
-static hps_status run_body_graph(Tier* T, const BatchShape& sh) {
-  std::vector<std::uint64_t> key = {sh.B, sh.own_bound, sh.batch_bound,
-                                    std::uint64_t(T->cur + 1), std::uint64_t(T->has_prev),
-                                    reinterpret_cast<std::uint64_t>(T->store), T->store_keys,
-                                    std::uint64_t(T->timing)};
-  for (int j = 0; j < T->J; ++j) key.push_back(sh.mb_bound[j]);
+// Write-back of table tb to the value store (a13, hbm_ps.hpp:224-232 +
+// MemPs::collect_updates) on st_wb after its body, in ascending key order.
+static hps_status enqueue_writeback(Tier* T, int tb) {
+  const int E = T->E, V = vec_of(E);
+  HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_body_tab[tb], 0));
+  if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[tb][0], T->st_wb));
+  const std::uint64_t work = T->Wmax * std::uint64_t(E / V);
+  // posted PCIe writes: a few CTAs saturate the link without holding SMs
+  const unsigned gw = T->store_on_host ? T->wb_ctas : grid_for(work, 256 * 4);
+  const int tpb = T->store_on_host ? T->zc_threads : 256;
+  auto k = V == 4 ? table_writeback_sorted_kernel<4, 4> : table_writeback_sorted_kernel<1, 4>;
+  launch_on(T, T->st_wb, k, gw, tpb, 0, (const std::uint64_t*)T->wsb[tb],
+            (const std::uint32_t*)T->wsib[tb], (const std::uint64_t*)&T->dsc->nws_tab[tb],
+            (const float*)T->tvals[tb], T->store, T->store_keys, E);
+  if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[tb][1], T->st_wb));
+  HPS_CUDA(cudaEventRecord(T->ev_wb[tb], T->st_wb));
+  T->wb_pending[tb] = true;
+  T->wb_timed[tb] = T->timing;
+  return HPS_OK;
+}
+
+// Fold a finished write-back's duration into the WRITEBACK timing slot.
+static void wb_account(Tier* T, int p, bool wait) {
+  if (!T->wb_timed[p]) return;
+  if (wait) cudaEventSynchronize(T->ev_wbt[p][1]);
+  else if (cudaEventQuery(T->ev_wbt[p][1]) != cudaSuccess) return;
+  float ms = 0;
+  cudaEventElapsedTime(&ms, T->ev_wbt[p][0], T->ev_wbt[p][1]);
+  T->acc_ms[HPS_T_WRITEBACK] += ms;
+  T->wb_timed[p] = false;
+}
+
+// Order stream s after the pending write-backs (of table p, or all: -1).
+static hps_status wb_fence(Tier* T, int p = -1, cudaStream_t s = nullptr) {
+  for (int q = 0; q < kTables; ++q) {
+    if ((p >= 0 && q != p) || !T->wb_pending[q]) continue;
+    HPS_CUDA(cudaStreamWaitEvent(s ? s : T->st, T->ev_wb[q], 0));
+  }
+  return HPS_OK;
+}
+
+// Capture `enqueue` on the current lane's stream once per key, then replay:
+// a whole prep or body becomes one cudaGraphLaunch.
+template <class Fn>
+static hps_status run_graph(Tier* T, const std::vector<std::uint64_t>& key, Fn&& enqueue) {
+  cudaStream_t s = T->L->st;
   auto it = T->graphs.find(key);
-  const int cur_before = T->cur;
-  const bool prev_before = T->has_prev;
   if (it == T->graphs.end()) {
-    if (T->graphs.size() >= 16) {  // bounded cache
+    if (T->graphs.size() >= 64) {  // bounded cache
       cudaGraphExecDestroy(T->graphs.begin()->second.exec);
       T->graphs.erase(T->graphs.begin());
     }
     GraphEntry ge;
-    const std::uint64_t l0 = T->launches;
+    const std::uint64_t l0 = T->launches, e0 = T->p2p_epoch;
     const std::size_t ev0 = T->ev_phase.size();
-    HPS_CUDA(cudaStreamBeginCapture(T->st, cudaStreamCaptureModeThreadLocal));
-    const hps_status s = enqueue_batch_body(T, sh, -1);
+    HPS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const hps_status st = enqueue();
     cudaGraph_t g = nullptr;
-    const cudaError_t ce = cudaStreamEndCapture(T->st, &g);
-    if (s != HPS_OK) {
+    const cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (st != HPS_OK) {
       if (g) cudaGraphDestroy(g);
-      return s;
+      return st;
     }
     if (ce != cudaSuccess)
       return set_error(HPS_ERR_CUDA, "cuda: graph capture: %s", cudaGetErrorString(ce));
-    const cudaError_t ie = cudaGraphInstantiate(&ge.exec, g, 0);
+    // node priorities follow the capturing stream (body high, prep low)
+    const cudaError_t ie =
+        cudaGraphInstantiate(&ge.exec, g, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess)
       return set_error(HPS_ERR_CUDA, "cuda: graph instantiate: %s", cudaGetErrorString(ie));
     ge.launches = T->launches - l0;
+    ge.epochs = T->p2p_epoch - e0;
     ge.ev_phase.assign(T->ev_phase.begin() + ev0, T->ev_phase.end());
-    ge.cur_after = T->cur;
-    ge.prev_after = T->has_prev;
+    ge.ev_lane.assign(T->ev_lane.begin() + ev0, T->ev_lane.end());
     T->launches = l0;  // counted per replay below
+    T->p2p_epoch = e0;
     T->ev_phase.resize(ev0);
-    T->cur = cur_before;
-    T->has_prev = prev_before;
+    T->ev_lane.resize(ev0);
     it = T->graphs.emplace(key, std::move(ge)).first;
   }
-  HPS_CUDA(cudaGraphLaunch(it->second.exec, T->st));
+  HPS_CUDA(cudaGraphLaunch(it->second.exec, s));
   T->launches += it->second.launches;
+  T->p2p_epoch += it->second.epochs;
   T->ev_phase.insert(T->ev_phase.end(), it->second.ev_phase.begin(), it->second.ev_phase.end());
-  T->cur = it->second.cur_after;
-  T->has_prev = it->second.prev_after;
+  T->ev_lane.insert(T->ev_lane.end(), it->second.ev_lane.begin(), it->second.ev_lane.end());
+  return HPS_OK;
+}
+
+
+// ------------------------------------------------------ the batch pipeline
+
+// Wait for the oldest in-flight batch and park its result in T->done.
+static void complete_oldest(Tier* T) {
+  const BatchPlan bp = T->inflight.front();
+  T->inflight.pop_front();
+  Tier::Done d{bp.id, HPS_OK, std::string(), hps_batch_stats{}};
+  const cudaError_t ce = cudaEventSynchronize(T->ev_body_sp[bp.sp]);
+  if (ce != cudaSuccess) {
+    d.st = set_error(HPS_ERR_CUDA, "cuda: %s", cudaGetErrorString(ce));
+    d.msg = error_message();
+  } else {
+    const BatchOut& o = T->hout[bp.sp];
+    const int G = T->G, J = T->J;
+    const std::uint64_t GJ = std::uint64_t(G) * J;
+    hps_batch_stats& st = d.stats;
+    st.loss_sum = o.loss;
+    std::uint64_t ex = 0;
+    for (int j = 0; j < J; ++j) {
+      const std::uint64_t sh = std::uint64_t(T->g) * J + j;
+      ex += sh < bp.B ? (bp.B - sh - 1) / GJ + 1 : 0;
+    }
+    st.examples = ex;
+    st.working_set = o.n_ws;
+    st.table_capacity = o.cap;
+    st.pulled_keys = o.pulled;
+    st.carried_rows = o.carried;
+    st.store_rows = o.stored;
+    st.exact_fallbacks = o.fallbacks;
+    st.served_keys = o.served;
+    st.occurrences = bp.occ_total;
+    if (o.err.code) {
+      cudaMemsetAsync(&T->dsc->err, 0, sizeof(DevError), T->st);
+      d.st = device_error_status(T, o.err, "device table: missing key ");
+      d.msg = error_message();
+    }
+  }
+  if (T->timing) timing_end(T);
+  for (int q = 0; q < kTables; ++q) wb_account(T, q, false);
+  if (T->trace) {  // never waits: the write-back shown is batch id-3's, if done
+    float v[8] = {};
+    for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&v[k], T->tr_base, T->tr[bp.sp][k]);
+    const int w = int((bp.id + 1) & 3);  // (id - 3) mod 4
+    if (T->store && bp.id >= 3 && cudaEventQuery(T->trw[w][1]) == cudaSuccess) {
+      cudaEventElapsedTime(&v[6], T->tr_base, T->trw[w][0]);
+      cudaEventElapsedTime(&v[7], T->tr_base, T->trw[w][1]);
+    }
+    std::fprintf(stderr,
+                 "[trace] batch %llu: stage %.3f-%.3f prep %.3f-%.3f body %.3f-%.3f | "
+                 "wb(batch-3) %.3f-%.3f\n",
+                 (unsigned long long)bp.id, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+  }
+  T->done.push_back(std::move(d));
+}
+
+// Every in-flight batch done; the main stream ordered after the write-backs.
+// The parity API (build / pull / push / drain / dump ...) starts from here.
+static hps_status quiesce(Tier* T) {
+  while (!T->inflight.empty()) complete_oldest(T);
+  return wb_fence(T);
+}
+
+// Stage (H2D + counts + range check, st_stage) -> prep (lane 1) -> body
+// (lane 0) -> write-back (st_wb) of one batch, all enqueued; the host blocks
+// only on the stage's count round-trip. At most kSlots batches are in flight.
+static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* offsets,
+                               const std::uint64_t* keys, const std::uint8_t* labels,
+                               int on_device, std::uint64_t* id_out) {
+  if (T->N != 1) return set_error(HPS_ERR_ARG, "train_batch: one node per box (nodes must be 1)");
+  if (B > T->Bmax)
+    return set_error(HPS_ERR_CAPACITY, "train_batch: %llu examples exceed max_batch_examples",
+                     (unsigned long long)B);
+  if (T->timing)  // phases are attributed without overlap: one batch at a time
+    while (!T->inflight.empty()) complete_oldest(T);
+  while (T->inflight.size() >= std::size_t(kSlots)) complete_oldest(T);
+  const int G = T->G, J = T->J;
+  BatchPlan bp;
+  bp.id = T->submitted;
+  bp.B = B;
+  bp.sp = int(T->submitted % kSlots);
+  bp.tb = next_table(T);
+  bp.tp = T->cur;
+  bp.tq = (T->store && T->prev >= 0 && T->prev != bp.tb && T->tab_wb[T->prev]) ? T->prev : -1;
+  bp.step = T->step;
+  const int sp = bp.sp;
+  // ---- stage into the tier's own buffers (captured graphs never see caller
+  // pointers), after the body that last used this staging slot
+  cudaStream_t ss = T->st_stage;
+  timing_begin(T);
+  mark_stage(T, -1);
+  if (T->sp_pending[sp]) HPS_CUDA(cudaStreamWaitEvent(ss, T->ev_body_sp[sp], 0));
+  if (T->trace) cudaEventRecord(T->tr[sp][0], ss);
+  std::uint64_t O = 0;
+  if (on_device) {
+    HPS_CUDA(cudaMemcpyAsync(T->b_off[sp], offsets, (B + 1) * 8, cudaMemcpyDeviceToDevice, ss));
+    HPS_CUDA(cudaMemcpyAsync(&T->hsc->total_unused, offsets + B, 8, cudaMemcpyDeviceToHost, ss));
+    HPS_CUDA(cudaStreamSynchronize(ss));
+    O = std::uint64_t(T->hsc->total_unused);
+    if (O > T->Omax)
+      return set_error(HPS_ERR_CAPACITY, "train_batch: %llu keys exceed max_batch_keys",
+                       (unsigned long long)O);
+    HPS_CUDA(cudaMemcpyAsync(T->b_keys[sp], keys, O * 8, cudaMemcpyDeviceToDevice, ss));
+    HPS_CUDA(cudaMemcpyAsync(T->b_lab[sp], labels, B, cudaMemcpyDeviceToDevice, ss));
+  } else {
+    O = std::uint64_t(offsets[B]);
+    if (O > T->Omax)
+      return set_error(HPS_ERR_CAPACITY, "train_batch: %llu keys exceed max_batch_keys",
+                       (unsigned long long)O);
+    HPS_CUDA(cudaMemcpyAsync(T->b_off[sp], offsets, (B + 1) * 8, cudaMemcpyHostToDevice, ss));
+    HPS_CUDA(cudaMemcpyAsync(T->b_keys[sp], keys, O * 8, cudaMemcpyHostToDevice, ss));
+    HPS_CUDA(cudaMemcpyAsync(T->b_lab[sp], labels, B, cudaMemcpyHostToDevice, ss));
+  }
+  HPS_CUDA(cudaMemsetAsync(T->dsc->counts[sp], 0, sizeof(T->dsc->counts[sp]), ss));
+  launch_on(T, ss, batch_count_kernel, kSMs * 4, 256, 0, (const std::int64_t*)T->b_off[sp],
+            (const std::uint64_t*)T->b_keys[sp], B, G, T->g, J,
+            T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts[sp],
+            &T->dsc->err);
+  HPS_CUDA(cudaMemcpyAsync(T->hsc->counts[sp], T->dsc->counts[sp], sizeof(T->dsc->counts[sp]),
+                           cudaMemcpyDeviceToHost, ss));
+  mark_stage(T, HPS_T_STAGE);
+  if (T->trace) cudaEventRecord(T->tr[sp][1], ss);
+  HPS_TRY(check_device_error(T, "device table: missing key ", true, ss));
+  for (int j = 0; j < J; ++j) bp.occ_total += T->hsc->counts[sp][j];
+  const std::uint64_t own = T->hsc->counts[sp][J];
+  if (own > T->Wmax || bp.occ_total > T->Omax)
+    return set_error(HPS_ERR_CAPACITY, "train_batch: batch exceeds configured maxima");
+  // ---- shape: power-of-two upper bounds of the counts, so one captured
+  // graph serves every batch of a shape
+  BatchShape sh;
+  sh.B = B;
+  sh.own_bound = shape_bound(own);
+  sh.batch_bound = shape_bound(std::uint64_t(T->hsc->counts[sp][J + 1]));
+  for (int j = 0; j < J; ++j) sh.mb_bound[j] = shape_bound(T->hsc->counts[sp][j]);
+  const std::int64_t first_mb = T->step * J;
+  if (T->cfg.inject_skip_sync >= first_mb && T->cfg.inject_skip_sync < first_mb + J)
+    bp.skip_mb = int(T->cfg.inject_skip_sync - first_mb);
+  // ---- prep on lane 1, beside the previous body
+  {
+    cudaStream_t ps = T->lane[1].st;
+    if (bp.tq >= 0 && T->body_pending[bp.tq])  // its rows final
+      HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tq], 0));
+    if (T->body_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tb], 0));
+    if (T->wb_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_wb[bp.tb], 0));
+    if (T->trace) cudaEventRecord(T->tr[sp][2], ps);
+    T->L = &T->lane[1];
+    open_lookback_context(T);
+    hps_status st;
+    if (T->use_graphs) {
+      const std::vector<std::uint64_t> key = {
+          1, B, sh.own_bound, sh.batch_bound, std::uint64_t(bp.tb), std::uint64_t(bp.tp + 1),
+          std::uint64_t(bp.tq + 1), std::uint64_t(sp), reinterpret_cast<std::uint64_t>(T->store),
+          T->store_keys, std::uint64_t(T->store_on_host), std::uint64_t(T->timing)};
+      st = run_graph(T, key, [&] { return enqueue_prep(T, sh, bp); });
+    } else {
+      st = enqueue_prep(T, sh, bp);
+    }
+    T->L = &T->lane[0];
+    HPS_TRY(st);
+    HPS_CUDA(cudaEventRecord(T->ev_prep, ps));
+    if (T->trace) cudaEventRecord(T->tr[sp][3], ps);
+  }
+  // ---- body on lane 0
+  HPS_CUDA(cudaStreamWaitEvent(T->st, T->ev_prep, 0));
+  if (T->trace) cudaEventRecord(T->tr[sp][4], T->st);
+  open_lookback_context(T);
+  T->prev = bp.tp;
+  T->cur = bp.tb;
+  T->ws = T->wsb[bp.tb];
+  T->ws_idx = T->wsib[bp.tb];
+  T->ws_sorted = true;
+  if (T->use_graphs && bp.skip_mb < 0) {
+    std::vector<std::uint64_t> key = {2, B, sh.own_bound, std::uint64_t(bp.tb),
+                                      std::uint64_t(bp.tp + 1), std::uint64_t(sp),
+                                      std::uint64_t(T->timing)};
+    for (int j = 0; j < J; ++j) key.push_back(sh.mb_bound[j]);
+    HPS_TRY(run_graph(T, key, [&] { return enqueue_body(T, sh, bp); }));
+  } else {
+    HPS_TRY(enqueue_body(T, sh, bp));
+  }
+  BatchOut* ho = &T->hout[sp];
+  const int tb = bp.tb;
+  HPS_CUDA(cudaMemcpyAsync(&ho->loss, &T->dsc->loss, 16, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->fallbacks, &T->dsc->fallbacks, 16, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->carried, &T->dsc->carried_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->stored, &T->dsc->stored_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->n_ws, &T->dsc->nws_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->cap, &T->dsc->cap[tb], 8, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->err, &T->dsc->err, sizeof(DevError), cudaMemcpyDeviceToHost, T->st));
+  if (T->trace) cudaEventRecord(T->tr[sp][5], T->st);
+  HPS_CUDA(cudaEventRecord(T->ev_body_tab[tb], T->st));
+  HPS_CUDA(cudaEventRecord(T->ev_body_sp[sp], T->st));
+  T->body_pending[tb] = true;
+  T->sp_pending[sp] = true;
+  // ---- write-back (collect) on st_wb, overlapping the next batch
+  T->tab_wb[tb] = T->store != nullptr;
+  if (T->store) {
+    HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_body_tab[tb], 0));
+    if (T->trace) cudaEventRecord(T->trw[bp.id & 3][0], T->st_wb);
+    HPS_TRY(enqueue_writeback(T, tb));
+    if (T->trace) cudaEventRecord(T->trw[bp.id & 3][1], T->st_wb);
+  }
+  T->inflight.push_back(bp);
+  ++T->submitted;
+  ++T->step;
+  if (id_out) *id_out = bp.id;
   return HPS_OK;
 }
 
@@ -1242,6 +1621,11 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   t->Wmax = c.max_working_set ? c.max_working_set : t->Omax;
   t->Wmax = std::max(t->Wmax, t->Omax);
   t->capmax = table_capacity(t->Wmax);
+  if (const char* v = std::getenv("HPS_PF_CTAS")) t->pf_ctas = unsigned(std::max(1, std::atoi(v)));
+  if (const char* v = std::getenv("HPS_WB_CTAS")) t->wb_ctas = unsigned(std::max(1, std::atoi(v)));
+  if (const char* v = std::getenv("HPS_TRACE")) t->trace = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
   {
     int bits = 64;
@@ -1283,11 +1667,46 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (e != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: cudaSetDevice(%d): %s", c.cuda_device,
                           cudaGetErrorString(e)));
-  if ((e = cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking)) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&t->st2, cudaStreamNonBlocking)) != cudaSuccess ||
-      (e = cudaEventCreateWithFlags(&t->fork, cudaEventDisableTiming)) != cudaSuccess ||
-      (e = cudaEventCreateWithFlags(&t->join, cudaEventDisableTiming)) != cudaSuccess)
-    return fail(set_error(HPS_ERR_CUDA, "cuda: stream: %s", cudaGetErrorString(e)));
+  {
+    auto ev = [&](cudaEvent_t* x, bool timed) {
+      if (e == cudaSuccess)
+        e = timed ? cudaEventCreate(x) : cudaEventCreateWithFlags(x, cudaEventDisableTiming);
+    };
+    // the body (critical path) outranks the work that overlaps it
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (!t->priorities) lo = hi = 0;
+    auto str = [&](cudaStream_t* x, int prio) {
+      if (e == cudaSuccess) e = cudaStreamCreateWithPriority(x, cudaStreamNonBlocking, prio);
+    };
+    str(&t->st, hi);
+    str(&t->st2, hi);
+    str(&t->lane[1].st, lo);
+    str(&t->st_stage, lo);
+    str(&t->st_wb, lo);
+    ev(&t->fork, false);
+    ev(&t->join, false);
+    ev(&t->ev_staged, false);
+    ev(&t->ev_prep, false);
+    for (int i = 0; i < kTables; ++i) {
+      ev(&t->ev_body_tab[i], false);
+      ev(&t->ev_wb[i], false);
+      ev(&t->ev_wbt[i][0], true);
+      ev(&t->ev_wbt[i][1], true);
+    }
+    for (auto& x : t->ev_body_sp) ev(&x, false);
+    if (t->trace) {
+      ev(&t->tr_base, true);
+      for (auto& row : t->tr)
+        for (auto& x : row) ev(&x, true);
+      for (auto& row : t->trw)
+        for (auto& x : row) ev(&x, true);
+      if (e == cudaSuccess) e = cudaEventRecord(t->tr_base, t->st);
+    }
+    t->lane[0].st = t->st;
+    if (e != cudaSuccess)
+      return fail(set_error(HPS_ERR_CUDA, "cuda: stream: %s", cudaGetErrorString(e)));
+  }
 
   {
     // dynamic shared memory of the model kernels (per-example scratch, streamed records)
@@ -1309,27 +1728,42 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(dsc, 1);
   if ((e = cudaMallocHost(&t->hsc, sizeof(Scalars))) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: host alloc: %s", cudaGetErrorString(e)));
-  A(tkeys[0], t->capmax);
-  A(tkeys[1], t->capmax);
-  A(tvals[0], t->capmax * E);
-  A(tvals[1], t->capmax * E);
-  A(ws, W);
-  A(ws_idx, W);
+  if ((e = cudaMallocHost(&t->hout, kSlots * sizeof(BatchOut))) != cudaSuccess)
+    return fail(set_error(HPS_ERR_CUDA, "cuda: host alloc: %s", cudaGetErrorString(e)));
+  for (int i = 0; i < kTables; ++i) {
+    A(tkeys[i], t->capmax);
+    A(tvals[i], t->capmax * E);
+    A(wsb[i], W);
+    A(wsib[i], W);
+    A(csrc[i], W);
+  }
+  A(need_key, W);
+  A(need_slot, W);
+  t->ws = t->wsb[0];
+  t->ws_idx = t->wsib[0];
   t->wsset_cap = 1;
   while (t->wsset_cap < 2 * std::max(O, W)) t->wsset_cap <<= 1;
   A(wsset, t->wsset_cap);
   const std::uint64_t S = std::max(O, W);
-  A(kA, S);
-  A(kB, S);
-  A(vA, S);
-  A(vB, S);
-  A(ghist, std::uint64_t(kMaxPasses) * kDigits);
-  t->status_words = std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1;
-  A(status, t->status_words);
-  A(ticket, 1);
-  A(b_off, t->Bmax + 1);
-  A(b_keys, O);
-  A(b_lab, t->Bmax);
+  const std::uint64_t status_words =
+      std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1;
+  for (Lane& l : t->lane) {
+    if ((s = dalloc(t, &l.kA, S)) != HPS_OK || (s = dalloc(t, &l.kB, S)) != HPS_OK ||
+        (s = dalloc(t, &l.vA, S)) != HPS_OK || (s = dalloc(t, &l.vB, S)) != HPS_OK ||
+        (s = dalloc(t, &l.ghist, std::uint64_t(kMaxPasses) * kDigits)) != HPS_OK ||
+        (s = dalloc(t, &l.status, status_words)) != HPS_OK ||
+        (s = dalloc(t, &l.ticket, 1)) != HPS_OK || (s = dalloc(t, &l.d, 1)) != HPS_OK)
+      return fail(s);
+    l.status_words = status_words;
+    cudaMemsetAsync(l.ticket, 0, 8, t->st);
+    cudaMemsetAsync(l.status, 0, status_words * 8, t->st);
+    cudaMemsetAsync(l.d, 0, sizeof(LaneDev), t->st);
+  }
+  for (int i = 0; i < kSlots; ++i) {
+    A(b_off[i], t->Bmax + 1);
+    A(b_keys[i], O);
+    A(b_lab[i], t->Bmax);
+  }
   A(occ_off, t->nmb_max + 1);
   A(ex_of, S);
   A(inv, S);
@@ -1358,12 +1792,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
 #undef A
-  cudaMemsetAsync(t->ticket, 0, 8, t->st);
   cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
   cudaMemsetAsync(t->key_done, 0, (S / (kLongSeg + 1) + 2) * 4, t->st);
-  cudaMemsetAsync(t->status, 0,
-                  (std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1) * 8,
-                  t->st);
   if ((e = cudaMemsetAsync(t->dsc, 0, sizeof(Scalars), t->st)) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: memset: %s", cudaGetErrorString(e)));
   // replicate_dense(init_dense(cfg)) — the init stream is host-side std::mt19937_64
@@ -1390,7 +1820,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
 hps_status hps_destroy(hps_tier_t t) {
   if (!t) return HPS_OK;
   cudaSetDevice(t->cfg.cuda_device);
-  if (t->st) cudaStreamSynchronize(t->st);
+  for (cudaStream_t x : {t->st, t->lane[1].st, t->st_stage, t->st_wb, t->st2})
+    if (x) cudaStreamSynchronize(x);
   if (t->comm) nccl().CommDestroy(t->comm);
   for (auto& c : t->pending) {
     cudaFree(c.keys);
@@ -1400,10 +1831,21 @@ hps_status hps_destroy(hps_tier_t t) {
   for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : t->allocs) cudaFree(p);
   if (t->hsc) cudaFreeHost(t->hsc);
+  if (t->hout) cudaFreeHost(t->hout);
   if (t->store_registered) cudaHostUnregister(t->store_host);
   for (auto& ev : t->evpool) cudaEventDestroy(ev);
   if (t->fork) cudaEventDestroy(t->fork);
   if (t->join) cudaEventDestroy(t->join);
+  for (int p = 0; p < kTables; ++p) {
+    for (cudaEvent_t x : {t->ev_wb[p], t->ev_body_tab[p], t->ev_wbt[p][0], t->ev_wbt[p][1]})
+      if (x) cudaEventDestroy(x);
+  }
+  for (cudaEvent_t x : t->ev_body_sp)
+    if (x) cudaEventDestroy(x);
+  for (cudaEvent_t x : {t->ev_staged, t->ev_prep})
+    if (x) cudaEventDestroy(x);
+  for (cudaStream_t x : {t->lane[1].st, t->st_stage, t->st_wb})
+    if (x) cudaStreamDestroy(x);
   if (t->st2) cudaStreamDestroy(t->st2);
   if (t->st) cudaStreamDestroy(t->st);
   delete t;
@@ -1414,15 +1856,25 @@ hps_status hps_destroy(hps_tier_t t) {
   if (!(t)) return set_error(HPS_ERR_ARG, "null handle");    \
   HPS_CUDA(cudaSetDevice((t)->cfg.cuda_device))
 
+// The parity API runs after every in-flight batch (and its write-back).
+#define HPS_ENTER_Q(t) \
+  HPS_ENTER(t);        \
+  HPS_TRY(quiesce(t))
+
 hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float* host_rows) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
   if (n > t->Wmax)
     return set_error(HPS_ERR_CAPACITY, "build: %llu keys exceed max_working_set %llu",
                      (unsigned long long)n, (unsigned long long)t->Wmax);
   if (n && !keys) return set_error(HPS_ERR_ARG, "null keys");
   if (n) {
-    HPS_CUDA(cudaMemcpyAsync(t->kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
-    launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
+    HPS_CUDA(cudaMemcpyAsync(t->lane[0].kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
+    launch(t, iota_kernel, grid_for(n), 256, 0, t->lane[0].vB, n);
+  }
+  {
+    const int nxt = next_table(t);
+    t->ws = t->wsb[nxt];
+    t->ws_idx = t->wsib[nxt];
   }
   const float* staged = nullptr;
   if (host_rows && n) {
@@ -1441,7 +1893,7 @@ hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float
   std::uint32_t* so = nullptr;
   open_lookback_context(t);
   if (n) {
-    radix_sort(t, t->kB, t->vB, Count{nullptr, n}, n, 64, true, &sk, &so);
+    radix_sort(t, t->lane[0].kB, t->lane[0].vB, Count{nullptr, n}, n, 64, true, &sk, &so);
     tile_scan(t, RunStartOwned{sk, std::uint64_t(t->G), std::uint64_t(t->g)},
               CompactEmit{sk, so, t->ws, t->ws_idx}, Count{nullptr, n}, n, &t->dsc->n_ws);
   } else {
@@ -1458,19 +1910,19 @@ static hps_status require_built(Tier* t) {
 }
 
 hps_status hps_pull(hps_tier_t t, const uint64_t* keys, uint64_t n, float* out_rows) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
   HPS_TRY(require_built(t));
   if (n > t->Omax)
     return set_error(HPS_ERR_CAPACITY, "pull: %llu keys exceed max_batch_keys",
                      (unsigned long long)n);
   if (n) {
-    HPS_CUDA(cudaMemcpyAsync(t->kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
-    launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
+    HPS_CUDA(cudaMemcpyAsync(t->lane[0].kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
+    launch(t, iota_kernel, grid_for(n), 256, 0, t->lane[0].vB, n);
   }
   PullPlan plan;
   open_lookback_context(t);
   if (t->G > 1) begin_round(t, false);
-  HPS_TRY(dedup_pull(t, t->kB, t->vB, Count{nullptr, n}, n, &plan, true));
+  HPS_TRY(dedup_pull(t, t->lane[0].kB, t->lane[0].vB, Count{nullptr, n}, n, &plan, true));
   HPS_TRY(check_device_error(t, "device table: missing key ", true));
   if (n) {
     launch(t, scatter_rows_kernel, grid_for(n * t->E), 256, 0, (const std::uint32_t*)t->inv,
@@ -1483,21 +1935,21 @@ hps_status hps_pull(hps_tier_t t, const uint64_t* keys, uint64_t n, float* out_r
 }
 
 hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uint64_t n) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
   HPS_TRY(require_built(t));
   if (n > t->Omax)
     return set_error(HPS_ERR_CAPACITY, "push: %llu keys exceed max_batch_keys",
                      (unsigned long long)n);
   if (n) {
-    HPS_CUDA(cudaMemcpyAsync(t->kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
+    HPS_CUDA(cudaMemcpyAsync(t->lane[0].kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
     HPS_CUDA(cudaMemcpyAsync(t->hstage, deltas, n * std::uint64_t(t->E) * 4,
                              cudaMemcpyHostToDevice, t->st));
-    launch(t, iota_kernel, grid_for(n), 256, 0, t->vB, n);
+    launch(t, iota_kernel, grid_for(n), 256, 0, t->lane[0].vB, n);
   }
   PullPlan plan;
   open_lookback_context(t);
   if (t->G > 1) begin_round(t, false);
-  HPS_TRY(dedup_pull(t, t->kB, t->vB, Count{nullptr, n}, n, &plan, false));
+  HPS_TRY(dedup_pull(t, t->lane[0].kB, t->lane[0].vB, Count{nullptr, n}, n, &plan, false));
   HPS_CUDA(cudaMemcpyAsync(&t->hsc->U, &t->dsc->U, 8, cudaMemcpyDeviceToHost, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
   // a duplicate key is reported only after the collective completes, so no
@@ -1552,8 +2004,9 @@ hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uin
 }
 
 hps_status hps_drain(hps_tier_t t) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
   HPS_TRY(require_built(t));
+  t->tab_wb[t->cur] = false;  // rows change after their write-back: no store proxy
   const int V = vec_of(t->E);
   for (int src : canonical_senders(t)) {
     for (auto& c : t->pending) {
@@ -1584,10 +2037,12 @@ hps_status hps_drain(hps_tier_t t) {
 
 hps_status hps_table_info(hps_tier_t t, uint64_t* capacity, uint64_t* occupancy,
                           uint64_t* width) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
   HPS_TRY(require_built(t));
-  HPS_CUDA(cudaMemcpyAsync(t->hsc->cap, t->dsc->cap, 16, cudaMemcpyDeviceToHost, t->st));
-  HPS_CUDA(cudaMemcpyAsync(t->hsc->nws_tab, t->dsc->nws_tab, 16, cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaMemcpyAsync(t->hsc->cap, t->dsc->cap, sizeof(t->dsc->cap), cudaMemcpyDeviceToHost,
+                           t->st));
+  HPS_CUDA(cudaMemcpyAsync(t->hsc->nws_tab, t->dsc->nws_tab, sizeof(t->dsc->nws_tab),
+                           cudaMemcpyDeviceToHost, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
   if (capacity) *capacity = t->hsc->cap[t->cur];
   if (occupancy) *occupancy = t->hsc->nws_tab[t->cur];
@@ -1614,11 +2069,11 @@ hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t*
   if (!t->ws_sorted) {  // after hps_train_batch: the sorted key list from the table itself
     open_lookback_context(t);
     tile_scan(t, LiveSlot{t->tkeys[t->cur]},
-              CompactEmit{t->tkeys[t->cur], nullptr, t->kB, nullptr}, Count{nullptr, cap}, cap,
-              &t->dsc->total);
+              CompactEmit{t->tkeys[t->cur], nullptr, t->lane[0].kB, nullptr}, Count{nullptr, cap}, cap,
+              &t->lane[0].d->total);
     std::uint64_t* sk = nullptr;
     std::uint32_t* so = nullptr;
-    radix_sort(t, t->kB, nullptr, Count{nullptr, occ}, occ, t->sort_bits, false, &sk, &so);
+    radix_sort(t, t->lane[0].kB, nullptr, Count{nullptr, occ}, occ, t->sort_bits, false, &sk, &so);
     HPS_CUDA(cudaMemcpyAsync(t->ws, sk, occ * 8, cudaMemcpyDeviceToDevice, t->st));
     t->ws_sorted = true;
   }
@@ -1647,7 +2102,7 @@ hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t*
 }
 
 hps_status hps_dense_sync(hps_tier_t t, float* buf, uint64_t len, int deterministic) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
   (void)deterministic;  // the canonical f64 sum serves both modes
   if (len == 0 || t->G == 1) return HPS_OK;  // a single replica is untouched
   const std::uint64_t nw = std::uint64_t(t->md.nw);
@@ -1673,23 +2128,36 @@ hps_status hps_dense_count(hps_tier_t t, uint64_t* n) {
 }
 
 hps_status hps_get_dense(hps_tier_t t, float* w) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
   HPS_CUDA(cudaMemcpyAsync(w, t->dense, std::uint64_t(t->md.nw) * 4, cudaMemcpyDeviceToHost, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
   return HPS_OK;
 }
 
 hps_status hps_set_dense(hps_tier_t t, const float* w) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
   HPS_CUDA(cudaMemcpyAsync(t->dense, w, std::uint64_t(t->md.nw) * 4, cudaMemcpyHostToDevice, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
   return HPS_OK;
 }
 
+hps_status hps_flush(hps_tier_t t) {
+  HPS_ENTER_Q(t);
+  HPS_CUDA(cudaStreamSynchronize(t->st_wb));
+  for (int p = 0; p < kTables; ++p) {
+    wb_account(t, p, true);
+    t->wb_pending[p] = false;
+  }
+  return HPS_OK;
+}
+
 hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on_device) {
-  HPS_ENTER(t);
+  HPS_ENTER_Q(t);
+  HPS_TRY(hps_flush(t));
   for (auto& kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
   t->graphs.clear();
+  for (bool& f : t->tab_wb) f = false;  // earlier tables wrote to another store
+  t->store_on_host = false;
   if (t->store_registered) {
     cudaHostUnregister(t->store_host);
     t->store_registered = false;
@@ -1713,13 +2181,14 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
     void* dp = nullptr;
     HPS_CUDA(cudaHostGetDevicePointer(&dp, rows, 0));
     t->store = static_cast<float*>(dp);
+    t->store_on_host = true;
   }
   t->store_keys = num_keys;
   return HPS_OK;
 }
 
 hps_status hps_set_timing(hps_tier_t t, int enable) {
-  if (!t) return set_error(HPS_ERR_ARG, "null handle");
+  HPS_ENTER_Q(t);
   t->timing = enable != 0;
   return HPS_OK;
 }
@@ -1750,97 +2219,41 @@ hps_status hps_stream(hps_tier_t t, void** stream) {
 
 // ----------------------------------------------------- hps_train_batch
 
+hps_status hps_submit_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
+                            const uint64_t* keys, const uint8_t* labels, int on_device) {
+  HPS_ENTER(t);
+  return submit_batch(t, B, offsets, keys, labels, on_device, nullptr);
+}
+
+hps_status hps_wait_batch(hps_tier_t t, hps_batch_stats* stats) {
+  HPS_ENTER(t);
+  if (t->done.empty()) {
+    if (t->inflight.empty()) return set_error(HPS_ERR_ARG, "wait_batch: no batch in flight");
+    complete_oldest(t);
+  }
+  Tier::Done d = std::move(t->done.front());
+  t->done.pop_front();
+  if (stats) *stats = d.stats;
+  if (d.st != HPS_OK) return set_error(d.st, "%s", d.msg.c_str());
+  return HPS_OK;
+}
+
 hps_status hps_train_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
                            const uint64_t* keys, const uint8_t* labels, int on_device,
                            hps_batch_stats* stats) {
   HPS_ENTER(t);
-  if (t->N != 1) return set_error(HPS_ERR_ARG, "train_batch: one node per box (nodes must be 1)");
-  if (B > t->Bmax)
-    return set_error(HPS_ERR_CAPACITY, "train_batch: %llu examples exceed max_batch_examples",
-                     (unsigned long long)B);
-  Tier* T = t;
-  const int G = T->G, J = T->J;
-  const std::uint64_t GJ = std::uint64_t(G) * J;
-  // ---- stage the batch into the tier's own buffers (so captured graphs
-  // never depend on caller pointers)
-  timing_begin(T);
-  if (on_device) {
-    std::int64_t last = 0;
-    HPS_CUDA(cudaMemcpyAsync(T->b_off, offsets, (B + 1) * 8, cudaMemcpyDeviceToDevice, T->st));
-    HPS_CUDA(cudaMemcpyAsync(&last, offsets + B, 8, cudaMemcpyDeviceToHost, T->st));
-    HPS_CUDA(cudaStreamSynchronize(T->st));
-    if (std::uint64_t(last) > T->Omax)
-      return set_error(HPS_ERR_CAPACITY, "train_batch: %llu keys exceed max_batch_keys",
-                       (unsigned long long)last);
-    HPS_CUDA(cudaMemcpyAsync(T->b_keys, keys, std::uint64_t(last) * 8, cudaMemcpyDeviceToDevice,
-                             T->st));
-    HPS_CUDA(cudaMemcpyAsync(T->b_lab, labels, B, cudaMemcpyDeviceToDevice, T->st));
-  } else {
-    const std::uint64_t O = std::uint64_t(offsets[B]);
-    if (O > T->Omax)
-      return set_error(HPS_ERR_CAPACITY, "train_batch: %llu keys exceed max_batch_keys",
-                       (unsigned long long)O);
-    HPS_CUDA(cudaMemcpyAsync(T->b_off, offsets, (B + 1) * 8, cudaMemcpyHostToDevice, T->st));
-    HPS_CUDA(cudaMemcpyAsync(T->b_keys, keys, O * 8, cudaMemcpyHostToDevice, T->st));
-    HPS_CUDA(cudaMemcpyAsync(T->b_lab, labels, B, cudaMemcpyHostToDevice, T->st));
+  std::uint64_t id = 0;
+  HPS_TRY(submit_batch(t, B, offsets, keys, labels, on_device, &id));
+  while (!t->inflight.empty() && t->inflight.front().id <= id) complete_oldest(t);
+  for (auto it = t->done.begin(); it != t->done.end(); ++it) {
+    if (it->id != id) continue;
+    Tier::Done d = std::move(*it);
+    t->done.erase(it);
+    if (stats) *stats = d.stats;
+    if (d.st != HPS_OK) return set_error(d.st, "%s", d.msg.c_str());
+    return HPS_OK;
   }
-  // ---- counts (one host round-trip per batch)
-  HPS_CUDA(cudaMemsetAsync(T->dsc->counts, 0, sizeof(T->dsc->counts), T->st));
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 8 * 3, T->st));  // loss, pulled, carried
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 16, T->st));  // fallbacks, served
-  launch(T, batch_count_kernel, kSMs * 4, 256, 0, (const std::int64_t*)T->b_off,
-         (const std::uint64_t*)T->b_keys, std::uint64_t(B), G, T->g, J,
-         T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts, &T->dsc->err);
-  HPS_CUDA(cudaMemcpyAsync(T->hsc->counts, T->dsc->counts, sizeof(T->dsc->counts),
-                           cudaMemcpyDeviceToHost, T->st));
-  HPS_TRY(check_device_error(T, "device table: missing key ", true));
-  std::uint64_t occ_total = 0;
-  for (int j = 0; j < J; ++j) occ_total += T->hsc->counts[j];
-  const std::uint64_t own = T->hsc->counts[J];
-  mark(T, HPS_T_STAGE);
-  if (own > T->Wmax || occ_total > T->Omax)
-    return set_error(HPS_ERR_CAPACITY, "train_batch: batch exceeds configured maxima");
-  // ---- the device-side body: launch-only, sized by power-of-two upper bounds
-  // of the counts, so one captured CUDA graph serves every batch of a shape
-  BatchShape sh;
-  sh.B = B;
-  sh.own_bound = shape_bound(own);
-  sh.batch_bound = shape_bound(std::uint64_t(T->hsc->counts[J + 1]));
-  for (int j = 0; j < J; ++j) sh.mb_bound[j] = shape_bound(T->hsc->counts[j]);
-  const std::int64_t first_mb = T->step * J;
-  const bool skip_in_batch = T->cfg.inject_skip_sync >= first_mb &&
-                             T->cfg.inject_skip_sync < first_mb + J;
-  open_lookback_context(T);  // eager, before capture or replay
-  if (T->use_graphs && !skip_in_batch) {
-    HPS_TRY(run_body_graph(T, sh));
-  } else {
-    HPS_TRY(enqueue_batch_body(T, sh, skip_in_batch ? int(T->cfg.inject_skip_sync - first_mb) : -1));
-  }
-  HPS_CUDA(cudaMemcpyAsync(&T->hsc->loss, &T->dsc->loss, 8 * 3, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&T->hsc->fallbacks, &T->dsc->fallbacks, 16, cudaMemcpyDeviceToHost,
-                           T->st));
-  HPS_CUDA(cudaMemcpyAsync(&T->hsc->n_ws, &T->dsc->n_ws, 8, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(T->hsc->cap, T->dsc->cap, 16, cudaMemcpyDeviceToHost, T->st));
-  HPS_TRY(check_device_error(T, "device table: missing key ", true));
-  ++T->step;
-  timing_end(T);
-  if (stats) {
-    stats->loss_sum = T->hsc->loss;
-    std::uint64_t ex = 0;
-    for (int j = 0; j < J; ++j) {
-      const std::uint64_t s = std::uint64_t(T->g) * J + j;
-      ex += s < B ? (B - s - 1) / GJ + 1 : 0;
-    }
-    stats->examples = ex;
-    stats->working_set = T->hsc->n_ws;
-    stats->table_capacity = T->hsc->cap[T->cur];
-    stats->pulled_keys = T->hsc->pulled;
-    stats->carried_rows = T->hsc->carried;
-    stats->exact_fallbacks = T->hsc->fallbacks;
-    stats->served_keys = T->hsc->served;
-    stats->occurrences = occ_total;
-  }
-  return HPS_OK;
+  return set_error(HPS_ERR_ARG, "train_batch: lost batch %llu", (unsigned long long)id);
 }
 
 hps_status hps_set_graphs(hps_tier_t t, int enable) {

@@ -74,6 +74,7 @@ class HpsBatchStats(ctypes.Structure):
         ("occurrences", ctypes.c_uint64),
         ("carried_rows", ctypes.c_uint64),
         ("exact_fallbacks", ctypes.c_uint64),
+        ("store_rows", ctypes.c_uint64),
     ]
 
 TIMING_SLOTS = ["total", "stage", "build", "dedup", "pull", "fwdbwd", "grads", "apply",
@@ -102,8 +103,11 @@ _SIGS = {
     "hps_get_dense": ([_P, _P], ctypes.c_int),
     "hps_set_dense": ([_P, _P], ctypes.c_int),
     "hps_attach_store": ([_P, _P, _U64, ctypes.c_int], ctypes.c_int),
+    "hps_flush": ([_P], ctypes.c_int),
     "hps_train_batch": ([_P, _U64, _P, _P, _P, ctypes.c_int,
                          ctypes.POINTER(HpsBatchStats)], ctypes.c_int),
+    "hps_submit_batch": ([_P, _U64, _P, _P, _P, ctypes.c_int], ctypes.c_int),
+    "hps_wait_batch": ([_P, ctypes.POINTER(HpsBatchStats)], ctypes.c_int),
     "hps_set_timing": ([_P, ctypes.c_int], ctypes.c_int),
     "hps_get_timing": ([_P, _P], ctypes.c_int),
     "hps_reset_timing": ([_P], ctypes.c_int),
@@ -332,19 +336,39 @@ class Tier:
             _check(lib().hps_attach_store(self._h, _ptr(rows), rows.shape[0], 0))
             self._store = rows
 
-    def train_batch(self, offsets, keys, labels, on_device: bool = False) -> HpsBatchStats:
-        st = HpsBatchStats()
+    def flush(self) -> None:
+        """Wait for the deferred write-backs (hps_flush): afterwards the
+        attached store holds every trained row."""
+        _check(lib().hps_flush(self._h))
+
+    @staticmethod
+    def _batch_args(offsets, keys, labels, on_device):
         if on_device:
             n = int(offsets[1])  # (ptr, num_examples) pairs for device buffers
-            _check(lib().hps_train_batch(self._h, n, ctypes.c_void_p(int(offsets[0])),
-                                         ctypes.c_void_p(int(keys)),
-                                         ctypes.c_void_p(int(labels)), 1, ctypes.byref(st)))
-        else:
-            o = np.ascontiguousarray(offsets, dtype=np.int64)
-            k = _u64(keys)
-            lab = np.ascontiguousarray(labels, dtype=np.uint8)
-            _check(lib().hps_train_batch(self._h, o.size - 1, _ptr(o), _ptr(k), _ptr(lab),
-                                         0, ctypes.byref(st)))
+            return (n, ctypes.c_void_p(int(offsets[0])), ctypes.c_void_p(int(keys)),
+                    ctypes.c_void_p(int(labels)), 1), None
+        o = np.ascontiguousarray(offsets, dtype=np.int64)
+        k = _u64(keys)
+        lab = np.ascontiguousarray(labels, dtype=np.uint8)
+        return (o.size - 1, _ptr(o), _ptr(k), _ptr(lab), 0), (o, k, lab)
+
+    def train_batch(self, offsets, keys, labels, on_device: bool = False) -> HpsBatchStats:
+        st = HpsBatchStats()
+        args, keep = self._batch_args(offsets, keys, labels, on_device)
+        _check(lib().hps_train_batch(self._h, *args, ctypes.byref(st)))
+        del keep
+        return st
+
+    def submit_batch(self, offsets, keys, labels, on_device: bool = False) -> None:
+        """Pipelined train_batch (hps_submit_batch): returns once the batch is
+        staged and enqueued; results come from wait_batch() in order."""
+        args, keep = self._batch_args(offsets, keys, labels, on_device)
+        _check(lib().hps_submit_batch(self._h, *args))
+        del keep
+
+    def wait_batch(self) -> HpsBatchStats:
+        st = HpsBatchStats()
+        _check(lib().hps_wait_batch(self._h, ctypes.byref(st)))
         return st
 
     def set_timing(self, on: bool) -> None:

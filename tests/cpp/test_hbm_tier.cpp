@@ -163,6 +163,7 @@ static void fused_batch_case() {
     for (std::uint64_t i = 0; i <= B; ++i) bo[i] = off[b * B + i] - off[b * B];
     h.train_batch(B, bo.data(), keys.data() + off[b * B], lab.data() + b * B);
   }
+  h.flush();  // deferred write-backs -> store
   const auto dense = h.dense();
   or_cfg c{};
   c.nodes = 1;

@@ -31,7 +31,8 @@ def new_tier(world, rank, **kw):
     return pkg.Tier(nodes=1, devices=world, rank=rank, cuda_device=rank, nccl_id=obj[0], **kw)
 
 
-def case_train(world, rank, oracle, E, layers, J, zipf, dims, B, nb, nnz, det=True):
+def case_train(world, rank, oracle, E, layers, J, zipf, dims, B, nb, nnz, det=True,
+               pipelined=False):
     off, keys, lab = pkg.gen_dataset(dims, B * nb + 3, nnz, zipf=zipf, seed=7)
     max_keys = int(max(off[min((b + 1) * B, len(off) - 1)] - off[b * B] for b in range(nb + 1)))
     tier = new_tier(world, rank, width=E, layer_dims=layers, minibatches=J, key_space=dims,
@@ -39,9 +40,17 @@ def case_train(world, rank, oracle, E, layers, J, zipf, dims, B, nb, nnz, det=Tr
     store = np.zeros((dims, E), dtype=np.float32)
     tier.attach_store(store)
     n = len(off) - 1
-    for b in range((n + B - 1) // B):
+    nbat = (n + B - 1) // B
+    for b in range(nbat):
         e0, e1 = b * B, min((b + 1) * B, n)
-        tier.train_batch(off[e0:e1 + 1] - off[e0], keys[off[e0]:off[e1]], lab[e0:e1])
+        if pipelined:  # two batches in flight (hps_submit_batch / hps_wait_batch)
+            tier.submit_batch(off[e0:e1 + 1] - off[e0], keys[off[e0]:off[e1]], lab[e0:e1])
+            if b:
+                tier.wait_batch()
+        else:
+            tier.train_batch(off[e0:e1 + 1] - off[e0], keys[off[e0]:off[e1]], lab[e0:e1])
+    if pipelined:
+        tier.wait_batch()
     dense = tier.get_dense()
     tier.close()
     wd, wk, wr = oracle.train_reference(make_cfg(1, world, E, layers, J=J), B, off, keys, lab)
@@ -161,6 +170,8 @@ def main():
     # many same-shape batches: captured-graph replays across both table parities
     results["train_replays"] = case_train(world, rank, oracle, 16, (8, 16, 1), 4, True, 50000,
                                           1024, 9, 30)
+    results["train_pipelined"] = case_train(world, rank, oracle, 16, (8, 16, 1), 4, True, 50000,
+                                            1024, 9, 30, pipelined=True)
     flags = torch.tensor([int(v) for v in results.values()], device="cuda")
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:

@@ -130,11 +130,12 @@ def test_loss_decreases_on_learnable_data(pkg):
 def test_graph_replays_bit_exact(pkg, oracle):
     """Same-shape batches make hps_train_batch replay its captured CUDA graph
     (both table parities); every replay must still be bit-exact, and equal to
-    the kernel-by-kernel (non-graph) execution."""
+    the kernel-by-kernel (non-graph) execution and to a run that flushes the
+    deferred write-back after every batch."""
     dims, B, nnz, nb = 20000, 512, 20, 9
     off, keys, lab = pkg.gen_dataset(dims, B * nb, nnz, zipf=True, seed=21)
     outs = []
-    for graphs in (True, False):
+    for graphs, flush_each in ((True, False), (False, False), (True, True)):
         tier = pkg.Tier(width=8, layer_dims=(8, 16, 1), minibatches=4, key_space=dims,
                         max_batch_examples=B, max_batch_keys=B * nnz)
         tier.set_graphs(graphs)
@@ -143,6 +144,8 @@ def test_graph_replays_bit_exact(pkg, oracle):
         for b in range(nb):
             tier.train_batch(off[b * B:(b + 1) * B + 1] - off[b * B],
                              keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B])
+            if flush_each:  # the deferred write-back never changes the result
+                tier.flush()
         outs.append((tier.get_dense(), store))
         tier.close()
     wd, wk, wr = oracle.train_reference(make_cfg(1, 1, 8, (8, 16, 1), J=4), B, off, keys, lab)
@@ -165,9 +168,64 @@ def test_dump_after_sort_free_build(pkg, oracle):
         tier.train_batch(off[b * B:(b + 1) * B + 1] - off[b * B],
                          keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B])
     dk, dr = tier.dump()
+    tier.flush()  # the second batch's write-back is deferred until here
     want = np.unique(keys[off[B]:off[2 * B]])
     assert np.array_equal(dk, want)
     assert np.array_equal(dr, store[want.astype(np.int64)])
     slots = tier.table_slots()
     assert np.array_equal(slots, oracle.table_build(want))  # layout == ascending insert
     tier.close()
+
+
+@pytest.mark.parametrize("store_kind", ["host", "device", "none"])
+def test_pipelined_submit_wait_bit_exact(pkg, oracle, store_kind):
+    """hps_submit_batch / hps_wait_batch keep two batches in flight: the next
+    batch's table is built (rows prefetched, from the table two builds back
+    or the store) beside the running body, write-backs are deferred. Results
+    must equal the oracle bit for bit, and equal hps_train_batch's, for a host
+    (zero-copy) store, an HBM store and no store (zeros for new rows)."""
+    import torch
+    dims, B, nnz, nb = 20000, 512, 20, 8
+    off, keys, lab = pkg.gen_dataset(dims, B * nb, nnz, zipf=True, seed=33)
+    tier = pkg.Tier(width=8, layer_dims=(8, 16, 1), minibatches=4, key_space=dims,
+                    max_batch_examples=B, max_batch_keys=B * nnz)
+    if store_kind == "host":
+        store = np.zeros((dims, 8), dtype=np.float32)
+        tier.attach_store(store)
+    elif store_kind == "device":
+        dstore = torch.zeros((dims, 8), dtype=torch.float32, device="cuda")
+        tier.attach_store(dstore.data_ptr(), on_device=True, num_keys=dims)
+    stats = []
+    for b in range(nb):
+        tier.submit_batch(off[b * B:(b + 1) * B + 1] - off[b * B],
+                          keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B])
+        if b % 3 == 2:  # waits lag submits irregularly
+            stats.append(tier.wait_batch())
+    while len(stats) < nb:
+        stats.append(tier.wait_batch())
+    with pytest.raises(pkg.Error):
+        tier.wait_batch()  # nothing left in flight
+    tier.flush()
+    dense = tier.get_dense()
+    tier.close()
+    if store_kind == "device":
+        torch.cuda.synchronize()
+        store = dstore.cpu().numpy()
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, 8, (8, 16, 1), J=4), B, off, keys, lab)
+    if store_kind == "none":
+        # no store: a key that left the table restarts from zeros; the dense
+        # weights must still match a plain train_batch run
+        ref = pkg.Tier(width=8, layer_dims=(8, 16, 1), minibatches=4, key_space=dims,
+                       max_batch_examples=B, max_batch_keys=B * nnz)
+        for b in range(nb):
+            ref.train_batch(off[b * B:(b + 1) * B + 1] - off[b * B],
+                            keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B])
+        assert np.array_equal(dense, ref.get_dense())
+        ref.close()
+        return
+    assert np.array_equal(dense, wd)
+    assert np.array_equal(store[wk.astype(np.int64)], wr)
+    assert all(s.examples == B for s in stats)
+    # rows read from the store + carried + proxied == working set
+    assert all(s.store_rows + s.carried_rows <= s.working_set for s in stats)
+    assert any(s.store_rows + s.carried_rows < s.working_set for s in stats[2:])
