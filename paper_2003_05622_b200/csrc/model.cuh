@@ -51,6 +51,7 @@ template <int LPE>
 __global__ void __launch_bounds__(128)
     fwd_bwd_kernel(ModelDims md, ShardMap sm, const float* __restrict__ dense,
                    const std::uint32_t* __restrict__ occ_off,
+                   const std::int64_t* __restrict__ goff,  // non-null: occurrence = batch index
                    const std::uint32_t* __restrict__ occ_row,  // row of each occurrence
                    const float* __restrict__ rows,
                    const std::uint8_t* __restrict__ labels,
@@ -85,7 +86,15 @@ __global__ void __launch_bounds__(128)
     // (the group's lanes load LPE row ids at once, every lane then issues its
     // LPE independent row loads before the in-order f64 chain)
     if (active) {
-      const std::uint32_t o0 = occ_off[k], o1 = occ_off[k + 1];
+      std::uint32_t o0, o1;
+      if (goff) {
+        const std::uint64_t ex = sm.first + k * sm.stride;
+        o0 = std::uint32_t(goff[ex]);
+        o1 = std::uint32_t(goff[ex + 1]);
+      } else {
+        o0 = occ_off[k];
+        o1 = occ_off[k + 1];
+      }
       for (int d0 = 0; d0 < E; d0 += LPE) {
         const int d = d0 + sub;
         double acc = 0.0;

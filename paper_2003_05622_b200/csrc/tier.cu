@@ -34,6 +34,7 @@
 #include "p2p.cuh"
 #include "sort.cuh"
 #include "table.cuh"
+#include "group.cuh"
 #include "tier_internal.h"
 
 namespace hpsgpu {
@@ -279,6 +280,14 @@ struct Tier {
   // zero-copy kernels on a host store run on a few SMs only: a PCIe access
   // stalls the memory pipeline of the SM issuing it for everyone on that SM
   unsigned pf_ctas = 8, wb_ctas = 4;
+  bool hash_dedup = true;                // group.cuh at G == 1 (HPS_DEDUP=sort: radix sort)
+  std::uint32_t* gcnt = nullptr;         // [capmax] per-slot occurrence counters (kept zero)
+  std::uint32_t* slot_uid = nullptr;     // [capmax]
+  std::uint32_t* occ_slot = nullptr;     // [S] slot of each occurrence
+  std::uint32_t* part_slot = nullptr;    // [kGroupParts][part_cap] claimed slots
+  std::uint32_t* part_n = nullptr;       // [kGroupParts * kGroupPartStride] claim counters
+  std::uint32_t* part_base = nullptr;    // [kGroupParts]
+  std::uint64_t part_cap = 0;
   // HPS_TRACE=1: timed events at the pipeline's stage boundaries, printed
   // per batch to stderr at completion (diagnostics)
   bool trace = false;
@@ -1195,18 +1204,71 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     const Count on_n{&T->dsc->counts[bp.sp][j], 0};
     const std::uint64_t ob = sh.mb_bound[j];
     const ShardMap sm{s, GJ, n};
-    // shard gather + dedup (a5)
-    if (n) {
-      tile_scan(T, ShardLen{sm, doff}, ShardLenEmit{T->occ_off, n}, Count{nullptr, n}, n,
-                &T->L->d->total);
-      launch(T, shard_gather_kernel, grid_for(n * 32), 256, 0, sm, doff, dkeys,
-             (const std::uint32_t*)T->occ_off, T->L->kB, T->L->vB, T->ex_of);
-    }
+    // shard dedup (a5) + pull (a6)
     PullPlan plan;
-    if (G > 1) begin_round(T, false);
-    HPS_TRY(dedup_pull(T, T->L->kB, T->L->vB, on_n, ob, &plan, true, true));
-    // compute (a7, a8, a9); rows are in uid order at every G
-    const std::uint32_t* occ_row = T->inv;
+    const std::uint32_t* occ_row = T->inv;  // occurrence -> row of `rows`
+    const float* rows = T->rows;
+    const std::int64_t* goff = nullptr;      // occurrence ids: shard-local (sort path)
+    if (G == 1 && T->hash_dedup &&
+        std::size_t(kGroupWarpThreads / 32) * 8 * ((n + 31) / 32) <= kGroupSmemMax) {
+      // grouped by batch-table slot (group.cuh): no sort, and the rows are
+      // read in place from the table
+      // counters: n_long (warp segments), n_big (repeats), n_items (CTA segments)
+      HPS_CUDA(cudaMemsetAsync(&T->dsc->n_long, 0, 24, T->st));
+      HPS_CUDA(cudaMemsetAsync(&T->dsc->U, 0, 8, T->st));
+      if (n) {
+        const std::uint32_t pcap = std::uint32_t(T->part_cap);
+        const std::uint64_t warps = ((n + 31) / 32) * kGroupPosGroups;
+        launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys,
+               (const std::uint64_t*)T->tkeys[T->cur],
+               (const std::uint64_t*)&T->dsc->cap[T->cur], T->gcnt, T->slot_uid, T->part_slot,
+               pcap, T->part_n, T->occ_slot, T->uidv, T->ex_of, &T->dsc->err);
+        launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)T->part_n,
+               (const std::uint32_t*)T->part_slot, pcap, T->part_base, T->slots,
+               (unsigned long long*)&T->dsc->U);
+        tile_scan(T, UidCount{T->slots, T->gcnt}, SegEmit{T->seg, Count{&T->dsc->U, 0}},
+                  Count{&T->dsc->U, 0}, ob, &T->L->d->total);
+        launch(T, group_place_kernel, grid_for(n * 32), 256, 0, sm, doff,
+               (const std::uint32_t*)T->occ_slot, (const std::uint32_t*)T->uidv,
+               (const std::uint32_t*)T->slot_uid, pcap, (const std::uint32_t*)T->part_base,
+               (const std::uint32_t*)T->seg, T->pos, T->inv);
+        launch(T, group_order_kernel, grid_for(ob), 256, 0,
+               (const unsigned long long*)&T->dsc->U, (const std::uint32_t*)T->seg, T->pos,
+               (const std::uint32_t*)T->ex_of, (const std::uint32_t*)T->slots, T->gcnt, T->exs,
+               T->long_list, &T->dsc->n_long, T->big_list, &T->dsc->n_items, T->part_n);
+        const std::uint32_t words = std::uint32_t((n + 31) / 32);
+        const std::size_t wsmem = std::size_t(kGroupWarpThreads / 32) * 2 * words * 4;
+        // (orank: the S-sized owner-rank buffer, unused at G == 1, collects the
+        // segments whose examples repeat the key)
+        launch(T, group_warp_kernel, kSMs * 4, kGroupWarpThreads, wsmem,
+               (const unsigned long long*)&T->dsc->n_long, (const std::uint32_t*)T->long_list,
+               (const std::uint32_t*)T->seg, (const std::uint32_t*)T->pos,
+               (const std::uint32_t*)T->ex_of, words, T->exs, T->orank, &T->dsc->n_big);
+        launch(T, group_cta_kernel, kSMs, kGroupThreads, std::size_t(2) * words * 4,
+               (const unsigned long long*)&T->dsc->n_items, (const std::uint32_t*)T->big_list,
+               (const std::uint32_t*)T->seg, (const std::uint32_t*)T->pos,
+               (const std::uint32_t*)T->ex_of, words, T->exs, T->orank, &T->dsc->n_big);
+        launch(T, group_dup_kernel, kSMs, kGroupThreads, 0,
+               (const unsigned long long*)&T->dsc->n_big, (const std::uint32_t*)T->orank,
+               (const std::uint32_t*)T->seg, (const std::uint32_t*)T->pos,
+               (const std::uint32_t*)T->ex_of, T->exs);
+      }
+      mark(T, HPS_T_DEDUP);
+      mark(T, HPS_T_PULL);
+      occ_row = T->occ_slot;
+      rows = T->tvals[T->cur];
+      goff = doff;  // occurrence ids are batch key indices
+    } else {
+      if (n) {
+        tile_scan(T, ShardLen{sm, doff}, ShardLenEmit{T->occ_off, n}, Count{nullptr, n}, n,
+                  &T->L->d->total);
+        launch(T, shard_gather_kernel, grid_for(n * 32), 256, 0, sm, doff, dkeys,
+               (const std::uint32_t*)T->occ_off, T->L->kB, T->L->vB, T->ex_of);
+      }
+      if (G > 1) begin_round(T, false);
+      HPS_TRY(dedup_pull(T, T->L->kB, T->L->vB, on_n, ob, &plan, true, true));
+    }
+    // compute (a7, a8, a9); rows are in uid order (or table slots) at every G
     if (n) {
       const int LPE = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
       const int epb = 128 / LPE;
@@ -1215,7 +1277,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
       const unsigned blocks = unsigned(std::min<std::uint64_t>((n + epb - 1) / epb, kSMs * 8));
       auto k = LPE == 8 ? fwd_bwd_kernel<8> : (LPE == 16 ? fwd_bwd_kernel<16> : fwd_bwd_kernel<32>);
       launch(T, k, blocks, 128, smem, T->md, sm, (const float*)T->dense,
-             (const std::uint32_t*)T->occ_off, occ_row, (const float*)T->rows, dlab, T->H,
+             (const std::uint32_t*)T->occ_off, goff, occ_row, rows, dlab, T->H,
              T->DL, T->DX, &T->dsc->loss, &T->dsc->err);
       mark(T, HPS_T_FWDBWD);
       // dense-grad reduce on the side stream, overlapping the sparse reduce
@@ -1624,6 +1686,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_PF_CTAS")) t->pf_ctas = unsigned(std::max(1, std::atoi(v)));
   if (const char* v = std::getenv("HPS_WB_CTAS")) t->wb_ctas = unsigned(std::max(1, std::atoi(v)));
   if (const char* v = std::getenv("HPS_TRACE")) t->trace = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_DEDUP")) t->hash_dedup = std::strcmp(v, "sort") != 0;
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
@@ -1720,6 +1783,10 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     cudaFuncSetAttribute(fwd_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(group_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kGroupSmemMax));
+    cudaFuncSetAttribute(group_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kGroupSmemMax));
   }
   const std::uint64_t O = t->Omax, W = t->Wmax, E = std::uint64_t(t->E);
   hps_status s = HPS_OK;
@@ -1739,6 +1806,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   }
   A(need_key, W);
   A(need_slot, W);
+  A(gcnt, t->capmax);
+  A(slot_uid, t->capmax);
   t->ws = t->wsb[0];
   t->ws_idx = t->wsib[0];
   t->wsset_cap = 1;
@@ -1773,6 +1842,11 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(slots, S);
   A(exs, S);
   A(orank, S);
+  A(occ_slot, S);
+  t->part_cap = S;  // a partition can never overflow
+  A(part_slot, std::uint64_t(kGroupParts) * S);
+  A(part_n, std::uint64_t(kGroupParts) * kGroupPartStride);
+  A(part_base, kGroupParts);
   A(otot, kMaxRanks);
   A(long_list, S);
   A(big_list, S / (kLongSeg + 1) + 2);
@@ -1792,6 +1866,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
 #undef A
+  cudaMemsetAsync(t->gcnt, 0, t->capmax * 4, t->st);
+  cudaMemsetAsync(t->part_n, 0, std::uint64_t(kGroupParts) * kGroupPartStride * 4, t->st);
   cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
   cudaMemsetAsync(t->key_done, 0, (S / (kLongSeg + 1) + 2) * 4, t->st);
   if ((e = cudaMemsetAsync(t->dsc, 0, sizeof(Scalars), t->st)) != cudaSuccess)

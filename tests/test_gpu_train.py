@@ -229,3 +229,35 @@ def test_pipelined_submit_wait_bit_exact(pkg, oracle, store_kind):
     # rows read from the store + carried + proxied == working set
     assert all(s.store_rows + s.carried_rows <= s.working_set for s in stats)
     assert any(s.store_rows + s.carried_rows < s.working_set for s in stats[2:])
+
+
+@pytest.mark.parametrize("dedup", ["hash", "sort"])
+def test_duplicate_keys_within_examples(pkg, oracle, dedup, monkeypatch):
+    """A key repeated inside one example is two occurrences (embed_sum adds
+    its row twice, backward accumulates it twice, model.hpp:59-117,182-187).
+    Both mini-batch dedup paths (slot grouping, group.cuh; radix sort) must
+    keep the occurrence order and match the oracle bit for bit. Hot keys make
+    long segments (the bitmap-ranked path)."""
+    monkeypatch.setenv("HPS_DEDUP", dedup)
+    rng = np.random.default_rng(12)
+    dims, n = 3000, 1500
+    lens = rng.integers(1, 60, size=n)
+    rows = []
+    for l in lens:
+        k = rng.integers(0, dims, size=l)
+        k[: l // 3] = rng.integers(0, 8, size=l // 3)  # hot, often repeated
+        rows.append(k)
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    keys = np.concatenate(rows).astype(np.uint64)
+    lab = rng.integers(0, 2, size=n).astype(np.uint8)
+    check_bit_exact(oracle, pkg, off, keys, lab, 512, E=8, layers=(8, 16, 1), J=4, dims=dims)
+
+
+def test_sort_dedup_path_bit_exact(pkg, oracle, monkeypatch):
+    """The radix-sort mini-batch dedup (HPS_DEDUP=sort, the G > 1 path)
+    stays bit-exact at G = 1 too."""
+    monkeypatch.setenv("HPS_DEDUP", "sort")
+    dims, B, nnz = 30000, 512, 20
+    off, keys, lab = pkg.gen_dataset(dims, B * 3, nnz, zipf=True, seed=5)
+    check_bit_exact(oracle, pkg, off, keys, lab, B, E=16, layers=(8, 16, 1), J=4, dims=dims)

@@ -195,7 +195,7 @@ int main() {
     const ShardMap sm{0, 1, n};
     t = time_ms([&] {
       fwd_bwd_kernel<16><<<std::min<std::uint64_t>((n + epb - 1) / epb, kSMs * 8), 128, smem>>>(
-          md, sm, dw, doff, drow, drows, dlab, H, DL, DX, dloss, derr);
+          md, sm, dw, doff, (const std::int64_t*)nullptr, drow, drows, dlab, H, DL, DX, dloss, derr);
     });
     CK(cudaGetLastError());
     printf("fwd_bwd_kernel<16> n=%llu x %u features: %.2f us\n", (unsigned long long)n, nnz,
