@@ -357,13 +357,21 @@ def run_ours(args, rank, world, local_rank):
     per_key_pull = 8 + 8 + 4 * E + 4 * E   # key + slot probe + row read + row write
     per_key_apply = 4 + 12 * E             # slot + delta read + row read + row write
     per_key_build = 8 + 8 + 4 * E + 4 * E
+    # sparse segment-reduce (a8, a9): per occurrence its example's dL/dx row
+    # (E f64) + the example id; per unique key its segment bounds + delta row
+    per_occ_sparse, per_key_sparse = 8 * E + 4, 8 + 4 * E
     phase_bytes = {
+        "sparse": occ * per_occ_sparse + pulled * per_key_sparse,
         "pull": pulled * per_key_pull,
         "apply": pulled * per_key_apply,
-        "build": ws * per_key_build + occ / J * 0,  # table part only
+        "build": ws * per_key_build,
         "writeback": ws * per_key_pull,
         "dedup": 12 * occ + 8 * pulled,
     }
+    if world == 1 and os.environ.get("HPS_DEDUP", "hash") != "sort":
+        # G = 1: fwd/bwd reads the rows in place from the table (a6 fused), so
+        # there is no pull kernel to put on the roofline
+        phase_bytes.pop("pull")
     rl = {}
     for name, nbytes in phase_bytes.items():
         ms = phases.get(name, 0.0)
@@ -371,7 +379,7 @@ def run_ours(args, rank, world, local_rank):
             gbs = nbytes / (ms / 1e3) / 1e9
             rl[name] = {"ms_per_step": ms / K, "algorithmic_bytes_per_step": nbytes / K,
                         "achieved_gbs": gbs, "frac": gbs / peak}
-    dominant = os.environ.get("HPS_ROOFLINE_KERNEL", "pull")
+    dominant = os.environ.get("HPS_ROOFLINE_KERNEL", "sparse")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -381,11 +389,15 @@ def run_ours(args, rank, world, local_rank):
         except Exception:
             traffic = None
     dom = rl.get(dominant, {})
-    roofline = {"bound": "hbm", "kernel": {"pull": "table_gather_kernel<4>",
-                                           "apply": "table_apply_kernel<4>"}.get(dominant, dominant),
+    names = {"sparse": "sparse segment-reduce + sgd_delta (sparse_short_kernel, big_plan/"
+                       "big_p1/big_p2_kernel), per mini-batch",
+             "pull": "table_gather_kernel<4>", "apply": "table_apply_kernel<4>"}
+    models = {"sparse": "O*(8E+4) + U*(8+4E)", "pull": "U*(8+8+8E)", "apply": "U*(4+12E)"}
+    roofline = {"bound": "hbm", "kernel": names.get(dominant, dominant),
                 "achieved": dom.get("achieved_gbs"), "peak": peak, "unit": "GB/s",
                 "frac": dom.get("frac"), "traffic": traffic, "peak_kind": peak_kind,
-                "bytes_model": {"pull": "U*(8+8+8E)", "apply": "U*(4+12E)"}.get(dominant),
+                "bytes_model": models.get(dominant),
+                "launches_per_step": J if dominant in ("sparse", "pull", "apply") else 1,
                 "phases": rl}
 
     # ---------------- CPU baseline (reference hot path, rank 0, N=1) ---------

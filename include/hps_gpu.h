@@ -88,7 +88,7 @@ typedef struct {
 
 /* Phase slots of hps_get_timing (ms accumulated over hps_train_batch calls,
  * measured with CUDA events on the tier's stream). */
-#define HPS_TIMING_SLOTS 10
+#define HPS_TIMING_SLOTS 11
 enum {
   HPS_T_TOTAL = 0,     /* whole batch */
   HPS_T_STAGE = 1,     /* H2D of the batch + per-shard counts (one D2H) */
@@ -99,7 +99,9 @@ enum {
   HPS_T_GRADS = 6,     /* dense-grad reduce + sparse segment-reduce (a8, a9) */
   HPS_T_APPLY = 7,     /* push exchange + canonical owner apply (a10, a11) */
   HPS_T_DENSE = 8,     /* dense sync + update (a12) */
-  HPS_T_WRITEBACK = 9  /* rows back to the value store (a13) */
+  HPS_T_WRITEBACK = 9, /* rows back to the value store (a13) */
+  HPS_T_SPARSE = 10    /* sparse segment-reduce + sgd_delta (a8, a9); GRADS is
+                          then the wait for the dense-grad reduce beside it */
 };
 
 const char* hps_last_error(void);

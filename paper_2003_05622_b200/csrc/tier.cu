@@ -1290,6 +1290,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                 T->dgrad, &T->dsc->fallbacks);
       HPS_CUDA(cudaEventRecord(T->join, T->st2));
       HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob));
+      mark(T, HPS_T_SPARSE);
       HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
     } else {
       HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));

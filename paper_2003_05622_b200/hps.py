@@ -78,7 +78,7 @@ class HpsBatchStats(ctypes.Structure):
     ]
 
 TIMING_SLOTS = ["total", "stage", "build", "dedup", "pull", "fwdbwd", "grads", "apply",
-                "dense", "writeback"]
+                "dense", "writeback", "sparse"]
 
 
 # Every symbol include/hps_gpu.h declares, with its ctypes signature.
