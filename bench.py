@@ -224,7 +224,7 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    LAG = 2  # waits trail submits by two: three batches in flight
+    LAG = 3  # waits trail submits by three: four batches in flight
 
     def timed_steps(submit_fn, n_steps, first):
         """Returns (event ms over the whole run of n_steps, per-step stats).

@@ -212,9 +212,12 @@ hps_status hps_train_batch(hps_tier_t h, uint64_t num_examples,
  * counts; the host blocks only on that round-trip), enqueues its table build
  * beside the previous batch's body, its body and its write-back, and returns.
  * hps_wait_batch returns the results of the oldest submitted batch not yet
- * waited for, in submission order. At most three batches are in flight (a
- * fourth submit first completes the oldest; its result stays queued). The caller's
- * buffers may be reused as soon as hps_submit_batch returns. Results are
+ * waited for, in submission order. At most four batches are in flight (a
+ * fifth submit first completes the oldest; its result stays queued). Device
+ * buffers and pageable host buffers may be reused as soon as hps_submit_batch
+ * returns; pinned host buffers are copied asynchronously and must stay
+ * unchanged until the batch's hps_wait_batch (the cudaMemcpyAsync rule). A
+ * key outside key_space is reported by hps_wait_batch. Results are
  * bit-identical to hps_train_batch on the same batches. COLLECTIVE. Every
  * other entry point completes all in-flight batches first. */
 hps_status hps_submit_batch(hps_tier_t h, uint64_t num_examples,

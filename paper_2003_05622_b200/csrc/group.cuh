@@ -16,7 +16,7 @@
 //                       the first touch of a slot claims its uid.
 //   (tile scan)         seg = exclusive scan of the uid counts.
 //   group_compact_kernel dense uids from the partitioned claims.
-//   group_place_kernel  occurrence q -> position seg[uid] + ticket; inv[q].
+//   group_place_kernel  occurrence q -> position seg[uid] + ticket.
 // Occurrence ids are batch key indices (off[ex] + position): unique, and in
 // the shard's occurrence order.
 //   group_order_kernel  segments <= kGroupShort: one thread sorts its few
@@ -178,8 +178,8 @@ struct SegEmit {
 };
 
 // Occurrence q (a batch key index of this shard) -> its position in the
-// segment (unordered for now) and inv[q]. One warp per example, lanes over
-// its positions.
+// segment (unordered for now). One warp per example, lanes over its
+// positions.
 __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__ off,
                                    const std::uint32_t* __restrict__ occ_slot,
                                    const std::uint32_t* __restrict__ tick,
@@ -187,8 +187,7 @@ __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__
                                    std::uint32_t part_cap,
                                    const std::uint32_t* __restrict__ part_base,
                                    const std::uint32_t* __restrict__ seg,
-                                   std::uint32_t* __restrict__ seg_occ,
-                                   std::uint32_t* __restrict__ inv) {
+                                   std::uint32_t* __restrict__ seg_occ) {
   __shared__ std::uint32_t pb[kGroupParts];
   if (threadIdx.x < kGroupParts) pb[threadIdx.x] = part_base[threadIdx.x];
   __syncthreads();
@@ -201,7 +200,6 @@ __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__
     for (std::int64_t q = b + lane; q < e; q += 32) {
       const std::uint32_t u = dense_uid(slot_uid[occ_slot[q]], part_cap, pb);
       seg_occ[seg[u] + tick[q]] = std::uint32_t(q);
-      inv[q] = u;
     }
   }
 }

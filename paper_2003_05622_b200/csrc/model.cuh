@@ -457,9 +457,11 @@ __device__ __forceinline__ void write_delta(float* out, std::uint64_t row, int E
   out[row * E + d] = -__fmul_rn(lr, g);
 }
 
-// Short segments, exact: one thread per (unique key, dim) sums the key's
-// occurrences in example order (4 independent loads per step, the adds in
-// order). Longer segments are queued for the chunked CTA path.
+// Short segments, exact: one thread per (unique key, DPT dims) sums the key's
+// occurrences in example order; its DPT dimension chains are independent
+// (DPT-wide row loads, DPT adds in flight), each in the reference order.
+// Longer segments are queued for the chunked CTA path.
+template <int DPT>
 __global__ void __launch_bounds__(256)
     sparse_short_kernel(int E, float lr, std::uint64_t n, const std::uint64_t* __restrict__ u_ptr,
                         const std::uint32_t* __restrict__ seg,
@@ -474,14 +476,15 @@ __global__ void __launch_bounds__(256)
   const std::uint64_t U = *u_ptr;
   if (pulled && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(pulled, (unsigned long long)U);
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-  const std::uint64_t total = U * std::uint64_t(E);
+  const int parts = E / DPT;
+  const std::uint64_t total = U * std::uint64_t(parts);
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < total;
        t += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint64_t u = t / std::uint64_t(E);
-    const int d = int(t - u * E);
+    const std::uint64_t u = t / std::uint64_t(parts);
+    const int d0 = int(t - u * parts) * DPT;
     const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
     if (p1 - p0 > std::uint32_t(kLongSeg)) {
-      if (d == 0) {
+      if (d0 == 0) {
         if (p1 - p0 > medium_max)
           big_list[atomicAdd(n_big, 1ull)] = std::uint32_t(u);
         else
@@ -489,16 +492,38 @@ __global__ void __launch_bounds__(256)
       }
       continue;
     }
-    double acc = 0.0;
+    double acc[DPT];
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) acc[i] = 0.0;
     std::uint32_t p = p0;
-    for (; p + 4 <= p1; p += 4) {
-      const std::uint32_t e0 = exs[p], e1 = exs[p + 1], e2 = exs[p + 2], e3 = exs[p + 3];
-      const double x0 = DX[std::uint64_t(e0) * E + d], x1 = DX[std::uint64_t(e1) * E + d];
-      const double x2 = DX[std::uint64_t(e2) * E + d], x3 = DX[std::uint64_t(e3) * E + d];
-      acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, x0), x1), x2), x3);
+    for (; p + 2 <= p1; p += 2) {  // two rows in flight
+      const double* r0 = DX + std::uint64_t(exs[p]) * E + d0;
+      const double* r1 = DX + std::uint64_t(exs[p + 1]) * E + d0;
+      double x0[DPT], x1[DPT];
+      if (DPT == 4) {
+        const double2 a0 = *reinterpret_cast<const double2*>(r0);
+        const double2 b0 = *reinterpret_cast<const double2*>(r0 + 2);
+        const double2 a1 = *reinterpret_cast<const double2*>(r1);
+        const double2 b1 = *reinterpret_cast<const double2*>(r1 + 2);
+        x0[0] = a0.x; x0[1 % DPT] = a0.y; x0[2 % DPT] = b0.x; x0[3 % DPT] = b0.y;
+        x1[0] = a1.x; x1[1 % DPT] = a1.y; x1[2 % DPT] = b1.x; x1[3 % DPT] = b1.y;
+      } else {
+#pragma unroll
+        for (int i = 0; i < DPT; ++i) {
+          x0[i] = r0[i];
+          x1[i] = r1[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(__dadd_rn(acc[i], x0[i]), x1[i]);
     }
-    for (; p < p1; ++p) acc = __dadd_rn(acc, DX[std::uint64_t(exs[p]) * E + d]);
-    write_delta(out, pos ? pos[u] : u, E, d, acc, inv_n, lr);
+    if (p < p1) {
+      const double* r0 = DX + std::uint64_t(exs[p]) * E + d0;
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(acc[i], r0[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) write_delta(out, pos ? pos[u] : u, E, d0 + i, acc[i], inv_n, lr);
   }
 }
 
@@ -611,17 +636,10 @@ __global__ void __launch_bounds__(kLongThreads)
   }
 }
 
-// ---- big segments (> kBigChunk occurrences): split over CTAs -------------
+// ---- big segments (> kLongSeg occurrences): split over CTAs --------------
 //
-// Work item w = (big key, chunk of kBigChunk occurrences). big_plan: prefix
-// of the per-key chunk counts. p1: per (item, slice, dim) Neumaier total and
-// sum|x|. p2: the item's offset is the total of the key's earlier chunks and
-// slices; the slice is re-walked for B; the key's last CTA combines all
-// chunks, certifies (certify_f32) and, rarely, recomputes the exact chain.
-constexpr int kBigThreads = 256;
-struct BigPart {
-  double hi, lo, a, b;
-};
+// Work item w = (big key, chunk of fuse_chunk(E) occurrences). big_plan:
+// prefix of the per-key chunk counts; big_fused_kernel (below) does the rest.
 struct ChunkSum {  // one chunk of one dimension: total (Neumaier), sum|x|, B bound
   double hi, lo, a, b;
 };
@@ -676,36 +694,73 @@ __device__ __forceinline__ void big_item(const std::uint32_t* chunk_off, std::ui
   *chunk = std::uint32_t(w - chunk_off[lo]);
 }
 
-__global__ void __launch_bounds__(kBigThreads)
-    big_p1_kernel(int E, int chunk, const std::uint32_t* __restrict__ big_list,
-                  const unsigned long long* __restrict__ n_big,
-                  const std::uint32_t* __restrict__ chunk_off,
-                  const unsigned long long* __restrict__ n_items,
-                  const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
-                  const double* __restrict__ DX, BigPart* __restrict__ part,
-                  ChunkSum* __restrict__ chunk_tot) {
-  __shared__ double sh[kBigThreads], sl[kBigThreads], sa[kBigThreads];
-  const int slices = kBigThreads / E;
+// ---- big segments: one fused kernel ---------------------------------------
+//
+// Work items (key, chunk) are taken in ticket order. A CTA loads its chunk's
+// values once into registers (kFusePer per thread and dimension), publishes
+// the chunk's per-dimension Neumaier total (flag), takes its prefix offset
+// from the totals of the key's earlier chunks (they hold earlier tickets, so
+// they are running or done and publish before they wait: no deadlock, no
+// serial chain), then computes its share of B from the same registers. The
+// key's last CTA combines all chunks and certifies (certify_f32), recomputing
+// the exact chain for any uncertified dimension.
+constexpr int kFuseThreads = 256;
+constexpr int kFusePer = 16;  // occurrences per slice of a chunk
+inline int fuse_chunk(int E) { return (kFuseThreads / E) * kFusePer; }
+
+__global__ void __launch_bounds__(kFuseThreads)
+    big_fused_kernel(int E, float lr, std::uint64_t n, const std::uint32_t* __restrict__ big_list,
+                     const unsigned long long* __restrict__ n_big,
+                     const std::uint32_t* __restrict__ chunk_off,
+                     const unsigned long long* __restrict__ n_items,
+                     const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
+                     const std::uint32_t* __restrict__ pos, const double* __restrict__ DX,
+                     ChunkSum* __restrict__ chunk_tot, unsigned* __restrict__ flags,
+                     unsigned long long* __restrict__ ticket, unsigned* __restrict__ key_done,
+                     float* __restrict__ out, unsigned long long* __restrict__ fallbacks) {
+  __shared__ double sh[kFuseThreads], sl[kFuseThreads], sa[kFuseThreads], sb[kFuseThreads];
+  __shared__ double stage[kFallbackChunk];
+  __shared__ bool bad[kFuseThreads];
+  __shared__ unsigned long long s_item;
+  __shared__ unsigned s_last;
+  const int slices = kFuseThreads / E;
+  const int chunk = slices * kFusePer;
   const int s = threadIdx.x / E, d = threadIdx.x - s * E;
+  const bool worker = s < slices;
   const std::uint64_t NB = *n_big, W = *n_items;
-  for (std::uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
+  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const std::uint64_t w = s_item;
+    if (w >= W) break;
     std::uint32_t ki, c;
     big_item(chunk_off, NB, w, &ki, &c);
-    if (s < slices) {
-      const std::uint32_t u = big_list[ki];
-      const std::uint32_t c0 = seg[u] + c * chunk;
-      const std::uint32_t c1 = min(seg[u + 1], c0 + chunk);
-      const std::uint32_t per = (c1 - c0 + slices - 1) / slices;
-      const std::uint32_t a0 = c0 + s * per, a1 = min(c1, a0 + per);
+    const std::uint32_t u = big_list[ki];
+    const std::uint32_t k0 = seg[u], k1 = seg[u + 1];
+    const std::uint32_t nch = chunk_off[ki + 1] - chunk_off[ki];
+    const std::uint64_t w0 = chunk_off[ki];
+    const std::uint32_t c0 = k0 + c * chunk, c1 = min(k1, c0 + std::uint32_t(chunk));
+    const std::uint32_t a0 = c0 + s * kFusePer;
+    const int cnt = worker && a0 < c1 ? int(min(c1 - a0, std::uint32_t(kFusePer))) : 0;
+    double x[kFusePer];
+    {
+      std::uint32_t e[kFusePer];
+#pragma unroll
+      for (int i = 0; i < kFusePer; ++i) e[i] = i < cnt ? exs[a0 + i] : 0u;
+#pragma unroll
+      for (int i = 0; i < kFusePer; ++i) x[i] = i < cnt ? DX[std::uint64_t(e[i]) * E + d] : 0.0;
+    }
+    if (worker) {
       DD t{0.0, 0.0};
       double asum = 0.0;
-#pragma unroll 8
-      for (std::uint32_t p = a0; p < a1; ++p) {
-        const double x = DX[std::uint64_t(exs[p]) * E + d];
-        t = dd_add(t, x);
-        asum = __dadd_ru(asum, fabs(x));
+#pragma unroll
+      for (int i = 0; i < kFusePer; ++i) {
+        if (i < cnt) {
+          t = dd_add(t, x[i]);
+          asum = __dadd_ru(asum, fabs(x[i]));
+        }
       }
-      part[w * kBigThreads + threadIdx.x] = BigPart{t.hi, t.lo, asum, 0.0};
       sh[threadIdx.x] = t.hi;
       sl[threadIdx.x] = t.lo;
       sa[threadIdx.x] = asum;
@@ -718,58 +773,34 @@ __global__ void __launch_bounds__(kBigThreads)
         ct = dd_add(ct, DD{sh[q * E + threadIdx.x], sl[q * E + threadIdx.x]});
         ca = __dadd_ru(ca, sa[q * E + threadIdx.x]);
       }
-      chunk_tot[w * E + threadIdx.x] = ChunkSum{ct.hi, ct.lo, ca, 0.0};
+      ChunkSum& cs = chunk_tot[w * E + threadIdx.x];
+      cs.hi = ct.hi;
+      cs.lo = ct.lo;
+      cs.a = ca;
+      __threadfence();
     }
     __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(kBigThreads)
-    big_p2_kernel(int E, int chunk, float lr, std::uint64_t n,
-                  const std::uint32_t* __restrict__ big_list,
-                  const unsigned long long* __restrict__ n_big,
-                  const std::uint32_t* __restrict__ chunk_off,
-                  const unsigned long long* __restrict__ n_items,
-                  const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
-                  const std::uint32_t* __restrict__ pos, const double* __restrict__ DX,
-                  BigPart* __restrict__ part, ChunkSum* __restrict__ chunk_tot,
-                  unsigned* __restrict__ key_done, float* __restrict__ out,
-                  unsigned long long* __restrict__ fallbacks) {
-  __shared__ double stage[kFallbackChunk];
-  __shared__ double sb[kBigThreads];
-  __shared__ bool bad[kBigThreads];
-  __shared__ unsigned s_last;
-  const int slices = kBigThreads / E;
-  const int s = threadIdx.x / E, d = threadIdx.x - s * E;
-  const bool worker = s < slices;
-  const std::uint64_t NB = *n_big, W = *n_items;
-  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-  for (std::uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
-    std::uint32_t ki, c;
-    big_item(chunk_off, NB, w, &ki, &c);
-    const std::uint32_t u = big_list[ki];
-    const std::uint32_t k0 = seg[u], k1 = seg[u + 1];
-    const std::uint32_t nch = chunk_off[ki + 1] - chunk_off[ki];
-    const std::uint64_t w0 = chunk_off[ki];  // the key's first item
+    if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned*>(&flags[w]) = 1u;
     if (worker) {
-      DD off{0.0, 0.0};  // earlier chunks' totals, then this chunk's earlier slices
+      // offset: the key's earlier chunks' totals in chunk order, then this
+      // chunk's earlier slices
+      DD off{0.0, 0.0};
       for (std::uint32_t cc = 0; cc < c; ++cc) {
-        const ChunkSum& ct = chunk_tot[(w0 + cc) * E + d];
-        off = dd_add(off, DD{ct.hi, ct.lo});
+        const std::uint64_t it = w0 + cc;
+        while (*reinterpret_cast<volatile const unsigned*>(&flags[it]) == 0u) __nanosleep(32);
+        __threadfence();
+        const double* bp = reinterpret_cast<const double*>(&chunk_tot[it * E + d]);
+        off = dd_add(off, DD{__ldcg(bp), __ldcg(bp + 1)});
       }
-      for (int q = 0; q < s; ++q) {
-        const BigPart& bp = part[w * kBigThreads + q * E + d];
-        off = dd_add(off, DD{bp.hi, bp.lo});
-      }
+      for (int q = 0; q < s; ++q) off = dd_add(off, DD{sh[q * E + d], sl[q * E + d]});
       const double o = dd_value(off);
-      const std::uint32_t c0 = k0 + c * chunk, c1 = min(k1, c0 + chunk);
-      const std::uint32_t per = (c1 - c0 + slices - 1) / slices;
-      const std::uint32_t a0 = c0 + s * per, a1 = min(c1, a0 + per);
       double l = 0.0, b = 0.0;
-#pragma unroll 8
-      for (std::uint32_t p = a0; p < a1; ++p) {
-        l = __dadd_rn(l, DX[std::uint64_t(exs[p]) * E + d]);
-        b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
+#pragma unroll
+      for (int i = 0; i < kFusePer; ++i) {
+        if (i < cnt) {
+          l = __dadd_rn(l, x[i]);
+          b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
+        }
       }
       sb[threadIdx.x] = b;
     }
@@ -804,12 +835,12 @@ __global__ void __launch_bounds__(kBigThreads)
     for (int dd = 0; dd < E; ++dd) {
       if (!bad[dd]) continue;
       double acc = 0.0;
-      for (std::uint32_t c0 = k0; c0 < k1; c0 += kFallbackChunk) {
-        const int cnt = int(k1 - c0 < kFallbackChunk ? k1 - c0 : kFallbackChunk);
-        for (int j = threadIdx.x; j < cnt; j += kBigThreads)
-          stage[j] = DX[std::uint64_t(exs[c0 + j]) * E + dd];
+      for (std::uint32_t cs0 = k0; cs0 < k1; cs0 += kFallbackChunk) {
+        const int m = int(k1 - cs0 < kFallbackChunk ? k1 - cs0 : kFallbackChunk);
+        for (int j = threadIdx.x; j < m; j += kFuseThreads)
+          stage[j] = DX[std::uint64_t(exs[cs0 + j]) * E + dd];
         __syncthreads();
-        if (int(threadIdx.x) == dd) acc = chain_sum(stage, cnt, acc);
+        if (int(threadIdx.x) == dd) acc = chain_sum(stage, m, acc);
         __syncthreads();
       }
       if (int(threadIdx.x) == dd) {

@@ -166,9 +166,9 @@ __global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys
 // working-set entry i (sorted key ws[i], slot wslot[i] in the fresh table):
 // csrc[i] = the key's slot in the previous table (copied by
 // table_carry_kernel once the previous batch is done, hbm_ps.hpp:86-98), else
-// the row comes from the table two builds back when that holds the key (its
-// final rows are exactly what its write-back puts into the store, and the
-// previous batch never touched the key), else the key joins the store list
+// the row comes from the table two (then three) builds back when that holds
+// the key (its final rows are exactly what its write-back puts into the store,
+// and the newer batches never touched the key), else the key joins the store list
 // (warp-contiguous, so in key order within a warp), else the row is zeros.
 __global__ void table_prefetch_probe_kernel(
     const std::uint64_t* __restrict__ ws, const std::uint32_t* __restrict__ wslot,
@@ -176,12 +176,14 @@ __global__ void table_prefetch_probe_kernel(
     std::uint32_t* __restrict__ csrc, const std::uint64_t* __restrict__ prev_keys,
     const std::uint64_t* __restrict__ prev_cap_ptr, const std::uint64_t* __restrict__ old_keys,
     const float* __restrict__ old_vals, const std::uint64_t* __restrict__ old_cap_ptr,
-    bool from_store, std::uint64_t store_keys, int E, std::uint64_t* __restrict__ need_key,
+    const std::uint64_t* __restrict__ old2_keys, const float* __restrict__ old2_vals,
+    const std::uint64_t* __restrict__ old2_cap_ptr, bool from_store, std::uint64_t store_keys, int E, std::uint64_t* __restrict__ need_key,
     std::uint32_t* __restrict__ need_slot, unsigned long long* __restrict__ n_need,
     unsigned long long* carried) {
   const std::uint64_t n = *n_ptr;
   const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
   const std::uint64_t ocap = old_cap_ptr ? *old_cap_ptr : 0;
+  const std::uint64_t o2cap = old2_cap_ptr ? *old2_cap_ptr : 0;
   const unsigned lane = threadIdx.x & 31;
   unsigned long long n_car = 0;
   const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
@@ -197,10 +199,17 @@ __global__ void table_prefetch_probe_kernel(
     if (live) csrc[i] = ps;
     bool need = false;
     if (live && ps == kNoSlot) {
+      // newest proxy first: its row is the key's latest
+      const float* src = nullptr;
       const std::uint32_t os = ocap ? probe_slot(old_keys, ocap, key) : kNoSlot;
-      float* dst = vals + std::uint64_t(slot) * E;
       if (os != kNoSlot) {
-        const float* src = old_vals + std::uint64_t(os) * E;
+        src = old_vals + std::uint64_t(os) * E;
+      } else if (o2cap) {
+        const std::uint32_t o2 = probe_slot(old2_keys, o2cap, key);
+        if (o2 != kNoSlot) src = old2_vals + std::uint64_t(o2) * E;
+      }
+      float* dst = vals + std::uint64_t(slot) * E;
+      if (src) {
         for (int d = 0; d < E; ++d) dst[d] = src[d];
       } else if (from_store && key < store_keys) {
         need = true;

@@ -20,6 +20,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -100,8 +101,10 @@ static NcclApi& nccl() {
 
 // --------------------------------------------------------- the tier ----
 
-constexpr int kTables = 3;  // current, previous (carry-over), the one before (store proxy)
-constexpr int kSlots = 3;   // staging slots = batches in flight
+// tables: current, previous (carry-over), and two older ones whose rows stand
+// in for the store while their write-backs drain (store proxies)
+constexpr int kTables = 4;
+constexpr int kSlots = 4;   // staging slots = batches in flight
 
 struct Scalars {
   std::uint64_t n_ws;          // working-set size of the current build
@@ -121,6 +124,8 @@ struct Scalars {
   unsigned long long epoch;    // P2P exchange round (parity selects the windows)
   std::uint32_t pad0, pad1;
   std::int64_t total_unused;   // host side: offsets[B] of a device batch
+  unsigned long long gn[4];      // grouping (prep lane): n_long, n_dup, n_huge
+  unsigned long long Ug[kTables][64];  // unique keys per (table, mini-batch), grouped path
   unsigned long long fallbacks;  // certified sums that needed the exact chain
   unsigned long long served;     // keys this rank served as owner (G > 1)
   DevError err;
@@ -140,9 +145,11 @@ struct BatchPlan {
   int tb = 0;         // its table
   int tp = -1;        // previous table (carry-over), -1 = none
   int tq = -1;        // table two builds back, usable as a store proxy, -1 = none
+  int tq2 = -1;       // three builds back, likewise
   std::int64_t step = 0;
   std::uint64_t occ_total = 0;
   int skip_mb = -1;
+  bool grouped = false;  // G == 1 slot grouping, done by the prep lane
 };
 
 struct GraphEntry {
@@ -198,7 +205,9 @@ struct Tier {
   cudaStream_t st = nullptr;            // == lane[0].st: bodies and the parity API
   cudaStream_t st2 = nullptr;           // side stream: dense-grad overlaps sparse reduce
   cudaEvent_t fork = nullptr, join = nullptr;
-  Lane lane[2];                         // 0: main (body), 1: prep (build of the next batch)
+  Lane lane[3];                         // 0: main (body), 1: prep (build of the next batch),
+                                        // 2: the next batch's mini-batch grouping
+  cudaEvent_t g_fork = nullptr, g_join = nullptr, g_ctx = nullptr;
   Lane* L = &lane[0];                   // the lane launch() enqueues on
   // The batch pipeline (the reference's 4-stage pipeline, pipeline.hpp:230-
   // 500, as streams): stage (H2D + counts, st_stage) -> prep (working set,
@@ -207,6 +216,8 @@ struct Tier {
   // Batch b+1 is staged and prepared while batch b trains; b's write-back
   // overlaps b+1.
   cudaStream_t st_stage = nullptr, st_wb = nullptr;
+  cudaStream_t st_pf = nullptr;         // prep's store gather, forked beside the grouping
+  cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
   cudaEvent_t ev_staged = nullptr, ev_prep = nullptr;
   cudaEvent_t ev_body_tab[kTables] = {}, ev_body_sp[kSlots] = {}, ev_wb[kTables] = {};
   cudaEvent_t ev_wbt[kTables][2] = {};  // write-back timing pairs
@@ -235,7 +246,7 @@ struct Tier {
   // before, whose rows stand in for the store while its write-back drains)
   std::uint64_t* tkeys[kTables] = {};
   float* tvals[kTables] = {};
-  int cur = -1, prev = -1;
+  int cur = -1, prev = -1, prev2 = -1;
 
   // working set
   std::uint64_t* ws = nullptr;       // sorted keys of the current table (when ws_sorted)
@@ -261,8 +272,10 @@ struct Tier {
                 *long_list = nullptr, *big_list = nullptr, *chunk_off = nullptr,
                 *orank = nullptr,
                 *key_done = nullptr;
-  BigPart* big_part = nullptr;
   ChunkSum* chunk_tot = nullptr;
+  unsigned* fuse_flags = nullptr;          // big_fused_kernel: chunk total published
+  unsigned long long* fuse_ticket = nullptr;
+  std::uint64_t fuse_items = 0;
   std::uint64_t* otot = nullptr;
   std::uint64_t* ukeys = nullptr;
   float *rows = nullptr, *deltas = nullptr, *hstage = nullptr, *staged = nullptr;
@@ -283,7 +296,18 @@ struct Tier {
   bool hash_dedup = true;                // group.cuh at G == 1 (HPS_DEDUP=sort: radix sort)
   std::uint32_t* gcnt = nullptr;         // [capmax] per-slot occurrence counters (kept zero)
   std::uint32_t* slot_uid = nullptr;     // [capmax]
-  std::uint32_t* occ_slot = nullptr;     // [S] slot of each occurrence
+  // slot grouping outputs, per table (prep of b+1 writes while body b reads):
+  // occurrence -> slot (batch key index), and per mini-batch region (at the
+  // sum of the earlier mini-batches' shape bounds) segments, example ids,
+  // uid -> slot; uid counts in Scalars::Ug
+  std::uint32_t* g_occslot[kTables] = {};
+  std::uint32_t* g_segb[kTables] = {};
+  std::uint32_t* g_exsb[kTables] = {};
+  std::uint32_t* g_uidb[kTables] = {};
+  std::uint64_t g_pool = 0;              // region pool size (elements)
+  // prep-only temporaries of the grouping
+  std::uint32_t *g_tick = nullptr, *g_segocc = nullptr, *g_exof = nullptr;
+  std::uint32_t *g_long = nullptr, *g_huge = nullptr, *g_dup = nullptr;
   std::uint32_t* part_slot = nullptr;    // [kGroupParts][part_cap] claimed slots
   std::uint32_t* part_n = nullptr;       // [kGroupParts * kGroupPartStride] claim counters
   std::uint32_t* part_base = nullptr;    // [kGroupParts]
@@ -296,8 +320,8 @@ struct Tier {
   cudaEvent_t tr_base = nullptr;
   cudaEvent_t tr[kSlots][6] = {};   // by staging slot: stage0 stage1 prep0 prep1 body0 body1
   cudaEvent_t trw[4][2] = {};  // write-back start/end by batch id % 4
-  std::uint64_t* need_key = nullptr;   // store rows of the build in flight
-  std::uint32_t* need_slot = nullptr;
+  std::uint64_t* need_key[kTables] = {};   // store rows of each table's build
+  std::uint32_t* need_slot[kTables] = {};
   bool store_registered = false;
   float* store_host = nullptr;
 
@@ -740,7 +764,7 @@ static void mark(Tier* t, int phase) {
     cudaEventCreate(&e);
     t->evpool.push_back(e);
   }
-  const int lane = t->L == &t->lane[1] ? 1 : 0;
+  const int lane = int(t->L - t->lane);
   cudaStream_t s = t->L->st;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
@@ -760,7 +784,7 @@ static void mark_stage(Tier* t, int phase) {
   t->L = &tmp;
   mark(t, phase);
   t->L = l;
-  t->ev_lane.back() = 2;
+  t->ev_lane.back() = 3;
 }
 
 static void timing_begin(Tier* t) {
@@ -773,7 +797,7 @@ static void timing_begin(Tier* t) {
 // mark to the last.
 static void timing_end(Tier* t) {
   if (!t->timing || t->ev_phase.size() < 2) return;
-  int last[3] = {-1, -1, -1};
+  int last[4] = {-1, -1, -1, -1};
   for (std::size_t i = 0; i < t->ev_phase.size(); ++i) {
     const int ln = t->ev_lane[i], p = t->ev_phase[i];
     if (last[ln] >= 0 && p > 0 && p < HPS_TIMING_SLOTS) {
@@ -823,6 +847,7 @@ static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* sta
            staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->E,
            &t->dsc->carried, &t->dsc->err);
   cudaMemcpyAsync(&t->dsc->nws_tab[nxt], &t->dsc->n_ws, 8, cudaMemcpyDeviceToDevice, t->st);
+  t->prev2 = t->prev;
   t->prev = prv;
   t->cur = nxt;
   t->tab_wb[nxt] = false;  // not a train-batch table: never a store proxy
@@ -957,46 +982,46 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
   return HPS_OK;
 }
 
-// Segment-length routing of the sparse reduce: <= kLongSeg in-order by a
-// sub-warp, (kLongSeg, kMediumMax] one CTA per key, longer ones split into
-// kBigChunkRun-occurrence chunks over CTAs.
+// Segment-length routing of the sparse reduce: <= kLongSeg in-order by one
+// thread per (key, 4 dims), longer ones split into fuse_chunk(E)-occurrence
+// chunks over CTAs (big_fused_kernel).
 constexpr int kMediumMax = kLongSeg;  // medium path off: chunks serve every long key
-constexpr int kBigChunkRun = 256;
 
 // Sparse segment-reduce launches: LPK lanes per short segment (pow2 >= E,
 // 4..32), then one CTA per long segment.
 static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint32_t* pos,
-                                      std::uint64_t u_upper) {
+                                      std::uint64_t u_upper, const std::uint64_t* U,
+                                      const std::uint32_t* seg, const std::uint32_t* exs) {
   const int E = t->E;
   if (E > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
   const float lr = t->cfg.learning_rate;
-  const std::uint64_t* U = &t->dsc->U;
-  const std::uint32_t* seg = t->seg;
-  const std::uint32_t* exs = t->exs;
   const double* DX = t->DX;
   unsigned long long* pulled = &t->dsc->pulled;
   unsigned long long* nl = &t->dsc->n_long;
   unsigned long long* nb = &t->dsc->n_big;
   if (t->G == 1) HPS_CUDA(cudaMemsetAsync(nl, 0, 16, t->st));  // G > 1: owner_rank_kernel
-launch(t, sparse_short_kernel, grid_for(std::max<std::uint64_t>(u_upper, 1) * E, 256, kSMs * 32),
-         256, 0, E, lr, n, U, seg, exs, pos, DX, t->deltas, pulled, t->long_list, nl, t->big_list,
-         nb, std::uint32_t(kMediumMax));
+  // DPT dims per thread (4 when E allows 32-byte row loads)
+  const int dpt = (E % 4 == 0) ? 4 : 1;
+  auto sk = dpt == 4 ? sparse_short_kernel<4> : sparse_short_kernel<1>;
+  launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,
+         E, lr, n, U, seg, exs, pos, DX, t->deltas, pulled, t->long_list, nl, t->big_list, nb,
+         std::uint32_t(kMediumMax));
   if (kMediumMax > kLongSeg)
     launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, 0, E, lr, n,
            (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos, DX,
            t->deltas, &t->dsc->fallbacks);
-  // big segments: plan (key, chunk) items, then the two passes over CTAs
-  launch(t, big_plan_kernel, 1, 256, 0, kBigChunkRun, (const std::uint32_t*)t->big_list,
+  // big segments: plan (key, chunk) items, then one fused pass over CTAs
+  // (ticket order; flags and ticket reset per launch)
+  const int chunk = fuse_chunk(E);
+  launch(t, big_plan_kernel, 1, 1024, 0, chunk, (const std::uint32_t*)t->big_list,
          (const unsigned long long*)nb, seg, t->chunk_off, &t->dsc->n_items);
-  launch(t, big_p1_kernel, kSMs * 4, kBigThreads, 0, E, kBigChunkRun,
-         (const std::uint32_t*)t->big_list,
-         (const unsigned long long*)nb, (const std::uint32_t*)t->chunk_off,
-         (const unsigned long long*)&t->dsc->n_items, seg, exs, DX, t->big_part, t->chunk_tot);
-  launch(t, big_p2_kernel, kSMs * 4, kBigThreads, 0, E, kBigChunkRun, lr, n,
-         (const std::uint32_t*)t->big_list,
-         (const unsigned long long*)nb, (const std::uint32_t*)t->chunk_off,
-         (const unsigned long long*)&t->dsc->n_items, seg, exs, pos, DX, t->big_part,
-         t->chunk_tot, t->key_done, t->deltas, &t->dsc->fallbacks);
+  HPS_CUDA(cudaMemsetAsync(t->fuse_flags, 0, t->fuse_items * 4, t->L->st));
+  HPS_CUDA(cudaMemsetAsync(t->fuse_ticket, 0, 8, t->L->st));
+  launch(t, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
+         (const std::uint32_t*)t->big_list, (const unsigned long long*)nb,
+         (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items, seg,
+         exs, pos, DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, t->deltas,
+         &t->dsc->fallbacks);
   return HPS_OK;
 }
 
@@ -1100,6 +1125,72 @@ inline std::uint64_t shape_bound(std::uint64_t x) {
   return p;
 }
 
+// Start of mini-batch j's region in the per-table grouping pools: the sum of
+// the earlier mini-batches' shape bounds (stable per shape, so captured
+// graphs hold across batches).
+static std::uint64_t group_region(const BatchShape& sh, int j) {
+  std::uint64_t r = 0;
+  for (int i = 0; i < j; ++i) r += sh.mb_bound[i];
+  return r;
+}
+
+// Mini-batch dedup of every shard of the batch by slot grouping (group.cuh),
+// on the prep lane: it depends only on the keys, so batch b+1's grouping runs
+// beside batch b's body. Outputs go to the table's pools (g_*[tb]).
+static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPlan& bp) {
+  const int G = T->G, J = T->J, tb = bp.tb;
+  const std::uint64_t B = sh.B, GJ = std::uint64_t(G) * J;
+  const std::int64_t* doff = T->b_off[bp.sp];
+  const std::uint64_t* dkeys = T->b_keys[bp.sp];
+  Lane& l = *T->L;
+  const std::uint32_t pcap = std::uint32_t(T->part_cap);
+  for (int j = 0; j < J; ++j) {
+    const std::uint64_t s = std::uint64_t(T->g) * J + j;
+    const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
+    const ShardMap sm{s, GJ, n};
+    const std::uint64_t ob = sh.mb_bound[j], r0 = group_region(sh, j);
+    std::uint32_t* seg = T->g_segb[tb] + r0 + j;  // U+1 entries per region
+    std::uint32_t* exs = T->g_exsb[tb] + r0;
+    std::uint32_t* uids = T->g_uidb[tb] + r0;
+    unsigned long long* U = &T->dsc->Ug[tb][j];
+    HPS_CUDA(cudaMemsetAsync(U, 0, 8, l.st));
+    HPS_CUDA(cudaMemsetAsync(T->dsc->gn, 0, sizeof(T->dsc->gn), l.st));
+    if (!n) continue;
+    const std::uint64_t warps = ((n + 31) / 32) * kGroupPosGroups;
+    launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys,
+           (const std::uint64_t*)T->tkeys[tb], (const std::uint64_t*)&T->dsc->cap[tb], T->gcnt,
+           T->slot_uid, T->part_slot, pcap, T->part_n, T->g_occslot[tb], T->g_tick, T->g_exof,
+           &T->dsc->err);
+    launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)T->part_n,
+           (const std::uint32_t*)T->part_slot, pcap, T->part_base, uids, U);
+    const Count Uc{reinterpret_cast<const std::uint64_t*>(U), 0};
+    tile_scan(T, UidCount{uids, T->gcnt}, SegEmit{seg, Uc}, Uc, ob, &l.d->total);
+    launch(T, group_place_kernel, grid_for(n * 32), 256, 0, sm, doff,
+           (const std::uint32_t*)T->g_occslot[tb], (const std::uint32_t*)T->g_tick,
+           (const std::uint32_t*)T->slot_uid, pcap, (const std::uint32_t*)T->part_base,
+           (const std::uint32_t*)seg, T->g_segocc);
+    launch(T, group_order_kernel, grid_for(ob), 256, 0, (const unsigned long long*)U,
+           (const std::uint32_t*)seg, T->g_segocc, (const std::uint32_t*)T->g_exof,
+           (const std::uint32_t*)uids, T->gcnt, exs, T->g_long, &T->dsc->gn[0], T->g_huge,
+           &T->dsc->gn[2], T->part_n);
+    const std::uint32_t words = std::uint32_t((n + 31) / 32);
+    const std::size_t wsmem = std::size_t(kGroupWarpThreads / 32) * 2 * words * 4;
+    launch(T, group_warp_kernel, kSMs * 4, kGroupWarpThreads, wsmem,
+           (const unsigned long long*)&T->dsc->gn[0], (const std::uint32_t*)T->g_long,
+           (const std::uint32_t*)seg, (const std::uint32_t*)T->g_segocc,
+           (const std::uint32_t*)T->g_exof, words, exs, T->g_dup, &T->dsc->gn[1]);
+    launch(T, group_cta_kernel, kSMs, kGroupThreads, std::size_t(2) * words * 4,
+           (const unsigned long long*)&T->dsc->gn[2], (const std::uint32_t*)T->g_huge,
+           (const std::uint32_t*)seg, (const std::uint32_t*)T->g_segocc,
+           (const std::uint32_t*)T->g_exof, words, exs, T->g_dup, &T->dsc->gn[1]);
+    launch(T, group_dup_kernel, kSMs, kGroupThreads, 0,
+           (const unsigned long long*)&T->dsc->gn[1], (const std::uint32_t*)T->g_dup,
+           (const std::uint32_t*)seg, (const std::uint32_t*)T->g_segocc,
+           (const std::uint32_t*)T->g_exof, exs);
+  }
+  return HPS_OK;
+}
+
 // Prep of one batch (lane 1, beside the previous batch's body): the sort-free
 // build of its table. Exact distinct count through a scratch set (it fixes
 // the capacity, hence the layout), ordered probing of the raw owned
@@ -1133,6 +1224,18 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
          (const std::uint64_t*)cap);
   launch(T, table_insert_dedup_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G),
          std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap, &T->dsc->err);
+  // the table's keys are final: the mini-batches' grouping forks onto lane 2
+  // and runs beside the rest of the build (joined at the end of the prep)
+  if (bp.grouped) {
+    HPS_CUDA(cudaEventRecord(T->g_fork, l.st));
+    HPS_CUDA(cudaStreamWaitEvent(T->lane[2].st, T->g_fork, 0));
+    T->L = &T->lane[2];
+    const hps_status gs = enqueue_grouping(T, sh, bp);
+    if (gs == HPS_OK) mark(T, HPS_T_DEDUP);
+    T->L = &l;
+    HPS_TRY(gs);
+    HPS_CUDA(cudaEventRecord(T->g_join, T->lane[2].st));
+  }
   // the distinct keys with their slots, ascending: compact the live slots,
   // sort them (n_ws items, ~3x fewer than the occurrences)
   tile_scan(T, LiveSlot{T->tkeys[tb]}, CompactEmit{T->tkeys[tb], nullptr, l.kB, l.vB},
@@ -1153,23 +1256,43 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   const std::uint64_t* qk = tq >= 0 ? T->tkeys[tq] : nullptr;
   const float* qv = tq >= 0 ? T->tvals[tq] : nullptr;
   const std::uint64_t* qc = tq >= 0 ? &T->dsc->cap[tq] : nullptr;
+  const int tq2 = bp.tq2;
+  const std::uint64_t* q2k = tq2 >= 0 ? T->tkeys[tq2] : nullptr;
+  const float* q2v = tq2 >= 0 ? T->tvals[tq2] : nullptr;
+  const std::uint64_t* q2c = tq2 >= 0 ? &T->dsc->cap[tq2] : nullptr;
   launch(T, table_prefetch_probe_kernel, grid_for(sh.own_bound), 256, 0,
          (const std::uint64_t*)T->wsb[tb], (const std::uint32_t*)T->wsib[tb],
-         (const std::uint64_t*)nws, T->tvals[tb], T->csrc[tb], pk, pc, qk, qv, qc,
-         T->store != nullptr, T->store_keys, E, T->need_key, T->need_slot,
+         (const std::uint64_t*)nws, T->tvals[tb], T->csrc[tb], pk, pc, qk, qv, qc, q2k, q2v, q2c,
+         T->store != nullptr, T->store_keys, E, T->need_key[tb], T->need_slot[tb],
          &T->dsc->stored_tab[tb], &T->dsc->carried_tab[tb]);
+  // the store list is ready: the store gather (enqueue_store_gather, its own
+  // stream, outside this graph) starts here, beside the grouping and the next
+  // batch's prep — PCIe-bound on a few CTAs vs. L2-bound on the rest
   if (T->store) {
-    const int V = vec_of(E);
-    const std::uint64_t work = sh.own_bound * std::uint64_t(E / V);
-    const unsigned gg = T->store_on_host ? T->pf_ctas : grid_for(work, 256 * 4);
-    const int tpb = T->store_on_host ? T->zc_threads : 256;
-    auto k = V == 4 ? store_gather_kernel<4, 4> : store_gather_kernel<1, 4>;
-    launch(T, k, gg, tpb, 0, (const std::uint64_t*)T->need_key,
-           (const std::uint32_t*)T->need_slot,
-           (const unsigned long long*)&T->dsc->stored_tab[tb], (const float*)T->store,
-           T->tvals[tb], E);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(l.st, &cs);
+    HPS_CUDA(cudaEventRecordWithFlags(
+        T->pf_fork, l.st, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
   }
+  if (bp.grouped) HPS_CUDA(cudaStreamWaitEvent(l.st, T->g_join, 0));
   mark(T, HPS_T_BUILD);
+  return HPS_OK;
+}
+
+// The store rows of table tb (host memory over PCIe, or HBM): a streaming
+// gather on st_pf, after the prep's store list; the batch's body waits for it.
+static hps_status enqueue_store_gather(Tier* T, const BatchShape& sh, int tb) {
+  const int E = T->E, V = vec_of(E);
+  HPS_CUDA(cudaStreamWaitEvent(T->st_pf, T->pf_fork, 0));
+  const std::uint64_t work = sh.own_bound * std::uint64_t(E / V);
+  const unsigned gg = T->store_on_host ? T->pf_ctas : grid_for(work, 256 * 4);
+  const int tpb = T->store_on_host ? T->zc_threads : 256;
+  auto k = V == 4 ? store_gather_kernel<4, 4> : store_gather_kernel<1, 4>;
+  launch_on(T, T->st_pf, k, gg, tpb, 0, (const std::uint64_t*)T->need_key[tb],
+            (const std::uint32_t*)T->need_slot[tb],
+            (const unsigned long long*)&T->dsc->stored_tab[tb], (const float*)T->store,
+            T->tvals[tb], E);
+  HPS_CUDA(cudaEventRecord(T->pf_join, T->st_pf));
   return HPS_OK;
 }
 
@@ -1209,53 +1332,21 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     const std::uint32_t* occ_row = T->inv;  // occurrence -> row of `rows`
     const float* rows = T->rows;
     const std::int64_t* goff = nullptr;      // occurrence ids: shard-local (sort path)
-    if (G == 1 && T->hash_dedup &&
-        std::size_t(kGroupWarpThreads / 32) * 8 * ((n + 31) / 32) <= kGroupSmemMax) {
-      // grouped by batch-table slot (group.cuh): no sort, and the rows are
-      // read in place from the table
-      // counters: n_long (warp segments), n_big (repeats), n_items (CTA segments)
-      HPS_CUDA(cudaMemsetAsync(&T->dsc->n_long, 0, 24, T->st));
-      HPS_CUDA(cudaMemsetAsync(&T->dsc->U, 0, 8, T->st));
-      if (n) {
-        const std::uint32_t pcap = std::uint32_t(T->part_cap);
-        const std::uint64_t warps = ((n + 31) / 32) * kGroupPosGroups;
-        launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys,
-               (const std::uint64_t*)T->tkeys[T->cur],
-               (const std::uint64_t*)&T->dsc->cap[T->cur], T->gcnt, T->slot_uid, T->part_slot,
-               pcap, T->part_n, T->occ_slot, T->uidv, T->ex_of, &T->dsc->err);
-        launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)T->part_n,
-               (const std::uint32_t*)T->part_slot, pcap, T->part_base, T->slots,
-               (unsigned long long*)&T->dsc->U);
-        tile_scan(T, UidCount{T->slots, T->gcnt}, SegEmit{T->seg, Count{&T->dsc->U, 0}},
-                  Count{&T->dsc->U, 0}, ob, &T->L->d->total);
-        launch(T, group_place_kernel, grid_for(n * 32), 256, 0, sm, doff,
-               (const std::uint32_t*)T->occ_slot, (const std::uint32_t*)T->uidv,
-               (const std::uint32_t*)T->slot_uid, pcap, (const std::uint32_t*)T->part_base,
-               (const std::uint32_t*)T->seg, T->pos, T->inv);
-        launch(T, group_order_kernel, grid_for(ob), 256, 0,
-               (const unsigned long long*)&T->dsc->U, (const std::uint32_t*)T->seg, T->pos,
-               (const std::uint32_t*)T->ex_of, (const std::uint32_t*)T->slots, T->gcnt, T->exs,
-               T->long_list, &T->dsc->n_long, T->big_list, &T->dsc->n_items, T->part_n);
-        const std::uint32_t words = std::uint32_t((n + 31) / 32);
-        const std::size_t wsmem = std::size_t(kGroupWarpThreads / 32) * 2 * words * 4;
-        // (orank: the S-sized owner-rank buffer, unused at G == 1, collects the
-        // segments whose examples repeat the key)
-        launch(T, group_warp_kernel, kSMs * 4, kGroupWarpThreads, wsmem,
-               (const unsigned long long*)&T->dsc->n_long, (const std::uint32_t*)T->long_list,
-               (const std::uint32_t*)T->seg, (const std::uint32_t*)T->pos,
-               (const std::uint32_t*)T->ex_of, words, T->exs, T->orank, &T->dsc->n_big);
-        launch(T, group_cta_kernel, kSMs, kGroupThreads, std::size_t(2) * words * 4,
-               (const unsigned long long*)&T->dsc->n_items, (const std::uint32_t*)T->big_list,
-               (const std::uint32_t*)T->seg, (const std::uint32_t*)T->pos,
-               (const std::uint32_t*)T->ex_of, words, T->exs, T->orank, &T->dsc->n_big);
-        launch(T, group_dup_kernel, kSMs, kGroupThreads, 0,
-               (const unsigned long long*)&T->dsc->n_big, (const std::uint32_t*)T->orank,
-               (const std::uint32_t*)T->seg, (const std::uint32_t*)T->pos,
-               (const std::uint32_t*)T->ex_of, T->exs);
-      }
+    const std::uint64_t* Uj = &T->dsc->U;      // this mini-batch's unique keys
+    const std::uint32_t* segj = T->seg;
+    const std::uint32_t* exsj = T->exs;
+    const std::uint32_t* slotsj = T->slots;      // uid -> table slot (G == 1)
+    if (bp.grouped) {
+      // grouped by batch-table slot on the prep lane (enqueue_grouping): no
+      // sort here, and fwd/bwd reads the rows in place from the table
+      const std::uint64_t r0 = group_region(sh, j);
+      Uj = reinterpret_cast<const std::uint64_t*>(&T->dsc->Ug[bp.tb][j]);
+      segj = T->g_segb[bp.tb] + r0 + j;
+      exsj = T->g_exsb[bp.tb] + r0;
+      slotsj = T->g_uidb[bp.tb] + r0;
       mark(T, HPS_T_DEDUP);
       mark(T, HPS_T_PULL);
-      occ_row = T->occ_slot;
+      occ_row = T->g_occslot[bp.tb];
       rows = T->tvals[T->cur];
       goff = doff;  // occurrence ids are batch key indices
     } else {
@@ -1289,7 +1380,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                 0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart, T->dg_done,
                 T->dgrad, &T->dsc->fallbacks);
       HPS_CUDA(cudaEventRecord(T->join, T->st2));
-      HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob));
+      HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob, Uj, segj, exsj));
       mark(T, HPS_T_SPARSE);
       HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
     } else {
@@ -1300,17 +1391,15 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     if (G == 1) {
       const std::uint64_t work = ob * std::uint64_t(E / V);
       if (V == 4)
-        launch(T, table_apply_kernel<4>, grid_for(work), 256, 0, (const std::uint32_t*)T->slots,
+        launch(T, table_apply_kernel<4>, grid_for(work), 256, 0, slotsj,
                (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
-               (const std::uint64_t*)nullptr, (const float*)T->deltas,
-               (const std::uint64_t*)&T->dsc->U, std::uint64_t(0), T->tvals[T->cur], E,
-               &T->dsc->err);
+               (const std::uint64_t*)nullptr, (const float*)T->deltas, Uj, std::uint64_t(0),
+               T->tvals[T->cur], E, &T->dsc->err);
       else
-        launch(T, table_apply_kernel<1>, grid_for(work), 256, 0, (const std::uint32_t*)T->slots,
+        launch(T, table_apply_kernel<1>, grid_for(work), 256, 0, slotsj,
                (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
-               (const std::uint64_t*)nullptr, (const float*)T->deltas,
-               (const std::uint64_t*)&T->dsc->U, std::uint64_t(0), T->tvals[T->cur], E,
-               &T->dsc->err);
+               (const std::uint64_t*)nullptr, (const float*)T->deltas, Uj, std::uint64_t(0),
+               T->tvals[T->cur], E, &T->dsc->err);
     } else {
       HPS_TRY(push_apply(T));
     }
@@ -1495,6 +1584,8 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   bp.tb = next_table(T);
   bp.tp = T->cur;
   bp.tq = (T->store && T->prev >= 0 && T->prev != bp.tb && T->tab_wb[T->prev]) ? T->prev : -1;
+  bp.tq2 = (bp.tq >= 0 && T->prev2 >= 0 && T->prev2 != bp.tb && T->tab_wb[T->prev2])
+               ? T->prev2 : -1;
   bp.step = T->step;
   const int sp = bp.sp;
   // ---- stage into the tier's own buffers (captured graphs never see caller
@@ -1529,11 +1620,29 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
             (const std::uint64_t*)T->b_keys[sp], B, G, T->g, J,
             T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts[sp],
             &T->dsc->err);
-  HPS_CUDA(cudaMemcpyAsync(T->hsc->counts[sp], T->dsc->counts[sp], sizeof(T->dsc->counts[sp]),
-                           cudaMemcpyDeviceToHost, ss));
-  mark_stage(T, HPS_T_STAGE);
-  if (T->trace) cudaEventRecord(T->tr[sp][1], ss);
-  HPS_TRY(check_device_error(T, "device table: missing key ", true, ss));
+  // Host batch at one rank: the shape counts follow from the offsets alone
+  // (per-shard occurrences; every key is owned), so the host does not wait
+  // for the copy — the device counts and the key-range check (its error is
+  // reported by hps_wait_batch) follow in stream order. Otherwise one
+  // round-trip (and at G > 1 the collective error agreement).
+  const bool host_counts = !on_device && G == 1;
+  if (host_counts) {
+    std::uint64_t* hc = T->hsc->counts[sp];
+    for (int i = 0; i < 66; ++i) hc[i] = 0;
+    for (std::uint64_t i = 0; i < B; ++i) hc[i % J] += std::uint64_t(offsets[i + 1] - offsets[i]);
+    hc[J] = O;
+    hc[J + 1] = O;
+    mark_stage(T, HPS_T_STAGE);
+    if (T->trace) cudaEventRecord(T->tr[sp][1], ss);
+    HPS_CUDA(cudaEventRecord(T->ev_staged, ss));
+  } else {
+    HPS_CUDA(cudaMemcpyAsync(T->hsc->counts[sp], T->dsc->counts[sp],
+                             sizeof(T->dsc->counts[sp]), cudaMemcpyDeviceToHost, ss));
+    mark_stage(T, HPS_T_STAGE);
+    if (T->trace) cudaEventRecord(T->tr[sp][1], ss);
+    HPS_CUDA(cudaEventRecord(T->ev_staged, ss));
+    HPS_TRY(check_device_error(T, "device table: missing key ", true, ss));
+  }
   for (int j = 0; j < J; ++j) bp.occ_total += T->hsc->counts[sp][j];
   const std::uint64_t own = T->hsc->counts[sp][J];
   if (own > T->Wmax || bp.occ_total > T->Omax)
@@ -1548,21 +1657,39 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   const std::int64_t first_mb = T->step * J;
   if (T->cfg.inject_skip_sync >= first_mb && T->cfg.inject_skip_sync < first_mb + J)
     bp.skip_mb = int(T->cfg.inject_skip_sync - first_mb);
+  {  // slot grouping (G == 1) when its shared-memory bitmaps fit
+    const std::uint64_t nmax = (B + std::uint64_t(G) * J - 1) / (std::uint64_t(G) * J);
+    const std::size_t words = std::size_t((nmax + 31) / 32);
+    bp.grouped = G == 1 && T->hash_dedup &&
+                 std::size_t(kGroupWarpThreads / 32) * 8 * words <= kGroupSmemMax;
+  }
   // ---- prep on lane 1, beside the previous body
   {
     cudaStream_t ps = T->lane[1].st;
+    HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_staged, 0));
     if (bp.tq >= 0 && T->body_pending[bp.tq])  // its rows final
       HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tq], 0));
+    if (bp.tq2 >= 0 && T->body_pending[bp.tq2])
+      HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tq2], 0));
     if (T->body_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tb], 0));
     if (T->wb_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_wb[bp.tb], 0));
     if (T->trace) cudaEventRecord(T->tr[sp][2], ps);
+    if (bp.grouped) {  // lane 2's look-back context: after the previous prep (whose
+      // graph ran lane 2's last grouping), before this one
+      HPS_CUDA(cudaStreamWaitEvent(T->lane[2].st, T->ev_prep, 0));
+      T->L = &T->lane[2];
+      open_lookback_context(T);
+      HPS_CUDA(cudaEventRecord(T->g_ctx, T->lane[2].st));
+      HPS_CUDA(cudaStreamWaitEvent(ps, T->g_ctx, 0));
+    }
     T->L = &T->lane[1];
     open_lookback_context(T);
     hps_status st;
     if (T->use_graphs) {
       const std::vector<std::uint64_t> key = {
           1, B, sh.own_bound, sh.batch_bound, std::uint64_t(bp.tb), std::uint64_t(bp.tp + 1),
-          std::uint64_t(bp.tq + 1), std::uint64_t(sp), reinterpret_cast<std::uint64_t>(T->store),
+          std::uint64_t(bp.tq + 1), std::uint64_t(bp.tq2 + 1), std::uint64_t(sp),
+          reinterpret_cast<std::uint64_t>(T->store),
           T->store_keys, std::uint64_t(T->store_on_host), std::uint64_t(T->timing)};
       st = run_graph(T, key, [&] { return enqueue_prep(T, sh, bp); });
     } else {
@@ -1572,11 +1699,14 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     HPS_TRY(st);
     HPS_CUDA(cudaEventRecord(T->ev_prep, ps));
     if (T->trace) cudaEventRecord(T->tr[sp][3], ps);
+    if (T->store) HPS_TRY(enqueue_store_gather(T, sh, bp.tb));
   }
-  // ---- body on lane 0
+  // ---- body on lane 0 (after its prep and its store rows)
   HPS_CUDA(cudaStreamWaitEvent(T->st, T->ev_prep, 0));
+  if (T->store) HPS_CUDA(cudaStreamWaitEvent(T->st, T->pf_join, 0));
   if (T->trace) cudaEventRecord(T->tr[sp][4], T->st);
   open_lookback_context(T);
+  T->prev2 = T->prev;
   T->prev = bp.tp;
   T->cur = bp.tb;
   T->ws = T->wsb[bp.tb];
@@ -1746,12 +1876,19 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     str(&t->st, hi);
     str(&t->st2, hi);
     str(&t->lane[1].st, lo);
+    str(&t->lane[2].st, lo);
     str(&t->st_stage, lo);
     str(&t->st_wb, lo);
+    str(&t->st_pf, lo);
     ev(&t->fork, false);
     ev(&t->join, false);
     ev(&t->ev_staged, false);
     ev(&t->ev_prep, false);
+    ev(&t->pf_fork, false);
+    ev(&t->g_fork, false);
+    ev(&t->g_join, false);
+    ev(&t->g_ctx, false);
+    ev(&t->pf_join, false);
     for (int i = 0; i < kTables; ++i) {
       ev(&t->ev_body_tab[i], false);
       ev(&t->ev_wb[i], false);
@@ -1805,8 +1942,10 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     A(wsib[i], W);
     A(csrc[i], W);
   }
-  A(need_key, W);
-  A(need_slot, W);
+  for (int i = 0; i < kTables; ++i) {
+    A(need_key[i], W);
+    A(need_slot[i], W);
+  }
   A(gcnt, t->capmax);
   A(slot_uid, t->capmax);
   t->ws = t->wsb[0];
@@ -1843,7 +1982,19 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(slots, S);
   A(exs, S);
   A(orank, S);
-  A(occ_slot, S);
+  t->g_pool = 2 * S + std::uint64_t(t->J) * 4096 + 64;  // >= the sum of the shape bounds
+  for (int i = 0; i < kTables; ++i) {
+    A(g_occslot[i], S);
+    A(g_segb[i], t->g_pool + 64);
+    A(g_exsb[i], t->g_pool);
+    A(g_uidb[i], t->g_pool);
+  }
+  A(g_tick, S);
+  A(g_segocc, S);
+  A(g_exof, S);
+  A(g_long, S);
+  A(g_huge, S);
+  A(g_dup, S);
   t->part_cap = S;  // a partition can never overflow
   A(part_slot, std::uint64_t(kGroupParts) * S);
   A(part_n, std::uint64_t(kGroupParts) * kGroupPartStride);
@@ -1853,8 +2004,11 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(big_list, S / (kLongSeg + 1) + 2);
   A(chunk_off, S / (kLongSeg + 1) + 3);
   A(key_done, S / (kLongSeg + 1) + 2);
-  A(big_part, (S / kBigChunkRun + S / (kLongSeg + 1) + 2) * std::uint64_t(kBigThreads));
-  A(chunk_tot, (S / kBigChunkRun + S / (kLongSeg + 1) + 2) * E);
+  // fused big-segment items: one per (key, chunk of fuse_chunk(E) occurrences)
+  t->fuse_items = S / std::uint64_t(fuse_chunk(int(E))) + S / (kLongSeg + 1) + 2;
+  A(chunk_tot, t->fuse_items * E);
+  A(fuse_flags, t->fuse_items);
+  A(fuse_ticket, 1);
   A(ukeys, S);
   if (G == 1) A(rows, S * E);  // G > 1: inside the exported window (peers write it)
   A(deltas, S * E);
@@ -1897,7 +2051,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
 hps_status hps_destroy(hps_tier_t t) {
   if (!t) return HPS_OK;
   cudaSetDevice(t->cfg.cuda_device);
-  for (cudaStream_t x : {t->st, t->lane[1].st, t->st_stage, t->st_wb, t->st2})
+  for (cudaStream_t x : {t->st, t->lane[1].st, t->lane[2].st, t->st_stage, t->st_wb, t->st2,
+                         t->st_pf})
     if (x) cudaStreamSynchronize(x);
   if (t->comm) nccl().CommDestroy(t->comm);
   for (auto& c : t->pending) {
@@ -1919,9 +2074,10 @@ hps_status hps_destroy(hps_tier_t t) {
   }
   for (cudaEvent_t x : t->ev_body_sp)
     if (x) cudaEventDestroy(x);
-  for (cudaEvent_t x : {t->ev_staged, t->ev_prep})
+  for (cudaEvent_t x : {t->ev_staged, t->ev_prep, t->pf_fork, t->pf_join, t->g_fork, t->g_join,
+                        t->g_ctx})
     if (x) cudaEventDestroy(x);
-  for (cudaStream_t x : {t->lane[1].st, t->st_stage, t->st_wb})
+  for (cudaStream_t x : {t->lane[1].st, t->lane[2].st, t->st_stage, t->st_wb, t->st_pf})
     if (x) cudaStreamDestroy(x);
   if (t->st2) cudaStreamDestroy(t->st2);
   if (t->st) cudaStreamDestroy(t->st);
@@ -2299,14 +2455,23 @@ hps_status hps_stream(hps_tier_t t, void** stream) {
 hps_status hps_submit_batch(hps_tier_t t, uint64_t B, const int64_t* offsets,
                             const uint64_t* keys, const uint8_t* labels, int on_device) {
   HPS_ENTER(t);
-  return submit_batch(t, B, offsets, keys, labels, on_device, nullptr);
+  if (!t->trace) return submit_batch(t, B, offsets, keys, labels, on_device, nullptr);
+  const auto h0 = std::chrono::steady_clock::now();
+  const hps_status s = submit_batch(t, B, offsets, keys, labels, on_device, nullptr);
+  const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
+  std::fprintf(stderr, "[trace] host submit %llu: %.0f us\n", (unsigned long long)(t->submitted - 1), us);
+  return s;
 }
 
 hps_status hps_wait_batch(hps_tier_t t, hps_batch_stats* stats) {
   HPS_ENTER(t);
   if (t->done.empty()) {
     if (t->inflight.empty()) return set_error(HPS_ERR_ARG, "wait_batch: no batch in flight");
+    const auto h0 = std::chrono::steady_clock::now();
     complete_oldest(t);
+    if (t->trace)
+      std::fprintf(stderr, "[trace] host wait: %.0f us\n",
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count());
   }
   Tier::Done d = std::move(t->done.front());
   t->done.pop_front();

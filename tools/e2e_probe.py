@@ -53,9 +53,9 @@ def main():
         t0 = time.perf_counter()
         for i in range(n):
             submit(i)
-            if i >= 2:
+            if i >= 3:
                 tier.wait_batch()
-        for _ in range(min(n, 2)):
+        for _ in range(min(n, 3)):
             tier.wait_batch()
         tier.flush()
         return (time.perf_counter() - t0) / n * 1e3
