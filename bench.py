@@ -332,14 +332,17 @@ def run_ours(args, rank, world, local_rank):
             host_step(i % P)
         for i in range(args.warmup):
             tier.wait_batch()
+        tier.flush()
         barrier()
+        rd0, wr0 = tier.store_traffic()
         e2e_ms, e2e_stats = timed_steps(host_step, args.steps, args.warmup)
         barrier()
+        rd1, wr1 = tier.store_traffic()
         e2e_ms_max = max_over_ranks(e2e_ms)
         h2d = sum(8 * (b[0].size) + 8 * b[1].size + b[2].size for b in
                   (hbatches[(args.warmup + i) % P] for i in range(args.steps))) / args.steps
-        h2d += sum(s.store_rows * E * 4 for s in e2e_stats) / args.steps
-        d2h = sum(s.working_set * E * 4 + 24 for s in e2e_stats) / args.steps
+        h2d += (rd1 - rd0) * E * 4 / args.steps        # store rows read by the builds
+        d2h = ((wr1 - wr0) * E * 4 + 24 * args.steps) / args.steps  # written back + stats
         e2e = {"value": args.steps * B / (e2e_ms_max / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(sum_over_ranks(h2d)),
                "d2h_bytes_per_step": int(sum_over_ranks(d2h)),

@@ -185,13 +185,22 @@ hps_status hps_set_dense(hps_tier_t h, const float* w);
 hps_status hps_attach_store(hps_tier_t h, float* rows, uint64_t num_keys,
                             int on_device);
 
-/* The write-back of batch b runs asynchronously, overlapping batch b+1 (the
- * reference's collect stage runs beside the next train step, pipeline.hpp:
- * 462-474); batch b+2's build waits for it, as prepare of step+2 waits for
- * collect of step (mem_ps.hpp freshness rule). hps_flush blocks until every
- * pending write-back has reached the store; after it (or hps_attach_store /
- * hps_destroy) the store holds every trained row. */
+/* Write-back (the reference's collect stage, pipeline.hpp:462-474) runs
+ * asynchronously beside the next batches. The four most recent batch tables
+ * stay resident in HBM; a row reaches the store when its table is recycled
+ * and no newer resident table holds the key (a newer one has the fresher row).
+ * Builds read the store only for keys outside the resident tables, after the
+ * write-backs they depend on (the mem_ps.hpp freshness rule: prepare of step
+ * t+2 after collect of step t). hps_flush blocks until every resident row has
+ * reached the store; after it (or hps_attach_store / hps_destroy, and before
+ * any other entry point runs) the store holds every trained row. */
 hps_status hps_flush(hps_tier_t h);
+
+/* Value-store traffic since hps_create: rows read by table builds (completed
+ * batches) and rows written back (eviction write-backs and flushes; a row a
+ * newer resident table still holds is written once it leaves, not every
+ * batch). */
+hps_status hps_store_traffic(hps_tier_t h, uint64_t* rows_read, uint64_t* rows_written);
 
 /* One whole batch through the tier, device-resident: working-set dedup ->
  * build (carry-over + store staging) -> J x {mini-batch dedup, pull

@@ -36,6 +36,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "hps_gpu.h"
@@ -287,8 +288,14 @@ class HbmTier {
   void attach_store(float* rows, std::uint64_t num_keys, bool on_device) {
     check(hps_attach_store(h_, rows, num_keys, on_device ? 1 : 0));
   }
-  // collect stage barrier: deferred write-backs have reached the store
+  // collect stage barrier: every resident row has reached the store
   void flush() { check(hps_flush(h_)); }
+  // (rows read from, rows written to) the value store since creation
+  std::pair<std::uint64_t, std::uint64_t> store_traffic() const {
+    std::uint64_t r = 0, w = 0;
+    check(hps_store_traffic(h_, &r, &w));
+    return {r, w};
+  }
   std::vector<float> dense() const {
     std::uint64_t n = 0;
     check(hps_dense_count(h_, &n));

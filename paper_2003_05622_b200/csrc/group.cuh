@@ -46,6 +46,37 @@ constexpr int kGroupParts = 32;         // uid claim counters (contention / kGro
 constexpr int kGroupPartStride = 32;    // u32 words between counters (one 128-B line each)
 constexpr std::size_t kGroupSmemMax = 200 * 1024;
 
+// Request table (G > 1): every key of this rank's shards once, so grouping
+// has a slot per key whoever owns it. Unordered CAS insert (the table is
+// internal, its layout free), read-first for hot keys. Warp per example.
+__global__ void rq_insert_kernel(const std::int64_t* __restrict__ off,
+                                 const std::uint64_t* __restrict__ keys, std::uint64_t B, int G,
+                                 int g, int J, std::uint64_t* __restrict__ rq,
+                                 const std::uint64_t* __restrict__ cap_ptr) {
+  const std::uint64_t cap = *cap_ptr, GJ = std::uint64_t(G) * J;
+  const unsigned lane = threadIdx.x & 31;
+  const std::uint64_t nw = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (std::uint64_t i = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5; i < B;
+       i += nw) {
+    if ((i % GJ) / J != std::uint64_t(g)) continue;
+    const std::int64_t b = off[i], e = off[i + 1];
+    for (std::int64_t p = b + lane; p < e; p += 32) {
+      const std::uint64_t k = keys[p];
+      std::uint64_t idx = mix64(k) & (cap - 1);
+      for (;;) {
+        const std::uint64_t seen = *reinterpret_cast<volatile const std::uint64_t*>(rq + idx);
+        if (seen == k) break;
+        if (seen == kEmptyKey) {
+          const unsigned long long old =
+              atomicCAS(reinterpret_cast<unsigned long long*>(rq + idx), kEmptyKey, k);
+          if (old == kEmptyKey || old == k) break;
+        }
+        idx = (idx + 1) & (cap - 1);
+      }
+    }
+  }
+}
+
 // Warp w: examples 32*(w / kGroupPosGroups) + lane, feature positions
 // p = w % kGroupPosGroups (mod kGroupPosGroups), in lock-step across the
 // lanes. Writes occ_slot[q], tick[q], ex_of[q]; counts per slot in cnt (zero
@@ -163,6 +194,18 @@ __device__ __forceinline__ std::uint32_t dense_uid(std::uint32_t packed, std::ui
   return part_base[p] + (packed - p * part_cap);
 }
 
+// G > 1: the unique keys of a grouped mini-batch in uid order (the exchange
+// sends them to their owners), from the request table.
+__global__ void uid_keys_kernel(const std::uint32_t* __restrict__ uid_slot,
+                                const std::uint64_t* __restrict__ rq,
+                                const unsigned long long* __restrict__ n_uid,
+                                std::uint64_t* __restrict__ ukeys) {
+  const std::uint64_t U = *n_uid;
+  for (std::uint64_t u = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; u < U;
+       u += std::uint64_t(gridDim.x) * blockDim.x)
+    ukeys[u] = rq[uid_slot[u]];
+}
+
 struct UidCount {  // count of uid u's occurrences (for the segment scan)
   const std::uint32_t* uid_slot;
   const std::uint32_t* cnt;
@@ -178,8 +221,8 @@ struct SegEmit {
 };
 
 // Occurrence q (a batch key index of this shard) -> its position in the
-// segment (unordered for now). One warp per example, lanes over its
-// positions.
+// segment (unordered for now), and (G > 1, rows arrive in uid order) its uid
+// inv[q]. One warp per example, lanes over its positions.
 __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__ off,
                                    const std::uint32_t* __restrict__ occ_slot,
                                    const std::uint32_t* __restrict__ tick,
@@ -187,7 +230,8 @@ __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__
                                    std::uint32_t part_cap,
                                    const std::uint32_t* __restrict__ part_base,
                                    const std::uint32_t* __restrict__ seg,
-                                   std::uint32_t* __restrict__ seg_occ) {
+                                   std::uint32_t* __restrict__ seg_occ,
+                                   std::uint32_t* __restrict__ inv) {
   __shared__ std::uint32_t pb[kGroupParts];
   if (threadIdx.x < kGroupParts) pb[threadIdx.x] = part_base[threadIdx.x];
   __syncthreads();
@@ -200,6 +244,7 @@ __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__
     for (std::int64_t q = b + lane; q < e; q += 32) {
       const std::uint32_t u = dense_uid(slot_uid[occ_slot[q]], part_cap, pb);
       seg_occ[seg[u] + tick[q]] = std::uint32_t(q);
+      if (inv) inv[q] = u;
     }
   }
 }

@@ -443,13 +443,10 @@ inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw 
 // then -(lr * g) into the push row of the key (pos[u], its position in the
 // owner-partitioned send order; identity when pos is null).
 //
-// Short segments (<= kLongSeg): LPK lanes per key; each round the group loads
-// up to 8 example ids, every lane issues its 8 independent DX loads into
-// registers, then adds them in order. Longer segments (hot Zipf keys: up to
-// the whole shard) are queued for sparse_delta_long_kernel.
+// Short segments (<= kLongSeg) are summed exactly in order by
+// sparse_short_kernel; longer ones (hot Zipf keys: up to the whole shard) are
+// queued for the chunked, certified big_fused_kernel.
 constexpr int kLongSeg = 32;
-constexpr int kBigChunk = 512;  // segments longer than this are split over CTAs
-constexpr int kStageDepth = 8;
 
 __device__ __forceinline__ void write_delta(float* out, std::uint64_t row, int E, int d,
                                             double acc, double inv_n, float lr) {
@@ -524,115 +521,6 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int i = 0; i < DPT; ++i) write_delta(out, pos ? pos[u] : u, E, d0 + i, acc[i], inv_n, lr);
-  }
-}
-
-// Long segments (hot keys): one CTA per key, in chunks of kLongChunk
-// occurrences whose example ids are staged in shared memory (one coalesced
-// pass). Thread (slice s, dim d) first sums dimension d over its slice of the
-// chunk (Neumaier, plus sum|x|); with the running total of earlier chunks and
-// slices as offset it then re-walks its slice accumulating the running-prefix
-// magnitudes B. Thread d combines and certifies (certify_f32); uncertified
-// dimensions are recomputed in the exact order (the CTA stages the values in
-// shared memory, one thread chains them).
-constexpr int kLongThreads = 256;
-constexpr int kLongChunk = kBigChunk;
-
-__global__ void __launch_bounds__(kLongThreads)
-    sparse_delta_long_kernel(int E, float lr, std::uint64_t n,
-                             const std::uint32_t* __restrict__ long_list,
-                             const unsigned long long* __restrict__ n_long,
-                             const std::uint32_t* __restrict__ seg,
-                             const std::uint32_t* __restrict__ exs,
-                             const std::uint32_t* __restrict__ pos,
-                             const double* __restrict__ DX, float* __restrict__ out,
-                             unsigned long long* __restrict__ fallbacks) {
-  __shared__ double th[kLongThreads], tl[kLongThreads], ta[kLongThreads], tb[kLongThreads];
-  __shared__ std::uint32_t sex[kLongChunk];
-  __shared__ double stage[kFallbackChunk];
-  __shared__ bool bad[kLongThreads];
-  const unsigned long long NL = *n_long;
-  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-  const int slices = kLongThreads / E;  // E <= 512
-  const int s = threadIdx.x / E, d = threadIdx.x - s * E;
-  const bool worker = s < slices;
-  for (unsigned long long li = blockIdx.x; li < NL; li += gridDim.x) {
-    const std::uint32_t u = long_list[li];
-    const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
-    DD run{0.0, 0.0};     // total of the chunks done (thread d < E keeps it)
-    DD S{0.0, 0.0};
-    double A = 0.0, B = 0.0;
-    for (std::uint32_t c0 = p0; c0 < p1; c0 += kLongChunk) {
-      const int cnt = int(p1 - c0 < std::uint32_t(kLongChunk) ? p1 - c0 : kLongChunk);
-      for (int j = threadIdx.x; j < cnt; j += kLongThreads) sex[j] = exs[c0 + j];
-      __syncthreads();
-      const int per = (cnt + slices - 1) / slices;
-      const int a0 = s * per, a1 = a0 + int(per) < cnt ? a0 + int(per) : cnt;
-      if (worker) {
-        DD t{0.0, 0.0};
-        double asum = 0.0;
-#pragma unroll 16
-        for (int p = a0; p < a1; ++p) {
-          const double x = DX[std::uint64_t(sex[p]) * E + d];
-          t = dd_add(t, x);
-          asum = __dadd_ru(asum, fabs(x));
-        }
-        th[threadIdx.x] = t.hi;
-        tl[threadIdx.x] = t.lo;
-        ta[threadIdx.x] = asum;
-      }
-      __syncthreads();
-      if (worker) {
-        DD off{0.0, 0.0};
-        for (int q = 0; q < s; ++q) off = dd_add(off, DD{th[q * E + d], tl[q * E + d]});
-        const double o = __dadd_rn(dd_value(run), dd_value(off));
-        double l = 0.0, b = 0.0;
-#pragma unroll 16
-        for (int p = a0; p < a1; ++p) {
-          l = __dadd_rn(l, DX[std::uint64_t(sex[p]) * E + d]);
-          b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
-        }
-        tb[threadIdx.x] = b;
-      }
-      __syncthreads();
-      if (worker) {
-        // every worker of dim d folds this chunk into its copy of the running
-        // state, in slice order (identical across the dim's workers)
-        for (int q = 0; q < slices; ++q) {
-          const DD tq{th[q * E + d], tl[q * E + d]};
-          run = dd_add(run, tq);
-          if (s == 0) {
-            S = dd_add(S, tq);
-            A = __dadd_ru(A, ta[q * E + d]);
-            B = __dadd_ru(B, tb[q * E + d]);
-          }
-        }
-      }
-      __syncthreads();
-    }
-    float g = 0.0f;
-    if (int(threadIdx.x) < E)
-      bad[threadIdx.x] = !certify_f32(dd_value(S), B, A, p1 - p0, (p1 - p0) + slices, inv_n, &g);
-    __syncthreads();
-    for (int dd = 0; dd < E; ++dd) {
-      if (!bad[dd]) continue;
-      double acc = 0.0;
-      for (std::uint32_t c0 = p0; c0 < p1; c0 += kFallbackChunk) {
-        const int cnt = int(p1 - c0 < kFallbackChunk ? p1 - c0 : kFallbackChunk);
-        for (int j = threadIdx.x; j < cnt; j += kLongThreads)
-          stage[j] = DX[std::uint64_t(exs[c0 + j]) * E + dd];
-        __syncthreads();
-        if (int(threadIdx.x) == dd) acc = chain_sum(stage, cnt, acc);
-        __syncthreads();
-      }
-      if (int(threadIdx.x) == dd) {
-        g = __double2float_rn(__dmul_rn(acc, inv_n));
-        if (fallbacks) atomicAdd(fallbacks, 1ull);
-      }
-    }
-    if (int(threadIdx.x) < E)
-      out[std::uint64_t(pos ? pos[u] : u) * E + threadIdx.x] = -__fmul_rn(lr, g);
-    __syncthreads();
   }
 }
 

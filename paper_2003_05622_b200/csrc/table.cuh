@@ -294,41 +294,87 @@ __global__ void table_carry_kernel(const std::uint32_t* __restrict__ csrc,
 }
 
 
-// Write-back in ascending key order with known slots; ILP independent row
-// loads per thread before their (posted, zero-copy for a host store) stores.
+// Eviction filter of a table's working set (sorted keys ws, slots wslot):
+// rows whose key a newer resident table also holds are skipped (that table
+// has the fresher row and writes it back itself later); the rest join a
+// warp-contiguous, hence key-ordered, list for the zero-copy writer.
+__global__ void table_evict_filter_kernel(const std::uint64_t* __restrict__ ws,
+                                          const std::uint32_t* __restrict__ wslot,
+                                          const std::uint64_t* __restrict__ n_ptr,
+                                          const std::uint64_t* __restrict__ k1,
+                                          const std::uint64_t* __restrict__ c1,
+                                          const std::uint64_t* __restrict__ k2,
+                                          const std::uint64_t* __restrict__ c2,
+                                          const std::uint64_t* __restrict__ k3,
+                                          const std::uint64_t* __restrict__ c3,
+                                          std::uint64_t store_keys,
+                                          std::uint64_t* __restrict__ out_key,
+                                          std::uint32_t* __restrict__ out_slot,
+                                          unsigned long long* __restrict__ n_out,
+                                          unsigned long long* __restrict__ total) {
+  const std::uint64_t n = *n_ptr;
+  const std::uint64_t cap1 = c1 ? *c1 : 0, cap2 = c2 ? *c2 : 0, cap3 = c3 ? *c3 : 0;
+  const unsigned lane = threadIdx.x & 31;
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  for (std::uint64_t base = blockIdx.x * std::uint64_t(blockDim.x) + (threadIdx.x & ~31u);
+       base < n; base += stride) {
+    const std::uint64_t i = base + lane;
+    bool keep = false;
+    std::uint64_t key = 0;
+    if (i < n) {
+      key = ws[i];
+      keep = key < store_keys && (!cap1 || probe_slot(k1, cap1, key) == kNoSlot) &&
+             (!cap2 || probe_slot(k2, cap2, key) == kNoSlot) &&
+             (!cap3 || probe_slot(k3, cap3, key) == kNoSlot);
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
+    if (m) {
+      unsigned long long at = 0;
+      if (lane == 0) {
+        at = atomicAdd(n_out, (unsigned long long)__popc(m));
+        atomicAdd(total, (unsigned long long)__popc(m));
+      }
+      at = __shfl_sync(0xFFFFFFFFu, at, 0);
+      if (keep) {
+        const unsigned r = __popc(m & ((1u << lane) - 1u));
+        out_key[at + r] = key;
+        out_slot[at + r] = wslot[i];
+      }
+    }
+  }
+}
+
+// The evicted rows of the list to the value store (zero-copy for a host
+// store): ILP independent row loads per thread before their posted stores.
 template <int VEC, int ILP>
-__global__ void table_writeback_sorted_kernel(const std::uint64_t* __restrict__ ws,
-                                              const std::uint32_t* __restrict__ wslot,
-                                              const std::uint64_t* __restrict__ n_ptr,
-                                              const float* __restrict__ vals,
-                                              float* __restrict__ store, std::uint64_t store_keys,
-                                              int E) {
+__global__ void store_scatter_kernel(const std::uint64_t* __restrict__ keys,
+                                     const std::uint32_t* __restrict__ slots,
+                                     const unsigned long long* __restrict__ n_ptr,
+                                     const float* __restrict__ vals, float* __restrict__ store,
+                                     int E) {
   using V = typename std::conditional<VEC == 4, float4, float>::type;
   const int tpk = E / VEC;
-  const std::uint64_t total = *n_ptr * std::uint64_t(tpk);
+  const std::uint64_t total = std::uint64_t(*n_ptr) * tpk;
   const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
   for (std::uint64_t t0 = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t0 < total;
        t0 += stride * ILP) {
     V v[ILP];
-    std::uint64_t key[ILP];
+    std::uint64_t dst[ILP];
 #pragma unroll
     for (int u = 0; u < ILP; ++u) {
       const std::uint64_t t = t0 + u * stride;
-      key[u] = ~std::uint64_t(0);
       if (t < total) {
         const std::uint64_t i = t / tpk;
         const int part = int(t - i * tpk);
-        key[u] = ws[i] * E + std::uint64_t(part) * VEC;
-        if (ws[i] >= store_keys) key[u] = ~std::uint64_t(0);
-        v[u] = reinterpret_cast<const V*>(vals + std::uint64_t(wslot[i]) * E)[part];
+        v[u] = reinterpret_cast<const V*>(vals + std::uint64_t(slots[i]) * E)[part];
+        dst[u] = keys[i] * E + std::uint64_t(part) * VEC;
       }
     }
 #pragma unroll
     for (int u = 0; u < ILP; ++u)
-      if (key[u] != ~std::uint64_t(0)) *reinterpret_cast<V*>(store + key[u]) = v[u];
+      if (t0 + u * stride < total) *reinterpret_cast<V*>(store + dst[u]) = v[u];
   }
 }
-
 
 // Row fill for the fresh table (hbm_ps.hpp:86-98): carry-over from the
 // previous table when the key was resident, else the staged host row

@@ -125,7 +125,10 @@ struct Scalars {
   std::uint32_t pad0, pad1;
   std::int64_t total_unused;   // host side: offsets[B] of a device batch
   unsigned long long gn[4];      // grouping (prep lane): n_long, n_dup, n_huge
+  unsigned long long wb_n[kTables];  // rows on each table's write-back list
+  unsigned long long wb_total;       // rows written to the store (cumulative)
   unsigned long long Ug[kTables][64];  // unique keys per (table, mini-batch), grouped path
+  std::uint64_t rq_capv;               // request-table capacity (G > 1)
   unsigned long long fallbacks;  // certified sums that needed the exact chain
   unsigned long long served;     // keys this rank served as owner (G > 1)
   DevError err;
@@ -223,7 +226,12 @@ struct Tier {
   cudaEvent_t ev_wbt[kTables][2] = {};  // write-back timing pairs
   bool body_pending[kTables] = {}, sp_pending[kSlots] = {}, wb_pending[kTables] = {},
        wb_timed[kTables] = {};
-  bool tab_wb[kTables] = {};            // table's final rows go to the current store
+  bool tab_wb[kTables] = {};            // a train table of the current store (its rows
+                                        // reach the store on eviction or flush)
+  bool tab_flushed[kTables] = {};       // ... and they are there already
+  std::uint64_t tab_age[kTables] = {};  // build order
+  std::uint64_t builds = 0;
+  std::uint64_t rows_read = 0;          // store rows read (completed batches, cumulative)
   std::deque<BatchPlan> inflight;       // submitted, not yet completed (<= kSlots)
   struct Done {
     std::uint64_t id;
@@ -301,6 +309,10 @@ struct Tier {
   // sum of the earlier mini-batches' shape bounds) segments, example ids,
   // uid -> slot; uid counts in Scalars::Ug
   std::uint32_t* g_occslot[kTables] = {};
+  std::uint32_t* g_inv[kTables] = {};      // G > 1: occurrence -> uid (rows come in uid order)
+  std::uint64_t* rq_keys[kTables] = {};    // G > 1: request table, the rank's shard keys
+  std::uint64_t rq_cap = 0;
+  std::uint64_t gslots = 0;                 // entries of gcnt / slot_uid
   std::uint32_t* g_segb[kTables] = {};
   std::uint32_t* g_exsb[kTables] = {};
   std::uint32_t* g_uidb[kTables] = {};
@@ -322,6 +334,8 @@ struct Tier {
   cudaEvent_t trw[4][2] = {};  // write-back start/end by batch id % 4
   std::uint64_t* need_key[kTables] = {};   // store rows of each table's build
   std::uint32_t* need_slot[kTables] = {};
+  std::uint64_t* wb_key[kTables] = {};     // each table's write-back list
+  std::uint32_t* wb_slot[kTables] = {};
   bool store_registered = false;
   float* store_host = nullptr;
 
@@ -402,11 +416,27 @@ static unsigned grid_for(std::uint64_t work, int threads = 256,
   return unsigned(std::max<std::uint64_t>(1, std::min<std::uint64_t>(b, cap)));
 }
 
+bool debug_sync_enabled();
+
+// HPS_DEBUG_SYNC=1 (diagnostics, graphs must be off): synchronise after every
+// launch and name the kernel that failed.
+template <class K>
+static void debug_sync(K* k, cudaStream_t s) {
+  if (!debug_sync_enabled()) return;
+  const cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    const char* name = "?";
+    cudaFuncGetName(&name, reinterpret_cast<const void*>(k));
+    std::fprintf(stderr, "[hps debug] kernel %s: %s\n", name, cudaGetErrorString(e));
+  }
+}
+
 template <class... KArgs, class... Args>
 static void launch(Tier* t, void (*k)(KArgs...), dim3 grid, dim3 block,
                    size_t smem, Args&&... args) {
   k<<<grid, block, smem, t->L->st>>>(std::forward<Args>(args)...);
   ++t->launches;
+  debug_sync(k, t->L->st);
 }
 
 template <class... KArgs, class... Args>
@@ -414,6 +444,7 @@ static void launch_on(Tier* t, cudaStream_t s, void (*k)(KArgs...), dim3 grid, d
                       size_t smem, Args&&... args) {
   k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
   ++t->launches;
+  debug_sync(k, s);
 }
 
 
@@ -851,6 +882,8 @@ static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* sta
   t->prev = prv;
   t->cur = nxt;
   t->tab_wb[nxt] = false;  // not a train-batch table: never a store proxy
+  t->tab_flushed[nxt] = false;
+  t->tab_age[nxt] = ++t->builds;
 }
 
 // ------------------------------------------------- dedup + pull (core) --
@@ -866,6 +899,8 @@ struct PullPlan {
   const std::uint32_t* pos = nullptr;     // null when G == 1
   std::uint64_t R = 0;                    // keys served as owner
 };
+
+static hps_status exchange_pull(Tier* t, std::uint64_t n, bool do_gather);
 
 static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint32_t* vin,
                              Count cn, std::uint64_t n, PullPlan* plan, bool do_gather,
@@ -901,10 +936,16 @@ static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint3
     }
     return HPS_OK;
   }
-  // G > 1: each unique key's rank among the keys of its owner (one look-back
-  // pass that also opens the exchange round), then (key, uid) pairs go
-  // straight into the owners' windows over NVLink; rows come back in uid order
   plan->pos = nullptr;
+  return exchange_pull(t, n, do_gather);
+}
+
+// G > 1, the unique keys t->ukeys[0 .. dsc->U): each key's rank among the
+// keys of its owner (one look-back pass that also opens the exchange round),
+// then (key, uid) pairs go straight into the owners' windows over NVLink;
+// rows come back in uid order into t->rows.
+static hps_status exchange_pull(Tier* t, std::uint64_t n, bool do_gather) {
+  const int V = vec_of(t->E);
   {
     const std::uint32_t nb = std::max<std::uint32_t>(
         1, std::uint32_t((n + kRankTile - 1) / kRankTile));
@@ -1006,10 +1047,6 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,
          E, lr, n, U, seg, exs, pos, DX, t->deltas, pulled, t->long_list, nl, t->big_list, nb,
          std::uint32_t(kMediumMax));
-  if (kMediumMax > kLongSeg)
-    launch(t, sparse_delta_long_kernel, kSMs * 2, kLongThreads, 0, E, lr, n,
-           (const std::uint32_t*)t->long_list, (const unsigned long long*)nl, seg, exs, pos, DX,
-           t->deltas, &t->dsc->fallbacks);
   // big segments: plan (key, chunk) items, then one fused pass over CTAs
   // (ticket order; flags and ticket reset per launch)
   const int chunk = fuse_chunk(E);
@@ -1157,8 +1194,11 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     HPS_CUDA(cudaMemsetAsync(T->dsc->gn, 0, sizeof(T->dsc->gn), l.st));
     if (!n) continue;
     const std::uint64_t warps = ((n + 31) / 32) * kGroupPosGroups;
-    launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys,
-           (const std::uint64_t*)T->tkeys[tb], (const std::uint64_t*)&T->dsc->cap[tb], T->gcnt,
+    // slot space: the batch table (G == 1: it holds every key) or the
+    // rank's request table (G > 1)
+    const std::uint64_t* gk = G == 1 ? T->tkeys[tb] : T->rq_keys[tb];
+    const std::uint64_t* gc = G == 1 ? &T->dsc->cap[tb] : &T->dsc->rq_capv;
+    launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys, gk, gc, T->gcnt,
            T->slot_uid, T->part_slot, pcap, T->part_n, T->g_occslot[tb], T->g_tick, T->g_exof,
            &T->dsc->err);
     launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)T->part_n,
@@ -1168,7 +1208,7 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     launch(T, group_place_kernel, grid_for(n * 32), 256, 0, sm, doff,
            (const std::uint32_t*)T->g_occslot[tb], (const std::uint32_t*)T->g_tick,
            (const std::uint32_t*)T->slot_uid, pcap, (const std::uint32_t*)T->part_base,
-           (const std::uint32_t*)seg, T->g_segocc);
+           (const std::uint32_t*)seg, T->g_segocc, G == 1 ? nullptr : T->g_inv[tb]);
     launch(T, group_order_kernel, grid_for(ob), 256, 0, (const unsigned long long*)U,
            (const std::uint32_t*)seg, T->g_segocc, (const std::uint32_t*)T->g_exof,
            (const std::uint32_t*)uids, T->gcnt, exs, T->g_long, &T->dsc->gn[0], T->g_huge,
@@ -1227,6 +1267,12 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   // the table's keys are final: the mini-batches' grouping forks onto lane 2
   // and runs beside the rest of the build (joined at the end of the prep)
   if (bp.grouped) {
+    if (G > 1) {  // the request table: every key of this rank's shards
+      HPS_CUDA(cudaMemsetAsync(T->rq_keys[tb], 0xFF, T->rq_cap * 8, l.st));
+      launch(T, rq_insert_kernel, grid_for(sh.B * 32), 256, 0, T->b_off[bp.sp],
+             (const std::uint64_t*)dkeys, sh.B, G, T->g, T->J, T->rq_keys[tb],
+             (const std::uint64_t*)&T->dsc->rq_capv);
+    }
     HPS_CUDA(cudaEventRecord(T->g_fork, l.st));
     HPS_CUDA(cudaStreamWaitEvent(T->lane[2].st, T->g_fork, 0));
     T->L = &T->lane[2];
@@ -1337,18 +1383,28 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     const std::uint32_t* exsj = T->exs;
     const std::uint32_t* slotsj = T->slots;      // uid -> table slot (G == 1)
     if (bp.grouped) {
-      // grouped by batch-table slot on the prep lane (enqueue_grouping): no
-      // sort here, and fwd/bwd reads the rows in place from the table
+      // grouped by slot on the prep lane (enqueue_grouping): no sort here
       const std::uint64_t r0 = group_region(sh, j);
       Uj = reinterpret_cast<const std::uint64_t*>(&T->dsc->Ug[bp.tb][j]);
       segj = T->g_segb[bp.tb] + r0 + j;
       exsj = T->g_exsb[bp.tb] + r0;
       slotsj = T->g_uidb[bp.tb] + r0;
-      mark(T, HPS_T_DEDUP);
-      mark(T, HPS_T_PULL);
-      occ_row = T->g_occslot[bp.tb];
-      rows = T->tvals[T->cur];
       goff = doff;  // occurrence ids are batch key indices
+      if (G == 1) {  // fwd/bwd reads the rows in place from the table
+        mark(T, HPS_T_DEDUP);
+        mark(T, HPS_T_PULL);
+        occ_row = T->g_occslot[bp.tb];
+        rows = T->tvals[T->cur];
+      } else {  // unique keys in uid order -> the NVLink exchange -> rows by uid
+        HPS_CUDA(cudaMemcpyAsync(&T->dsc->U, Uj, 8, cudaMemcpyDeviceToDevice, T->st));
+        launch(T, uid_keys_kernel, grid_for(ob), 256, 0, slotsj,
+               (const std::uint64_t*)T->rq_keys[bp.tb], (const unsigned long long*)Uj,
+               T->ukeys);
+        begin_round(T, false);
+        HPS_TRY(exchange_pull(T, ob, true));
+        Uj = &T->dsc->U;
+        occ_row = T->g_inv[bp.tb];
+      }
     } else {
       if (n) {
         tile_scan(T, ShardLen{sm, doff}, ShardLenEmit{T->occ_off, n}, Count{nullptr, n}, n,
@@ -1411,24 +1467,65 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
   return HPS_OK;
 }
 
-// Write-back of table tb to the value store (a13, hbm_ps.hpp:224-232 +
-// MemPs::collect_updates) on st_wb after its body, in ascending key order.
-static hps_status enqueue_writeback(Tier* T, int tb) {
+// Write-back of table t to the value store (a13: dump_node ->
+// MemPs::collect_updates, hbm_ps.hpp:224-232, mem_ps.hpp:210-245) on st_wb,
+// after its body: the rows no newer resident train table holds (`newer`, up
+// to 3; those hold fresher rows and write them back themselves), in key
+// order. The store is exact for every key outside the resident tables, which
+// is all the next builds read from it; hps_flush makes it exact for all keys.
+static hps_status enqueue_writeback(Tier* T, int t, const int* newer, int n_newer) {
   const int E = T->E, V = vec_of(E);
-  HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_body_tab[tb], 0));
-  if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[tb][0], T->st_wb));
+  HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_body_tab[t], 0));
+  if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[t][0], T->st_wb));
+  const std::uint64_t* nk[3] = {nullptr, nullptr, nullptr};
+  const std::uint64_t* nc[3] = {nullptr, nullptr, nullptr};
+  for (int i = 0; i < n_newer && i < 3; ++i) {
+    nk[i] = T->tkeys[newer[i]];
+    nc[i] = &T->dsc->cap[newer[i]];
+  }
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->wb_n[t], 0, 8, T->st_wb));
+  launch_on(T, T->st_wb, table_evict_filter_kernel, grid_for(T->Wmax), 256, 0,
+            (const std::uint64_t*)T->wsb[t], (const std::uint32_t*)T->wsib[t],
+            (const std::uint64_t*)&T->dsc->nws_tab[t], nk[0], nc[0], nk[1], nc[1], nk[2], nc[2],
+            T->store_keys, T->wb_key[t], T->wb_slot[t], &T->dsc->wb_n[t], &T->dsc->wb_total);
   const std::uint64_t work = T->Wmax * std::uint64_t(E / V);
   // posted PCIe writes: a few CTAs saturate the link without holding SMs
   const unsigned gw = T->store_on_host ? T->wb_ctas : grid_for(work, 256 * 4);
   const int tpb = T->store_on_host ? T->zc_threads : 256;
-  auto k = V == 4 ? table_writeback_sorted_kernel<4, 4> : table_writeback_sorted_kernel<1, 4>;
-  launch_on(T, T->st_wb, k, gw, tpb, 0, (const std::uint64_t*)T->wsb[tb],
-            (const std::uint32_t*)T->wsib[tb], (const std::uint64_t*)&T->dsc->nws_tab[tb],
-            (const float*)T->tvals[tb], T->store, T->store_keys, E);
-  if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[tb][1], T->st_wb));
-  HPS_CUDA(cudaEventRecord(T->ev_wb[tb], T->st_wb));
-  T->wb_pending[tb] = true;
-  T->wb_timed[tb] = T->timing;
+  auto k = V == 4 ? store_scatter_kernel<4, 4> : store_scatter_kernel<1, 4>;
+  launch_on(T, T->st_wb, k, gw, tpb, 0, (const std::uint64_t*)T->wb_key[t],
+            (const std::uint32_t*)T->wb_slot[t], (const unsigned long long*)&T->dsc->wb_n[t],
+            (const float*)T->tvals[t], T->store, E);
+  if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[t][1], T->st_wb));
+  HPS_CUDA(cudaEventRecord(T->ev_wb[t], T->st_wb));
+  T->wb_pending[t] = true;
+  T->wb_timed[t] = T->timing;
+  return HPS_OK;
+}
+
+// Train tables of the current store newer than table t (newest first).
+static int newer_tables(const Tier* T, int t, int* out) {
+  int n = 0;
+  for (int q = 0; q < kTables; ++q)
+    if (q != t && T->tab_wb[q] && T->tab_age[q] > T->tab_age[t]) out[n++] = q;
+  std::sort(out, out + n, [T](int a, int b) { return T->tab_age[a] > T->tab_age[b]; });
+  return std::min(n, 3);
+}
+
+// Every resident train table's rows that are not in the store yet, oldest
+// first (enqueue-only on st_wb): afterwards the store holds every trained row.
+static hps_status flush_all(Tier* T) {
+  if (!T->store) return HPS_OK;
+  int order[kTables], n = 0;
+  for (int q = 0; q < kTables; ++q)
+    if (T->tab_wb[q] && !T->tab_flushed[q]) order[n++] = q;
+  std::sort(order, order + n, [T](int a, int b) { return T->tab_age[a] < T->tab_age[b]; });
+  for (int i = 0; i < n; ++i) {
+    int newer[kTables];
+    const int nn = newer_tables(T, order[i], newer);
+    HPS_TRY(enqueue_writeback(T, order[i], newer, nn));
+    T->tab_flushed[order[i]] = true;
+  }
   return HPS_OK;
 }
 
@@ -1529,6 +1626,7 @@ static void complete_oldest(Tier* T) {
     st.pulled_keys = o.pulled;
     st.carried_rows = o.carried;
     st.store_rows = o.stored;
+    T->rows_read += o.stored;
     st.exact_fallbacks = o.fallbacks;
     st.served_keys = o.served;
     st.occurrences = bp.occ_total;
@@ -1560,6 +1658,7 @@ static void complete_oldest(Tier* T) {
 // The parity API (build / pull / push / drain / dump ...) starts from here.
 static hps_status quiesce(Tier* T) {
   while (!T->inflight.empty()) complete_oldest(T);
+  HPS_TRY(flush_all(T));
   return wb_fence(T);
 }
 
@@ -1660,7 +1759,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   {  // slot grouping (G == 1) when its shared-memory bitmaps fit
     const std::uint64_t nmax = (B + std::uint64_t(G) * J - 1) / (std::uint64_t(G) * J);
     const std::size_t words = std::size_t((nmax + 31) / 32);
-    bp.grouped = G == 1 && T->hash_dedup &&
+    bp.grouped = T->hash_dedup &&
                  std::size_t(kGroupWarpThreads / 32) * 8 * words <= kGroupSmemMax;
   }
   // ---- prep on lane 1, beside the previous body
@@ -1735,13 +1834,20 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   HPS_CUDA(cudaEventRecord(T->ev_body_sp[sp], T->st));
   T->body_pending[tb] = true;
   T->sp_pending[sp] = true;
-  // ---- write-back (collect) on st_wb, overlapping the next batch
   T->tab_wb[tb] = T->store != nullptr;
-  if (T->store) {
-    HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_body_tab[tb], 0));
+  T->tab_flushed[tb] = false;
+  T->tab_age[tb] = ++T->builds;
+  // ---- eviction write-back (the collect stage) on st_wb, overlapping the
+  // next batches: the table the next build recycles gives up its rows now
+  const int tr = next_table(T);
+  if (T->store && T->tab_wb[tr] && !T->tab_flushed[tr] && tr != tb) {
+    int newer[kTables];
+    const int nn = newer_tables(T, tr, newer);
+    HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_prep, 0));  // this batch's keys are final
     if (T->trace) cudaEventRecord(T->trw[bp.id & 3][0], T->st_wb);
-    HPS_TRY(enqueue_writeback(T, tb));
+    HPS_TRY(enqueue_writeback(T, tr, newer, nn));
     if (T->trace) cudaEventRecord(T->trw[bp.id & 3][1], T->st_wb);
+    T->tab_flushed[tr] = true;
   }
   T->inflight.push_back(bp);
   ++T->submitted;
@@ -1757,6 +1863,14 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
 using namespace hpsgpu;
 
 struct hps_tier : public hpsgpu::Tier {};
+
+bool hpsgpu::debug_sync_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("HPS_DEBUG_SYNC");
+    return v && std::atoi(v) != 0;
+  }();
+  return on;
+}
 
 extern "C" {
 
@@ -1818,6 +1932,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_WB_CTAS")) t->wb_ctas = unsigned(std::max(1, std::atoi(v)));
   if (const char* v = std::getenv("HPS_TRACE")) t->trace = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_DEDUP")) t->hash_dedup = std::strcmp(v, "sort") != 0;
+  if (const char* v = std::getenv("HPS_GRAPHS")) t->use_graphs = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
@@ -1945,9 +2060,16 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   for (int i = 0; i < kTables; ++i) {
     A(need_key[i], W);
     A(need_slot[i], W);
+    A(wb_key[i], W);
+    A(wb_slot[i], W);
   }
-  A(gcnt, t->capmax);
-  A(slot_uid, t->capmax);
+  // per-slot grouping arrays cover the largest slot space: the batch table
+  // (G == 1) or the request table (G > 1)
+  t->rq_cap = 1;
+  while (t->rq_cap < 2 * std::max(O, W)) t->rq_cap <<= 1;
+  t->gslots = G > 1 ? std::max(t->capmax, t->rq_cap) : t->capmax;
+  A(gcnt, t->gslots);
+  A(slot_uid, t->gslots);
   t->ws = t->wsb[0];
   t->ws_idx = t->wsib[0];
   t->wsset_cap = 1;
@@ -1985,6 +2107,10 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   t->g_pool = 2 * S + std::uint64_t(t->J) * 4096 + 64;  // >= the sum of the shape bounds
   for (int i = 0; i < kTables; ++i) {
     A(g_occslot[i], S);
+    if (G > 1) {
+      A(g_inv[i], S);
+      A(rq_keys[i], t->rq_cap);
+    }
     A(g_segb[i], t->g_pool + 64);
     A(g_exsb[i], t->g_pool);
     A(g_uidb[i], t->g_pool);
@@ -2021,12 +2147,14 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
 #undef A
-  cudaMemsetAsync(t->gcnt, 0, t->capmax * 4, t->st);
+  cudaMemsetAsync(t->gcnt, 0, t->gslots * 4, t->st);
   cudaMemsetAsync(t->part_n, 0, std::uint64_t(kGroupParts) * kGroupPartStride * 4, t->st);
   cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
   cudaMemsetAsync(t->key_done, 0, (S / (kLongSeg + 1) + 2) * 4, t->st);
   if ((e = cudaMemsetAsync(t->dsc, 0, sizeof(Scalars), t->st)) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: memset: %s", cudaGetErrorString(e)));
+  t->hsc->rq_capv = t->rq_cap;
+  cudaMemcpyAsync(&t->dsc->rq_capv, &t->hsc->rq_capv, 8, cudaMemcpyHostToDevice, t->st);
   // replicate_dense(init_dense(cfg)) — the init stream is host-side std::mt19937_64
   {
     std::vector<float> w(t->md.nw);
@@ -2051,6 +2179,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
 hps_status hps_destroy(hps_tier_t t) {
   if (!t) return HPS_OK;
   cudaSetDevice(t->cfg.cuda_device);
+  if (t->dsc) quiesce(t);  // in-flight batches, then every resident row to the store
   for (cudaStream_t x : {t->st, t->lane[1].st, t->lane[2].st, t->st_stage, t->st_wb, t->st2,
                          t->st_pf})
     if (x) cudaStreamSynchronize(x);
@@ -2239,7 +2368,7 @@ hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uin
 hps_status hps_drain(hps_tier_t t) {
   HPS_ENTER_Q(t);
   HPS_TRY(require_built(t));
-  t->tab_wb[t->cur] = false;  // rows change after their write-back: no store proxy
+  t->tab_flushed[t->cur] = false;  // its rows changed: written back again
   const int V = vec_of(t->E);
   for (int src : canonical_senders(t)) {
     for (auto& c : t->pending) {
@@ -2375,12 +2504,22 @@ hps_status hps_set_dense(hps_tier_t t, const float* w) {
 }
 
 hps_status hps_flush(hps_tier_t t) {
-  HPS_ENTER_Q(t);
+  HPS_ENTER_Q(t);  // (quiesce: in-flight batches done, every resident row queued)
   HPS_CUDA(cudaStreamSynchronize(t->st_wb));
   for (int p = 0; p < kTables; ++p) {
     wb_account(t, p, true);
     t->wb_pending[p] = false;
   }
+  return HPS_OK;
+}
+
+hps_status hps_store_traffic(hps_tier_t t, uint64_t* rows_read, uint64_t* rows_written) {
+  HPS_ENTER(t);
+  HPS_CUDA(cudaMemcpyAsync(&t->hsc->wb_total, &t->dsc->wb_total, 8, cudaMemcpyDeviceToHost,
+                           t->st_wb));
+  HPS_CUDA(cudaStreamSynchronize(t->st_wb));
+  if (rows_read) *rows_read = t->rows_read;
+  if (rows_written) *rows_written = t->hsc->wb_total;
   return HPS_OK;
 }
 

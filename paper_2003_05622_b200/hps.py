@@ -104,6 +104,8 @@ _SIGS = {
     "hps_set_dense": ([_P, _P], ctypes.c_int),
     "hps_attach_store": ([_P, _P, _U64, ctypes.c_int], ctypes.c_int),
     "hps_flush": ([_P], ctypes.c_int),
+    "hps_store_traffic": ([_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)],
+                          ctypes.c_int),
     "hps_train_batch": ([_P, _U64, _P, _P, _P, ctypes.c_int,
                          ctypes.POINTER(HpsBatchStats)], ctypes.c_int),
     "hps_submit_batch": ([_P, _U64, _P, _P, _P, ctypes.c_int], ctypes.c_int),
@@ -335,6 +337,12 @@ class Tier:
                 raise Error(1, "store must be a C-contiguous float32 array")
             _check(lib().hps_attach_store(self._h, _ptr(rows), rows.shape[0], 0))
             self._store = rows
+
+    def store_traffic(self):
+        """(rows read from, rows written to) the value store since creation."""
+        r, w = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().hps_store_traffic(self._h, ctypes.byref(r), ctypes.byref(w)))
+        return r.value, w.value
 
     def flush(self) -> None:
         """Wait for the deferred write-backs (hps_flush): afterwards the
