@@ -160,6 +160,11 @@ __global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys
   }
 }
 
+// Row-source tags in the top bits of csrc (slots stay below 2^30).
+constexpr std::uint32_t kSrcMask = 0xC0000000u;
+constexpr std::uint32_t kSrcProxy1 = 0x40000000u;  // the table two builds back
+constexpr std::uint32_t kSrcProxy2 = 0x80000000u;  // three builds back
+
 // Pipelined build, prep half (runs beside the previous batch's body), in two
 // kernels so that PCIe latency never sits behind HBM probes:
 // table_prefetch_probe_kernel (full grid, HBM only), one thread per
@@ -175,8 +180,7 @@ __global__ void table_prefetch_probe_kernel(
     const std::uint64_t* __restrict__ n_ptr, float* __restrict__ vals,
     std::uint32_t* __restrict__ csrc, const std::uint64_t* __restrict__ prev_keys,
     const std::uint64_t* __restrict__ prev_cap_ptr, const std::uint64_t* __restrict__ old_keys,
-    const float* __restrict__ old_vals, const std::uint64_t* __restrict__ old_cap_ptr,
-    const std::uint64_t* __restrict__ old2_keys, const float* __restrict__ old2_vals,
+    const std::uint64_t* __restrict__ old_cap_ptr, const std::uint64_t* __restrict__ old2_keys,
     const std::uint64_t* __restrict__ old2_cap_ptr, bool from_store, std::uint64_t store_keys, int E, std::uint64_t* __restrict__ need_key,
     std::uint32_t* __restrict__ need_slot, unsigned long long* __restrict__ n_need,
     unsigned long long* carried) {
@@ -196,26 +200,29 @@ __global__ void table_prefetch_probe_kernel(
     const std::uint32_t slot = live ? wslot[i] : 0;
     std::uint32_t ps = kNoSlot;
     if (live && pcap) ps = probe_slot(prev_keys, pcap, key);
-    if (live) csrc[i] = ps;
     bool need = false;
     if (live && ps == kNoSlot) {
-      // newest proxy first: its row is the key's latest
-      const float* src = nullptr;
+      // newest proxy first: its row is the key's latest. The copy itself is
+      // table_carry_kernel's (in the body, when the source rows are final),
+      // so this prep never waits for the batches still training.
+      std::uint32_t src = kNoSlot;
       const std::uint32_t os = ocap ? probe_slot(old_keys, ocap, key) : kNoSlot;
       if (os != kNoSlot) {
-        src = old_vals + std::uint64_t(os) * E;
+        src = kSrcProxy1 | os;
       } else if (o2cap) {
         const std::uint32_t o2 = probe_slot(old2_keys, o2cap, key);
-        if (o2 != kNoSlot) src = old2_vals + std::uint64_t(o2) * E;
+        if (o2 != kNoSlot) src = kSrcProxy2 | o2;
       }
-      float* dst = vals + std::uint64_t(slot) * E;
-      if (src) {
-        for (int d = 0; d < E; ++d) dst[d] = src[d];
+      csrc[i] = src;
+      if (src != kNoSlot) {
       } else if (from_store && key < store_keys) {
         need = true;
       } else {
+        float* dst = vals + std::uint64_t(slot) * E;
         for (int d = 0; d < E; ++d) dst[d] = 0.0f;
       }
+    } else if (live) {
+      csrc[i] = ps;  // carry-over from the previous table (tag 0)
     }
     n_car += (live && ps != kNoSlot);
     const unsigned m = __ballot_sync(0xFFFFFFFFu, need);
@@ -267,12 +274,15 @@ __global__ void store_gather_kernel(const std::uint64_t* __restrict__ need_key,
   }
 }
 
-// Pipelined build, body half: the carried rows, after the previous batch.
+// Pipelined build, body half: the rows from the resident tables (the
+// previous table's carry-over, or a proxy's), once those batches are done.
 template <int VEC>
 __global__ void table_carry_kernel(const std::uint32_t* __restrict__ csrc,
                                    const std::uint32_t* __restrict__ wslot,
                                    const std::uint64_t* __restrict__ n_ptr,
-                                   const float* __restrict__ prev_vals, float* __restrict__ vals,
+                                   const float* __restrict__ prev_vals,
+                                   const float* __restrict__ p1_vals,
+                                   const float* __restrict__ p2_vals, float* __restrict__ vals,
                                    int E) {
   const int tpk = E / VEC;
   const std::uint64_t n = *n_ptr;
@@ -282,7 +292,9 @@ __global__ void table_carry_kernel(const std::uint32_t* __restrict__ csrc,
     const std::uint32_t ps = csrc[i];
     if (ps == kNoSlot) continue;
     const int part = int(t - i * tpk);
-    const float* src = prev_vals + std::uint64_t(ps) * E + part * VEC;
+    const std::uint32_t tag = ps & kSrcMask;
+    const float* base = tag == kSrcProxy1 ? p1_vals : (tag == kSrcProxy2 ? p2_vals : prev_vals);
+    const float* src = base + std::uint64_t(ps & ~kSrcMask) * E + part * VEC;
     float* dst = vals + std::uint64_t(wslot[i]) * E + part * VEC;
     if (VEC == 4) {
       st_f4(dst, ld_f4(src));

@@ -101,10 +101,12 @@ static NcclApi& nccl() {
 
 // --------------------------------------------------------- the tier ----
 
-// tables: current, previous (carry-over), and two older ones whose rows stand
-// in for the store while their write-backs drain (store proxies)
-constexpr int kTables = 4;
-constexpr int kSlots = 4;   // staging slots = batches in flight
+// tables: current, previous (carry-over), two older ones whose rows stand in
+// for the store (store proxies, copied by the body), and one more so the
+// table a body reads as its oldest proxy is recycled two builds later
+constexpr int kTables = 5;
+constexpr int kSlots = 5;   // staging slots (rotating with the tables: one graph per slot per shape)
+constexpr int kMaxInflight = 4;  // batches in flight
 
 struct Scalars {
   std::uint64_t n_ws;          // working-set size of the current build
@@ -223,6 +225,7 @@ struct Tier {
   cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
   cudaEvent_t ev_staged = nullptr, ev_prep = nullptr;
   cudaEvent_t ev_body_tab[kTables] = {}, ev_body_sp[kSlots] = {}, ev_wb[kTables] = {};
+  cudaEvent_t ev_carry_sp[kSlots] = {};  // a body's resident-table copies are done
   cudaEvent_t ev_wbt[kTables][2] = {};  // write-back timing pairs
   bool body_pending[kTables] = {}, sp_pending[kSlots] = {}, wb_pending[kTables] = {},
        wb_timed[kTables] = {};
@@ -255,6 +258,7 @@ struct Tier {
   std::uint64_t* tkeys[kTables] = {};
   float* tvals[kTables] = {};
   int cur = -1, prev = -1, prev2 = -1;
+  int hist[kTables] = {-1, -1, -1, -1, -1};  // table of the k-th most recent build
 
   // working set
   std::uint64_t* ws = nullptr;       // sorted keys of the current table (when ws_sorted)
@@ -332,6 +336,7 @@ struct Tier {
   cudaEvent_t tr_base = nullptr;
   cudaEvent_t tr[kSlots][6] = {};   // by staging slot: stage0 stage1 prep0 prep1 body0 body1
   cudaEvent_t trw[4][2] = {};  // write-back start/end by batch id % 4
+  cudaEvent_t trg[kSlots][2] = {};  // store gather start/end by staging slot
   std::uint64_t* need_key[kTables] = {};   // store rows of each table's build
   std::uint32_t* need_slot[kTables] = {};
   std::uint64_t* wb_key[kTables] = {};     // each table's write-back list
@@ -884,6 +889,8 @@ static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* sta
   t->tab_wb[nxt] = false;  // not a train-batch table: never a store proxy
   t->tab_flushed[nxt] = false;
   t->tab_age[nxt] = ++t->builds;
+  for (int k = kTables - 1; k > 0; --k) t->hist[k] = t->hist[k - 1];
+  t->hist[0] = nxt;
 }
 
 // ------------------------------------------------- dedup + pull (core) --
@@ -1300,15 +1307,13 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   const std::uint64_t* pk = tp >= 0 ? T->tkeys[tp] : nullptr;
   const std::uint64_t* pc = tp >= 0 ? &T->dsc->cap[tp] : nullptr;
   const std::uint64_t* qk = tq >= 0 ? T->tkeys[tq] : nullptr;
-  const float* qv = tq >= 0 ? T->tvals[tq] : nullptr;
   const std::uint64_t* qc = tq >= 0 ? &T->dsc->cap[tq] : nullptr;
   const int tq2 = bp.tq2;
   const std::uint64_t* q2k = tq2 >= 0 ? T->tkeys[tq2] : nullptr;
-  const float* q2v = tq2 >= 0 ? T->tvals[tq2] : nullptr;
   const std::uint64_t* q2c = tq2 >= 0 ? &T->dsc->cap[tq2] : nullptr;
   launch(T, table_prefetch_probe_kernel, grid_for(sh.own_bound), 256, 0,
          (const std::uint64_t*)T->wsb[tb], (const std::uint32_t*)T->wsib[tb],
-         (const std::uint64_t*)nws, T->tvals[tb], T->csrc[tb], pk, pc, qk, qv, qc, q2k, q2v, q2c,
+         (const std::uint64_t*)nws, T->tvals[tb], T->csrc[tb], pk, pc, qk, qc, q2k, q2c,
          T->store != nullptr, T->store_keys, E, T->need_key[tb], T->need_slot[tb],
          &T->dsc->stored_tab[tb], &T->dsc->carried_tab[tb]);
   // the store list is ready: the store gather (enqueue_store_gather, its own
@@ -1330,6 +1335,10 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
 static hps_status enqueue_store_gather(Tier* T, const BatchShape& sh, int tb) {
   const int E = T->E, V = vec_of(E);
   HPS_CUDA(cudaStreamWaitEvent(T->st_pf, T->pf_fork, 0));
+  // the store rows of keys last held by the table four builds back (not a
+  // proxy of this batch) arrive with its eviction write-back
+  const int te = T->hist[3];
+  if (te >= 0 && T->wb_pending[te]) HPS_CUDA(cudaStreamWaitEvent(T->st_pf, T->ev_wb[te], 0));
   const std::uint64_t work = sh.own_bound * std::uint64_t(E / V);
   const unsigned gg = T->store_on_host ? T->pf_ctas : grid_for(work, 256 * 4);
   const int tpb = T->store_on_host ? T->zc_threads : 256;
@@ -1356,13 +1365,21 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
   mark(T, -1);
   HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 16, T->st));       // loss, pulled
   HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 16, T->st));  // fallbacks, served
-  if (bp.tp >= 0) {
+  if (bp.tp >= 0) {  // rows from the resident tables (carry-over, proxies)
     const int V = vec_of(E);
     const unsigned gc = grid_for(sh.own_bound * std::uint64_t(E / V));
     auto k = V == 4 ? table_carry_kernel<4> : table_carry_kernel<1>;
     launch(T, k, gc, 256, 0, (const std::uint32_t*)T->csrc[bp.tb],
            (const std::uint32_t*)T->wsib[bp.tb], (const std::uint64_t*)&T->dsc->nws_tab[bp.tb],
-           (const float*)T->tvals[bp.tp], T->tvals[bp.tb], E);
+           (const float*)T->tvals[bp.tp], (const float*)(bp.tq >= 0 ? T->tvals[bp.tq] : nullptr),
+           (const float*)(bp.tq2 >= 0 ? T->tvals[bp.tq2] : nullptr), T->tvals[bp.tb], E);
+  }
+  {  // the proxies may be recycled from here on (see submit_batch)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(T->st, &cs);
+    HPS_CUDA(cudaEventRecordWithFlags(T->ev_carry_sp[bp.sp], T->st,
+                                      cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                          : 0));
   }
   mark(T, HPS_T_BUILD);
   // ---- mini-batches
@@ -1639,17 +1656,20 @@ static void complete_oldest(Tier* T) {
   if (T->timing) timing_end(T);
   for (int q = 0; q < kTables; ++q) wb_account(T, q, false);
   if (T->trace) {  // never waits: the write-back shown is batch id-3's, if done
-    float v[8] = {};
+    float v[8] = {}, gv[2] = {};
     for (int k = 0; k < 6; ++k) cudaEventElapsedTime(&v[k], T->tr_base, T->tr[bp.sp][k]);
+    if (T->store)
+      for (int k = 0; k < 2; ++k) cudaEventElapsedTime(&gv[k], T->tr_base, T->trg[bp.sp][k]);
     const int w = int((bp.id + 1) & 3);  // (id - 3) mod 4
     if (T->store && bp.id >= 3 && cudaEventQuery(T->trw[w][1]) == cudaSuccess) {
       cudaEventElapsedTime(&v[6], T->tr_base, T->trw[w][0]);
       cudaEventElapsedTime(&v[7], T->tr_base, T->trw[w][1]);
     }
     std::fprintf(stderr,
-                 "[trace] batch %llu: stage %.3f-%.3f prep %.3f-%.3f body %.3f-%.3f | "
-                 "wb(batch-3) %.3f-%.3f\n",
-                 (unsigned long long)bp.id, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+                 "[trace] batch %llu: stage %.3f-%.3f prep %.3f-%.3f gather %.3f-%.3f "
+                 "body %.3f-%.3f | wb(batch-3) %.3f-%.3f\n",
+                 (unsigned long long)bp.id, v[0], v[1], v[2], v[3], gv[0], gv[1], v[4], v[5], v[6],
+                 v[7]);
   }
   T->done.push_back(std::move(d));
 }
@@ -1674,7 +1694,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
                      (unsigned long long)B);
   if (T->timing)  // phases are attributed without overlap: one batch at a time
     while (!T->inflight.empty()) complete_oldest(T);
-  while (T->inflight.size() >= std::size_t(kSlots)) complete_oldest(T);
+  while (T->inflight.size() >= std::size_t(kMaxInflight)) complete_oldest(T);
   const int G = T->G, J = T->J;
   BatchPlan bp;
   bp.id = T->submitted;
@@ -1766,10 +1786,12 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   {
     cudaStream_t ps = T->lane[1].st;
     HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_staged, 0));
-    if (bp.tq >= 0 && T->body_pending[bp.tq])  // its rows final
-      HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tq], 0));
-    if (bp.tq2 >= 0 && T->body_pending[bp.tq2])
-      HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tq2], 0));
+    // (the proxies' rows are copied by this batch's body, after theirs); the
+    // batch two back read the table this build recycles as its oldest proxy
+    if (bp.id >= 2) {
+      const int sp2 = int((bp.id - 2) % kSlots);
+      HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_carry_sp[sp2], 0));
+    }
     if (T->body_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tb], 0));
     if (T->wb_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_wb[bp.tb], 0));
     if (T->trace) cudaEventRecord(T->tr[sp][2], ps);
@@ -1798,7 +1820,14 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     HPS_TRY(st);
     HPS_CUDA(cudaEventRecord(T->ev_prep, ps));
     if (T->trace) cudaEventRecord(T->tr[sp][3], ps);
-    if (T->store) HPS_TRY(enqueue_store_gather(T, sh, bp.tb));
+    if (T->store) {
+      if (T->trace) {
+        HPS_CUDA(cudaStreamWaitEvent(T->st_pf, T->pf_fork, 0));
+        cudaEventRecord(T->trg[sp][0], T->st_pf);
+      }
+      HPS_TRY(enqueue_store_gather(T, sh, bp.tb));
+      if (T->trace) cudaEventRecord(T->trg[sp][1], T->st_pf);
+    }
   }
   // ---- body on lane 0 (after its prep and its store rows)
   HPS_CUDA(cudaStreamWaitEvent(T->st, T->ev_prep, 0));
@@ -1813,7 +1842,8 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   T->ws_sorted = true;
   if (T->use_graphs && bp.skip_mb < 0) {
     std::vector<std::uint64_t> key = {2, B, sh.own_bound, std::uint64_t(bp.tb),
-                                      std::uint64_t(bp.tp + 1), std::uint64_t(sp),
+                                      std::uint64_t(bp.tp + 1), std::uint64_t(bp.tq + 1),
+                                      std::uint64_t(bp.tq2 + 1), std::uint64_t(sp),
                                       std::uint64_t(T->timing)};
     for (int j = 0; j < J; ++j) key.push_back(sh.mb_bound[j]);
     HPS_TRY(run_graph(T, key, [&] { return enqueue_body(T, sh, bp); }));
@@ -1837,10 +1867,15 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   T->tab_wb[tb] = T->store != nullptr;
   T->tab_flushed[tb] = false;
   T->tab_age[tb] = ++T->builds;
+  for (int k = kTables - 1; k > 0; --k) T->hist[k] = T->hist[k - 1];
+  T->hist[0] = tb;
   // ---- eviction write-back (the collect stage) on st_wb, overlapping the
-  // next batches: the table the next build recycles gives up its rows now
-  const int tr = next_table(T);
-  if (T->store && T->tab_wb[tr] && !T->tab_flushed[tr] && tr != tb) {
+  // next batches: the next batch reads its rows from the tables of this and
+  // the two previous batches, and the store — so the table three builds back
+  // gives up its rows now (those no newer table holds), and the next batch's
+  // store gather waits for it
+  const int tr = T->hist[3];
+  if (tr >= 0 && T->store && T->tab_wb[tr] && !T->tab_flushed[tr]) {
     int newer[kTables];
     const int nn = newer_tables(T, tr, newer);
     HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_prep, 0));  // this batch's keys are final
@@ -2011,11 +2046,14 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
       ev(&t->ev_wbt[i][1], true);
     }
     for (auto& x : t->ev_body_sp) ev(&x, false);
+    for (auto& x : t->ev_carry_sp) ev(&x, false);
     if (t->trace) {
       ev(&t->tr_base, true);
       for (auto& row : t->tr)
         for (auto& x : row) ev(&x, true);
       for (auto& row : t->trw)
+        for (auto& x : row) ev(&x, true);
+      for (auto& row : t->trg)
         for (auto& x : row) ev(&x, true);
       if (e == cudaSuccess) e = cudaEventRecord(t->tr_base, t->st);
     }
@@ -2202,6 +2240,8 @@ hps_status hps_destroy(hps_tier_t t) {
       if (x) cudaEventDestroy(x);
   }
   for (cudaEvent_t x : t->ev_body_sp)
+    if (x) cudaEventDestroy(x);
+  for (cudaEvent_t x : t->ev_carry_sp)
     if (x) cudaEventDestroy(x);
   for (cudaEvent_t x : {t->ev_staged, t->ev_prep, t->pf_fork, t->pf_join, t->g_fork, t->g_join,
                         t->g_ctx})

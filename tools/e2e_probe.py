@@ -4,6 +4,13 @@ workload: where do the host<->device milliseconds go? Diagnostic only.
   python tools/e2e_probe.py [--steps 40] [--store host|device] [--batch host|device]
 """
 import argparse
+import os as _os
+
+# The batch pipeline drives several concurrent streams (stage, prep, grouping,
+# store gather, body, dense-grad side stream, write-back): with CUDA's default
+# 8 hardware work queues, two of them can share a queue and one stream's
+# waits stall another's work. Must be set before the CUDA context exists.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import os
 import sys
 import time
