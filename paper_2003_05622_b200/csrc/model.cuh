@@ -536,7 +536,9 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
                                 const unsigned long long* __restrict__ n_big,
                                 const std::uint32_t* __restrict__ seg,
                                 std::uint32_t* __restrict__ chunk_off,
-                                unsigned long long* __restrict__ n_items) {
+                                unsigned long long* __restrict__ n_items,
+                                std::uint32_t* __restrict__ item_key,
+                                std::uint32_t* __restrict__ item_chunk) {
   __shared__ std::uint32_t ws[32];
   const std::uint64_t NB = *n_big;
   std::uint32_t carry = 0;
@@ -558,7 +560,13 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
     __syncthreads();
     std::uint32_t pre = carry;
     for (unsigned w = 0; w < warp; ++w) pre += ws[w];
-    if (i < NB) chunk_off[i] = pre + x - v;
+    if (i < NB) {
+      chunk_off[i] = pre + x - v;
+      for (std::uint32_t c = 0; c < v; ++c) {  // the item table: item -> (key, chunk)
+        item_key[pre + x - v + c] = std::uint32_t(i);
+        item_chunk[pre + x - v + c] = c;
+      }
+    }
     std::uint32_t tot = 0;
     for (unsigned w = 0; w < blockDim.x / 32; ++w) tot += ws[w];
     __syncthreads();
@@ -568,18 +576,6 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
     chunk_off[NB] = carry;
     *n_items = carry;
   }
-}
-
-__device__ __forceinline__ void big_item(const std::uint32_t* chunk_off, std::uint64_t NB,
-                                         std::uint64_t w, std::uint32_t* key_idx,
-                                         std::uint32_t* chunk) {
-  std::uint64_t lo = 0, hi = NB;  // last key with chunk_off <= w
-  while (hi - lo > 1) {
-    const std::uint64_t mid = (lo + hi) / 2;
-    if (chunk_off[mid] <= w) lo = mid; else hi = mid;
-  }
-  *key_idx = std::uint32_t(lo);
-  *chunk = std::uint32_t(w - chunk_off[lo]);
 }
 
 // ---- big segments: one fused kernel ---------------------------------------
@@ -601,6 +597,8 @@ __global__ void __launch_bounds__(kFuseThreads)
                      const unsigned long long* __restrict__ n_big,
                      const std::uint32_t* __restrict__ chunk_off,
                      const unsigned long long* __restrict__ n_items,
+                     const std::uint32_t* __restrict__ item_key,
+                     const std::uint32_t* __restrict__ item_chunk,
                      const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
                      const std::uint32_t* __restrict__ pos, const double* __restrict__ DX,
                      ChunkSum* __restrict__ chunk_tot, unsigned* __restrict__ flags,
@@ -622,12 +620,11 @@ __global__ void __launch_bounds__(kFuseThreads)
     __syncthreads();
     const std::uint64_t w = s_item;
     if (w >= W) break;
-    std::uint32_t ki, c;
-    big_item(chunk_off, NB, w, &ki, &c);
+    const std::uint32_t ki = item_key[w], c = item_chunk[w];
     const std::uint32_t u = big_list[ki];
     const std::uint32_t k0 = seg[u], k1 = seg[u + 1];
     const std::uint32_t nch = chunk_off[ki + 1] - chunk_off[ki];
-    const std::uint64_t w0 = chunk_off[ki];
+    const std::uint64_t w0 = w - c;  // the key's first item
     const std::uint32_t c0 = k0 + c * chunk, c1 = min(k1, c0 + std::uint32_t(chunk));
     const std::uint32_t a0 = c0 + s * kFusePer;
     const int cnt = worker && a0 < c1 ? int(min(c1 - a0, std::uint32_t(kFusePer))) : 0;
@@ -673,11 +670,23 @@ __global__ void __launch_bounds__(kFuseThreads)
       // offset: the key's earlier chunks' totals in chunk order, then this
       // chunk's earlier slices
       DD off{0.0, 0.0};
+      // every earlier chunk's total published (flags polled 4 at a time),
+      // one fence, then their totals with plain loads, added in chunk order
+      for (std::uint32_t g0 = 0; g0 < c; g0 += 4) {
+        bool ready;
+        do {
+          ready = true;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (g0 + q < c)
+              ready &= *reinterpret_cast<volatile const unsigned*>(&flags[w0 + g0 + q]) != 0u;
+          if (!ready) __nanosleep(32);
+        } while (!ready);
+      }
+      __threadfence();
+#pragma unroll 4
       for (std::uint32_t cc = 0; cc < c; ++cc) {
-        const std::uint64_t it = w0 + cc;
-        while (*reinterpret_cast<volatile const unsigned*>(&flags[it]) == 0u) __nanosleep(32);
-        __threadfence();
-        const double* bp = reinterpret_cast<const double*>(&chunk_tot[it * E + d]);
+        const double* bp = reinterpret_cast<const double*>(&chunk_tot[(w0 + cc) * E + d]);
         off = dd_add(off, DD{__ldcg(bp), __ldcg(bp + 1)});
       }
       for (int q = 0; q < s; ++q) off = dd_add(off, DD{sh[q * E + d], sl[q * E + d]});
@@ -709,6 +718,7 @@ __global__ void __launch_bounds__(kFuseThreads)
     if (int(threadIdx.x) < E) {
       DD S{0.0, 0.0};
       double A = 0.0, B = 0.0;
+#pragma unroll 4
       for (std::uint32_t cc = 0; cc < nch; ++cc) {
         const double* bp = reinterpret_cast<const double*>(&chunk_tot[(w0 + cc) * E + threadIdx.x]);
         S = dd_add(S, DD{__ldcg(bp), __ldcg(bp + 1)});

@@ -286,6 +286,7 @@ struct Tier {
                 *key_done = nullptr;
   ChunkSum* chunk_tot = nullptr;
   unsigned* fuse_flags = nullptr;          // big_fused_kernel: chunk total published
+  std::uint32_t *item_key = nullptr, *item_chunk = nullptr;  // item -> (big key, chunk)
   unsigned long long* fuse_ticket = nullptr;
   std::uint64_t fuse_items = 0;
   std::uint64_t* otot = nullptr;
@@ -1058,13 +1059,15 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   // (ticket order; flags and ticket reset per launch)
   const int chunk = fuse_chunk(E);
   launch(t, big_plan_kernel, 1, 1024, 0, chunk, (const std::uint32_t*)t->big_list,
-         (const unsigned long long*)nb, seg, t->chunk_off, &t->dsc->n_items);
+         (const unsigned long long*)nb, seg, t->chunk_off, &t->dsc->n_items, t->item_key,
+         t->item_chunk);
   HPS_CUDA(cudaMemsetAsync(t->fuse_flags, 0, t->fuse_items * 4, t->L->st));
   HPS_CUDA(cudaMemsetAsync(t->fuse_ticket, 0, 8, t->L->st));
   launch(t, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
          (const std::uint32_t*)t->big_list, (const unsigned long long*)nb,
-         (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items, seg,
-         exs, pos, DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, t->deltas,
+         (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
+         (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs, pos, DX,
+         t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, t->deltas,
          &t->dsc->fallbacks);
   return HPS_OK;
 }
@@ -2172,6 +2175,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   t->fuse_items = S / std::uint64_t(fuse_chunk(int(E))) + S / (kLongSeg + 1) + 2;
   A(chunk_tot, t->fuse_items * E);
   A(fuse_flags, t->fuse_items);
+  A(item_key, t->fuse_items);
+  A(item_chunk, t->fuse_items);
   A(fuse_ticket, 1);
   A(ukeys, S);
   if (G == 1) A(rows, S * E);  // G > 1: inside the exported window (peers write it)
