@@ -578,6 +578,14 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
   }
 }
 
+// Acquire load (gpu scope): later loads of this thread observe what the
+// releasing writer published before the flag.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ---- big segments: one fused kernel ---------------------------------------
 //
 // Work items (key, chunk) are taken in ticket order. A CTA loads its chunk's
@@ -662,10 +670,14 @@ __global__ void __launch_bounds__(kFuseThreads)
       cs.hi = ct.hi;
       cs.lo = ct.lo;
       cs.a = ca;
-      __threadfence();
     }
     __syncthreads();
-    if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned*>(&flags[w]) = 1u;
+    // one release after the barrier covers every writer of the block
+    // (cumulativity), instead of a fence per writer
+    if (threadIdx.x == 0) {
+      __threadfence();
+      *reinterpret_cast<volatile unsigned*>(&flags[w]) = 1u;
+    }
     if (worker) {
       // offset: the key's earlier chunks' totals in chunk order, then this
       // chunk's earlier slices
@@ -678,12 +690,10 @@ __global__ void __launch_bounds__(kFuseThreads)
           ready = true;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (g0 + q < c)
-              ready &= *reinterpret_cast<volatile const unsigned*>(&flags[w0 + g0 + q]) != 0u;
+            if (g0 + q < c) ready &= ld_acquire_u32(&flags[w0 + g0 + q]) != 0u;
           if (!ready) __nanosleep(32);
         } while (!ready);
       }
-      __threadfence();
 #pragma unroll 4
       for (std::uint32_t cc = 0; cc < c; ++cc) {
         const double* bp = reinterpret_cast<const double*>(&chunk_tot[(w0 + cc) * E + d]);
@@ -707,13 +717,16 @@ __global__ void __launch_bounds__(kFuseThreads)
       for (int q = 0; q < slices; ++q) cb = __dadd_ru(cb, sb[q * E + threadIdx.x]);
       chunk_tot[w * E + threadIdx.x].b = cb;
     }
-    // the key's last CTA certifies
-    __threadfence();
+    // the key's last CTA certifies (one release before the count, one
+    // acquire after it, each by one thread around the barriers)
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&key_done[ki], 1u) == nch - 1;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&key_done[ki], 1u) == nch - 1;
+      if (s_last) __threadfence();
+    }
     __syncthreads();
     if (!s_last) continue;
-    __threadfence();
     float g = 0.0f;
     if (int(threadIdx.x) < E) {
       DD S{0.0, 0.0};
