@@ -186,6 +186,20 @@ struct Lane {
   std::uint64_t status_words = 0;
 };
 
+// The temporaries of one grouping lane (mini-batches j = lane mod
+// kGroupLanes are grouped on it, beside the other lanes).
+constexpr int kGroupLanes = 4;
+struct GroupState {
+  std::uint32_t* gcnt = nullptr;       // [gslots] per-slot occurrence counters (kept zero)
+  std::uint32_t* slot_uid = nullptr;   // [gslots]
+  std::uint32_t* part_slot = nullptr;  // [kGroupParts][part_cap] claimed slots
+  std::uint32_t* part_n = nullptr;     // [kGroupParts * kGroupPartStride] claim counters
+  std::uint32_t* part_base = nullptr;  // [kGroupParts]
+  std::uint32_t *g_long = nullptr, *g_huge = nullptr, *g_dup = nullptr;  // segment lists
+  unsigned long long* gn = nullptr;    // [4] n_long, n_dup, n_huge
+  cudaEvent_t join = nullptr, ctx = nullptr;
+};
+
 // Per-batch results read back at hps_wait_batch (pinned).
 struct BatchOut {
   double loss;
@@ -210,9 +224,12 @@ struct Tier {
   cudaStream_t st = nullptr;            // == lane[0].st: bodies and the parity API
   cudaStream_t st2 = nullptr;           // side stream: dense-grad overlaps sparse reduce
   cudaEvent_t fork = nullptr, join = nullptr;
-  Lane lane[3];                         // 0: main (body), 1: prep (build of the next batch),
-                                        // 2: the next batch's mini-batch grouping
-  cudaEvent_t g_fork = nullptr, g_join = nullptr, g_ctx = nullptr;
+  Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
+                                        // 2..: the next batch's mini-batch groupings
+  GroupState gs[kGroupLanes];           // per grouping lane: its temporaries
+  int group_lanes = 1;                  // grouping lanes in use (HPS_GROUP_LANES; 1 is
+                                        // best on c2: more lanes contend with the body)
+  cudaEvent_t g_fork = nullptr;
   Lane* L = &lane[0];                   // the lane launch() enqueues on
   // The batch pipeline (the reference's 4-stage pipeline, pipeline.hpp:230-
   // 500, as streams): stage (H2D + counts, st_stage) -> prep (working set,
@@ -307,8 +324,6 @@ struct Tier {
   // stalls the memory pipeline of the SM issuing it for everyone on that SM
   unsigned pf_ctas = 8, wb_ctas = 4;
   bool hash_dedup = true;                // group.cuh at G == 1 (HPS_DEDUP=sort: radix sort)
-  std::uint32_t* gcnt = nullptr;         // [capmax] per-slot occurrence counters (kept zero)
-  std::uint32_t* slot_uid = nullptr;     // [capmax]
   // slot grouping outputs, per table (prep of b+1 writes while body b reads):
   // occurrence -> slot (batch key index), and per mini-batch region (at the
   // sum of the earlier mini-batches' shape bounds) segments, example ids,
@@ -324,10 +339,7 @@ struct Tier {
   std::uint64_t g_pool = 0;              // region pool size (elements)
   // prep-only temporaries of the grouping
   std::uint32_t *g_tick = nullptr, *g_segocc = nullptr, *g_exof = nullptr;
-  std::uint32_t *g_long = nullptr, *g_huge = nullptr, *g_dup = nullptr;
-  std::uint32_t* part_slot = nullptr;    // [kGroupParts][part_cap] claimed slots
-  std::uint32_t* part_n = nullptr;       // [kGroupParts * kGroupPartStride] claim counters
-  std::uint32_t* part_base = nullptr;    // [kGroupParts]
+
   std::uint64_t part_cap = 0;
   // HPS_TRACE=1: timed events at the pipeline's stage boundaries, printed
   // per batch to stderr at completion (diagnostics)
@@ -821,7 +833,7 @@ static void mark_stage(Tier* t, int phase) {
   t->L = &tmp;
   mark(t, phase);
   t->L = l;
-  t->ev_lane.back() = 3;
+  t->ev_lane.back() = 2 + kGroupLanes;
 }
 
 static void timing_begin(Tier* t) {
@@ -834,7 +846,8 @@ static void timing_begin(Tier* t) {
 // mark to the last.
 static void timing_end(Tier* t) {
   if (!t->timing || t->ev_phase.size() < 2) return;
-  int last[4] = {-1, -1, -1, -1};
+  int last[3 + kGroupLanes];
+  for (int& v : last) v = -1;
   for (std::size_t i = 0; i < t->ev_phase.size(); ++i) {
     const int ln = t->ev_lane[i], p = t->ev_phase[i];
     if (last[ln] >= 0 && p > 0 && p < HPS_TIMING_SLOTS) {
@@ -1184,14 +1197,15 @@ static std::uint64_t group_region(const BatchShape& sh, int j) {
 // Mini-batch dedup of every shard of the batch by slot grouping (group.cuh),
 // on the prep lane: it depends only on the keys, so batch b+1's grouping runs
 // beside batch b's body. Outputs go to the table's pools (g_*[tb]).
-static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPlan& bp) {
+static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPlan& bp,
+                                   GroupState& g, int lane) {
   const int G = T->G, J = T->J, tb = bp.tb;
   const std::uint64_t B = sh.B, GJ = std::uint64_t(G) * J;
   const std::int64_t* doff = T->b_off[bp.sp];
   const std::uint64_t* dkeys = T->b_keys[bp.sp];
   Lane& l = *T->L;
   const std::uint32_t pcap = std::uint32_t(T->part_cap);
-  for (int j = 0; j < J; ++j) {
+  for (int j = lane; j < J; j += T->group_lanes) {
     const std::uint64_t s = std::uint64_t(T->g) * J + j;
     const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
     const ShardMap sm{s, GJ, n};
@@ -1199,43 +1213,44 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     std::uint32_t* seg = T->g_segb[tb] + r0 + j;  // U+1 entries per region
     std::uint32_t* exs = T->g_exsb[tb] + r0;
     std::uint32_t* uids = T->g_uidb[tb] + r0;
+    std::uint32_t* segocc = T->g_segocc + r0;  // (positions are per mini-batch)
     unsigned long long* U = &T->dsc->Ug[tb][j];
     HPS_CUDA(cudaMemsetAsync(U, 0, 8, l.st));
-    HPS_CUDA(cudaMemsetAsync(T->dsc->gn, 0, sizeof(T->dsc->gn), l.st));
+    HPS_CUDA(cudaMemsetAsync(g.gn, 0, 4 * sizeof(unsigned long long), l.st));
     if (!n) continue;
     const std::uint64_t warps = ((n + 31) / 32) * kGroupPosGroups;
     // slot space: the batch table (G == 1: it holds every key) or the
     // rank's request table (G > 1)
     const std::uint64_t* gk = G == 1 ? T->tkeys[tb] : T->rq_keys[tb];
     const std::uint64_t* gc = G == 1 ? &T->dsc->cap[tb] : &T->dsc->rq_capv;
-    launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys, gk, gc, T->gcnt,
-           T->slot_uid, T->part_slot, pcap, T->part_n, T->g_occslot[tb], T->g_tick, T->g_exof,
+    launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys, gk, gc, g.gcnt,
+           g.slot_uid, g.part_slot, pcap, g.part_n, T->g_occslot[tb], T->g_tick, T->g_exof,
            &T->dsc->err);
-    launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)T->part_n,
-           (const std::uint32_t*)T->part_slot, pcap, T->part_base, uids, U);
+    launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)g.part_n,
+           (const std::uint32_t*)g.part_slot, pcap, g.part_base, uids, U);
     const Count Uc{reinterpret_cast<const std::uint64_t*>(U), 0};
-    tile_scan(T, UidCount{uids, T->gcnt}, SegEmit{seg, Uc}, Uc, ob, &l.d->total);
+    tile_scan(T, UidCount{uids, g.gcnt}, SegEmit{seg, Uc}, Uc, ob, &l.d->total);
     launch(T, group_place_kernel, grid_for(n * 32), 256, 0, sm, doff,
            (const std::uint32_t*)T->g_occslot[tb], (const std::uint32_t*)T->g_tick,
-           (const std::uint32_t*)T->slot_uid, pcap, (const std::uint32_t*)T->part_base,
-           (const std::uint32_t*)seg, T->g_segocc, G == 1 ? nullptr : T->g_inv[tb]);
+           (const std::uint32_t*)g.slot_uid, pcap, (const std::uint32_t*)g.part_base,
+           (const std::uint32_t*)seg, segocc, G == 1 ? nullptr : T->g_inv[tb]);
     launch(T, group_order_kernel, grid_for(ob), 256, 0, (const unsigned long long*)U,
-           (const std::uint32_t*)seg, T->g_segocc, (const std::uint32_t*)T->g_exof,
-           (const std::uint32_t*)uids, T->gcnt, exs, T->g_long, &T->dsc->gn[0], T->g_huge,
-           &T->dsc->gn[2], T->part_n);
+           (const std::uint32_t*)seg, segocc, (const std::uint32_t*)T->g_exof,
+           (const std::uint32_t*)uids, g.gcnt, exs, g.g_long, &g.gn[0], g.g_huge,
+           &g.gn[2], g.part_n);
     const std::uint32_t words = std::uint32_t((n + 31) / 32);
     const std::size_t wsmem = std::size_t(kGroupWarpThreads / 32) * 2 * words * 4;
     launch(T, group_warp_kernel, kSMs * 4, kGroupWarpThreads, wsmem,
-           (const unsigned long long*)&T->dsc->gn[0], (const std::uint32_t*)T->g_long,
-           (const std::uint32_t*)seg, (const std::uint32_t*)T->g_segocc,
-           (const std::uint32_t*)T->g_exof, words, exs, T->g_dup, &T->dsc->gn[1]);
+           (const unsigned long long*)&g.gn[0], (const std::uint32_t*)g.g_long,
+           (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
+           (const std::uint32_t*)T->g_exof, words, exs, g.g_dup, &g.gn[1]);
     launch(T, group_cta_kernel, kSMs, kGroupThreads, std::size_t(2) * words * 4,
-           (const unsigned long long*)&T->dsc->gn[2], (const std::uint32_t*)T->g_huge,
-           (const std::uint32_t*)seg, (const std::uint32_t*)T->g_segocc,
-           (const std::uint32_t*)T->g_exof, words, exs, T->g_dup, &T->dsc->gn[1]);
+           (const unsigned long long*)&g.gn[2], (const std::uint32_t*)g.g_huge,
+           (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
+           (const std::uint32_t*)T->g_exof, words, exs, g.g_dup, &g.gn[1]);
     launch(T, group_dup_kernel, kSMs, kGroupThreads, 0,
-           (const unsigned long long*)&T->dsc->gn[1], (const std::uint32_t*)T->g_dup,
-           (const std::uint32_t*)seg, (const std::uint32_t*)T->g_segocc,
+           (const unsigned long long*)&g.gn[1], (const std::uint32_t*)g.g_dup,
+           (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
            (const std::uint32_t*)T->g_exof, exs);
   }
   return HPS_OK;
@@ -1284,13 +1299,16 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
              (const std::uint64_t*)&T->dsc->rq_capv);
     }
     HPS_CUDA(cudaEventRecord(T->g_fork, l.st));
-    HPS_CUDA(cudaStreamWaitEvent(T->lane[2].st, T->g_fork, 0));
-    T->L = &T->lane[2];
-    const hps_status gs = enqueue_grouping(T, sh, bp);
-    if (gs == HPS_OK) mark(T, HPS_T_DEDUP);
-    T->L = &l;
-    HPS_TRY(gs);
-    HPS_CUDA(cudaEventRecord(T->g_join, T->lane[2].st));
+    for (int gl = 0; gl < T->group_lanes && gl < T->J; ++gl) {
+      Lane& ln = T->lane[2 + gl];
+      HPS_CUDA(cudaStreamWaitEvent(ln.st, T->g_fork, 0));
+      T->L = &ln;
+      const hps_status st = enqueue_grouping(T, sh, bp, T->gs[gl], gl);
+      if (st == HPS_OK && gl == 0) mark(T, HPS_T_DEDUP);
+      T->L = &l;
+      HPS_TRY(st);
+      HPS_CUDA(cudaEventRecord(T->gs[gl].join, ln.st));
+    }
   }
   // the distinct keys with their slots, ascending: compact the live slots,
   // sort them (n_ws items, ~3x fewer than the occurrences)
@@ -1328,7 +1346,9 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
     HPS_CUDA(cudaEventRecordWithFlags(
         T->pf_fork, l.st, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
   }
-  if (bp.grouped) HPS_CUDA(cudaStreamWaitEvent(l.st, T->g_join, 0));
+  if (bp.grouped)
+    for (int gl = 0; gl < T->group_lanes && gl < T->J; ++gl)
+      HPS_CUDA(cudaStreamWaitEvent(l.st, T->gs[gl].join, 0));
   mark(T, HPS_T_BUILD);
   return HPS_OK;
 }
@@ -1800,11 +1820,14 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     if (T->trace) cudaEventRecord(T->tr[sp][2], ps);
     if (bp.grouped) {  // lane 2's look-back context: after the previous prep (whose
       // graph ran lane 2's last grouping), before this one
-      HPS_CUDA(cudaStreamWaitEvent(T->lane[2].st, T->ev_prep, 0));
-      T->L = &T->lane[2];
-      open_lookback_context(T);
-      HPS_CUDA(cudaEventRecord(T->g_ctx, T->lane[2].st));
-      HPS_CUDA(cudaStreamWaitEvent(ps, T->g_ctx, 0));
+      for (int gl = 0; gl < T->group_lanes && gl < J; ++gl) {
+        Lane& ln = T->lane[2 + gl];
+        HPS_CUDA(cudaStreamWaitEvent(ln.st, T->ev_prep, 0));
+        T->L = &ln;
+        open_lookback_context(T);
+        HPS_CUDA(cudaEventRecord(T->gs[gl].ctx, ln.st));
+        HPS_CUDA(cudaStreamWaitEvent(ps, T->gs[gl].ctx, 0));
+      }
     }
     T->L = &T->lane[1];
     open_lookback_context(T);
@@ -1971,6 +1994,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_TRACE")) t->trace = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_DEDUP")) t->hash_dedup = std::strcmp(v, "sort") != 0;
   if (const char* v = std::getenv("HPS_GRAPHS")) t->use_graphs = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_GROUP_LANES"))
+    t->group_lanes = std::min(kGroupLanes, std::max(1, std::atoi(v)));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
@@ -2029,7 +2054,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     str(&t->st, hi);
     str(&t->st2, hi);
     str(&t->lane[1].st, lo);
-    str(&t->lane[2].st, lo);
+    for (int gl = 0; gl < kGroupLanes; ++gl) str(&t->lane[2 + gl].st, lo);
     str(&t->st_stage, lo);
     str(&t->st_wb, lo);
     str(&t->st_pf, lo);
@@ -2039,8 +2064,10 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     ev(&t->ev_prep, false);
     ev(&t->pf_fork, false);
     ev(&t->g_fork, false);
-    ev(&t->g_join, false);
-    ev(&t->g_ctx, false);
+    for (GroupState& g : t->gs) {
+      ev(&g.join, false);
+      ev(&g.ctx, false);
+    }
     ev(&t->pf_join, false);
     for (int i = 0; i < kTables; ++i) {
       ev(&t->ev_body_tab[i], false);
@@ -2109,8 +2136,11 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   t->rq_cap = 1;
   while (t->rq_cap < 2 * std::max(O, W)) t->rq_cap <<= 1;
   t->gslots = G > 1 ? std::max(t->capmax, t->rq_cap) : t->capmax;
-  A(gcnt, t->gslots);
-  A(slot_uid, t->gslots);
+  for (GroupState& g : t->gs) {
+    if ((s = dalloc(t, &g.gcnt, t->gslots)) != HPS_OK ||
+        (s = dalloc(t, &g.slot_uid, t->gslots)) != HPS_OK)
+      return fail(s);
+  }
   t->ws = t->wsb[0];
   t->ws_idx = t->wsib[0];
   t->wsset_cap = 1;
@@ -2119,11 +2149,14 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   const std::uint64_t S = std::max(O, W);
   const std::uint64_t status_words =
       std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1;
-  for (Lane& l : t->lane) {
-    if ((s = dalloc(t, &l.kA, S)) != HPS_OK || (s = dalloc(t, &l.kB, S)) != HPS_OK ||
-        (s = dalloc(t, &l.vA, S)) != HPS_OK || (s = dalloc(t, &l.vB, S)) != HPS_OK ||
-        (s = dalloc(t, &l.ghist, std::uint64_t(kMaxPasses) * kDigits)) != HPS_OK ||
-        (s = dalloc(t, &l.status, status_words)) != HPS_OK ||
+  for (int li = 0; li < 2 + kGroupLanes; ++li) {
+    Lane& l = t->lane[li];
+    if (li < 2 &&  // the grouping lanes only scan: no radix scratch
+        ((s = dalloc(t, &l.kA, S)) != HPS_OK || (s = dalloc(t, &l.kB, S)) != HPS_OK ||
+         (s = dalloc(t, &l.vA, S)) != HPS_OK || (s = dalloc(t, &l.vB, S)) != HPS_OK ||
+         (s = dalloc(t, &l.ghist, std::uint64_t(kMaxPasses) * kDigits)) != HPS_OK))
+      return fail(s);
+    if ((s = dalloc(t, &l.status, status_words)) != HPS_OK ||
         (s = dalloc(t, &l.ticket, 1)) != HPS_OK || (s = dalloc(t, &l.d, 1)) != HPS_OK)
       return fail(s);
     l.status_words = status_words;
@@ -2157,15 +2190,20 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     A(g_uidb[i], t->g_pool);
   }
   A(g_tick, S);
-  A(g_segocc, S);
+  A(g_segocc, t->g_pool);
   A(g_exof, S);
-  A(g_long, S);
-  A(g_huge, S);
-  A(g_dup, S);
+  for (GroupState& g : t->gs) {
+    if ((s = dalloc(t, &g.g_long, S)) != HPS_OK || (s = dalloc(t, &g.g_huge, S)) != HPS_OK ||
+        (s = dalloc(t, &g.g_dup, S)) != HPS_OK || (s = dalloc(t, &g.gn, 4)) != HPS_OK)
+      return fail(s);
+  }
   t->part_cap = S;  // a partition can never overflow
-  A(part_slot, std::uint64_t(kGroupParts) * S);
-  A(part_n, std::uint64_t(kGroupParts) * kGroupPartStride);
-  A(part_base, kGroupParts);
+  for (GroupState& g : t->gs) {
+    if ((s = dalloc(t, &g.part_slot, std::uint64_t(kGroupParts) * S)) != HPS_OK ||
+        (s = dalloc(t, &g.part_n, std::uint64_t(kGroupParts) * kGroupPartStride)) != HPS_OK ||
+        (s = dalloc(t, &g.part_base, kGroupParts)) != HPS_OK)
+      return fail(s);
+  }
   A(otot, kMaxRanks);
   A(long_list, S);
   A(big_list, S / (kLongSeg + 1) + 2);
@@ -2190,8 +2228,10 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
 #undef A
-  cudaMemsetAsync(t->gcnt, 0, t->gslots * 4, t->st);
-  cudaMemsetAsync(t->part_n, 0, std::uint64_t(kGroupParts) * kGroupPartStride * 4, t->st);
+  for (GroupState& g : t->gs) {
+    cudaMemsetAsync(g.gcnt, 0, t->gslots * 4, t->st);
+    cudaMemsetAsync(g.part_n, 0, std::uint64_t(kGroupParts) * kGroupPartStride * 4, t->st);
+  }
   cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
   cudaMemsetAsync(t->key_done, 0, (S / (kLongSeg + 1) + 2) * 4, t->st);
   if ((e = cudaMemsetAsync(t->dsc, 0, sizeof(Scalars), t->st)) != cudaSuccess)
@@ -2223,9 +2263,10 @@ hps_status hps_destroy(hps_tier_t t) {
   if (!t) return HPS_OK;
   cudaSetDevice(t->cfg.cuda_device);
   if (t->dsc) quiesce(t);  // in-flight batches, then every resident row to the store
-  for (cudaStream_t x : {t->st, t->lane[1].st, t->lane[2].st, t->st_stage, t->st_wb, t->st2,
-                         t->st_pf})
+  for (cudaStream_t x : {t->st, t->lane[1].st, t->st_stage, t->st_wb, t->st2, t->st_pf})
     if (x) cudaStreamSynchronize(x);
+  for (int gl = 0; gl < kGroupLanes; ++gl)
+    if (t->lane[2 + gl].st) cudaStreamSynchronize(t->lane[2 + gl].st);
   if (t->comm) nccl().CommDestroy(t->comm);
   for (auto& c : t->pending) {
     cudaFree(c.keys);
@@ -2248,11 +2289,15 @@ hps_status hps_destroy(hps_tier_t t) {
     if (x) cudaEventDestroy(x);
   for (cudaEvent_t x : t->ev_carry_sp)
     if (x) cudaEventDestroy(x);
-  for (cudaEvent_t x : {t->ev_staged, t->ev_prep, t->pf_fork, t->pf_join, t->g_fork, t->g_join,
-                        t->g_ctx})
+  for (cudaEvent_t x : {t->ev_staged, t->ev_prep, t->pf_fork, t->pf_join, t->g_fork})
     if (x) cudaEventDestroy(x);
-  for (cudaStream_t x : {t->lane[1].st, t->lane[2].st, t->st_stage, t->st_wb, t->st_pf})
+  for (GroupState& g : t->gs)
+    for (cudaEvent_t x : {g.join, g.ctx})
+      if (x) cudaEventDestroy(x);
+  for (cudaStream_t x : {t->lane[1].st, t->st_stage, t->st_wb, t->st_pf})
     if (x) cudaStreamDestroy(x);
+  for (int gl = 0; gl < kGroupLanes; ++gl)
+    if (t->lane[2 + gl].st) cudaStreamDestroy(t->lane[2 + gl].st);
   if (t->st2) cudaStreamDestroy(t->st2);
   if (t->st) cudaStreamDestroy(t->st);
   delete t;
