@@ -274,24 +274,32 @@ __global__ void __launch_bounds__(kSortThreads)
     if (tile == 0 && total) *total = 0;
     return;
   }
-  // blocked arrangement: thread t owns items base + t*16 .. +15
-  const std::uint64_t tb = base + std::uint64_t(threadIdx.x) * kScanItems;
+  // warp-striped arrangement: warp w owns items base + w*512 .. +511, and in
+  // round it its lane handles item + it*32 + lane (coalesced loads; the
+  // emits see exactly the same exclusive prefixes as a blocked walk)
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const std::uint64_t wb = base + std::uint64_t(warp) * (32 * kScanItems);
   std::uint32_t vals[kScanItems];
-  std::uint32_t s = 0;
 #pragma unroll
   for (int it = 0; it < kScanItems; ++it) {
-    const std::uint64_t idx = tb + it;
+    const std::uint64_t idx = wb + it * 32 + lane;
     vals[it] = idx < n ? f(idx) : 0u;
-    s += vals[it];
   }
-  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  std::uint32_t x = s;
+  // per round: inclusive scan across the lanes; rounds chain in order
+  std::uint32_t incl[kScanItems];
+  std::uint32_t wtot = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-    if (lane >= unsigned(o)) x += y;
+  for (int it = 0; it < kScanItems; ++it) {
+    std::uint32_t x = vals[it];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= unsigned(o)) x += y;
+    }
+    incl[it] = wtot + x;  // within the warp's 512 items
+    wtot += __shfl_sync(0xFFFFFFFFu, x, 31);
   }
-  if (lane == 31) ws[warp] = x;
+  if (lane == 0) ws[warp] = wtot;
   __syncthreads();
   if (threadIdx.x == 0) {
     std::uint32_t agg = 0;
@@ -312,12 +320,11 @@ __global__ void __launch_bounds__(kSortThreads)
   __syncthreads();
   std::uint32_t wpre = 0;
   for (unsigned w = 0; w < warp; ++w) wpre += ws[w];
-  std::uint64_t run = s_pre + wpre + (x - s);
+  const std::uint64_t run = s_pre + wpre;
 #pragma unroll
   for (int it = 0; it < kScanItems; ++it) {
-    const std::uint64_t idx = tb + it;
-    if (idx < n) em(idx, vals[it], run);
-    run += vals[it];
+    const std::uint64_t idx = wb + it * 32 + lane;
+    if (idx < n) em(idx, vals[it], run + incl[it] - vals[it]);
   }
 }
 
