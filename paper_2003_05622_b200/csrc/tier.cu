@@ -154,7 +154,8 @@ struct BatchPlan {
   std::int64_t step = 0;
   std::uint64_t occ_total = 0;
   int skip_mb = -1;
-  bool grouped = false;  // G == 1 slot grouping, done by the prep lane
+  bool grouped = false;  // slot grouping (prep lane, and the body's side branch)
+  int prep_mbs = 0;      // mini-batches grouped by the prep
 };
 
 struct GraphEntry {
@@ -186,9 +187,9 @@ struct Lane {
   std::uint64_t status_words = 0;
 };
 
-// The temporaries of one grouping lane (mini-batches j = lane mod
-// kGroupLanes are grouped on it, beside the other lanes).
-constexpr int kGroupLanes = 4;
+// The temporaries of one grouping context: the prep's (lane 2) and the
+// body's (lane 3).
+constexpr int kGroupLanes = 2;
 struct GroupState {
   std::uint32_t* gcnt = nullptr;       // [gslots] per-slot occurrence counters (kept zero)
   std::uint32_t* slot_uid = nullptr;   // [gslots]
@@ -226,9 +227,12 @@ struct Tier {
   cudaEvent_t fork = nullptr, join = nullptr;
   Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
                                         // 2..: the next batch's mini-batch groupings
-  GroupState gs[kGroupLanes];           // per grouping lane: its temporaries
-  int group_lanes = 1;                  // grouping lanes in use (HPS_GROUP_LANES; 1 is
-                                        // best on c2: more lanes contend with the body)
+  GroupState gs[kGroupLanes];           // [0]: the prep's grouping, [1]: the body's
+  int prep_mbs = 0;                     // mini-batches the prep groups (HPS_PREP_GROUP;
+                                        // 0 = auto); the body groups the rest, each
+                                        // beside the previous mini-batch's compute
+  cudaEvent_t gmb_done[64] = {};        // body grouping: mini-batch j ready
+  cudaEvent_t b_fork = nullptr;
   cudaEvent_t g_fork = nullptr;
   Lane* L = &lane[0];                   // the lane launch() enqueues on
   // The batch pipeline (the reference's 4-stage pipeline, pipeline.hpp:230-
@@ -338,7 +342,11 @@ struct Tier {
   std::uint32_t* g_uidb[kTables] = {};
   std::uint64_t g_pool = 0;              // region pool size (elements)
   // prep-only temporaries of the grouping
-  std::uint32_t *g_tick = nullptr, *g_segocc = nullptr, *g_exof = nullptr;
+  // occurrence-indexed temporaries, per table: a prep groups batch b+1 while
+  // the body of batch b groups its own later mini-batches
+  std::uint32_t* g_tick[kTables] = {};
+  std::uint32_t* g_segocc[kTables] = {};
+  std::uint32_t* g_exof[kTables] = {};
 
   std::uint64_t part_cap = 0;
   // HPS_TRACE=1: timed events at the pipeline's stage boundaries, printed
@@ -1198,14 +1206,15 @@ static std::uint64_t group_region(const BatchShape& sh, int j) {
 // on the prep lane: it depends only on the keys, so batch b+1's grouping runs
 // beside batch b's body. Outputs go to the table's pools (g_*[tb]).
 static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPlan& bp,
-                                   GroupState& g, int lane) {
+                                   GroupState& g, int j0, int j1,
+                                   const cudaEvent_t* mb_done = nullptr) {
   const int G = T->G, J = T->J, tb = bp.tb;
   const std::uint64_t B = sh.B, GJ = std::uint64_t(G) * J;
   const std::int64_t* doff = T->b_off[bp.sp];
   const std::uint64_t* dkeys = T->b_keys[bp.sp];
   Lane& l = *T->L;
   const std::uint32_t pcap = std::uint32_t(T->part_cap);
-  for (int j = lane; j < J; j += T->group_lanes) {
+  for (int j = j0; j < j1 && j < J; ++j) {
     const std::uint64_t s = std::uint64_t(T->g) * J + j;
     const std::uint64_t n = s < B ? (B - s - 1) / GJ + 1 : 0;
     const ShardMap sm{s, GJ, n};
@@ -1213,29 +1222,32 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     std::uint32_t* seg = T->g_segb[tb] + r0 + j;  // U+1 entries per region
     std::uint32_t* exs = T->g_exsb[tb] + r0;
     std::uint32_t* uids = T->g_uidb[tb] + r0;
-    std::uint32_t* segocc = T->g_segocc + r0;  // (positions are per mini-batch)
+    std::uint32_t* segocc = T->g_segocc[tb] + r0;  // (positions are per mini-batch)
     unsigned long long* U = &T->dsc->Ug[tb][j];
     HPS_CUDA(cudaMemsetAsync(U, 0, 8, l.st));
     HPS_CUDA(cudaMemsetAsync(g.gn, 0, 4 * sizeof(unsigned long long), l.st));
-    if (!n) continue;
+    if (!n) {
+      if (mb_done) HPS_CUDA(cudaEventRecord(mb_done[j], l.st));
+      continue;
+    }
     const std::uint64_t warps = ((n + 31) / 32) * kGroupPosGroups;
     // slot space: the batch table (G == 1: it holds every key) or the
     // rank's request table (G > 1)
     const std::uint64_t* gk = G == 1 ? T->tkeys[tb] : T->rq_keys[tb];
     const std::uint64_t* gc = G == 1 ? &T->dsc->cap[tb] : &T->dsc->rq_capv;
     launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys, gk, gc, g.gcnt,
-           g.slot_uid, g.part_slot, pcap, g.part_n, T->g_occslot[tb], T->g_tick, T->g_exof,
+           g.slot_uid, g.part_slot, pcap, g.part_n, T->g_occslot[tb], T->g_tick[tb], T->g_exof[tb],
            &T->dsc->err);
     launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)g.part_n,
            (const std::uint32_t*)g.part_slot, pcap, g.part_base, uids, U);
     const Count Uc{reinterpret_cast<const std::uint64_t*>(U), 0};
     tile_scan(T, UidCount{uids, g.gcnt}, SegEmit{seg, Uc}, Uc, ob, &l.d->total);
     launch(T, group_place_kernel, grid_for(n * 32), 256, 0, sm, doff,
-           (const std::uint32_t*)T->g_occslot[tb], (const std::uint32_t*)T->g_tick,
+           (const std::uint32_t*)T->g_occslot[tb], (const std::uint32_t*)T->g_tick[tb],
            (const std::uint32_t*)g.slot_uid, pcap, (const std::uint32_t*)g.part_base,
            (const std::uint32_t*)seg, segocc, G == 1 ? nullptr : T->g_inv[tb]);
     launch(T, group_order_kernel, grid_for(ob), 256, 0, (const unsigned long long*)U,
-           (const std::uint32_t*)seg, segocc, (const std::uint32_t*)T->g_exof,
+           (const std::uint32_t*)seg, segocc, (const std::uint32_t*)T->g_exof[tb],
            (const std::uint32_t*)uids, g.gcnt, exs, g.g_long, &g.gn[0], g.g_huge,
            &g.gn[2], g.part_n);
     const std::uint32_t words = std::uint32_t((n + 31) / 32);
@@ -1243,15 +1255,16 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     launch(T, group_warp_kernel, kSMs * 4, kGroupWarpThreads, wsmem,
            (const unsigned long long*)&g.gn[0], (const std::uint32_t*)g.g_long,
            (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
-           (const std::uint32_t*)T->g_exof, words, exs, g.g_dup, &g.gn[1]);
+           (const std::uint32_t*)T->g_exof[tb], words, exs, g.g_dup, &g.gn[1]);
     launch(T, group_cta_kernel, kSMs, kGroupThreads, std::size_t(2) * words * 4,
            (const unsigned long long*)&g.gn[2], (const std::uint32_t*)g.g_huge,
            (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
-           (const std::uint32_t*)T->g_exof, words, exs, g.g_dup, &g.gn[1]);
+           (const std::uint32_t*)T->g_exof[tb], words, exs, g.g_dup, &g.gn[1]);
     launch(T, group_dup_kernel, kSMs, kGroupThreads, 0,
            (const unsigned long long*)&g.gn[1], (const std::uint32_t*)g.g_dup,
            (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
-           (const std::uint32_t*)T->g_exof, exs);
+           (const std::uint32_t*)T->g_exof[tb], exs);
+    if (mb_done) HPS_CUDA(cudaEventRecord(mb_done[j], l.st));
   }
   return HPS_OK;
 }
@@ -1299,16 +1312,14 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
              (const std::uint64_t*)&T->dsc->rq_capv);
     }
     HPS_CUDA(cudaEventRecord(T->g_fork, l.st));
-    for (int gl = 0; gl < T->group_lanes && gl < T->J; ++gl) {
-      Lane& ln = T->lane[2 + gl];
-      HPS_CUDA(cudaStreamWaitEvent(ln.st, T->g_fork, 0));
-      T->L = &ln;
-      const hps_status st = enqueue_grouping(T, sh, bp, T->gs[gl], gl);
-      if (st == HPS_OK && gl == 0) mark(T, HPS_T_DEDUP);
-      T->L = &l;
-      HPS_TRY(st);
-      HPS_CUDA(cudaEventRecord(T->gs[gl].join, ln.st));
-    }
+    Lane& ln = T->lane[2];
+    HPS_CUDA(cudaStreamWaitEvent(ln.st, T->g_fork, 0));
+    T->L = &ln;
+    const hps_status st = enqueue_grouping(T, sh, bp, T->gs[0], 0, bp.prep_mbs);
+    if (st == HPS_OK) mark(T, HPS_T_DEDUP);
+    T->L = &l;
+    HPS_TRY(st);
+    HPS_CUDA(cudaEventRecord(T->gs[0].join, ln.st));
   }
   // the distinct keys with their slots, ascending: compact the live slots,
   // sort them (n_ws items, ~3x fewer than the occurrences)
@@ -1346,9 +1357,7 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
     HPS_CUDA(cudaEventRecordWithFlags(
         T->pf_fork, l.st, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
   }
-  if (bp.grouped)
-    for (int gl = 0; gl < T->group_lanes && gl < T->J; ++gl)
-      HPS_CUDA(cudaStreamWaitEvent(l.st, T->gs[gl].join, 0));
+  if (bp.grouped) HPS_CUDA(cudaStreamWaitEvent(l.st, T->gs[0].join, 0));
   mark(T, HPS_T_BUILD);
   return HPS_OK;
 }
@@ -1397,6 +1406,17 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
            (const float*)T->tvals[bp.tp], (const float*)(bp.tq >= 0 ? T->tvals[bp.tq] : nullptr),
            (const float*)(bp.tq2 >= 0 ? T->tvals[bp.tq2] : nullptr), T->tvals[bp.tb], E);
   }
+  // the mini-batches the prep did not group: grouped here on a side branch
+  // (lane 3), each ready before its mini-batch and beside the previous one
+  const bool side = bp.grouped && bp.prep_mbs < J;
+  if (side) {
+    HPS_CUDA(cudaEventRecord(T->b_fork, T->st));
+    HPS_CUDA(cudaStreamWaitEvent(T->lane[3].st, T->b_fork, 0));
+    T->L = &T->lane[3];
+    const hps_status gst = enqueue_grouping(T, sh, bp, T->gs[1], bp.prep_mbs, J, T->gmb_done);
+    T->L = &T->lane[0];
+    HPS_TRY(gst);
+  }
   {  // the proxies may be recycled from here on (see submit_batch)
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(T->st, &cs);
@@ -1418,6 +1438,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     const std::uint32_t* occ_row = T->inv;  // occurrence -> row of `rows`
     const float* rows = T->rows;
     const std::int64_t* goff = nullptr;      // occurrence ids: shard-local (sort path)
+    if (side && j >= bp.prep_mbs) HPS_CUDA(cudaStreamWaitEvent(T->st, T->gmb_done[j], 0));
     const std::uint64_t* Uj = &T->dsc->U;      // this mini-batch's unique keys
     const std::uint32_t* segj = T->seg;
     const std::uint32_t* exsj = T->exs;
@@ -1804,6 +1825,12 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     const std::size_t words = std::size_t((nmax + 31) / 32);
     bp.grouped = T->hash_dedup &&
                  std::size_t(kGroupWarpThreads / 32) * 8 * words <= kGroupSmemMax;
+    // who groups what: with a host store the prep is short next to the PCIe
+    // traffic and takes every mini-batch; with an HBM store the body takes
+    // the later half beside its compute (c2: 0.80 vs 0.85 ms/step; with a host
+    // store 1.36 vs 1.49)
+    bp.prep_mbs = T->prep_mbs > 0 ? std::min(T->prep_mbs, J)
+                                  : (T->store_on_host ? J : std::max(1, J / 2));
   }
   // ---- prep on lane 1, beside the previous body
   {
@@ -1820,14 +1847,12 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     if (T->trace) cudaEventRecord(T->tr[sp][2], ps);
     if (bp.grouped) {  // lane 2's look-back context: after the previous prep (whose
       // graph ran lane 2's last grouping), before this one
-      for (int gl = 0; gl < T->group_lanes && gl < J; ++gl) {
-        Lane& ln = T->lane[2 + gl];
-        HPS_CUDA(cudaStreamWaitEvent(ln.st, T->ev_prep, 0));
-        T->L = &ln;
-        open_lookback_context(T);
-        HPS_CUDA(cudaEventRecord(T->gs[gl].ctx, ln.st));
-        HPS_CUDA(cudaStreamWaitEvent(ps, T->gs[gl].ctx, 0));
-      }
+      Lane& ln = T->lane[2];
+      HPS_CUDA(cudaStreamWaitEvent(ln.st, T->ev_prep, 0));
+      T->L = &ln;
+      open_lookback_context(T);
+      HPS_CUDA(cudaEventRecord(T->gs[0].ctx, ln.st));
+      HPS_CUDA(cudaStreamWaitEvent(ps, T->gs[0].ctx, 0));
     }
     T->L = &T->lane[1];
     open_lookback_context(T);
@@ -1836,7 +1861,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
       const std::vector<std::uint64_t> key = {
           1, B, sh.own_bound, sh.batch_bound, std::uint64_t(bp.tb), std::uint64_t(bp.tp + 1),
           std::uint64_t(bp.tq + 1), std::uint64_t(bp.tq2 + 1), std::uint64_t(sp),
-          reinterpret_cast<std::uint64_t>(T->store),
+          std::uint64_t(bp.prep_mbs), reinterpret_cast<std::uint64_t>(T->store),
           T->store_keys, std::uint64_t(T->store_on_host), std::uint64_t(T->timing)};
       st = run_graph(T, key, [&] { return enqueue_prep(T, sh, bp); });
     } else {
@@ -1858,6 +1883,17 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   // ---- body on lane 0 (after its prep and its store rows)
   HPS_CUDA(cudaStreamWaitEvent(T->st, T->ev_prep, 0));
   if (T->store) HPS_CUDA(cudaStreamWaitEvent(T->st, T->pf_join, 0));
+  if (bp.grouped && bp.prep_mbs < J) {  // lane 3's look-back context (the body's
+    // grouping branch): after the previous body, before this one
+    Lane& l3 = T->lane[3];
+    if (bp.id >= 1)
+      HPS_CUDA(cudaStreamWaitEvent(l3.st, T->ev_body_sp[(bp.id - 1) % kSlots], 0));
+    T->L = &l3;
+    open_lookback_context(T);
+    T->L = &T->lane[0];
+    HPS_CUDA(cudaEventRecord(T->gs[1].ctx, l3.st));
+    HPS_CUDA(cudaStreamWaitEvent(T->st, T->gs[1].ctx, 0));
+  }
   if (T->trace) cudaEventRecord(T->tr[sp][4], T->st);
   open_lookback_context(T);
   T->prev2 = T->prev;
@@ -1870,7 +1906,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     std::vector<std::uint64_t> key = {2, B, sh.own_bound, std::uint64_t(bp.tb),
                                       std::uint64_t(bp.tp + 1), std::uint64_t(bp.tq + 1),
                                       std::uint64_t(bp.tq2 + 1), std::uint64_t(sp),
-                                      std::uint64_t(T->timing)};
+                                      std::uint64_t(bp.prep_mbs), std::uint64_t(T->timing)};
     for (int j = 0; j < J; ++j) key.push_back(sh.mb_bound[j]);
     HPS_TRY(run_graph(T, key, [&] { return enqueue_body(T, sh, bp); }));
   } else {
@@ -1994,8 +2030,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_TRACE")) t->trace = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_DEDUP")) t->hash_dedup = std::strcmp(v, "sort") != 0;
   if (const char* v = std::getenv("HPS_GRAPHS")) t->use_graphs = std::atoi(v) != 0;
-  if (const char* v = std::getenv("HPS_GROUP_LANES"))
-    t->group_lanes = std::min(kGroupLanes, std::max(1, std::atoi(v)));
+  if (const char* v = std::getenv("HPS_PREP_GROUP"))
+    t->prep_mbs = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
@@ -2064,6 +2100,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     ev(&t->ev_prep, false);
     ev(&t->pf_fork, false);
     ev(&t->g_fork, false);
+    ev(&t->b_fork, false);
+    for (auto& x : t->gmb_done) ev(&x, false);
     for (GroupState& g : t->gs) {
       ev(&g.join, false);
       ev(&g.ctx, false);
@@ -2189,9 +2227,11 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     A(g_exsb[i], t->g_pool);
     A(g_uidb[i], t->g_pool);
   }
-  A(g_tick, S);
-  A(g_segocc, t->g_pool);
-  A(g_exof, S);
+  for (int i = 0; i < kTables; ++i) {
+    A(g_tick[i], S);
+    A(g_segocc[i], t->g_pool);
+    A(g_exof[i], S);
+  }
   for (GroupState& g : t->gs) {
     if ((s = dalloc(t, &g.g_long, S)) != HPS_OK || (s = dalloc(t, &g.g_huge, S)) != HPS_OK ||
         (s = dalloc(t, &g.g_dup, S)) != HPS_OK || (s = dalloc(t, &g.gn, 4)) != HPS_OK)
@@ -2289,7 +2329,9 @@ hps_status hps_destroy(hps_tier_t t) {
     if (x) cudaEventDestroy(x);
   for (cudaEvent_t x : t->ev_carry_sp)
     if (x) cudaEventDestroy(x);
-  for (cudaEvent_t x : {t->ev_staged, t->ev_prep, t->pf_fork, t->pf_join, t->g_fork})
+  for (cudaEvent_t x : {t->ev_staged, t->ev_prep, t->pf_fork, t->pf_join, t->g_fork, t->b_fork})
+    if (x) cudaEventDestroy(x);
+  for (cudaEvent_t x : t->gmb_done)
     if (x) cudaEventDestroy(x);
   for (GroupState& g : t->gs)
     for (cudaEvent_t x : {g.join, g.ctx})
