@@ -32,13 +32,17 @@ def new_tier(world, rank, **kw):
 
 
 def case_train(world, rank, oracle, E, layers, J, zipf, dims, B, nb, nnz, det=True,
-               pipelined=False):
+               pipelined=False, hbm_store=False):
     off, keys, lab = pkg.gen_dataset(dims, B * nb + 3, nnz, zipf=zipf, seed=7)
     max_keys = int(max(off[min((b + 1) * B, len(off) - 1)] - off[b * B] for b in range(nb + 1)))
     tier = new_tier(world, rank, width=E, layer_dims=layers, minibatches=J, key_space=dims,
                     deterministic=det, max_batch_examples=B, max_batch_keys=max_keys)
-    store = np.zeros((dims, E), dtype=np.float32)
-    tier.attach_store(store)
+    if hbm_store:  # HBM value store: the body groups its later mini-batches
+        dstore = torch.zeros((dims, E), dtype=torch.float32, device="cuda")
+        tier.attach_store(dstore.data_ptr(), on_device=True, num_keys=dims)
+    else:
+        store = np.zeros((dims, E), dtype=np.float32)
+        tier.attach_store(store)
     n = len(off) - 1
     nbat = (n + B - 1) // B
     for b in range(nbat):
@@ -53,6 +57,9 @@ def case_train(world, rank, oracle, E, layers, J, zipf, dims, B, nb, nnz, det=Tr
         tier.wait_batch()
     dense = tier.get_dense()
     tier.close()
+    if hbm_store:
+        torch.cuda.synchronize()
+        store = dstore.cpu().numpy()
     wd, wk, wr = oracle.train_reference(make_cfg(1, world, E, layers, J=J), B, off, keys, lab)
     ok = True
     if det:
@@ -172,6 +179,8 @@ def main():
                                           1024, 9, 30)
     results["train_pipelined"] = case_train(world, rank, oracle, 16, (8, 16, 1), 4, True, 50000,
                                             1024, 9, 30, pipelined=True)
+    results["train_hbm_store"] = case_train(world, rank, oracle, 8, (8, 16, 1), 4, True, 30000,
+                                            1024, 7, 24, pipelined=True, hbm_store=True)
     flags = torch.tensor([int(v) for v in results.values()], device="cuda")
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:

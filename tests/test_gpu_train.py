@@ -261,3 +261,33 @@ def test_sort_dedup_path_bit_exact(pkg, oracle, monkeypatch):
     dims, B, nnz = 30000, 512, 20
     off, keys, lab = pkg.gen_dataset(dims, B * 3, nnz, zipf=True, seed=5)
     check_bit_exact(oracle, pkg, off, keys, lab, B, E=16, layers=(8, 16, 1), J=4, dims=dims)
+
+
+@pytest.mark.parametrize("J,prep_group", [(1, None), (3, None), (5, None), (4, "1"), (4, "3")])
+def test_hbm_store_grouping_split_bit_exact(pkg, oracle, monkeypatch, J, prep_group):
+    """With an HBM value store the body groups its later mini-batches on a side
+    branch while the prep groups the first ones (HPS_PREP_GROUP moves the
+    split): every split must stay bit-exact, including odd J."""
+    import torch
+    if prep_group is not None:
+        monkeypatch.setenv("HPS_PREP_GROUP", prep_group)
+    dims, B, nnz, nb = 20000, 600, 16, 7
+    off, keys, lab = pkg.gen_dataset(dims, B * nb, nnz, zipf=True, seed=40 + J)
+    tier = pkg.Tier(width=8, layer_dims=(8, 16, 1), minibatches=J, key_space=dims,
+                    max_batch_examples=B, max_batch_keys=B * nnz)
+    dstore = torch.zeros((dims, 8), dtype=torch.float32, device="cuda")
+    tier.attach_store(dstore.data_ptr(), on_device=True, num_keys=dims)
+    for b in range(nb):
+        tier.submit_batch(off[b * B:(b + 1) * B + 1] - off[b * B],
+                          keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B])
+        if b >= 2:
+            tier.wait_batch()
+    for _ in range(2):
+        tier.wait_batch()
+    dense = tier.get_dense()
+    tier.close()
+    torch.cuda.synchronize()
+    store = dstore.cpu().numpy()
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, 8, (8, 16, 1), J=J), B, off, keys, lab)
+    assert np.array_equal(dense, wd)
+    assert np.array_equal(store[wk.astype(np.int64)], wr)
