@@ -322,7 +322,7 @@ constexpr int kFallbackChunk = 2048;  // doubles staged per round (16 KB)
 //       (sum of earlier T) -> B; the last CTA of a weight group combines the
 //       slices, certifies, and recomputes uncertified weights in the exact
 //       order (the warp stages the products, lane 0 chains them).
-constexpr int kDGSlices = 32;
+constexpr int kDGSlices = 128;
 
 struct WeightRef {
   int hi, di;
@@ -364,74 +364,111 @@ __global__ void __launch_bounds__(32)
   slot[2] = a;
 }
 
+// Per weight (one warp), the slices' totals scanned in slice order: each
+// slice's offset (the total of the slices before it, for its B walk) and the
+// weight's total S and sum|x| A. Summation order inside the offsets is
+// covered by certify_f32's error terms, so a warp scan serves.
+__global__ void __launch_bounds__(128)
+    dense_grad_scan_kernel(ModelDims md, const double* __restrict__ part,
+                           double* __restrict__ off, double* __restrict__ tot) {
+  constexpr int kPer = kDGSlices / 32;
+  const int w = int(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5));
+  if (w >= md.nw) return;
+  const unsigned lane = threadIdx.x & 31;
+  const double* base = part + std::uint64_t(w) * kDGSlices * 4;
+  DD mine{0.0, 0.0};
+  double a = 0.0;
+  DD loc[kPer];
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int sl = int(lane) * kPer + i;
+    loc[i] = DD{base[sl * 4], base[sl * 4 + 1]};
+    mine = dd_add(mine, loc[i]);
+    a = __dadd_ru(a, base[sl * 4 + 2]);
+  }
+  DD incl = mine;  // inclusive scan over the lanes
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double hi = __shfl_up_sync(0xFFFFFFFFu, incl.hi, o);
+    const double lo = __shfl_up_sync(0xFFFFFFFFu, incl.lo, o);
+    if (lane >= unsigned(o)) incl = dd_add(DD{hi, lo}, incl);
+  }
+  DD run{__shfl_up_sync(0xFFFFFFFFu, incl.hi, 1), __shfl_up_sync(0xFFFFFFFFu, incl.lo, 1)};
+  if (lane == 0) run = DD{0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    off[std::uint64_t(w) * kDGSlices + lane * kPer + i] = dd_value(run);
+    run = dd_add(run, loc[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a = __dadd_ru(a, __shfl_xor_sync(0xFFFFFFFFu, a, o));
+  if (lane == 31) {
+    tot[std::uint64_t(w) * 4] = incl.hi;
+    tot[std::uint64_t(w) * 4 + 1] = incl.lo;
+  }
+  if (lane == 0) tot[std::uint64_t(w) * 4 + 2] = a;
+}
+
 __global__ void __launch_bounds__(32)
     dense_grad_p2_kernel(ModelDims md, std::uint64_t n, const double* __restrict__ H,
                          const double* __restrict__ DL, double* __restrict__ part,
-                         unsigned* __restrict__ done, float* __restrict__ grad,
-                         unsigned long long* __restrict__ fallbacks) {
-  __shared__ double stage[kFallbackChunk];
+                         const double* __restrict__ off) {
   const int w = blockIdx.x * 32 + threadIdx.x;
-  const bool live = w < md.nw;
-  const WeightRef r = live ? weight_ref(md, w) : WeightRef{0, 0, false};
+  if (w >= md.nw) return;
+  const WeightRef r = weight_ref(md, w);
   const std::uint64_t per = (n + kDGSlices - 1) / kDGSlices;
-  if (live) {
-    const double* base = part + std::uint64_t(w) * kDGSlices * 4;
-    DD off{0.0, 0.0};
-    for (unsigned s = 0; s < blockIdx.y; ++s) off = dd_add(off, DD{base[s * 4], base[s * 4 + 1]});
-    const double o = dd_value(off);
-    const std::uint64_t k0 = blockIdx.y * per, k1 = k0 + per < n ? k0 + per : n;
-    double l = 0.0, b = 0.0;
+  const double o = off[std::uint64_t(w) * kDGSlices + blockIdx.y];
+  const std::uint64_t k0 = blockIdx.y * per, k1 = k0 + per < n ? k0 + per : n;
+  double l = 0.0, b = 0.0;
 #pragma unroll 4
-    for (std::uint64_t k = k0; k < k1; ++k) {
-      l = __dadd_rn(l, weight_term(md, H, DL, r, k));
-      b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
-    }
-    part[(std::uint64_t(w) * kDGSlices + blockIdx.y) * 4 + 3] = b;
+  for (std::uint64_t k = k0; k < k1; ++k) {
+    l = __dadd_rn(l, weight_term(md, H, DL, r, k));
+    b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
   }
-  __threadfence();
-  unsigned last = 0;
-  if (threadIdx.x == 0) last = atomicAdd(&done[blockIdx.x], 1u) == kDGSlices - 1;
-  last = __shfl_sync(0xFFFFFFFFu, last, 0);
-  if (!last) return;
-  __threadfence();
-  if (threadIdx.x == 0) done[blockIdx.x] = 0;  // ready for the next launch
+  part[(std::uint64_t(w) * kDGSlices + blockIdx.y) * 4 + 3] = b;
+}
+
+// Per weight (one warp): B = sum of the slices' bounds (round-up, any
+// order), certify against S and A (certify_f32), and in the rare uncertified
+// case recompute the exact sequential chain (staged through shared memory).
+constexpr int kDGFinWarps = 4;
+constexpr int kDGStage = 1024;  // doubles staged per warp and round
+__global__ void __launch_bounds__(32 * kDGFinWarps)
+    dense_grad_fin_kernel(ModelDims md, std::uint64_t n, const double* __restrict__ H,
+                          const double* __restrict__ DL, const double* __restrict__ part,
+                          const double* __restrict__ tot, float* __restrict__ grad,
+                          unsigned long long* __restrict__ fallbacks) {
+  __shared__ double stage[kDGFinWarps][kDGStage];
+  const unsigned lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int w = int(blockIdx.x * kDGFinWarps + wi);
+  if (w >= md.nw) return;
+  const double* base = part + std::uint64_t(w) * kDGSlices * 4;
+  double b = 0.0;
+#pragma unroll
+  for (int i = 0; i < kDGSlices / 32; ++i) b = __dadd_ru(b, base[(lane * (kDGSlices / 32) + i) * 4 + 3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b = __dadd_ru(b, __shfl_xor_sync(0xFFFFFFFFu, b, o));
+  const std::uint64_t per = (n + kDGSlices - 1) / kDGSlices;
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  const DD S{tot[std::uint64_t(w) * 4], tot[std::uint64_t(w) * 4 + 1]};
   float g = 0.0f;
-  bool ok = true;
-  if (live) {
-    DD S{0.0, 0.0};
-    double A = 0.0, B = 0.0;
-    const double* base = part + std::uint64_t(w) * kDGSlices * 4;
-    for (int s = 0; s < kDGSlices; ++s) {
-      S = dd_add(S, DD{__ldcg(base + s * 4), __ldcg(base + s * 4 + 1)});
-      A = __dadd_ru(A, __ldcg(base + s * 4 + 2));
-      B = __dadd_ru(B, __ldcg(base + s * 4 + 3));
-    }
-    ok = certify_f32(dd_value(S), B, A, n, per + kDGSlices, inv_n, &g);
-  }
-  unsigned todo = __ballot_sync(0xFFFFFFFFu, !ok);
-  while (todo) {
-    const int src = __ffs(todo) - 1;
-    todo &= todo - 1;
-    WeightRef sr;
-    sr.hi = __shfl_sync(0xFFFFFFFFu, r.hi, src);
-    sr.di = __shfl_sync(0xFFFFFFFFu, r.di, src);
-    sr.bias = __shfl_sync(0xFFFFFFFFu, r.bias, src);
+  const bool ok = certify_f32(dd_value(S), b, tot[std::uint64_t(w) * 4 + 2], n, per + kDGSlices,
+                              inv_n, &g);
+  if (!ok) {  // the exact chain, in order (rare)
+    const WeightRef r = weight_ref(md, w);
     double acc = 0.0;
-    for (std::uint64_t c0 = 0; c0 < n; c0 += kFallbackChunk) {
-      const int cnt = int(n - c0 < kFallbackChunk ? n - c0 : kFallbackChunk);
-      for (int j = threadIdx.x; j < cnt; j += 32) stage[j] = weight_term(md, H, DL, sr, c0 + j);
+    for (std::uint64_t c0 = 0; c0 < n; c0 += kDGStage) {
+      const int cnt = int(n - c0 < kDGStage ? n - c0 : kDGStage);
+      for (int j = int(lane); j < cnt; j += 32) stage[wi][j] = weight_term(md, H, DL, r, c0 + j);
       __syncwarp();
-      if (threadIdx.x == 0) acc = chain_sum(stage, cnt, acc);
+      if (lane == 0) acc = chain_sum(stage[wi], cnt, acc);
       __syncwarp();
     }
     acc = __shfl_sync(0xFFFFFFFFu, acc, 0);
-    if (int(threadIdx.x) == src) {
-      g = __double2float_rn(__dmul_rn(acc, inv_n));
-      if (fallbacks) atomicAdd(fallbacks, 1ull);
-    }
+    g = __double2float_rn(__dmul_rn(acc, inv_n));
+    if (lane == 0 && fallbacks) atomicAdd(fallbacks, 1ull);
   }
-  if (live) grad[w] = g;
+  if (lane == 0) grad[w] = g;
 }
 
 inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw + 31) / 32); }

@@ -317,7 +317,7 @@ struct Tier {
 
   // model
   double *H = nullptr, *DL = nullptr, *DX = nullptr, *dpart = nullptr;
-  unsigned* dg_done = nullptr;
+  double *dg_off = nullptr, *dg_tot = nullptr;  // dense-grad slice offsets, totals
   float *dense = nullptr, *dgrad = nullptr;
 
   // value store (MEM-PS stand-in)
@@ -1493,9 +1493,15 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
       HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
       launch_on(T, T->st2, dense_grad_p1_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
                 0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart);
+      launch_on(T, T->st2, dense_grad_scan_kernel, unsigned((T->md.nw + 3) / 4), 128, 0, T->md,
+                (const double*)T->dpart, T->dg_off, T->dg_tot);
       launch_on(T, T->st2, dense_grad_p2_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
-                0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart, T->dg_done,
-                T->dgrad, &T->dsc->fallbacks);
+                0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart,
+                (const double*)T->dg_off);
+      launch_on(T, T->st2, dense_grad_fin_kernel,
+                unsigned((T->md.nw + kDGFinWarps - 1) / kDGFinWarps), 32 * kDGFinWarps, 0, T->md,
+                n, (const double*)T->H, (const double*)T->DL, (const double*)T->dpart,
+                (const double*)T->dg_tot, T->dgrad, &T->dsc->fallbacks);
       HPS_CUDA(cudaEventRecord(T->join, T->st2));
       HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob, Uj, segj, exsj));
       mark(T, HPS_T_SPARSE);
@@ -2264,7 +2270,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(DL, t->nmb_max * std::uint64_t(t->md.dw) + 2);
   A(DX, t->nmb_max * E);
   A(dpart, std::uint64_t(t->md.nw) * kDGSlices * 4);
-  A(dg_done, dense_grad_groups(t->md));
+  A(dg_off, std::uint64_t(t->md.nw) * kDGSlices);
+  A(dg_tot, std::uint64_t(t->md.nw) * 4);
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
 #undef A
@@ -2272,7 +2279,6 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     cudaMemsetAsync(g.gcnt, 0, t->gslots * 4, t->st);
     cudaMemsetAsync(g.part_n, 0, std::uint64_t(kGroupParts) * kGroupPartStride * 4, t->st);
   }
-  cudaMemsetAsync(t->dg_done, 0, dense_grad_groups(t->md) * 4, t->st);
   cudaMemsetAsync(t->key_done, 0, (S / (kLongSeg + 1) + 2) * 4, t->st);
   if ((e = cudaMemsetAsync(t->dsc, 0, sizeof(Scalars), t->st)) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: memset: %s", cudaGetErrorString(e)));
