@@ -98,18 +98,39 @@ __global__ void __launch_bounds__(128)
       for (int d0 = 0; d0 < E; d0 += LPE) {
         const int d = d0 + sub;
         double acc = 0.0;
-        for (std::uint32_t c = o0; c < o1; c += LPE) {
-          const int len = int(o1 - c < std::uint32_t(LPE) ? o1 - c : LPE);
-          const std::uint32_t my_row = sub < len ? occ_row[c + sub] : 0u;
-          float v[LPE];
+        // the row ids of 8 rounds (8 x LPE features) load at once, then rounds
+        // go in pairs: 2 x LPE independent row loads in flight per lane before
+        // the in-order f64 adds
+        constexpr int kIdRounds = 8;
+        for (std::uint32_t base = o0; base < o1; base += kIdRounds * LPE) {
+          std::uint32_t ids[kIdRounds];
 #pragma unroll
-          for (int r = 0; r < LPE; ++r) {
-            const std::uint32_t rid = __shfl_sync(gmask, my_row, r, LPE);
-            v[r] = (r < len && d < E) ? rows[std::uint64_t(rid) * E + d] : 0.0f;
+          for (int t = 0; t < kIdRounds; ++t) {
+            const std::uint32_t p = base + t * LPE + sub;
+            ids[t] = p < o1 ? occ_row[p] : 0u;
           }
 #pragma unroll
-          for (int r = 0; r < LPE; ++r)
-            if (r < len) acc = __dadd_rn(acc, double(v[r]));
+          for (int t = 0; t < kIdRounds; t += 2) {
+            const std::uint32_t c = base + t * LPE;
+            if (c >= o1) break;
+            const int len0 = int(o1 - c < std::uint32_t(LPE) ? o1 - c : LPE);
+            const std::uint32_t c1 = c + LPE;
+            const int len1 = c1 < o1 ? int(o1 - c1 < std::uint32_t(LPE) ? o1 - c1 : LPE) : 0;
+            float v0[LPE], v1[LPE];
+#pragma unroll
+            for (int r = 0; r < LPE; ++r) {
+              const std::uint32_t r0 = __shfl_sync(gmask, ids[t], r, LPE);
+              const std::uint32_t r1 = __shfl_sync(gmask, ids[t + 1], r, LPE);
+              v0[r] = (r < len0 && d < E) ? rows[std::uint64_t(r0) * E + d] : 0.0f;
+              v1[r] = (r < len1 && d < E) ? rows[std::uint64_t(r1) * E + d] : 0.0f;
+            }
+#pragma unroll
+            for (int r = 0; r < LPE; ++r)
+              if (r < len0) acc = __dadd_rn(acc, double(v0[r]));
+#pragma unroll
+            for (int r = 0; r < LPE; ++r)
+              if (r < len1) acc = __dadd_rn(acc, double(v1[r]));
+          }
         }
         if (d < E) hrec[d] = acc;
       }
