@@ -55,6 +55,11 @@ CONFIGS = {
     "c3": dict(dims=10**8, E=64, B=65536, nnz=100, zipf=False, J=4, layers=(8, 16, 1),
                text="c3 (SGD, no Adagrad yet): 100M-key table, E=64, batch 65536, "
                     "100 uniform keys/example, MLP {8,16,1}, J=4"),
+    # the MEM-PS host tier at scale (1B keys x E=16 = 64 GB of
+    # store; GPU box only)
+    "c5": dict(dims=10**9, E=16, B=131072, nnz=100, zipf=False, J=4, layers=(8, 16, 1),
+               text="c5: 1B-key value store (64 GB), E=16, batch 131072, 100 uniform "
+                    "keys/example, MLP {8,16,1}, J=4"),
 }
 
 
