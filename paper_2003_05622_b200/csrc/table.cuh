@@ -23,7 +23,9 @@
 namespace hpsgpu {
 
 __global__ void table_clear_kernel(std::uint64_t* __restrict__ keys,
-                                   const std::uint64_t* __restrict__ cap_ptr) {
+                                   const std::uint64_t* __restrict__ cap_ptr,
+                                   const unsigned* __restrict__ only_if = nullptr) {
+  if (only_if && *only_if == 0u) return;  // conditional pass (graph-stable)
   const std::uint64_t cap = *cap_ptr;
   for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        i < cap; i += std::uint64_t(gridDim.x) * blockDim.x)
@@ -72,9 +74,10 @@ __global__ void table_insert_kernel(const std::uint64_t* __restrict__ ws,
 
 // ---- sort-free build from the raw batch keys (hps_train_batch) ---------
 //
-// 1. ws_count_kernel: exact count of the distinct owned keys through a
-//    scratch hash set (atomicCAS; the capacity of the real table, hence its
-//    layout, depends on that count).
+// 1. table_insert_dedup_kernel, speculative: at the previous table's
+//    capacity, counting the distinct keys as they claim empty slots;
+//    table_spec_check_kernel redoes the build at the counted capacity when it
+//    differs (the layout depends on the capacity, hence on the count).
 // 2. table_insert_dedup_kernel: ordered linear probing of every owned
 //    occurrence; a thread that meets its own key stops. Ordered probing is
 //    history-independent for sets, so the layout equals ascending insertion
@@ -83,47 +86,21 @@ __global__ void table_insert_kernel(const std::uint64_t* __restrict__ ws,
 //    key order (table_prefetch_probe / store_gather / table_carry) and
 //    written back in key order (table_writeback_sorted).
 
-__global__ void ws_count_kernel(const std::uint64_t* __restrict__ keys,
-                                const std::int64_t* __restrict__ o_ptr, std::uint64_t G,
-                                std::uint64_t g, std::uint64_t* __restrict__ set,
-                                std::uint64_t set_mask, unsigned long long* __restrict__ n_ws) {
-  const std::uint64_t O = std::uint64_t(*o_ptr);
-  unsigned long long mine = 0;
-  for (std::uint64_t q = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; q < O;
-       q += std::uint64_t(gridDim.x) * blockDim.x) {
-    const std::uint64_t k = keys[q];
-    if (k % G != g) continue;
-    std::uint64_t idx = mix64(k) & set_mask;
-    for (;;) {
-      // read first: hot keys are already present, no atomic (and no contention)
-      const std::uint64_t seen = *reinterpret_cast<volatile const std::uint64_t*>(set + idx);
-      if (seen == k) break;
-      if (seen != kEmptyKey) {
-        idx = (idx + 1) & set_mask;
-        continue;
-      }
-      const unsigned long long old =
-          atomicCAS(reinterpret_cast<unsigned long long*>(set + idx), kEmptyKey, k);
-      if (old == kEmptyKey) {
-        ++mine;
-        break;
-      }
-      if (old == k) break;
-      idx = (idx + 1) & set_mask;
-    }
-  }
-  // warp-aggregated count
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
-  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(n_ws, mine);
-}
-
+// Counts the distinct keys as it goes (every occupied slot is claimed from
+// EMPTY exactly once, duplicates and displaced keys included) into *n_new.
+// Speculative pass (spec_fail non-null): a table that fills up sets
+// *spec_fail instead of raising. only_if non-null: run only if *only_if.
 __global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys,
                                           const std::int64_t* __restrict__ o_ptr,
                                           std::uint64_t G, std::uint64_t g,
                                           std::uint64_t* __restrict__ tkeys,
                                           const std::uint64_t* __restrict__ cap_ptr,
-                                          DevError* err) {
+                                          DevError* err, unsigned long long* __restrict__ n_new,
+                                          unsigned* __restrict__ spec_fail,
+                                          const unsigned* __restrict__ only_if) {
+  if (only_if && *only_if == 0u) return;
   const std::uint64_t O = std::uint64_t(*o_ptr), cap = *cap_ptr;
+  unsigned long long placed = 0;
   for (std::uint64_t q = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; q < O;
        q += std::uint64_t(gridDim.x) * blockDim.x) {
     std::uint64_t cur = keys[q];
@@ -142,22 +119,54 @@ __global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys
       if (seen < cur) {
         idx = (idx + 1) & (cap - 1);
         if (probes > cap) {
-          raise_error(err, 4, cur);
+          if (spec_fail) *spec_fail = 1u;
+          else raise_error(err, 4, cur);
           break;
         }
         continue;
       }
       const std::uint64_t old = atomicMin(reinterpret_cast<unsigned long long*>(tkeys + idx),
                                           static_cast<unsigned long long>(cur));
-      if (old == kEmptyKey || old == cur) break;  // placed / already present
-      if (old > cur) cur = old;                   // displaced: carry the larger key
+      if (old == kEmptyKey) {  // placed
+        ++placed;
+        break;
+      }
+      if (old == cur) break;       // already present
+      if (old > cur) cur = old;    // displaced: carry the larger key
       idx = (idx + 1) & (cap - 1);
       if (probes > cap) {
-        raise_error(err, 4, cur);
+        if (spec_fail) *spec_fail = 1u;
+        else raise_error(err, 4, cur);
         break;
       }
     }
   }
+  for (int o = 16; o > 0; o >>= 1) placed += __shfl_xor_sync(0xFFFFFFFFu, placed, o);
+  if ((threadIdx.x & 31) == 0 && placed && n_new) atomicAdd(n_new, placed);
+}
+
+// After the speculative insert: if the count asks for another capacity (or
+// the table filled up), set *redo, the right capacity, and reset the count
+// for the redo pass; otherwise clear *redo.
+__global__ void table_spec_check_kernel(unsigned long long* __restrict__ n,
+                                        std::uint64_t* __restrict__ cap,
+                                        unsigned* __restrict__ spec_fail,
+                                        unsigned* __restrict__ redo) {
+  const std::uint64_t needed = table_capacity(*n);
+  if (*spec_fail || needed != *cap) {
+    *redo = 1u;
+    *cap = needed;
+    *n = 0;
+    *spec_fail = 0u;
+  } else {
+    *redo = 0u;
+  }
+}
+
+// The capacity guess of the speculative build: the previous table's.
+__global__ void table_guess_kernel(const std::uint64_t* __restrict__ prev_cap,
+                                   std::uint64_t fallback, std::uint64_t* __restrict__ cap) {
+  *cap = prev_cap ? *prev_cap : fallback;
 }
 
 // Row-source tags in the top bits of csrc (slots stay below 2^30).

@@ -131,6 +131,7 @@ struct Scalars {
   unsigned long long wb_total;       // rows written to the store (cumulative)
   unsigned long long Ug[kTables][64];  // unique keys per (table, mini-batch), grouped path
   std::uint64_t rq_capv;               // request-table capacity (G > 1)
+  unsigned spec_fail, redo;            // speculative table build (prep)
   unsigned long long fallbacks;  // certified sums that needed the exact chain
   unsigned long long served;     // keys this rank served as owner (G > 1)
   DevError err;
@@ -288,8 +289,6 @@ struct Tier {
   std::uint32_t* wsib[kTables] = {};
   std::uint32_t* csrc[kTables] = {};  // carry source slot per working-set entry
   bool ws_sorted = true;
-  std::uint64_t* wsset = nullptr;    // scratch hash set of the sort-free build
-  std::uint64_t wsset_cap = 0;
 
   // batch staging (double-buffered)
   std::int64_t* b_off[kSlots] = {};
@@ -883,7 +882,7 @@ static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* sta
   launch(t, table_capacity_kernel, 1, 1, 0, (const std::uint64_t*)&t->dsc->n_ws,
          &t->dsc->cap[nxt]);
   launch(t, table_clear_kernel, grid_for(t->capmax), 256, 0, t->tkeys[nxt],
-         (const std::uint64_t*)&t->dsc->cap[nxt]);
+         (const std::uint64_t*)&t->dsc->cap[nxt], (const unsigned*)nullptr);
   launch(t, table_insert_kernel, grid_for(n_upper), 256, 0, (const std::uint64_t*)t->ws,
          (const std::uint64_t*)&t->dsc->n_ws, t->tkeys[nxt],
          (const std::uint64_t*)&t->dsc->cap[nxt], &t->dsc->err);
@@ -1286,22 +1285,30 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   std::uint64_t* nws = &T->dsc->nws_tab[tb];
   std::uint64_t* cap = &T->dsc->cap[tb];
   mark(T, -1);
-  std::uint64_t setcap = 1;
-  while (setcap < 2 * sh.own_bound) setcap <<= 1;
-  setcap = std::min(setcap, T->wsset_cap);
-  HPS_CUDA(cudaMemsetAsync(T->wsset, 0xFF, setcap * 8, l.st));
   HPS_CUDA(cudaMemsetAsync(nws, 0, 8, l.st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->carried_tab[tb], 0, 8, l.st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->stored_tab[tb], 0, 8, l.st));
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->spec_fail, 0, 4, l.st));
   const unsigned gk = grid_for(sh.batch_bound, 256, kSMs * 8);
-  launch(T, ws_count_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G), std::uint64_t(T->g),
-         T->wsset, setcap - 1, (unsigned long long*)nws);
-  launch(T, table_capacity_kernel, 1, 1, 0, (const std::uint64_t*)nws, cap);
   const std::uint64_t cap_bound = table_capacity(sh.own_bound);
+  // speculative build at the previous table's capacity (a steady workload
+  // keeps it), counting the distinct keys; the check redoes the build at the
+  // counted capacity when it differs — the layout is the same either way
+  launch(T, table_guess_kernel, 1, 1, 0, bp.tp >= 0 ? (const std::uint64_t*)&T->dsc->cap[bp.tp]
+                                                    : (const std::uint64_t*)nullptr,
+         std::min(cap_bound, T->capmax), cap);  // (the shape bound may exceed the buffers)
   launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[tb],
-         (const std::uint64_t*)cap);
+         (const std::uint64_t*)cap, (const unsigned*)nullptr);
   launch(T, table_insert_dedup_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G),
-         std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap, &T->dsc->err);
+         std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap, &T->dsc->err,
+         (unsigned long long*)nws, &T->dsc->spec_fail, (const unsigned*)nullptr);
+  launch(T, table_spec_check_kernel, 1, 1, 0, (unsigned long long*)nws, cap, &T->dsc->spec_fail,
+         &T->dsc->redo);
+  launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[tb],
+         (const std::uint64_t*)cap, (const unsigned*)&T->dsc->redo);
+  launch(T, table_insert_dedup_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G),
+         std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap, &T->dsc->err,
+         (unsigned long long*)nws, (unsigned*)nullptr, (const unsigned*)&T->dsc->redo);
   // the table's keys are final: the mini-batches' grouping forks onto lane 2
   // and runs beside the rest of the build (joined at the end of the prep)
   if (bp.grouped) {
@@ -2187,9 +2194,6 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   }
   t->ws = t->wsb[0];
   t->ws_idx = t->wsib[0];
-  t->wsset_cap = 1;
-  while (t->wsset_cap < 2 * std::max(O, W)) t->wsset_cap <<= 1;
-  A(wsset, t->wsset_cap);
   const std::uint64_t S = std::max(O, W);
   const std::uint64_t status_words =
       std::max<std::uint64_t>(std::uint64_t(kDigits) * sort_tiles(S), scan_tiles(S)) + 1;
