@@ -550,32 +550,34 @@ __global__ void __launch_bounds__(256)
     double acc[DPT];
 #pragma unroll
     for (int i = 0; i < DPT; ++i) acc[i] = 0.0;
+    // four rows in flight per step (independent loads), added in order
     std::uint32_t p = p0;
-    for (; p + 2 <= p1; p += 2) {  // two rows in flight
-      const double* r0 = DX + std::uint64_t(exs[p]) * E + d0;
-      const double* r1 = DX + std::uint64_t(exs[p + 1]) * E + d0;
-      double x0[DPT], x1[DPT];
-      if (DPT == 4) {
-        const double2 a0 = *reinterpret_cast<const double2*>(r0);
-        const double2 b0 = *reinterpret_cast<const double2*>(r0 + 2);
-        const double2 a1 = *reinterpret_cast<const double2*>(r1);
-        const double2 b1 = *reinterpret_cast<const double2*>(r1 + 2);
-        x0[0] = a0.x; x0[1 % DPT] = a0.y; x0[2 % DPT] = b0.x; x0[3 % DPT] = b0.y;
-        x1[0] = a1.x; x1[1 % DPT] = a1.y; x1[2 % DPT] = b1.x; x1[3 % DPT] = b1.y;
-      } else {
+    for (; p + 4 <= p1; p += 4) {
+      double x[4][DPT];
 #pragma unroll
-        for (int i = 0; i < DPT; ++i) {
-          x0[i] = r0[i];
-          x1[i] = r1[i];
+      for (int r = 0; r < 4; ++r) {
+        const double* row = DX + std::uint64_t(exs[p + r]) * E + d0;
+        if (DPT == 4) {
+          const double2 a = *reinterpret_cast<const double2*>(row);
+          const double2 b = *reinterpret_cast<const double2*>(row + 2);
+          x[r][0] = a.x;
+          x[r][1 % DPT] = a.y;
+          x[r][2 % DPT] = b.x;
+          x[r][3 % DPT] = b.y;
+        } else {
+#pragma unroll
+          for (int i = 0; i < DPT; ++i) x[r][i] = row[i];
         }
       }
 #pragma unroll
-      for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(__dadd_rn(acc[i], x0[i]), x1[i]);
-    }
-    if (p < p1) {
-      const double* r0 = DX + std::uint64_t(exs[p]) * E + d0;
+      for (int r = 0; r < 4; ++r)
 #pragma unroll
-      for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(acc[i], r0[i]);
+        for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(acc[i], x[r][i]);
+    }
+    for (; p < p1; ++p) {
+      const double* row = DX + std::uint64_t(exs[p]) * E + d0;
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(acc[i], row[i]);
     }
 #pragma unroll
     for (int i = 0; i < DPT; ++i) write_delta(out, pos ? pos[u] : u, E, d0 + i, acc[i], inv_n, lr);
