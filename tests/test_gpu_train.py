@@ -53,6 +53,7 @@ def check_bit_exact(oracle, pkg, off, keys, lab, B, *, E, layers, J, dims):
     (1, (1,), 1, False),
     (64, (8, 16, 1), 4, True),
     (12, (16, 8, 1), 3, True),
+    (128, (8, 16, 1), 8, True),
 ])
 def test_train_bit_exact_vs_oracle(pkg, oracle, E, layers, J, zipf):
     dims, B, nnz = 30000, 512, 20
