@@ -588,6 +588,9 @@ __global__ void __launch_bounds__(256)
 //
 // Work item w = (big key, chunk of fuse_chunk(E) occurrences). big_plan:
 // prefix of the per-key chunk counts; big_fused_kernel (below) does the rest.
+constexpr int kLocalChunks = 1;             // single-chunk keys: one CTA, no flags
+constexpr std::uint32_t kLocalItem = 0xFFFFFFFFu;
+
 struct ChunkSum {  // one chunk of one dimension: total (Neumaier), sum|x|, B bound
   double hi, lo, a, b;
 };
@@ -604,10 +607,11 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
   std::uint32_t carry = 0;
   for (std::uint64_t b0 = 0; b0 < NB; b0 += blockDim.x) {
     const std::uint64_t i = b0 + threadIdx.x;
-    std::uint32_t v = 0;
+    std::uint32_t v = 0, nchk = 0;
     if (i < NB) {
       const std::uint32_t u = big_list[i];
-      v = (seg[u + 1] - seg[u] + chunk - 1) / chunk;
+      nchk = (seg[u + 1] - seg[u] + chunk - 1) / chunk;
+      v = nchk <= std::uint32_t(kLocalChunks) ? 1u : nchk;  // one CTA walks a short key
     }
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     std::uint32_t x = v;
@@ -624,7 +628,7 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
       chunk_off[i] = pre + x - v;
       for (std::uint32_t c = 0; c < v; ++c) {  // the item table: item -> (key, chunk)
         item_key[pre + x - v + c] = std::uint32_t(i);
-        item_chunk[pre + x - v + c] = c;
+        item_chunk[pre + x - v + c] = v == 1 && nchk <= std::uint32_t(kLocalChunks) ? kLocalItem : c;
       }
     }
     std::uint32_t tot = 0;
@@ -660,7 +664,7 @@ constexpr int kFuseThreads = 256;
 constexpr int kFusePer = 16;  // occurrences per slice of a chunk
 inline int fuse_chunk(int E) { return (kFuseThreads / E) * kFusePer; }
 
-__global__ void __launch_bounds__(kFuseThreads)
+__global__ void __launch_bounds__(kFuseThreads, 3)
     big_fused_kernel(int E, float lr, std::uint64_t n, const std::uint32_t* __restrict__ big_list,
                      const unsigned long long* __restrict__ n_big,
                      const std::uint32_t* __restrict__ chunk_off,
@@ -673,6 +677,7 @@ __global__ void __launch_bounds__(kFuseThreads)
                      unsigned long long* __restrict__ ticket, unsigned* __restrict__ key_done,
                      float* __restrict__ out, unsigned long long* __restrict__ fallbacks) {
   __shared__ double sh[kFuseThreads], sl[kFuseThreads], sa[kFuseThreads], sb[kFuseThreads];
+  __shared__ double rh[kFuseThreads], rl[kFuseThreads];  // local path: running chunk total
   __shared__ double stage[kFallbackChunk];
   __shared__ bool bad[kFuseThreads];
   __shared__ unsigned long long s_item;
@@ -691,6 +696,99 @@ __global__ void __launch_bounds__(kFuseThreads)
     const std::uint32_t ki = item_key[w], c = item_chunk[w];
     const std::uint32_t u = big_list[ki];
     const std::uint32_t k0 = seg[u], k1 = seg[u + 1];
+    if (c == kLocalItem) {
+      // the whole key on this CTA: chunks in order, the running total in
+      // shared memory, no flags, no cross-CTA certification
+      const std::uint32_t nchk = (k1 - k0 + std::uint32_t(chunk) - 1) / std::uint32_t(chunk);
+      DD S{0.0, 0.0};
+      double A = 0.0, B = 0.0;
+      if (int(threadIdx.x) < E) {
+        rh[threadIdx.x] = 0.0;
+        rl[threadIdx.x] = 0.0;
+      }
+      for (std::uint32_t cc = 0; cc < nchk; ++cc) {
+        const std::uint32_t q0 = k0 + cc * chunk, q1 = min(k1, q0 + std::uint32_t(chunk));
+        const std::uint32_t a0 = q0 + s * kFusePer;
+        const int cnt = worker && a0 < q1 ? int(min(q1 - a0, std::uint32_t(kFusePer))) : 0;
+        double x[kFusePer];
+        {
+          std::uint32_t e[kFusePer];
+#pragma unroll
+          for (int i = 0; i < kFusePer; ++i) e[i] = i < cnt ? exs[a0 + i] : 0u;
+#pragma unroll
+          for (int i = 0; i < kFusePer; ++i)
+            x[i] = i < cnt ? DX[std::uint64_t(e[i]) * E + d] : 0.0;
+        }
+        if (worker) {
+          DD t{0.0, 0.0};
+          double asum = 0.0;
+#pragma unroll
+          for (int i = 0; i < kFusePer; ++i) {
+            if (i < cnt) {
+              t = dd_add(t, x[i]);
+              asum = __dadd_ru(asum, fabs(x[i]));
+            }
+          }
+          sh[threadIdx.x] = t.hi;
+          sl[threadIdx.x] = t.lo;
+          sa[threadIdx.x] = asum;
+        }
+        __syncthreads();
+        if (worker) {  // offset: earlier chunks, then this chunk's earlier slices
+          DD off{rh[d], rl[d]};
+          for (int q = 0; q < s; ++q) off = dd_add(off, DD{sh[q * E + d], sl[q * E + d]});
+          const double o = dd_value(off);
+          double l = 0.0, b = 0.0;
+#pragma unroll
+          for (int i = 0; i < kFusePer; ++i) {
+            if (i < cnt) {
+              l = __dadd_rn(l, x[i]);
+              b = __dadd_ru(b, fabs(__dadd_rn(o, l)));
+            }
+          }
+          sb[threadIdx.x] = b;
+        }
+        __syncthreads();
+        if (int(threadIdx.x) < E) {  // fold the chunk, slices in order
+          DD run{rh[threadIdx.x], rl[threadIdx.x]};
+          for (int q = 0; q < slices; ++q) {
+            const DD tq{sh[q * E + threadIdx.x], sl[q * E + threadIdx.x]};
+            run = dd_add(run, tq);
+            S = dd_add(S, tq);
+            A = __dadd_ru(A, sa[q * E + threadIdx.x]);
+            B = __dadd_ru(B, sb[q * E + threadIdx.x]);
+          }
+          rh[threadIdx.x] = run.hi;
+          rl[threadIdx.x] = run.lo;
+        }
+        __syncthreads();
+      }
+      float g = 0.0f;
+      if (int(threadIdx.x) < E)
+        bad[threadIdx.x] = !certify_f32(dd_value(S), B, A, k1 - k0, (k1 - k0) + slices + nchk,
+                                        inv_n, &g);
+      __syncthreads();
+      for (int dd = 0; dd < E; ++dd) {
+        if (!bad[dd]) continue;
+        double acc = 0.0;
+        for (std::uint32_t cs0 = k0; cs0 < k1; cs0 += kFallbackChunk) {
+          const int m = int(k1 - cs0 < kFallbackChunk ? k1 - cs0 : kFallbackChunk);
+          for (int j = threadIdx.x; j < m; j += kFuseThreads)
+            stage[j] = DX[std::uint64_t(exs[cs0 + j]) * E + dd];
+          __syncthreads();
+          if (int(threadIdx.x) == dd) acc = chain_sum(stage, m, acc);
+          __syncthreads();
+        }
+        if (int(threadIdx.x) == dd) {
+          g = __double2float_rn(__dmul_rn(acc, inv_n));
+          if (fallbacks) atomicAdd(fallbacks, 1ull);
+        }
+      }
+      if (int(threadIdx.x) < E)
+        out[std::uint64_t(pos ? pos[u] : u) * E + threadIdx.x] = -__fmul_rn(lr, g);
+      __syncthreads();
+      continue;
+    }
     const std::uint32_t nch = chunk_off[ki + 1] - chunk_off[ki];
     const std::uint64_t w0 = w - c;  // the key's first item
     const std::uint32_t c0 = k0 + c * chunk, c1 = min(k1, c0 + std::uint32_t(chunk));
