@@ -374,7 +374,10 @@ def run_ours(args, rank, world, local_rank):
     per_key_build = 8 + 8 + 4 * E + 4 * E
     # sparse segment-reduce (a8, a9): per occurrence its example's dL/dx row
     # (E f64) + the example id; per unique key its segment bounds + delta row
-    per_occ_sparse, per_key_sparse = 8 * E + 4, 8 + 4 * E
+    # (at one rank the delta is added in place: the table row read + written)
+    fused_apply = world == 1 and os.environ.get("HPS_DEDUP", "hash") != "sort"
+    per_occ_sparse = 8 * E + 4
+    per_key_sparse = 8 + 8 * E if fused_apply else 8 + 4 * E
     phase_bytes = {
         "sparse": occ * per_occ_sparse + pulled * per_key_sparse,
         "pull": pulled * per_key_pull,
@@ -383,10 +386,12 @@ def run_ours(args, rank, world, local_rank):
         "writeback": ws * per_key_pull,
         "dedup": 12 * occ + 8 * pulled,
     }
-    if world == 1 and os.environ.get("HPS_DEDUP", "hash") != "sort":
-        # G = 1: fwd/bwd reads the rows in place from the table (a6 fused), so
-        # there is no pull kernel to put on the roofline
+    if fused_apply:
+        # G = 1: fwd/bwd reads the rows in place from the table (a6 fused) and
+        # the sparse reduce applies the deltas in place (a10/a11 fused), so
+        # there is no pull or apply kernel to put on the roofline
         phase_bytes.pop("pull")
+        phase_bytes.pop("apply")
     rl = {}
     for name, nbytes in phase_bytes.items():
         ms = phases.get(name, 0.0)
@@ -404,10 +409,12 @@ def run_ours(args, rank, world, local_rank):
         except Exception:
             traffic = None
     dom = rl.get(dominant, {})
-    names = {"sparse": "sparse segment-reduce + sgd_delta (sparse_short_kernel, big_plan/"
-                       "big_p1/big_p2_kernel), per mini-batch",
+    names = {"sparse": "sparse segment-reduce + sgd_delta" + (" + in-place apply" if fused_apply
+                                                              else "") +
+                       " (sparse_short_kernel, big_plan_kernel, big_fused_kernel), per mini-batch",
              "pull": "table_gather_kernel<4>", "apply": "table_apply_kernel<4>"}
-    models = {"sparse": "O*(8E+4) + U*(8+4E)", "pull": "U*(8+8+8E)", "apply": "U*(4+12E)"}
+    models = {"sparse": "O*(8E+4) + U*(8+8E)" if fused_apply else "O*(8E+4) + U*(8+4E)",
+              "pull": "U*(8+8+8E)", "apply": "U*(4+12E)"}
     roofline = {"bound": "hbm", "kernel": names.get(dominant, dominant),
                 "achieved": dom.get("achieved_gbs"), "peak": peak, "unit": "GB/s",
                 "frac": dom.get("frac"), "traffic": traffic, "peak_kind": peak_kind,

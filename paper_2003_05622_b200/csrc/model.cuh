@@ -506,10 +506,29 @@ inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw 
 // queued for the chunked, certified big_fused_kernel.
 constexpr int kLongSeg = 32;
 
-__device__ __forceinline__ void write_delta(float* out, std::uint64_t row, int E, int d,
+// Where a key's sgd_delta goes: the push row (pos[u], or u), or — one rank,
+// the key's slot known (apply_slot) — straight into the table row:
+// v = v + d in f32, DeviceTable::accumulate (device_table.hpp:88-95), the
+// delta being final when written (one writer per key and dimension).
+struct DeltaOut {
+  float* out;
+  const std::uint32_t* pos;
+  const std::uint32_t* apply_slot;
+  float* table;
+  __device__ __forceinline__ void put(std::uint64_t u, int E, int d, float delta) const {
+    if (apply_slot) {
+      float* v = table + std::uint64_t(apply_slot[u]) * E + d;
+      *v = __fadd_rn(*v, delta);
+    } else {
+      out[std::uint64_t(pos ? pos[u] : u) * E + d] = delta;
+    }
+  }
+};
+
+__device__ __forceinline__ void write_delta(const DeltaOut& o, std::uint64_t u, int E, int d,
                                             double acc, double inv_n, float lr) {
   const float g = __double2float_rn(__dmul_rn(acc, inv_n));
-  out[row * E + d] = -__fmul_rn(lr, g);
+  o.put(u, E, d, -__fmul_rn(lr, g));
 }
 
 // Short segments, exact: one thread per (unique key, DPT dims) sums the key's
@@ -520,9 +539,8 @@ template <int DPT>
 __global__ void __launch_bounds__(256)
     sparse_short_kernel(int E, float lr, std::uint64_t n, const std::uint64_t* __restrict__ u_ptr,
                         const std::uint32_t* __restrict__ seg,
-                        const std::uint32_t* __restrict__ exs,
-                        const std::uint32_t* __restrict__ pos,
-                        const double* __restrict__ DX, float* __restrict__ out,
+                        const std::uint32_t* __restrict__ exs, DeltaOut dout,
+                        const double* __restrict__ DX,
                         unsigned long long* __restrict__ pulled,
                         std::uint32_t* __restrict__ long_list,
                         unsigned long long* __restrict__ n_long,
@@ -580,7 +598,7 @@ __global__ void __launch_bounds__(256)
       for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(acc[i], row[i]);
     }
 #pragma unroll
-    for (int i = 0; i < DPT; ++i) write_delta(out, pos ? pos[u] : u, E, d0 + i, acc[i], inv_n, lr);
+    for (int i = 0; i < DPT; ++i) write_delta(dout, u, E, d0 + i, acc[i], inv_n, lr);
   }
 }
 
@@ -672,10 +690,10 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
                      const std::uint32_t* __restrict__ item_key,
                      const std::uint32_t* __restrict__ item_chunk,
                      const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
-                     const std::uint32_t* __restrict__ pos, const double* __restrict__ DX,
+                     DeltaOut dout, const double* __restrict__ DX,
                      ChunkSum* __restrict__ chunk_tot, unsigned* __restrict__ flags,
                      unsigned long long* __restrict__ ticket, unsigned* __restrict__ key_done,
-                     float* __restrict__ out, unsigned long long* __restrict__ fallbacks) {
+                     unsigned long long* __restrict__ fallbacks) {
   __shared__ double sh[kFuseThreads], sl[kFuseThreads], sa[kFuseThreads], sb[kFuseThreads];
   __shared__ double rh[kFuseThreads], rl[kFuseThreads];  // local path: running chunk total
   __shared__ double stage[kFallbackChunk];
@@ -785,7 +803,7 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
         }
       }
       if (int(threadIdx.x) < E)
-        out[std::uint64_t(pos ? pos[u] : u) * E + threadIdx.x] = -__fmul_rn(lr, g);
+        dout.put(u, E, int(threadIdx.x), -__fmul_rn(lr, g));
       __syncthreads();
       continue;
     }
@@ -918,7 +936,7 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
       }
     }
     if (int(threadIdx.x) < E)
-      out[std::uint64_t(pos ? pos[u] : u) * E + threadIdx.x] = -__fmul_rn(lr, g);
+      dout.put(u, E, int(threadIdx.x), -__fmul_rn(lr, g));
     __syncthreads();
   }
 }

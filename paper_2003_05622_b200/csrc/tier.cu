@@ -1060,7 +1060,11 @@ constexpr int kMediumMax = kLongSeg;  // medium path off: chunks serve every lon
 // 4..32), then one CTA per long segment.
 static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint32_t* pos,
                                       std::uint64_t u_upper, const std::uint64_t* U,
-                                      const std::uint32_t* seg, const std::uint32_t* exs) {
+                                      const std::uint32_t* seg, const std::uint32_t* exs,
+                                      const std::uint32_t* apply_slot = nullptr) {
+  // apply_slot non-null (one rank, the keys' table slots known): the deltas
+  // go straight into the current table, no delta rows and no apply launch
+  const DeltaOut dout{t->deltas, pos, apply_slot, apply_slot ? t->tvals[t->cur] : nullptr};
   const int E = t->E;
   if (E > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
   const float lr = t->cfg.learning_rate;
@@ -1073,7 +1077,7 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   const int dpt = (E % 4 == 0) ? 4 : 1;
   auto sk = dpt == 4 ? sparse_short_kernel<4> : sparse_short_kernel<1>;
   launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,
-         E, lr, n, U, seg, exs, pos, DX, t->deltas, pulled, t->long_list, nl, t->big_list, nb,
+         E, lr, n, U, seg, exs, dout, DX, pulled, t->long_list, nl, t->big_list, nb,
          std::uint32_t(kMediumMax));
   // big segments: plan (key, chunk) items, then one fused pass over CTAs
   // (ticket order; flags and ticket reset per launch)
@@ -1086,9 +1090,8 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   launch(t, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
          (const std::uint32_t*)t->big_list, (const unsigned long long*)nb,
          (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
-         (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs, pos, DX,
-         t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, t->deltas,
-         &t->dsc->fallbacks);
+         (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs, dout, DX,
+         t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, &t->dsc->fallbacks);
   return HPS_OK;
 }
 
@@ -1510,15 +1513,18 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                 n, (const double*)T->H, (const double*)T->DL, (const double*)T->dpart,
                 (const double*)T->dg_tot, T->dgrad, &T->dsc->fallbacks);
       HPS_CUDA(cudaEventRecord(T->join, T->st2));
-      HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob, Uj, segj, exsj));
+      HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob, Uj, segj, exsj,
+                                  bp.grouped && G == 1 ? slotsj : nullptr));
       mark(T, HPS_T_SPARSE);
       HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
     } else {
       HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));
     }
     mark(T, HPS_T_GRADS);
-    // push + canonical apply (a10, a11)
-    if (G == 1) {
+    // push + canonical apply (a10, a11); grouped at one rank the sparse
+    // reduce already applied each key's delta in place
+    if (G == 1 && bp.grouped) {
+    } else if (G == 1) {
       const std::uint64_t work = ob * std::uint64_t(E / V);
       if (V == 4)
         launch(T, table_apply_kernel<4>, grid_for(work), 256, 0, slotsj,
