@@ -7,6 +7,13 @@ namespace hpsgpu {
 
 constexpr std::uint64_t kEmptyKey = ~std::uint64_t{0};  // device_table.hpp:34
 constexpr std::uint32_t kNoSlot = 0xFFFFFFFFu;
+
+// Programmatic dependent launch (sm_90+): kernels are launched with
+// programmatic stream serialization, so a kernel may start while its
+// predecessor's last blocks finish; every kernel first waits here until the
+// predecessor's memory operations are visible (a no-op without such a
+// dependency).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 constexpr int kSMs = 148;  // B200: 2 dies x 74 SMs
 
 // Device error word: the first failure wins; the host maps it to the

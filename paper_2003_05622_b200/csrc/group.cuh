@@ -53,6 +53,7 @@ __global__ void rq_insert_kernel(const std::int64_t* __restrict__ off,
                                  const std::uint64_t* __restrict__ keys, std::uint64_t B, int G,
                                  int g, int J, std::uint64_t* __restrict__ rq,
                                  const std::uint64_t* __restrict__ cap_ptr) {
+  pdl_wait();
   const std::uint64_t cap = *cap_ptr, GJ = std::uint64_t(G) * J;
   const unsigned lane = threadIdx.x & 31;
   const std::uint64_t nw = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -93,6 +94,7 @@ __global__ void group_probe_kernel(ShardMap sm, const std::int64_t* __restrict__
                                    std::uint32_t* __restrict__ occ_slot,
                                    std::uint32_t* __restrict__ tick,
                                    std::uint32_t* __restrict__ ex_of, DevError* err) {
+  pdl_wait();
   const std::uint64_t cap = *cap_ptr;
   const unsigned lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -164,6 +166,7 @@ __global__ void group_compact_kernel(const std::uint32_t* __restrict__ part_n,
                                      std::uint32_t part_cap, std::uint32_t* __restrict__ part_base,
                                      std::uint32_t* __restrict__ uid_slot,
                                      unsigned long long* __restrict__ n_uid) {
+  pdl_wait();
   __shared__ std::uint32_t base[kGroupParts + 1];
   if (threadIdx.x == 0) {
     std::uint32_t run = 0;
@@ -200,6 +203,7 @@ __global__ void uid_keys_kernel(const std::uint32_t* __restrict__ uid_slot,
                                 const std::uint64_t* __restrict__ rq,
                                 const unsigned long long* __restrict__ n_uid,
                                 std::uint64_t* __restrict__ ukeys) {
+  pdl_wait();
   const std::uint64_t U = *n_uid;
   for (std::uint64_t u = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; u < U;
        u += std::uint64_t(gridDim.x) * blockDim.x)
@@ -232,6 +236,7 @@ __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__
                                    const std::uint32_t* __restrict__ seg,
                                    std::uint32_t* __restrict__ seg_occ,
                                    std::uint32_t* __restrict__ inv) {
+  pdl_wait();
   __shared__ std::uint32_t pb[kGroupParts];
   if (threadIdx.x < kGroupParts) pb[threadIdx.x] = part_base[threadIdx.x];
   __syncthreads();
@@ -264,6 +269,7 @@ __global__ void group_order_kernel(const unsigned long long* __restrict__ n_uid,
                                    std::uint32_t* __restrict__ huge_list,
                                    unsigned long long* __restrict__ n_huge,
                                    std::uint32_t* __restrict__ part_n) {
+  pdl_wait();
   const std::uint64_t U = *n_uid;
   if (blockIdx.x == 0 && threadIdx.x < kGroupParts) part_n[threadIdx.x * kGroupPartStride] = 0;
   for (std::uint64_t u = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; u < U;
@@ -328,6 +334,7 @@ __global__ void __launch_bounds__(kGroupWarpThreads)
                       const std::uint32_t* __restrict__ ex_of, std::uint32_t words,
                       std::uint32_t* __restrict__ exs, std::uint32_t* __restrict__ dup_list,
                       unsigned long long* __restrict__ n_dup) {
+  pdl_wait();
   constexpr int R = kGroupWarpMax / 32;
   extern __shared__ std::uint32_t wsm[];  // per warp: bitmap[words], prefix[words]
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -395,6 +402,7 @@ __global__ void __launch_bounds__(kGroupThreads)
                      const std::uint32_t* __restrict__ ex_of, std::uint32_t words,
                      std::uint32_t* __restrict__ exs, std::uint32_t* __restrict__ dup_list,
                      unsigned long long* __restrict__ n_dup) {
+  pdl_wait();
   extern __shared__ std::uint32_t cbm[];  // bitmap[words], prefix[words]
   __shared__ std::uint32_t wsum[kGroupThreads / 32];
   __shared__ int s_dup;
@@ -464,6 +472,7 @@ __global__ void __launch_bounds__(kGroupThreads)
                      const std::uint32_t* __restrict__ seg,
                      const std::uint32_t* __restrict__ seg_occ,
                      const std::uint32_t* __restrict__ ex_of, std::uint32_t* __restrict__ exs) {
+  pdl_wait();
   const std::uint64_t ND = *n_dup;
   for (std::uint64_t li = blockIdx.x; li < ND; li += gridDim.x) {
     const std::uint32_t u = dup_list[li];

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(128)
                    double* __restrict__ H, double* __restrict__ DL,
                    double* __restrict__ DX, double* __restrict__ loss,
                    DevError* err) {
+  pdl_wait();
   extern __shared__ double smem[];
   constexpr int kEPB = 128 / LPE;  // examples per block
   float* W = reinterpret_cast<float*>(smem);
@@ -366,6 +367,7 @@ __device__ __forceinline__ double weight_term(const ModelDims& md, const double*
 __global__ void __launch_bounds__(32)
     dense_grad_p1_kernel(ModelDims md, std::uint64_t n, const double* __restrict__ H,
                          const double* __restrict__ DL, double* __restrict__ part) {
+  pdl_wait();
   const int w = blockIdx.x * 32 + threadIdx.x;
   if (w >= md.nw) return;
   const WeightRef r = weight_ref(md, w);
@@ -392,6 +394,7 @@ __global__ void __launch_bounds__(32)
 __global__ void __launch_bounds__(128)
     dense_grad_scan_kernel(ModelDims md, const double* __restrict__ part,
                            double* __restrict__ off, double* __restrict__ tot) {
+  pdl_wait();
   constexpr int kPer = kDGSlices / 32;
   const int w = int(blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5));
   if (w >= md.nw) return;
@@ -434,6 +437,7 @@ __global__ void __launch_bounds__(32)
     dense_grad_p2_kernel(ModelDims md, std::uint64_t n, const double* __restrict__ H,
                          const double* __restrict__ DL, double* __restrict__ part,
                          const double* __restrict__ off) {
+  pdl_wait();
   const int w = blockIdx.x * 32 + threadIdx.x;
   if (w >= md.nw) return;
   const WeightRef r = weight_ref(md, w);
@@ -459,6 +463,7 @@ __global__ void __launch_bounds__(32 * kDGFinWarps)
                           const double* __restrict__ DL, const double* __restrict__ part,
                           const double* __restrict__ tot, float* __restrict__ grad,
                           unsigned long long* __restrict__ fallbacks) {
+  pdl_wait();
   __shared__ double stage[kDGFinWarps][kDGStage];
   const unsigned lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   const int w = int(blockIdx.x * kDGFinWarps + wi);
@@ -546,6 +551,7 @@ __global__ void __launch_bounds__(256)
                         unsigned long long* __restrict__ n_long,
                         std::uint32_t* __restrict__ big_list,
                         unsigned long long* __restrict__ n_big, std::uint32_t medium_max) {
+  pdl_wait();
   const std::uint64_t U = *u_ptr;
   if (pulled && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(pulled, (unsigned long long)U);
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
@@ -620,6 +626,7 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
                                 unsigned long long* __restrict__ n_items,
                                 std::uint32_t* __restrict__ item_key,
                                 std::uint32_t* __restrict__ item_chunk) {
+  pdl_wait();
   __shared__ std::uint32_t ws[32];
   const std::uint64_t NB = *n_big;
   std::uint32_t carry = 0;
@@ -694,6 +701,7 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
                      ChunkSum* __restrict__ chunk_tot, unsigned* __restrict__ flags,
                      unsigned long long* __restrict__ ticket, unsigned* __restrict__ key_done,
                      unsigned long long* __restrict__ fallbacks) {
+  pdl_wait();
   __shared__ double sh[kFuseThreads], sl[kFuseThreads], sa[kFuseThreads], sb[kFuseThreads];
   __shared__ double rh[kFuseThreads], rl[kFuseThreads];  // local path: running chunk total
   __shared__ double stage[kFallbackChunk];
@@ -951,6 +959,7 @@ __global__ void dense_update_kernel(float* __restrict__ w,
                                     float lr, int apply, float* __restrict__ sum_out,
                                     DevError* err, const float* bufs_odd = nullptr,
                                     const unsigned long long* round = nullptr) {
+  pdl_wait();
   if (round && (*round & 1)) bufs = bufs_odd;  // P2P window parity of this round
   for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        i < len; i += std::uint64_t(gridDim.x) * blockDim.x) {

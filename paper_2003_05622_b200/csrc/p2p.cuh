@@ -47,7 +47,8 @@ struct P2PCtx {
   __device__ __forceinline__ const PeerWindows& cur(std::uint64_t e) const { return par[e & 1]; }
 };
 
-__global__ void epoch_inc_kernel(unsigned long long* epoch) { *epoch += 1; }
+__global__ void epoch_inc_kernel(unsigned long long* epoch) {
+  pdl_wait(); *epoch += 1; }
 
 __device__ __forceinline__ void st_release_sys(std::uint64_t* p, std::uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
@@ -77,6 +78,7 @@ __device__ __forceinline__ void signal_peers(const PeerWindows& pw, int G, int m
 // Waits until every source raised `phase` to the current round in this
 // rank's flags.
 __global__ void p2p_wait_kernel(P2PCtx ctx, int G, int me, int phase, DevError* err) {
+  pdl_wait();
   if (threadIdx.x >= unsigned(G)) return;
   const std::uint64_t epoch = ctx.round();
   const std::uint64_t* f = ctx.par[0].flags[me] + threadIdx.x * kPhases + phase;
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(kRankThreads)
                       const std::uint64_t* __restrict__ u_ptr, int G, LookBack lb,
                       std::uint32_t* __restrict__ orank, std::uint64_t* __restrict__ otot,
                       unsigned long long* epoch, unsigned long long* clear2) {
+  pdl_wait();
   __shared__ std::uint32_t wcnt[kRankThreads / 32][kMaxRanks];
   __shared__ std::uint32_t base[kMaxRanks];
   __shared__ std::uint64_t s_tile;
@@ -176,6 +179,7 @@ __global__ void p2p_send_keys_kernel(P2PCtx ctx, int G, int me, std::uint64_t sl
                                      const std::uint32_t* __restrict__ orank,
                                      const std::uint64_t* __restrict__ otot,
                                      unsigned* done_ctr) {
+  pdl_wait();
   const std::uint64_t epoch = ctx.round();
   const PeerWindows& pw = ctx.cur(epoch);
   const std::uint64_t U = *u_ptr;
@@ -205,6 +209,7 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
                                       std::uint32_t* __restrict__ rslots, int E,
                                       unsigned* done_ctr, unsigned long long* served,
                                       DevError* err) {
+  pdl_wait();
   const std::uint64_t epoch = ctx.round();
   const PeerWindows& pw = ctx.cur(epoch);
   const std::uint64_t* my_keys = pw.keys[me];
@@ -255,6 +260,7 @@ __global__ void p2p_send_deltas_kernel(P2PCtx ctx, int G, int me, std::uint64_t 
                                        const std::uint32_t* __restrict__ orank,
                                        const float* __restrict__ deltas, int E,
                                        unsigned* done_ctr) {
+  pdl_wait();
   const std::uint64_t epoch = ctx.round();
   const PeerWindows& pw = ctx.cur(epoch);
   const int tpk = E / VEC;
@@ -283,6 +289,7 @@ template <int VEC>
 __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
                                  const std::uint32_t* __restrict__ rslots,
                                  float* __restrict__ tvals, int E) {
+  pdl_wait();
   const PeerWindows& pw = ctx.cur(ctx.round());
   const std::uint64_t* my_hdr = pw.hdr[me];
   const float* my_deltas = pw.deltas[me];
@@ -315,6 +322,7 @@ __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
 __global__ void p2p_dense_update_kernel(P2PCtx ctx, int G, int me, int nodes, int devices,
                                         std::uint64_t nw, float* __restrict__ w, float lr,
                                         int apply, float* __restrict__ sum_out, DevError* err) {
+  pdl_wait();
   __shared__ int ok;
   const std::uint64_t epoch = ctx.round();
   if (threadIdx.x == 0) ok = 1;
@@ -354,6 +362,7 @@ __global__ void p2p_dense_update_kernel(P2PCtx ctx, int G, int me, int nodes, in
 // window, region `me`.
 __global__ void p2p_send_dense_kernel(P2PCtx ctx, int G, int me, std::uint64_t nw,
                                       const float* __restrict__ grad, unsigned* done_ctr) {
+  pdl_wait();
   const std::uint64_t epoch = ctx.round();
   const PeerWindows& pw = ctx.cur(epoch);
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < nw * G;

@@ -131,6 +131,7 @@ __device__ __forceinline__ std::uint64_t look_back(const LookBack& lb, std::uint
 __global__ void __launch_bounds__(kSortThreads)
     onesweep_hist_kernel(const std::uint64_t* __restrict__ keys, Count cnt_n, int passes,
                          std::uint32_t mod_G, std::uint32_t* __restrict__ hist) {
+  pdl_wait();
   __shared__ std::uint32_t h[kMaxPasses * kDigits];
   const int np = passes ? passes : 1;
   for (int i = threadIdx.x; i < np * kDigits; i += kSortThreads) h[i] = 0;
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kSortThreads)
 
 // In-place exclusive scan of each pass's 256 counts (one CTA per pass).
 __global__ void __launch_bounds__(kDigits) onesweep_scan_kernel(std::uint32_t* __restrict__ hist) {
+  pdl_wait();
   __shared__ std::uint32_t ws[kDigits / 32];
   std::uint32_t* h = hist + blockIdx.x * kDigits;
   const std::uint32_t v = h[threadIdx.x];
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(kSortThreads)
                          const std::uint32_t* __restrict__ vin, Count cnt_n, Digit dig,
                          const std::uint32_t* __restrict__ digit_base, LookBack lb,
                          std::uint64_t* __restrict__ kout, std::uint32_t* __restrict__ vout) {
+  pdl_wait();
   __shared__ std::uint32_t wcnt[kSortWarps][kDigits];
   __shared__ std::uint32_t gbase[kDigits];
   __shared__ std::uint64_t s_tile;
@@ -263,6 +266,7 @@ constexpr int kScanTile = kSortThreads * kScanItems;  // 4096
 template <class F, class Em>
 __global__ void __launch_bounds__(kSortThreads)
     scan_lookback_kernel(F f, Em em, Count cnt_n, LookBack lb, std::uint64_t* __restrict__ total) {
+  pdl_wait();
   __shared__ std::uint32_t ws[kSortWarps];
   __shared__ std::uint64_t s_tile, s_pre;
   if (threadIdx.x == 0) s_tile = atomicAdd(lb.ticket, 1ull) - lb.base;

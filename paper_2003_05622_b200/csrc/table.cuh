@@ -25,6 +25,7 @@ namespace hpsgpu {
 __global__ void table_clear_kernel(std::uint64_t* __restrict__ keys,
                                    const std::uint64_t* __restrict__ cap_ptr,
                                    const unsigned* __restrict__ only_if = nullptr) {
+  pdl_wait();
   if (only_if && *only_if == 0u) return;  // conditional pass (graph-stable)
   const std::uint64_t cap = *cap_ptr;
   for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
@@ -34,6 +35,7 @@ __global__ void table_clear_kernel(std::uint64_t* __restrict__ keys,
 
 __global__ void table_capacity_kernel(const std::uint64_t* __restrict__ n_ptr,
                                       std::uint64_t* __restrict__ cap_ptr) {
+  pdl_wait();
   *cap_ptr = table_capacity(*n_ptr);
 }
 
@@ -43,6 +45,7 @@ __global__ void table_insert_kernel(const std::uint64_t* __restrict__ ws,
                                     std::uint64_t* __restrict__ keys,
                                     const std::uint64_t* __restrict__ cap_ptr,
                                     DevError* err) {
+  pdl_wait();
   const std::uint64_t n = *n_ptr, cap = *cap_ptr;
   for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        i < n; i += std::uint64_t(gridDim.x) * blockDim.x) {
@@ -98,6 +101,7 @@ __global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys
                                           DevError* err, unsigned long long* __restrict__ n_new,
                                           unsigned* __restrict__ spec_fail,
                                           const unsigned* __restrict__ only_if) {
+  pdl_wait();
   if (only_if && *only_if == 0u) return;
   const std::uint64_t O = std::uint64_t(*o_ptr), cap = *cap_ptr;
   unsigned long long placed = 0;
@@ -152,6 +156,7 @@ __global__ void table_spec_check_kernel(unsigned long long* __restrict__ n,
                                         std::uint64_t* __restrict__ cap,
                                         unsigned* __restrict__ spec_fail,
                                         unsigned* __restrict__ redo) {
+  pdl_wait();
   const std::uint64_t needed = table_capacity(*n);
   if (*spec_fail || needed != *cap) {
     *redo = 1u;
@@ -166,6 +171,7 @@ __global__ void table_spec_check_kernel(unsigned long long* __restrict__ n,
 // The capacity guess of the speculative build: the previous table's.
 __global__ void table_guess_kernel(const std::uint64_t* __restrict__ prev_cap,
                                    std::uint64_t fallback, std::uint64_t* __restrict__ cap) {
+  pdl_wait();
   *cap = prev_cap ? *prev_cap : fallback;
 }
 
@@ -193,6 +199,7 @@ __global__ void table_prefetch_probe_kernel(
     const std::uint64_t* __restrict__ old2_cap_ptr, bool from_store, std::uint64_t store_keys, int E, std::uint64_t* __restrict__ need_key,
     std::uint32_t* __restrict__ need_slot, unsigned long long* __restrict__ n_need,
     unsigned long long* carried) {
+  pdl_wait();
   const std::uint64_t n = *n_ptr;
   const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
   const std::uint64_t ocap = old_cap_ptr ? *old_cap_ptr : 0;
@@ -259,6 +266,7 @@ __global__ void store_gather_kernel(const std::uint64_t* __restrict__ need_key,
                                     const unsigned long long* __restrict__ n_need,
                                     const float* __restrict__ store, float* __restrict__ vals,
                                     int E) {
+  pdl_wait();
   using V = typename std::conditional<VEC == 4, float4, float>::type;
   const int tpk = E / VEC;
   const std::uint64_t total = std::uint64_t(*n_need) * tpk;
@@ -293,6 +301,7 @@ __global__ void table_carry_kernel(const std::uint32_t* __restrict__ csrc,
                                    const float* __restrict__ p1_vals,
                                    const float* __restrict__ p2_vals, float* __restrict__ vals,
                                    int E) {
+  pdl_wait();
   const int tpk = E / VEC;
   const std::uint64_t n = *n_ptr;
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
@@ -333,6 +342,7 @@ __global__ void table_evict_filter_kernel(const std::uint64_t* __restrict__ ws,
                                           std::uint32_t* __restrict__ out_slot,
                                           unsigned long long* __restrict__ n_out,
                                           unsigned long long* __restrict__ total) {
+  pdl_wait();
   const std::uint64_t n = *n_ptr;
   const std::uint64_t cap1 = c1 ? *c1 : 0, cap2 = c2 ? *c2 : 0, cap3 = c3 ? *c3 : 0;
   const unsigned lane = threadIdx.x & 31;
@@ -373,6 +383,7 @@ __global__ void store_scatter_kernel(const std::uint64_t* __restrict__ keys,
                                      const unsigned long long* __restrict__ n_ptr,
                                      const float* __restrict__ vals, float* __restrict__ store,
                                      int E) {
+  pdl_wait();
   using V = typename std::conditional<VEC == 4, float4, float>::type;
   const int tpk = E / VEC;
   const std::uint64_t total = std::uint64_t(*n_ptr) * tpk;
@@ -414,6 +425,7 @@ __global__ void table_fill_kernel(
     const float* __restrict__ staged_rows,
     const float* __restrict__ store, std::uint64_t store_keys, int E,
     unsigned long long* carried, DevError* err) {
+  pdl_wait();
   const int tpk = E / VEC;
   const std::uint64_t n = *n_ptr, cap = *cap_ptr;
   const std::uint64_t pcap = prev_cap_ptr ? *prev_cap_ptr : 0;
@@ -461,6 +473,7 @@ __global__ void table_gather_kernel(const std::uint64_t* __restrict__ qkeys,
                                     float* __restrict__ out_rows,
                                     std::uint32_t* __restrict__ out_slots,
                                     int E, DevError* err) {
+  pdl_wait();
   const int tpk = E / VEC;
   const std::uint64_t n = n_ptr ? *n_ptr : n_host;
   const std::uint64_t cap = *cap_ptr;
@@ -500,6 +513,7 @@ __global__ void table_apply_kernel(const std::uint32_t* __restrict__ slots,
                                    const std::uint64_t* __restrict__ n_ptr,
                                    std::uint64_t n_host, float* __restrict__ vals,
                                    int E, DevError* err) {
+  pdl_wait();
   const int tpk = E / VEC;
   const std::uint64_t n = n_ptr ? *n_ptr : n_host;
   const std::uint64_t total = n * std::uint64_t(tpk);
@@ -546,6 +560,7 @@ __global__ void table_dump_kernel(const std::uint64_t* __restrict__ ws,
                                   float* __restrict__ store, std::uint64_t store_keys,
                                   float* __restrict__ out_rows, int E,
                                   DevError* err) {
+  pdl_wait();
   const int tpk = E / VEC;
   const std::uint64_t n = *n_ptr, cap = *cap_ptr;
   const std::uint64_t total = n * std::uint64_t(tpk);

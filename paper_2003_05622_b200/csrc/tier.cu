@@ -456,20 +456,32 @@ static void debug_sync(K* k, cudaStream_t s) {
   }
 }
 
-template <class... KArgs, class... Args>
-static void launch(Tier* t, void (*k)(KArgs...), dim3 grid, dim3 block,
-                   size_t smem, Args&&... args) {
-  k<<<grid, block, smem, t->L->st>>>(std::forward<Args>(args)...);
-  ++t->launches;
-  debug_sync(k, t->L->st);
-}
+bool pdl_enabled();
 
+// Every launch allows programmatic dependent launch (see pdl_wait): the
+// kernel's blocks may start as the predecessor's last ones drain.
 template <class... KArgs, class... Args>
 static void launch_on(Tier* t, cudaStream_t s, void (*k)(KArgs...), dim3 grid, dim3 block,
                       size_t smem, Args&&... args) {
-  k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
   ++t->launches;
   debug_sync(k, s);
+}
+
+template <class... KArgs, class... Args>
+static void launch(Tier* t, void (*k)(KArgs...), dim3 grid, dim3 block,
+                   size_t smem, Args&&... args) {
+  launch_on(t, t->L->st, k, grid, block, smem, std::forward<Args>(args)...);
 }
 
 
@@ -532,6 +544,7 @@ static hps_status device_error_status(Tier* t, const DevError& e, const char* mi
 // ------------------------------------------------------ small kernels ----
 
 __global__ void iota_kernel(std::uint32_t* v, std::uint64_t n) {
+  pdl_wait();
   for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        i < n; i += std::uint64_t(gridDim.x) * blockDim.x)
     v[i] = std::uint32_t(i);
@@ -545,6 +558,7 @@ __global__ void batch_count_kernel(const std::int64_t* __restrict__ off,
                                    std::uint64_t key_space,
                                    std::uint64_t* __restrict__ counts,
                                    DevError* err) {
+  pdl_wait();
   __shared__ unsigned long long c[66];
   for (int i = threadIdx.x; i <= J; i += blockDim.x) c[i] = 0;
   __syncthreads();
@@ -578,6 +592,7 @@ __global__ void shard_gather_kernel(ShardMap sm, const std::int64_t* __restrict_
                                     std::uint64_t* __restrict__ kout,
                                     std::uint32_t* __restrict__ vout,
                                     std::uint32_t* __restrict__ ex_of) {
+  pdl_wait();
   const unsigned lane = threadIdx.x & 31;
   const std::uint64_t w0 = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const std::uint64_t nw = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -599,6 +614,7 @@ __global__ void scatter_rows_kernel(const std::uint32_t* __restrict__ inv,
                                     std::uint64_t n, int E,
                                     const float* __restrict__ rows,
                                     float* __restrict__ out) {
+  pdl_wait();
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        t < n * E; t += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint64_t i = t / E;
@@ -615,6 +631,7 @@ __global__ void permute_rows_kernel(const std::uint32_t* __restrict__ inv,
                                     std::uint64_t n, int E,
                                     const float* __restrict__ in,
                                     float* __restrict__ out) {
+  pdl_wait();
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
        t < n * E; t += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint64_t i = t / E;
@@ -709,6 +726,7 @@ struct UniqueEmit {  // inverse index + CSR segments of a sorted (key, occ) list
 // --------------------------------------------------- sort / scan drivers
 
 __global__ void context_open_kernel(std::uint32_t* context, unsigned long long* ticket) {
+  pdl_wait();
   *context += 1;
   *ticket = 0;
 }
@@ -1979,6 +1997,14 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
 using namespace hpsgpu;
 
 struct hps_tier : public hpsgpu::Tier {};
+
+bool hpsgpu::pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("HPS_PDL");
+    return !v || std::atoi(v) != 0;
+  }();
+  return on;
+}
 
 bool hpsgpu::debug_sync_enabled() {
   static const bool on = [] {
