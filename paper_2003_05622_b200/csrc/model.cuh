@@ -100,8 +100,15 @@ __global__ void __launch_bounds__(128)
         const int d = d0 + sub;
         double acc = 0.0;
         // the row ids of 8 rounds (8 x LPE features) load at once, then rounds
-        // go in pairs: 2 x LPE independent row loads in flight per lane before
-        // the in-order f64 adds
+        // go in groups of kInFlight: kInFlight x LPE independent row loads in
+        // flight per lane before the in-order f64 adds. Two: more registers
+        // would cost resident blocks and push a mini-batch past one wave
+        // (measured: 3 or 4 rounds run slower on c2)
+#ifdef HPS_FB_ROUNDS
+        constexpr int kInFlight = HPS_FB_ROUNDS;
+#else
+        constexpr int kInFlight = 2;
+#endif
         constexpr int kIdRounds = 8;
         for (std::uint32_t base = o0; base < o1; base += kIdRounds * LPE) {
           std::uint32_t ids[kIdRounds];
@@ -111,26 +118,26 @@ __global__ void __launch_bounds__(128)
             ids[t] = p < o1 ? occ_row[p] : 0u;
           }
 #pragma unroll
-          for (int t = 0; t < kIdRounds; t += 2) {
+          for (int t = 0; t < kIdRounds; t += kInFlight) {
             const std::uint32_t c = base + t * LPE;
             if (c >= o1) break;
-            const int len0 = int(o1 - c < std::uint32_t(LPE) ? o1 - c : LPE);
-            const std::uint32_t c1 = c + LPE;
-            const int len1 = c1 < o1 ? int(o1 - c1 < std::uint32_t(LPE) ? o1 - c1 : LPE) : 0;
-            float v0[LPE], v1[LPE];
+            int len[kInFlight];
+            float v[kInFlight][LPE];
 #pragma unroll
-            for (int r = 0; r < LPE; ++r) {
-              const std::uint32_t r0 = __shfl_sync(gmask, ids[t], r, LPE);
-              const std::uint32_t r1 = __shfl_sync(gmask, ids[t + 1], r, LPE);
-              v0[r] = (r < len0 && d < E) ? rows[std::uint64_t(r0) * E + d] : 0.0f;
-              v1[r] = (r < len1 && d < E) ? rows[std::uint64_t(r1) * E + d] : 0.0f;
+            for (int q = 0; q < kInFlight; ++q) {
+              const std::uint32_t cq = c + q * LPE;
+              len[q] = cq < o1 ? int(o1 - cq < std::uint32_t(LPE) ? o1 - cq : LPE) : 0;
+#pragma unroll
+              for (int r = 0; r < LPE; ++r) {
+                const std::uint32_t rid = __shfl_sync(gmask, ids[t + q], r, LPE);
+                v[q][r] = (r < len[q] && d < E) ? rows[std::uint64_t(rid) * E + d] : 0.0f;
+              }
             }
 #pragma unroll
-            for (int r = 0; r < LPE; ++r)
-              if (r < len0) acc = __dadd_rn(acc, double(v0[r]));
+            for (int q = 0; q < kInFlight; ++q)
 #pragma unroll
-            for (int r = 0; r < LPE; ++r)
-              if (r < len1) acc = __dadd_rn(acc, double(v1[r]));
+              for (int r = 0; r < LPE; ++r)
+                if (r < len[q]) acc = __dadd_rn(acc, double(v[q][r]));
           }
         }
         if (d < E) hrec[d] = acc;
@@ -508,8 +515,33 @@ inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw 
 //
 // Short segments (<= kLongSeg) are summed exactly in order by
 // sparse_short_kernel; longer ones (hot Zipf keys: up to the whole shard) are
-// queued for the chunked, certified big_fused_kernel.
+// listed by big_classify_kernel for the chunked, certified big_fused_kernel.
+// The two paths write disjoint keys and run side by side.
 constexpr int kLongSeg = 32;
+
+// The keys whose segment is longer than kLongSeg -> big_list. It reads the
+// grouping only, so it runs beside fwd/bwd on the big path's stream.
+__global__ void __launch_bounds__(256)
+    big_classify_kernel(const std::uint64_t* __restrict__ u_ptr,
+                        const std::uint32_t* __restrict__ seg, std::uint32_t* __restrict__ big_list,
+                        unsigned long long* __restrict__ n_big) {
+  pdl_wait();
+  const std::uint64_t U = *u_ptr;
+  const unsigned lane = threadIdx.x & 31;
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  // whole warps iterate together (warp-aggregated appends)
+  for (std::uint64_t b = std::uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); b < U;
+       b += stride) {
+    const std::uint64_t u = b + lane;
+    const bool big = u < U && seg[u + 1] - seg[u] > std::uint32_t(kLongSeg);
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, big);
+    if (!m) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(n_big, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (big) big_list[base + __popc(m & ((1u << lane) - 1))] = std::uint32_t(u);
+  }
+}
 
 // Where a key's sgd_delta goes: the push row (pos[u], or u), or — one rank,
 // the key's slot known (apply_slot) — straight into the table row:
@@ -539,18 +571,14 @@ __device__ __forceinline__ void write_delta(const DeltaOut& o, std::uint64_t u, 
 // Short segments, exact: one thread per (unique key, DPT dims) sums the key's
 // occurrences in example order; its DPT dimension chains are independent
 // (DPT-wide row loads, DPT adds in flight), each in the reference order.
-// Longer segments are queued for the chunked CTA path.
+// Longer segments belong to the chunked CTA path (big_classify_kernel).
 template <int DPT>
 __global__ void __launch_bounds__(256)
     sparse_short_kernel(int E, float lr, std::uint64_t n, const std::uint64_t* __restrict__ u_ptr,
                         const std::uint32_t* __restrict__ seg,
                         const std::uint32_t* __restrict__ exs, DeltaOut dout,
                         const double* __restrict__ DX,
-                        unsigned long long* __restrict__ pulled,
-                        std::uint32_t* __restrict__ long_list,
-                        unsigned long long* __restrict__ n_long,
-                        std::uint32_t* __restrict__ big_list,
-                        unsigned long long* __restrict__ n_big, std::uint32_t medium_max) {
+                        unsigned long long* __restrict__ pulled) {
   pdl_wait();
   const std::uint64_t U = *u_ptr;
   if (pulled && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(pulled, (unsigned long long)U);
@@ -562,15 +590,7 @@ __global__ void __launch_bounds__(256)
     const std::uint64_t u = t / std::uint64_t(parts);
     const int d0 = int(t - u * parts) * DPT;
     const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
-    if (p1 - p0 > std::uint32_t(kLongSeg)) {
-      if (d0 == 0) {
-        if (p1 - p0 > medium_max)
-          big_list[atomicAdd(n_big, 1ull)] = std::uint32_t(u);
-        else
-          long_list[atomicAdd(n_long, 1ull)] = std::uint32_t(u);
-      }
-      continue;
-    }
+    if (p1 - p0 > std::uint32_t(kLongSeg)) continue;
     double acc[DPT];
 #pragma unroll
     for (int i = 0; i < DPT; ++i) acc[i] = 0.0;

@@ -226,6 +226,8 @@ struct Tier {
   cudaStream_t st = nullptr;            // == lane[0].st: bodies and the parity API
   cudaStream_t st2 = nullptr;           // side stream: dense-grad overlaps sparse reduce
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t st3 = nullptr;           // side stream: the big-segment path (classify, plan,
+  cudaEvent_t fork3 = nullptr, join3 = nullptr;  // fused reduce) beside fwd/bwd + short path
   Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
                                         // 2..: the next batch's mini-batch groupings
   GroupState gs[kGroupLanes];           // [0]: the prep's grouping, [1]: the body's
@@ -301,7 +303,7 @@ struct Tier {
                 *seg = nullptr, *uidv = nullptr, *pos = nullptr,
                 *slots = nullptr,
                 *exs = nullptr,
-                *long_list = nullptr, *big_list = nullptr, *chunk_off = nullptr,
+                *big_list = nullptr, *chunk_off = nullptr,
                 *orank = nullptr,
                 *key_done = nullptr;
   ChunkSum* chunk_tot = nullptr;
@@ -352,6 +354,7 @@ struct Tier {
   // per batch to stderr at completion (diagnostics)
   bool trace = false;
   bool priorities = true;
+  bool big_side = true;                 // big-segment path on st3 (HPS_BIG_SIDE=0: on st)
   int zc_threads = 1024;  // CTA size of the zero-copy kernels
   cudaEvent_t tr_base = nullptr;
   cudaEvent_t tr[kSlots][6] = {};   // by staging slot: stage0 stage1 prep0 prep1 body0 body1
@@ -1072,10 +1075,28 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
 // Segment-length routing of the sparse reduce: <= kLongSeg in-order by one
 // thread per (key, 4 dims), longer ones split into fuse_chunk(E)-occurrence
 // chunks over CTAs (big_fused_kernel).
-constexpr int kMediumMax = kLongSeg;  // medium path off: chunks serve every long key
+//
+// The big-segment path's preparation, on st3 beside fwd/bwd: list the keys
+// with segments over kLongSeg (big_classify_kernel), plan their (key, chunk)
+// items, reset the fused kernel's flags and ticket.
+static hps_status launch_big_plan(Tier* t, std::uint64_t u_upper, const std::uint64_t* U,
+                                  const std::uint32_t* seg) {
+  unsigned long long* nb = &t->dsc->n_big;
+  cudaStream_t bs = t->big_side ? t->st3 : t->st;
+  HPS_CUDA(cudaMemsetAsync(nb, 0, 8, bs));
+  launch_on(t, bs, big_classify_kernel, grid_for(std::max<std::uint64_t>(u_upper, 1)), 256, 0,
+            U, seg, t->big_list, nb);
+  launch_on(t, bs, big_plan_kernel, 1, 1024, 0, fuse_chunk(t->E),
+            (const std::uint32_t*)t->big_list, (const unsigned long long*)nb, seg, t->chunk_off,
+            &t->dsc->n_items, t->item_key, t->item_chunk);
+  HPS_CUDA(cudaMemsetAsync(t->fuse_flags, 0, t->fuse_items * 4, bs));
+  HPS_CUDA(cudaMemsetAsync(t->fuse_ticket, 0, 8, bs));
+  return HPS_OK;
+}
 
-// Sparse segment-reduce launches: LPK lanes per short segment (pow2 >= E,
-// 4..32), then one CTA per long segment.
+// The sparse segment-reduce: short segments on the body stream, big ones
+// (planned by launch_big_plan) in one fused pass over CTAs on st3 (ticket
+// order). The caller forks st3 after fwd/bwd and joins it (join3).
 static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint32_t* pos,
                                       std::uint64_t u_upper, const std::uint64_t* U,
                                       const std::uint32_t* seg, const std::uint32_t* exs,
@@ -1087,29 +1108,19 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   if (E > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
   const float lr = t->cfg.learning_rate;
   const double* DX = t->DX;
-  unsigned long long* pulled = &t->dsc->pulled;
-  unsigned long long* nl = &t->dsc->n_long;
-  unsigned long long* nb = &t->dsc->n_big;
-  if (t->G == 1) HPS_CUDA(cudaMemsetAsync(nl, 0, 16, t->st));  // G > 1: owner_rank_kernel
+  cudaStream_t bs = t->big_side ? t->st3 : t->st;
+  launch_on(t, bs, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
+            (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big,
+            (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
+            (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs, dout,
+            DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, &t->dsc->fallbacks);
+  HPS_CUDA(cudaEventRecord(t->join3, bs));
   // DPT dims per thread (4 when E allows 32-byte row loads)
   const int dpt = (E % 4 == 0) ? 4 : 1;
   auto sk = dpt == 4 ? sparse_short_kernel<4> : sparse_short_kernel<1>;
   launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,
-         E, lr, n, U, seg, exs, dout, DX, pulled, t->long_list, nl, t->big_list, nb,
-         std::uint32_t(kMediumMax));
-  // big segments: plan (key, chunk) items, then one fused pass over CTAs
-  // (ticket order; flags and ticket reset per launch)
-  const int chunk = fuse_chunk(E);
-  launch(t, big_plan_kernel, 1, 1024, 0, chunk, (const std::uint32_t*)t->big_list,
-         (const unsigned long long*)nb, seg, t->chunk_off, &t->dsc->n_items, t->item_key,
-         t->item_chunk);
-  HPS_CUDA(cudaMemsetAsync(t->fuse_flags, 0, t->fuse_items * 4, t->L->st));
-  HPS_CUDA(cudaMemsetAsync(t->fuse_ticket, 0, 8, t->L->st));
-  launch(t, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
-         (const std::uint32_t*)t->big_list, (const unsigned long long*)nb,
-         (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
-         (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs, dout, DX,
-         t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, &t->dsc->fallbacks);
+         E, lr, n, U, seg, exs, dout, DX, &t->dsc->pulled);
+  HPS_CUDA(cudaStreamWaitEvent(t->st, t->join3, 0));
   return HPS_OK;
 }
 
@@ -1506,6 +1517,12 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     }
     // compute (a7, a8, a9); rows are in uid order (or table slots) at every G
     if (n) {
+      // the big-segment plan beside fwd/bwd (st3)
+      if (T->big_side) {
+        HPS_CUDA(cudaEventRecord(T->fork3, T->st));
+        HPS_CUDA(cudaStreamWaitEvent(T->st3, T->fork3, 0));
+      }
+      HPS_TRY(launch_big_plan(T, ob, Uj, segj));
       const int LPE = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
       const int epb = 128 / LPE;
       const size_t smem = size_t((T->md.nw + 1) & ~1) * 4 +
@@ -1531,6 +1548,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                 n, (const double*)T->H, (const double*)T->DL, (const double*)T->dpart,
                 (const double*)T->dg_tot, T->dgrad, &T->dsc->fallbacks);
       HPS_CUDA(cudaEventRecord(T->join, T->st2));
+      if (T->big_side) HPS_CUDA(cudaStreamWaitEvent(T->st3, T->fork, 0));  // after fwd/bwd
       HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob, Uj, segj, exsj,
                                   bp.grouped && G == 1 ? slotsj : nullptr));
       mark(T, HPS_T_SPARSE);
@@ -2078,6 +2096,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_PREP_GROUP"))
     t->prep_mbs = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_BIG_SIDE")) t->big_side = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
   {
@@ -2134,6 +2153,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     };
     str(&t->st, hi);
     str(&t->st2, hi);
+    str(&t->st3, hi);
     str(&t->lane[1].st, lo);
     for (int gl = 0; gl < kGroupLanes; ++gl) str(&t->lane[2 + gl].st, lo);
     str(&t->st_stage, lo);
@@ -2141,6 +2161,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     str(&t->st_pf, lo);
     ev(&t->fork, false);
     ev(&t->join, false);
+    ev(&t->fork3, false);
+    ev(&t->join3, false);
     ev(&t->ev_staged, false);
     ev(&t->ev_prep, false);
     ev(&t->pf_fork, false);
@@ -2287,7 +2309,6 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
       return fail(s);
   }
   A(otot, kMaxRanks);
-  A(long_list, S);
   A(big_list, S / (kLongSeg + 1) + 2);
   A(chunk_off, S / (kLongSeg + 1) + 3);
   A(key_done, S / (kLongSeg + 1) + 2);
@@ -2345,7 +2366,7 @@ hps_status hps_destroy(hps_tier_t t) {
   if (!t) return HPS_OK;
   cudaSetDevice(t->cfg.cuda_device);
   if (t->dsc) quiesce(t);  // in-flight batches, then every resident row to the store
-  for (cudaStream_t x : {t->st, t->lane[1].st, t->st_stage, t->st_wb, t->st2, t->st_pf})
+  for (cudaStream_t x : {t->st, t->lane[1].st, t->st_stage, t->st_wb, t->st2, t->st3, t->st_pf})
     if (x) cudaStreamSynchronize(x);
   for (int gl = 0; gl < kGroupLanes; ++gl)
     if (t->lane[2 + gl].st) cudaStreamSynchronize(t->lane[2 + gl].st);
@@ -2363,6 +2384,8 @@ hps_status hps_destroy(hps_tier_t t) {
   for (auto& ev : t->evpool) cudaEventDestroy(ev);
   if (t->fork) cudaEventDestroy(t->fork);
   if (t->join) cudaEventDestroy(t->join);
+  if (t->fork3) cudaEventDestroy(t->fork3);
+  if (t->join3) cudaEventDestroy(t->join3);
   for (int p = 0; p < kTables; ++p) {
     for (cudaEvent_t x : {t->ev_wb[p], t->ev_body_tab[p], t->ev_wbt[p][0], t->ev_wbt[p][1]})
       if (x) cudaEventDestroy(x);
@@ -2383,6 +2406,7 @@ hps_status hps_destroy(hps_tier_t t) {
   for (int gl = 0; gl < kGroupLanes; ++gl)
     if (t->lane[2 + gl].st) cudaStreamDestroy(t->lane[2 + gl].st);
   if (t->st2) cudaStreamDestroy(t->st2);
+  if (t->st3) cudaStreamDestroy(t->st3);
   if (t->st) cudaStreamDestroy(t->st);
   delete t;
   return HPS_OK;
