@@ -411,7 +411,8 @@ def run_ours(args, rank, world, local_rank):
     dom = rl.get(dominant, {})
     names = {"sparse": "sparse segment-reduce + sgd_delta" + (" + in-place apply" if fused_apply
                                                               else "") +
-                       " (sparse_short_kernel, big_plan_kernel, big_fused_kernel), per mini-batch",
+                       " (sparse_short_kernel; big_classify_kernel, big_plan_kernel, big_fused_kernel"
+                       " on a side stream), per mini-batch",
              "pull": "table_gather_kernel<4>", "apply": "table_apply_kernel<4>"}
     models = {"sparse": "O*(8E+4) + U*(8+8E)" if fused_apply else "O*(8E+4) + U*(8+4E)",
               "pull": "U*(8+8+8E)", "apply": "U*(4+12E)"}
