@@ -89,12 +89,50 @@ __global__ void table_insert_kernel(const std::uint64_t* __restrict__ ws,
 //    key order (table_prefetch_probe / store_gather / table_carry) and
 //    written back in key order (table_writeback_sorted).
 
+// Ordered insert of one key (atomicMin, the larger key carried on); true if
+// it claimed an EMPTY slot. A table that fills up sets *spec_fail
+// (speculative pass) or raises.
+__device__ __forceinline__ bool insert_ordered(std::uint64_t cur, std::uint64_t* tkeys,
+                                               std::uint64_t cap, unsigned* spec_fail,
+                                               DevError* err) {
+  const std::uint64_t key = cur;
+  std::uint64_t idx = mix64(cur) & (cap - 1);
+  for (std::uint64_t probes = 0;; ++probes) {
+    // slots only ever decrease: a read that shows cur (present) or a smaller
+    // key (advance) decides exactly what the atomic would; hot keys then
+    // cost plain cached loads instead of serialised atomics
+    const std::uint64_t seen = *reinterpret_cast<volatile const std::uint64_t*>(tkeys + idx);
+    if (seen == cur) return false;
+    if (seen > cur) {
+      const std::uint64_t old = atomicMin(reinterpret_cast<unsigned long long*>(tkeys + idx),
+                                          static_cast<unsigned long long>(cur));
+      if (old == kEmptyKey) return true;  // placed
+      if (old == cur) return false;       // already present
+      if (old > cur) cur = old;           // displaced: carry the larger key
+    }
+    idx = (idx + 1) & (cap - 1);
+    if (probes > cap) {
+      if (spec_fail) *spec_fail = 1u;
+      else raise_error(err, 4, key);
+      return false;
+    }
+  }
+}
+
 // Counts the distinct keys as it goes (every occupied slot is claimed from
 // EMPTY exactly once, duplicates and displaced keys included) into *n_new.
 // Speculative pass (spec_fail non-null): a table that fills up sets
 // *spec_fail instead of raising. only_if non-null: run only if *only_if.
-__global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys,
-                                          const std::int64_t* __restrict__ o_ptr,
+//
+// Position-major, like group_probe_kernel: warp w takes examples
+// 32*(w / kInsertPosGroups) + lane at feature positions w % kInsertPosGroups
+// (mod kInsertPosGroups). Sorted features put a hot key at the same position
+// in most examples, so __match_any_sync leaves one lane per distinct key of
+// the warp to insert it (a set insert is idempotent) instead of a burst of
+// same-address atomics.
+constexpr int kInsertPosGroups = 32;
+__global__ void table_insert_dedup_kernel(const std::int64_t* __restrict__ off, std::uint64_t B,
+                                          const std::uint64_t* __restrict__ keys,
                                           std::uint64_t G, std::uint64_t g,
                                           std::uint64_t* __restrict__ tkeys,
                                           const std::uint64_t* __restrict__ cap_ptr,
@@ -103,50 +141,44 @@ __global__ void table_insert_dedup_kernel(const std::uint64_t* __restrict__ keys
                                           const unsigned* __restrict__ only_if) {
   pdl_wait();
   if (only_if && *only_if == 0u) return;
-  const std::uint64_t O = std::uint64_t(*o_ptr), cap = *cap_ptr;
+  const std::uint64_t cap = *cap_ptr;
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const std::uint64_t nw = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
   unsigned long long placed = 0;
-  for (std::uint64_t q = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; q < O;
-       q += std::uint64_t(gridDim.x) * blockDim.x) {
-    std::uint64_t cur = keys[q];
-    if (cur % G != g) continue;
-    if (cur == kEmptyKey) {
-      raise_error(err, 1, cur);
-      continue;
+  for (std::uint64_t w = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5;
+       (w / kInsertPosGroups) * 32 < B; w += nw) {
+    const int pg = int(w % kInsertPosGroups);
+    const std::uint64_t ex = (w / kInsertPosGroups) * 32 + lane;
+    std::int64_t b = 0, len = 0;
+    if (ex < B) {
+      b = off[ex];
+      len = off[ex + 1] - b;
     }
-    std::uint64_t idx = mix64(cur) & (cap - 1);
-    for (std::uint64_t probes = 0;; ++probes) {
-      // slots only ever decrease: a read that shows cur (present) or a smaller
-      // key (advance) decides exactly what the atomic would; hot keys then
-      // cost plain cached loads instead of serialised atomics
-      const std::uint64_t seen = *reinterpret_cast<volatile const std::uint64_t*>(tkeys + idx);
-      if (seen == cur) break;
-      if (seen < cur) {
-        idx = (idx + 1) & (cap - 1);
-        if (probes > cap) {
-          if (spec_fail) *spec_fail = 1u;
-          else raise_error(err, 4, cur);
-          break;
+    std::int64_t maxlen = len;
+    for (int o = 16; o > 0; o >>= 1) {
+      const std::int64_t y = __shfl_xor_sync(0xFFFFFFFFu, maxlen, o);
+      maxlen = y > maxlen ? y : maxlen;
+    }
+    for (std::int64_t p = pg; p < maxlen; p += kInsertPosGroups) {
+      std::uint64_t cur = kEmptyKey;
+      bool act = p < len;
+      if (act) {
+        cur = keys[b + p];
+        if (cur % G != g) {  // another rank's key
+          act = false;
+          cur = kEmptyKey;
+        } else if (cur == kEmptyKey) {
+          raise_error(err, 1, cur);
+          act = false;
         }
-        continue;
       }
-      const std::uint64_t old = atomicMin(reinterpret_cast<unsigned long long*>(tkeys + idx),
-                                          static_cast<unsigned long long>(cur));
-      if (old == kEmptyKey) {  // placed
-        ++placed;
-        break;
-      }
-      if (old == cur) break;       // already present
-      if (old > cur) cur = old;    // displaced: carry the larger key
-      idx = (idx + 1) & (cap - 1);
-      if (probes > cap) {
-        if (spec_fail) *spec_fail = 1u;
-        else raise_error(err, 4, cur);
-        break;
-      }
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, static_cast<unsigned long long>(cur));
+      if (act && (peers & lt) == 0u && insert_ordered(cur, tkeys, cap, spec_fail, err)) ++placed;
     }
   }
   for (int o = 16; o > 0; o >>= 1) placed += __shfl_xor_sync(0xFFFFFFFFu, placed, o);
-  if ((threadIdx.x & 31) == 0 && placed && n_new) atomicAdd(n_new, placed);
+  if (lane == 0 && placed && n_new) atomicAdd(n_new, placed);
 }
 
 // After the speculative insert: if the count asks for another capacity (or

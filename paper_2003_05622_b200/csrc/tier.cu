@@ -354,7 +354,8 @@ struct Tier {
   // per batch to stderr at completion (diagnostics)
   bool trace = false;
   bool priorities = true;
-  bool big_side = true;                 // big-segment path on st3 (HPS_BIG_SIDE=0: on st)
+  bool big_side = true;
+  int ws_sort = -1;  // prep sorts the working set by key: 1/0 (HPS_WS_SORT), -1 = for a host store                 // big-segment path on st3 (HPS_BIG_SIDE=0: on st)
   int zc_threads = 1024;  // CTA size of the zero-copy kernels
   cudaEvent_t tr_base = nullptr;
   cudaEvent_t tr[kSlots][6] = {};   // by staging slot: stage0 stage1 prep0 prep1 body0 body1
@@ -1300,6 +1301,9 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
   return HPS_OK;
 }
 
+// Whether the prep sorts the working set by key (Tier::ws_sort).
+static bool ws_sorted(const Tier* T) { return T->ws_sort < 0 ? T->store_on_host : T->ws_sort != 0; }
+
 // Prep of one batch (lane 1, beside the previous batch's body): the sort-free
 // build of its table. Exact distinct count through a scratch set (it fixes
 // the capacity, hence the layout), ordered probing of the raw owned
@@ -1313,7 +1317,6 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   const int G = T->G, E = T->E, tb = bp.tb;
   Lane& l = *T->L;
   const std::uint64_t* dkeys = T->b_keys[bp.sp];
-  const std::int64_t* o_ptr = T->b_off[bp.sp] + sh.B;
   std::uint64_t* nws = &T->dsc->nws_tab[tb];
   std::uint64_t* cap = &T->dsc->cap[tb];
   mark(T, -1);
@@ -1331,16 +1334,17 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
          std::min(cap_bound, T->capmax), cap);  // (the shape bound may exceed the buffers)
   launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[tb],
          (const std::uint64_t*)cap, (const unsigned*)nullptr);
-  launch(T, table_insert_dedup_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G),
-         std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap, &T->dsc->err,
-         (unsigned long long*)nws, &T->dsc->spec_fail, (const unsigned*)nullptr);
+  launch(T, table_insert_dedup_kernel, gk, 256, 0, (const std::int64_t*)T->b_off[bp.sp], sh.B,
+         dkeys, std::uint64_t(G), std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap,
+         &T->dsc->err, (unsigned long long*)nws, &T->dsc->spec_fail, (const unsigned*)nullptr);
   launch(T, table_spec_check_kernel, 1, 1, 0, (unsigned long long*)nws, cap, &T->dsc->spec_fail,
          &T->dsc->redo);
   launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[tb],
          (const std::uint64_t*)cap, (const unsigned*)&T->dsc->redo);
-  launch(T, table_insert_dedup_kernel, gk, 256, 0, dkeys, o_ptr, std::uint64_t(G),
-         std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap, &T->dsc->err,
-         (unsigned long long*)nws, (unsigned*)nullptr, (const unsigned*)&T->dsc->redo);
+  launch(T, table_insert_dedup_kernel, gk, 256, 0, (const std::int64_t*)T->b_off[bp.sp], sh.B,
+         dkeys, std::uint64_t(G), std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap,
+         &T->dsc->err, (unsigned long long*)nws, (unsigned*)nullptr,
+         (const unsigned*)&T->dsc->redo);
   // the table's keys are final: the mini-batches' grouping forks onto lane 2
   // and runs beside the rest of the build (joined at the end of the prep)
   if (bp.grouped) {
@@ -1360,13 +1364,19 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
     HPS_TRY(st);
     HPS_CUDA(cudaEventRecord(T->gs[0].join, ln.st));
   }
-  // the distinct keys with their slots, ascending: compact the live slots,
-  // sort them (n_ws items, ~3x fewer than the occurrences)
+  // the distinct keys with their slots: compact the live slots (slot order),
+  // then sort them by key (n_ws items, ~3x fewer than the occurrences) when
+  // the value store is in host memory. Key order is not needed for results
+  // (row sources, store lists and write-back are per key; hps_dump sorts on
+  // demand), but it keeps the zero-copy store gather and write-back walking
+  // host memory in address order: unsorted, e2e at c2 fell from 12.7M to
+  // 8.2M ex/s, while an HBM store gains 5% without the sort.
   tile_scan(T, LiveSlot{T->tkeys[tb]}, CompactEmit{T->tkeys[tb], nullptr, l.kB, l.vB},
             Count{cap, 0}, cap_bound, &l.d->total);
-  std::uint64_t* sk = nullptr;
-  std::uint32_t* so = nullptr;
-  radix_sort(T, l.kB, l.vB, Count{nws, 0}, sh.own_bound, T->sort_bits, true, &sk, &so);
+  std::uint64_t* sk = l.kB;
+  std::uint32_t* so = l.vB;
+  if (ws_sorted(T))
+    radix_sort(T, l.kB, l.vB, Count{nws, 0}, sh.own_bound, T->sort_bits, true, &sk, &so);
   const std::uint64_t wcopy = std::min(sh.own_bound, T->Wmax);  // bound, within the buffers
   HPS_CUDA(cudaMemcpyAsync(T->wsb[tb], sk, wcopy * 8, cudaMemcpyDeviceToDevice, l.st));
   HPS_CUDA(cudaMemcpyAsync(T->wsib[tb], so, wcopy * 4, cudaMemcpyDeviceToDevice, l.st));
@@ -1956,7 +1966,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   T->cur = bp.tb;
   T->ws = T->wsb[bp.tb];
   T->ws_idx = T->wsib[bp.tb];
-  T->ws_sorted = true;
+  T->ws_sorted = ws_sorted(T);
   if (T->use_graphs && bp.skip_mb < 0) {
     std::vector<std::uint64_t> key = {2, B, sh.own_bound, std::uint64_t(bp.tb),
                                       std::uint64_t(bp.tp + 1), std::uint64_t(bp.tq + 1),
@@ -2097,6 +2107,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     t->prep_mbs = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_BIG_SIDE")) t->big_side = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_WS_SORT")) t->ws_sort = std::atoi(v) != 0 ? 1 : 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
   {
@@ -2626,7 +2637,10 @@ hps_status hps_table_slots(hps_tier_t t, uint64_t* slot_keys, float* rows) {
 hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t* n_out) {
   std::uint64_t occ = 0, cap = 0;
   HPS_TRY(hps_table_info(t, &cap, &occ, nullptr));
-  if (!t->ws_sorted) {  // after hps_train_batch: the sorted key list from the table itself
+  // the working set in key order: t->ws when the build sorted it, else sorted
+  // here from the table itself into scratch (t->ws stays paired with ws_idx)
+  const std::uint64_t* wsk = t->ws;
+  if (!t->ws_sorted) {
     open_lookback_context(t);
     tile_scan(t, LiveSlot{t->tkeys[t->cur]},
               CompactEmit{t->tkeys[t->cur], nullptr, t->lane[0].kB, nullptr}, Count{nullptr, cap}, cap,
@@ -2634,24 +2648,22 @@ hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t*
     std::uint64_t* sk = nullptr;
     std::uint32_t* so = nullptr;
     radix_sort(t, t->lane[0].kB, nullptr, Count{nullptr, occ}, occ, t->sort_bits, false, &sk, &so);
-    HPS_CUDA(cudaMemcpyAsync(t->ws, sk, occ * 8, cudaMemcpyDeviceToDevice, t->st));
-    t->ws_sorted = true;
+    wsk = sk;
   }
-  // The working set of the current table is still in t->ws (sorted).
   const int V = vec_of(t->E);
   const std::uint64_t work = occ * std::uint64_t(t->E / V);
   if (occ) {
     if (V == 4)
-      launch(t, table_dump_kernel<4>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
+      launch(t, table_dump_kernel<4>, grid_for(work), 256, 0, wsk,
              (const std::uint64_t*)&t->dsc->nws_tab[t->cur], (const std::uint64_t*)t->tkeys[t->cur],
              (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
              (float*)nullptr, std::uint64_t(0), t->rows, t->E, &t->dsc->err);
     else
-      launch(t, table_dump_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
+      launch(t, table_dump_kernel<1>, grid_for(work), 256, 0, wsk,
              (const std::uint64_t*)&t->dsc->nws_tab[t->cur], (const std::uint64_t*)t->tkeys[t->cur],
              (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
              (float*)nullptr, std::uint64_t(0), t->rows, t->E, &t->dsc->err);
-    if (keys_out) HPS_CUDA(cudaMemcpyAsync(keys_out, t->ws, occ * 8, cudaMemcpyDeviceToHost, t->st));
+    if (keys_out) HPS_CUDA(cudaMemcpyAsync(keys_out, wsk, occ * 8, cudaMemcpyDeviceToHost, t->st));
     if (rows_out)
       HPS_CUDA(cudaMemcpyAsync(rows_out, t->rows, occ * std::uint64_t(t->E) * 4,
                                cudaMemcpyDeviceToHost, t->st));
