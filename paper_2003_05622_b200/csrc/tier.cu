@@ -2140,6 +2140,12 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     m.hw = hw;
     m.dw = dw;
     m.maxw = maxw;
+    // the order-free embed_sum bound (model.cuh embed_sum_exact): 29 is the
+    // exactness limit; HPS_EMBED_SLACK may only tighten it (tests use it to
+    // force the in-order fallback for part of a batch)
+    m.exact_slack = 29;
+    if (const char* v = std::getenv("HPS_EMBED_SLACK"))
+      m.exact_slack = std::max(-1, std::min(29, std::atoi(v)));
   }
 
   auto fail = [&](hps_status s) {

@@ -292,3 +292,17 @@ def test_hbm_store_grouping_split_bit_exact(pkg, oracle, monkeypatch, J, prep_gr
     wd, wk, wr = oracle.train_reference(make_cfg(1, 1, 8, (8, 16, 1), J=J), B, off, keys, lab)
     assert np.array_equal(dense, wd)
     assert np.array_equal(store[wk.astype(np.int64)], wr)
+
+
+@pytest.mark.parametrize("slack", ["-1", "8", "29"])
+@pytest.mark.parametrize("E,nnz", [(8, 20), (16, 100)])
+def test_embed_sum_order_free_and_fallback_bit_exact(pkg, oracle, monkeypatch, slack, E, nnz):
+    """fwd/bwd's embed_sum takes the order-free path (whole rows per lane,
+    recursive halving) only where the f64 sum is exact in any order
+    (model.cuh embed_sum_exact); HPS_EMBED_SLACK tightens the bound so the
+    in-order fallback runs for all (-1) or part (8) of the examples, mixed
+    within one mini-batch, against the same oracle."""
+    monkeypatch.setenv("HPS_EMBED_SLACK", slack)
+    dims, B = 30000, 512
+    off, keys, lab = pkg.gen_dataset(dims, B * 3, nnz, zipf=True, seed=11)
+    check_bit_exact(oracle, pkg, off, keys, lab, B, E=E, layers=(8, 16, 1), J=4, dims=dims)
