@@ -194,6 +194,30 @@ def reference_arm(args, rank):
 
 # ------------------------------------------------------------------- ours --
 
+NVLINK_GBS = 900.0  # NVLink 5 per GPU per direction (spec; not measured on this pool)
+
+
+def remote_unique_keys(batches, D, J):
+    """Unique keys per (device, mini-batch) shard whose owner is another rank,
+    summed over shards and over the batch pool: what the key/row/delta
+    all-to-alls carry. Shards follow shard_batch (sharding.hpp:29-42): example
+    i -> device (i % (D*J)) / J, mini-batch (i % (D*J)) % J; owner key % D
+    (topology.hpp:61-65)."""
+    import numpy as np
+    total = 0
+    S = D * J
+    for o, k, _ in batches:
+        nex = o.size - 1
+        ex = np.repeat(np.arange(nex, dtype=np.uint64), np.diff(o).astype(np.int64))
+        shard = ex % np.uint64(S)
+        ku = k.view(np.uint64)
+        u = np.sort(ku * np.uint64(S) + shard)
+        u = u[np.concatenate(([True], u[1:] != u[:-1]))]
+        ukey, ush = u // np.uint64(S), u % np.uint64(S)
+        total += int(np.count_nonzero(ukey % np.uint64(D) != ush // np.uint64(J)))
+    return float(total)
+
+
 def ph_steps_frac(args):
     """Work counters of the value pass rescaled to the phase-timing pass."""
     return max(10, args.steps // 4) / args.steps
@@ -423,6 +447,24 @@ def run_ours(args, rank, world, local_rank):
                 "launches_per_step": J if dominant in ("sparse", "pull", "apply") else 1,
                 "phases": rl}
 
+    # ---------------- NVLink roofline of the key/row/delta all-to-alls (N>1) --
+    nvlink = None
+    if world > 1:
+        remote = remote_unique_keys(batches, world, J) / P   # per step, all ranks
+        xfer_ms = max_over_ranks(phases.get("pull", 0.0) + phases.get("apply", 0.0)) / K
+        per_gpu = remote * (8 + 4 * E + 4 * E) / world        # sent by one GPU per step
+        if xfer_ms > 0:
+            gbs = per_gpu / (xfer_ms / 1e3) / 1e9
+            nvlink = {"bound": "nvlink", "achieved": gbs, "peak": NVLINK_GBS, "unit": "GB/s",
+                      "frac": gbs / NVLINK_GBS, "peak_kind": "spec (NVLink 5, per GPU per "
+                      "direction)", "bytes_model": "remote unique keys x (8 key + 4E row + 4E "
+                      "delta) / N, per GPU per direction",
+                      "remote_keys_per_step": remote, "bytes_per_gpu_per_step": per_gpu,
+                      "ms_per_step": xfer_ms,
+                      "phases": "pull (key a2a, owner probe+gather, row a2a) + apply (delta "
+                                "a2a, canonical apply): the time includes the owner-side work "
+                                "and the flag waits, so the link rate is a lower bound"}
+
     # ---------------- CPU baseline (reference hot path, rank 0, N=1) ---------
     cpu = None
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
@@ -457,6 +499,7 @@ def run_ours(args, rank, world, local_rank):
                               "overlaps b+1), one event region ending in hps_flush")},
             "e2e": e2e,
             "roofline": roofline,
+            "nvlink": nvlink,
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": all_launch,

@@ -42,7 +42,9 @@ typedef enum {
   HPS_ERR_KEY_RANGE = 8,     /* pipeline.hpp:367-371 ingest range check */
   HPS_ERR_CUDA = 9,
   HPS_ERR_NCCL = 10,
-  HPS_ERR_CAPACITY = 11      /* a batch larger than the configured maxima */
+  HPS_ERR_CAPACITY = 11,     /* a batch larger than the configured maxima */
+  HPS_ERR_CORRUPT = 12       /* a parameter file failed validation
+                                (hps::CorruptionError, ssd_ps.hpp:495-520) */
 } hps_status;
 
 typedef struct hps_tier* hps_tier_t;
@@ -253,6 +255,46 @@ hps_status hps_kernel_launches(hps_tier_t h, uint64_t* n);
 
 /* The CUDA stream the handle launches on (cudaStream_t as void*). */
 hps_status hps_stream(hps_tier_t h, void** stream);
+
+/* ------------------------------- parameter files (SSD-PS on-disk format) */
+
+/* Trained tables leave the tier in the reference's parameter-file format
+ * (ssd_ps.hpp:50-56: "HPSF" | version 1 | record_count u16 | width u16 |
+ * reserved u16, then record_count x (key u64 | E f32 embedding | E f32
+ * opt_state), then the zlib CRC-32 of header + records), so the reference
+ * SsdStore recovers, loads, fscks and stats them unchanged (SURVEY §8(f)
+ * row 3). Host-only; no GPU needed. */
+
+/* CRC-32 as zlib's crc32(crc, data, n) (the footer checksum). */
+uint32_t hps_crc32(uint32_t crc, const void* data, uint64_t n);
+
+/* SsdStore::dump (ssd_ps.hpp:229-243) + write_chunk (420-450): the n
+ * records (keys strictly ascending, the std::map order) as
+ * ceil(n / file_capacity) files dir/pf_<first_id + i>.bin, each written to a
+ * temporary name and renamed. opt_state NULL writes zeros (SparseParam(width),
+ * types.hpp:36). *files_out = files written. Errors: file_capacity outside
+ * [1, 65535] and n == 0 use the reference's messages (ssd_ps.hpp:159-160,
+ * 227). */
+hps_status hps_pfile_write(const char* dir, const uint64_t* keys,
+                           const float* rows, const float* opt_state,
+                           uint64_t n, uint32_t width, uint32_t file_capacity,
+                           uint64_t first_id, uint64_t* files_out);
+
+/* SsdStore::read_file_at (ssd_ps.hpp:495-535): one file, validated (magic,
+ * version, width vs *width_out when it is non-zero, size, CRC) with the
+ * reference's messages (HPS_ERR_CORRUPT). keys/rows/opt_state all NULL is a
+ * sizing call (sets *n_out, *width_out). */
+hps_status hps_pfile_read(const char* path, uint64_t* keys, float* rows,
+                          float* opt_state, uint64_t cap, uint64_t* n_out,
+                          uint32_t* width_out);
+
+/* HbmTier::dump_node (hbm_ps.hpp:224-232) of this rank's table, written as
+ * parameter files (the MEM-PS collect -> SSD-PS dump path, mem_ps.hpp:
+ * 210-245): hps_dump + hps_pfile_write with zero opt_state. Ranks hold
+ * disjoint keys, so every rank can export into one directory with disjoint
+ * id ranges. */
+hps_status hps_export(hps_tier_t h, const char* dir, uint32_t file_capacity,
+                      uint64_t first_id, uint64_t* files_out);
 
 /* -------------------------------------------------- synthetic inputs */
 

@@ -261,6 +261,15 @@ class HbmTier {
     return out;
   }
 
+  // dump_node written as reference parameter files pf_<first_id + i>.bin
+  // (ssd_ps.hpp:50-56) that SsdStore recovers unchanged. Returns the count.
+  std::uint64_t export_files(const std::string& dir, std::uint32_t file_capacity = 4096,
+                             std::uint64_t first_id = 0) {
+    std::uint64_t files = 0;
+    check(hps_export(h_, dir.c_str(), file_capacity, first_id, &files));
+    return files;
+  }
+
   // SyncSession::run (hbm_ps.hpp:303-310). COLLECTIVE.
   void synchronize(std::vector<float>& buf, bool deterministic) {
     check(hps_dense_sync(h_, buf.data(), buf.size(), deterministic ? 1 : 0));

@@ -32,6 +32,7 @@
 #include "hps/oracle.hpp"
 #include "hps/pipeline.hpp"
 #include "hps/sharding.hpp"
+#include "hps/ssd_ps.hpp"
 #include "hps/topology.hpp"
 #include "hps/transport.hpp"
 
@@ -427,6 +428,69 @@ int ref_hot_path_export(void* p, float* dense_out, std::uint64_t* n_sparse_out,
     std::copy(w.begin(), w.end(), dense_out);
     export_sparse(h->store, h->rc.embedding_dim, n_sparse_out, sparse_keys_out,
                   sparse_rows_out, sparse_cap);
+  });
+}
+
+// ---- parameter files: the reference SsdStore itself (ssd_ps.hpp) ----------
+
+// SsdStore::dump of (key, emb, opt) records into a fresh directory: the
+// reference's own bytes, to compare ours against.
+int ref_store_dump(const char* dir, std::uint64_t width, std::uint64_t file_capacity,
+                   const std::uint64_t* keys, const float* emb, const float* opt,
+                   std::uint64_t n) {
+  return guarded([&] {
+    StoreConfig sc;
+    sc.dir = dir;
+    sc.embedding_dim = width;
+    sc.file_capacity = file_capacity;
+    sc.background_compaction = false;
+    SsdStore st(sc);
+    std::map<ParamKey, SparseParam> m;
+    for (std::uint64_t i = 0; i < n; ++i) {
+      SparseParam p(width);
+      std::copy(emb + i * width, emb + (i + 1) * width, p.embedding.begin());
+      if (opt) std::copy(opt + i * width, opt + (i + 1) * width, p.opt_state.begin());
+      m.emplace(keys[i], std::move(p));
+    }
+    st.dump(m);
+  });
+}
+
+// SsdStore recover + load of every key + fsck + stats on an existing
+// directory (width 0 = inferred from the files). Records come back in key
+// order. info[0..5] = files, live_records, stale_records, fsck ok,
+// fsck files_scanned, recovered_invalid_files.
+int ref_store_load_all(const char* dir, std::uint64_t width, std::uint64_t* keys, float* emb,
+                       float* opt, std::uint64_t cap, std::uint64_t* n_out,
+                       std::uint64_t* info) {
+  return guarded([&] {
+    StoreConfig sc;
+    sc.dir = dir;
+    sc.embedding_dim = width;
+    sc.background_compaction = false;
+    SsdStore st(sc);
+    auto all = st.all_keys();
+    std::sort(all.begin(), all.end());
+    check(all.size() <= cap, "ref_store_load_all: cap");
+    const auto res = st.load(all);
+    check(res.missing.empty(), "ref_store_load_all: missing keys");
+    const std::size_t w = st.embedding_dim();
+    std::uint64_t i = 0;
+    for (const auto& [k, p] : res.found) {
+      keys[i] = k;
+      std::copy(p.embedding.begin(), p.embedding.end(), emb + i * w);
+      std::copy(p.opt_state.begin(), p.opt_state.end(), opt + i * w);
+      ++i;
+    }
+    *n_out = i;
+    const auto s = st.stats();
+    const auto f = st.fsck();
+    info[0] = s.files;
+    info[1] = s.live_records;
+    info[2] = s.stale_records;
+    info[3] = f.ok ? 1 : 0;
+    info[4] = f.files_scanned;
+    info[5] = s.recovered_invalid_files;
   });
 }
 

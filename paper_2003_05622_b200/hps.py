@@ -29,7 +29,7 @@ STATUS = {
     0: "HPS_OK", 1: "HPS_ERR_ARG", 2: "HPS_ERR_MISSING_KEY", 3: "HPS_ERR_DUPLICATE",
     4: "HPS_ERR_OVERFLOW", 5: "HPS_ERR_NONFINITE", 6: "HPS_ERR_NOT_BUILT",
     7: "HPS_ERR_WIDTH", 8: "HPS_ERR_KEY_RANGE", 9: "HPS_ERR_CUDA", 10: "HPS_ERR_NCCL",
-    11: "HPS_ERR_CAPACITY",
+    11: "HPS_ERR_CAPACITY", 12: "HPS_ERR_CORRUPT",
 }
 
 
@@ -116,6 +116,12 @@ _SIGS = {
     "hps_kernel_launches": ([_P, _U64P], ctypes.c_int),
     "hps_set_graphs": ([_P, ctypes.c_int], ctypes.c_int),
     "hps_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
+    "hps_crc32": ([ctypes.c_uint32, _P, _U64], ctypes.c_uint32),
+    "hps_pfile_write": ([ctypes.c_char_p, _P, _P, _P, _U64, ctypes.c_uint32, ctypes.c_uint32,
+                         _U64, _U64P], ctypes.c_int),
+    "hps_pfile_read": ([ctypes.c_char_p, _P, _P, _P, _U64, _U64P,
+                        ctypes.POINTER(ctypes.c_uint32)], ctypes.c_int),
+    "hps_export": ([_P, ctypes.c_char_p, ctypes.c_uint32, _U64, _U64P], ctypes.c_int),
     "hps_gen_dataset": ([_U64, _U64, _U64, ctypes.c_int, ctypes.c_double, _U64,
                          ctypes.c_double, _U64, _P, _P, _P], ctypes.c_int),
 }
@@ -158,6 +164,39 @@ def _f32(a) -> np.ndarray:
 
 
 # --------------------------------------------------------------- dataset ----
+
+def crc32(data: bytes, crc: int = 0) -> int:
+    """zlib-compatible CRC-32 (the parameter-file footer, ssd_ps.hpp:516)."""
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    return int(lib().hps_crc32(crc, _ptr(buf), buf.size))
+
+
+def write_param_files(directory: str, keys, rows, opt_state=None, file_capacity: int = 4096,
+                      first_id: int = 0) -> int:
+    """SsdStore::dump (ssd_ps.hpp:229-243) format: ascending keys written as
+    pf_<first_id + i>.bin files of file_capacity records. Returns the file count."""
+    k = _u64(keys)
+    r = _f32(rows).reshape(k.size, -1) if k.size else np.empty((0, 1), np.float32)
+    o = None if opt_state is None else _f32(opt_state).reshape(r.shape)
+    nf = ctypes.c_uint64()
+    _check(lib().hps_pfile_write(os.fsencode(directory), _ptr(k), _ptr(r),
+                                 _ptr(o) if o is not None else None, k.size, r.shape[1],
+                                 file_capacity, first_id, ctypes.byref(nf)))
+    return nf.value
+
+
+def read_param_file(path: str, width: int = 0):
+    """SsdStore::read_file_at (ssd_ps.hpp:495-535): validated (keys, emb, opt_state)."""
+    n, w = ctypes.c_uint64(), ctypes.c_uint32(width)
+    p = os.fsencode(path)
+    _check(lib().hps_pfile_read(p, None, None, None, 0, ctypes.byref(n), ctypes.byref(w)))
+    keys = np.empty(n.value, np.uint64)
+    emb = np.empty((n.value, w.value), np.float32)
+    opt = np.empty((n.value, w.value), np.float32)
+    _check(lib().hps_pfile_read(p, _ptr(keys), _ptr(emb), _ptr(opt), n.value,
+                                ctypes.byref(n), ctypes.byref(w)))
+    return keys, emb, opt
+
 
 def gen_dataset(dims: int, num_examples: int, nnz: int, zipf: bool = False,
                 zipf_s: float = 1.0, seed: int = 1, signal_scale: float = 6.0,
@@ -301,6 +340,13 @@ class Tier:
         n = ctypes.c_uint64()
         _check(lib().hps_dump(self._h, _ptr(keys), _ptr(rows), ctypes.byref(n)))
         return keys[: n.value], rows[: n.value]
+
+    def export(self, directory: str, file_capacity: int = 4096, first_id: int = 0) -> int:
+        """hps_export: this rank's table as reference parameter files."""
+        nf = ctypes.c_uint64()
+        _check(lib().hps_export(self._h, os.fsencode(directory), file_capacity, first_id,
+                                ctypes.byref(nf)))
+        return nf.value
 
     def dense_sync(self, buf, deterministic: bool = True) -> np.ndarray:
         b = _f32(buf).copy()

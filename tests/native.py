@@ -203,7 +203,35 @@ class RefLib:
         L.ref_hot_path_run.argtypes = [_P, ctypes.c_size_t, ctypes.c_size_t,
                                        ctypes.POINTER(ctypes.c_double)]
         L.ref_hot_path_export.argtypes = [_P, _P, ctypes.POINTER(_U64), _P, _P, _U64]
+        L.ref_store_dump.argtypes = [ctypes.c_char_p, _U64, _U64, _P, _P, _P, _U64]
+        L.ref_store_load_all.argtypes = [ctypes.c_char_p, _U64, _P, _P, _P, _U64,
+                                         ctypes.POINTER(_U64), _P]
         self.L = L
+
+    def store_dump(self, directory, keys, emb, opt=None, file_capacity=4096):
+        """The reference SsdStore::dump into `directory` (ssd_ps.hpp:229-243)."""
+        k = np.ascontiguousarray(keys, np.uint64)
+        e = np.ascontiguousarray(emb, np.float32)
+        o = None if opt is None else np.ascontiguousarray(opt, np.float32)
+        self._ok(self.L.ref_store_dump(os.fsencode(directory), e.shape[1], file_capacity,
+                                       ptr(k), ptr(e), ptr(o) if o is not None else None,
+                                       k.size))
+
+    def store_load_all(self, directory, width, cap, infer_width=False):
+        """The reference SsdStore recover + load(all keys) + stats + fsck
+        (infer_width: the store reads the width from the files)."""
+        keys = np.empty(max(cap, 1), np.uint64)
+        emb = np.empty((max(cap, 1), width), np.float32)
+        opt = np.empty((max(cap, 1), width), np.float32)
+        n = _U64()
+        info = np.zeros(6, np.uint64)
+        self._ok(self.L.ref_store_load_all(os.fsencode(directory), 0 if infer_width else width,
+                                           ptr(keys), ptr(emb),
+                                           ptr(opt), cap, ctypes.byref(n), ptr(info)))
+        m = n.value
+        return keys[:m], emb[:m], opt[:m], dict(zip(
+            ["files", "live_records", "stale_records", "fsck_ok", "fsck_files",
+             "recovered_invalid"], (int(v) for v in info)))
 
     def err(self) -> str:
         return self.L.ref_last_error().decode()

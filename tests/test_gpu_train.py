@@ -178,6 +178,37 @@ def test_dump_after_sort_free_build(pkg, oracle):
     tier.close()
 
 
+def test_export_trained_table_as_reference_parameter_files(pkg, oracle, tmp_path):
+    """hps_export: the trained table leaves as SSD-PS parameter files
+    (ssd_ps.hpp:50-56) that the unmodified reference SsdStore recovers, loads
+    and fscks, holding exactly train_reference's rows for the last batch's
+    keys (bit-exact) and zero opt_state (plain SGD leaves it untouched,
+    model.hpp:204)."""
+    from native import RefLib
+    ref = RefLib()
+    dims, B, nnz, E, layers, J = 50000, 1024, 30, 16, (8, 16, 1), 4
+    off, keys, lab = pkg.gen_dataset(dims, 3 * B, nnz, zipf=True, seed=12)
+    tier = pkg.Tier(width=E, layer_dims=layers, minibatches=J, key_space=dims,
+                    max_batch_examples=B, max_batch_keys=B * nnz)
+    store = np.zeros((dims, E), dtype=np.float32)
+    tier.attach_store(store)
+    for b in range(3):
+        tier.train_batch(off[b * B:(b + 1) * B + 1] - off[b * B],
+                         keys[off[b * B]:off[(b + 1) * B]], lab[b * B:(b + 1) * B])
+    nf = tier.export(str(tmp_path), file_capacity=1000, first_id=7)
+    tier.flush()
+    tier.close()
+    want = np.unique(keys[off[2 * B]:off[3 * B]])
+    assert nf == -(-want.size // 1000)
+    k, e, o, info = ref.store_load_all(str(tmp_path), E, want.size)
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, layers, J=J), B, off, keys, lab)
+    assert np.array_equal(k, want)
+    rows = dict(zip(wk.tolist(), wr))
+    assert e.tobytes() == np.stack([rows[int(x)] for x in k]).tobytes()
+    assert not o.any()
+    assert info["fsck_ok"] == 1 and info["files"] == nf and info["live_records"] == want.size
+
+
 @pytest.mark.parametrize("store_kind", ["host", "device", "none"])
 def test_pipelined_submit_wait_bit_exact(pkg, oracle, store_kind):
     """hps_submit_batch / hps_wait_batch keep two batches in flight: the next
