@@ -76,20 +76,30 @@ __device__ __forceinline__ void signal_peers(const PeerWindows& pw, int G, int m
 }
 
 // Waits until every source raised `phase` to the current round in this
-// rank's flags.
+// rank's flags: threads < G poll one source each (bounded: a dead peer
+// raises an error instead of hanging), then the whole CTA proceeds. Every
+// thread of the block must call it.
+__device__ __forceinline__ void wait_sources(const P2PCtx& ctx, int G, int me, int phase,
+                                             DevError* err) {
+  if (threadIdx.x < unsigned(G)) {
+    const std::uint64_t epoch = ctx.round();
+    const std::uint64_t* f = ctx.par[0].flags[me] + threadIdx.x * kPhases + phase;
+    long long spins = 0;
+    while (ld_acquire_sys(f) < epoch) {
+      if (++spins > (1ll << 27)) {  // ~10 s: a peer died; fail instead of hanging
+        raise_error(err, 10 /*HPS_ERR_NCCL*/, std::uint64_t(threadIdx.x));
+        break;
+      }
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __global__ void p2p_wait_kernel(P2PCtx ctx, int G, int me, int phase, DevError* err) {
   pdl_wait();
-  if (threadIdx.x >= unsigned(G)) return;
-  const std::uint64_t epoch = ctx.round();
-  const std::uint64_t* f = ctx.par[0].flags[me] + threadIdx.x * kPhases + phase;
-  long long spins = 0;
-  while (ld_acquire_sys(f) < epoch) {
-    if (++spins > (1ll << 27)) {  // ~10 s: a peer died; fail instead of hanging
-      raise_error(err, 10 /*HPS_ERR_NCCL*/, std::uint64_t(threadIdx.x));
-      return;
-    }
-    __nanosleep(64);
-  }
+  wait_sources(ctx, G, me, phase, err);
 }
 
 // Owner ranks of the sorted unique keys: orank[u] = number of earlier unique
@@ -208,8 +218,9 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
                                       const std::uint64_t* __restrict__ cap_ptr,
                                       std::uint32_t* __restrict__ rslots, int E,
                                       unsigned* done_ctr, unsigned long long* served,
-                                      DevError* err) {
+                                      DevError* err, int wait_phase) {
   pdl_wait();
+  if (wait_phase >= 0) wait_sources(ctx, G, me, wait_phase, err);  // the requests arrived
   const std::uint64_t epoch = ctx.round();
   const PeerWindows& pw = ctx.cur(epoch);
   const std::uint64_t* my_keys = pw.keys[me];
@@ -288,8 +299,10 @@ __global__ void p2p_send_deltas_kernel(P2PCtx ctx, int G, int me, std::uint64_t 
 template <int VEC>
 __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
                                  const std::uint32_t* __restrict__ rslots,
-                                 float* __restrict__ tvals, int E) {
+                                 float* __restrict__ tvals, int E, int G, int wait_phase,
+                                 DevError* err) {
   pdl_wait();
+  if (wait_phase >= 0) wait_sources(ctx, G, me, wait_phase, err);  // the deltas arrived
   const PeerWindows& pw = ctx.cur(ctx.round());
   const std::uint64_t* my_hdr = pw.hdr[me];
   const float* my_deltas = pw.deltas[me];

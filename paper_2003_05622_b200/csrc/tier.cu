@@ -355,6 +355,7 @@ struct Tier {
   bool trace = false;
   bool priorities = true;
   bool big_side = true;
+  bool fold_wait = true;  // the exchange waits inside the consuming kernel (HPS_FOLD_WAIT=0: own launch)
   int ws_sort = -1;  // prep sorts the working set by key: 1/0 (HPS_WS_SORT), -1 = for a host store                 // big-segment path on st3 (HPS_BIG_SIDE=0: on st)
   int zc_threads = 1024;  // CTA size of the zero-copy kernels
   cudaEvent_t tr_base = nullptr;
@@ -1006,20 +1007,18 @@ static hps_status exchange_pull(Tier* t, std::uint64_t n, bool do_gather) {
   launch(t, p2p_send_keys_kernel, grid_for(n, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
          (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
          (const std::uint32_t*)t->orank, (const std::uint64_t*)t->otot, t->done_ctr);
-  p2p_wait(t, kPhKeys);
+  // the keys wait is folded into serve_rows (each CTA polls the flags) unless
+  // there is no gather or HPS_FOLD_WAIT=0
+  const bool fold = do_gather && t->fold_wait;
+  if (!fold) p2p_wait(t, kPhKeys);
   mark(t, HPS_T_DEDUP);
   if (do_gather) {
     const std::uint64_t work = t->Omax * std::uint64_t(t->E / V);
-    if (V == 4)
-      launch(t, p2p_serve_rows_kernel<4>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
-             (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
-             (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->done_ctr,
-             &t->dsc->served, &t->dsc->err);
-    else
-      launch(t, p2p_serve_rows_kernel<1>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
-             (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
-             (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->done_ctr,
-             &t->dsc->served, &t->dsc->err);
+    auto k = V == 4 ? p2p_serve_rows_kernel<4> : p2p_serve_rows_kernel<1>;
+    launch(t, k, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
+           (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
+           (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->done_ctr,
+           &t->dsc->served, &t->dsc->err, fold ? int(kPhKeys) : -1);
     p2p_wait(t, kPhRows);
     mark(t, HPS_T_PULL);
   }
@@ -1040,16 +1039,14 @@ static hps_status push_apply(Tier* t) {
     launch(t, p2p_send_deltas_kernel<1>, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G,
            t->g, t->slot, (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
            (const std::uint32_t*)t->orank, (const float*)t->deltas, t->E, t->done_ctr);
-  p2p_wait(t, kPhDeltas);
+  if (!t->fold_wait) p2p_wait(t, kPhDeltas);
+  bool first = t->fold_wait;  // the first apply waits for every source's deltas
+  auto k = V == 4 ? p2p_apply_kernel<4> : p2p_apply_kernel<1>;
   for (int src : canonical_senders(t)) {
-    if (V == 4)
-      launch(t, p2p_apply_kernel<4>, grid_for(t->slot * std::uint64_t(t->E / V), 256, kSMs * 2), 256, 0,
-             t->ctx, t->g, src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur],
-             t->E);
-    else
-      launch(t, p2p_apply_kernel<1>, grid_for(t->slot * std::uint64_t(t->E / V), 256, kSMs * 2), 256, 0,
-             t->ctx, t->g, src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur],
-             t->E);
+    launch(t, k, grid_for(t->slot * std::uint64_t(t->E / V), 256, kSMs * 2), 256, 0, t->ctx, t->g,
+           src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur], t->E, t->G,
+           first ? int(kPhDeltas) : -1, &t->dsc->err);
+    first = false;
   }
   return HPS_OK;
 }
@@ -2107,6 +2104,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     t->prep_mbs = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_BIG_SIDE")) t->big_side = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_FOLD_WAIT")) t->fold_wait = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_WS_SORT")) t->ws_sort = std::atoi(v) != 0 ? 1 : 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
