@@ -35,6 +35,7 @@ struct PeerWindows {
   float* dense[kMaxRanks];           // peer's dense window base
   float* rows[kMaxRanks];            // peer's requester row buffer
   std::uint64_t* flags[kMaxRanks];   // peer's flag array
+  int cta_sys_fence;                 // 1: every CTA fences at system scope (HPS_CTA_FENCE=sys)
 };
 
 // Both parity copies of every rank's windows plus the device-resident round
@@ -60,12 +61,21 @@ __device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) 
 }
 
 // Called by every CTA after its P2P stores; the last CTA to finish raises
-// this rank's flag for `phase` in every peer.
+// this rank's flag for `phase` in every peer. Each CTA releases its stores
+// to the done counter at GPU scope; the last CTA acquires them through the
+// counter, and its system-scope fence (cumulative over what it observed)
+// plus the st.release.sys flag publish every CTA's stores to the peers. A
+// system fence in every CTA (HPS_CTA_FENCE=sys, the earlier scheme) costs
+// ≈ 6 µs more per phase (tools/p2p_phase_probe.cu: 3.2 MB at the G = 2
+// interleave, 22.2 -> 16.4 µs per round).
 __device__ __forceinline__ void signal_peers(const PeerWindows& pw, int G, int me, int phase,
                                              std::uint64_t epoch, unsigned* done_ctr) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (pw.cta_sys_fence)
+      __threadfence_system();
+    else
+      __threadfence();
     const unsigned prev = atomicAdd(done_ctr, 1u);
     if (prev == gridDim.x * gridDim.y - 1) {
       *done_ctr = 0;

@@ -1209,6 +1209,11 @@ static hps_status setup_p2p(Tier* t, std::uint64_t S) {
       w.rows[p] = reinterpret_cast<float*>(base + o_rows);
     }
   }
+  {
+    const char* v = std::getenv("HPS_CTA_FENCE");
+    const int sys = v && std::strcmp(v, "sys") == 0;
+    t->ctx.par[0].cta_sys_fence = t->ctx.par[1].cta_sys_fence = sys;
+  }
   t->ctx.epoch = &t->dsc->epoch;
   begin_round(t);  // round 1 (flags start at 0)
   return HPS_OK;
