@@ -60,26 +60,29 @@ __device__ __forceinline__ std::uint64_t ld_acquire_sys(const std::uint64_t* p) 
   return v;
 }
 
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // Called by every CTA after its P2P stores; the last CTA to finish raises
-// this rank's flag for `phase` in every peer. Each CTA releases its stores
-// to the done counter at GPU scope; the last CTA acquires them through the
-// counter, and its system-scope fence (cumulative over what it observed)
-// plus the st.release.sys flag publish every CTA's stores to the peers. A
-// system fence in every CTA (HPS_CTA_FENCE=sys, the earlier scheme) costs
-// ≈ 6 µs more per phase (tools/p2p_phase_probe.cu: 3.2 MB at the G = 2
-// interleave, 22.2 -> 16.4 µs per round).
+// this rank's flag for `phase` in every peer. After the CTA barrier, thread
+// 0's acq_rel add on the done counter releases the CTA's stores at GPU scope
+// and, in the last CTA, acquires every earlier CTA's (the adds form one
+// release sequence); its st.release.sys flag then publishes all of them to
+// the peers. A system fence in every CTA (HPS_CTA_FENCE=sys, the earlier
+// scheme) costs ≈ 6 µs more per phase (tools/p2p_phase_probe.cu: 3.2 MB at
+// the G = 2 interleave, 22.2 -> 16.4 µs per round).
 __device__ __forceinline__ void signal_peers(const PeerWindows& pw, int G, int me, int phase,
                                              std::uint64_t epoch, unsigned* done_ctr) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (pw.cta_sys_fence)
-      __threadfence_system();
-    else
-      __threadfence();
-    const unsigned prev = atomicAdd(done_ctr, 1u);
+    if (pw.cta_sys_fence) __threadfence_system();
+    const unsigned prev = atom_add_acq_rel_gpu(done_ctr, 1u);
     if (prev == gridDim.x * gridDim.y - 1) {
       *done_ctr = 0;
-      __threadfence_system();
+      if (pw.cta_sys_fence) __threadfence_system();
       for (int p = 0; p < G; ++p) st_release_sys(pw.flags[p] + me * kPhases + phase, epoch);
     }
   }
