@@ -202,9 +202,11 @@ __device__ __forceinline__ std::uint32_t dense_uid(std::uint32_t packed, std::ui
 __global__ void uid_keys_kernel(const std::uint32_t* __restrict__ uid_slot,
                                 const std::uint64_t* __restrict__ rq,
                                 const unsigned long long* __restrict__ n_uid,
-                                std::uint64_t* __restrict__ ukeys) {
+                                std::uint64_t* __restrict__ ukeys,
+                                unsigned long long* __restrict__ u_out) {
   pdl_wait();
   const std::uint64_t U = *n_uid;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *u_out = U;  // the exchange's key count
   for (std::uint64_t u = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; u < U;
        u += std::uint64_t(gridDim.x) * blockDim.x)
     ukeys[u] = rq[uid_slot[u]];

@@ -1508,10 +1508,11 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
         occ_row = T->g_occslot[bp.tb];
         rows = T->tvals[T->cur];
       } else {  // unique keys in uid order -> the NVLink exchange -> rows by uid
-        HPS_CUDA(cudaMemcpyAsync(&T->dsc->U, Uj, 8, cudaMemcpyDeviceToDevice, T->st));
+        // (the kernel also copies the count into dsc->U: no memcpy node,
+        // which would break the programmatic-launch chain)
         launch(T, uid_keys_kernel, grid_for(ob), 256, 0, slotsj,
                (const std::uint64_t*)T->rq_keys[bp.tb], (const unsigned long long*)Uj,
-               T->ukeys);
+               T->ukeys, reinterpret_cast<unsigned long long*>(&T->dsc->U));
         begin_round(T, false);
         HPS_TRY(exchange_pull(T, ob, true));
         Uj = &T->dsc->U;
