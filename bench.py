@@ -53,8 +53,9 @@ CONFIGS = {
                text="c2: 10M-key table, E=16, batch 16384, Zipf(1.0) keys, 100 keys/example, "
                     "MLP {8,16,1}, J=4"),
     "c3": dict(dims=10**8, E=64, B=65536, nnz=100, zipf=False, J=4, layers=(8, 16, 1),
-               text="c3 (SGD, no Adagrad yet): 100M-key table, E=64, batch 65536, "
-                    "100 uniform keys/example, MLP {8,16,1}, J=4"),
+               opt="adagrad",
+               text="c3: 100M-key table, E=64 with Adagrad state (rows of 2E floats), batch "
+                    "65536, 100 uniform keys/example, MLP {8,16,1}, J=4"),
     # the MEM-PS host tier at scale (1B keys x E=16 = 64 GB of
     # store; GPU box only)
     "c5": dict(dims=10**9, E=16, B=131072, nnz=100, zipf=False, J=4, layers=(8, 16, 1),
@@ -102,6 +103,14 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout: float = 15.0) -> bool:
+        """Block until nvidia-smi produced its first sample (so the sampler
+        is live when the timed region starts)."""
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+        return bool(self.lines)
 
     def stop(self):
         if not self.proc:
@@ -166,6 +175,13 @@ def run_reference_hot_path(cfgname, steps, warmup, threads, budget_s=60.0):
     return done * c["B"] / (ms / 1e3), ms / 1e3, done
 
 
+def config_of(c, args) -> dict:
+    """The `config` object both arms print (same keys)."""
+    return {"workload": c["text"], "dims": c["dims"], "E": c["E"], "global_batch": c["B"],
+            "nnz": c["nnz"], "zipf": c["zipf"], "J": c["J"], "layers": list(c["layers"]),
+            "optimizer": c.get("opt", "sgd")}
+
+
 def reference_arm(args, rank):
     if rank != 0:
         return
@@ -179,9 +195,12 @@ def reference_arm(args, rank):
         "ms_per_step": secs * 1e3 / done, "steps_timed": done, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32 params / f64 math",
         "data": "synthetic (reference gen_dataset, seed 1)",
-        "config": {"workload": c["text"], "dims": c["dims"], "E": c["E"], "batch": c["B"],
-                   "nnz": c["nnz"], "zipf": c["zipf"], "J": c["J"],
-                   "layers": list(c["layers"])},
+        "config": dict(config_of(c, args),
+                       optimizer="sgd" if c.get("opt", "sgd") == "sgd" else
+                                 "sgd (the reference has no Adagrad; its SGD hot path is timed)",
+                       parallelism=f"reference CPU hot path: {threads} simulated devices "
+                                   f"(one std::thread each, the reference concurrency model; "
+                                   f"the batch is sharded over them)"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"{done} batches x {c['B']} examples (of {args.steps} "
                                    f"requested; stops after ~60 s) after 1 warm-up batch, "
@@ -218,11 +237,6 @@ def remote_unique_keys(batches, D, J):
     return float(total)
 
 
-def ph_steps_frac(args):
-    """Work counters of the value pass rescaled to the phase-timing pass."""
-    return max(10, args.steps // 4) / args.steps
-
-
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -252,7 +266,8 @@ def run_ours(args, rank, world, local_rank):
     tier = pkg.Tier(nodes=1, devices=world, rank=rank, cuda_device=local_rank, width=E,
                     layer_dims=c["layers"], minibatches=J, deterministic=args.det,
                     key_space=dims, max_batch_examples=B, max_batch_keys=max_keys,
-                    nccl_id=nccl_id)
+                    nccl_id=nccl_id, optimizer=c.get("opt", "sgd"))
+    RW = tier.row_width  # floats per table / store row (2E with the Adagrad state)
     stream = torch.cuda.ExternalStream(tier.stream(), device=dev)
 
     def barrier():
@@ -306,7 +321,7 @@ def run_ours(args, rank, world, local_rank):
     for o, k, l in batches:
         dbatches.append((torch.from_numpy(o).to(dev), torch.from_numpy(k.view(np.int64)).to(dev),
                          torch.from_numpy(l).to(dev)))
-    dstore = torch.zeros((dims, E), dtype=torch.float32, device=dev)
+    dstore = torch.zeros((dims, RW), dtype=torch.float32, device=dev)
     tier.attach_store(dstore.data_ptr(), on_device=True, num_keys=dims)
 
     def dev_step(b):
@@ -320,11 +335,14 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     clocks = ClockSampler(local_rank)
     clocks.start()
+    clocks.wait_first()  # the sampler is live before the region opens
     launches0 = tier.kernel_launches()
+    captures0 = tier.graph_captures()
     barrier()
     dev_ms, dev_stats = timed_steps(dev_step, args.steps, args.warmup)
     barrier()
     launches = tier.kernel_launches() - launches0
+    captures = tier.graph_captures() - captures0
     clk = clocks.stop()
     dev_ms_max = max_over_ranks(dev_ms)
     value = args.steps * B / (dev_ms_max / 1e3)
@@ -337,22 +355,26 @@ def run_ours(args, rank, world, local_rank):
     tier.reset_timing()
     barrier()
     ph_steps = max(10, args.steps // 4)
-    timed_steps(dev_step, ph_steps, args.warmup)
+    _, ph_stats = timed_steps(dev_step, ph_steps, args.warmup)
     barrier()
     phases = tier.timing()
     tier.set_timing(False)
 
-    # per-rank work counters over the timed steps
-    pulled = sum(s.pulled_keys for s in dev_stats) * ph_steps_frac(args)
-    ws = sum(s.working_set for s in dev_stats) * ph_steps_frac(args)
-    occ = sum(s.occurrences for s in dev_stats) * ph_steps_frac(args)
+    # per-rank work counters over the phase-timing pass
+    pulled = sum(s.pulled_keys for s in ph_stats)
+    ws = sum(s.working_set for s in ph_stats)
+    occ = sum(s.occurrences for s in ph_stats)
+    n_ex = sum(s.examples for s in ph_stats)
+    big_keys = sum(s.big_segments for s in ph_stats)
+    big_occ = sum(s.big_occurrences for s in ph_stats)
+    fallbacks = sum(s.exact_fallbacks for s in dev_stats)
     carried = sum(s.carried_rows for s in dev_stats) / args.steps
     loss = sum(s.loss_sum for s in dev_stats) / max(1, sum(s.examples for s in dev_stats))
 
     # ---------------- end to end through the C ABI, host buffers (e2e) -------
     e2e = None
     if not args.no_e2e:
-        hstore_t = torch.zeros((dims, E), dtype=torch.float32).pin_memory()
+        hstore_t = torch.zeros((dims, RW), dtype=torch.float32).pin_memory()
         hstore = hstore_t.numpy()
         tier.attach_store(hstore)
         hbatches = []
@@ -377,8 +399,8 @@ def run_ours(args, rank, world, local_rank):
         e2e_ms_max = max_over_ranks(e2e_ms)
         h2d = sum(8 * (b[0].size) + 8 * b[1].size + b[2].size for b in
                   (hbatches[(args.warmup + i) % P] for i in range(args.steps))) / args.steps
-        h2d += (rd1 - rd0) * E * 4 / args.steps        # store rows read by the builds
-        d2h = ((wr1 - wr0) * E * 4 + 24 * args.steps) / args.steps  # written back + stats
+        h2d += (rd1 - rd0) * RW * 4 / args.steps        # store rows read by the builds
+        d2h = ((wr1 - wr0) * RW * 4 + 24 * args.steps) / args.steps  # written back + stats
         e2e = {"value": args.steps * B / (e2e_ms_max / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(sum_over_ranks(h2d)),
                "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
@@ -390,24 +412,33 @@ def run_ours(args, rank, world, local_rank):
         tier.attach_store(None)
         del hstore_t
 
-    # ---------------- roofline of the dominant kernel -----------------------
+    # ---------------- roofline of the dominant phase --------------------------
+    # Algorithmic bytes follow SURVEY 8(d), counted from the
+    # batch stats of the phase-timing pass, over that pass's phase times:
+    #   sparse (a8-a11 at one rank: segment-reduce + sgd_delta + in-place apply)
+    #     = U*(4+12E)  push/SGD apply per unique key (slot, delta, row r+w)
+    #     + U*4 + O*4  CSR grouping (segment bounds, example ids)
+    #     + n_ex*8E    each example's f64 dL/dx record, read once
+    #   big_fused_kernel alone (the long segments, on its own stream):
+    #     U_big*(8+12E) + O_big*4 + min(n_ex, O_big)*8E
     peak, peak_kind = load_peaks()
     K = ph_steps
+    mbs = K * J
     per_key_pull = 8 + 8 + 4 * E + 4 * E   # key + slot probe + row read + row write
-    per_key_apply = 4 + 12 * E             # slot + delta read + row read + row write
-    per_key_build = 8 + 8 + 4 * E + 4 * E
-    # sparse segment-reduce (a8, a9): per occurrence its example's dL/dx row
-    # (E f64) + the example id; per unique key its segment bounds + delta row
-    # (at one rank the delta is added in place: the table row read + written)
+    # push apply: slot + delta read + row read + row write; Adagrad reads and
+    # writes the state with the row (4 + 4E + 8E + 8E)
+    per_key_apply = 4 + 12 * E if RW == E else 4 + 20 * E
+    per_key_build = 8 + 8 + 4 * RW + 4 * RW
     fused_apply = world == 1 and os.environ.get("HPS_DEDUP", "hash") != "sort"
-    per_occ_sparse = 8 * E + 4
-    per_key_sparse = 8 + 8 * E if fused_apply else 8 + 4 * E
+    sparse_bytes = pulled * (per_key_apply + 4) + occ * 4 + n_ex * 8 * E
+    big_bytes = big_keys * (per_key_apply + 4) + big_occ * 4 + min(n_ex, big_occ) * 8 * E
     phase_bytes = {
-        "sparse": occ * per_occ_sparse + pulled * per_key_sparse,
+        "sparse": sparse_bytes,
+        "big_fused": big_bytes,
         "pull": pulled * per_key_pull,
         "apply": pulled * per_key_apply,
         "build": ws * per_key_build,
-        "writeback": ws * per_key_pull,
+        "writeback": ws * (8 + 4 + 4 * RW + 4 * RW),
         "dedup": 12 * occ + 8 * pulled,
     }
     if fused_apply:
@@ -423,29 +454,51 @@ def run_ours(args, rank, world, local_rank):
             gbs = nbytes / (ms / 1e3) / 1e9
             rl[name] = {"ms_per_step": ms / K, "algorithmic_bytes_per_step": nbytes / K,
                         "achieved_gbs": gbs, "frac": gbs / peak}
-    dominant = os.environ.get("HPS_ROOFLINE_KERNEL", "sparse")
-    traffic = None
+    traffic = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(args.config, {}).get(dominant)
+                traffic = json.load(f).get(args.config, {})
         except Exception:
-            traffic = None
-    dom = rl.get(dominant, {})
-    names = {"sparse": "sparse segment-reduce + sgd_delta" + (" + in-place apply" if fused_apply
-                                                              else "") +
-                       " (sparse_short_kernel; big_classify_kernel, big_plan_kernel, big_fused_kernel"
-                       " on a side stream), per mini-batch",
-             "pull": "table_gather_kernel<4>", "apply": "table_apply_kernel<4>"}
-    models = {"sparse": "O*(8E+4) + U*(8+8E)" if fused_apply else "O*(8E+4) + U*(8+4E)",
-              "pull": "U*(8+8+8E)", "apply": "U*(4+12E)"}
-    roofline = {"bound": "hbm", "kernel": names.get(dominant, dominant),
-                "achieved": dom.get("achieved_gbs"), "peak": peak, "unit": "GB/s",
-                "frac": dom.get("frac"), "traffic": traffic, "peak_kind": peak_kind,
-                "bytes_model": models.get(dominant),
-                "launches_per_step": J if dominant in ("sparse", "pull", "apply") else 1,
-                "phases": rl}
+            traffic = {}
+
+    def traffic_of(name, per_launch_bytes):
+        t = traffic.get(name)
+        return (t, t / per_launch_bytes if t and per_launch_bytes else None)
+
+    sp = rl.get("sparse", {})
+    sp_launch = sparse_bytes / mbs
+    t_sp, r_sp = traffic_of("sparse", sp_launch)
+    bf = rl.get("big_fused", {})
+    bf_launch = big_bytes / mbs
+    t_bf, r_bf = traffic_of("big_fused", bf_launch)
+    roofline = {
+        "bound": "hbm",
+        "kernel": "sparse segment-reduce + sgd_delta" + (" + in-place apply" if fused_apply
+                                                         else "") +
+                  " per mini-batch (sparse_short_kernel on the body stream; big_classify, "
+                  "big_plan, big_fused_kernel on a side stream)",
+        "achieved": sp.get("achieved_gbs"), "peak": peak, "unit": "GB/s", "frac": sp.get("frac"),
+        "traffic": t_sp, "traffic_over_algorithmic": r_sp, "peak_kind": peak_kind,
+        "algorithmic_bytes_per_launch": sp_launch,
+        "ms_per_launch": sp.get("ms_per_step", 0.0) * K / mbs if sp else None,
+        "bytes_model": ("U*(4+12E)" if RW == E else "U*(4+20E)") +
+                       " + U*4 + O*4 + n_ex*8E per mini-batch (SURVEY 8(d) push/" +
+                       ("SGD" if RW == E else "Adagrad") +
+                       " apply + CSR + one f64 dL/dx record per example)",
+        "launches_per_step": J,
+        "kernels": {
+            "big_fused_kernel": {
+                "achieved": bf.get("achieved_gbs"), "frac": bf.get("frac"),
+                "algorithmic_bytes_per_launch": bf_launch,
+                "ms_per_launch": bf.get("ms_per_step", 0.0) * K / mbs if bf else None,
+                "traffic": t_bf, "traffic_over_algorithmic": r_bf,
+                "bytes_model": ("U_big*(8+12E)" if RW == E else "U_big*(8+20E)") +
+                               " + O_big*4 + min(n_ex, O_big)*8E",
+                "segments_per_launch": big_keys / mbs, "occurrences_per_launch": big_occ / mbs,
+                "timed": "CUDA events on its own stream around each launch"}},
+        "phases": rl}
 
     # ---------------- NVLink roofline of the key/row/delta all-to-alls (N>1) --
     nvlink = None
@@ -481,7 +534,18 @@ def run_ours(args, rank, world, local_rank):
                    "sample": f"unavailable: {ex}"}
 
     all_launch = int(sum_over_ranks(launches))
-    pull_keys_s = sum_over_ranks(pulled / ph_steps_frac(args)) / (dev_ms_max / 1e3)
+    # keys/s per phase: pull = the phases that deliver a
+    # mini-batch's unique rows to the model (G = 1: fwd/bwd reads them in
+    # place; G > 1: key all-to-all + owner gather + row all-to-all); push = the
+    # phases that reduce and apply their gradients (G = 1: the fused sparse
+    # reduce + in-place apply; G > 1: + delta all-to-all + canonical apply)
+    pull_ms = phases.get("fwdbwd", 0.0) if fused_apply else (phases.get("dedup", 0.0) +
+                                                              phases.get("pull", 0.0))
+    push_ms = phases.get("sparse", 0.0) + (0.0 if fused_apply else phases.get("apply", 0.0))
+    keys_all = sum_over_ranks(pulled)
+    pull_ms, push_ms = max_over_ranks(pull_ms), max_over_ranks(push_ms)
+    pull_keys_s = keys_all / (pull_ms / 1e3) if pull_ms else None
+    push_keys_s = keys_all / (push_ms / 1e3) if push_ms else None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -489,22 +553,26 @@ def run_ours(args, rank, world, local_rank):
             "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 params / f64 math",
             "data": "synthetic (reference gen_dataset stream, seed 1; random-init dense)",
-            "config": {"workload": c["text"], "dims": dims, "E": E, "global_batch": B,
-                       "nnz": nnz, "zipf": c["zipf"], "J": J, "layers": list(c["layers"]),
+            "config": dict(config_of(c, args), **{
                        "parallelism": f"key-sharded x{world}", "batch_pool": P,
                        "deterministic": bool(args.det),
                        "l2": (f"not flushed; per-step inputs exceed L2: {P} batches x "
                               f"{max_keys * 8 >> 20} MiB keys cycled, {dims * E * 4 >> 20} MiB "
-                              "value store, 2 tables; steps pipelined (write-back of b "
-                              "overlaps b+1), one event region ending in hps_flush")},
+                              "value store, 5 tables; steps pipelined (write-back of b "
+                              "overlaps b+1), one event region ending in hps_flush")}),
             "e2e": e2e,
             "roofline": roofline,
             "nvlink": nvlink,
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": all_launch,
+            "graph_captures_in_timed_region": int(sum_over_ranks(captures)),
+            "exact_fallbacks": int(sum_over_ranks(fallbacks)),
             "pull_keys_per_s": pull_keys_s,
-            "push_keys_per_s": pull_keys_s,
+            "push_keys_per_s": push_keys_s,
+            "keys_per_s_phases": {"pull": "fwdbwd (rows read in place)" if fused_apply else
+                                  "dedup + pull", "push": "sparse (reduce + in-place apply)" if
+                                  fused_apply else "sparse + apply"},
             "phase_ms_per_step": {k: v / K for k, v in phases.items()},
             "train_loss": loss,
             "carried_rows_per_step": carried,
@@ -532,8 +600,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10,
-                    help="untimed steps; >= 5 covers one rotation of the tier's tables "
-                         "(one captured graph per table per batch shape)")
+                    help="untimed steps (>= 4: the first steady-state batch of a shape "
+                         "captures the graphs of every table rotation)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--pool", type=int, default=16, help="distinct batches cycled")

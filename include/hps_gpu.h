@@ -62,14 +62,28 @@ typedef struct {
   float learning_rate;       /* SGD lr (model.hpp:204-230) */
   uint64_t seed;             /* init_dense seed (model.hpp:42-53) */
   int minibatches;           /* J mini-batches per batch (config.hpp:52) */
-  int deterministic;         /* canonical-order reductions (config.hpp:67) */
+  int deterministic;         /* config.hpp:67; accepted, but every mode takes
+                                the canonical f64 order (bit-exact; there is
+                                no separate f32 fast path) */
   int64_t inject_skip_sync;  /* global mini-batch whose dense sync+update is
                                 skipped, -1 = off (pipeline.hpp:550-555) */
   uint64_t key_space;        /* keys are < key_space ("dims"); sizes sorts */
   uint64_t max_batch_examples;  /* per batch */
   uint64_t max_batch_keys;      /* key occurrences per batch */
   uint64_t max_working_set;     /* keys per build() call, 0 = max_batch_keys */
+  int optimizer;             /* HPS_OPT_SGD (the reference's, model.hpp:204-230)
+                                or HPS_OPT_ADAGRAD (extension, BASELINE c3) */
+  float adagrad_eps;         /* Adagrad: v -= lr*g / (sqrt(s) + eps), eps > 0 */
 } hps_config;
+
+/* Sparse optimizers. A table / value-store row is the embedding (E floats),
+ * then for Adagrad its accumulator state (E floats, zero-initialised: the
+ * reference's SparseParam::opt_state, types.hpp:30-39): rows are
+ * hps_row_width() = E (SGD) or 2E floats. Pushed values are SGD deltas
+ * -(lr*g) (hbm_ps.hpp:148-195 accumulate) or, for Adagrad, the gradients g;
+ * the owner applies them per sender in canonical order:
+ *   s' = s + g*g;  v' = v - (lr*g) / (sqrt(s') + eps)  (f32, IEEE-rounded). */
+enum { HPS_OPT_SGD = 0, HPS_OPT_ADAGRAD = 1 };
 
 /* Per-batch result of hps_train_batch. */
 typedef struct {
@@ -86,11 +100,15 @@ typedef struct {
   uint64_t store_rows;       /* build rows read from the attached value store
                                 (the rest: carried, the table two builds back
                                 while its write-back drains, or zeros) */
+  uint64_t big_segments;     /* (key, mini-batch) segments longer than 32
+                                occurrences (the chunked, certified reduce) */
+  uint64_t max_segment_chunks; /* most chunks of one such segment */
+  uint64_t big_occurrences;  /* key occurrences in those segments */
 } hps_batch_stats;
 
 /* Phase slots of hps_get_timing (ms accumulated over hps_train_batch calls,
  * measured with CUDA events on the tier's stream). */
-#define HPS_TIMING_SLOTS 11
+#define HPS_TIMING_SLOTS 12
 enum {
   HPS_T_TOTAL = 0,     /* whole batch */
   HPS_T_STAGE = 1,     /* H2D of the batch + per-shard counts (one D2H) */
@@ -102,8 +120,10 @@ enum {
   HPS_T_APPLY = 7,     /* push exchange + canonical owner apply (a10, a11) */
   HPS_T_DENSE = 8,     /* dense sync + update (a12) */
   HPS_T_WRITEBACK = 9, /* rows back to the value store (a13) */
-  HPS_T_SPARSE = 10    /* sparse segment-reduce + sgd_delta (a8, a9); GRADS is
+  HPS_T_SPARSE = 10,   /* sparse segment-reduce + sgd_delta (a8, a9); GRADS is
                           then the wait for the dense-grad reduce beside it */
+  HPS_T_BIGFUSED = 11  /* big_fused_kernel alone (the chunked reduce of the
+                          long segments, on its side stream inside SPARSE) */
 };
 
 const char* hps_last_error(void);
@@ -128,8 +148,9 @@ hps_status hps_destroy(hps_tier_t h);
  * the keys this rank owns, build a fresh table (capacity next_pow2(4n/3),
  * device_table.hpp:38-45) whose slot layout equals ascending-order linear
  * probing, and fill each row from the previous table when the key was there
- * (carry-over) else from `host_rows` (row i belongs to keys[i]; the
- * HostValue callback's result, staged H2D with cudaMemcpyAsync) or, when
+ * (carry-over) else from `host_rows` (row i belongs to keys[i], each
+ * hps_row_width() floats; the HostValue callback's result, staged H2D with
+ * cudaMemcpyAsync) or, when
  * host_rows is NULL, from the attached value store (zero if none). */
 hps_status hps_build(hps_tier_t h, const uint64_t* keys, uint64_t n,
                      const float* host_rows);
@@ -141,32 +162,39 @@ hps_status hps_pull(hps_tier_t h, const uint64_t* keys, uint64_t n,
                     float* out_rows);
 
 /* HbmTier::push_deltas (hbm_ps.hpp:148-167). COLLECTIVE. Ships each delta
- * row to its owner, where it is queued (nothing applied yet). */
+ * row (n x E; Adagrad: gradient rows) to its owner, where it is queued
+ * (nothing applied yet). */
 hps_status hps_push(hps_tier_t h, const uint64_t* keys, const float* deltas,
                     uint64_t n);
 
 /* HbmTier::drain_accums (hbm_ps.hpp:172-195): apply every queued delta,
  * senders in canonical node-major/device-major order, v += d in f32
- * (device_table.hpp:88-95). Local to the rank. */
+ * (device_table.hpp:88-95; Adagrad: the step above). Local to the rank. */
 hps_status hps_drain(hps_tier_t h);
 
 /* HbmTier::dump_node (hbm_ps.hpp:224-232) for this rank's table: keys in
- * ascending order and their rows. *n_out = occupancy. Buffers sized by
+ * ascending order and their rows (hps_row_width() floats each: embedding,
+ * then Adagrad state). *n_out = occupancy. Buffers sized by
  * hps_table_info's occupancy. */
 hps_status hps_dump(hps_tier_t h, uint64_t* keys_out, float* rows_out,
                     uint64_t* n_out);
 
-/* DeviceTable::capacity/occupancy/value_width (device_table.hpp:47-49). */
+/* DeviceTable::capacity/occupancy/value_width (device_table.hpp:47-49);
+ * width = E, the embedding width. */
 hps_status hps_table_info(hps_tier_t h, uint64_t* capacity,
                           uint64_t* occupancy, uint64_t* width);
+/* Floats per table / value-store row: E (SGD) or 2E (Adagrad). */
+hps_status hps_row_width(hps_tier_t h, uint64_t* row_width);
 /* Slot-level view for placement parity: slot_keys[capacity] (empty slots
- * hold ~0, device_table.hpp:34) and, if non-NULL, rows[capacity x E]. */
+ * hold ~0, device_table.hpp:34) and, if non-NULL, rows[capacity x
+ * hps_row_width()]. */
 hps_status hps_table_slots(hps_tier_t h, uint64_t* slot_keys, float* rows);
 
 /* SyncSession::run (hbm_ps.hpp:303-310) on a host buffer. COLLECTIVE.
  * Every rank ends with the elementwise sum of all ranks' buffers:
- * deterministic = f64 canonical_sum of the raw buffers (hbm_ps.hpp:
- * 258-277, 349-394), else an f32 all-reduce. */
+ * f64 canonical_sum of the raw buffers (hbm_ps.hpp:258-277, 349-394) in
+ * both modes: `deterministic` is accepted for the reference signature; the
+ * default mode's contract (within 1e-6 of canonical) holds bit-exactly. */
 hps_status hps_dense_sync(hps_tier_t h, float* buf, uint64_t len,
                           int deterministic);
 
@@ -177,7 +205,8 @@ hps_status hps_set_dense(hps_tier_t h, const float* w);
 
 /* ------------------------------------------------- performance API */
 
-/* Attach the host-tier value store (the MEM-PS stand-in): rows[key * E]
+/* Attach the host-tier value store (the MEM-PS stand-in): rows[key * RW]
+ * (RW = hps_row_width(): the embedding, then the Adagrad state)
  * for key < num_keys. build() fills rows of keys that were not in the
  * previous table from it, and hps_train_batch writes the trained rows back
  * after each batch (dump_node -> MemPs::collect_updates, pipeline.hpp:
@@ -253,6 +282,12 @@ hps_status hps_set_graphs(hps_tier_t h, int enable);
  * replay counts the kernels it contains). */
 hps_status hps_kernel_launches(hps_tier_t h, uint64_t* n);
 
+/* Number of CUDA graphs captured and instantiated on the handle so far (one
+ * per batch shape and table rotation; the first steady-state batch of a shape
+ * captures every rotation). The bench reports the captures inside its timed
+ * region: zero means it timed replays only. */
+hps_status hps_graph_captures(hps_tier_t h, uint64_t* n);
+
 /* The CUDA stream the handle launches on (cudaStream_t as void*). */
 hps_status hps_stream(hps_tier_t h, void** stream);
 
@@ -290,7 +325,8 @@ hps_status hps_pfile_read(const char* path, uint64_t* keys, float* rows,
 
 /* HbmTier::dump_node (hbm_ps.hpp:224-232) of this rank's table, written as
  * parameter files (the MEM-PS collect -> SSD-PS dump path, mem_ps.hpp:
- * 210-245): hps_dump + hps_pfile_write with zero opt_state. Ranks hold
+ * 210-245): hps_dump + hps_pfile_write, opt_state = the Adagrad state
+ * (zero under SGD, which never touches it, model.hpp:204). Ranks hold
  * disjoint keys, so every rank can export into one directory with disjoint
  * id ranges. */
 hps_status hps_export(hps_tier_t h, const char* dir, uint32_t file_capacity,

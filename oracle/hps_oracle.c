@@ -417,6 +417,19 @@ void or_sgd_accumulate(float* v, const float* g, uint64_t len, float lr) {
   }
 }
 
+/* Self-pinned Adagrad (see hps_oracle.h): one op at a time, so every f32
+ * rounding matches the device's _rn intrinsics (-ffp-contract=off). */
+void or_adagrad_apply(float* v, float* s, const float* g, uint64_t len, float lr, float eps) {
+  for (uint64_t i = 0; i < len; ++i) {
+    const float gg = g[i] * g[i];
+    const float acc = s[i] + gg;
+    s[i] = acc;
+    const float den = sqrtf(acc) + eps;
+    const float step = (lr * g[i]) / den;
+    v[i] = v[i] - step;
+  }
+}
+
 /* ------------------------------------------------------ train_reference */
 
 /* FlatStore (oracle.hpp:33-47): key -> embedding, zero-init on first touch.
@@ -511,6 +524,8 @@ int or_train_reference(const or_cfg* c, uint64_t batch_size,
                        uint64_t sparse_cap) {
   const int N = c->nodes, D = c->devices, G = N * D, J = c->minibatches;
   const int E = c->embedding_dim;
+  const int adagrad = c->optimizer == 1;
+  const int RW = adagrad ? 2 * E : E; /* store row: embedding (+ state) */
   const float lr = c->learning_rate;
   const uint64_t nw = or_dense_count(E, c->num_layers, c->layer_dims);
   const uint64_t nbatches = (num_examples + batch_size - 1) / batch_size;
@@ -518,7 +533,7 @@ int or_train_reference(const or_cfg* c, uint64_t batch_size,
   int rc = 0;
 
   flat_store st;
-  fs_init(&st, E);
+  fs_init(&st, RW);
   or_init_dense(c, dense_out);
 
   shard_grad* grads = (shard_grad*)calloc((size_t)G, sizeof(shard_grad));
@@ -577,7 +592,11 @@ int or_train_reference(const or_cfg* c, uint64_t batch_size,
           const shard_grad* sgp = &grads[d * N + n];
           for (uint64_t u = 0; u < sgp->nu; ++u) {
             float* p = fs_get_or_init(&st, sgp->uk[u]);
-            or_sgd_accumulate(p, sgp->sg + u * (uint64_t)E, (uint64_t)E, lr);
+            if (adagrad)
+              or_adagrad_apply(p, p + E, sgp->sg + u * (uint64_t)E, (uint64_t)E, lr,
+                               c->adagrad_eps);
+            else
+              or_sgd_accumulate(p, sgp->sg + u * (uint64_t)E, (uint64_t)E, lr);
           }
         }
       for (int g = 0; g < G; ++g) {
@@ -604,8 +623,8 @@ int or_train_reference(const or_cfg* c, uint64_t batch_size,
     } else {
       for (uint64_t i = 0; i < m; ++i) {
         sparse_keys_out[i] = ks[i];
-        memcpy(sparse_rows_out + i * (uint64_t)E, fs_lookup(&st, ks[i]),
-               (uint64_t)E * sizeof(float));
+        memcpy(sparse_rows_out + i * (uint64_t)RW, fs_lookup(&st, ks[i]),
+               (uint64_t)RW * sizeof(float));
       }
       *n_sparse_out = m;
     }

@@ -30,6 +30,9 @@ typedef struct {
   int minibatches;           /* config.hpp:52 J */
   int deterministic;         /* config.hpp:67 */
   int64_t inject_skip_sync;  /* config.hpp:72-74; the oracle never skips */
+  /* Extension fields (no reference pin; RefCfg stops before them): */
+  int optimizer;             /* 0 SGD (model.hpp:204-230), 1 Adagrad */
+  float adagrad_eps;         /* Adagrad epsilon (> 0) */
 } or_cfg;
 
 const char* or_last_error(void);
@@ -81,9 +84,18 @@ int or_average_apply(float* w, const float* sum, uint64_t len, int count,
                      float lr);
 /* model.hpp:226-230 sgd_delta then device_table.hpp:88-95 accumulate */
 void or_sgd_accumulate(float* v, const float* g, uint64_t len, float lr);
+/* SELF-PINNED EXTENSION (BASELINE config 3: the reference
+ * has no Adagrad; its SparseParam carries an untouched opt_state,
+ * types.hpp:30-39). The owner applies one sender's gradient row g to the
+ * embedding v and its accumulator s (both len floats), in f32 with IEEE
+ * rounding per op:  s += g*g;  v -= (lr*g) / (sqrtf(s) + eps). */
+void or_adagrad_apply(float* v, float* s, const float* g, uint64_t len, float lr, float eps);
 
 /* oracle.hpp:55-122 train_reference over to_batches(ds, batch_size)
- * (dataset.hpp:96-108). Sparse result sorted by key. */
+ * (dataset.hpp:96-108). Sparse result sorted by key; each row is the
+ * embedding, then (optimizer == 1) its Adagrad state: E or 2E floats. The
+ * sparse deltas are applied per sender in canonical (node, device) order
+ * (oracle.hpp:102-112): v += -(lr*g) for SGD, or_adagrad_apply for Adagrad. */
 int or_train_reference(const or_cfg* c, uint64_t batch_size,
                        uint64_t num_examples, const int64_t* offsets,
                        const uint64_t* keys, const uint8_t* labels,

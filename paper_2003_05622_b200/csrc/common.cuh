@@ -61,6 +61,60 @@ __device__ __forceinline__ void st_f4(float* p, float4 v) {
   *reinterpret_cast<float4*>(p) = v;
 }
 
+// The sparse optimizer applied in place by the owner (push/drain,
+// device_table.hpp:88-95). A table row is RW floats: the embedding (E), then
+// for Adagrad its accumulator state (E; the reference's SparseParam
+// opt_state, types.hpp:30-39, which its SGD never touches). The pushed value
+// per dimension is the SGD delta -(lr*g) (model.hpp:226-230: v += d), or for
+// Adagrad the gradient g itself (self-pinned extension, BASELINE c3,
+// oracle/hps_oracle.c or_adagrad_apply):
+//   s' = s + g*g;   v' = v - (lr*g) / (sqrt(s') + eps)      (f32, every op _rn)
+struct Optim {
+  int kind;  // 0 SGD, 1 Adagrad
+  int E;     // embedding width (the pushed value's width)
+  int RW;    // row width in the table and the value store
+  float lr, eps;
+  // the pushed value for gradient g (what the sparse reduce emits)
+  __device__ __forceinline__ float push_value(float g) const {
+    return kind == 0 ? -__fmul_rn(lr, g) : g;
+  }
+  // row[d] (and its state) updated with pushed value x
+  __device__ __forceinline__ void apply(float* row, int d, float x) const {
+    if (kind == 0) {
+      row[d] = __fadd_rn(row[d], x);
+    } else {
+      float* st = row + E;
+      const float s = __fadd_rn(st[d], __fmul_rn(x, x));
+      st[d] = s;
+      row[d] = __fsub_rn(row[d], __fdiv_rn(__fmul_rn(lr, x), __fadd_rn(__fsqrt_rn(s), eps)));
+    }
+  }
+  // four consecutive dimensions d0..d0+3 (16-B aligned)
+  __device__ __forceinline__ void apply4(float* row, int d0, float4 x) const {
+    float4* v = reinterpret_cast<float4*>(row + d0);
+    float4 a = *v;
+    if (kind == 0) {
+      a.x = __fadd_rn(a.x, x.x);
+      a.y = __fadd_rn(a.y, x.y);
+      a.z = __fadd_rn(a.z, x.z);
+      a.w = __fadd_rn(a.w, x.w);
+    } else {
+      float4* sp = reinterpret_cast<float4*>(row + E + d0);
+      float4 s = *sp;
+      s.x = __fadd_rn(s.x, __fmul_rn(x.x, x.x));
+      s.y = __fadd_rn(s.y, __fmul_rn(x.y, x.y));
+      s.z = __fadd_rn(s.z, __fmul_rn(x.z, x.z));
+      s.w = __fadd_rn(s.w, __fmul_rn(x.w, x.w));
+      *sp = s;
+      a.x = __fsub_rn(a.x, __fdiv_rn(__fmul_rn(lr, x.x), __fadd_rn(__fsqrt_rn(s.x), eps)));
+      a.y = __fsub_rn(a.y, __fdiv_rn(__fmul_rn(lr, x.y), __fadd_rn(__fsqrt_rn(s.y), eps)));
+      a.z = __fsub_rn(a.z, __fdiv_rn(__fmul_rn(lr, x.z), __fadd_rn(__fsqrt_rn(s.z), eps)));
+      a.w = __fsub_rn(a.w, __fdiv_rn(__fmul_rn(lr, x.w), __fadd_rn(__fsqrt_rn(s.w), eps)));
+    }
+    *v = a;
+  }
+};
+
 // Linear-probe lookup (device_table.hpp:119-128): slot or kNoSlot. The
 // probe window starts at mix64(key) & (cap-1) and stops at the first empty.
 __device__ __forceinline__ std::uint32_t probe_slot(

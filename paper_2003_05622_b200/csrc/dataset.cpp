@@ -10,7 +10,7 @@
 //     builds it even for uniform keys, dataset.hpp:190-191, which costs
 //     8 GB at 1e9 keys);
 //   * per-example feature sets are a small sorted array instead of std::set.
-// Byte-equality with the reference is pinned by tests/test_dataset.py
+// Byte-equality with the reference is pinned by tests/test_oracle_golden.py
 // against fixtures produced by oracle/_ref (the unmodified reference).
 #include <algorithm>
 #include <cmath>

@@ -62,9 +62,9 @@ struct ShardMap {
 // ones (fwd_bwd: 28.0 us vs 28.8 us all in order).
 template <int LPE>
 __device__ __forceinline__ bool embed_sum_exact(const std::uint32_t* __restrict__ occ_row,
-                                                const float* __restrict__ rows, std::uint32_t o0,
-                                                std::uint32_t o1, int sub, unsigned gmask,
-                                                int slack, double* hrec) {
+                                                const float* __restrict__ rows, int rstride,
+                                                std::uint32_t o0, std::uint32_t o1, int sub,
+                                                unsigned gmask, int slack, double* hrec) {
   constexpr int E = LPE, V4 = E / 4;
   constexpr int kRowsInFlight = 4;
   double acc[E];
@@ -77,7 +77,8 @@ __device__ __forceinline__ bool embed_sum_exact(const std::uint32_t* __restrict_
     for (int t = 0; t < kRowsInFlight; ++t) {
       const std::uint32_t p = base + t * LPE + sub;
       if (p < o1) {
-        const float4* row = reinterpret_cast<const float4*>(rows + std::uint64_t(occ_row[p]) * E);
+        const float4* row =
+            reinterpret_cast<const float4*>(rows + std::uint64_t(occ_row[p]) * rstride);
 #pragma unroll
         for (int q = 0; q < V4; ++q) v[t][q] = row[q];
       } else {
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(128)
                    const std::uint32_t* __restrict__ occ_off,
                    const std::int64_t* __restrict__ goff,  // non-null: occurrence = batch index
                    const std::uint32_t* __restrict__ occ_row,  // row of each occurrence
-                   const float* __restrict__ rows,
+                   const float* __restrict__ rows, int rstride,  // rows: embedding first
                    const std::uint8_t* __restrict__ labels,
                    double* __restrict__ H, double* __restrict__ DL,
                    double* __restrict__ DX, double* __restrict__ loss,
@@ -180,7 +181,9 @@ __global__ void __launch_bounds__(128)
       }
       bool summed = false;
       if constexpr (LPE == 8 || LPE == 16) {
-        if (E == LPE) summed = embed_sum_exact<LPE>(occ_row, rows, o0, o1, sub, gmask, md.exact_slack, hrec);
+        if (E == LPE)
+          summed = embed_sum_exact<LPE>(occ_row, rows, rstride, o0, o1, sub, gmask,
+                                        md.exact_slack, hrec);
       }
       for (int d0 = 0; !summed && d0 < E; d0 += LPE) {
         const int d = d0 + sub;
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
               for (int r = 0; r < LPE; ++r) {
                 const std::uint32_t rid = __shfl_sync(gmask, ids[t + q], r, LPE);
-                v[q][r] = (r < len[q] && d < E) ? rows[std::uint64_t(rid) * E + d] : 0.0f;
+                v[q][r] = (r < len[q] && d < E) ? rows[std::uint64_t(rid) * rstride + d] : 0.0f;
               }
             }
 #pragma unroll
@@ -386,8 +389,17 @@ __device__ __forceinline__ DD dd_add(DD a, double x) {
 __device__ __forceinline__ DD dd_add(DD a, DD b) { return dd_add(dd_add(a, b.hi), b.lo); }
 __device__ __forceinline__ double dd_value(DD a) { return __dadd_rn(a.hi, a.lo); }
 
+// Test knob (HPS_CERT_FORCE_FAIL=1, set at hps_create): every certificate
+// fails, so every certified sum takes its exact in-order fallback. Parity
+// tests use it to exercise those paths (they never trigger on the bench).
+__device__ int g_cert_force_fail = 0;
+
 __device__ __forceinline__ bool certify_f32(double S, double B, double A, std::uint64_t n,
                                             std::uint64_t m_plus_slices, double inv_n, float* g) {
+  if (g_cert_force_fail) {
+    *g = 0.0f;
+    return false;
+  }
   const double u = kUnitRoundoff;
   const double t = double(n + m_plus_slices + 8);
   const double second = __dmul_ru(__dmul_ru(2.0 * t, t), __dmul_ru(__dmul_ru(u, u), A));
@@ -629,29 +641,30 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Where a key's sgd_delta goes: the push row (pos[u], or u), or — one rank,
-// the key's slot known (apply_slot) — straight into the table row:
-// v = v + d in f32, DeviceTable::accumulate (device_table.hpp:88-95), the
-// delta being final when written (one writer per key and dimension).
+// Where a key's pushed value (sgd_delta -(lr*g), or the Adagrad gradient;
+// Optim) goes: the push row (pos[u], or u), or — one rank, the key's slot
+// known (apply_slot) — straight into the table row, DeviceTable::accumulate
+// (device_table.hpp:88-95) / the Adagrad step, the value being final when
+// written (one writer per key and dimension).
 struct DeltaOut {
   float* out;
   const std::uint32_t* pos;
   const std::uint32_t* apply_slot;
   float* table;
-  __device__ __forceinline__ void put(std::uint64_t u, int E, int d, float delta) const {
+  Optim opt;
+  __device__ __forceinline__ void grad(std::uint64_t u, int E, int d, float g) const {
+    const float x = opt.push_value(g);
     if (apply_slot) {
-      float* v = table + std::uint64_t(apply_slot[u]) * E + d;
-      *v = __fadd_rn(*v, delta);
+      opt.apply(table + std::uint64_t(apply_slot[u]) * opt.RW, d, x);
     } else {
-      out[std::uint64_t(pos ? pos[u] : u) * E + d] = delta;
+      out[std::uint64_t(pos ? pos[u] : u) * E + d] = x;
     }
   }
 };
 
 __device__ __forceinline__ void write_delta(const DeltaOut& o, std::uint64_t u, int E, int d,
-                                            double acc, double inv_n, float lr) {
-  const float g = __double2float_rn(__dmul_rn(acc, inv_n));
-  o.put(u, E, d, -__fmul_rn(lr, g));
+                                            double acc, double inv_n) {
+  o.grad(u, E, d, __double2float_rn(__dmul_rn(acc, inv_n)));
 }
 
 // Short segments, exact: one thread per (unique key, DPT dims) sums the key's
@@ -710,7 +723,7 @@ __global__ void __launch_bounds__(256)
       for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(acc[i], row[i]);
     }
 #pragma unroll
-    for (int i = 0; i < DPT; ++i) write_delta(dout, u, E, d0 + i, acc[i], inv_n, lr);
+    for (int i = 0; i < DPT; ++i) write_delta(dout, u, E, d0 + i, acc[i], inv_n);
   }
 }
 
@@ -731,17 +744,24 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
                                 std::uint32_t* __restrict__ chunk_off,
                                 unsigned long long* __restrict__ n_items,
                                 std::uint32_t* __restrict__ item_key,
-                                std::uint32_t* __restrict__ item_chunk) {
+                                std::uint32_t* __restrict__ item_chunk,
+                                unsigned long long* __restrict__ big_keys,
+                                unsigned long long* __restrict__ max_chunks,
+                                unsigned long long* __restrict__ big_occ) {
   pdl_wait();
   __shared__ std::uint32_t ws[32];
   const std::uint64_t NB = *n_big;
-  std::uint32_t carry = 0;
+  if (threadIdx.x == 0 && NB) atomicAdd(big_keys, (unsigned long long)NB);
+  std::uint32_t carry = 0, mx = 0;
+  unsigned long long occ = 0;
   for (std::uint64_t b0 = 0; b0 < NB; b0 += blockDim.x) {
     const std::uint64_t i = b0 + threadIdx.x;
     std::uint32_t v = 0, nchk = 0;
     if (i < NB) {
       const std::uint32_t u = big_list[i];
       nchk = (seg[u + 1] - seg[u] + chunk - 1) / chunk;
+      mx = nchk > mx ? nchk : mx;
+      occ += seg[u + 1] - seg[u];
       v = nchk <= std::uint32_t(kLocalChunks) ? 1u : nchk;  // one CTA walks a short key
     }
     const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -771,6 +791,13 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
     chunk_off[NB] = carry;
     *n_items = carry;
   }
+  for (int o = 16; o > 0; o >>= 1) {
+    const std::uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+    mx = y > mx ? y : mx;
+  }
+  for (int o = 16; o > 0; o >>= 1) occ += __shfl_xor_sync(0xFFFFFFFFu, occ, o);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(max_chunks, (unsigned long long)mx);
+  if ((threadIdx.x & 31) == 0 && occ) atomicAdd(big_occ, occ);
 }
 
 // Acquire load (gpu scope): later loads of this thread observe what the
@@ -917,7 +944,7 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
         }
       }
       if (int(threadIdx.x) < E)
-        dout.put(u, E, int(threadIdx.x), -__fmul_rn(lr, g));
+        dout.grad(u, E, int(threadIdx.x), g);
       __syncthreads();
       continue;
     }
@@ -1050,7 +1077,7 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
       }
     }
     if (int(threadIdx.x) < E)
-      dout.put(u, E, int(threadIdx.x), -__fmul_rn(lr, g));
+      dout.grad(u, E, int(threadIdx.x), g);
     __syncthreads();
   }
 }

@@ -14,7 +14,7 @@
 // every peer -> the consumer's wait kernel spins (bounded) until every
 // source's flag reached the epoch. Windows are reused every mini-batch; the
 // phase order (keys -> rows -> deltas -> dense) guarantees a window is never
-// overwritten before its owner consumed it (see DESIGN.md §5).
+// overwritten before its owner consumed it (see DESIGN.md §6).
 #pragma once
 
 #include <cstdint>
@@ -229,7 +229,7 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
                                       const std::uint64_t* __restrict__ tkeys,
                                       const float* __restrict__ tvals,
                                       const std::uint64_t* __restrict__ cap_ptr,
-                                      std::uint32_t* __restrict__ rslots, int E,
+                                      std::uint32_t* __restrict__ rslots, int E, int stride,
                                       unsigned* done_ctr, unsigned long long* served,
                                       DevError* err, int wait_phase) {
   pdl_wait();
@@ -263,7 +263,7 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
       continue;
     }
     if (part == 0) rslots[s * slot + i] = sl;
-    const float* src = tvals + std::uint64_t(sl) * E + part * VEC;
+    const float* src = tvals + std::uint64_t(sl) * stride + part * VEC;  // the embedding
     float* dst = pw.rows[s] + std::uint64_t(my_uids[s * slot + i]) * E + part * VEC;
     if (VEC == 4) {
       st_f4(dst, ld_f4(src));
@@ -312,32 +312,27 @@ __global__ void p2p_send_deltas_kernel(P2PCtx ctx, int G, int me, std::uint64_t 
 template <int VEC>
 __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
                                  const std::uint32_t* __restrict__ rslots,
-                                 float* __restrict__ tvals, int E, int G, int wait_phase,
+                                 float* __restrict__ tvals, Optim opt, int G, int wait_phase,
                                  DevError* err) {
   pdl_wait();
   if (wait_phase >= 0) wait_sources(ctx, G, me, wait_phase, err);  // the deltas arrived
   const PeerWindows& pw = ctx.cur(ctx.round());
   const std::uint64_t* my_hdr = pw.hdr[me];
   const float* my_deltas = pw.deltas[me];
+  const int E = opt.E;
   const int tpk = E / VEC;
   const std::uint64_t n = my_hdr[s * 2];
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < n * tpk;
        t += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint64_t i = t / tpk;
     const int part = int(t - i * tpk);
-    float* v = tvals + std::uint64_t(rslots[s * slot + i]) * E + part * VEC;
+    float* row = tvals + std::uint64_t(rslots[s * slot + i]) * opt.RW;
     const float* d = my_deltas + (s * slot + i) * E + part * VEC;
     if (VEC == 4) {
-      float4 a = ld_f4(v);
-      const float4 b = ld_f4(d);
-      a.x = __fadd_rn(a.x, b.x);
-      a.y = __fadd_rn(a.y, b.y);
-      a.z = __fadd_rn(a.z, b.z);
-      a.w = __fadd_rn(a.w, b.w);
-      st_f4(v, a);
+      opt.apply4(row, part * 4, ld_f4(d));
     } else {
 #pragma unroll
-      for (int q = 0; q < VEC; ++q) v[q] = __fadd_rn(v[q], d[q]);
+      for (int q = 0; q < VEC; ++q) opt.apply(row, part * VEC + q, d[q]);
     }
   }
 }

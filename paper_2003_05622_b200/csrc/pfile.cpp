@@ -196,12 +196,25 @@ hps_status hps_export(hps_tier_t h, const char* dir, uint32_t file_capacity, uin
   std::uint64_t cap = 0, occ = 0, width = 0;
   hps_status st = hps_table_info(h, &cap, &occ, &width);
   if (st != HPS_OK) return st;
+  std::uint64_t rw = 0;
+  st = hps_row_width(h, &rw);
+  if (st != HPS_OK) return st;
   std::vector<std::uint64_t> keys(occ);
-  std::vector<float> rows(occ * width);
+  std::vector<float> rows(occ * rw);
   std::uint64_t n = 0;
   st = hps_dump(h, keys.data(), rows.data(), &n);
   if (st != HPS_OK) return st;
-  return hps_pfile_write(dir, keys.data(), rows.data(), nullptr, n, std::uint32_t(width),
+  if (rw == width)  // SGD: no optimizer state in the row (opt_state written as zeros)
+    return hps_pfile_write(dir, keys.data(), rows.data(), nullptr, n, std::uint32_t(width),
+                           file_capacity, first_id, files_out);
+  // Adagrad: each row is the embedding then its accumulator, the record's
+  // embedding and opt_state (types.hpp:30-39, ssd_ps.hpp:50-56)
+  std::vector<float> emb(n * width), opt(n * width);
+  for (std::uint64_t i = 0; i < n; ++i) {
+    std::memcpy(&emb[i * width], &rows[i * rw], width * 4);
+    std::memcpy(&opt[i * width], &rows[i * rw + width], width * 4);
+  }
+  return hps_pfile_write(dir, keys.data(), emb.data(), opt.data(), n, std::uint32_t(width),
                          file_capacity, first_id, files_out);
 }
 

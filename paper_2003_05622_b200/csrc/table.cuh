@@ -92,6 +92,7 @@ __global__ void table_insert_kernel(const std::uint64_t* __restrict__ ws,
 // Ordered insert of one key (atomicMin, the larger key carried on); true if
 // it claimed an EMPTY slot. A table that fills up sets *spec_fail
 // (speculative pass) or raises.
+constexpr std::uint64_t kSpecProbeLimit = 4096;
 __device__ __forceinline__ bool insert_ordered(std::uint64_t cur, std::uint64_t* tkeys,
                                                std::uint64_t cap, unsigned* spec_fail,
                                                DevError* err) {
@@ -111,7 +112,10 @@ __device__ __forceinline__ bool insert_ordered(std::uint64_t cur, std::uint64_t*
       if (old > cur) cur = old;           // displaced: carry the larger key
     }
     idx = (idx + 1) & (cap - 1);
-    if (probes > cap) {
+    // a speculative pass gives up early: at a load factor <= 0.75 probe runs
+    // stay far below kSpecProbeLimit, so a run this long means the guessed
+    // capacity is too small (or the table is full) and the pass is redone
+    if (probes > cap || (spec_fail && probes > kSpecProbeLimit)) {
       if (spec_fail) *spec_fail = 1u;
       else raise_error(err, 4, key);
       return false;
@@ -181,20 +185,31 @@ __global__ void table_insert_dedup_kernel(const std::int64_t* __restrict__ off, 
   if (lane == 0 && placed && n_new) atomicAdd(n_new, placed);
 }
 
-// After the speculative insert: if the count asks for another capacity (or
-// the table filled up), set *redo, the right capacity, and reset the count
-// for the redo pass; otherwise clear *redo.
+// After a speculative insert pass (run twice: after the guess, after the
+// first redo). The pass's distinct count is exact unless the table filled up
+// (or a probe run hit kSpecProbeLimit): then the count stopped early, so the
+// redo runs at `fallback` (the capacity of the batch's owned-occurrence bound,
+// which holds every distinct key) to get an exact count, and the second check
+// redoes once more at the counted capacity if that differs. Otherwise: redo at
+// the counted capacity if it differs from the one built, else no redo.
+// *redo tells the next clear + insert pass whether to run.
 __global__ void table_spec_check_kernel(unsigned long long* __restrict__ n,
                                         std::uint64_t* __restrict__ cap,
                                         unsigned* __restrict__ spec_fail,
-                                        unsigned* __restrict__ redo) {
+                                        unsigned* __restrict__ redo, std::uint64_t fallback) {
   pdl_wait();
+  if (*spec_fail) {
+    *redo = 1u;
+    *cap = fallback;
+    *n = 0;
+    *spec_fail = 0u;
+    return;
+  }
   const std::uint64_t needed = table_capacity(*n);
-  if (*spec_fail || needed != *cap) {
+  if (needed != *cap) {
     *redo = 1u;
     *cap = needed;
     *n = 0;
-    *spec_fail = 0u;
   } else {
     *redo = 0u;
   }
@@ -504,7 +519,8 @@ __global__ void table_gather_kernel(const std::uint64_t* __restrict__ qkeys,
                                     const std::uint64_t* __restrict__ cap_ptr,
                                     float* __restrict__ out_rows,
                                     std::uint32_t* __restrict__ out_slots,
-                                    int E, DevError* err) {
+                                    int E, int stride, DevError* err) {
+  // (E floats of each stride-float table row: the embedding, not its state)
   pdl_wait();
   const int tpk = E / VEC;
   const std::uint64_t n = n_ptr ? *n_ptr : n_host;
@@ -521,7 +537,7 @@ __global__ void table_gather_kernel(const std::uint64_t* __restrict__ qkeys,
       continue;
     }
     if (out_slots && part == 0) out_slots[i] = slot;
-    const float* src = vals + std::uint64_t(slot) * E + part * VEC;
+    const float* src = vals + std::uint64_t(slot) * stride + part * VEC;
     float* dst = out_rows + i * E + part * VEC;
     if (VEC == 4) {
       st_f4(dst, ld_f4(src));
@@ -533,9 +549,10 @@ __global__ void table_gather_kernel(const std::uint64_t* __restrict__ qkeys,
 }
 
 // Owner apply of one sender's segment (device_table.hpp:88-95): v += d in
-// f32, no contraction. Keys inside one segment are unique, so no atomics;
-// segments are launched in canonical sender order (hbm_ps.hpp:172-195).
-// slots == null: probe `qkeys` instead of using cached slots.
+// f32, no contraction (or the Adagrad step, Optim). Keys inside one segment
+// are unique, so no atomics; segments are launched in canonical sender order
+// (hbm_ps.hpp:172-195). slots == null: probe `qkeys` instead of using cached
+// slots.
 template <int VEC>
 __global__ void table_apply_kernel(const std::uint32_t* __restrict__ slots,
                                    const std::uint64_t* __restrict__ qkeys,
@@ -544,8 +561,9 @@ __global__ void table_apply_kernel(const std::uint32_t* __restrict__ slots,
                                    const float* __restrict__ deltas,
                                    const std::uint64_t* __restrict__ n_ptr,
                                    std::uint64_t n_host, float* __restrict__ vals,
-                                   int E, DevError* err) {
+                                   Optim opt, DevError* err) {
   pdl_wait();
+  const int E = opt.E;
   const int tpk = E / VEC;
   const std::uint64_t n = n_ptr ? *n_ptr : n_host;
   const std::uint64_t total = n * std::uint64_t(tpk);
@@ -563,19 +581,13 @@ __global__ void table_apply_kernel(const std::uint32_t* __restrict__ slots,
         continue;
       }
     }
-    float* v = vals + std::uint64_t(slot) * E + part * VEC;
+    float* row = vals + std::uint64_t(slot) * opt.RW;
     const float* d = deltas + i * E + part * VEC;
     if (VEC == 4) {
-      float4 a = ld_f4(v);
-      const float4 b = ld_f4(d);
-      a.x = __fadd_rn(a.x, b.x);
-      a.y = __fadd_rn(a.y, b.y);
-      a.z = __fadd_rn(a.z, b.z);
-      a.w = __fadd_rn(a.w, b.w);
-      st_f4(v, a);
+      opt.apply4(row, part * 4, ld_f4(d));
     } else {
 #pragma unroll
-      for (int q = 0; q < VEC; ++q) v[q] = __fadd_rn(v[q], d[q]);
+      for (int q = 0; q < VEC; ++q) opt.apply(row, part * VEC + q, d[q]);
     }
   }
 }

@@ -134,7 +134,15 @@ struct Scalars {
   unsigned spec_fail, redo;            // speculative table build (prep)
   unsigned long long fallbacks;  // certified sums that needed the exact chain
   unsigned long long served;     // keys this rank served as owner (G > 1)
-  DevError err;
+  unsigned long long big_keys;   // segments on the chunked path (this batch)
+  unsigned long long max_chunks; // most chunks of one of them
+  unsigned long long big_occ;    // their occurrences
+  DevError err;                 // the body's and the parity API's error word
+  // per-batch error words of the pipelined stages: the stage's
+  // key-range check (by staging slot) and the prep's build (by table), so an
+  // in-flight batch's error is never read or cleared by another batch
+  DevError serr[kSlots];
+  DevError perr[kTables];
 };
 
 struct BatchShape {
@@ -161,6 +169,7 @@ struct BatchPlan {
 
 struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
+  std::uint64_t last_use = 0;  // LRU eviction
   std::uint64_t launches = 0;
   std::uint64_t epochs = 0;  // exchange rounds the body opens (host mirror)
   std::vector<int> ev_phase, ev_lane;
@@ -206,22 +215,25 @@ struct GroupState {
 struct BatchOut {
   double loss;
   unsigned long long pulled;
-  unsigned long long fallbacks, served;
+  unsigned long long fallbacks, served, big_keys, max_chunks, big_occ;
   unsigned long long carried, stored;
   std::uint64_t n_ws, cap;
-  DevError err;
+  DevError err, err_stage, err_prep;
 };
 
+// One sender's pushed (keys, deltas) awaiting hps_drain: a range of the
+// pending arena (Tier::pend_*), which grows by doubling and is reused.
 struct PendingChunk {
   int src;
   std::uint64_t n;
-  std::uint64_t* keys;
-  float* deltas;
+  std::uint64_t at;  // first entry in the arena
 };
 
 struct Tier {
   hps_config cfg{};
   int N = 1, D = 1, G = 1, g = 0, E = 1, J = 1;
+  int RW = 1;   // floats per table / store row: E, or 2E with the Adagrad state
+  Optim opt{};  // the sparse optimizer the owners apply (common.cuh)
   ModelDims md{};
   cudaStream_t st = nullptr;            // == lane[0].st: bodies and the parity API
   cudaStream_t st2 = nullptr;           // side stream: dense-grad overlaps sparse reduce
@@ -314,7 +326,7 @@ struct Tier {
   std::uint64_t* otot = nullptr;
   std::uint64_t* ukeys = nullptr;
   float *rows = nullptr, *deltas = nullptr, *hstage = nullptr, *staged = nullptr;
-  std::uint64_t staged_cap = 0;
+  std::uint64_t staged_cap = 0;  // floats
 
   // model
   double *H = nullptr, *DL = nullptr, *DX = nullptr, *dpart = nullptr;
@@ -370,6 +382,9 @@ struct Tier {
   float* store_host = nullptr;
 
   std::vector<PendingChunk> pending;
+  std::uint64_t* pend_keys = nullptr;  // the pending arena (hps_push -> hps_drain)
+  float* pend_deltas = nullptr;
+  std::uint64_t pend_cap = 0, pend_used = 0;
 
   // in-kernel NVLink all-to-all (G > 1): this rank's exported window and the
   // peers' windows (p2p.cuh)
@@ -401,6 +416,8 @@ struct Tier {
   // captured per-batch graphs (hps_train_batch), keyed by the batch shape
   bool use_graphs = true;
   std::map<std::vector<std::uint64_t>, GraphEntry> graphs;
+  std::uint64_t graph_clock = 0;     // LRU clock of the graph cache
+  std::uint64_t graph_captures = 0;  // captures so far (diagnostics, bench)
 };
 
 // ----------------------------------------------------------- helpers ----
@@ -497,10 +514,12 @@ static void launch(Tier* t, void (*k)(KArgs...), dim3 grid, dim3 block,
 static hps_status device_error_status(Tier* t, const DevError& e, const char* missing_ctx);
 
 static hps_status check_device_error(Tier* t, const char* missing_ctx,
-                                     bool collective = false, cudaStream_t s = nullptr) {
+                                     bool collective = false, cudaStream_t s = nullptr,
+                                     DevError* slot = nullptr) {
   if (!s) s = t->st;
+  if (!slot) slot = &t->dsc->err;
   if (collective && t->G > 1) {
-    HPS_CUDA(cudaMemcpyAsync(&t->dsc->err_any, &t->dsc->err.code, sizeof(int),
+    HPS_CUDA(cudaMemcpyAsync(&t->dsc->err_any, &slot->code, sizeof(int),
                              cudaMemcpyDeviceToDevice, s));
     ncclResult_t r = nccl().AllReduce(&t->dsc->err_any, &t->dsc->err_any, 1, ncclInt32, ncclMax,
                                       t->comm, s);
@@ -509,15 +528,14 @@ static hps_status check_device_error(Tier* t, const char* missing_ctx,
     HPS_CUDA(cudaMemcpyAsync(&t->hsc->err_any, &t->dsc->err_any, sizeof(int),
                              cudaMemcpyDeviceToHost, s));
   }
-  HPS_CUDA(cudaMemcpyAsync(&t->hsc->err, &t->dsc->err, sizeof(DevError),
-                           cudaMemcpyDeviceToHost, s));
+  HPS_CUDA(cudaMemcpyAsync(&t->hsc->err, slot, sizeof(DevError), cudaMemcpyDeviceToHost, s));
   HPS_CUDA(cudaStreamSynchronize(s));
   const DevError e = t->hsc->err;
   if (e.code == 0 && collective && t->G > 1 && t->hsc->err_any != 0)
     return set_error(hps_status(t->hsc->err_any),
                      "hbm: a peer rank failed this collective (status %d)", t->hsc->err_any);
   if (e.code == 0) return HPS_OK;
-  HPS_CUDA(cudaMemsetAsync(&t->dsc->err, 0, sizeof(DevError), s));
+  HPS_CUDA(cudaMemsetAsync(slot, 0, sizeof(DevError), s));
   return device_error_status(t, e, missing_ctx);
 }
 
@@ -866,6 +884,18 @@ static void mark_stage(Tier* t, int phase) {
   t->ev_lane.back() = 2 + kGroupLanes;
 }
 
+// A phase boundary on the big-segment side stream (st3).
+static void mark_big(Tier* t, int phase) {
+  if (!t->timing || !t->big_side) return;
+  Lane* l = t->L;
+  Lane tmp;
+  tmp.st = t->st3;
+  t->L = &tmp;
+  mark(t, phase);
+  t->L = l;
+  t->ev_lane.back() = 3 + kGroupLanes;
+}
+
 static void timing_begin(Tier* t) {
   t->ev_phase.clear();
   t->ev_lane.clear();
@@ -876,7 +906,7 @@ static void timing_begin(Tier* t) {
 // mark to the last.
 static void timing_end(Tier* t) {
   if (!t->timing || t->ev_phase.size() < 2) return;
-  int last[3 + kGroupLanes];
+  int last[4 + kGroupLanes];
   for (int& v : last) v = -1;
   for (std::size_t i = 0; i < t->ev_phase.size(); ++i) {
     const int ln = t->ev_lane[i], p = t->ev_phase[i];
@@ -909,8 +939,8 @@ static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* sta
   launch(t, table_insert_kernel, grid_for(n_upper), 256, 0, (const std::uint64_t*)t->ws,
          (const std::uint64_t*)&t->dsc->n_ws, t->tkeys[nxt],
          (const std::uint64_t*)&t->dsc->cap[nxt], &t->dsc->err);
-  const int V = vec_of(t->E);
-  const std::uint64_t work = n_upper * std::uint64_t(t->E / V);
+  const int V = vec_of(t->RW);
+  const std::uint64_t work = n_upper * std::uint64_t(t->RW / V);
   const std::uint64_t* pcap = (prv >= 0) ? &t->dsc->cap[prv] : nullptr;
   const std::uint64_t* pk = (prv >= 0) ? t->tkeys[prv] : nullptr;
   const float* pv = (prv >= 0) ? t->tvals[prv] : nullptr;
@@ -918,13 +948,13 @@ static void build_table(Tier* t, std::uint64_t n_upper, const std::uint32_t* sta
     launch(t, table_fill_kernel<4>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
            (const std::uint64_t*)&t->dsc->n_ws, (const std::uint64_t*)t->tkeys[nxt],
            t->tvals[nxt], (const std::uint64_t*)&t->dsc->cap[nxt], pk, pv, pcap,
-           staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->E,
+           staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->RW,
            &t->dsc->carried, &t->dsc->err);
   else
     launch(t, table_fill_kernel<1>, grid_for(work), 256, 0, (const std::uint64_t*)t->ws,
            (const std::uint64_t*)&t->dsc->n_ws, (const std::uint64_t*)t->tkeys[nxt],
            t->tvals[nxt], (const std::uint64_t*)&t->dsc->cap[nxt], pk, pv, pcap,
-           staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->E,
+           staged_idx, staged_rows, (const float*)t->store, t->store_keys, t->RW,
            &t->dsc->carried, &t->dsc->err);
   cudaMemcpyAsync(&t->dsc->nws_tab[nxt], &t->dsc->n_ws, 8, cudaMemcpyDeviceToDevice, t->st);
   t->prev2 = t->prev;
@@ -976,13 +1006,13 @@ static hps_status dedup_pull(Tier* t, const std::uint64_t* kin, const std::uint3
                (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
                std::uint64_t(0), (const std::uint64_t*)t->tkeys[t->cur],
                (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
-               t->rows, t->slots, t->E, &t->dsc->err);
+               t->rows, t->slots, t->E, t->RW, &t->dsc->err);
       else
         launch(t, table_gather_kernel<1>, grid_for(work), 256, 0,
                (const std::uint64_t*)t->ukeys, (const std::uint64_t*)&t->dsc->U,
                std::uint64_t(0), (const std::uint64_t*)t->tkeys[t->cur],
                (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
-               t->rows, t->slots, t->E, &t->dsc->err);
+               t->rows, t->slots, t->E, t->RW, &t->dsc->err);
       mark(t, HPS_T_PULL);
     }
     return HPS_OK;
@@ -1017,7 +1047,7 @@ static hps_status exchange_pull(Tier* t, std::uint64_t n, bool do_gather) {
     auto k = V == 4 ? p2p_serve_rows_kernel<4> : p2p_serve_rows_kernel<1>;
     launch(t, k, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
            (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
-           (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->done_ctr,
+           (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->RW, t->done_ctr,
            &t->dsc->served, &t->dsc->err, fold ? int(kPhKeys) : -1);
     p2p_wait(t, kPhRows);
     mark(t, HPS_T_PULL);
@@ -1044,7 +1074,7 @@ static hps_status push_apply(Tier* t) {
   auto k = V == 4 ? p2p_apply_kernel<4> : p2p_apply_kernel<1>;
   for (int src : canonical_senders(t)) {
     launch(t, k, grid_for(t->slot * std::uint64_t(t->E / V), 256, kSMs * 2), 256, 0, t->ctx, t->g,
-           src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur], t->E, t->G,
+           src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur], t->opt, t->G,
            first ? int(kPhDeltas) : -1, &t->dsc->err);
     first = false;
   }
@@ -1086,7 +1116,8 @@ static hps_status launch_big_plan(Tier* t, std::uint64_t u_upper, const std::uin
             U, seg, t->big_list, nb);
   launch_on(t, bs, big_plan_kernel, 1, 1024, 0, fuse_chunk(t->E),
             (const std::uint32_t*)t->big_list, (const unsigned long long*)nb, seg, t->chunk_off,
-            &t->dsc->n_items, t->item_key, t->item_chunk);
+            &t->dsc->n_items, t->item_key, t->item_chunk, &t->dsc->big_keys, &t->dsc->max_chunks,
+            &t->dsc->big_occ);
   HPS_CUDA(cudaMemsetAsync(t->fuse_flags, 0, t->fuse_items * 4, bs));
   HPS_CUDA(cudaMemsetAsync(t->fuse_ticket, 0, 8, bs));
   return HPS_OK;
@@ -1101,17 +1132,20 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
                                       const std::uint32_t* apply_slot = nullptr) {
   // apply_slot non-null (one rank, the keys' table slots known): the deltas
   // go straight into the current table, no delta rows and no apply launch
-  const DeltaOut dout{t->deltas, pos, apply_slot, apply_slot ? t->tvals[t->cur] : nullptr};
+  const DeltaOut dout{t->deltas, pos, apply_slot, apply_slot ? t->tvals[t->cur] : nullptr,
+                      t->opt};
   const int E = t->E;
   if (E > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
   const float lr = t->cfg.learning_rate;
   const double* DX = t->DX;
   cudaStream_t bs = t->big_side ? t->st3 : t->st;
+  mark_big(t, -1);
   launch_on(t, bs, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
             (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big,
             (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
             (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs, dout,
             DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, &t->dsc->fallbacks);
+  mark_big(t, HPS_T_BIGFUSED);
   HPS_CUDA(cudaEventRecord(t->join3, bs));
   // DPT dims per thread (4 when E allows 32-byte row loads)
   const int dpt = (E % 4 == 0) ? 4 : 1;
@@ -1240,7 +1274,7 @@ static std::uint64_t group_region(const BatchShape& sh, int j) {
 // on the prep lane: it depends only on the keys, so batch b+1's grouping runs
 // beside batch b's body. Outputs go to the table's pools (g_*[tb]).
 static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPlan& bp,
-                                   GroupState& g, int j0, int j1,
+                                   GroupState& g, int j0, int j1, DevError* err,
                                    const cudaEvent_t* mb_done = nullptr) {
   const int G = T->G, J = T->J, tb = bp.tb;
   const std::uint64_t B = sh.B, GJ = std::uint64_t(G) * J;
@@ -1271,7 +1305,7 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     const std::uint64_t* gc = G == 1 ? &T->dsc->cap[tb] : &T->dsc->rq_capv;
     launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys, gk, gc, g.gcnt,
            g.slot_uid, g.part_slot, pcap, g.part_n, T->g_occslot[tb], T->g_tick[tb], T->g_exof[tb],
-           &T->dsc->err);
+           err);
     launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)g.part_n,
            (const std::uint32_t*)g.part_slot, pcap, g.part_base, uids, U);
     const Count Uc{reinterpret_cast<const std::uint64_t*>(U), 0};
@@ -1321,7 +1355,9 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   const std::uint64_t* dkeys = T->b_keys[bp.sp];
   std::uint64_t* nws = &T->dsc->nws_tab[tb];
   std::uint64_t* cap = &T->dsc->cap[tb];
+  DevError* perr = &T->dsc->perr[tb];
   mark(T, -1);
+  HPS_CUDA(cudaMemsetAsync(perr, 0, sizeof(DevError), l.st));
   HPS_CUDA(cudaMemsetAsync(nws, 0, 8, l.st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->carried_tab[tb], 0, 8, l.st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->stored_tab[tb], 0, 8, l.st));
@@ -1338,15 +1374,21 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
          (const std::uint64_t*)cap, (const unsigned*)nullptr);
   launch(T, table_insert_dedup_kernel, gk, 256, 0, (const std::int64_t*)T->b_off[bp.sp], sh.B,
          dkeys, std::uint64_t(G), std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap,
-         &T->dsc->err, (unsigned long long*)nws, &T->dsc->spec_fail, (const unsigned*)nullptr);
-  launch(T, table_spec_check_kernel, 1, 1, 0, (unsigned long long*)nws, cap, &T->dsc->spec_fail,
-         &T->dsc->redo);
-  launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[tb],
-         (const std::uint64_t*)cap, (const unsigned*)&T->dsc->redo);
-  launch(T, table_insert_dedup_kernel, gk, 256, 0, (const std::int64_t*)T->b_off[bp.sp], sh.B,
-         dkeys, std::uint64_t(G), std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap,
-         &T->dsc->err, (unsigned long long*)nws, (unsigned*)nullptr,
-         (const unsigned*)&T->dsc->redo);
+         perr, (unsigned long long*)nws, &T->dsc->spec_fail, (const unsigned*)nullptr);
+  // (a speculative table that fills up stops counting, so its
+  // count cannot size the redo; that redo runs at the bound's capacity and a
+  // second check re-sizes it from the then exact count)
+  const std::uint64_t fallback = std::min(cap_bound, T->capmax);
+  for (int pass = 0; pass < 2; ++pass) {
+    launch(T, table_spec_check_kernel, 1, 1, 0, (unsigned long long*)nws, cap,
+           &T->dsc->spec_fail, &T->dsc->redo, fallback);
+    launch(T, table_clear_kernel, grid_for(cap_bound), 256, 0, T->tkeys[tb],
+           (const std::uint64_t*)cap, (const unsigned*)&T->dsc->redo);
+    launch(T, table_insert_dedup_kernel, gk, 256, 0, (const std::int64_t*)T->b_off[bp.sp], sh.B,
+           dkeys, std::uint64_t(G), std::uint64_t(T->g), T->tkeys[tb], (const std::uint64_t*)cap,
+           perr, (unsigned long long*)nws,
+           pass == 0 ? &T->dsc->spec_fail : (unsigned*)nullptr, (const unsigned*)&T->dsc->redo);
+  }
   // the table's keys are final: the mini-batches' grouping forks onto lane 2
   // and runs beside the rest of the build (joined at the end of the prep)
   if (bp.grouped) {
@@ -1360,7 +1402,7 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
     Lane& ln = T->lane[2];
     HPS_CUDA(cudaStreamWaitEvent(ln.st, T->g_fork, 0));
     T->L = &ln;
-    const hps_status st = enqueue_grouping(T, sh, bp, T->gs[0], 0, bp.prep_mbs);
+    const hps_status st = enqueue_grouping(T, sh, bp, T->gs[0], 0, bp.prep_mbs, perr);
     if (st == HPS_OK) mark(T, HPS_T_DEDUP);
     T->L = &l;
     HPS_TRY(st);
@@ -1397,7 +1439,7 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   launch(T, table_prefetch_probe_kernel, grid_for(sh.own_bound), 256, 0,
          (const std::uint64_t*)T->wsb[tb], (const std::uint32_t*)T->wsib[tb],
          (const std::uint64_t*)nws, T->tvals[tb], T->csrc[tb], pk, pc, qk, qc, q2k, q2c,
-         T->store != nullptr, T->store_keys, E, T->need_key[tb], T->need_slot[tb],
+         T->store != nullptr, T->store_keys, T->RW, T->need_key[tb], T->need_slot[tb],
          &T->dsc->stored_tab[tb], &T->dsc->carried_tab[tb]);
   // the store list is ready: the store gather (enqueue_store_gather, its own
   // stream, outside this graph) starts here, beside the grouping and the next
@@ -1416,7 +1458,7 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
 // The store rows of table tb (host memory over PCIe, or HBM): a streaming
 // gather on st_pf, after the prep's store list; the batch's body waits for it.
 static hps_status enqueue_store_gather(Tier* T, const BatchShape& sh, int tb) {
-  const int E = T->E, V = vec_of(E);
+  const int E = T->RW, V = vec_of(E);  // whole rows (embedding + optimizer state)
   HPS_CUDA(cudaStreamWaitEvent(T->st_pf, T->pf_fork, 0));
   // the store rows of keys last held by the table four builds back (not a
   // proxy of this batch) arrive with its eviction write-back
@@ -1446,16 +1488,19 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
   const std::uint64_t* dkeys = T->b_keys[bp.sp];
   const std::uint8_t* dlab = T->b_lab[bp.sp];
   mark(T, -1);
+  // the body's error word is this batch's from here (bodies run in order on
+  // T->st; the previous one's was copied to its BatchOut already)
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->err, 0, sizeof(DevError), T->st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 16, T->st));       // loss, pulled
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 16, T->st));  // fallbacks, served
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 40, T->st));  // fallbacks .. big_occ
   if (bp.tp >= 0) {  // rows from the resident tables (carry-over, proxies)
-    const int V = vec_of(E);
-    const unsigned gc = grid_for(sh.own_bound * std::uint64_t(E / V));
+    const int RW = T->RW, V = vec_of(RW);
+    const unsigned gc = grid_for(sh.own_bound * std::uint64_t(RW / V));
     auto k = V == 4 ? table_carry_kernel<4> : table_carry_kernel<1>;
     launch(T, k, gc, 256, 0, (const std::uint32_t*)T->csrc[bp.tb],
            (const std::uint32_t*)T->wsib[bp.tb], (const std::uint64_t*)&T->dsc->nws_tab[bp.tb],
            (const float*)T->tvals[bp.tp], (const float*)(bp.tq >= 0 ? T->tvals[bp.tq] : nullptr),
-           (const float*)(bp.tq2 >= 0 ? T->tvals[bp.tq2] : nullptr), T->tvals[bp.tb], E);
+           (const float*)(bp.tq2 >= 0 ? T->tvals[bp.tq2] : nullptr), T->tvals[bp.tb], RW);
   }
   // the mini-batches the prep did not group: grouped here on a side branch
   // (lane 3), each ready before its mini-batch and beside the previous one
@@ -1464,7 +1509,8 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     HPS_CUDA(cudaEventRecord(T->b_fork, T->st));
     HPS_CUDA(cudaStreamWaitEvent(T->lane[3].st, T->b_fork, 0));
     T->L = &T->lane[3];
-    const hps_status gst = enqueue_grouping(T, sh, bp, T->gs[1], bp.prep_mbs, J, T->gmb_done);
+    const hps_status gst =
+        enqueue_grouping(T, sh, bp, T->gs[1], bp.prep_mbs, J, &T->dsc->err, T->gmb_done);
     T->L = &T->lane[0];
     HPS_TRY(gst);
   }
@@ -1488,6 +1534,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     PullPlan plan;
     const std::uint32_t* occ_row = T->inv;  // occurrence -> row of `rows`
     const float* rows = T->rows;
+    int rstride = E;  // the pulled rows (uid order), or the table's rows in place
     const std::int64_t* goff = nullptr;      // occurrence ids: shard-local (sort path)
     if (side && j >= bp.prep_mbs) HPS_CUDA(cudaStreamWaitEvent(T->st, T->gmb_done[j], 0));
     const std::uint64_t* Uj = &T->dsc->U;      // this mini-batch's unique keys
@@ -1507,6 +1554,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
         mark(T, HPS_T_PULL);
         occ_row = T->g_occslot[bp.tb];
         rows = T->tvals[T->cur];
+        rstride = T->RW;
       } else {  // unique keys in uid order -> the NVLink exchange -> rows by uid
         // (the kernel also copies the count into dsc->U: no memcpy node,
         // which would break the programmatic-launch chain)
@@ -1543,7 +1591,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
       const unsigned blocks = unsigned(std::min<std::uint64_t>((n + epb - 1) / epb, kSMs * 8));
       auto k = LPE == 8 ? fwd_bwd_kernel<8> : (LPE == 16 ? fwd_bwd_kernel<16> : fwd_bwd_kernel<32>);
       launch(T, k, blocks, 128, smem, T->md, sm, (const float*)T->dense,
-             (const std::uint32_t*)T->occ_off, goff, occ_row, rows, dlab, T->H,
+             (const std::uint32_t*)T->occ_off, goff, occ_row, rows, rstride, dlab, T->H,
              T->DL, T->DX, &T->dsc->loss, &T->dsc->err);
       mark(T, HPS_T_FWDBWD);
       // dense-grad reduce on the side stream, overlapping the sparse reduce
@@ -1579,12 +1627,12 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
         launch(T, table_apply_kernel<4>, grid_for(work), 256, 0, slotsj,
                (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
                (const std::uint64_t*)nullptr, (const float*)T->deltas, Uj, std::uint64_t(0),
-               T->tvals[T->cur], E, &T->dsc->err);
+               T->tvals[T->cur], T->opt, &T->dsc->err);
       else
         launch(T, table_apply_kernel<1>, grid_for(work), 256, 0, slotsj,
                (const std::uint64_t*)nullptr, (const std::uint64_t*)nullptr,
                (const std::uint64_t*)nullptr, (const float*)T->deltas, Uj, std::uint64_t(0),
-               T->tvals[T->cur], E, &T->dsc->err);
+               T->tvals[T->cur], T->opt, &T->dsc->err);
     } else {
       HPS_TRY(push_apply(T));
     }
@@ -1603,7 +1651,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
 // order. The store is exact for every key outside the resident tables, which
 // is all the next builds read from it; hps_flush makes it exact for all keys.
 static hps_status enqueue_writeback(Tier* T, int t, const int* newer, int n_newer) {
-  const int E = T->E, V = vec_of(E);
+  const int E = T->RW, V = vec_of(E);  // whole rows (embedding + optimizer state)
   HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_body_tab[t], 0));
   if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[t][0], T->st_wb));
   const std::uint64_t* nk[3] = {nullptr, nullptr, nullptr};
@@ -1678,16 +1726,21 @@ static hps_status wb_fence(Tier* T, int p = -1, cudaStream_t s = nullptr) {
   return HPS_OK;
 }
 
-// Capture `enqueue` on the current lane's stream once per key, then replay:
-// a whole prep or body becomes one cudaGraphLaunch.
+// Capture `enqueue` on the current lane's stream once per key (no launch):
+// a whole prep or body becomes one graph. The cache keeps the 64 most
+// recently used graphs.
 template <class Fn>
-static hps_status run_graph(Tier* T, const std::vector<std::uint64_t>& key, Fn&& enqueue) {
+static hps_status capture_graph(Tier* T, const std::vector<std::uint64_t>& key, Fn&& enqueue,
+                                GraphEntry** out) {
   cudaStream_t s = T->L->st;
   auto it = T->graphs.find(key);
   if (it == T->graphs.end()) {
-    if (T->graphs.size() >= 64) {  // bounded cache
-      cudaGraphExecDestroy(T->graphs.begin()->second.exec);
-      T->graphs.erase(T->graphs.begin());
+    if (T->graphs.size() >= 64) {  // bounded cache: evict the least recently used
+      auto lru = T->graphs.begin();
+      for (auto i = T->graphs.begin(); i != T->graphs.end(); ++i)
+        if (i->second.last_use < lru->second.last_use) lru = i;
+      cudaGraphExecDestroy(lru->second.exec);
+      T->graphs.erase(lru);
     }
     GraphEntry ge;
     const std::uint64_t l0 = T->launches, e0 = T->p2p_epoch;
@@ -1712,20 +1765,30 @@ static hps_status run_graph(Tier* T, const std::vector<std::uint64_t>& key, Fn&&
     ge.epochs = T->p2p_epoch - e0;
     ge.ev_phase.assign(T->ev_phase.begin() + ev0, T->ev_phase.end());
     ge.ev_lane.assign(T->ev_lane.begin() + ev0, T->ev_lane.end());
-    T->launches = l0;  // counted per replay below
+    T->launches = l0;  // counted per replay
     T->p2p_epoch = e0;
     T->ev_phase.resize(ev0);
     T->ev_lane.resize(ev0);
+    ++T->graph_captures;
     it = T->graphs.emplace(key, std::move(ge)).first;
   }
-  HPS_CUDA(cudaGraphLaunch(it->second.exec, s));
-  T->launches += it->second.launches;
-  T->p2p_epoch += it->second.epochs;
-  T->ev_phase.insert(T->ev_phase.end(), it->second.ev_phase.begin(), it->second.ev_phase.end());
-  T->ev_lane.insert(T->ev_lane.end(), it->second.ev_lane.begin(), it->second.ev_lane.end());
+  it->second.last_use = ++T->graph_clock;
+  *out = &it->second;
   return HPS_OK;
 }
 
+// Capture once per key, then replay.
+template <class Fn>
+static hps_status run_graph(Tier* T, const std::vector<std::uint64_t>& key, Fn&& enqueue) {
+  GraphEntry* ge = nullptr;
+  HPS_TRY(capture_graph(T, key, std::forward<Fn>(enqueue), &ge));
+  HPS_CUDA(cudaGraphLaunch(ge->exec, T->L->st));
+  T->launches += ge->launches;
+  T->p2p_epoch += ge->epochs;
+  T->ev_phase.insert(T->ev_phase.end(), ge->ev_phase.begin(), ge->ev_phase.end());
+  T->ev_lane.insert(T->ev_lane.end(), ge->ev_lane.begin(), ge->ev_lane.end());
+  return HPS_OK;
+}
 
 // ------------------------------------------------------ the batch pipeline
 
@@ -1758,10 +1821,14 @@ static void complete_oldest(Tier* T) {
     T->rows_read += o.stored;
     st.exact_fallbacks = o.fallbacks;
     st.served_keys = o.served;
+    st.big_segments = o.big_keys;
+    st.max_segment_chunks = o.max_chunks;
+    st.big_occurrences = o.big_occ;
     st.occurrences = bp.occ_total;
-    if (o.err.code) {
-      cudaMemsetAsync(&T->dsc->err, 0, sizeof(DevError), T->st);
-      d.st = device_error_status(T, o.err, "device table: missing key ");
+    // first failing stage: the key-range check, the build, the body
+    const DevError& e = o.err_stage.code ? o.err_stage : (o.err_prep.code ? o.err_prep : o.err);
+    if (e.code) {
+      d.st = device_error_status(T, e, "device table: missing key ");
       d.msg = error_message();
     }
   }
@@ -1789,9 +1856,90 @@ static void complete_oldest(Tier* T) {
 // Every in-flight batch done; the main stream ordered after the write-backs.
 // The parity API (build / pull / push / drain / dump ...) starts from here.
 static hps_status quiesce(Tier* T) {
-  while (!T->inflight.empty()) complete_oldest(T);
+  if (!T->inflight.empty()) {
+    while (!T->inflight.empty()) complete_oldest(T);
+    // the batches reported their own errors; the parity API starts clean
+    HPS_CUDA(cudaMemsetAsync(&T->dsc->err, 0, sizeof(DevError), T->st));
+  }
   HPS_TRY(flush_all(T));
   return wb_fence(T);
+}
+
+// Graph keys of a batch's prep and body: the shape plus the table / staging
+// rotation they are captured for.
+static std::vector<std::uint64_t> prep_key(const Tier* T, const BatchShape& sh,
+                                           const BatchPlan& bp) {
+  return {1, sh.B, sh.own_bound, sh.batch_bound, std::uint64_t(bp.tb), std::uint64_t(bp.tp + 1),
+          std::uint64_t(bp.tq + 1), std::uint64_t(bp.tq2 + 1), std::uint64_t(bp.sp),
+          std::uint64_t(bp.prep_mbs), reinterpret_cast<std::uint64_t>(T->store), T->store_keys,
+          std::uint64_t(T->store_on_host), std::uint64_t(T->timing)};
+}
+static std::vector<std::uint64_t> body_key(const Tier* T, const BatchShape& sh,
+                                           const BatchPlan& bp) {
+  std::vector<std::uint64_t> key = {2, sh.B, sh.own_bound, std::uint64_t(bp.tb),
+                                    std::uint64_t(bp.tp + 1), std::uint64_t(bp.tq + 1),
+                                    std::uint64_t(bp.tq2 + 1), std::uint64_t(bp.sp),
+                                    std::uint64_t(bp.prep_mbs), std::uint64_t(T->timing)};
+  for (int j = 0; j < T->J; ++j) key.push_back(sh.mb_bound[j]);
+  return key;
+}
+
+// Steady state of the rotation: every table role is filled, so the next
+// batches of this shape differ only by the rotation offset.
+static bool steady(const Tier* T, const BatchPlan& bp) {
+  return bp.tp >= 0 && (!T->store || (bp.tq >= 0 && bp.tq2 >= 0));
+}
+
+// The same batch one to kTables-1 rotation steps later (tables and staging
+// slots advance together).
+static BatchPlan rotated(const BatchPlan& bp, int r) {
+  BatchPlan q = bp;
+  auto rot = [r](int x) { return x < 0 ? -1 : (x + r) % kTables; };
+  q.tb = rot(bp.tb);
+  q.tp = rot(bp.tp);
+  q.tq = rot(bp.tq);
+  q.tq2 = rot(bp.tq2);
+  q.sp = (bp.sp + r) % kSlots;
+  return q;
+}
+
+// The first steady batch of a shape captures the prep (body) graphs of all
+// kTables rotations at once, so the batches that follow never pay a capture
+// and instantiate (five warm-ups reached 2 of the 5 rotations,
+// leaving three captures inside the timed region). Capture only: nothing is
+// launched; the lanes' host look-back state is reset per capture (captured
+// launches bake context-relative tickets) and restored.
+static hps_status precapture_rotations(Tier* T, const BatchShape& sh, const BatchPlan& bp,
+                                       bool body) {
+  const int lanes[2] = {body ? 0 : 1, body ? 3 : 2};
+  std::uint64_t tk[2];
+  std::uint32_t lb[2];
+  for (int i = 0; i < 2; ++i) {
+    tk[i] = T->lane[lanes[i]].tickets;
+    lb[i] = T->lane[lanes[i]].lb_local;
+  }
+  const int cur = T->cur;
+  hps_status st = HPS_OK;
+  for (int r = 1; r < kTables && st == HPS_OK; ++r) {
+    const BatchPlan q = rotated(bp, r);
+    for (int i = 0; i < 2; ++i) {
+      T->lane[lanes[i]].tickets = tk[i];
+      T->lane[lanes[i]].lb_local = lb[i];
+    }
+    GraphEntry* ge = nullptr;
+    if (body) {
+      T->cur = q.tb;
+      st = capture_graph(T, body_key(T, sh, q), [&] { return enqueue_body(T, sh, q); }, &ge);
+    } else {
+      st = capture_graph(T, prep_key(T, sh, q), [&] { return enqueue_prep(T, sh, q); }, &ge);
+    }
+  }
+  T->cur = cur;
+  for (int i = 0; i < 2; ++i) {
+    T->lane[lanes[i]].tickets = tk[i];
+    T->lane[lanes[i]].lb_local = lb[i];
+  }
+  return st;
 }
 
 // Stage (H2D + counts + range check, st_stage) -> prep (lane 1) -> body
@@ -1847,10 +1995,11 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     HPS_CUDA(cudaMemcpyAsync(T->b_lab[sp], labels, B, cudaMemcpyHostToDevice, ss));
   }
   HPS_CUDA(cudaMemsetAsync(T->dsc->counts[sp], 0, sizeof(T->dsc->counts[sp]), ss));
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->serr[sp], 0, sizeof(DevError), ss));
   launch_on(T, ss, batch_count_kernel, kSMs * 4, 256, 0, (const std::int64_t*)T->b_off[sp],
             (const std::uint64_t*)T->b_keys[sp], B, G, T->g, J,
             T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts[sp],
-            &T->dsc->err);
+            &T->dsc->serr[sp]);
   // Host batch at one rank: the shape counts follow from the offsets alone
   // (per-shard occurrences; every key is owned), so the host does not wait
   // for the copy — the device counts and the key-range check (its error is
@@ -1872,7 +2021,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     mark_stage(T, HPS_T_STAGE);
     if (T->trace) cudaEventRecord(T->tr[sp][1], ss);
     HPS_CUDA(cudaEventRecord(T->ev_staged, ss));
-    HPS_TRY(check_device_error(T, "device table: missing key ", true, ss));
+    HPS_TRY(check_device_error(T, "device table: missing key ", true, ss, &T->dsc->serr[sp]));
   }
   for (int j = 0; j < J; ++j) bp.occ_total += T->hsc->counts[sp][j];
   const std::uint64_t own = T->hsc->counts[sp][J];
@@ -1928,12 +2077,10 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     open_lookback_context(T);
     hps_status st;
     if (T->use_graphs) {
-      const std::vector<std::uint64_t> key = {
-          1, B, sh.own_bound, sh.batch_bound, std::uint64_t(bp.tb), std::uint64_t(bp.tp + 1),
-          std::uint64_t(bp.tq + 1), std::uint64_t(bp.tq2 + 1), std::uint64_t(sp),
-          std::uint64_t(bp.prep_mbs), reinterpret_cast<std::uint64_t>(T->store),
-          T->store_keys, std::uint64_t(T->store_on_host), std::uint64_t(T->timing)};
-      st = run_graph(T, key, [&] { return enqueue_prep(T, sh, bp); });
+      const std::vector<std::uint64_t> key = prep_key(T, sh, bp);
+      st = HPS_OK;
+      if (steady(T, bp) && !T->graphs.count(key)) st = precapture_rotations(T, sh, bp, false);
+      if (st == HPS_OK) st = run_graph(T, key, [&] { return enqueue_prep(T, sh, bp); });
     } else {
       st = enqueue_prep(T, sh, bp);
     }
@@ -1973,11 +2120,8 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   T->ws_idx = T->wsib[bp.tb];
   T->ws_sorted = ws_sorted(T);
   if (T->use_graphs && bp.skip_mb < 0) {
-    std::vector<std::uint64_t> key = {2, B, sh.own_bound, std::uint64_t(bp.tb),
-                                      std::uint64_t(bp.tp + 1), std::uint64_t(bp.tq + 1),
-                                      std::uint64_t(bp.tq2 + 1), std::uint64_t(sp),
-                                      std::uint64_t(bp.prep_mbs), std::uint64_t(T->timing)};
-    for (int j = 0; j < J; ++j) key.push_back(sh.mb_bound[j]);
+    const std::vector<std::uint64_t> key = body_key(T, sh, bp);
+    if (steady(T, bp) && !T->graphs.count(key)) HPS_TRY(precapture_rotations(T, sh, bp, true));
     HPS_TRY(run_graph(T, key, [&] { return enqueue_body(T, sh, bp); }));
   } else {
     HPS_TRY(enqueue_body(T, sh, bp));
@@ -1985,12 +2129,16 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   BatchOut* ho = &T->hout[sp];
   const int tb = bp.tb;
   HPS_CUDA(cudaMemcpyAsync(&ho->loss, &T->dsc->loss, 16, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->fallbacks, &T->dsc->fallbacks, 16, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->fallbacks, &T->dsc->fallbacks, 40, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&ho->carried, &T->dsc->carried_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&ho->stored, &T->dsc->stored_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&ho->n_ws, &T->dsc->nws_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&ho->cap, &T->dsc->cap[tb], 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&ho->err, &T->dsc->err, sizeof(DevError), cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->err_stage, &T->dsc->serr[sp], sizeof(DevError),
+                           cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->err_prep, &T->dsc->perr[tb], sizeof(DevError),
+                           cudaMemcpyDeviceToHost, T->st));
   if (T->trace) cudaEventRecord(T->tr[sp][5], T->st);
   HPS_CUDA(cudaEventRecord(T->ev_body_tab[tb], T->st));
   HPS_CUDA(cudaEventRecord(T->ev_body_sp[sp], T->st));
@@ -2087,6 +2235,10 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     if (c.layer_dims[l] < 1 || c.layer_dims[l] > std::uint64_t(kMaxHidden))
       return set_error(HPS_ERR_ARG, "layer width must be in [1, %d]", kMaxHidden);
   if (c.embedding_dim > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
+  if (c.optimizer != HPS_OPT_SGD && c.optimizer != HPS_OPT_ADAGRAD)
+    return set_error(HPS_ERR_ARG, "config: optimizer must be HPS_OPT_SGD or HPS_OPT_ADAGRAD");
+  if (c.optimizer == HPS_OPT_ADAGRAD && !(c.adagrad_eps > 0.0f))
+    return set_error(HPS_ERR_ARG, "config: adagrad_eps must be positive");
   if (G > 1 && !nccl_id) return set_error(HPS_ERR_ARG, "nccl_id required when N*D > 1");
   if (G > 1 && !nccl().ok) return set_error(HPS_ERR_NCCL, "nccl: %s", nccl().why.c_str());
 
@@ -2098,6 +2250,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   t->g = c.rank;
   t->E = c.embedding_dim;
   t->J = c.minibatches;
+  t->RW = c.optimizer == HPS_OPT_ADAGRAD ? 2 * t->E : t->E;
+  t->opt = Optim{c.optimizer, t->E, t->RW, c.learning_rate, c.adagrad_eps};
   t->Bmax = std::max<std::uint64_t>(c.max_batch_examples, 1);
   t->Omax = std::max<std::uint64_t>(c.max_batch_keys, 1);
   t->Wmax = c.max_working_set ? c.max_working_set : t->Omax;
@@ -2162,6 +2316,13 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (e != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: cudaSetDevice(%d): %s", c.cuda_device,
                           cudaGetErrorString(e)));
+  {  // test knob: every certified sum takes its exact fallback (model.cuh)
+    const char* v = std::getenv("HPS_CERT_FORCE_FAIL");
+    const int force = v ? std::atoi(v) != 0 : 0;
+    e = cudaMemcpyToSymbol(g_cert_force_fail, &force, sizeof(int));
+    if (e != cudaSuccess)
+      return fail(set_error(HPS_ERR_CUDA, "cuda: %s", cudaGetErrorString(e)));
+  }
   {
     auto ev = [&](cudaEvent_t* x, bool timed) {
       if (e == cudaSuccess)
@@ -2248,7 +2409,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     return fail(set_error(HPS_ERR_CUDA, "cuda: host alloc: %s", cudaGetErrorString(e)));
   for (int i = 0; i < kTables; ++i) {
     A(tkeys[i], t->capmax);
-    A(tvals[i], t->capmax * E);
+    A(tvals[i], t->capmax * std::uint64_t(t->RW));
     A(wsb[i], W);
     A(wsib[i], W);
     A(csrc[i], W);
@@ -2394,10 +2555,8 @@ hps_status hps_destroy(hps_tier_t t) {
   for (int gl = 0; gl < kGroupLanes; ++gl)
     if (t->lane[2 + gl].st) cudaStreamSynchronize(t->lane[2 + gl].st);
   if (t->comm) nccl().CommDestroy(t->comm);
-  for (auto& c : t->pending) {
-    cudaFree(c.keys);
-    cudaFree(c.deltas);
-  }
+  cudaFree(t->pend_keys);
+  cudaFree(t->pend_deltas);
   for (auto& kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
   for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : t->allocs) cudaFree(p);
@@ -2444,6 +2603,19 @@ hps_status hps_destroy(hps_tier_t t) {
   HPS_ENTER(t);        \
   HPS_TRY(quiesce(t))
 
+// The growable staging scratch (HostValue rows of hps_build, hps_dump's
+// rows), at least `floats` floats.
+static hps_status ensure_staged(Tier* t, std::uint64_t floats) {
+  if (t->staged_cap >= floats) return HPS_OK;
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  if (t->staged) cudaFree(t->staged);
+  t->staged = nullptr;
+  t->staged_cap = 0;
+  HPS_CUDA(cudaMalloc(&t->staged, floats * 4));
+  t->staged_cap = floats;
+  return HPS_OK;
+}
+
 hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float* host_rows) {
   HPS_ENTER_Q(t);
   if (n > t->Wmax)
@@ -2461,14 +2633,8 @@ hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float
   }
   const float* staged = nullptr;
   if (host_rows && n) {
-    if (t->staged_cap < n) {
-      if (t->staged) cudaFree(t->staged);
-      t->staged = nullptr;
-      t->staged_cap = 0;
-      HPS_CUDA(cudaMalloc(&t->staged, n * std::uint64_t(t->E) * 4));
-      t->staged_cap = n;
-    }
-    HPS_CUDA(cudaMemcpyAsync(t->staged, host_rows, n * std::uint64_t(t->E) * 4,
+    HPS_TRY(ensure_staged(t, n * std::uint64_t(t->RW)));
+    HPS_CUDA(cudaMemcpyAsync(t->staged, host_rows, n * std::uint64_t(t->RW) * 4,
                              cudaMemcpyHostToDevice, t->st));
     staged = t->staged;
   }
@@ -2572,14 +2738,35 @@ hps_status hps_push(hps_tier_t t, const uint64_t* keys, const float* deltas, uin
     }
   }
   if (dup) return set_error(HPS_ERR_ARG, "push: keys must be unique (a key->delta map)");
+  const std::uint64_t E = std::uint64_t(t->E);
+  std::uint64_t need = t->pend_used;
+  for (int s = 0; s < t->G; ++s) need += cnt[s];
+  if (need > t->pend_cap) {  // grow the arena (doubling), keeping what is pending
+    const std::uint64_t nc = std::max<std::uint64_t>(need, 2 * t->pend_cap);
+    std::uint64_t* nk = nullptr;
+    float* nd = nullptr;
+    HPS_CUDA(cudaMalloc(&nk, nc * 8));
+    HPS_CUDA(cudaMalloc(&nd, nc * E * 4));
+    if (t->pend_used) {
+      HPS_CUDA(cudaMemcpyAsync(nk, t->pend_keys, t->pend_used * 8, cudaMemcpyDeviceToDevice, t->st));
+      HPS_CUDA(cudaMemcpyAsync(nd, t->pend_deltas, t->pend_used * E * 4, cudaMemcpyDeviceToDevice,
+                               t->st));
+    }
+    HPS_CUDA(cudaStreamSynchronize(t->st));
+    cudaFree(t->pend_keys);
+    cudaFree(t->pend_deltas);
+    t->pend_keys = nk;
+    t->pend_deltas = nd;
+    t->pend_cap = nc;
+  }
   for (int s = 0; s < t->G; ++s) {
     if (!cnt[s]) continue;
-    PendingChunk c{s, cnt[s], nullptr, nullptr};
-    HPS_CUDA(cudaMalloc(&c.keys, c.n * 8));
-    HPS_CUDA(cudaMalloc(&c.deltas, c.n * std::uint64_t(t->E) * 4));
-    HPS_CUDA(cudaMemcpyAsync(c.keys, srckeys[s], c.n * 8, cudaMemcpyDeviceToDevice, t->st));
-    HPS_CUDA(cudaMemcpyAsync(c.deltas, srcdel[s], c.n * std::uint64_t(t->E) * 4,
+    PendingChunk c{s, cnt[s], t->pend_used};
+    HPS_CUDA(cudaMemcpyAsync(t->pend_keys + c.at, srckeys[s], c.n * 8, cudaMemcpyDeviceToDevice,
+                             t->st));
+    HPS_CUDA(cudaMemcpyAsync(t->pend_deltas + c.at * E, srcdel[s], c.n * E * 4,
                              cudaMemcpyDeviceToDevice, t->st));
+    t->pend_used += c.n;
     t->pending.push_back(c);
   }
   HPS_CUDA(cudaStreamSynchronize(t->st));
@@ -2597,24 +2784,23 @@ hps_status hps_drain(hps_tier_t t) {
       const std::uint64_t work = c.n * std::uint64_t(t->E / V);
       if (V == 4)
         launch(t, table_apply_kernel<4>, grid_for(work), 256, 0,
-               (const std::uint32_t*)nullptr, (const std::uint64_t*)c.keys,
+               (const std::uint32_t*)nullptr, (const std::uint64_t*)(t->pend_keys + c.at),
                (const std::uint64_t*)t->tkeys[t->cur],
-               (const std::uint64_t*)&t->dsc->cap[t->cur], (const float*)c.deltas,
-               (const std::uint64_t*)nullptr, c.n, t->tvals[t->cur], t->E, &t->dsc->err);
+               (const std::uint64_t*)&t->dsc->cap[t->cur],
+               (const float*)(t->pend_deltas + c.at * std::uint64_t(t->E)),
+               (const std::uint64_t*)nullptr, c.n, t->tvals[t->cur], t->opt, &t->dsc->err);
       else
         launch(t, table_apply_kernel<1>, grid_for(work), 256, 0,
-               (const std::uint32_t*)nullptr, (const std::uint64_t*)c.keys,
+               (const std::uint32_t*)nullptr, (const std::uint64_t*)(t->pend_keys + c.at),
                (const std::uint64_t*)t->tkeys[t->cur],
-               (const std::uint64_t*)&t->dsc->cap[t->cur], (const float*)c.deltas,
-               (const std::uint64_t*)nullptr, c.n, t->tvals[t->cur], t->E, &t->dsc->err);
+               (const std::uint64_t*)&t->dsc->cap[t->cur],
+               (const float*)(t->pend_deltas + c.at * std::uint64_t(t->E)),
+               (const std::uint64_t*)nullptr, c.n, t->tvals[t->cur], t->opt, &t->dsc->err);
     }
   }
   const hps_status s = check_device_error(t, "device table: accumulate to missing key ");
-  for (auto& c : t->pending) {
-    cudaFree(c.keys);
-    cudaFree(c.deltas);
-  }
   t->pending.clear();
+  t->pend_used = 0;
   return s;
 }
 
@@ -2633,13 +2819,19 @@ hps_status hps_table_info(hps_tier_t t, uint64_t* capacity, uint64_t* occupancy,
   return HPS_OK;
 }
 
+hps_status hps_row_width(hps_tier_t t, uint64_t* row_width) {
+  if (!t || !row_width) return set_error(HPS_ERR_ARG, "null argument");
+  *row_width = std::uint64_t(t->RW);
+  return HPS_OK;
+}
+
 hps_status hps_table_slots(hps_tier_t t, uint64_t* slot_keys, float* rows) {
   std::uint64_t cap = 0;
   HPS_TRY(hps_table_info(t, &cap, nullptr, nullptr));
   if (slot_keys)
     HPS_CUDA(cudaMemcpyAsync(slot_keys, t->tkeys[t->cur], cap * 8, cudaMemcpyDeviceToHost, t->st));
   if (rows)
-    HPS_CUDA(cudaMemcpyAsync(rows, t->tvals[t->cur], cap * std::uint64_t(t->E) * 4,
+    HPS_CUDA(cudaMemcpyAsync(rows, t->tvals[t->cur], cap * std::uint64_t(t->RW) * 4,
                              cudaMemcpyDeviceToHost, t->st));
   HPS_CUDA(cudaStreamSynchronize(t->st));
   return HPS_OK;
@@ -2662,22 +2854,23 @@ hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t*
     radix_sort(t, t->lane[0].kB, nullptr, Count{nullptr, occ}, occ, t->sort_bits, false, &sk, &so);
     wsk = sk;
   }
-  const int V = vec_of(t->E);
-  const std::uint64_t work = occ * std::uint64_t(t->E / V);
+  const int V = vec_of(t->RW);
+  const std::uint64_t work = occ * std::uint64_t(t->RW / V);
+  if (occ) HPS_TRY(ensure_staged(t, occ * std::uint64_t(t->RW)));
   if (occ) {
     if (V == 4)
       launch(t, table_dump_kernel<4>, grid_for(work), 256, 0, wsk,
              (const std::uint64_t*)&t->dsc->nws_tab[t->cur], (const std::uint64_t*)t->tkeys[t->cur],
              (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
-             (float*)nullptr, std::uint64_t(0), t->rows, t->E, &t->dsc->err);
+             (float*)nullptr, std::uint64_t(0), t->staged, t->RW, &t->dsc->err);
     else
       launch(t, table_dump_kernel<1>, grid_for(work), 256, 0, wsk,
              (const std::uint64_t*)&t->dsc->nws_tab[t->cur], (const std::uint64_t*)t->tkeys[t->cur],
              (const float*)t->tvals[t->cur], (const std::uint64_t*)&t->dsc->cap[t->cur],
-             (float*)nullptr, std::uint64_t(0), t->rows, t->E, &t->dsc->err);
+             (float*)nullptr, std::uint64_t(0), t->staged, t->RW, &t->dsc->err);
     if (keys_out) HPS_CUDA(cudaMemcpyAsync(keys_out, wsk, occ * 8, cudaMemcpyDeviceToHost, t->st));
     if (rows_out)
-      HPS_CUDA(cudaMemcpyAsync(rows_out, t->rows, occ * std::uint64_t(t->E) * 4,
+      HPS_CUDA(cudaMemcpyAsync(rows_out, t->staged, occ * std::uint64_t(t->RW) * 4,
                                cudaMemcpyDeviceToHost, t->st));
   }
   HPS_TRY(check_device_error(t, "device table: missing key "));
@@ -2687,7 +2880,7 @@ hps_status hps_dump(hps_tier_t t, uint64_t* keys_out, float* rows_out, uint64_t*
 
 hps_status hps_dense_sync(hps_tier_t t, float* buf, uint64_t len, int deterministic) {
   HPS_ENTER_Q(t);
-  (void)deterministic;  // the canonical f64 sum serves both modes
+  (void)deterministic;  // the canonical f64 sum serves both modes (hps_gpu.h)
   if (len == 0 || t->G == 1) return HPS_OK;  // a single replica is untouched
   const std::uint64_t nw = std::uint64_t(t->md.nw);
   float* sum = t->hstage;
@@ -2767,7 +2960,7 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
                         at.type == cudaMemoryTypeHost;
     cudaGetLastError();
     if (!pinned) {
-      HPS_CUDA(cudaHostRegister(rows, num_keys * std::uint64_t(t->E) * 4,
+      HPS_CUDA(cudaHostRegister(rows, num_keys * std::uint64_t(t->RW) * 4,
                                 cudaHostRegisterMapped | cudaHostRegisterPortable));
       t->store_registered = true;
       t->store_host = rows;
@@ -2802,6 +2995,12 @@ hps_status hps_reset_timing(hps_tier_t t) {
 hps_status hps_kernel_launches(hps_tier_t t, uint64_t* n) {
   if (!t || !n) return set_error(HPS_ERR_ARG, "null argument");
   *n = t->launches;
+  return HPS_OK;
+}
+
+hps_status hps_graph_captures(hps_tier_t t, uint64_t* n) {
+  if (!t || !n) return set_error(HPS_ERR_ARG, "null argument");
+  *n = t->graph_captures;
   return HPS_OK;
 }
 

@@ -60,6 +60,8 @@ class HpsConfig(ctypes.Structure):
         ("max_batch_examples", ctypes.c_uint64),
         ("max_batch_keys", ctypes.c_uint64),
         ("max_working_set", ctypes.c_uint64),
+        ("optimizer", ctypes.c_int),
+        ("adagrad_eps", ctypes.c_float),
     ]
 
 
@@ -75,10 +77,15 @@ class HpsBatchStats(ctypes.Structure):
         ("carried_rows", ctypes.c_uint64),
         ("exact_fallbacks", ctypes.c_uint64),
         ("store_rows", ctypes.c_uint64),
+        ("big_segments", ctypes.c_uint64),
+        ("max_segment_chunks", ctypes.c_uint64),
+        ("big_occurrences", ctypes.c_uint64),
     ]
 
+OPTIMIZERS = {"sgd": 0, "adagrad": 1}
+
 TIMING_SLOTS = ["total", "stage", "build", "dedup", "pull", "fwdbwd", "grads", "apply",
-                "dense", "writeback", "sparse"]
+                "dense", "writeback", "sparse", "big_fused"]
 
 
 # Every symbol include/hps_gpu.h declares, with its ctypes signature.
@@ -114,6 +121,8 @@ _SIGS = {
     "hps_get_timing": ([_P, _P], ctypes.c_int),
     "hps_reset_timing": ([_P], ctypes.c_int),
     "hps_kernel_launches": ([_P, _U64P], ctypes.c_int),
+    "hps_graph_captures": ([_P, _U64P], ctypes.c_int),
+    "hps_row_width": ([_P, _U64P], ctypes.c_int),
     "hps_set_graphs": ([_P, ctypes.c_int], ctypes.c_int),
     "hps_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
     "hps_crc32": ([ctypes.c_uint32, _P, _U64], ctypes.c_uint32),
@@ -251,7 +260,8 @@ class Tier:
                  seed: int = 42, minibatches: int = 4, deterministic: bool = True,
                  inject_skip_sync: int = -1, key_space: int = 0,
                  max_batch_examples: int = 1 << 16, max_batch_keys: int = 1 << 20,
-                 max_working_set: int = 0, nccl_id: Optional[bytes] = None):
+                 max_working_set: int = 0, nccl_id: Optional[bytes] = None,
+                 optimizer: str = "sgd", adagrad_eps: float = 1e-8):
         cfg = HpsConfig()
         cfg.nodes, cfg.devices_per_node, cfg.rank = nodes, devices, rank
         cfg.cuda_device, cfg.embedding_dim = cuda_device, width
@@ -269,8 +279,14 @@ class Tier:
         cfg.max_batch_examples = max_batch_examples
         cfg.max_batch_keys = max_batch_keys
         cfg.max_working_set = max_working_set
+        if optimizer not in OPTIMIZERS:
+            raise Error(1, f"config: unknown optimizer {optimizer!r}")
+        cfg.optimizer = OPTIMIZERS[optimizer]
+        cfg.adagrad_eps = adagrad_eps
         self.cfg = cfg
         self.width = width
+        # floats per table / store row: the embedding, then the Adagrad state
+        self.row_width = 2 * width if optimizer == "adagrad" else width
         self.topology = Topology(nodes, devices)
         self.rank = rank
         self._h = ctypes.c_void_p(0)
@@ -298,7 +314,7 @@ class Tier:
     def build(self, keys, host_rows=None) -> None:
         k = _u64(keys)
         rows = None if host_rows is None else _f32(host_rows).reshape(-1)
-        if rows is not None and rows.size != k.size * self.width:
+        if rows is not None and rows.size != k.size * self.row_width:
             raise Error(7, "hbm: host value width mismatch")
         _check(lib().hps_build(self._h, _ptr(k), k.size,
                                _ptr(rows) if rows is not None else None))
@@ -328,7 +344,7 @@ class Tier:
     def table_slots(self, with_rows: bool = False):
         cap, _, _ = self.table_info()
         keys = np.empty(cap, dtype=np.uint64)
-        rows = np.empty((cap, self.width), dtype=np.float32) if with_rows else None
+        rows = np.empty((cap, self.row_width), dtype=np.float32) if with_rows else None
         _check(lib().hps_table_slots(self._h, _ptr(keys),
                                      _ptr(rows) if with_rows else None))
         return (keys, rows) if with_rows else keys
@@ -336,7 +352,7 @@ class Tier:
     def dump(self):
         _, occ, _ = self.table_info()
         keys = np.empty(occ, dtype=np.uint64)
-        rows = np.empty((occ, self.width), dtype=np.float32)
+        rows = np.empty((occ, self.row_width), dtype=np.float32)
         n = ctypes.c_uint64()
         _check(lib().hps_dump(self._h, _ptr(keys), _ptr(rows), ctypes.byref(n)))
         return keys[: n.value], rows[: n.value]
@@ -370,8 +386,8 @@ class Tier:
         _check(lib().hps_set_dense(self._h, _ptr(a)))
 
     def attach_store(self, rows, on_device: bool = False, num_keys: Optional[int] = None):
-        """rows: host numpy float32 [num_keys, E] (kept alive here) or a device
-        pointer (int) with num_keys."""
+        """rows: host numpy float32 [num_keys, row_width] (kept alive here) or a
+        device pointer (int) with num_keys."""
         if rows is None:
             _check(lib().hps_attach_store(self._h, None, 0, 0))
             self._store = None
@@ -381,6 +397,8 @@ class Tier:
         else:
             if rows.dtype != np.float32 or not rows.flags.c_contiguous:
                 raise Error(1, "store must be a C-contiguous float32 array")
+            if rows.ndim != 2 or rows.shape[1] != self.row_width:
+                raise Error(7, "hbm: value store row width mismatch")
             _check(lib().hps_attach_store(self._h, _ptr(rows), rows.shape[0], 0))
             self._store = rows
 
@@ -442,6 +460,11 @@ class Tier:
     def kernel_launches(self) -> int:
         n = ctypes.c_uint64()
         _check(lib().hps_kernel_launches(self._h, ctypes.byref(n)))
+        return n.value
+
+    def graph_captures(self) -> int:
+        n = ctypes.c_uint64()
+        _check(lib().hps_graph_captures(self._h, ctypes.byref(n)))
         return n.value
 
     def stream(self) -> int:

@@ -35,11 +35,13 @@ class Cfg(ctypes.Structure):
         ("learning_rate", ctypes.c_float), ("seed", ctypes.c_uint64),
         ("minibatches", ctypes.c_int), ("deterministic", ctypes.c_int),
         ("inject_skip_sync", ctypes.c_int64),
+        # extension fields (or_cfg only; RefCfg stops before them)
+        ("optimizer", ctypes.c_int), ("adagrad_eps", ctypes.c_float),
     ]
 
 
 def make_cfg(nodes=1, devices=1, E=8, layers=(8, 16, 1), lr=0.05, seed=42, J=4,
-             det=True, skip=-1) -> Cfg:
+             det=True, skip=-1, optimizer="sgd", eps=1e-8) -> Cfg:
     c = Cfg()
     c.nodes, c.devices, c.embedding_dim = nodes, devices, E
     c.num_layers = len(layers)
@@ -50,6 +52,8 @@ def make_cfg(nodes=1, devices=1, E=8, layers=(8, 16, 1), lr=0.05, seed=42, J=4,
     c.minibatches = J
     c.deterministic = int(det)
     c.inject_skip_sync = skip
+    c.optimizer = {"sgd": 0, "adagrad": 1}[optimizer]
+    c.adagrad_eps = eps
     return c
 
 
@@ -81,6 +85,7 @@ class Oracle:
         L.or_canonical_sum.argtypes = [ctypes.c_int, ctypes.c_int, _P, _U64, _P]
         L.or_average_apply.argtypes = [_P, _P, _U64, ctypes.c_int, ctypes.c_float]
         L.or_sgd_accumulate.argtypes = [_P, _P, _U64, ctypes.c_float]
+        L.or_adagrad_apply.argtypes = [_P, _P, _P, _U64, ctypes.c_float, ctypes.c_float]
         L.or_train_reference.argtypes = [ctypes.POINTER(Cfg), _U64, _U64, _P, _P, _P, _P,
                                          ctypes.POINTER(_U64), _P, _P, _U64]
         L.or_auc.argtypes, L.or_auc.restype = [_P, _P, _U64], ctypes.c_double
@@ -152,6 +157,14 @@ class Oracle:
         self.L.or_canonical_sum(nodes, devices, ptr(b), b.shape[1], ptr(out))
         return out
 
+    def adagrad_apply(self, v, s, g, lr, eps):
+        """or_adagrad_apply in place on float32 copies; returns (v, s)."""
+        v = np.array(v, dtype=np.float32)
+        s = np.array(s, dtype=np.float32)
+        g = np.ascontiguousarray(g, dtype=np.float32)
+        self.L.or_adagrad_apply(ptr(v), ptr(s), ptr(g), v.size, lr, eps)
+        return v, s
+
     def train_reference(self, cfg: Cfg, batch_size, offsets, keys, labels):
         o = np.ascontiguousarray(offsets, dtype=np.int64)
         k = np.ascontiguousarray(keys, dtype=np.uint64)
@@ -160,7 +173,7 @@ class Oracle:
         dense = np.empty(dense_count(E, list(cfg.layer_dims)[: cfg.num_layers]), np.float32)
         cap = max(1, len(np.unique(k)))
         sk = np.empty(cap, dtype=np.uint64)
-        sr = np.empty((cap, E), dtype=np.float32)
+        sr = np.empty((cap, 2 * E if cfg.optimizer == 1 else E), dtype=np.float32)
         n = _U64()
         rc = self.L.or_train_reference(ctypes.byref(cfg), batch_size, o.size - 1, ptr(o), ptr(k),
                                        ptr(lab), ptr(dense), ctypes.byref(n), ptr(sk), ptr(sr),
@@ -304,6 +317,14 @@ class RefLib:
                                              ptr(args[4]), ptr(args[5]), args[4].size, ptr(preds),
                                              ptr(dg), ptr(sg)))
         return preds, dg, sg
+
+    def adagrad_apply(self, v, s, g, lr, eps):
+        """or_adagrad_apply in place on float32 copies; returns (v, s)."""
+        v = np.array(v, dtype=np.float32)
+        s = np.array(s, dtype=np.float32)
+        g = np.ascontiguousarray(g, dtype=np.float32)
+        self.L.or_adagrad_apply(ptr(v), ptr(s), ptr(g), v.size, lr, eps)
+        return v, s
 
     def train_reference(self, cfg: Cfg, batch_size, offsets, keys, labels):
         o = np.ascontiguousarray(offsets, np.int64)

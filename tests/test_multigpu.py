@@ -28,3 +28,4 @@ def test_multi_rank_parity():
     out = p.stdout + p.stderr
     assert p.returncode == 0, out[-6000:]
     assert "CASE train_e8: PASS" in out
+    assert "CASE train_adagrad: PASS" in out

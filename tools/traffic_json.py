@@ -4,7 +4,8 @@ kernels (tools/profile_r.sh: sparse_traffic.csv).
 traffic = dram__bytes_read.sum + dram__bytes_write.sum summed over the
 kernels of one mini-batch (big_classify, big_plan, big_fused, sparse_short),
 averaged over the mini-batches captured. bench.py reports it as
-roofline.traffic for the "sparse" phase.
+roofline.traffic for the "sparse" phase, and big_fused_kernel's own per-launch
+traffic as roofline.kernels.big_fused_kernel.traffic.
 
 usage: python tools/traffic_json.py gpurun_out/sparse_traffic.csv [config]
 """
@@ -41,6 +42,10 @@ def main() -> None:
     except (OSError, ValueError):
         doc = {}
     doc.setdefault(config, {})["sparse"] = int(round(total / max(mbs, 1)))
+    big = [l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0)
+           for l in launches if "big_fused" in l["name"]]
+    if big:  # per launch of big_fused_kernel alone
+        doc[config]["big_fused"] = int(round(sum(big) / len(big)))
     doc["_note"] = (
         "dram__bytes_read.sum + dram__bytes_write.sum summed over the sparse segment-reduce "
         "kernels of one mini-batch (" + ", ".join(KERNELS) + "), averaged over " + str(mbs) +
