@@ -56,6 +56,13 @@ CONFIGS = {
                opt="adagrad",
                text="c3: 100M-key table, E=64 with Adagrad state (rows of 2E floats), batch "
                     "65536, 100 uniform keys/example, MLP {8,16,1}, J=4"),
+    # the multi-slot ads model (100 fields, multi-hot up to 300
+    # keys/example, key = slot * 1e6 + id) with the wide MLP on tcgen05
+    "c4": dict(dims=100 * 10**6, E=16, B=16384, nnz=300, zipf=True, J=4,
+               layers=(512, 256, 128, 1), gen="multislot",
+               text="c4: multi-slot ads model, 100 slots x 1M ids (100M-key table), multi-hot "
+                    "1..300 keys/example (Zipf ids), E=16 sum-combined, MLP {512,256,128,1} "
+                    "(3xTF32 tcgen05 GEMMs), batch 16384, J=4"),
     # the MEM-PS host tier at scale (1B keys x E=16 = 64 GB of
     # store; GPU box only)
     "c5": dict(dims=10**9, E=16, B=131072, nnz=100, zipf=False, J=4, layers=(8, 16, 1),
@@ -151,6 +158,16 @@ def host_threads() -> int:
     return p
 
 
+def make_data(c, n, seed=1):
+    """The config's synthetic batch stream: the reference gen_dataset
+    restatement, or (c4) the multi-slot generator (no reference one exists)."""
+    import paper_2003_05622_b200 as pkg
+    if c.get("gen") == "multislot":
+        return pkg.gen_multislot(n, slots=100, ids_per_slot=c["dims"] // 100,
+                                 max_keys=c["nnz"], seed=seed)
+    return pkg.gen_dataset(c["dims"], n, c["nnz"], zipf=c["zipf"], seed=seed)
+
+
 def run_reference_hot_path(cfgname, steps, warmup, threads, budget_s=60.0):
     """The reference's own HBM-PS hot path (oracle/_ref, the unmodified
     headers): one std::thread per simulated device running the device-worker
@@ -161,7 +178,10 @@ def run_reference_hot_path(cfgname, steps, warmup, threads, budget_s=60.0):
     c = CONFIGS[cfgname]
     ref = RefLib()
     pool = max(1, min(steps + warmup, 4))
-    off, keys, lab = ref.gen_dataset(c["dims"], pool * c["B"], c["nnz"], c["zipf"])
+    if c.get("gen") == "multislot":
+        off, keys, lab = make_data(c, pool * c["B"])
+    else:
+        off, keys, lab = ref.gen_dataset(c["dims"], pool * c["B"], c["nnz"], c["zipf"])
     cfg = make_cfg(1, threads, c["E"], c["layers"], J=c["J"], det=True)
     hp = RefHotPath(ref, cfg, c["B"], off, keys, lab)
     if warmup:
@@ -251,7 +271,7 @@ def run_ours(args, rank, world, local_rank):
 
     # batch pool (identical on every rank: the node's batch stream)
     P = args.pool
-    off, keys, lab = pkg.gen_dataset(dims, P * B, nnz, zipf=c["zipf"], seed=1)
+    off, keys, lab = make_data(c, P * B)
     batches = []
     for b in range(P):
         o = (off[b * B:(b + 1) * B + 1] - off[b * B]).astype(np.int64)

@@ -183,6 +183,12 @@ hps_status hps_dump(hps_tier_t h, uint64_t* keys_out, float* rows_out,
  * width = E, the embedding width. */
 hps_status hps_table_info(hps_tier_t h, uint64_t* capacity,
                           uint64_t* occupancy, uint64_t* width);
+/* DeviceTable::contains / get (device_table.hpp:76-85) for a batch of keys
+ * against this rank's current table, without the missing-key error:
+ * found[i] = 1 and, if rows is non-NULL, rows[i] = the key's row
+ * (hps_row_width() floats), else found[i] = 0. Local (not collective). */
+hps_status hps_table_lookup(hps_tier_t h, const uint64_t* keys, uint64_t n, uint8_t* found,
+                            float* rows);
 /* Floats per table / value-store row: E (SGD) or 2E (Adagrad). */
 hps_status hps_row_width(hps_tier_t h, uint64_t* row_width);
 /* Slot-level view for placement parity: slot_keys[capacity] (empty slots
@@ -288,6 +294,17 @@ hps_status hps_kernel_launches(hps_tier_t h, uint64_t* n);
  * region: zero means it timed replays only. */
 hps_status hps_graph_captures(hps_tier_t h, uint64_t* n);
 
+/* Diagnostics: one tcgen05 TF32 GEMM of the wide-MLP path (mlp.cuh) on
+ * device pointers, synchronous: D(m, n) = sum_k A(m, k) B(n, k) with
+ * A(m, k) = A[m*a_m + k*a_k], B(n, k) = B[n*b_n + k*b_k] (b_ones_col: row
+ * N-1 of B is all ones), epilogue epi: 0 store (split-K slice z at
+ * D + z*M*ldd), 1 bias + relu, 2 mask(m, n) = mask[m*ldm + n] > 0, 3 f64 to
+ * Dd. For the numerics tests against a PyTorch fp32 reference. */
+hps_status hps_debug_gemm_tf32(int M, int N, int K, const float* A, int64_t a_m, int64_t a_k,
+                               const float* B, int64_t b_n, int64_t b_k, int b_ones_col, int epi,
+                               float* D, double* Dd, int64_t ldd, const float* bias,
+                               const float* mask, int64_t ldm, int splits);
+
 /* The CUDA stream the handle launches on (cudaStream_t as void*). */
 hps_status hps_stream(hps_tier_t h, void** stream);
 
@@ -333,6 +350,16 @@ hps_status hps_export(hps_tier_t h, const char* dir, uint32_t file_capacity,
                       uint64_t first_id, uint64_t* files_out);
 
 /* -------------------------------------------------- synthetic inputs */
+
+/* BASELINE config 4's multi-slot input (a new generator; the reference has
+ * none): T ~ U{1..max_keys} draws per example of key = slot * ids_per_slot +
+ * id, slot uniform over `slots`, id ~ Zipf(zipf_s); sorted unique per example;
+ * planted-logistic labels. keys must hold num_examples * max_keys entries;
+ * *n_keys_out = offsets[num_examples]. Host-only. */
+hps_status hps_gen_multislot(uint64_t slots, uint64_t ids_per_slot, uint64_t num_examples,
+                             uint64_t max_keys, double zipf_s, uint64_t seed,
+                             double signal_scale, int64_t* offsets, uint64_t* keys,
+                             uint8_t* labels, uint64_t* n_keys_out);
 
 /* The reference generator gen_dataset (dataset.hpp:180-227) restated
  * byte-for-byte (mt19937_64 stream, planted logistic labels, inverse-CDF

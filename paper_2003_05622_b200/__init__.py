@@ -6,7 +6,7 @@ ctypes binding plus a host-side mirror of the reference ``hps::HbmTier`` API.
 """
 from . import hps  # noqa: F401
 from .hps import (DeviceTable, Error, HbmTier, Tier, Topology, canonical_order,  # noqa: F401
-                  gen_dataset, lib, synchronize, unique_id)
+                  gen_dataset, gen_multislot, lib, synchronize, unique_id)
 
-__all__ = ["hps", "Tier", "HbmTier", "DeviceTable", "Topology", "Error", "gen_dataset",
+__all__ = ["hps", "Tier", "HbmTier", "DeviceTable", "Topology", "Error", "gen_dataset", "gen_multislot",
            "synchronize", "canonical_order", "unique_id", "lib"]

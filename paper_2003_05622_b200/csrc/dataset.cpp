@@ -153,3 +153,49 @@ extern "C" hps_status hps_gen_dataset(uint64_t dims, uint64_t num_examples,
   offsets[num_examples] = int64_t(num_examples * nnz);
   return HPS_OK;
 }
+
+// BASELINE config 4's multi-slot ads input (no reference generator exists;
+// SURVEY 8(d) c4): every example draws T ~ U{1..max_keys} (slot, id) pairs,
+// slot ~ U{0..slots-1}, id ~ Zipf(zipf_s) over ids_per_slot (a hot head per
+// slot), key = slot * ids_per_slot + id, kept sorted and unique per example
+// (so an example holds up to max_keys keys over up to `slots` fields,
+// multi-hot within a field). Labels follow the planted logistic of
+// gen_dataset over the example's keys. One mt19937_64 stream: deterministic.
+extern "C" hps_status hps_gen_multislot(uint64_t slots, uint64_t ids_per_slot,
+                                        uint64_t num_examples, uint64_t max_keys,
+                                        double zipf_s, uint64_t seed, double signal_scale,
+                                        int64_t* offsets, uint64_t* keys, uint8_t* labels,
+                                        uint64_t* n_keys_out) {
+  using namespace hpsgpu;
+  if (!slots || !ids_per_slot || !max_keys)
+    return set_error(HPS_ERR_ARG, "gen: slots, ids_per_slot and max_keys must be positive");
+  if (slots > ~std::uint64_t(0) / ids_per_slot)
+    return set_error(HPS_ERR_ARG, "gen: key space overflows 64 bits");
+  if (!offsets || !keys || !labels || !n_keys_out)
+    return set_error(HPS_ERR_ARG, "gen: null output buffer");
+  std::mt19937_64 rng(seed);
+  const ZipfTable zt(ids_per_slot, zipf_s);
+  const PlantedModel pm{0, stream_value(seed, 100), stream_value(seed, 101), signal_scale, 1};
+  std::uint64_t at = 0;
+  for (std::uint64_t e = 0; e < num_examples; ++e) {
+    offsets[e] = int64_t(at);
+    std::uint64_t* f = keys + at;
+    std::size_t have = 0;
+    const std::uint64_t T =
+        1 + std::min<std::uint64_t>(std::uint64_t(unit_of(rng()) * double(max_keys)), max_keys - 1);
+    for (std::uint64_t t = 0; t < T; ++t) {
+      const std::uint64_t s =
+          std::min<std::uint64_t>(std::uint64_t(unit_of(rng()) * double(slots)), slots - 1);
+      const std::uint64_t id = zt.draw(unit_of(rng()));
+      insert_sorted(f, have, s * ids_per_slot + id);
+    }
+    at += have;
+    double z = 0.0;
+    for (std::size_t i = 0; i < have; ++i) z += pm.weight(f[i]);
+    const double p = 1.0 / (1.0 + std::exp(-z * signal_scale / std::sqrt(double(have))));
+    labels[e] = (unit_of(rng()) < p) ? 1 : 0;
+  }
+  offsets[num_examples] = int64_t(at);
+  *n_keys_out = at;
+  return HPS_OK;
+}

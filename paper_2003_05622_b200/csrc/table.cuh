@@ -548,6 +548,27 @@ __global__ void table_gather_kernel(const std::uint64_t* __restrict__ qkeys,
   }
 }
 
+// Local lookups (DeviceTable::contains / get, device_table.hpp:76-85) without
+// the missing-key error: found[i] = 1 and the key's RW-float row (when rows
+// is non-null), else found[i] = 0. One thread per key.
+__global__ void table_lookup_kernel(const std::uint64_t* __restrict__ qkeys, std::uint64_t n,
+                                    const std::uint64_t* __restrict__ keys,
+                                    const float* __restrict__ vals,
+                                    const std::uint64_t* __restrict__ cap_ptr, int RW,
+                                    std::uint8_t* __restrict__ found, float* __restrict__ rows) {
+  pdl_wait();
+  const std::uint64_t cap = *cap_ptr;
+  for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t key = qkeys[i];
+    const std::uint32_t slot = key == kEmptyKey ? kNoSlot : probe_slot(keys, cap, key);
+    found[i] = slot != kNoSlot;
+    if (rows)
+      for (int d = 0; d < RW; ++d)
+        rows[i * RW + d] = slot != kNoSlot ? vals[std::uint64_t(slot) * RW + d] : 0.0f;
+  }
+}
+
 // Owner apply of one sender's segment (device_table.hpp:88-95): v += d in
 // f32, no contraction (or the Adagrad step, Optim). Keys inside one segment
 // are unique, so no atomics; segments are launched in canonical sender order

@@ -36,6 +36,7 @@
 #include "sort.cuh"
 #include "table.cuh"
 #include "group.cuh"
+#include "mlp.cuh"
 #include "tier_internal.h"
 
 namespace hpsgpu {
@@ -330,6 +331,18 @@ struct Tier {
 
   // model
   double *H = nullptr, *DL = nullptr, *DX = nullptr, *dpart = nullptr;
+  // wide MLP path (mlp.cuh; a hidden layer wider than kMaxHidden, or
+  // HPS_WIDE=1): per-shard activations and deltas (f32, [nshard][width]),
+  // split-K partials of the weight gradients
+  bool wide = false;
+  bool gemm_split3 = true;   // 3xTF32 (HPS_TF32_1X=1: plain TF32)
+  std::uint64_t nshard = 0;  // examples of a mini-batch shard, at most
+  float* wX = nullptr;
+  float* wH[kMaxLayers] = {};
+  float* wdZ[kMaxLayers] = {};
+  float* wdz = nullptr;
+  float* wP = nullptr;
+  std::uint64_t wP_cap = 0;
   double *dg_off = nullptr, *dg_tot = nullptr;  // dense-grad slice offsets, totals
   float *dense = nullptr, *dgrad = nullptr;
 
@@ -1100,6 +1113,102 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
   return HPS_OK;
 }
 
+// One tcgen05 GEMM (mlp.cuh) on stream s; BN by N, split-K over grid.z.
+static void launch_gemm(Tier* t, cudaStream_t s, GemmArgs g, int splits = 1) {
+  splits = std::max(1, splits);
+  const int kps = ((g.K + splits - 1) / splits + kGemmBK - 1) / kGemmBK * kGemmBK;
+  splits = (g.K + kps - 1) / kps;
+  g.k_per_split = kps;
+  g.split3 = t->gemm_split3 ? 1 : 0;
+  auto smem = [&](int bn) { return gemm_smem(bn, g.split3 != 0); };
+  const unsigned gm = unsigned((g.M + kGemmBM - 1) / kGemmBM);
+  if (g.N > 128) {
+    launch_on(t, s, umma_gemm_kernel<256>, dim3(gm, unsigned((g.N + 255) / 256), unsigned(splits)),
+              kGemmThreads, smem(256), g);
+  } else if (g.N > 64) {
+    launch_on(t, s, umma_gemm_kernel<128>, dim3(gm, 1, unsigned(splits)), kGemmThreads, smem(128),
+              g);
+  } else if (g.N > 32) {
+    launch_on(t, s, umma_gemm_kernel<64>, dim3(gm, 1, unsigned(splits)), kGemmThreads, smem(64), g);
+  } else {
+    launch_on(t, s, umma_gemm_kernel<32>, dim3(gm, 1, unsigned(splits)), kGemmThreads, smem(32), g);
+  }
+}
+
+// Forward + backward of one mini-batch shard on the wide path (mlp.cuh): the
+// activations and the dL/dx records on the body stream, the weight gradients
+// on st2 beside the sparse reduce (fork recorded after dX, joined by the
+// caller through t->join), all into t->dgrad in the reference layout.
+static hps_status enqueue_wide(Tier* t, const ShardMap& sm, std::uint64_t n,
+                               const std::int64_t* goff, const std::uint32_t* occ_row,
+                               const float* rows, int rstride, const std::uint8_t* dlab) {
+  const ModelDims& md = t->md;
+  const int L = md.L, E = t->E;
+  launch(t, wide_embed_kernel, grid_for(n * 32), 256, 0, sm, goff,
+         (const std::uint32_t*)t->occ_off, occ_row, rows, rstride, E, t->wX);
+  const float* hin = t->wX;
+  for (int l = 0; l + 1 < L; ++l) {  // hidden layers: Z = H W^T + b, relu
+    const int out = md.dims[l], in = md.ins[l];
+    const float* W = t->dense + md.offs[l];
+    GemmArgs g{};
+    g.M = int(n), g.N = out, g.K = in;
+    g.A = hin, g.a_m = in, g.a_k = 1;
+    g.B = W, g.b_n = in, g.b_k = 1;
+    g.epi = kEpiBiasRelu, g.D = t->wH[l], g.ldd = out, g.bias = W + std::int64_t(in) * out;
+    launch_gemm(t, t->st, g);
+    hin = t->wH[l];
+  }
+  {  // output layer, sigmoid, loss, output delta -> the last hidden layer's dZ
+    const int K = md.ins[L - 1];
+    const float* W = t->dense + md.offs[L - 1];
+    launch(t, wide_head_kernel, grid_for(n * 32), 256, 0, sm, K, W, W + K, hin, dlab, t->wdz,
+           t->wdZ[L - 2], &t->dsc->loss, &t->dsc->err);
+  }
+  for (int l = L - 2; l >= 0; --l) {  // dZ_{l-1} = (dZ_l W_l) .* [H_{l-1} > 0]; dX at l = 0
+    const int out = md.dims[l], in = md.ins[l];
+    GemmArgs g{};
+    g.M = int(n), g.N = in, g.K = out;
+    g.A = t->wdZ[l], g.a_m = out, g.a_k = 1;
+    g.B = t->dense + md.offs[l], g.b_n = 1, g.b_k = in;
+    if (l > 0) {
+      g.epi = kEpiMask, g.D = t->wdZ[l - 1], g.ldd = in, g.mask = t->wH[l - 1], g.ldm = in;
+    } else {
+      g.epi = kEpiF64, g.Dd = t->DX, g.ldd = in;
+    }
+    launch_gemm(t, t->st, g);
+  }
+  mark(t, HPS_T_FWDBWD);
+  // weight gradients beside the sparse reduce
+  HPS_CUDA(cudaEventRecord(t->fork, t->st));
+  HPS_CUDA(cudaStreamWaitEvent(t->st2, t->fork, 0));
+  {
+    const int K = md.ins[L - 1];
+    launch_on(t, t->st2, wide_head_grad_kernel, unsigned((K + 1 + 31) / 32), 256, 0, n, K,
+              (const float*)t->wdz, (const float*)t->wH[L - 2], t->dgrad + md.offs[L - 1]);
+  }
+  for (int l = L - 2; l >= 0; --l) {  // [dW_l | db_l] = dZ_l^T [H_{l-1} | 1] / n
+    const int out = md.dims[l], in = md.ins[l];
+    GemmArgs g{};
+    g.M = out, g.N = in + 1, g.K = int(n);
+    g.A = t->wdZ[l], g.a_m = 1, g.a_k = out;
+    g.B = l > 0 ? t->wH[l - 1] : t->wX, g.b_n = 1, g.b_k = in, g.b_ones_col = 1;
+    g.epi = kEpiStore, g.D = t->wP, g.ldd = in + 1;
+    const int bn = g.N > 128 ? 256 : (g.N > 64 ? 128 : (g.N > 32 ? 64 : 32));
+    const int tiles = ((out + kGemmBM - 1) / kGemmBM) * ((g.N + bn - 1) / bn);
+    int splits = std::max(1, kSMs / tiles);
+    splits = int(std::min<std::uint64_t>(std::uint64_t(splits), (n + kGemmBK - 1) / kGemmBK));
+    while (splits > 1 && std::uint64_t(splits) * out * (in + 1) > t->wP_cap) --splits;
+    const int kps = ((int(n) + splits - 1) / splits + kGemmBK - 1) / kGemmBK * kGemmBK;
+    splits = (int(n) + kps - 1) / kps;
+    launch_gemm(t, t->st2, g, splits);
+    float* gW = t->dgrad + md.offs[l];
+    launch_on(t, t->st2, wide_wgrad_reduce_kernel, grid_for(std::uint64_t(out) * (in + 1)), 256, 0,
+              (const float*)t->wP, splits, out, in, n, gW, gW + std::int64_t(in) * out);
+  }
+  HPS_CUDA(cudaEventRecord(t->join, t->st2));
+  return HPS_OK;
+}
+
 // Segment-length routing of the sparse reduce: <= kLongSeg in-order by one
 // thread per (key, 4 dims), longer ones split into fuse_chunk(E)-occurrence
 // chunks over CTAs (big_fused_kernel).
@@ -1584,6 +1693,9 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
         HPS_CUDA(cudaStreamWaitEvent(T->st3, T->fork3, 0));
       }
       HPS_TRY(launch_big_plan(T, ob, Uj, segj));
+      if (T->wide) {  // tcgen05 GEMMs (mlp.cuh); the weight gradients fork onto st2
+        HPS_TRY(enqueue_wide(T, sm, n, goff, occ_row, rows, rstride, dlab));
+      } else {
       const int LPE = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
       const int epb = 128 / LPE;
       const size_t smem = size_t((T->md.nw + 1) & ~1) * 4 +
@@ -1609,6 +1721,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                 n, (const double*)T->H, (const double*)T->DL, (const double*)T->dpart,
                 (const double*)T->dg_tot, T->dgrad, &T->dsc->fallbacks);
       HPS_CUDA(cudaEventRecord(T->join, T->st2));
+      }
       if (T->big_side) HPS_CUDA(cudaStreamWaitEvent(T->st3, T->fork, 0));  // after fwd/bwd
       HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob, Uj, segj, exsj,
                                   bp.grouped && G == 1 ? slotsj : nullptr));
@@ -2231,9 +2344,20 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     return set_error(HPS_ERR_ARG, "config: learning_rate must be positive");
   if (c.max_batch_keys >= (1ull << 31) || c.max_batch_examples >= (1ull << 31))
     return set_error(HPS_ERR_ARG, "batch maxima must be < 2^31");
-  for (int l = 0; l < c.num_layers; ++l)
-    if (c.layer_dims[l] < 1 || c.layer_dims[l] > std::uint64_t(kMaxHidden))
-      return set_error(HPS_ERR_ARG, "layer width must be in [1, %d]", kMaxHidden);
+  // layers up to kMaxHidden wide run the exact f64 fwd_bwd_kernel; a wider
+  // hidden layer (or HPS_WIDE=1) selects the tcgen05 GEMM path (mlp.cuh)
+  bool wide = false;
+  {
+    const char* v = std::getenv("HPS_WIDE");
+    wide = v && std::atoi(v) != 0;
+  }
+  for (int l = 0; l < c.num_layers; ++l) {
+    if (c.layer_dims[l] < 1 || c.layer_dims[l] > 4096)
+      return set_error(HPS_ERR_ARG, "layer width must be in [1, 4096]");
+    if (c.layer_dims[l] > std::uint64_t(kMaxHidden)) wide = true;
+  }
+  if (wide && c.num_layers < 2)
+    return set_error(HPS_ERR_ARG, "the wide MLP path needs a hidden layer");
   if (c.embedding_dim > 256) return set_error(HPS_ERR_ARG, "embedding_dim <= 256");
   if (c.optimizer != HPS_OPT_SGD && c.optimizer != HPS_OPT_ADAGRAD)
     return set_error(HPS_ERR_ARG, "config: optimizer must be HPS_OPT_SGD or HPS_OPT_ADAGRAD");
@@ -2250,6 +2374,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   t->g = c.rank;
   t->E = c.embedding_dim;
   t->J = c.minibatches;
+  t->wide = wide;
+  if (const char* v = std::getenv("HPS_TF32_1X")) t->gemm_split3 = std::atoi(v) == 0;
   t->RW = c.optimizer == HPS_OPT_ADAGRAD ? 2 * t->E : t->E;
   t->opt = Optim{c.optimizer, t->E, t->RW, c.learning_rate, c.adagrad_eps};
   t->Bmax = std::max<std::uint64_t>(c.max_batch_examples, 1);
@@ -2270,6 +2396,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_WS_SORT")) t->ws_sort = std::atoi(v) != 0 ? 1 : 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
+  t->nshard = (t->Bmax + std::uint64_t(G) * t->cfg.minibatches - 1) /
+              (std::uint64_t(G) * t->cfg.minibatches);
   {
     int bits = 64;
     if (c.key_space) {
@@ -2387,12 +2515,20 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     const size_t need_grad = 0;
     const size_t need_fwd = size_t((t->md.nw + 1) & ~1) * 4 +
                             size_t(16) * (t->md.hw + t->md.dw + t->md.maxw) * 8;
-    if (need_grad > size_t(big) || need_fwd > size_t(big))
+    if (!t->wide && (need_grad > size_t(big) || need_fwd > size_t(big)))
       return fail(set_error(HPS_ERR_ARG, "dense model too large for the fused kernels"));
 
     cudaFuncSetAttribute(fwd_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(umma_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(gemm_smem(256, true)));
+    cudaFuncSetAttribute(umma_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(gemm_smem(128, true)));
+    cudaFuncSetAttribute(umma_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(gemm_smem(64, true)));
+    cudaFuncSetAttribute(umma_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(gemm_smem(32, true)));
     cudaFuncSetAttribute(group_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kGroupSmemMax));
     cudaFuncSetAttribute(group_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2507,12 +2643,28 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (G == 1) A(rows, S * E);  // G > 1: inside the exported window (peers write it)
   A(deltas, S * E);
   A(hstage, S * E);
-  A(H, t->nmb_max * std::uint64_t(t->md.hw) + 2);   // +2: 16-B rounded bulk copies
-  A(DL, t->nmb_max * std::uint64_t(t->md.dw) + 2);
+  if (!t->wide) {  // the exact path's per-example records
+    A(H, t->nmb_max * std::uint64_t(t->md.hw) + 2);   // +2: 16-B rounded bulk copies
+    A(DL, t->nmb_max * std::uint64_t(t->md.dw) + 2);
+  } else {
+    const std::uint64_t ns = t->nshard;
+    A(wX, ns * E);
+    std::uint64_t pmax = std::uint64_t(kSMs) * kGemmBM * 256;
+    for (int l = 0; l + 1 < t->md.L; ++l) {
+      A(wH[l], ns * std::uint64_t(t->md.dims[l]));
+      A(wdZ[l], ns * std::uint64_t(t->md.dims[l]));
+      pmax = std::max(pmax, std::uint64_t(t->md.dims[l]) * (t->md.ins[l] + 1));
+    }
+    A(wdz, ns);
+    A(wP, pmax);
+    t->wP_cap = pmax;
+  }
   A(DX, t->nmb_max * E);
-  A(dpart, std::uint64_t(t->md.nw) * kDGSlices * 4);
-  A(dg_off, std::uint64_t(t->md.nw) * kDGSlices);
-  A(dg_tot, std::uint64_t(t->md.nw) * 4);
+  if (!t->wide) {  // the certified dense-gradient reduce of the exact path
+    A(dpart, std::uint64_t(t->md.nw) * kDGSlices * 4);
+    A(dg_off, std::uint64_t(t->md.nw) * kDGSlices);
+    A(dg_tot, std::uint64_t(t->md.nw) * 4);
+  }
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
 #undef A
@@ -2825,6 +2977,30 @@ hps_status hps_row_width(hps_tier_t t, uint64_t* row_width) {
   return HPS_OK;
 }
 
+hps_status hps_table_lookup(hps_tier_t t, const uint64_t* keys, uint64_t n, uint8_t* found,
+                            float* rows) {
+  HPS_ENTER_Q(t);
+  HPS_TRY(require_built(t));
+  if (n > t->Omax)
+    return set_error(HPS_ERR_CAPACITY, "lookup: %llu keys exceed max_batch_keys",
+                     (unsigned long long)n);
+  if (!n) return HPS_OK;
+  if (!keys || !found) return set_error(HPS_ERR_ARG, "null argument");
+  HPS_TRY(ensure_staged(t, n * std::uint64_t(t->RW)));
+  auto* dfound = reinterpret_cast<std::uint8_t*>(t->lane[0].vB);  // (n bytes <= Omax x 4)
+  HPS_CUDA(cudaMemcpyAsync(t->lane[0].kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
+  launch(t, table_lookup_kernel, grid_for(n), 256, 0, (const std::uint64_t*)t->lane[0].kB, n,
+         (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
+         (const std::uint64_t*)&t->dsc->cap[t->cur], t->RW, dfound,
+         rows ? t->staged : (float*)nullptr);
+  HPS_CUDA(cudaMemcpyAsync(found, dfound, n, cudaMemcpyDeviceToHost, t->st));
+  if (rows)
+    HPS_CUDA(cudaMemcpyAsync(rows, t->staged, n * std::uint64_t(t->RW) * 4,
+                             cudaMemcpyDeviceToHost, t->st));
+  HPS_CUDA(cudaStreamSynchronize(t->st));
+  return HPS_OK;
+}
+
 hps_status hps_table_slots(hps_tier_t t, uint64_t* slot_keys, float* rows) {
   std::uint64_t cap = 0;
   HPS_TRY(hps_table_info(t, &cap, nullptr, nullptr));
@@ -2995,6 +3171,35 @@ hps_status hps_reset_timing(hps_tier_t t) {
 hps_status hps_kernel_launches(hps_tier_t t, uint64_t* n) {
   if (!t || !n) return set_error(HPS_ERR_ARG, "null argument");
   *n = t->launches;
+  return HPS_OK;
+}
+
+hps_status hps_debug_gemm_tf32(int M, int N, int K, const float* A, int64_t a_m, int64_t a_k,
+                               const float* B, int64_t b_n, int64_t b_k, int b_ones_col, int epi,
+                               float* D, double* Dd, int64_t ldd, const float* bias,
+                               const float* mask, int64_t ldm, int splits) {
+  if (M < 1 || N < 1 || K < 1 || !A || !B || (epi == kEpiF64 ? !Dd : !D))
+    return set_error(HPS_ERR_ARG, "debug_gemm: bad arguments");
+  static Tier scratch;  // launch bookkeeping only
+  {
+    const char* v = std::getenv("HPS_TF32_1X");
+    scratch.gemm_split3 = !(v && std::atoi(v) != 0);
+  }
+  GemmArgs g{};
+  g.M = M, g.N = N, g.K = K;
+  g.A = A, g.a_m = a_m, g.a_k = a_k;
+  g.B = B, g.b_n = b_n, g.b_k = b_k, g.b_ones_col = b_ones_col;
+  g.epi = epi, g.D = D, g.Dd = Dd, g.ldd = ldd, g.bias = bias, g.mask = mask, g.ldm = ldm;
+  for (int bn : {32, 64, 128, 256}) {
+    const int smem = int(gemm_smem(bn, true));
+    if (bn == 32) cudaFuncSetAttribute(umma_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (bn == 64) cudaFuncSetAttribute(umma_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (bn == 128) cudaFuncSetAttribute(umma_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (bn == 256) cudaFuncSetAttribute(umma_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+  launch_gemm(&scratch, nullptr, g, splits);
+  HPS_CUDA(cudaGetLastError());
+  HPS_CUDA(cudaDeviceSynchronize());
   return HPS_OK;
 }
 

@@ -123,8 +123,15 @@ _SIGS = {
     "hps_kernel_launches": ([_P, _U64P], ctypes.c_int),
     "hps_graph_captures": ([_P, _U64P], ctypes.c_int),
     "hps_row_width": ([_P, _U64P], ctypes.c_int),
+    "hps_table_lookup": ([_P, _P, _U64, _P, _P], ctypes.c_int),
+    "hps_debug_gemm_tf32": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int64,
+                             ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                             ctypes.c_int, _P, _P, ctypes.c_int64, _P, _P, ctypes.c_int64,
+                             ctypes.c_int], ctypes.c_int),
     "hps_set_graphs": ([_P, ctypes.c_int], ctypes.c_int),
     "hps_stream": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
+    "hps_gen_multislot": ([_U64, _U64, _U64, _U64, ctypes.c_double, _U64, ctypes.c_double, _P,
+                           _P, _P, _U64P], ctypes.c_int),
     "hps_crc32": ([ctypes.c_uint32, _P, _U64], ctypes.c_uint32),
     "hps_pfile_write": ([ctypes.c_char_p, _P, _P, _P, _U64, ctypes.c_uint32, ctypes.c_uint32,
                          _U64, _U64P], ctypes.c_int),
@@ -218,6 +225,20 @@ def gen_dataset(dims: int, num_examples: int, nnz: int, zipf: bool = False,
                                  signal_scale, clusters, _ptr(offsets), _ptr(keys),
                                  _ptr(labels)))
     return offsets, keys, labels
+
+
+def gen_multislot(num_examples: int, slots: int = 100, ids_per_slot: int = 10**6,
+                  max_keys: int = 300, zipf_s: float = 1.0, seed: int = 1,
+                  signal_scale: float = 6.0):
+    """BASELINE c4's multi-slot input (hps_gen_multislot) -> (offsets, keys, labels)."""
+    offsets = np.empty(num_examples + 1, dtype=np.int64)
+    keys = np.empty(num_examples * max_keys, dtype=np.uint64)
+    labels = np.empty(num_examples, dtype=np.uint8)
+    n = ctypes.c_uint64()
+    _check(lib().hps_gen_multislot(slots, ids_per_slot, num_examples, max_keys, zipf_s, seed,
+                                   signal_scale, _ptr(offsets), _ptr(keys), _ptr(labels),
+                                   ctypes.byref(n)))
+    return offsets, keys[: n.value].copy(), labels
 
 
 def unique_id() -> bytes:
