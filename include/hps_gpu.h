@@ -104,6 +104,9 @@ typedef struct {
                                 occurrences (the chunked, certified reduce) */
   uint64_t max_segment_chunks; /* most chunks of one such segment */
   uint64_t big_occurrences;  /* key occurrences in those segments */
+  uint64_t mid_segments;     /* segments of 33..mid length (HPS_MID_SEG, default
+                                1024) summed exactly by one warp each; longer
+                                ones take the chunked certified reduce */
 } hps_batch_stats;
 
 /* Phase slots of hps_get_timing (ms accumulated over hps_train_batch calls,
@@ -171,6 +174,13 @@ hps_status hps_push(hps_tier_t h, const uint64_t* keys, const float* deltas,
  * senders in canonical node-major/device-major order, v += d in f32
  * (device_table.hpp:88-95; Adagrad: the step above). Local to the rank. */
 hps_status hps_drain(hps_tier_t h);
+
+/* DeviceTable::accumulate (device_table.hpp:88-95) of one sender's unique
+ * (keys, deltas) on this rank's own table, in place (Adagrad: the step);
+ * local, not collective: the in-process hps:: adapter (hps_gpu/hbm_ps.hpp)
+ * queues each sender's deltas and applies them in canonical order with it. */
+hps_status hps_apply_local(hps_tier_t h, const uint64_t* keys, const float* deltas,
+                           uint64_t n);
 
 /* HbmTier::dump_node (hbm_ps.hpp:224-232) for this rank's table: keys in
  * ascending order and their rows (hps_row_width() floats each: embedding,

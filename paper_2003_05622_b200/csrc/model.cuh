@@ -617,12 +617,25 @@ inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw 
 // The two paths write disjoint keys and run side by side.
 constexpr int kLongSeg = 32;
 
-// The keys whose segment is longer than kLongSeg -> big_list. It reads the
-// grouping only, so it runs beside fwd/bwd on the big path's stream.
+// The keys whose segment is longer than kLongSeg: up to mid_max occurrences
+// -> mid_list (sparse_mid_kernel, an exact warp chain), longer -> big_list
+// (the chunked, certified big_fused_kernel). It reads the grouping only, so it
+// runs beside fwd/bwd on the big path's stream.
+__device__ __forceinline__ void warp_append(bool pick, std::uint32_t u, std::uint32_t* list,
+                                            unsigned long long* n, unsigned lane) {
+  const unsigned m = __ballot_sync(0xFFFFFFFFu, pick);
+  if (!m) return;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(n, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  if (pick) list[base + __popc(m & ((1u << lane) - 1))] = u;
+}
+
 __global__ void __launch_bounds__(256)
     big_classify_kernel(const std::uint64_t* __restrict__ u_ptr,
                         const std::uint32_t* __restrict__ seg, std::uint32_t* __restrict__ big_list,
-                        unsigned long long* __restrict__ n_big) {
+                        unsigned long long* __restrict__ n_big, std::uint32_t mid_max,
+                        std::uint32_t* __restrict__ mid_list, unsigned long long* __restrict__ n_mid) {
   pdl_wait();
   const std::uint64_t U = *u_ptr;
   const unsigned lane = threadIdx.x & 31;
@@ -631,13 +644,10 @@ __global__ void __launch_bounds__(256)
   for (std::uint64_t b = std::uint64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u); b < U;
        b += stride) {
     const std::uint64_t u = b + lane;
-    const bool big = u < U && seg[u + 1] - seg[u] > std::uint32_t(kLongSeg);
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, big);
-    if (!m) continue;
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(n_big, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
-    if (big) big_list[base + __popc(m & ((1u << lane) - 1))] = std::uint32_t(u);
+    const std::uint32_t len = u < U ? seg[u + 1] - seg[u] : 0u;
+    warp_append(len > mid_max, std::uint32_t(u), big_list, n_big, lane);
+    warp_append(len > std::uint32_t(kLongSeg) && len <= mid_max, std::uint32_t(u), mid_list, n_mid,
+                lane);
   }
 }
 
@@ -724,6 +734,72 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int i = 0; i < DPT; ++i) write_delta(dout, u, E, d0 + i, acc[i], inv_n);
+  }
+}
+
+// Medium segments (kLongSeg < length <= mid_max): one warp per (key, block of
+// W dims) sums each dimension exactly in the reference order (model.hpp:
+// 182-187) — no certificate, no cross-CTA look-back. The segment is walked in
+// tiles of 32 occurrences: lane i loads the tile's i-th example id, then the
+// warp loads the tile's dL/dx values (RPI rows of W dims per instruction, all
+// independent, the next tile's in flight during this tile's chain), and lanes
+// 0..W-1 run the in-order f64 chain over the tile through shuffles.
+// RPI = 32 / W rows per load: E <= W = 32 / RPI (E > 32: RPI = 1, blocks of
+// 32 dims).
+template <int RPI>
+__global__ void __launch_bounds__(256)
+    sparse_mid_kernel(int E, std::uint64_t n, const unsigned long long* __restrict__ n_mid,
+                      const std::uint32_t* __restrict__ mid_list,
+                      const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
+                      DeltaOut dout, const double* __restrict__ DX,
+                      unsigned long long* __restrict__ mid_keys) {
+  pdl_wait();
+  if (mid_keys && blockIdx.x == 0 && threadIdx.x == 0 && *n_mid)
+    atomicAdd(mid_keys, (unsigned long long)*n_mid);
+  constexpr int W = 32 / RPI;   // dims per block
+  constexpr int T = 32;         // occurrences per tile
+  constexpr int NV = T / RPI;   // values per lane per tile
+  const unsigned lane = threadIdx.x & 31;
+  const int rg = int(lane) / W, dl = int(lane) % W;
+  const int nblk = (E + W - 1) / W;
+  const std::uint64_t items = *n_mid * std::uint64_t(nblk);
+  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  const std::uint64_t nwarps = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (std::uint64_t it = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5; it < items;
+       it += nwarps) {
+    const std::uint32_t u = mid_list[it / nblk];
+    const int d = int(it % nblk) * W + dl;
+    const bool dv = d < E;
+    const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
+    auto load = [&](std::uint32_t t, double* v) {
+      const std::uint32_t e = t + lane < p1 ? exs[t + lane] : 0u;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const int k = i * RPI + rg;
+        const std::uint32_t ek = __shfl_sync(0xFFFFFFFFu, e, k);
+        v[i] = (t + k < p1 && dv) ? DX[std::uint64_t(ek) * E + d] : 0.0;
+      }
+    };
+    double cur[NV], nxt[NV];
+    load(p0, cur);
+    double acc = 0.0;
+    for (std::uint32_t t = p0; t < p1; t += T) {
+      const bool more = t + T < p1;
+      if (more) load(t + T, nxt);
+      const int cnt = int(p1 - t < std::uint32_t(T) ? p1 - t : T);
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int q = 0; q < RPI; ++q) {
+          const double x = __shfl_sync(0xFFFFFFFFu, cur[i], q * W + dl);
+          if (i * RPI + q < cnt) acc = __dadd_rn(acc, x);
+        }
+      if (more) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) cur[i] = nxt[i];
+      }
+    }
+    if (rg == 0 && dv) dout.grad(u, E, d, __double2float_rn(__dmul_rn(acc, inv_n)));
   }
 }
 

@@ -138,6 +138,8 @@ struct Scalars {
   unsigned long long big_keys;   // segments on the chunked path (this batch)
   unsigned long long max_chunks; // most chunks of one of them
   unsigned long long big_occ;    // their occurrences
+  unsigned long long mid_keys;   // segments on the exact warp-chain path (this batch)
+  unsigned long long n_mid;      // this mini-batch's medium segments
   DevError err;                 // the body's and the parity API's error word
   // per-batch error words of the pipelined stages: the stage's
   // key-range check (by staging slot) and the prep's build (by table), so an
@@ -216,7 +218,7 @@ struct GroupState {
 struct BatchOut {
   double loss;
   unsigned long long pulled;
-  unsigned long long fallbacks, served, big_keys, max_chunks, big_occ;
+  unsigned long long fallbacks, served, big_keys, max_chunks, big_occ, mid_keys;
   unsigned long long carried, stored;
   std::uint64_t n_ws, cap;
   DevError err, err_stage, err_prep;
@@ -241,6 +243,10 @@ struct Tier {
   cudaEvent_t fork = nullptr, join = nullptr;
   cudaStream_t st3 = nullptr;           // side stream: the big-segment path (classify, plan,
   cudaEvent_t fork3 = nullptr, join3 = nullptr;  // fused reduce) beside fwd/bwd + short path
+  cudaStream_t st4 = nullptr;           // side stream: the medium segments (sparse_mid_kernel)
+  cudaEvent_t fork4 = nullptr, join4 = nullptr;
+  std::uint32_t mid_max = 1024;         // medium segments: kLongSeg < length <= mid_max
+                                        // (HPS_MID_SEG; kLongSeg disables the path)
   Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
                                         // 2..: the next batch's mini-batch groupings
   GroupState gs[kGroupLanes];           // [0]: the prep's grouping, [1]: the body's
@@ -316,7 +322,7 @@ struct Tier {
                 *seg = nullptr, *uidv = nullptr, *pos = nullptr,
                 *slots = nullptr,
                 *exs = nullptr,
-                *big_list = nullptr, *chunk_off = nullptr,
+                *big_list = nullptr, *chunk_off = nullptr, *mid_list = nullptr,
                 *orank = nullptr,
                 *key_done = nullptr;
   ChunkSum* chunk_tot = nullptr;
@@ -1221,8 +1227,9 @@ static hps_status launch_big_plan(Tier* t, std::uint64_t u_upper, const std::uin
   unsigned long long* nb = &t->dsc->n_big;
   cudaStream_t bs = t->big_side ? t->st3 : t->st;
   HPS_CUDA(cudaMemsetAsync(nb, 0, 8, bs));
+  HPS_CUDA(cudaMemsetAsync(&t->dsc->n_mid, 0, 8, bs));
   launch_on(t, bs, big_classify_kernel, grid_for(std::max<std::uint64_t>(u_upper, 1)), 256, 0,
-            U, seg, t->big_list, nb);
+            U, seg, t->big_list, nb, t->mid_max, t->mid_list, &t->dsc->n_mid);
   launch_on(t, bs, big_plan_kernel, 1, 1024, 0, fuse_chunk(t->E),
             (const std::uint32_t*)t->big_list, (const unsigned long long*)nb, seg, t->chunk_off,
             &t->dsc->n_items, t->item_key, t->item_chunk, &t->dsc->big_keys, &t->dsc->max_chunks,
@@ -1248,6 +1255,29 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   const float lr = t->cfg.learning_rate;
   const double* DX = t->DX;
   cudaStream_t bs = t->big_side ? t->st3 : t->st;
+  // medium segments: exact warp chains on st4, beside the big and short paths
+  // (after the classification on bs and fwd/bwd's dL/dx)
+  cudaStream_t ms = t->big_side ? t->st4 : t->st;
+  if (t->big_side) {
+    HPS_CUDA(cudaEventRecord(t->fork4, bs));
+    HPS_CUDA(cudaStreamWaitEvent(ms, t->fork4, 0));
+  }
+  if (t->mid_max > std::uint32_t(kLongSeg)) {
+    if (E <= 8) {
+      launch_on(t, ms, sparse_mid_kernel<4>, kSMs * 8, 256, 0, E, n,
+                (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
+                exs, dout, DX, &t->dsc->mid_keys);
+    } else if (E <= 16) {
+      launch_on(t, ms, sparse_mid_kernel<2>, kSMs * 8, 256, 0, E, n,
+                (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
+                exs, dout, DX, &t->dsc->mid_keys);
+    } else {
+      launch_on(t, ms, sparse_mid_kernel<1>, kSMs * 8, 256, 0, E, n,
+                (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
+                exs, dout, DX, &t->dsc->mid_keys);
+    }
+  }
+  if (t->big_side) HPS_CUDA(cudaEventRecord(t->join4, ms));
   mark_big(t, -1);
   launch_on(t, bs, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
             (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big,
@@ -1262,6 +1292,7 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,
          E, lr, n, U, seg, exs, dout, DX, &t->dsc->pulled);
   HPS_CUDA(cudaStreamWaitEvent(t->st, t->join3, 0));
+  if (t->big_side) HPS_CUDA(cudaStreamWaitEvent(t->st, t->join4, 0));
   return HPS_OK;
 }
 
@@ -1601,7 +1632,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
   // T->st; the previous one's was copied to its BatchOut already)
   HPS_CUDA(cudaMemsetAsync(&T->dsc->err, 0, sizeof(DevError), T->st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 16, T->st));       // loss, pulled
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 40, T->st));  // fallbacks .. big_occ
+  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 48, T->st));  // fallbacks .. mid_keys
   if (bp.tp >= 0) {  // rows from the resident tables (carry-over, proxies)
     const int RW = T->RW, V = vec_of(RW);
     const unsigned gc = grid_for(sh.own_bound * std::uint64_t(RW / V));
@@ -1937,6 +1968,7 @@ static void complete_oldest(Tier* T) {
     st.big_segments = o.big_keys;
     st.max_segment_chunks = o.max_chunks;
     st.big_occurrences = o.big_occ;
+    st.mid_segments = o.mid_keys;
     st.occurrences = bp.occ_total;
     // first failing stage: the key-range check, the build, the body
     const DevError& e = o.err_stage.code ? o.err_stage : (o.err_prep.code ? o.err_prep : o.err);
@@ -2242,7 +2274,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   BatchOut* ho = &T->hout[sp];
   const int tb = bp.tb;
   HPS_CUDA(cudaMemcpyAsync(&ho->loss, &T->dsc->loss, 16, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->fallbacks, &T->dsc->fallbacks, 40, cudaMemcpyDeviceToHost, T->st));
+  HPS_CUDA(cudaMemcpyAsync(&ho->fallbacks, &T->dsc->fallbacks, 48, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&ho->carried, &T->dsc->carried_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&ho->stored, &T->dsc->stored_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
   HPS_CUDA(cudaMemcpyAsync(&ho->n_ws, &T->dsc->nws_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
@@ -2392,6 +2424,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     t->prep_mbs = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_BIG_SIDE")) t->big_side = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_MID_SEG"))
+    t->mid_max = std::uint32_t(std::max(kLongSeg, std::atoi(v)));
   if (const char* v = std::getenv("HPS_FOLD_WAIT")) t->fold_wait = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_WS_SORT")) t->ws_sort = std::atoi(v) != 0 ? 1 : 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
@@ -2466,6 +2500,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     str(&t->st, hi);
     str(&t->st2, hi);
     str(&t->st3, hi);
+    str(&t->st4, hi);
     str(&t->lane[1].st, lo);
     for (int gl = 0; gl < kGroupLanes; ++gl) str(&t->lane[2 + gl].st, lo);
     str(&t->st_stage, lo);
@@ -2475,6 +2510,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     ev(&t->join, false);
     ev(&t->fork3, false);
     ev(&t->join3, false);
+    ev(&t->fork4, false);
+    ev(&t->join4, false);
     ev(&t->ev_staged, false);
     ev(&t->ev_prep, false);
     ev(&t->pf_fork, false);
@@ -2630,6 +2667,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   }
   A(otot, kMaxRanks);
   A(big_list, S / (kLongSeg + 1) + 2);
+  A(mid_list, S / (kLongSeg + 1) + 2);
   A(chunk_off, S / (kLongSeg + 1) + 3);
   A(key_done, S / (kLongSeg + 1) + 2);
   // fused big-segment items: one per (key, chunk of fuse_chunk(E) occurrences)
@@ -2702,7 +2740,8 @@ hps_status hps_destroy(hps_tier_t t) {
   if (!t) return HPS_OK;
   cudaSetDevice(t->cfg.cuda_device);
   if (t->dsc) quiesce(t);  // in-flight batches, then every resident row to the store
-  for (cudaStream_t x : {t->st, t->lane[1].st, t->st_stage, t->st_wb, t->st2, t->st3, t->st_pf})
+  for (cudaStream_t x :
+       {t->st, t->lane[1].st, t->st_stage, t->st_wb, t->st2, t->st3, t->st4, t->st_pf})
     if (x) cudaStreamSynchronize(x);
   for (int gl = 0; gl < kGroupLanes; ++gl)
     if (t->lane[2 + gl].st) cudaStreamSynchronize(t->lane[2 + gl].st);
@@ -2720,6 +2759,8 @@ hps_status hps_destroy(hps_tier_t t) {
   if (t->join) cudaEventDestroy(t->join);
   if (t->fork3) cudaEventDestroy(t->fork3);
   if (t->join3) cudaEventDestroy(t->join3);
+  if (t->fork4) cudaEventDestroy(t->fork4);
+  if (t->join4) cudaEventDestroy(t->join4);
   for (int p = 0; p < kTables; ++p) {
     for (cudaEvent_t x : {t->ev_wb[p], t->ev_body_tab[p], t->ev_wbt[p][0], t->ev_wbt[p][1]})
       if (x) cudaEventDestroy(x);
@@ -2741,6 +2782,7 @@ hps_status hps_destroy(hps_tier_t t) {
     if (t->lane[2 + gl].st) cudaStreamDestroy(t->lane[2 + gl].st);
   if (t->st2) cudaStreamDestroy(t->st2);
   if (t->st3) cudaStreamDestroy(t->st3);
+  if (t->st4) cudaStreamDestroy(t->st4);
   if (t->st) cudaStreamDestroy(t->st);
   delete t;
   return HPS_OK;
@@ -2954,6 +2996,27 @@ hps_status hps_drain(hps_tier_t t) {
   t->pending.clear();
   t->pend_used = 0;
   return s;
+}
+
+hps_status hps_apply_local(hps_tier_t t, const uint64_t* keys, const float* deltas, uint64_t n) {
+  HPS_ENTER_Q(t);
+  HPS_TRY(require_built(t));
+  if (n > t->Omax)
+    return set_error(HPS_ERR_CAPACITY, "apply: %llu keys exceed max_batch_keys",
+                     (unsigned long long)n);
+  if (!n) return HPS_OK;
+  if (!keys || !deltas) return set_error(HPS_ERR_ARG, "null argument");
+  t->tab_flushed[t->cur] = false;  // its rows change: written back again
+  const std::uint64_t E = std::uint64_t(t->E);
+  HPS_CUDA(cudaMemcpyAsync(t->lane[0].kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
+  HPS_CUDA(cudaMemcpyAsync(t->hstage, deltas, n * E * 4, cudaMemcpyHostToDevice, t->st));
+  const int V = vec_of(t->E);
+  auto k = V == 4 ? table_apply_kernel<4> : table_apply_kernel<1>;
+  launch(t, k, grid_for(n * std::uint64_t(t->E / V)), 256, 0, (const std::uint32_t*)nullptr,
+         (const std::uint64_t*)t->lane[0].kB, (const std::uint64_t*)t->tkeys[t->cur],
+         (const std::uint64_t*)&t->dsc->cap[t->cur], (const float*)t->hstage,
+         (const std::uint64_t*)nullptr, n, t->tvals[t->cur], t->opt, &t->dsc->err);
+  return check_device_error(t, "device table: accumulate to missing key ");
 }
 
 hps_status hps_table_info(hps_tier_t t, uint64_t* capacity, uint64_t* occupancy,

@@ -80,6 +80,7 @@ class HpsBatchStats(ctypes.Structure):
         ("big_segments", ctypes.c_uint64),
         ("max_segment_chunks", ctypes.c_uint64),
         ("big_occurrences", ctypes.c_uint64),
+        ("mid_segments", ctypes.c_uint64),
     ]
 
 OPTIMIZERS = {"sgd": 0, "adagrad": 1}
@@ -124,6 +125,7 @@ _SIGS = {
     "hps_graph_captures": ([_P, _U64P], ctypes.c_int),
     "hps_row_width": ([_P, _U64P], ctypes.c_int),
     "hps_table_lookup": ([_P, _P, _U64, _P, _P], ctypes.c_int),
+    "hps_apply_local": ([_P, _P, _P, _U64], ctypes.c_int),
     "hps_debug_gemm_tf32": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.c_int64,
                              ctypes.c_int64, _P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                              ctypes.c_int, _P, _P, ctypes.c_int64, _P, _P, ctypes.c_int64,

@@ -79,6 +79,7 @@ def test_adagrad_train_bit_exact(pkg, oracle, E, J, zipf, store_kind, pipelined)
 def test_adagrad_big_segments_and_forced_fallback(pkg, oracle, monkeypatch):
     """Hot keys (chunked big_fused path, its fused Adagrad apply), with every
     certificate forced to fail (the exact fallbacks feed the same apply)."""
+    monkeypatch.setenv("HPS_MID_SEG", "32")  # the long segments on the certified path
     for force in ("0", "1"):
         monkeypatch.setenv("HPS_CERT_FORCE_FAIL", force)
         dims, B, E = 20000, 4096, 16

@@ -87,6 +87,7 @@ def test_config2_full_size_bit_exact(pkg, oracle, store_kind):
 def test_forced_certificate_failure_takes_exact_fallbacks(pkg, oracle, monkeypatch, E, B, nnz,
                                                           chunks):
     monkeypatch.setenv("HPS_CERT_FORCE_FAIL", "1")
+    monkeypatch.setenv("HPS_MID_SEG", "32")  # every long segment on the certified path
     dims, J, layers, nb = 20000, 4, (8, 16, 1), 3
     off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=17)
     tier = pkg.Tier(width=E, layer_dims=layers, minibatches=J, key_space=dims,
@@ -109,9 +110,38 @@ def test_forced_certificate_failure_takes_exact_fallbacks(pkg, oracle, monkeypat
     assert np.array_equal(store[wk.astype(np.int64)], wr)
 
 
-def test_certificate_default_is_off(pkg, oracle):
+@pytest.mark.parametrize("mid", ["32", "128", "1024", "100000"])
+@pytest.mark.parametrize("E", [4, 16, 64])
+def test_mid_segment_warp_chains_bit_exact(pkg, oracle, monkeypatch, mid, E):
+    """Segments of 33..HPS_MID_SEG occurrences are summed by one warp each in
+    the exact reference order (sparse_mid_kernel); longer ones by the chunked
+    certified reduce. Every split point gives the oracle's bits."""
+    monkeypatch.setenv("HPS_MID_SEG", mid)
+    dims, B, J = 20000, 4096, 4
+    off, keys, lab = pkg.gen_dataset(dims, 2 * B, 20, zipf=True, seed=29)
+    tier = pkg.Tier(width=E, minibatches=J, key_space=dims, max_batch_examples=B,
+                    max_batch_keys=max_keys_of(off, B))
+    store = np.zeros((dims, E), dtype=np.float32)
+    tier.attach_store(store)
+    stats = [tier.train_batch(o, k, l) for o, k, l in batches_of(off, keys, lab, B)]
+    tier.flush()
+    dense = tier.get_dense()
+    tier.close()
+    if mid == "32":
+        assert all(s.mid_segments == 0 for s in stats)
+    else:
+        assert all(s.mid_segments > 0 for s in stats)
+    if mid == "100000":
+        assert all(s.big_segments == 0 for s in stats)
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, (8, 16, 1), J=J), B, off, keys, lab)
+    assert np.array_equal(dense, wd)
+    assert np.array_equal(store[wk.astype(np.int64)], wr)
+
+
+def test_certificate_default_is_off(pkg, oracle, monkeypatch):
     """Without the knob the bench-like workload needs no fallback (a tier
     created after a forced one resets the device flag)."""
+    monkeypatch.setenv("HPS_MID_SEG", "32")
     dims, E, B, nnz, J = 20000, 16, 4096, 20, 4
     off, keys, lab = pkg.gen_dataset(dims, B, nnz, zipf=True, seed=17)
     tier = pkg.Tier(width=E, minibatches=J, key_space=dims, max_batch_examples=B,
