@@ -257,6 +257,12 @@ def remote_unique_keys(batches, D, J):
     return float(total)
 
 
+def trace(msg):
+    if os.environ.get("HPS_BENCH_TRACE"):
+        print(f"[bench {os.environ.get('RANK', '0')} {time.time():.1f}] {msg}", file=sys.stderr,
+              flush=True)
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -289,6 +295,7 @@ def run_ours(args, rank, world, local_rank):
                     nccl_id=nccl_id, optimizer=c.get("opt", "sgd"))
     RW = tier.row_width  # floats per table / store row (2E with the Adagrad state)
     stream = torch.cuda.ExternalStream(tier.stream(), device=dev)
+    trace("tier created")
 
     def barrier():
         if world > 1:
@@ -297,7 +304,7 @@ def run_ours(args, rank, world, local_rank):
 
     LAG = 3  # waits trail submits by three: four batches in flight
 
-    def timed_steps(submit_fn, n_steps, first):
+    def timed_steps(submit_fn, n_steps, first):  # noqa: C901
         """Returns (event ms over the whole run of n_steps, per-step stats).
 
         One region, not per-step brackets: steps are pipelined through the
@@ -315,6 +322,8 @@ def run_ours(args, rank, world, local_rank):
             submit_fn((first + i) % P)
             if i >= LAG:
                 stats.append(tier.wait_batch())
+            if i < 8 or i % 50 == 0:
+                trace(f"step {i} submitted")
         while len(stats) < n_steps:
             stats.append(tier.wait_batch())
         tier.flush()
@@ -350,8 +359,10 @@ def run_ours(args, rank, world, local_rank):
 
     for i in range(args.warmup):
         dev_step(i % P)
+        trace(f"warmup submit {i}")
     for i in range(args.warmup):
         tier.wait_batch()
+    trace("warmup done")
     barrier()
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -360,6 +371,7 @@ def run_ours(args, rank, world, local_rank):
     captures0 = tier.graph_captures()
     barrier()
     dev_ms, dev_stats = timed_steps(dev_step, args.steps, args.warmup)
+    trace("timed value pass done")
     barrier()
     launches = tier.kernel_launches() - launches0
     captures = tier.graph_captures() - captures0
@@ -378,6 +390,7 @@ def run_ours(args, rank, world, local_rank):
     _, ph_stats = timed_steps(dev_step, ph_steps, args.warmup)
     barrier()
     phases = tier.timing()
+    trace("timing pass done")
     tier.set_timing(False)
 
     # per-rank work counters over the phase-timing pass
@@ -553,7 +566,10 @@ def run_ours(args, rank, world, local_rank):
             cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
 
+    # (collectives: every rank calls them, in this order)
     all_launch = int(sum_over_ranks(launches))
+    captures_all = int(sum_over_ranks(captures))
+    fallbacks_all = int(sum_over_ranks(fallbacks))
     # keys/s per phase: pull = the phases that deliver a
     # mini-batch's unique rows to the model (G = 1: fwd/bwd reads them in
     # place; G > 1: key all-to-all + owner gather + row all-to-all); push = the
@@ -586,8 +602,8 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": all_launch,
-            "graph_captures_in_timed_region": int(sum_over_ranks(captures)),
-            "exact_fallbacks": int(sum_over_ranks(fallbacks)),
+            "graph_captures_in_timed_region": captures_all,
+            "exact_fallbacks": fallbacks_all,
             "pull_keys_per_s": pull_keys_s,
             "push_keys_per_s": push_keys_s,
             "keys_per_s_phases": {"pull": "fwdbwd (rows read in place)" if fused_apply else

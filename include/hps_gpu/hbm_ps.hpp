@@ -481,6 +481,7 @@ class SyncSession {
   }
   int rounds() const { return 1; }  // one all-gather over NVSwitch
   void run(int g, std::vector<float>& buf) {
+    std::lock_guard lk(tr_->lock(g));  // (other threads may use device g's handle)
     check_status(hps_dense_sync(tr_->handle(g), buf.data(), buf.size(), det_ ? 1 : 0));
   }
 

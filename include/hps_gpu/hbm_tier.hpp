@@ -23,9 +23,11 @@
 // Differences a caller of the reference must know:
 //   * one object per GPU/process (or per thread driving one GPU); the
 //     reference's lockstep device-worker threads map 1:1 onto ranks;
-//   * HostValue may be called for owned keys whose row then comes from the
-//     previous table (carry-over wins on the device); it must be a pure
-//     lookup, as the reference's prepared-map/host_embedding callbacks are;
+//   * HostValue is called only for owned keys the previous table does not
+//     hold (the device carries those over, hbm_ps.hpp:89-98);
+//   * the in-process, all-devices form with the reference's own signatures
+//     (HbmTier(topo, policy, width, Transport*), get(keys, Endpoint), ...) is
+//     hps_gpu/hbm_ps.hpp (namespace hps);
 //   * PartitionPolicy is always modulo (range_split exists in the reference
 //     only for its Appendix-A unit test).
 #pragma once
@@ -83,20 +85,20 @@ class DeviceTableView {
   std::size_t capacity() const { return info().cap; }
   std::size_t occupancy() const { return info().occ; }
   std::size_t value_width() const { return info().width; }
-  bool contains(ParamKey key) const {
-    std::vector<ParamKey> slots(capacity());
-    check(hps_table_slots(h_, slots.data(), nullptr));
-    return key != ~ParamKey{0} && std::find(slots.begin(), slots.end(), key) != slots.end();
+  bool contains(ParamKey key) const {  // one device probe (hps_table_lookup)
+    std::uint8_t f = 0;
+    check(hps_table_lookup(h_, &key, 1, &f, nullptr));
+    return f != 0;
   }
   std::vector<float> get(ParamKey key) const {
-    const Info in = info();
-    std::vector<ParamKey> slots(in.cap);
-    std::vector<float> rows(in.cap * in.width);
-    check(hps_table_slots(h_, slots.data(), rows.data()));
-    for (std::size_t i = 0; i < in.cap; ++i)
-      if (slots[i] == key && key != ~ParamKey{0})
-        return std::vector<float>(rows.begin() + i * in.width, rows.begin() + (i + 1) * in.width);
-    throw Error(HPS_ERR_MISSING_KEY, "device table: missing key " + std::to_string(key));
+    std::uint64_t rw = 0;
+    check(hps_row_width(h_, &rw));
+    std::uint8_t f = 0;
+    std::vector<float> row(rw);
+    check(hps_table_lookup(h_, &key, 1, &f, row.data()));
+    if (!f) throw Error(HPS_ERR_MISSING_KEY, "device table: missing key " + std::to_string(key));
+    row.resize(info().width);  // the embedding (an optimizer state stays on the device)
+    return row;
   }
   template <class Fn>  // Fn(ParamKey, const float*), slot order
   void for_each(Fn&& fn) const {
@@ -185,11 +187,18 @@ class HbmTier {
     std::vector<ParamKey> owned;
     for (ParamKey k : merged)
       if (topo_.owner_of(k) == rank_) owned.push_back(k);
-    std::vector<float> rows(owned.size() * width_);
+    std::uint64_t rw = 0;
+    check(hps_row_width(h_, &rw));
+    std::vector<std::uint8_t> carried(owned.size(), 0);
+    if (built_ && !owned.empty())  // keys the previous table holds: the device carries them
+      check(hps_table_lookup(h_, owned.data(), owned.size(), carried.data(), nullptr));
+    std::vector<float> rows(owned.size() * rw, 0.0f);
     for (std::size_t i = 0; i < owned.size(); ++i) {
+      if (carried[i]) continue;
       const auto v = host_value(owned[i]);
-      if (v.size() != width_) throw Error(HPS_ERR_WIDTH, "hbm: host value width mismatch");
-      std::copy(v.begin(), v.end(), rows.begin() + i * width_);
+      if (v.size() != width_ && v.size() != rw)
+        throw Error(HPS_ERR_WIDTH, "hbm: host value width mismatch");
+      std::copy(v.begin(), v.end(), rows.begin() + i * rw);
     }
     check(hps_build(h_, owned.data(), owned.size(), rows.data()));
     built_ = true;

@@ -680,7 +680,10 @@ __device__ __forceinline__ void write_delta(const DeltaOut& o, std::uint64_t u, 
 // Short segments, exact: one thread per (unique key, DPT dims) sums the key's
 // occurrences in example order; its DPT dimension chains are independent
 // (DPT-wide row loads, DPT adds in flight), each in the reference order.
-// Longer segments belong to the chunked CTA path (big_classify_kernel).
+// Longer segments belong to the mid / big paths (big_classify_kernel). With
+// the in-place apply (one rank) the key's table slot is loaded and its row
+// prefetched into L2 before the reduction, so the apply's read-modify-write
+// does not add two more dependent round trips after it.
 template <int DPT>
 __global__ void __launch_bounds__(256)
     sparse_short_kernel(int E, float lr, std::uint64_t n, const std::uint64_t* __restrict__ u_ptr,
@@ -689,6 +692,7 @@ __global__ void __launch_bounds__(256)
                         const double* __restrict__ DX,
                         unsigned long long* __restrict__ pulled) {
   pdl_wait();
+  (void)lr;
   const std::uint64_t U = *u_ptr;
   if (pulled && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(pulled, (unsigned long long)U);
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
@@ -698,6 +702,12 @@ __global__ void __launch_bounds__(256)
        t += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint64_t u = t / std::uint64_t(parts);
     const int d0 = int(t - u * parts) * DPT;
+    std::uint32_t slot = 0;
+    if (dout.apply_slot) {  // independent of the reduction: issue it first
+      slot = dout.apply_slot[u];
+      const float* rp = dout.table + std::uint64_t(slot) * dout.opt.RW + d0;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
+    }
     const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
     if (p1 - p0 > std::uint32_t(kLongSeg)) continue;
     double acc[DPT];
@@ -710,13 +720,13 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const double* row = DX + std::uint64_t(exs[p + r]) * E + d0;
-        if (DPT == 4) {
-          const double2 a = *reinterpret_cast<const double2*>(row);
-          const double2 b = *reinterpret_cast<const double2*>(row + 2);
-          x[r][0] = a.x;
-          x[r][1 % DPT] = a.y;
-          x[r][2 % DPT] = b.x;
-          x[r][3 % DPT] = b.y;
+        if (DPT % 2 == 0) {
+#pragma unroll
+          for (int i = 0; i < DPT; i += 2) {
+            const double2 a = *reinterpret_cast<const double2*>(row + i);
+            x[r][i] = a.x;
+            x[r][(i + 1) % DPT] = a.y;
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < DPT; ++i) x[r][i] = row[i];
@@ -732,22 +742,54 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int i = 0; i < DPT; ++i) acc[i] = __dadd_rn(acc[i], row[i]);
     }
+    if (dout.apply_slot) {
+      float* rowp = dout.table + std::uint64_t(slot) * dout.opt.RW;
 #pragma unroll
-    for (int i = 0; i < DPT; ++i) write_delta(dout, u, E, d0 + i, acc[i], inv_n);
+      for (int i = 0; i < DPT; i += (DPT % 4 == 0 ? 4 : 1)) {
+        if (DPT % 4 == 0) {
+          float4 g;
+          g.x = dout.opt.push_value(__double2float_rn(__dmul_rn(acc[i], inv_n)));
+          g.y = dout.opt.push_value(__double2float_rn(__dmul_rn(acc[(i + 1) % DPT], inv_n)));
+          g.z = dout.opt.push_value(__double2float_rn(__dmul_rn(acc[(i + 2) % DPT], inv_n)));
+          g.w = dout.opt.push_value(__double2float_rn(__dmul_rn(acc[(i + 3) % DPT], inv_n)));
+          dout.opt.apply4(rowp, d0 + i, g);
+        } else {
+          dout.opt.apply(rowp, d0 + i,
+                         dout.opt.push_value(__double2float_rn(__dmul_rn(acc[i], inv_n))));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) write_delta(dout, u, E, d0 + i, acc[i], inv_n);
+    }
   }
 }
 
 // Medium segments (kLongSeg < length <= mid_max): one warp per (key, block of
 // W dims) sums each dimension exactly in the reference order (model.hpp:
-// 182-187) — no certificate, no cross-CTA look-back. The segment is walked in
-// tiles of 32 occurrences: lane i loads the tile's i-th example id, then the
-// warp loads the tile's dL/dx values (RPI rows of W dims per instruction, all
-// independent, the next tile's in flight during this tile's chain), and lanes
-// 0..W-1 run the in-order f64 chain over the tile through shuffles.
-// RPI = 32 / W rows per load: E <= W = 32 / RPI (E > 32: RPI = 1, blocks of
-// 32 dims).
+// 182-187) — no certificate, no cross-CTA look-back. The warp first copies the
+// segment's example ids into shared memory (all loads in flight at once), then
+// streams the dL/dx rows through a ring of kMidRing tiles of 32 occurrences
+// with cp.async (no registers held while in flight, kMidRing - 1 tiles ahead
+// of the chain), and lanes 0..W-1 run the in-order f64 chain over each tile
+// from shared memory. RPI = 32 / W rows per copy instruction: E <= W (E > 32:
+// RPI = 1, blocks of 32 dims).
+constexpr int kMidRing = 6;         // tiles in flight per warp
+constexpr int kMidWarps = 2;        // warps per block
+constexpr int kMidMaxSeg = 1024;    // longest segment the id staging holds
+
+__host__ __device__ constexpr std::size_t mid_smem(int rpi) {
+  return std::size_t(kMidWarps) * (kMidMaxSeg * 4 + std::size_t(kMidRing) * 32 * (32 / rpi) * 8);
+}
+
+__device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(valid ? 8 : 0));
+}
+
 template <int RPI>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32 * kMidWarps)
     sparse_mid_kernel(int E, std::uint64_t n, const unsigned long long* __restrict__ n_mid,
                       const std::uint32_t* __restrict__ mid_list,
                       const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
@@ -758,8 +800,12 @@ __global__ void __launch_bounds__(256)
     atomicAdd(mid_keys, (unsigned long long)*n_mid);
   constexpr int W = 32 / RPI;   // dims per block
   constexpr int T = 32;         // occurrences per tile
-  constexpr int NV = T / RPI;   // values per lane per tile
-  const unsigned lane = threadIdx.x & 31;
+  constexpr int NV = T / RPI;   // copies per lane per tile
+  extern __shared__ __align__(16) unsigned char mid_sm[];
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* wbase = mid_sm + std::size_t(wib) * (kMidMaxSeg * 4 + kMidRing * T * W * 8);
+  std::uint32_t* sx = reinterpret_cast<std::uint32_t*>(wbase);          // the segment's ids
+  double* ring = reinterpret_cast<double*>(wbase + kMidMaxSeg * 4);     // [kMidRing][T][W]
   const int rg = int(lane) / W, dl = int(lane) % W;
   const int nblk = (E + W - 1) / W;
   const std::uint64_t items = *n_mid * std::uint64_t(nblk);
@@ -770,35 +816,46 @@ __global__ void __launch_bounds__(256)
     const std::uint32_t u = mid_list[it / nblk];
     const int d = int(it % nblk) * W + dl;
     const bool dv = d < E;
-    const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
-    auto load = [&](std::uint32_t t, double* v) {
-      const std::uint32_t e = t + lane < p1 ? exs[t + lane] : 0u;
+    const std::uint32_t p0 = seg[u], L = seg[u + 1] - p0;  // L <= kMidMaxSeg
+    for (std::uint32_t i = lane; i < L; i += 32) sx[i] = exs[p0 + i];
+    __syncwarp();
+    const int tiles = int((L + T - 1) / T);
+    auto issue = [&](int t) {  // tile t's dL/dx values into ring slot t % kMidRing
+      double* slot = ring + std::size_t(t % kMidRing) * T * W;
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
-        const int k = i * RPI + rg;
-        const std::uint32_t ek = __shfl_sync(0xFFFFFFFFu, e, k);
-        v[i] = (t + k < p1 && dv) ? DX[std::uint64_t(ek) * E + d] : 0.0;
+        const std::uint32_t k = std::uint32_t(t * T + i * RPI + rg);
+        const bool ok = k < L && dv;
+        const double* src = DX + (ok ? std::uint64_t(sx[k]) * E + d : 0);
+        cp_async8_zfill(slot + (i * RPI + rg) * W + dl, src, ok);
       }
+      asm volatile("cp.async.commit_group;\n" ::);
     };
-    double cur[NV], nxt[NV];
-    load(p0, cur);
-    double acc = 0.0;
-    for (std::uint32_t t = p0; t < p1; t += T) {
-      const bool more = t + T < p1;
-      if (more) load(t + T, nxt);
-      const int cnt = int(p1 - t < std::uint32_t(T) ? p1 - t : T);
 #pragma unroll
-      for (int i = 0; i < NV; ++i)
-#pragma unroll
-        for (int q = 0; q < RPI; ++q) {
-          const double x = __shfl_sync(0xFFFFFFFFu, cur[i], q * W + dl);
-          if (i * RPI + q < cnt) acc = __dadd_rn(acc, x);
-        }
-      if (more) {
-#pragma unroll
-        for (int i = 0; i < NV; ++i) cur[i] = nxt[i];
-      }
+    for (int t = 0; t < kMidRing - 1; ++t) {
+      if (t < tiles) issue(t);
+      else asm volatile("cp.async.commit_group;\n" ::);  // (empty groups keep the count)
     }
+    double acc = 0.0;
+    for (int t = 0; t < tiles; ++t) {
+      if (t + kMidRing - 1 < tiles) issue(t + kMidRing - 1);
+      else asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kMidRing - 1));  // tile t landed (mine)
+      __syncwarp();                                                    // (and every lane's)
+      const double* slot = ring + std::size_t(t % kMidRing) * T * W;
+      const int cnt = int(L - std::uint32_t(t) * T < std::uint32_t(T) ? L - t * T : T);
+      if (rg == 0) {
+        double x[T];
+#pragma unroll
+        for (int k = 0; k < T; ++k) x[k] = slot[k * W + dl];
+#pragma unroll
+        for (int k = 0; k < T; ++k)
+          if (k < cnt) acc = __dadd_rn(acc, x[k]);
+      }
+      __syncwarp();  // the slot is refilled kMidRing - 1 tiles later
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncwarp();
     if (rg == 0 && dv) dout.grad(u, E, d, __double2float_rn(__dmul_rn(acc, inv_n)));
   }
 }

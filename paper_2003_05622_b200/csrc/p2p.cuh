@@ -25,7 +25,11 @@
 namespace hpsgpu {
 
 constexpr int kMaxRanks = 8;
-enum P2PPhase { kPhKeys = 0, kPhRows = 1, kPhDeltas = 2, kPhDense = 3, kPhases = 4 };
+// kPhKeys..kPhDense: the four-phase exchange of the parity API and the sort
+// path; kPhX / kPhY: the fused two-phase round of the batch body (below).
+enum P2PPhase {
+  kPhKeys = 0, kPhRows = 1, kPhDeltas = 2, kPhDense = 3, kPhX = 4, kPhY = 5, kPhases = 6
+};
 
 struct PeerWindows {
   std::uint64_t* keys[kMaxRanks];    // peer's keys window base
@@ -231,7 +235,7 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
                                       const std::uint64_t* __restrict__ cap_ptr,
                                       std::uint32_t* __restrict__ rslots, int E, int stride,
                                       unsigned* done_ctr, unsigned long long* served,
-                                      DevError* err, int wait_phase) {
+                                      DevError* err, int wait_phase, int sig_phase) {
   pdl_wait();
   if (wait_phase >= 0) wait_sources(ctx, G, me, wait_phase, err);  // the requests arrived
   const std::uint64_t epoch = ctx.round();
@@ -272,7 +276,7 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
       for (int q = 0; q < VEC; ++q) dst[q] = src[q];
     }
   }
-  signal_peers(pw, G, me, kPhRows, epoch, done_ctr);
+  signal_peers(pw, G, me, sig_phase, epoch, done_ctr);
 }
 
 // Requester -> owners: delta rows (send order) into the owner's deltas
@@ -313,7 +317,7 @@ template <int VEC>
 __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
                                  const std::uint32_t* __restrict__ rslots,
                                  float* __restrict__ tvals, Optim opt, int G, int wait_phase,
-                                 DevError* err) {
+                                 DevError* err, int cnt_field) {
   pdl_wait();
   if (wait_phase >= 0) wait_sources(ctx, G, me, wait_phase, err);  // the deltas arrived
   const PeerWindows& pw = ctx.cur(ctx.round());
@@ -321,7 +325,7 @@ __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
   const float* my_deltas = pw.deltas[me];
   const int E = opt.E;
   const int tpk = E / VEC;
-  const std::uint64_t n = my_hdr[s * 2];
+  const std::uint64_t n = my_hdr[s * 2 + cnt_field];
   for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < n * tpk;
        t += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint64_t i = t / tpk;
@@ -342,14 +346,15 @@ __global__ void p2p_apply_kernel(P2PCtx ctx, int me, int s, std::uint64_t slot,
 // same launch. One CTA.
 __global__ void p2p_dense_update_kernel(P2PCtx ctx, int G, int me, int nodes, int devices,
                                         std::uint64_t nw, float* __restrict__ w, float lr,
-                                        int apply, float* __restrict__ sum_out, DevError* err) {
+                                        int apply, float* __restrict__ sum_out, DevError* err,
+                                        int wait_phase) {
   pdl_wait();
   __shared__ int ok;
   const std::uint64_t epoch = ctx.round();
   if (threadIdx.x == 0) ok = 1;
   __syncthreads();
-  if (threadIdx.x < unsigned(G)) {
-    const std::uint64_t* f = ctx.par[0].flags[me] + threadIdx.x * kPhases + kPhDense;
+  if (threadIdx.x < unsigned(G) && wait_phase >= 0) {
+    const std::uint64_t* f = ctx.par[0].flags[me] + threadIdx.x * kPhases + wait_phase;
     long long spins = 0;
     while (ld_acquire_sys(f) < epoch) {
       if (++spins > (1ll << 27)) {
@@ -393,6 +398,72 @@ __global__ void p2p_send_dense_kernel(P2PCtx ctx, int G, int me, std::uint64_t n
     pw.dense[p][me * nw + i] = grad[i];
   }
   signal_peers(pw, G, me, kPhDense, epoch, done_ctr);
+}
+
+// ---- the fused round of the batch body (two phases per mini-batch) -------
+//
+// Round r of a batch carries, in ONE signalled phase X from every rank to
+// every owner: the sparse deltas of mini-batch j (in the owner's request
+// order of j, counted in hdr[.][2s+1]), the dense replica of j, and the keys
+// of mini-batch j+1 (hdr[.][2s]). Each owner then waits X, applies the
+// senders' deltas in canonical order (p2p_apply_kernel, the rows cached when
+// it served j), does the canonical dense sum + update, and only then serves
+// j+1's rows (phase Y) — so j+1 reads every row after j's apply, the
+// reference's read-after-apply order (oracle.hpp:85-112), with two lockstep
+// points per mini-batch instead of four (keys, rows, deltas, dense). Windows
+// alternate parity by round, and every round but a batch's last ends in Y,
+// so no rank is ever more than one round ahead of a peer.
+template <int VEC>
+__global__ void p2p_send_x_kernel(P2PCtx ctx, int G, int me, std::uint64_t slot, int E,
+                                  const std::uint64_t* __restrict__ dkeys,
+                                  const std::uint64_t* __restrict__ du_ptr,
+                                  const std::uint32_t* __restrict__ dorank,
+                                  const std::uint64_t* __restrict__ dotot,
+                                  const float* __restrict__ deltas, std::uint64_t nw,
+                                  const float* __restrict__ grad,
+                                  const std::uint64_t* __restrict__ nkeys,
+                                  const std::uint64_t* __restrict__ nu_ptr,
+                                  const std::uint32_t* __restrict__ norank,
+                                  const std::uint64_t* __restrict__ notot, unsigned* done_ctr) {
+  pdl_wait();
+  const std::uint64_t epoch = ctx.round();
+  const PeerWindows& pw = ctx.cur(epoch);
+  const std::uint64_t DU = deltas ? *du_ptr : 0, NU = nkeys ? *nu_ptr : 0;
+  if (blockIdx.x == 0 && threadIdx.x < unsigned(G)) {
+    const int o = threadIdx.x;
+    pw.hdr[o][me * 2] = NU ? notot[o] : 0;      // keys of j+1 (served in Y)
+    pw.hdr[o][me * 2 + 1] = DU ? dotot[o] : 0;  // deltas of j (applied after X)
+  }
+  const std::uint64_t stride = std::uint64_t(gridDim.x) * blockDim.x;
+  const std::uint64_t t0 = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x;
+  const int tpk = E / VEC;
+  for (std::uint64_t t = t0; t < DU * tpk; t += stride) {  // deltas -> owners' windows
+    const std::uint64_t u = t / tpk;
+    const int part = int(t - u * tpk);
+    const int o = int(dkeys[u] % std::uint64_t(G));
+    const float* src = deltas + u * E + part * VEC;
+    float* dst = pw.deltas[o] + (me * slot + dorank[u]) * E + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, ld_f4(src));
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) dst[q] = src[q];
+    }
+  }
+  if (grad)  // dense replica -> every peer (all-gather)
+    for (std::uint64_t t = t0; t < nw * G; t += stride) {
+      const int p = int(t / nw);
+      const std::uint64_t i = t - std::uint64_t(p) * nw;
+      pw.dense[p][me * nw + i] = grad[i];
+    }
+  for (std::uint64_t u = t0; u < NU; u += stride) {  // next keys -> owners
+    const std::uint64_t k = nkeys[u];
+    const int o = int(k % std::uint64_t(G));
+    const std::uint64_t at = me * slot + norank[u];
+    pw.keys[o][at] = k;
+    pw.uids[o][at] = std::uint32_t(u);
+  }
+  signal_peers(pw, G, me, kPhX, epoch, done_ctr);
 }
 
 }  // namespace hpsgpu

@@ -140,6 +140,8 @@ struct Scalars {
   unsigned long long big_occ;    // their occurrences
   unsigned long long mid_keys;   // segments on the exact warp-chain path (this batch)
   unsigned long long n_mid;      // this mini-batch's medium segments
+  unsigned long long Ux[2];      // fused exchange: unique keys of mini-batch j, by j & 1
+  unsigned long long xclear[2];  // (scratch for owner_rank_kernel's clear words)
   DevError err;                 // the body's and the parity API's error word
   // per-batch error words of the pipelined stages: the stage's
   // key-range check (by staging slot) and the prep's build (by table), so an
@@ -245,7 +247,8 @@ struct Tier {
   cudaEvent_t fork3 = nullptr, join3 = nullptr;  // fused reduce) beside fwd/bwd + short path
   cudaStream_t st4 = nullptr;           // side stream: the medium segments (sparse_mid_kernel)
   cudaEvent_t fork4 = nullptr, join4 = nullptr;
-  std::uint32_t mid_max = 1024;         // medium segments: kLongSeg < length <= mid_max
+  int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
+  std::uint32_t mid_max = 512;          // medium segments: kLongSeg < length <= mid_max
                                         // (HPS_MID_SEG; kLongSeg disables the path)
   Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
                                         // 2..: the next batch's mini-batch groupings
@@ -332,6 +335,12 @@ struct Tier {
   std::uint64_t fuse_items = 0;
   std::uint64_t* otot = nullptr;
   std::uint64_t* ukeys = nullptr;
+  // fused exchange (G > 1, grouped; HPS_XFUSE=0: the four-phase exchange):
+  // unique keys, owner ranks and per-owner counts of mini-batch j, by j & 1
+  bool xfuse = true;
+  std::uint64_t* xukeys[2] = {};
+  std::uint32_t* xorank[2] = {};
+  std::uint64_t* xotot[2] = {};
   float *rows = nullptr, *deltas = nullptr, *hstage = nullptr, *staged = nullptr;
   std::uint64_t staged_cap = 0;  // floats
 
@@ -436,6 +445,7 @@ struct Tier {
   bool use_graphs = true;
   std::map<std::vector<std::uint64_t>, GraphEntry> graphs;
   std::uint64_t graph_clock = 0;     // LRU clock of the graph cache
+  std::vector<cudaGraphExec_t> retired;  // evicted graphs, destroyed once nothing is in flight
   std::uint64_t graph_captures = 0;  // captures so far (diagnostics, bench)
 };
 
@@ -1067,7 +1077,7 @@ static hps_status exchange_pull(Tier* t, std::uint64_t n, bool do_gather) {
     launch(t, k, grid_for(work, 256, kSMs * 4), 256, 0, t->ctx, t->G, t->g, t->slot,
            (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
            (const std::uint64_t*)&t->dsc->cap[t->cur], t->w_rslots, t->E, t->RW, t->done_ctr,
-           &t->dsc->served, &t->dsc->err, fold ? int(kPhKeys) : -1);
+           &t->dsc->served, &t->dsc->err, fold ? int(kPhKeys) : -1, int(kPhRows));
     p2p_wait(t, kPhRows);
     mark(t, HPS_T_PULL);
   }
@@ -1094,7 +1104,7 @@ static hps_status push_apply(Tier* t) {
   for (int src : canonical_senders(t)) {
     launch(t, k, grid_for(t->slot * std::uint64_t(t->E / V), 256, kSMs * 2), 256, 0, t->ctx, t->g,
            src, t->slot, (const std::uint32_t*)t->w_rslots, t->tvals[t->cur], t->opt, t->G,
-           first ? int(kPhDeltas) : -1, &t->dsc->err);
+           first ? int(kPhDeltas) : -1, &t->dsc->err, 0);
     first = false;
   }
   return HPS_OK;
@@ -1115,7 +1125,7 @@ static hps_status dense_sync_update(Tier* t, bool apply) {
   launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->ctx, t->G, t->g, nw,
          (const float*)t->dgrad, t->done_ctr);
   launch(t, p2p_dense_update_kernel, 1, 256, 0, t->ctx, t->G, t->g, t->N, t->D, nw, t->dense,
-         t->cfg.learning_rate, int(apply), (float*)nullptr, &t->dsc->err);
+         t->cfg.learning_rate, int(apply), (float*)nullptr, &t->dsc->err, int(kPhDense));
   return HPS_OK;
 }
 
@@ -1263,19 +1273,11 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
     HPS_CUDA(cudaStreamWaitEvent(ms, t->fork4, 0));
   }
   if (t->mid_max > std::uint32_t(kLongSeg)) {
-    if (E <= 8) {
-      launch_on(t, ms, sparse_mid_kernel<4>, kSMs * 8, 256, 0, E, n,
-                (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
-                exs, dout, DX, &t->dsc->mid_keys);
-    } else if (E <= 16) {
-      launch_on(t, ms, sparse_mid_kernel<2>, kSMs * 8, 256, 0, E, n,
-                (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
-                exs, dout, DX, &t->dsc->mid_keys);
-    } else {
-      launch_on(t, ms, sparse_mid_kernel<1>, kSMs * 8, 256, 0, E, n,
-                (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
-                exs, dout, DX, &t->dsc->mid_keys);
-    }
+    const int rpi = E <= 8 ? 4 : (E <= 16 ? 2 : 1);
+    auto mk = rpi == 4 ? sparse_mid_kernel<4> : (rpi == 2 ? sparse_mid_kernel<2> : sparse_mid_kernel<1>);
+    launch_on(t, ms, mk, kSMs * 4, 32 * kMidWarps, mid_smem(rpi), E, n,
+              (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
+              exs, dout, DX, &t->dsc->mid_keys);
   }
   if (t->big_side) HPS_CUDA(cudaEventRecord(t->join4, ms));
   mark_big(t, -1);
@@ -1286,9 +1288,10 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
             DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, &t->dsc->fallbacks);
   mark_big(t, HPS_T_BIGFUSED);
   HPS_CUDA(cudaEventRecord(t->join3, bs));
-  // DPT dims per thread (4 when E allows 32-byte row loads)
-  const int dpt = (E % 4 == 0) ? 4 : 1;
-  auto sk = dpt == 4 ? sparse_short_kernel<4> : sparse_short_kernel<1>;
+  // DPT dims per thread (8 / 4 when E allows 64- / 32-byte row loads)
+  const int dpt = t->short_dpt ? t->short_dpt : ((E % 8 == 0) ? 8 : ((E % 4 == 0) ? 4 : 1));
+  auto sk = dpt == 8 ? sparse_short_kernel<8>
+                     : (dpt == 4 ? sparse_short_kernel<4> : sparse_short_kernel<1>);
   launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,
          E, lr, n, U, seg, exs, dout, DX, &t->dsc->pulled);
   HPS_CUDA(cudaStreamWaitEvent(t->st, t->join3, 0));
@@ -1616,6 +1619,75 @@ static hps_status enqueue_store_gather(Tier* T, const BatchShape& sh, int tb) {
   return HPS_OK;
 }
 
+// Fused exchange (p2p.cuh p2p_send_x_kernel): mini-batch j's unique keys in
+// uid order and their owner ranks into the j & 1 buffers; the owner-rank pass
+// opens the next exchange round (device epoch).
+static void x_keys(Tier* T, const BatchShape& sh, const BatchPlan& bp, int j) {
+  const int q = j & 1;
+  const std::uint64_t r0 = group_region(sh, j), ob = sh.mb_bound[j];
+  launch(T, uid_keys_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)(T->g_uidb[bp.tb] + r0),
+         (const std::uint64_t*)T->rq_keys[bp.tb],
+         (const unsigned long long*)&T->dsc->Ug[bp.tb][j], T->xukeys[q], &T->dsc->Ux[q]);
+  const std::uint32_t nb =
+      std::max<std::uint32_t>(1, std::uint32_t((ob + kRankTile - 1) / kRankTile));
+  ++T->p2p_epoch;  // host mirror of the round the kernel opens
+  launch(T, owner_rank_kernel, nb, kRankThreads, 0, (const std::uint64_t*)T->xukeys[q],
+         (const std::uint64_t*)&T->dsc->Ux[q], T->G, next_lookback(T, nb), T->xorank[q],
+         T->xotot[q], &T->dsc->epoch, T->dsc->xclear);
+}
+
+// One fused round: the deltas of mini-batch jd (-1: none) and the dense
+// replica (dense) go to the owners with the keys of mini-batch jk (-1: none)
+// in one signalled phase X; then this rank, as owner, applies every sender's
+// deltas in canonical order, updates the dense weights, and serves jk's rows
+// (phase Y), waiting for its own.
+static hps_status x_round(Tier* T, int jd, bool dense, int jk) {
+  const int V = vec_of(T->E), G = T->G;
+  const int qd = jd & 1, qk = jk & 1;
+  auto sx = V == 4 ? p2p_send_x_kernel<4> : p2p_send_x_kernel<1>;
+  launch(T, sx, grid_for(T->Omax * std::uint64_t(T->E / V), 256, kSMs * 4), 256, 0, T->ctx, G,
+         T->g, T->slot, T->E, (const std::uint64_t*)(jd >= 0 ? T->xukeys[qd] : nullptr),
+         (const std::uint64_t*)(jd >= 0 ? &T->dsc->Ux[qd] : nullptr),
+         (const std::uint32_t*)(jd >= 0 ? T->xorank[qd] : nullptr),
+         (const std::uint64_t*)(jd >= 0 ? T->xotot[qd] : nullptr),
+         (const float*)(jd >= 0 ? T->deltas : nullptr), std::uint64_t(T->md.nw),
+         (const float*)(dense ? T->dgrad : nullptr),
+         (const std::uint64_t*)(jk >= 0 ? T->xukeys[qk] : nullptr),
+         (const std::uint64_t*)(jk >= 0 ? &T->dsc->Ux[qk] : nullptr),
+         (const std::uint32_t*)(jk >= 0 ? T->xorank[qk] : nullptr),
+         (const std::uint64_t*)(jk >= 0 ? T->xotot[qk] : nullptr), T->done_ctr);
+  bool waited = false;
+  if (jd >= 0) {  // owner apply, senders in canonical order; the first waits for X
+    auto k = V == 4 ? p2p_apply_kernel<4> : p2p_apply_kernel<1>;
+    for (int src : canonical_senders(T)) {
+      launch(T, k, grid_for(T->slot * std::uint64_t(T->E / V), 256, kSMs * 2), 256, 0, T->ctx,
+             T->g, src, T->slot, (const std::uint32_t*)T->w_rslots, T->tvals[T->cur], T->opt, G,
+             waited ? -1 : int(kPhX), &T->dsc->err, 1);
+      waited = true;
+    }
+  }
+  mark(T, HPS_T_APPLY);
+  if (dense) {
+    launch(T, p2p_dense_update_kernel, 1, 256, 0, T->ctx, G, T->g, T->N, T->D,
+           std::uint64_t(T->md.nw), T->dense, T->cfg.learning_rate, 1, (float*)nullptr,
+           &T->dsc->err, waited ? -1 : int(kPhX));
+    waited = true;
+  }
+  mark(T, HPS_T_DENSE);
+  if (jk >= 0) {  // serve the next mini-batch's rows (after the apply), then wait for ours
+    auto k = V == 4 ? p2p_serve_rows_kernel<4> : p2p_serve_rows_kernel<1>;
+    launch(T, k, grid_for(T->Omax * std::uint64_t(T->E / V), 256, kSMs * 4), 256, 0, T->ctx, G,
+           T->g, T->slot, (const std::uint64_t*)T->tkeys[T->cur], (const float*)T->tvals[T->cur],
+           (const std::uint64_t*)&T->dsc->cap[T->cur], T->w_rslots, T->E, T->RW, T->done_ctr,
+           &T->dsc->served, &T->dsc->err, waited ? -1 : int(kPhX), int(kPhY));
+    p2p_wait(T, kPhY);
+  } else if (!waited) {
+    launch(T, p2p_wait_kernel, 1, 32, 0, T->ctx, G, T->g, int(kPhX), &T->dsc->err);
+  }
+  mark(T, HPS_T_PULL);
+  return HPS_OK;
+}
+
 // The body of one batch (lane 0): carried rows from the previous table, then
 // J x {shard gather, dedup, pull, fwd/bwd, sparse reduce, push + canonical
 // apply, dense sync + update}. Enqueue-only (no host synchronisation, no
@@ -1662,6 +1734,13 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                                                                           : 0));
   }
   mark(T, HPS_T_BUILD);
+  // G > 1 fused exchange: the first round carries only mini-batch 0's keys
+  const bool xf = G > 1 && bp.grouped && T->xfuse;
+  if (xf) {
+    x_keys(T, sh, bp, 0);
+    mark(T, HPS_T_DEDUP);
+    HPS_TRY(x_round(T, -1, false, 0));
+  }
   // ---- mini-batches
   const int V = vec_of(E);
   for (int j = 0; j < J; ++j) {
@@ -1695,6 +1774,9 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
         occ_row = T->g_occslot[bp.tb];
         rows = T->tvals[T->cur];
         rstride = T->RW;
+      } else if (xf) {  // rows of this mini-batch arrived in the previous round (uid order)
+        Uj = reinterpret_cast<const std::uint64_t*>(&T->dsc->Ux[j & 1]);
+        occ_row = T->g_inv[bp.tb];
       } else {  // unique keys in uid order -> the NVLink exchange -> rows by uid
         // (the kernel also copies the count into dsc->U: no memcpy node,
         // which would break the programmatic-launch chain)
@@ -1762,6 +1844,14 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
       HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));
     }
     mark(T, HPS_T_GRADS);
+    if (xf) {  // one fused round: deltas + dense replica of j, keys of j + 1
+      const bool next = j + 1 < J;
+      if (next) x_keys(T, sh, bp, j + 1);
+      else begin_round(T, true);
+      mark(T, HPS_T_DEDUP);
+      HPS_TRY(x_round(T, j, j != bp.skip_mb, next ? j + 1 : -1));
+      continue;
+    }
     // push + canonical apply (a10, a11); grouped at one rank the sparse
     // reduce already applied each key's delta in place
     if (G == 1 && bp.grouped) {
@@ -1871,19 +1961,20 @@ static hps_status wb_fence(Tier* T, int p = -1, cudaStream_t s = nullptr) {
 }
 
 // Capture `enqueue` on the current lane's stream once per key (no launch):
-// a whole prep or body becomes one graph. The cache keeps the 64 most
-// recently used graphs.
+// a whole prep or body becomes one graph. The cache keeps the 256 most
+// recently used graphs; an evicted one may still be running (batches are in
+// flight), so it is destroyed only at the next quiesce.
 template <class Fn>
 static hps_status capture_graph(Tier* T, const std::vector<std::uint64_t>& key, Fn&& enqueue,
                                 GraphEntry** out) {
   cudaStream_t s = T->L->st;
   auto it = T->graphs.find(key);
   if (it == T->graphs.end()) {
-    if (T->graphs.size() >= 64) {  // bounded cache: evict the least recently used
+    if (T->graphs.size() >= 256) {  // bounded cache: evict the least recently used
       auto lru = T->graphs.begin();
       for (auto i = T->graphs.begin(); i != T->graphs.end(); ++i)
         if (i->second.last_use < lru->second.last_use) lru = i;
-      cudaGraphExecDestroy(lru->second.exec);
+      T->retired.push_back(lru->second.exec);
       T->graphs.erase(lru);
     }
     GraphEntry ge;
@@ -2005,6 +2096,11 @@ static hps_status quiesce(Tier* T) {
     while (!T->inflight.empty()) complete_oldest(T);
     // the batches reported their own errors; the parity API starts clean
     HPS_CUDA(cudaMemsetAsync(&T->dsc->err, 0, sizeof(DevError), T->st));
+  }
+  if (!T->retired.empty()) {  // no batch in flight: evicted graphs can go
+    HPS_CUDA(cudaStreamSynchronize(T->st));
+    for (cudaGraphExec_t g : T->retired) cudaGraphExecDestroy(g);
+    T->retired.clear();
   }
   HPS_TRY(flush_all(T));
   return wb_fence(T);
@@ -2424,9 +2520,15 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     t->prep_mbs = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_BIG_SIDE")) t->big_side = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_SHORT_DPT")) {
+    const int d = std::atoi(v);
+    if (d == 1 || (d == 4 && c.embedding_dim % 4 == 0) || (d == 8 && c.embedding_dim % 8 == 0))
+      t->short_dpt = d;
+  }
   if (const char* v = std::getenv("HPS_MID_SEG"))
-    t->mid_max = std::uint32_t(std::max(kLongSeg, std::atoi(v)));
+    t->mid_max = std::uint32_t(std::min(kMidMaxSeg, std::max(kLongSeg, std::atoi(v))));
   if (const char* v = std::getenv("HPS_FOLD_WAIT")) t->fold_wait = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_XFUSE")) t->xfuse = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_WS_SORT")) t->ws_sort = std::atoi(v) != 0 ? 1 : 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
@@ -2558,6 +2660,12 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     cudaFuncSetAttribute(fwd_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(sparse_mid_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(mid_smem(1)));
+    cudaFuncSetAttribute(sparse_mid_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(mid_smem(2)));
+    cudaFuncSetAttribute(sparse_mid_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(mid_smem(4)));
     cudaFuncSetAttribute(umma_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(gemm_smem(256, true)));
     cudaFuncSetAttribute(umma_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2678,6 +2786,12 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   A(item_chunk, t->fuse_items);
   A(fuse_ticket, 1);
   A(ukeys, S);
+  if (G > 1)
+    for (int q = 0; q < 2; ++q) {
+      A(xukeys[q], S);
+      A(xorank[q], S);
+      A(xotot[q], kMaxRanks);
+    }
   if (G == 1) A(rows, S * E);  // G > 1: inside the exported window (peers write it)
   A(deltas, S * E);
   A(hstage, S * E);
@@ -2749,6 +2863,7 @@ hps_status hps_destroy(hps_tier_t t) {
   cudaFree(t->pend_keys);
   cudaFree(t->pend_deltas);
   for (auto& kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
+  for (cudaGraphExec_t g : t->retired) cudaGraphExecDestroy(g);
   for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : t->allocs) cudaFree(p);
   if (t->hsc) cudaFreeHost(t->hsc);
@@ -3044,23 +3159,24 @@ hps_status hps_table_lookup(hps_tier_t t, const uint64_t* keys, uint64_t n, uint
                             float* rows) {
   HPS_ENTER_Q(t);
   HPS_TRY(require_built(t));
-  if (n > t->Omax)
-    return set_error(HPS_ERR_CAPACITY, "lookup: %llu keys exceed max_batch_keys",
-                     (unsigned long long)n);
   if (!n) return HPS_OK;
   if (!keys || !found) return set_error(HPS_ERR_ARG, "null argument");
-  HPS_TRY(ensure_staged(t, n * std::uint64_t(t->RW)));
-  auto* dfound = reinterpret_cast<std::uint8_t*>(t->lane[0].vB);  // (n bytes <= Omax x 4)
-  HPS_CUDA(cudaMemcpyAsync(t->lane[0].kB, keys, n * 8, cudaMemcpyHostToDevice, t->st));
-  launch(t, table_lookup_kernel, grid_for(n), 256, 0, (const std::uint64_t*)t->lane[0].kB, n,
-         (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
-         (const std::uint64_t*)&t->dsc->cap[t->cur], t->RW, dfound,
-         rows ? t->staged : (float*)nullptr);
-  HPS_CUDA(cudaMemcpyAsync(found, dfound, n, cudaMemcpyDeviceToHost, t->st));
-  if (rows)
-    HPS_CUDA(cudaMemcpyAsync(rows, t->staged, n * std::uint64_t(t->RW) * 4,
-                             cudaMemcpyDeviceToHost, t->st));
-  HPS_CUDA(cudaStreamSynchronize(t->st));
+  const std::uint64_t RW = std::uint64_t(t->RW);
+  for (std::uint64_t c0 = 0; c0 < n; c0 += t->Omax) {  // chunks within the key scratch
+    const std::uint64_t m = std::min(t->Omax, n - c0);
+    HPS_TRY(ensure_staged(t, m * RW));
+    auto* dfound = reinterpret_cast<std::uint8_t*>(t->lane[0].vB);  // (m bytes <= Omax x 4)
+    HPS_CUDA(cudaMemcpyAsync(t->lane[0].kB, keys + c0, m * 8, cudaMemcpyHostToDevice, t->st));
+    launch(t, table_lookup_kernel, grid_for(m), 256, 0, (const std::uint64_t*)t->lane[0].kB, m,
+           (const std::uint64_t*)t->tkeys[t->cur], (const float*)t->tvals[t->cur],
+           (const std::uint64_t*)&t->dsc->cap[t->cur], t->RW, dfound,
+           rows ? t->staged : (float*)nullptr);
+    HPS_CUDA(cudaMemcpyAsync(found + c0, dfound, m, cudaMemcpyDeviceToHost, t->st));
+    if (rows)
+      HPS_CUDA(cudaMemcpyAsync(rows + c0 * RW, t->staged, m * RW * 4, cudaMemcpyDeviceToHost,
+                               t->st));
+    HPS_CUDA(cudaStreamSynchronize(t->st));
+  }
   return HPS_OK;
 }
 
@@ -3131,7 +3247,7 @@ hps_status hps_dense_sync(hps_tier_t t, float* buf, uint64_t len, int determinis
     launch(t, p2p_send_dense_kernel, grid_for(nw * t->G), 256, 0, t->ctx, t->G, t->g, nw,
            (const float*)t->dgrad, t->done_ctr);
     launch(t, p2p_dense_update_kernel, 1, 256, 0, t->ctx, t->G, t->g, t->N, t->D, nw,
-           (float*)nullptr, 1.0f, 0, sum, &t->dsc->err);
+           (float*)nullptr, 1.0f, 0, sum, &t->dsc->err, int(kPhDense));
     HPS_CUDA(cudaMemcpyAsync(buf + c0, sum, L * 4, cudaMemcpyDeviceToHost, t->st));
   }
   return check_device_error(t, "device table: missing key ", true);

@@ -181,6 +181,11 @@ def main():
                                           1024, 5, 24, pipelined=True, optimizer="adagrad")
     results["train_adagrad_hbm"] = case_train(world, rank, oracle, 8, (8, 16, 1), 4, True, 20000,
                                               512, 4, 20, hbm_store=True, optimizer="adagrad")
+    # the four-phase exchange (HPS_XFUSE=0) next to the default fused rounds
+    os.environ["HPS_XFUSE"] = "0"
+    results["train_xfuse0"] = case_train(world, rank, oracle, 16, (8, 16, 1), 4, True, 50000,
+                                         1024, 5, 30, pipelined=True)
+    del os.environ["HPS_XFUSE"]
     flags = torch.tensor([int(v) for v in results.values()], device="cuda")
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:
