@@ -170,77 +170,103 @@ __device__ __forceinline__ void put_split(char* dst, std::size_t lo_off, std::si
   }
 }
 
-// Stage a rows x kGemmBK tile of X(r, k) (r in [r0, r0+rows), k in [k0, k0+32),
-// zero outside [0, R) x [0, klim)) into the canonical layout at dst:
-// byte offset (r/8)*1024 + (k/4)*128 + (r%8)*16 + (k%4)*4 (the lo parts of a
-// split at dst + lo_off, same layout).
-__device__ __forceinline__ void stage_tile(float* dst, int rows, const float* X, std::int64_t x_r,
-                                           std::int64_t x_k, int r0, int R, int k0, int klim,
-                                           int ones_row, bool split, std::size_t lo_off) {
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async4_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 4 : 0));
+}
+
+// Issue the cp.async copies of a rows x kGemmBK tile of X(r, k) (r in
+// [r0, r0+rows), k in [k0, k0+32), zero outside [0, R) x [0, klim)) into the
+// canonical layout at dst: byte (r/8)*1024 + (k/4)*128 + (r%8)*16 + (k%4)*4.
+// No registers are held while the copies are in flight. The ones row (the
+// bias column of the weight-gradient GEMM) is written directly.
+__device__ __forceinline__ void stage_tile_async(float* dst, int rows, const float* X,
+                                                 std::int64_t x_r, std::int64_t x_k, int r0,
+                                                 int R, int k0, int klim, int ones_row) {
   const int tid = threadIdx.x;
+  char* base = reinterpret_cast<char*>(dst);
   if (x_k == 1 && (x_r & 3) == 0 && (reinterpret_cast<std::uintptr_t>(X) & 15) == 0 &&
       (klim & 3) == 0) {
-    // K contiguous: 16-byte loads; thread -> (row % 8) fastest, then the
-    // K chunk, so consecutive threads fill consecutive 16-byte smem slots
+    // K contiguous: one 16-byte copy per core-matrix row; thread -> (row % 8)
+    // fastest, then the K chunk
     const int chunks = rows * (kGemmBK / 4);
     for (int c = tid; c < chunks; c += kGemmThreads) {
       const int r8 = c & 7, kc = (c >> 3) & 7, rg = c >> 6;
       const int r = rg * 8 + r8, gr = r0 + r, gk = k0 + kc * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      char* at = base + rg * 1024 + kc * 128 + r8 * 16;
       if (gr == ones_row) {
-        if (gk < klim) v = make_float4(1.f, 1.f, 1.f, 1.f);
-      } else if (gr < R && gk < klim) {
-        v = *reinterpret_cast<const float4*>(X + gr * x_r + gk);
-      }
-      char* at = reinterpret_cast<char*>(dst) + rg * 1024 + kc * 128 + r8 * 16;
-      if (split) {
-        const float4 hi = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-        *reinterpret_cast<float4*>(at) = hi;
-        *reinterpret_cast<float4*>(at + lo_off) =
-            make_float4(__fsub_rn(v.x, hi.x), __fsub_rn(v.y, hi.y), __fsub_rn(v.z, hi.z),
-                        __fsub_rn(v.w, hi.w));
+        *reinterpret_cast<float4*>(at) =
+            gk < klim ? make_float4(1.f, 1.f, 1.f, 1.f) : make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
-        *reinterpret_cast<float4*>(at) = v;
+        const bool ok = gr < R && gk < klim;
+        cp_async16_zfill(at, ok ? X + gr * x_r + gk : X, ok);
       }
     }
   } else {
-    // general strides (transposed operands): thread -> row fastest
+    // general strides (transposed operands): 4-byte copies, row fastest
     const int elems = rows * kGemmBK;
     for (int e = tid; e < elems; e += kGemmThreads) {
       const int r = e % rows, k = e / rows;
       const int gr = r0 + r, gk = k0 + k;
-      float v = 0.f;
+      char* at = base + (r >> 3) * 1024 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
       if (gr == ones_row) {
-        if (gk < klim) v = 1.f;
-      } else if (gr < R && gk < klim) {
-        v = X[gr * x_r + std::int64_t(gk) * x_k];
+        *reinterpret_cast<float*>(at) = gk < klim ? 1.f : 0.f;
+      } else {
+        const bool ok = gr < R && gk < klim;
+        cp_async4_zfill(at, ok ? X + gr * x_r + std::int64_t(gk) * x_k : X, ok);
       }
-      put_split(reinterpret_cast<char*>(dst), lo_off,
-                std::size_t((r >> 3) * 1024 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4), v, split);
     }
   }
 }
 
-// Dynamic shared memory of umma_gemm_kernel<BN>: 2 stages x (A + B tiles),
-// twice that for the 3xTF32 hi/lo split.
+// 3xTF32: split a landed stage in place, hi = tf32_rna(x) over x, lo = x - hi
+// at + lo_off (same layout). Each thread converts 16-byte chunks.
+__device__ __forceinline__ void split_stage(char* base, std::size_t bytes, std::size_t lo_off) {
+  for (std::size_t o = std::size_t(threadIdx.x) * 16; o < bytes; o += kGemmThreads * 16) {
+    const float4 v = *reinterpret_cast<const float4*>(base + o);
+    const float4 hi = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    *reinterpret_cast<float4*>(base + o) = hi;
+    *reinterpret_cast<float4*>(base + lo_off + o) =
+        make_float4(__fsub_rn(v.x, hi.x), __fsub_rn(v.y, hi.y), __fsub_rn(v.z, hi.z),
+                    __fsub_rn(v.w, hi.w));
+  }
+}
+
+// Stages in the shared-memory ring of umma_gemm_kernel<BN>: as many as fit in
+// ~200 KB, 2..4. A stage is the A and B tiles (twice that with the split).
+__host__ __device__ constexpr int gemm_stages(int bn, bool split) {
+  return (200 * 1024) / int(std::size_t(kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1)) < 2
+             ? 2
+             : ((200 * 1024) / int(std::size_t(kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1)) > 4
+                    ? 4
+                    : (200 * 1024) / int(std::size_t(kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1)));
+}
 __host__ __device__ constexpr std::size_t gemm_smem(int bn, bool split) {
-  return std::size_t(2) * (kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1);
+  return std::size_t(gemm_stages(bn, split)) * (kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1);
 }
 
 // D(m, n) = sum_k A(m, k) B(n, k) (+ epilogue), (3x)TF32 -> FP32 on tcgen05.
 // grid (ceil(M/128), ceil(N/BN), k slices); dynamic smem gemm_smem(BN, split3).
+// K walks a ring of gemm_stages() stages: the copies of stage it + S - 1 are
+// issued (cp.async) before stage it is consumed, so global latency overlaps
+// the MMAs; a stage's buffer is refilled once the MMAs that read it committed.
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) {
   pdl_wait();
   extern __shared__ __align__(1024) std::uint8_t gsm[];
   const bool split = g.split3 != 0;
+  const int S = gemm_stages(BN, split);
   // per stage: A hi, B hi (, A lo, B lo)
   constexpr std::size_t kA = std::size_t(kGemmBM) * kGemmBK * 4, kB = std::size_t(BN) * kGemmBK * 4;
   const std::size_t stage_bytes = (kA + kB) * (split ? 2 : 1);
-  float* sA[2] = {reinterpret_cast<float*>(gsm), reinterpret_cast<float*>(gsm + stage_bytes)};
-  float* sB[2] = {reinterpret_cast<float*>(gsm + kA), reinterpret_cast<float*>(gsm + stage_bytes + kA)};
   const std::size_t lo_off = kA + kB;  // lo parts follow the stage's hi tiles
-  __shared__ __align__(8) std::uint64_t bar[2];
+  __shared__ __align__(8) std::uint64_t bar[4];
   __shared__ std::uint32_t tmem_base_sh;
   constexpr int kCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -254,8 +280,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (threadIdx.x == 32) {
-    mbar_init1(&bar[0]);
-    mbar_init1(&bar[1]);
+    for (int i = 0; i < 4; ++i) mbar_init1(&bar[i]);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   tc_fence_before();
@@ -265,18 +290,40 @@ __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) 
   const std::uint32_t idesc = umma_idesc_tf32(kGemmBM, BN);
   const int nk = (ke - kb + kGemmBK - 1) / kGemmBK;
   const int ones_row = g.b_ones_col ? g.N - 1 - n0 : -1;  // tile-local row of the ones column
+  const int RB = g.b_ones_col ? g.N - 1 - n0 : g.N - n0;
+  const float* Bt = g.B + std::int64_t(n0) * g.b_n;
+  auto stage_ptr = [&](int i) { return gsm + std::size_t(i % S) * stage_bytes; };
+  auto issue = [&](int i) {  // copies of k-stage i (an empty group past the end)
+    if (i < nk) {
+      const int k0 = kb + i * kGemmBK;
+      std::uint8_t* sp = stage_ptr(i);
+      stage_tile_async(reinterpret_cast<float*>(sp), kGemmBM, g.A, g.a_m, g.a_k, m0, g.M, k0, ke,
+                       -1);
+      stage_tile_async(reinterpret_cast<float*>(sp + kA), BN, Bt, g.b_n, g.b_k, 0, RB, k0, ke,
+                       ones_row);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  for (int i = 0; i < S - 1; ++i) issue(i);
   for (int it = 0; it < nk; ++it) {
-    const int s = it & 1;
-    if (it >= 2) mbar_wait_parity(&bar[s], std::uint32_t(((it - 2) >> 1) & 1));
-    const int k0 = kb + it * kGemmBK;
-    stage_tile(sA[s], kGemmBM, g.A, g.a_m, g.a_k, m0, g.M, k0, ke, -1, split, lo_off);
-    stage_tile(sB[s], BN, g.B + std::int64_t(n0) * g.b_n, g.b_n, g.b_k, 0,
-               g.b_ones_col ? g.N - 1 - n0 : g.N - n0, k0, ke, ones_row, split, lo_off);
-    fence_async_smem();
+    // the buffer of k-stage it + S - 1 was last read by the MMAs of it - 1
+    if (it >= 1) mbar_wait_parity(&bar[(it - 1) % S], std::uint32_t(((it - 1) / S) & 1));
+    issue(it + S - 1);
+    // this thread's copies of stage it landed (S - 1 younger groups may pend)
+    if (S == 4) asm volatile("cp.async.wait_group 3;\n" ::: "memory");
+    else if (S == 3) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+    else asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    std::uint8_t* sp = stage_ptr(it);
+    if (split) {
+      split_stage(reinterpret_cast<char*>(sp), kA + kB, lo_off);
+      __syncthreads();
+    }
+    fence_async_smem();  // generic-proxy smem writes -> the tensor core's async proxy
     __syncthreads();
     if (threadIdx.x == 0) {
       tc_fence_after();
-      const std::uint32_t a0 = smem_u32_addr(sA[s]), b0 = smem_u32_addr(sB[s]);
+      const std::uint32_t a0 = smem_u32_addr(sp), b0 = smem_u32_addr(sp + kA);
       const std::uint32_t lo = std::uint32_t(lo_off);
 #pragma unroll
       for (int kk = 0; kk < kGemmBK / 8; ++kk) {
@@ -291,10 +338,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) 
           umma_tf32(tmem, ah, bh, idesc, (it | kk) != 0);
         }
       }
-      umma_commit(&bar[s]);
+      umma_commit(&bar[it % S]);
     }
   }
-  if (nk > 0) mbar_wait_parity(&bar[(nk - 1) & 1], std::uint32_t(((nk - 1) >> 1) & 1));
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  if (nk > 0) mbar_wait_parity(&bar[(nk - 1) % S], std::uint32_t(((nk - 1) / S) & 1));
   tc_fence_after();
   // epilogue: thread owns output row m0 + 32*warp + lane
   const int m = m0 + warp * 32 + lane;
@@ -337,16 +385,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) 
 
 // ---- CUDA-core kernels of the wide path -------------------------------
 
-// X[k][d] = f32(sum over the example's features of row[d]) in f64, feature
-// order (embed_sum, model.hpp:84-95). One warp per example, lanes over d.
+// X[k][d] = f32(sum over the example's features of row[d]) (embed_sum,
+// model.hpp:84-95), accumulated in f64. The wide path is not bit-exact (its
+// GEMMs are 3xTF32), so the sum need not follow the feature order: one warp per
+// example, lanes over features (independent 16-byte row loads), then a
+// shuffle tree over the lanes per dimension — the feature-ordered chain of
+// dependent loads cost ~0.2 ms per mini-batch at c4's 150 keys per example.
 __global__ void __launch_bounds__(256)
     wide_embed_kernel(ShardMap sm, const std::int64_t* __restrict__ goff,
                       const std::uint32_t* __restrict__ occ_off,
                       const std::uint32_t* __restrict__ occ_row, const float* __restrict__ rows,
                       int rstride, int E, float* __restrict__ X) {
   pdl_wait();
+  constexpr int kDims = 16;  // dims per pass (4 float4 per row)
   const int lane = threadIdx.x & 31;
   const std::uint64_t warps = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const bool vec = (E % 4 == 0) && (rstride % 4 == 0);
   for (std::uint64_t k = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5;
        k < sm.count; k += warps) {
     std::uint32_t o0, o1;
@@ -358,13 +412,39 @@ __global__ void __launch_bounds__(256)
       o0 = occ_off[k];
       o1 = occ_off[k + 1];
     }
-    for (int d0 = 0; d0 < E; d0 += 32) {
-      const int d = d0 + lane;
-      double acc = 0.0;
-      if (d < E)
-        for (std::uint32_t p = o0; p < o1; ++p)
-          acc = __dadd_rn(acc, double(rows[std::uint64_t(occ_row[p]) * rstride + d]));
-      if (d < E) X[k * E + d] = __double2float_rn(acc);
+    for (int d0 = 0; d0 < E; d0 += kDims) {
+      const int nd = E - d0 < kDims ? E - d0 : kDims;
+      double acc[kDims];
+#pragma unroll
+      for (int i = 0; i < kDims; ++i) acc[i] = 0.0;
+      for (std::uint32_t p = o0 + lane; p < o1; p += 32) {
+        const float* row = rows + std::uint64_t(occ_row[p]) * rstride + d0;
+        if (vec && nd == kDims) {
+#pragma unroll
+          for (int q = 0; q < kDims / 4; ++q) {
+            const float4 v = ld_f4(row + 4 * q);
+            acc[4 * q] += double(v.x);
+            acc[4 * q + 1] += double(v.y);
+            acc[4 * q + 2] += double(v.z);
+            acc[4 * q + 3] += double(v.w);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < kDims; ++i)
+            if (i < nd) acc[i] += double(row[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kDims; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xFFFFFFFFu, acc[i], o);
+      if (lane < nd) {
+        double v = acc[0];
+#pragma unroll
+        for (int i = 1; i < kDims; ++i)
+          if (lane == i) v = acc[i];
+        X[k * E + d0 + lane] = __double2float_rn(v);
+      }
     }
   }
 }
@@ -403,24 +483,24 @@ __global__ void __launch_bounds__(256)
 }
 
 // Output layer's gradients: g[i] = sum_k dz[k] H[k][i] / n (i < K), bias
-// g[K] = sum_k dz[k] / n. One block per 32 columns, fixed reduction order.
+// g[K] = sum_k dz[k] / n. One block per column: threads stride the examples,
+// then a fixed-order block reduction (deterministic).
 __global__ void __launch_bounds__(256)
     wide_head_grad_kernel(std::uint64_t n, int K, const float* __restrict__ dz,
                           const float* __restrict__ H, float* __restrict__ g) {
   pdl_wait();
-  __shared__ float part[8][33];
-  const int col = blockIdx.x * 32 + (threadIdx.x & 31), wp = threadIdx.x >> 5;
+  __shared__ float part[256];
+  const int col = blockIdx.x;
   float acc = 0.f;
-  if (col <= K)
-    for (std::uint64_t k = wp; k < n; k += 8)
-      acc = __fadd_rn(acc, col < K ? __fmul_rn(dz[k], H[k * K + col]) : dz[k]);
-  part[wp][threadIdx.x & 31] = acc;
+  for (std::uint64_t k = threadIdx.x; k < n; k += blockDim.x)
+    acc = __fadd_rn(acc, col < K ? __fmul_rn(dz[k], H[k * K + col]) : dz[k]);
+  part[threadIdx.x] = acc;
   __syncthreads();
-  if (wp == 0 && col <= K) {
-    float s = 0.f;
-    for (int q = 0; q < 8; ++q) s = __fadd_rn(s, part[q][threadIdx.x & 31]);
-    g[col] = n ? __fdiv_rn(s, float(n)) : 0.f;
+  for (int w = 128; w > 0; w >>= 1) {
+    if (int(threadIdx.x) < w) part[threadIdx.x] = __fadd_rn(part[threadIdx.x], part[threadIdx.x + w]);
+    __syncthreads();
   }
+  if (threadIdx.x == 0) g[col] = n ? __fdiv_rn(part[0], float(n)) : 0.f;
 }
 
 // Split-K reduce of [dW | db] partials P[z][o][i] (i <= in, column `in` is the

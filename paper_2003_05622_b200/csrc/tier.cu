@@ -1138,12 +1138,11 @@ static void launch_gemm(Tier* t, cudaStream_t s, GemmArgs g, int splits = 1) {
   g.split3 = t->gemm_split3 ? 1 : 0;
   auto smem = [&](int bn) { return gemm_smem(bn, g.split3 != 0); };
   const unsigned gm = unsigned((g.M + kGemmBM - 1) / kGemmBM);
-  if (g.N > 128) {
-    launch_on(t, s, umma_gemm_kernel<256>, dim3(gm, unsigned((g.N + 255) / 256), unsigned(splits)),
-              kGemmThreads, smem(256), g);
-  } else if (g.N > 64) {
-    launch_on(t, s, umma_gemm_kernel<128>, dim3(gm, 1, unsigned(splits)), kGemmThreads, smem(128),
-              g);
+  // N > 64 in 128-wide tiles (256 would halve the CTAs and, with the 3xTF32
+  // split, fit only two pipeline stages: measured 78 us vs ~30 us per c4 GEMM)
+  if (g.N > 64) {
+    launch_on(t, s, umma_gemm_kernel<128>, dim3(gm, unsigned((g.N + 127) / 128), unsigned(splits)),
+              kGemmThreads, smem(128), g);
   } else if (g.N > 32) {
     launch_on(t, s, umma_gemm_kernel<64>, dim3(gm, 1, unsigned(splits)), kGemmThreads, smem(64), g);
   } else {
@@ -1199,7 +1198,7 @@ static hps_status enqueue_wide(Tier* t, const ShardMap& sm, std::uint64_t n,
   HPS_CUDA(cudaStreamWaitEvent(t->st2, t->fork, 0));
   {
     const int K = md.ins[L - 1];
-    launch_on(t, t->st2, wide_head_grad_kernel, unsigned((K + 1 + 31) / 32), 256, 0, n, K,
+    launch_on(t, t->st2, wide_head_grad_kernel, unsigned(K + 1), 256, 0, n, K,
               (const float*)t->wdz, (const float*)t->wH[L - 2], t->dgrad + md.offs[L - 1]);
   }
   for (int l = L - 2; l >= 0; --l) {  // [dW_l | db_l] = dZ_l^T [H_{l-1} | 1] / n
@@ -1209,7 +1208,7 @@ static hps_status enqueue_wide(Tier* t, const ShardMap& sm, std::uint64_t n,
     g.A = t->wdZ[l], g.a_m = 1, g.a_k = out;
     g.B = l > 0 ? t->wH[l - 1] : t->wX, g.b_n = 1, g.b_k = in, g.b_ones_col = 1;
     g.epi = kEpiStore, g.D = t->wP, g.ldd = in + 1;
-    const int bn = g.N > 128 ? 256 : (g.N > 64 ? 128 : (g.N > 32 ? 64 : 32));
+    const int bn = g.N > 64 ? 128 : (g.N > 32 ? 64 : 32);
     const int tiles = ((out + kGemmBM - 1) / kGemmBM) * ((g.N + bn - 1) / bn);
     int splits = std::max(1, kSMs / tiles);
     splits = int(std::min<std::uint64_t>(std::uint64_t(splits), (n + kGemmBK - 1) / kGemmBK));
@@ -2666,8 +2665,6 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
                          int(mid_smem(2)));
     cudaFuncSetAttribute(sparse_mid_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(mid_smem(4)));
-    cudaFuncSetAttribute(umma_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(gemm_smem(256, true)));
     cudaFuncSetAttribute(umma_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(gemm_smem(128, true)));
     cudaFuncSetAttribute(umma_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3369,12 +3366,11 @@ hps_status hps_debug_gemm_tf32(int M, int N, int K, const float* A, int64_t a_m,
   g.A = A, g.a_m = a_m, g.a_k = a_k;
   g.B = B, g.b_n = b_n, g.b_k = b_k, g.b_ones_col = b_ones_col;
   g.epi = epi, g.D = D, g.Dd = Dd, g.ldd = ldd, g.bias = bias, g.mask = mask, g.ldm = ldm;
-  for (int bn : {32, 64, 128, 256}) {
+  for (int bn : {32, 64, 128}) {
     const int smem = int(gemm_smem(bn, true));
     if (bn == 32) cudaFuncSetAttribute(umma_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (bn == 64) cudaFuncSetAttribute(umma_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (bn == 128) cudaFuncSetAttribute(umma_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (bn == 256) cudaFuncSetAttribute(umma_gemm_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   launch_gemm(&scratch, nullptr, g, splits);
   HPS_CUDA(cudaGetLastError());
