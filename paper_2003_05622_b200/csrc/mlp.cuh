@@ -239,10 +239,11 @@ __device__ __forceinline__ void split_stage(char* base, std::size_t bytes, std::
 }
 
 // Stages in the shared-memory ring of umma_gemm_kernel<BN>: as many as fit in
-// ~200 KB, 2..4. A stage is the A and B tiles (twice that with the split).
+// ~200 KB, 3..4 (BN <= 128). A stage is the A and B tiles (twice that with the
+// split).
 __host__ __device__ constexpr int gemm_stages(int bn, bool split) {
-  return (200 * 1024) / int(std::size_t(kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1)) < 2
-             ? 2
+  return (200 * 1024) / int(std::size_t(kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1)) < 3
+             ? 3
              : ((200 * 1024) / int(std::size_t(kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1)) > 4
                     ? 4
                     : (200 * 1024) / int(std::size_t(kGemmBM + bn) * kGemmBK * 4 * (split ? 2 : 1)));
@@ -306,19 +307,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) 
   };
   for (int i = 0; i < S - 1; ++i) issue(i);
   for (int it = 0; it < nk; ++it) {
-    // the buffer of k-stage it + S - 1 was last read by the MMAs of it - 1
-    if (it >= 1) mbar_wait_parity(&bar[(it - 1) % S], std::uint32_t(((it - 1) / S) & 1));
-    issue(it + S - 1);
-    // this thread's copies of stage it landed (S - 1 younger groups may pend)
-    if (S == 4) asm volatile("cp.async.wait_group 3;\n" ::: "memory");
-    else if (S == 3) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
+    // this thread's copies of stage it landed (stages it+1 .. it+S-2 may pend)
+    if (S == 4) asm volatile("cp.async.wait_group 2;\n" ::: "memory");
     else asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     __syncthreads();
     std::uint8_t* sp = stage_ptr(it);
-    if (split) {
-      split_stage(reinterpret_cast<char*>(sp), kA + kB, lo_off);
-      __syncthreads();
-    }
+    if (split) split_stage(reinterpret_cast<char*>(sp), kA + kB, lo_off);
     fence_async_smem();  // generic-proxy smem writes -> the tensor core's async proxy
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -340,12 +334,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) 
       }
       umma_commit(&bar[it % S]);
     }
+    // while stage it's MMAs run: refill the buffer stage it-1 used, once its
+    // MMAs committed, with stage it + S - 1 (then convert stage it + 1)
+    if (it >= 1) mbar_wait_parity(&bar[(it - 1) % S], std::uint32_t(((it - 1) / S) & 1));
+    issue(it + S - 1);
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   if (nk > 0) mbar_wait_parity(&bar[(nk - 1) % S], std::uint32_t(((nk - 1) / S) & 1));
   tc_fence_after();
-  // epilogue: thread owns output row m0 + 32*warp + lane
-  const int m = m0 + warp * 32 + lane;
+  // epilogue: TMEM lane = output row; a thread loads its row's 16 columns at a
+  // time, the warp transposes them through shared memory (the drained stage
+  // ring) and stores / reads row segments: 16 lanes cover one row's 64 bytes
+  // (a thread-per-row store would touch 32 rows per instruction)
+  float* tile = reinterpret_cast<float*>(gsm) + warp * (32 * 17);
   for (int c = 0; c < BN; c += 16) {
     float v[16];
     if (nk > 0) {
@@ -354,12 +355,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) 
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.f;
     }
-    if (m >= g.M) continue;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int n = n0 + c + i;
-      if (n >= g.N) break;
-      float x = v[i];
+    for (int i = 0; i < 16; ++i) tile[lane * 17 + i] = v[i];
+    __syncwarp();
+    const int col = lane & 15, n = n0 + c + col;
+#pragma unroll 4
+    for (int q = 0; q < 16; ++q) {
+      const int r = 2 * q + (lane >> 4);
+      const int m = m0 + warp * 32 + r;
+      if (m >= g.M || n >= g.N) continue;
+      float x = tile[r * 17 + col];
       switch (g.epi) {
         case kEpiBiasRelu:
           x = __fadd_rn(x, g.bias[n]);
@@ -375,6 +380,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) umma_gemm_kernel(GemmArgs g) 
           g.D[std::int64_t(blockIdx.z) * g.M * g.ldd + std::int64_t(m) * g.ldd + n] = x;
       }
     }
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();

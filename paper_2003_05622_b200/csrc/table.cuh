@@ -338,6 +338,53 @@ __global__ void store_gather_kernel(const std::uint64_t* __restrict__ need_key,
   }
 }
 
+// DMA staging (Tier::dma): staged row i -> its table slot, and the reverse
+// compaction of evicted rows for the D2H copy. *n_ptr rows, RW floats each.
+template <int VEC>
+__global__ void staged_rows_to_slots_kernel(const float* __restrict__ staged,
+                                            const std::uint32_t* __restrict__ slots,
+                                            const unsigned long long* __restrict__ n_ptr,
+                                            float* __restrict__ vals, int RW) {
+  pdl_wait();
+  const int tpk = RW / VEC;
+  const std::uint64_t total = std::uint64_t(*n_ptr) * tpk;
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    const float* src = staged + i * RW + part * VEC;
+    float* dst = vals + std::uint64_t(slots[i]) * RW + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, ld_f4(src));
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) dst[q] = src[q];
+    }
+  }
+}
+template <int VEC>
+__global__ void slots_to_staged_rows_kernel(const std::uint32_t* __restrict__ slots,
+                                            const unsigned long long* __restrict__ n_ptr,
+                                            const float* __restrict__ vals,
+                                            float* __restrict__ staged, int RW) {
+  pdl_wait();
+  const int tpk = RW / VEC;
+  const std::uint64_t total = std::uint64_t(*n_ptr) * tpk;
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = t / tpk;
+    const int part = int(t - i * tpk);
+    const float* src = vals + std::uint64_t(slots[i]) * RW + part * VEC;
+    float* dst = staged + i * RW + part * VEC;
+    if (VEC == 4) {
+      st_f4(dst, ld_f4(src));
+    } else {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) dst[q] = src[q];
+    }
+  }
+}
+
 // Pipelined build, body half: the rows from the resident tables (the
 // previous table's carry-over, or a proxy's), once those batches are done.
 template <int VEC>

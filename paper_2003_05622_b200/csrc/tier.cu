@@ -27,6 +27,7 @@
 #include <deque>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -408,6 +409,31 @@ struct Tier {
   std::uint32_t* wb_slot[kTables] = {};
   bool store_registered = false;
   float* store_host = nullptr;
+  // MEM-PS staging through host threads + DMA (HPS_STAGE=dma, or auto for a
+  // host store over 16 GB: c3, c5): the store rows a build needs are gathered
+  // by host threads into pinned staging and copied with one cudaMemcpyAsync;
+  // the evicted rows are compacted on the device, copied back with one
+  // cudaMemcpyAsync and scattered into the store by host threads. Zero-copy
+  // SM gathers of random 64-byte host rows reach ~11 GB/s on c5; 16 host
+  // threads gather at 22-30 GB/s and the DMA runs at ~55 GB/s (round 1,
+  // tools/pcie_probe.cu).
+  int stage_mode = -1;  // HPS_STAGE: 1 dma, 0 zero-copy, -1 auto
+  bool dma = false;
+  float* store_hptr = nullptr;           // the host store (pinned or pageable)
+  struct DmaJob {
+    const std::uint64_t* cnt;            // pinned: rows in this transfer
+    const std::uint64_t* keys;           // pinned: their keys
+    float* rows;                         // pinned staging rows
+    float* store;
+    int RW;
+    int threads;
+    bool scatter;                        // false: store -> rows, true: rows -> store
+  };
+  DmaJob gjob{}, wjob{};
+  std::uint64_t *g_hcnt = nullptr, *g_hkeys = nullptr, *w_hcnt = nullptr, *w_hkeys = nullptr;
+  float *g_hrows = nullptr, *w_hrows = nullptr;  // pinned staging
+  float *g_drows = nullptr, *w_drows = nullptr;  // device staging
+  std::vector<void*> pinned;
 
   std::vector<PendingChunk> pending;
   std::uint64_t* pend_keys = nullptr;  // the pending arena (hps_push -> hps_drain)
@@ -1597,6 +1623,55 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   return HPS_OK;
 }
 
+// Host side of a DMA transfer (cudaLaunchHostFunc, in stream order): copy
+// *cnt rows between the host store and the pinned staging, split over host
+// threads (the rows are random 64-512-byte records: host threads gather at
+// memory speed, the PCIe link then sees one contiguous DMA).
+static void CUDART_CB dma_host_rows(void* p) {
+  const Tier::DmaJob& j = *static_cast<const Tier::DmaJob*>(p);
+  const std::uint64_t n = *j.cnt;
+  const std::size_t rb = std::size_t(j.RW) * 4;
+  auto work = [&](std::uint64_t a, std::uint64_t b) {
+    for (std::uint64_t i = a; i < b; ++i) {
+      float* st = j.store + j.keys[i] * std::uint64_t(j.RW);
+      float* sg = j.rows + i * std::uint64_t(j.RW);
+      if (j.scatter) std::memcpy(st, sg, rb);
+      else std::memcpy(sg, st, rb);
+    }
+  };
+  const int T = (n < 4096 || j.threads < 2) ? 1 : j.threads;
+  if (T == 1) {
+    work(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const std::uint64_t per = (n + T - 1) / T;
+  for (int t = 1; t < T; ++t)
+    th.emplace_back(work, std::min(n, per * t), std::min(n, per * (t + 1)));
+  work(0, std::min(n, per));
+  for (auto& x : th) x.join();
+}
+
+// DMA staging of the store rows of table tb (host store, Tier::dma): the
+// prep's list (keys, slots, count) to pinned memory, host threads gather the
+// rows, one H2D copy, then the rows into their slots. Sizes are the shape's
+// bound (known when enqueued); the count is read on both sides at run time.
+static hps_status enqueue_store_gather_dma(Tier* T, const BatchShape& sh, int tb) {
+  const std::uint64_t RW = std::uint64_t(T->RW);
+  const std::uint64_t bound = std::min(sh.own_bound, T->Wmax);
+  cudaStream_t s = T->st_pf;
+  HPS_CUDA(cudaMemcpyAsync(T->g_hcnt, &T->dsc->stored_tab[tb], 8, cudaMemcpyDeviceToHost, s));
+  HPS_CUDA(cudaMemcpyAsync(T->g_hkeys, T->need_key[tb], bound * 8, cudaMemcpyDeviceToHost, s));
+  HPS_CUDA(cudaLaunchHostFunc(s, dma_host_rows, &T->gjob));
+  HPS_CUDA(cudaMemcpyAsync(T->g_drows, T->g_hrows, bound * RW * 4, cudaMemcpyHostToDevice, s));
+  const int V = vec_of(T->RW);
+  auto k = V == 4 ? staged_rows_to_slots_kernel<4> : staged_rows_to_slots_kernel<1>;
+  launch_on(T, s, k, grid_for(bound * (RW / V)), 256, 0, (const float*)T->g_drows,
+            (const std::uint32_t*)T->need_slot[tb],
+            (const unsigned long long*)&T->dsc->stored_tab[tb], T->tvals[tb], T->RW);
+  return HPS_OK;
+}
+
 // The store rows of table tb (host memory over PCIe, or HBM): a streaming
 // gather on st_pf, after the prep's store list; the batch's body waits for it.
 static hps_status enqueue_store_gather(Tier* T, const BatchShape& sh, int tb) {
@@ -1606,6 +1681,11 @@ static hps_status enqueue_store_gather(Tier* T, const BatchShape& sh, int tb) {
   // proxy of this batch) arrive with its eviction write-back
   const int te = T->hist[3];
   if (te >= 0 && T->wb_pending[te]) HPS_CUDA(cudaStreamWaitEvent(T->st_pf, T->ev_wb[te], 0));
+  if (T->dma) {
+    HPS_TRY(enqueue_store_gather_dma(T, sh, tb));
+    HPS_CUDA(cudaEventRecord(T->pf_join, T->st_pf));
+    return HPS_OK;
+  }
   const std::uint64_t work = sh.own_bound * std::uint64_t(E / V);
   const unsigned gg = T->store_on_host ? T->pf_ctas : grid_for(work, 256 * 4);
   const int tpb = T->store_on_host ? T->zc_threads : 256;
@@ -1899,6 +1979,23 @@ static hps_status enqueue_writeback(Tier* T, int t, const int* newer, int n_newe
             (const std::uint64_t*)&T->dsc->nws_tab[t], nk[0], nc[0], nk[1], nc[1], nk[2], nc[2],
             T->store_keys, T->wb_key[t], T->wb_slot[t], &T->dsc->wb_n[t], &T->dsc->wb_total);
   const std::uint64_t work = T->Wmax * std::uint64_t(E / V);
+  if (T->dma) {  // rows compacted on the device, one D2H copy, host threads scatter
+    auto kc = V == 4 ? slots_to_staged_rows_kernel<4> : slots_to_staged_rows_kernel<1>;
+    launch_on(T, T->st_wb, kc, grid_for(work), 256, 0, (const std::uint32_t*)T->wb_slot[t],
+              (const unsigned long long*)&T->dsc->wb_n[t], (const float*)T->tvals[t], T->w_drows,
+              E);
+    HPS_CUDA(cudaMemcpyAsync(T->w_hcnt, &T->dsc->wb_n[t], 8, cudaMemcpyDeviceToHost, T->st_wb));
+    HPS_CUDA(cudaMemcpyAsync(T->w_hkeys, T->wb_key[t], T->Wmax * 8, cudaMemcpyDeviceToHost,
+                             T->st_wb));
+    HPS_CUDA(cudaMemcpyAsync(T->w_hrows, T->w_drows, T->Wmax * std::uint64_t(E) * 4,
+                             cudaMemcpyDeviceToHost, T->st_wb));
+    HPS_CUDA(cudaLaunchHostFunc(T->st_wb, dma_host_rows, &T->wjob));
+    if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[t][1], T->st_wb));
+    HPS_CUDA(cudaEventRecord(T->ev_wb[t], T->st_wb));
+    T->wb_pending[t] = true;
+    T->wb_timed[t] = T->timing;
+    return HPS_OK;
+  }
   // posted PCIe writes: a few CTAs saturate the link without holding SMs
   const unsigned gw = T->store_on_host ? T->wb_ctas : grid_for(work, 256 * 4);
   const int tpb = T->store_on_host ? T->zc_threads : 256;
@@ -2528,6 +2625,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     t->mid_max = std::uint32_t(std::min(kMidMaxSeg, std::max(kLongSeg, std::atoi(v))));
   if (const char* v = std::getenv("HPS_FOLD_WAIT")) t->fold_wait = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_XFUSE")) t->xfuse = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_STAGE"))
+    t->stage_mode = std::strcmp(v, "dma") == 0 ? 1 : (std::strcmp(v, "zc") == 0 ? 0 : -1);
   if (const char* v = std::getenv("HPS_WS_SORT")) t->ws_sort = std::atoi(v) != 0 ? 1 : 0;
   if (const char* v = std::getenv("HPS_ZC_THREADS")) t->zc_threads = std::max(32, std::atoi(v));
   t->nmb_max = t->Bmax;  // a shard never exceeds the batch
@@ -2866,6 +2965,7 @@ hps_status hps_destroy(hps_tier_t t) {
   if (t->hsc) cudaFreeHost(t->hsc);
   if (t->hout) cudaFreeHost(t->hout);
   if (t->store_registered) cudaHostUnregister(t->store_host);
+  for (void* p : t->pinned) cudaFreeHost(p);
   for (auto& ev : t->evpool) cudaEventDestroy(ev);
   if (t->fork) cudaEventDestroy(t->fork);
   if (t->join) cudaEventDestroy(t->join);
@@ -3303,6 +3403,8 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
   }
   t->store = nullptr;
   t->store_keys = 0;
+  t->store_hptr = nullptr;
+  t->dma = false;
   if (!rows || !num_keys) return HPS_OK;
   if (on_device) {
     t->store = rows;
@@ -3321,6 +3423,36 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
     HPS_CUDA(cudaHostGetDevicePointer(&dp, rows, 0));
     t->store = static_cast<float*>(dp);
     t->store_on_host = true;
+    t->store_hptr = rows;
+    const std::uint64_t bytes = num_keys * std::uint64_t(t->RW) * 4;
+    t->dma = t->stage_mode == 1 || (t->stage_mode < 0 && bytes > (std::uint64_t(16) << 30));
+    if (t->dma && !t->g_hrows) {  // pinned + device staging, once
+      const std::uint64_t W = t->Wmax, RWb = std::uint64_t(t->RW) * 4;
+      auto pin = [&](void** p, std::uint64_t b) {
+        const cudaError_t e = cudaMallocHost(p, b);
+        if (e == cudaSuccess) t->pinned.push_back(*p);
+        return e;
+      };
+      void *a = nullptr, *b = nullptr, *c = nullptr, *d = nullptr, *e2 = nullptr, *f = nullptr;
+      HPS_CUDA(pin(&a, 8));
+      HPS_CUDA(pin(&b, W * 8));
+      HPS_CUDA(pin(&c, W * RWb));
+      HPS_CUDA(pin(&d, 8));
+      HPS_CUDA(pin(&e2, W * 8));
+      HPS_CUDA(pin(&f, W * RWb));
+      t->g_hcnt = static_cast<std::uint64_t*>(a);
+      t->g_hkeys = static_cast<std::uint64_t*>(b);
+      t->g_hrows = static_cast<float*>(c);
+      t->w_hcnt = static_cast<std::uint64_t*>(d);
+      t->w_hkeys = static_cast<std::uint64_t*>(e2);
+      t->w_hrows = static_cast<float*>(f);
+      HPS_TRY(dalloc(t, &t->g_drows, W * std::uint64_t(t->RW)));
+      HPS_TRY(dalloc(t, &t->w_drows, W * std::uint64_t(t->RW)));
+    }
+    const int threads =
+        std::max(1, std::min(32, int(std::thread::hardware_concurrency()) / 2));
+    t->gjob = Tier::DmaJob{t->g_hcnt, t->g_hkeys, t->g_hrows, rows, t->RW, threads, false};
+    t->wjob = Tier::DmaJob{t->w_hcnt, t->w_hkeys, t->w_hrows, rows, t->RW, threads, true};
   }
   t->store_keys = num_keys;
   return HPS_OK;

@@ -230,3 +230,35 @@ def test_in_flight_error_is_reported_by_its_own_batch(pkg):
     tier.wait_batch()
     tier.wait_batch()  # the earlier batches are unaffected
     tier.close()
+
+
+@pytest.mark.parametrize("optimizer", ["sgd", "adagrad"])
+def test_dma_staging_bit_exact(pkg, oracle, monkeypatch, optimizer):
+    """HPS_STAGE=dma (the default for host stores over 16 GB: c3, c5): store
+    rows gathered by host threads into pinned staging + one H2D copy per
+    build, evicted rows compacted on the device + one D2H copy + host-thread
+    scatter (mem_ps.hpp:114-159 prepare, 210-245 collect). Pipelined, 4 batches
+    in flight, so builds read rows other batches' write-backs just returned."""
+    monkeypatch.setenv("HPS_STAGE", "dma")
+    dims, B, nnz, nb, E = 30000, 512, 20, 10, 8
+    off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=44)
+    tier = pkg.Tier(width=E, minibatches=4, key_space=dims, max_batch_examples=B,
+                    max_batch_keys=max_keys_of(off, B), optimizer=optimizer)
+    store = np.zeros((dims, tier.row_width), np.float32)
+    tier.attach_store(store)
+    stats = []
+    for i, (o, k, l) in enumerate(batches_of(off, keys, lab, B)):
+        tier.submit_batch(o, k, l)
+        if i >= 3:
+            stats.append(tier.wait_batch())
+    while len(stats) < nb:
+        stats.append(tier.wait_batch())
+    tier.flush()
+    dense = tier.get_dense()
+    rd, wr_rows = tier.store_traffic()
+    tier.close()
+    assert rd > 0 and wr_rows > 0
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, (8, 16, 1), J=4, optimizer=optimizer),
+                                        B, off, keys, lab)
+    assert np.array_equal(dense, wd)
+    assert np.array_equal(store[wk.astype(np.int64)], wr)
