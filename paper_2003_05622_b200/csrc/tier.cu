@@ -143,6 +143,7 @@ struct Scalars {
   unsigned long long n_mid;      // this mini-batch's medium segments
   unsigned long long Ux[2];      // fused exchange: unique keys of mini-batch j, by j & 1
   unsigned long long xclear[2];  // (scratch for owner_rank_kernel's clear words)
+  unsigned long long xscratch[4];  // (scratch: the prep's owner-rank pass opens no round)
   DevError err;                 // the body's and the parity API's error word
   // per-batch error words of the pipelined stages: the stage's
   // key-range check (by staging slot) and the prep's build (by table), so an
@@ -342,6 +343,12 @@ struct Tier {
   std::uint64_t* xukeys[2] = {};
   std::uint32_t* xorank[2] = {};
   std::uint64_t* xotot[2] = {};
+  // ... computed by the prep's grouping instead (per table, mini-batch j at
+  // its grouping region; HPS_XPREP=0: in the body, x_keys)
+  bool xprep = true;
+  std::uint64_t* pxukeys[kTables] = {};
+  std::uint32_t* pxorank[kTables] = {};
+  std::uint64_t* pxotot[kTables] = {};   // [64][kMaxRanks]
   float *rows = nullptr, *deltas = nullptr, *hstage = nullptr, *staged = nullptr;
   std::uint64_t staged_cap = 0;  // floats
 
@@ -409,8 +416,8 @@ struct Tier {
   std::uint32_t* wb_slot[kTables] = {};
   bool store_registered = false;
   float* store_host = nullptr;
-  // MEM-PS staging through host threads + DMA (HPS_STAGE=dma, or auto for a
-  // host store over 16 GB: c3, c5): the store rows a build needs are gathered
+  // MEM-PS staging through host threads + DMA (HPS_STAGE=dma; zero-copy SM
+  // gathers are the default, measured faster here): the store rows a build needs are gathered
   // by host threads into pinned staging and copied with one cudaMemcpyAsync;
   // the evicted rows are compacted on the device, copied back with one
   // cudaMemcpyAsync and scattered into the store by host threads. Zero-copy
@@ -1500,6 +1507,20 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
            (const unsigned long long*)&g.gn[1], (const std::uint32_t*)g.g_dup,
            (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
            (const std::uint32_t*)T->g_exof[tb], exs);
+    if (G > 1 && T->xfuse && T->xprep) {
+      // the fused exchange's keys of this mini-batch, off the body's path:
+      // unique keys in uid order and their owner ranks (no round opened here)
+      std::uint64_t* xk = T->pxukeys[tb] + r0;
+      launch(T, uid_keys_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)uids,
+             (const std::uint64_t*)T->rq_keys[tb], (const unsigned long long*)U, xk,
+             &T->dsc->xscratch[0]);
+      const std::uint32_t nb =
+          std::max<std::uint32_t>(1, std::uint32_t((ob + kRankTile - 1) / kRankTile));
+      launch(T, owner_rank_kernel, nb, kRankThreads, 0, (const std::uint64_t*)xk,
+             (const std::uint64_t*)U, T->G, next_lookback(T, nb), T->pxorank[tb] + r0,
+             T->pxotot[tb] + std::uint64_t(j) * kMaxRanks, &T->dsc->xscratch[1],
+             &T->dsc->xscratch[2]);
+    }
     if (mb_done) HPS_CUDA(cudaEventRecord(mb_done[j], l.st));
   }
   return HPS_OK;
@@ -1720,21 +1741,43 @@ static void x_keys(Tier* T, const BatchShape& sh, const BatchPlan& bp, int j) {
 // in one signalled phase X; then this rank, as owner, applies every sender's
 // deltas in canonical order, updates the dense weights, and serves jk's rows
 // (phase Y), waiting for its own.
-static hps_status x_round(Tier* T, int jd, bool dense, int jk) {
+// Where mini-batch j's exchange keys live: the prep's pools (xprep) or the
+// body's j & 1 buffers (x_keys).
+struct XKeys {
+  const std::uint64_t* keys = nullptr;
+  const std::uint64_t* count = nullptr;
+  const std::uint32_t* orank = nullptr;
+  const std::uint64_t* otot = nullptr;
+};
+static XKeys x_src(const Tier* T, const BatchShape& sh, const BatchPlan& bp, int j) {
+  XKeys x;
+  if (j < 0) return x;
+  if (T->xprep) {
+    const std::uint64_t r0 = group_region(sh, j);
+    x.keys = T->pxukeys[bp.tb] + r0;
+    x.count = reinterpret_cast<const std::uint64_t*>(&T->dsc->Ug[bp.tb][j]);
+    x.orank = T->pxorank[bp.tb] + r0;
+    x.otot = T->pxotot[bp.tb] + std::uint64_t(j) * kMaxRanks;
+  } else {
+    const int q = j & 1;
+    x.keys = T->xukeys[q];
+    x.count = reinterpret_cast<const std::uint64_t*>(&T->dsc->Ux[q]);
+    x.orank = T->xorank[q];
+    x.otot = T->xotot[q];
+  }
+  return x;
+}
+
+static hps_status x_round(Tier* T, const BatchShape& sh, const BatchPlan& bp, int jd, bool dense,
+                          int jk) {
   const int V = vec_of(T->E), G = T->G;
-  const int qd = jd & 1, qk = jk & 1;
+  const XKeys xd = x_src(T, sh, bp, jd), xk = x_src(T, sh, bp, jk);
   auto sx = V == 4 ? p2p_send_x_kernel<4> : p2p_send_x_kernel<1>;
   launch(T, sx, grid_for(T->Omax * std::uint64_t(T->E / V), 256, kSMs * 4), 256, 0, T->ctx, G,
-         T->g, T->slot, T->E, (const std::uint64_t*)(jd >= 0 ? T->xukeys[qd] : nullptr),
-         (const std::uint64_t*)(jd >= 0 ? &T->dsc->Ux[qd] : nullptr),
-         (const std::uint32_t*)(jd >= 0 ? T->xorank[qd] : nullptr),
-         (const std::uint64_t*)(jd >= 0 ? T->xotot[qd] : nullptr),
+         T->g, T->slot, T->E, xd.keys, xd.count, xd.orank, xd.otot,
          (const float*)(jd >= 0 ? T->deltas : nullptr), std::uint64_t(T->md.nw),
-         (const float*)(dense ? T->dgrad : nullptr),
-         (const std::uint64_t*)(jk >= 0 ? T->xukeys[qk] : nullptr),
-         (const std::uint64_t*)(jk >= 0 ? &T->dsc->Ux[qk] : nullptr),
-         (const std::uint32_t*)(jk >= 0 ? T->xorank[qk] : nullptr),
-         (const std::uint64_t*)(jk >= 0 ? T->xotot[qk] : nullptr), T->done_ctr);
+         (const float*)(dense ? T->dgrad : nullptr), xk.keys, xk.count, xk.orank, xk.otot,
+         T->done_ctr);
   bool waited = false;
   if (jd >= 0) {  // owner apply, senders in canonical order; the first waits for X
     auto k = V == 4 ? p2p_apply_kernel<4> : p2p_apply_kernel<1>;
@@ -1816,9 +1859,10 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
   // G > 1 fused exchange: the first round carries only mini-batch 0's keys
   const bool xf = G > 1 && bp.grouped && T->xfuse;
   if (xf) {
-    x_keys(T, sh, bp, 0);
+    if (T->xprep) begin_round(T, true);
+    else x_keys(T, sh, bp, 0);
     mark(T, HPS_T_DEDUP);
-    HPS_TRY(x_round(T, -1, false, 0));
+    HPS_TRY(x_round(T, sh, bp, -1, false, 0));
   }
   // ---- mini-batches
   const int V = vec_of(E);
@@ -1854,7 +1898,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
         rows = T->tvals[T->cur];
         rstride = T->RW;
       } else if (xf) {  // rows of this mini-batch arrived in the previous round (uid order)
-        Uj = reinterpret_cast<const std::uint64_t*>(&T->dsc->Ux[j & 1]);
+        Uj = x_src(T, sh, bp, j).count;
         occ_row = T->g_inv[bp.tb];
       } else {  // unique keys in uid order -> the NVLink exchange -> rows by uid
         // (the kernel also copies the count into dsc->U: no memcpy node,
@@ -1925,10 +1969,12 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
     mark(T, HPS_T_GRADS);
     if (xf) {  // one fused round: deltas + dense replica of j, keys of j + 1
       const bool next = j + 1 < J;
-      if (next) x_keys(T, sh, bp, j + 1);
+      if (next && side && j + 1 >= bp.prep_mbs)  // its grouping (and keys) on the side branch
+        HPS_CUDA(cudaStreamWaitEvent(T->st, T->gmb_done[j + 1], 0));
+      if (next && !T->xprep) x_keys(T, sh, bp, j + 1);
       else begin_round(T, true);
       mark(T, HPS_T_DEDUP);
-      HPS_TRY(x_round(T, j, j != bp.skip_mb, next ? j + 1 : -1));
+      HPS_TRY(x_round(T, sh, bp, j, j != bp.skip_mb, next ? j + 1 : -1));
       continue;
     }
     // push + canonical apply (a10, a11); grouped at one rank the sparse
@@ -2625,6 +2671,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     t->mid_max = std::uint32_t(std::min(kMidMaxSeg, std::max(kLongSeg, std::atoi(v))));
   if (const char* v = std::getenv("HPS_FOLD_WAIT")) t->fold_wait = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_XFUSE")) t->xfuse = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_XPREP")) t->xprep = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_STAGE"))
     t->stage_mode = std::strcmp(v, "dma") == 0 ? 1 : (std::strcmp(v, "zc") == 0 ? 0 : -1);
   if (const char* v = std::getenv("HPS_WS_SORT")) t->ws_sort = std::atoi(v) != 0 ? 1 : 0;
@@ -2851,6 +2898,11 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     A(g_segb[i], t->g_pool + 64);
     A(g_exsb[i], t->g_pool);
     A(g_uidb[i], t->g_pool);
+    if (G > 1) {
+      A(pxukeys[i], t->g_pool);
+      A(pxorank[i], t->g_pool);
+      A(pxotot[i], std::uint64_t(64) * kMaxRanks);
+    }
   }
   for (int i = 0; i < kTables; ++i) {
     A(g_tick[i], S);
@@ -3425,7 +3477,11 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
     t->store_on_host = true;
     t->store_hptr = rows;
     const std::uint64_t bytes = num_keys * std::uint64_t(t->RW) * 4;
-    t->dma = t->stage_mode == 1 || (t->stage_mode < 0 && bytes > (std::uint64_t(16) << 30));
+    // measured (profiles/r2_bench_c5*.json, c3): bound-sized DMA + host-thread
+    // copies lost to zero-copy on this box (c5 e2e 1.52M vs 1.60M ex/s, c3
+    // 0.29M vs 0.55M), so zero-copy stays the default; HPS_STAGE=dma selects it
+    (void)bytes;
+    t->dma = t->stage_mode == 1;
     if (t->dma && !t->g_hrows) {  // pinned + device staging, once
       const std::uint64_t W = t->Wmax, RWb = std::uint64_t(t->RW) * 4;
       auto pin = [&](void** p, std::uint64_t b) {

@@ -186,6 +186,11 @@ def main():
     results["train_xfuse0"] = case_train(world, rank, oracle, 16, (8, 16, 1), 4, True, 50000,
                                          1024, 5, 30, pipelined=True)
     del os.environ["HPS_XFUSE"]
+    # the fused round with its keys computed in the body (HPS_XPREP=0)
+    os.environ["HPS_XPREP"] = "0"
+    results["train_xprep0"] = case_train(world, rank, oracle, 8, (8, 16, 1), 4, True, 30000,
+                                         1024, 5, 24, pipelined=True, hbm_store=True)
+    del os.environ["HPS_XPREP"]
     flags = torch.tensor([int(v) for v in results.values()], device="cuda")
     dist.all_reduce(flags, op=dist.ReduceOp.MIN)
     if rank == 0:

@@ -234,7 +234,7 @@ def test_in_flight_error_is_reported_by_its_own_batch(pkg):
 
 @pytest.mark.parametrize("optimizer", ["sgd", "adagrad"])
 def test_dma_staging_bit_exact(pkg, oracle, monkeypatch, optimizer):
-    """HPS_STAGE=dma (the default for host stores over 16 GB: c3, c5): store
+    """HPS_STAGE=dma (the north_star staging: host threads + cudaMemcpyAsync): store
     rows gathered by host threads into pinned staging + one H2D copy per
     build, evicted rows compacted on the device + one D2H copy + host-thread
     scatter (mem_ps.hpp:114-159 prepare, 210-245 collect). Pipelined, 4 batches
