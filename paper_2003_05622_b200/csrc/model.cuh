@@ -185,6 +185,46 @@ __global__ void __launch_bounds__(128)
           summed = embed_sum_exact<LPE>(occ_row, rows, rstride, o0, o1, sub, gmask,
                                         md.exact_slack, hrec);
       }
+      // two dims per lane (8-byte row loads, two chains) when the row is a
+      // multiple of 2 x LPE wide and 8-byte aligned (c3: E = 64 on 32 lanes):
+      // one walk over the features instead of two
+      if (!summed && LPE == 32 && E % (2 * LPE) == 0 && rstride % 2 == 0) {
+        for (int d0 = 0; d0 < E; d0 += 2 * LPE) {
+          const int d = d0 + 2 * sub;
+          double acc0 = 0.0, acc1 = 0.0;
+          constexpr int kIdRounds = 8;
+          for (std::uint32_t base = o0; base < o1; base += kIdRounds * LPE) {
+            std::uint32_t ids[kIdRounds];
+#pragma unroll
+            for (int t = 0; t < kIdRounds; ++t) {
+              const std::uint32_t p = base + t * LPE + sub;
+              ids[t] = p < o1 ? occ_row[p] : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t < kIdRounds; ++t) {
+              const std::uint32_t c = base + t * LPE;
+              if (c >= o1) break;
+              const int len = int(o1 - c < std::uint32_t(LPE) ? o1 - c : LPE);
+              float2 v[LPE];
+#pragma unroll
+              for (int r = 0; r < LPE; ++r) {
+                const std::uint32_t rid = __shfl_sync(gmask, ids[t], r, LPE);
+                v[r] = r < len ? *reinterpret_cast<const float2*>(rows + std::uint64_t(rid) * rstride + d)
+                               : make_float2(0.f, 0.f);
+              }
+#pragma unroll
+              for (int r = 0; r < LPE; ++r)
+                if (r < len) {
+                  acc0 = __dadd_rn(acc0, double(v[r].x));
+                  acc1 = __dadd_rn(acc1, double(v[r].y));
+                }
+            }
+          }
+          hrec[d] = acc0;
+          hrec[d + 1] = acc1;
+        }
+        summed = true;
+      }
       for (int d0 = 0; !summed && d0 < E; d0 += LPE) {
         const int d = d0 + sub;
         double acc = 0.0;
