@@ -1320,8 +1320,9 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
             DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, &t->dsc->fallbacks);
   mark_big(t, HPS_T_BIGFUSED);
   HPS_CUDA(cudaEventRecord(t->join3, bs));
-  // DPT dims per thread (8 / 4 when E allows 64- / 32-byte row loads)
-  const int dpt = t->short_dpt ? t->short_dpt : ((E % 8 == 0) ? 8 : ((E % 4 == 0) ? 4 : 1));
+  // DPT dims per thread: 4 when E allows 32-byte row loads (8 measured 1-2%
+  // slower in the pipelined c2 step: fewer threads in flight; HPS_SHORT_DPT=8)
+  const int dpt = t->short_dpt ? t->short_dpt : ((E % 4 == 0) ? 4 : 1);
   auto sk = dpt == 8 ? sparse_short_kernel<8>
                      : (dpt == 4 ? sparse_short_kernel<4> : sparse_short_kernel<1>);
   launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,

@@ -15,7 +15,7 @@ import json
 import os
 import sys
 
-KERNELS = ("big_classify", "big_plan", "big_fused", "sparse_short")
+KERNELS = ("big_classify", "big_plan", "big_fused", "sparse_short", "sparse_mid")
 
 
 def main() -> None:
@@ -50,7 +50,7 @@ def main() -> None:
         "dram__bytes_read.sum + dram__bytes_write.sum summed over the sparse segment-reduce "
         "kernels of one mini-batch (" + ", ".join(KERNELS) + "), averaged over " + str(mbs) +
         " mini-batches; ncu with its default cache control (caches flushed before each kernel), "
-        "profiles/r1_sparse_traffic.csv. Reads are the dL/dx records, the CSR grouping and the "
+        "profiles/r2_sparse_traffic.csv. Reads are the dL/dx records, the CSR grouping and the "
         "table rows the in-place apply updates; the row writes stay in L2 within a kernel")
     json.dump(doc, open(out_path, "w"), indent=1)
     print(json.dumps(doc[config]), mbs, "mini-batches")
