@@ -158,6 +158,15 @@ hps_status hps_destroy(hps_tier_t h);
 hps_status hps_build(hps_tier_t h, const uint64_t* keys, uint64_t n,
                      const float* host_rows);
 
+/* hps_build for keys the CALLER placed on this device (hbm_ps.hpp:74-80
+ * with any PartitionPolicy, e.g. range_split, topology.hpp:67-71): every
+ * given key is kept, no key % (N*D) filter. Used by the in-process hps::
+ * adapter (hps_gpu/hbm_ps.hpp), whose get/push route by the policy on the
+ * host; the collective hps_pull/hps_push/hps_train_* route by key % (N*D)
+ * and must not be mixed with a non-modulo placement. */
+hps_status hps_build_placed(hps_tier_t h, const uint64_t* keys, uint64_t n,
+                            const float* host_rows);
+
 /* HbmTier::get (hbm_ps.hpp:112-143). COLLECTIVE. Rows for `keys` (host
  * array, any order) written to out_rows (n x E, aligned with keys). Keys
  * owned by other ranks travel as pull request/response all-to-alls. */

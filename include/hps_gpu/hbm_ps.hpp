@@ -31,8 +31,9 @@
 // Threading follows the reference: get / push_deltas / drain_accums /
 // table_at may be called from any thread (one mutex per device handle);
 // SyncSession::run is a collective, one call per device, as in the reference.
-// PartitionPolicy::range_split (used only by the reference's Appendix-A unit
-// test) is rejected: device placement is key % (N*D) (topology.hpp:61-65).
+// Placement follows the PartitionPolicy on the host (modulo or range_split,
+// topology.hpp:58-72): build_node hands each device exactly its keys
+// (hps_build_placed), get/push/drain route by the same policy.
 #pragma once
 
 #include <algorithm>
@@ -99,7 +100,7 @@ struct Topology {
 // topology.hpp:58-72
 struct PartitionPolicy {
   std::function<int(ParamKey)> device_of_key;
-  bool is_modulo = false;  // (B200 build) the placement the device tier implements
+  bool is_modulo = false;  // (B200 build) key % (N*D), the collective C-ABI path's placement
 
   static PartitionPolicy modulo(const Topology& topo) {
     const int total = topo.total_devices();
@@ -270,7 +271,6 @@ class HbmTier {
     check(tr_ != nullptr, "hbm: the B200 tier needs its Transport (the device handles)");
     check(tr_->topology().total_devices() == topo.total_devices(),
           "hbm: transport topology mismatch");
-    check(policy_.is_modulo, "hbm: the device tier places keys by key % (N*D) only");
     check(tr_->width() == width, "hbm: width mismatch");
     for (auto& p : pending_) p.resize(topo.total_devices());
   }
@@ -292,7 +292,7 @@ class HbmTier {
       const int g = topo_.global_index(node, d);
       std::vector<ParamKey> owned;
       for (ParamKey k : merged)
-        if (policy_(k) == g) owned.push_back(k);
+        if (owner_of(k) == g) owned.push_back(k);
       std::vector<std::uint8_t> carried(owned.size(), 0);
       std::lock_guard lk(tr_->lock(g));
       if (built_[g] && !owned.empty())
@@ -305,7 +305,8 @@ class HbmTier {
         if (v.size() != width_ && v.size() != rw) throw Error("hbm: host value width mismatch");
         std::copy(v.begin(), v.end(), rows.begin() + i * rw);
       }
-      check_status(hps_build(tr_->handle(g), owned.data(), owned.size(), rows.data()));
+      check_status(
+          hps_build_placed(tr_->handle(g), owned.data(), owned.size(), rows.data()));
       built_[g] = true;
     }
   }
@@ -321,7 +322,7 @@ class HbmTier {
                                              Endpoint requester) {
     (void)requester;
     std::map<int, std::vector<ParamKey>> by_owner;
-    for (ParamKey k : keys) by_owner[policy_(k)].push_back(k);
+    for (ParamKey k : keys) by_owner[owner_of(k)].push_back(k);
     std::map<ParamKey, std::vector<float>> out;
     const std::size_t rw = tr_->row_width();
     for (auto& [g, ks] : by_owner) {
@@ -350,7 +351,7 @@ class HbmTier {
     std::map<int, std::vector<std::pair<ParamKey, const std::vector<float>*>>> parts;
     for (const auto& [k, v] : deltas) {
       if (v.size() != width_) throw Error("hbm: delta width mismatch");
-      parts[policy_(k)].emplace_back(k, &v);
+      parts[owner_of(k)].emplace_back(k, &v);
     }
     std::lock_guard lk(mu_);
     for (auto& [g, kv] : parts) {  // one message per (owner, push), keys unique within it
@@ -387,7 +388,7 @@ class HbmTier {
   void accumulate(const std::map<ParamKey, std::vector<float>>& deltas, Endpoint src) {
     push_deltas(deltas, src);
     std::vector<int> owners;
-    for (const auto& kv : deltas) owners.push_back(policy_(kv.first));
+    for (const auto& kv : deltas) owners.push_back(owner_of(kv.first));
     std::sort(owners.begin(), owners.end());
     owners.erase(std::unique(owners.begin(), owners.end()), owners.end());
     for (int g : owners) drain_accums(topo_.endpoint_of(g));
@@ -428,6 +429,14 @@ class HbmTier {
   }
 
  private:
+  int owner_of(ParamKey k) const {
+    const int g = policy_(k);
+    if (g < 0 || g >= topo_.total_devices())
+      throw Error("hbm: partition policy placed key " + std::to_string(k) + " on device " +
+                  std::to_string(g) + " of " + std::to_string(topo_.total_devices()));
+    return g;
+  }
+
   struct Message {  // one push_deltas call's share for one owner (kAccum)
     std::vector<ParamKey> keys;
     std::vector<float> vals;

@@ -3075,8 +3075,8 @@ static hps_status ensure_staged(Tier* t, std::uint64_t floats) {
   return HPS_OK;
 }
 
-hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float* host_rows) {
-  HPS_ENTER_Q(t);
+static hps_status build_impl(Tier* t, const uint64_t* keys, uint64_t n, const float* host_rows,
+                             bool owned_only) {
   if (n > t->Wmax)
     return set_error(HPS_ERR_CAPACITY, "build: %llu keys exceed max_working_set %llu",
                      (unsigned long long)n, (unsigned long long)t->Wmax);
@@ -3102,7 +3102,11 @@ hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float
   open_lookback_context(t);
   if (n) {
     radix_sort(t, t->lane[0].kB, t->lane[0].vB, Count{nullptr, n}, n, 64, true, &sk, &so);
-    tile_scan(t, RunStartOwned{sk, std::uint64_t(t->G), std::uint64_t(t->g)},
+    // owned_only: keep key % G == g; otherwise every given key (the caller
+    // placed them, e.g. a range-split policy)
+    const std::uint64_t G = owned_only ? std::uint64_t(t->G) : 1;
+    const std::uint64_t g = owned_only ? std::uint64_t(t->g) : 0;
+    tile_scan(t, RunStartOwned{sk, G, g},
               CompactEmit{sk, so, t->ws, t->ws_idx}, Count{nullptr, n}, n, &t->dsc->n_ws);
   } else {
     HPS_CUDA(cudaMemsetAsync(&t->dsc->n_ws, 0, 8, t->st));
@@ -3110,6 +3114,17 @@ hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float
   build_table(t, n, t->ws_idx, staged);
   t->ws_sorted = true;
   return check_device_error(t, "device table: missing key ");
+}
+
+hps_status hps_build(hps_tier_t t, const uint64_t* keys, uint64_t n, const float* host_rows) {
+  HPS_ENTER_Q(t);
+  return build_impl(t, keys, n, host_rows, true);
+}
+
+hps_status hps_build_placed(hps_tier_t t, const uint64_t* keys, uint64_t n,
+                            const float* host_rows) {
+  HPS_ENTER_Q(t);
+  return build_impl(t, keys, n, host_rows, false);
 }
 
 static hps_status require_built(Tier* t) {

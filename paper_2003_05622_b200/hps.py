@@ -100,6 +100,7 @@ _SIGS = {
     "hps_create": ([ctypes.POINTER(HpsConfig), _P, ctypes.POINTER(_P)], ctypes.c_int),
     "hps_destroy": ([_P], ctypes.c_int),
     "hps_build": ([_P, _P, _U64, _P], ctypes.c_int),
+    "hps_build_placed": ([_P, _P, _U64, _P], ctypes.c_int),
     "hps_pull": ([_P, _P, _U64, _P], ctypes.c_int),
     "hps_push": ([_P, _P, _P, _U64], ctypes.c_int),
     "hps_drain": ([_P], ctypes.c_int),
@@ -341,6 +342,15 @@ class Tier:
             raise Error(7, "hbm: host value width mismatch")
         _check(lib().hps_build(self._h, _ptr(k), k.size,
                                _ptr(rows) if rows is not None else None))
+
+    def build_placed(self, keys, host_rows=None) -> None:
+        """hps_build_placed: every given key is kept (the caller placed them)."""
+        k = _u64(keys)
+        rows = None if host_rows is None else _f32(host_rows).reshape(-1)
+        if rows is not None and rows.size != k.size * self.row_width:
+            raise Error(7, "hbm: host value width mismatch")
+        _check(lib().hps_build_placed(self._h, _ptr(k), k.size,
+                                      _ptr(rows) if rows is not None else None))
 
     def pull(self, keys) -> np.ndarray:
         k = _u64(keys)

@@ -101,6 +101,45 @@ static void unit_cases(int G) {
   }
 }
 
+// test_hbm_ps.cpp:42-60: the worked range split — keys <= 50 on device 0,
+// the rest on device 1, then get/accumulate routed by the same policy.
+static void range_split_case(int G) {
+  const Topology topo(1, G);
+  Transport::Options o;
+  o.max_batch_keys = 64;
+  Transport tr(topo, 1, o);
+  HbmTier hbm(topo, PartitionPolicy::range_split(50), 1, &tr);
+  const std::vector<ParamKey> keys = {4, 5, 11, 50, 53, 56, 61, 87, 98};
+  auto keyed = [](ParamKey k) { return std::vector<float>{float(k)}; };
+  if (G < 2) {  // the policy names device 1, which a 1-device topology lacks
+    bool threw = false;
+    try {
+      hbm.build_all({keys}, keyed);
+    } catch (const Error& e) {
+      threw = std::strstr(e.what(), "on device 1 of 1") != nullptr;
+    }
+    CHECK(threw);
+    return;
+  }
+  hbm.build_all({keys}, keyed);
+  std::vector<ParamKey> dev0, dev1;
+  hbm.table_at(0, 0)->for_each([&](ParamKey k, const float* v) {
+    dev0.push_back(k);
+    CHECK(v[0] == float(k));
+  });
+  hbm.table_at(0, 1)->for_each([&](ParamKey k, const float*) { dev1.push_back(k); });
+  std::sort(dev0.begin(), dev0.end());
+  std::sort(dev1.begin(), dev1.end());
+  CHECK((dev0 == std::vector<ParamKey>{4, 5, 11, 50}));
+  CHECK((dev1 == std::vector<ParamKey>{53, 56, 61, 87, 98}));
+  hbm.accumulate({{50, {0.5f}}, {53, {0.25f}}}, Endpoint{0, 0});
+  auto v = hbm.get({53, 50, 4}, Endpoint{0, 1});
+  CHECK((v[50] == std::vector<float>{50.5f}));
+  CHECK((v[53] == std::vector<float>{53.25f}));
+  CHECK((v[4] == std::vector<float>{4.0f}));
+  CHECK(hbm.table_at(1)->contains(53) && !hbm.table_at(0)->contains(53));
+}
+
 // pipeline.hpp:502-566 over the hps:: API, vs oracle train_reference.
 static void device_worker_loop(int G) {
   const int E = 8, J = 4, L = 3;
@@ -207,6 +246,7 @@ int main(int argc, char** argv) {
   const int G = argc > 1 ? std::atoi(argv[1]) : 1;
   try {
     unit_cases(G);
+    range_split_case(G);
     device_worker_loop(G);
   } catch (const std::exception& e) {
     std::printf("FAIL uncaught: %s\n", e.what());
