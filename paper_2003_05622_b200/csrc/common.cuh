@@ -69,6 +69,25 @@ __device__ __forceinline__ void st_f4(float* p, float4 v) {
 // Adagrad the gradient g itself (self-pinned extension, BASELINE c3,
 // oracle/hps_oracle.c or_adagrad_apply):
 //   s' = s + g*g;   v' = v - (lr*g) / (sqrt(s') + eps)      (f32, every op _rn)
+// 16-byte global -> shared copy (async proxy), zero-filled when !valid
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 struct Optim {
   int kind;  // 0 SGD, 1 Adagrad
   int E;     // embedding width (the pushed value's width)

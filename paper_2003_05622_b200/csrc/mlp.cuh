@@ -170,11 +170,6 @@ __device__ __forceinline__ void put_split(char* dst, std::size_t lo_off, std::si
   }
 }
 
-__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-               "r"(valid ? 16 : 0));
-}
 __device__ __forceinline__ void cp_async4_zfill(void* smem, const void* gmem, bool valid) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),

@@ -126,6 +126,69 @@ __device__ __forceinline__ bool embed_sum_exact(const std::uint32_t* __restrict_
   return true;
 }
 
+// embed_sum of one example in feature order (model.hpp embed_sum), E == LPE
+// lanes, E % 4 == 0: the group's rows stream through a shared-memory tile
+// (two chunks of kTileRows rows, cp.async 16-byte copies spread over the
+// lanes, chunk c + 1 in flight while chunk c is summed), and lane d runs the
+// in-order f64 chain of dimension d from shared memory — one LDS, one
+// conversion and one DADD per feature instead of a shuffle, an address and a
+// predicated scalar load per (feature, lane).
+constexpr int kTileRows = 32;
+template <int LPE>
+__host__ __device__ constexpr int embed_tile_floats() { return 2 * kTileRows * LPE; }
+
+template <int LPE>
+__device__ __forceinline__ void embed_sum_tiled(const std::uint32_t* __restrict__ occ_row,
+                                                const float* __restrict__ rows, int rstride,
+                                                std::uint32_t o0, std::uint32_t o1, int sub,
+                                                unsigned gmask, float* tile, double* hrec) {
+  constexpr int E = LPE, V4 = E / 4, CR = kTileRows;
+  constexpr int NL = CR * V4 / LPE;  // 16-byte copies per lane per chunk
+  constexpr int IDR = CR / LPE;      // row ids per lane per chunk
+  static_assert(LPE % V4 == 0 && CR % LPE == 0, "tile shape");
+  const std::uint32_t nrows = o1 - o0;
+  const int nchunks = int((nrows + CR - 1) / CR);
+  auto issue = [&](int c) {
+    const std::uint32_t cb = o0 + std::uint32_t(c) * CR;
+    std::uint32_t id[IDR];
+#pragma unroll
+    for (int t = 0; t < IDR; ++t) {
+      const std::uint32_t p = cb + std::uint32_t(sub + LPE * t);
+      id[t] = p < o1 ? occ_row[p] : 0u;
+    }
+    float* buf = tile + (c & 1) * CR * E;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+      // copy f = j*LPE + sub: row r = f / V4, quarter q = f % V4; the row's
+      // id sits in id[j / V4] of lane r % LPE
+      const int f = j * LPE + sub, r = f / V4, q = f % V4;
+      const std::uint32_t rid = __shfl_sync(gmask, id[j / V4], r % LPE, LPE);
+      const bool ok = cb + std::uint32_t(r) < o1;
+      cp_async16_zfill(buf + r * E + q * 4, rows + (ok ? std::uint64_t(rid) * rstride + q * 4 : 0),
+                       ok);
+    }
+    cp_async_commit();
+  };
+  if (nchunks > 0) issue(0);
+  double acc = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) issue(c + 1);
+    else cp_async_commit();  // (an empty group keeps the count)
+    cp_async_wait<1>();      // chunk c landed (this lane's copies) ...
+    __syncwarp(gmask);       // ... and every lane's
+    const float* buf = tile + (c & 1) * CR * E;
+    const int cnt = int(min(nrows - std::uint32_t(c) * CR, std::uint32_t(CR)));
+    float v[CR];
+#pragma unroll
+    for (int i = 0; i < CR; ++i) v[i] = buf[i * E + sub];
+#pragma unroll
+    for (int i = 0; i < CR; ++i)
+      if (i < cnt) acc = __dadd_rn(acc, double(v[i]));
+    __syncwarp(gmask);  // the buffer is refilled by issue(c + 2)
+  }
+  hrec[sub] = acc;
+}
+
 // Forward + per-example backward. LPE lanes per example (power of two
 // <= 32); each example's scratch lives in shared memory. Writes the H and DL
 // records (for the dense-gradient reduction), DX = dL/dx (for the sparse
@@ -140,7 +203,7 @@ __global__ void __launch_bounds__(128)
                    const std::uint8_t* __restrict__ labels,
                    double* __restrict__ H, double* __restrict__ DL,
                    double* __restrict__ DX, double* __restrict__ loss,
-                   DevError* err) {
+                   DevError* err, int tiled) {
   pdl_wait();
   extern __shared__ double smem[];
   constexpr int kEPB = 128 / LPE;  // examples per block
@@ -159,6 +222,10 @@ __global__ void __launch_bounds__(128)
   double* hrec = scratch + slot * per_ex;     // [hw]: x | h1 | h2 ...
   double* zrec = hrec + md.hw;                // [dw]: z per layer, then dl
   double* dprev = zrec + md.dw;               // [maxw]
+  // embed tiles (embed_sum_tiled) after the per-example scratch, 16-B aligned
+  float* tile = reinterpret_cast<float*>(
+                    (reinterpret_cast<std::uintptr_t>(scratch + kEPB * per_ex) + 15) & ~std::uintptr_t(15)) +
+                std::size_t(slot) * embed_tile_floats<LPE>();
   const int E = md.E;
   double loss_acc = 0.0;
 
@@ -181,9 +248,13 @@ __global__ void __launch_bounds__(128)
       }
       bool summed = false;
       if constexpr (LPE == 8 || LPE == 16) {
-        if (E == LPE)
+        if (E == LPE && tiled) {
+          embed_sum_tiled<LPE>(occ_row, rows, rstride, o0, o1, sub, gmask, tile, hrec);
+          summed = true;
+        } else if (E == LPE) {
           summed = embed_sum_exact<LPE>(occ_row, rows, rstride, o0, o1, sub, gmask,
                                         md.exact_slack, hrec);
+        }
       }
       // two dims per lane (8-byte row loads, two chains) when the row is a
       // multiple of 2 x LPE wide and 8-byte aligned (c3: E = 64 on 32 lanes):
@@ -345,17 +416,6 @@ __global__ void __launch_bounds__(128)
   if (sub == 0 && loss_acc != 0.0) atomicAdd(loss, loss_acc);
 }
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::);
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 // ---- TMA bulk copy + mbarrier helpers (sm_90+/sm_100a async proxy) ----
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -1252,6 +1312,156 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
     if (int(threadIdx.x) < E)
       dout.grad(u, E, int(threadIdx.x), g);
     __syncthreads();
+  }
+}
+
+// ---- big segments: one CTA per key --------------------------------------
+//
+// The alternative to big_fused_kernel's cross-CTA chunks (HPS_BIG=key, the
+// default): one 1024-thread CTA owns a key, so nothing crosses CTAs — no
+// flags, no fences, no polling. Thread (s, d) takes slice s (kBigPer
+// consecutive occurrences of the key's ordered segment) of dimension d per
+// chunk of slices x kBigPer occurrences, holds its values in registers and
+//   1. adds them into its Neumaier total (S) and sum|x| (A), and publishes
+//      the slice total;
+//   2. takes its offset = the running total of the earlier chunks + the
+//      earlier slices' totals (one f64 chain in slice order; its error is
+//      within the (m + slices) u A term of certify_f32), and adds |offset +
+//      in-slice prefix| into its share of B;
+// the last slice carries the running total to the next chunk. After the
+// last chunk a tree over the slices combines S (double-double), A and B
+// (rounded up), and certify_f32 decides each dimension exactly as for
+// big_fused_kernel; an uncertified dimension recomputes the in-order chain.
+constexpr int kBigThreads = 1024;
+constexpr int kBigPer = 16;  // occurrences per thread and chunk (in registers)
+
+__host__ __device__ constexpr int big_slices(int E) { return kBigThreads / E; }
+__host__ __device__ constexpr std::size_t big_smem(int E) {
+  return (std::size_t(5) * big_slices(E) * E + E) * 8;
+}
+
+__global__ void __launch_bounds__(kBigThreads, 1)
+    big_key_kernel(int E, std::uint64_t n, const std::uint32_t* __restrict__ big_list,
+                   const unsigned long long* __restrict__ n_big,
+                   const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
+                   DeltaOut dout, const double* __restrict__ DX,
+                   unsigned long long* __restrict__ fallbacks,
+                   unsigned long long* __restrict__ big_keys,
+                   unsigned long long* __restrict__ max_chunks,
+                   unsigned long long* __restrict__ big_occ) {
+  pdl_wait();
+  extern __shared__ double bk[];
+  __shared__ bool bad[256];
+  const int slices = kBigThreads / E, SE = slices * E;
+  double* sh = bk;       // [slices][E] this chunk's slice totals
+  double* rt = sh + SE;  // [E] running total of the earlier chunks
+  double* r0 = rt + E;   // [slices][E] the final tree: S.hi, S.lo, A, B
+  double* r1 = r0 + SE;
+  double* r2 = r1 + SE;
+  double* r3 = r2 + SE;
+  const int s = int(threadIdx.x) / E, d = int(threadIdx.x) - s * E;
+  const bool worker = s < slices;
+  const std::uint32_t chunk = std::uint32_t(slices) * kBigPer;
+  const std::uint64_t NB = *n_big;
+  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && NB) atomicAdd(big_keys, (unsigned long long)NB);
+  for (std::uint64_t ki = blockIdx.x; ki < NB; ki += gridDim.x) {
+    const std::uint32_t u = big_list[ki];
+    const std::uint32_t k0 = seg[u], k1 = seg[u + 1];
+    const std::uint32_t nch = (k1 - k0 + chunk - 1) / chunk;
+    if (threadIdx.x == 0) {
+      atomicAdd(big_occ, (unsigned long long)(k1 - k0));
+      atomicMax(max_chunks, (unsigned long long)nch);
+    }
+    if (int(threadIdx.x) < E) rt[threadIdx.x] = 0.0;
+    DD S{0.0, 0.0};
+    double A = 0.0, B = 0.0;
+    for (std::uint32_t c = 0; c < nch; ++c) {
+      const std::uint32_t a0 = k0 + c * chunk + std::uint32_t(s) * kBigPer;
+      const int cnt = worker && a0 < k1 ? int(min(k1 - a0, std::uint32_t(kBigPer))) : 0;
+      double x[kBigPer];
+      {
+        std::uint32_t e[kBigPer];
+#pragma unroll
+        for (int i = 0; i < kBigPer; ++i) e[i] = i < cnt ? exs[a0 + i] : 0u;
+#pragma unroll
+        for (int i = 0; i < kBigPer; ++i) x[i] = i < cnt ? DX[std::uint64_t(e[i]) * E + d] : 0.0;
+      }
+      DD t{0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < kBigPer; ++i)
+        if (i < cnt) {
+          t = dd_add(t, x[i]);
+          A = __dadd_ru(A, fabs(x[i]));
+        }
+      S = dd_add(S, t);
+      if (worker) sh[s * E + d] = dd_value(t);
+      __syncthreads();
+      double o = 0.0;
+      if (worker) {
+        o = rt[d];
+        for (int q = 0; q < s; ++q) o = __dadd_rn(o, sh[q * E + d]);
+        double l = 0.0;
+#pragma unroll
+        for (int i = 0; i < kBigPer; ++i)
+          if (i < cnt) {
+            l = __dadd_rn(l, x[i]);
+            B = __dadd_ru(B, fabs(__dadd_rn(o, l)));
+          }
+      }
+      __syncthreads();  // every offset read rt before the last slice moves it
+      if (worker && s == slices - 1) rt[d] = __dadd_rn(o, sh[s * E + d]);
+    }
+    if (worker) {
+      r0[s * E + d] = S.hi;
+      r1[s * E + d] = S.lo;
+      r2[s * E + d] = A;
+      r3[s * E + d] = B;
+    }
+    __syncthreads();
+    int h = 1;
+    while (h < slices) h <<= 1;
+    for (h >>= 1; h >= 1; h >>= 1) {
+      if (worker && s < h && s + h < slices) {
+        const int i = s * E + d, j = (s + h) * E + d;
+        const DD a = dd_add(DD{r0[i], r1[i]}, DD{r0[j], r1[j]});
+        r0[i] = a.hi;
+        r1[i] = a.lo;
+        r2[i] = __dadd_ru(r2[i], r2[j]);
+        r3[i] = __dadd_ru(r3[i], r3[j]);
+      }
+      __syncthreads();
+    }
+    float g = 0.0f;
+    if (int(threadIdx.x) < E) {
+      const std::uint32_t m = k1 - k0;
+      bad[threadIdx.x] = !certify_f32(dd_value(DD{r0[threadIdx.x], r1[threadIdx.x]}),
+                                      r3[threadIdx.x], r2[threadIdx.x], m,
+                                      // offsets: slices x nch terms; S: <= 2 slices (nch + 1)
+                                      // double-double adds beyond the n terms
+                                      std::uint64_t(m) + 2 * std::uint64_t(slices) * (nch + 1) + nch,
+                                      inv_n, &g);
+    }
+    __syncthreads();
+    double* stage = r0;  // the tree is read: SE doubles of staging
+    for (int dd = 0; dd < E; ++dd) {
+      if (!bad[dd]) continue;
+      double acc = 0.0;
+      for (std::uint32_t cs0 = k0; cs0 < k1; cs0 += std::uint32_t(SE)) {
+        const int mm = int(min(k1 - cs0, std::uint32_t(SE)));
+        for (int j = threadIdx.x; j < mm; j += kBigThreads)
+          stage[j] = DX[std::uint64_t(exs[cs0 + j]) * E + dd];
+        __syncthreads();
+        if (int(threadIdx.x) == dd) acc = chain_sum(stage, mm, acc);
+        __syncthreads();
+      }
+      if (int(threadIdx.x) == dd) {
+        g = __double2float_rn(__dmul_rn(acc, inv_n));
+        if (fallbacks) atomicAdd(fallbacks, 1ull);
+      }
+    }
+    if (int(threadIdx.x) < E) dout.grad(u, E, int(threadIdx.x), g);
+    __syncthreads();  // shared memory is the next key's
   }
 }
 

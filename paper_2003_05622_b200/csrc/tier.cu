@@ -251,6 +251,8 @@ struct Tier {
   cudaEvent_t fork4 = nullptr, join4 = nullptr;
   int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
   std::uint32_t mid_max = 512;          // medium segments: kLongSeg < length <= mid_max
+  bool fb_tile = true;  // fwd/bwd embed_sum through shared-memory row tiles (HPS_FB_TILE=0: off)
+  bool big_key = true;  // longer segments: one CTA per key (HPS_BIG=fused: chunks over CTAs)
                                         // (HPS_MID_SEG; kLongSeg disables the path)
   Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
                                         // 2..: the next batch's mini-batch groupings
@@ -1272,6 +1274,7 @@ static hps_status launch_big_plan(Tier* t, std::uint64_t u_upper, const std::uin
   HPS_CUDA(cudaMemsetAsync(&t->dsc->n_mid, 0, 8, bs));
   launch_on(t, bs, big_classify_kernel, grid_for(std::max<std::uint64_t>(u_upper, 1)), 256, 0,
             U, seg, t->big_list, nb, t->mid_max, t->mid_list, &t->dsc->n_mid);
+  if (t->big_key) return HPS_OK;  // big_key_kernel plans nothing
   launch_on(t, bs, big_plan_kernel, 1, 1024, 0, fuse_chunk(t->E),
             (const std::uint32_t*)t->big_list, (const unsigned long long*)nb, seg, t->chunk_off,
             &t->dsc->n_items, t->item_key, t->item_chunk, &t->dsc->big_keys, &t->dsc->max_chunks,
@@ -1313,11 +1316,18 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   }
   if (t->big_side) HPS_CUDA(cudaEventRecord(t->join4, ms));
   mark_big(t, -1);
-  launch_on(t, bs, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
-            (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big,
-            (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
-            (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs, dout,
-            DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done, &t->dsc->fallbacks);
+  if (t->big_key)
+    launch_on(t, bs, big_key_kernel, kSMs, kBigThreads, big_smem(E), E, n,
+              (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big, seg,
+              exs, dout, DX, &t->dsc->fallbacks, &t->dsc->big_keys, &t->dsc->max_chunks,
+              &t->dsc->big_occ);
+  else
+    launch_on(t, bs, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
+              (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big,
+              (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
+              (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs,
+              dout, DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done,
+              &t->dsc->fallbacks);
   mark_big(t, HPS_T_BIGFUSED);
   HPS_CUDA(cudaEventRecord(t->join3, bs));
   // DPT dims per thread: 4 when E allows 32-byte row loads (8 measured 1-2%
@@ -1935,13 +1945,16 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
       } else {
       const int LPE = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
       const int epb = 128 / LPE;
+      // the shared-memory row tiles of embed_sum_tiled (E == LPE, 16-B rows)
+      const int tiled = T->fb_tile && E == LPE && E % 4 == 0 && rstride % 4 == 0;
       const size_t smem = size_t((T->md.nw + 1) & ~1) * 4 +
-                          size_t(epb) * (T->md.hw + T->md.dw + T->md.maxw) * 8;
+                          size_t(epb) * (T->md.hw + T->md.dw + T->md.maxw) * 8 +
+                          (tiled ? 16 + size_t(epb) * 2 * kTileRows * LPE * 4 : 0);
       const unsigned blocks = unsigned(std::min<std::uint64_t>((n + epb - 1) / epb, kSMs * 8));
       auto k = LPE == 8 ? fwd_bwd_kernel<8> : (LPE == 16 ? fwd_bwd_kernel<16> : fwd_bwd_kernel<32>);
       launch(T, k, blocks, 128, smem, T->md, sm, (const float*)T->dense,
              (const std::uint32_t*)T->occ_off, goff, occ_row, rows, rstride, dlab, T->H,
-             T->DL, T->DX, &T->dsc->loss, &T->dsc->err);
+             T->DL, T->DX, &T->dsc->loss, &T->dsc->err, tiled);
       mark(T, HPS_T_FWDBWD);
       // dense-grad reduce on the side stream, overlapping the sparse reduce
       HPS_CUDA(cudaEventRecord(T->fork, T->st));
@@ -2663,6 +2676,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     t->prep_mbs = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_BIG_SIDE")) t->big_side = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_BIG")) t->big_key = std::strcmp(v, "fused") != 0;
+  if (const char* v = std::getenv("HPS_FB_TILE")) t->fb_tile = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_SHORT_DPT")) {
     const int d = std::atoi(v);
     if (d == 1 || (d == 4 && c.embedding_dim % 4 == 0) || (d == 8 && c.embedding_dim % 8 == 0))

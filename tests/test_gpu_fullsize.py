@@ -45,9 +45,18 @@ def max_segment(off, keys, B, J):
     return int(c.max())
 
 
-@pytest.mark.parametrize("store_kind", ["host", "device"])
-def test_config2_full_size_bit_exact(pkg, oracle, store_kind):
+def big_chunk(E, big):
+    """Occurrences per chunk of the long-segment kernels: big_key_kernel
+    (HPS_BIG=key: 1024 threads, one CTA per key) and big_fused_kernel
+    (HPS_BIG=fused: 256 threads, chunks over CTAs); 16 per thread."""
+    return ((1024 if big == "key" else 256) // E) * 16
+
+
+@pytest.mark.parametrize("store_kind,big", [("host", "key"), ("device", "key"),
+                                            ("host", "fused")])
+def test_config2_full_size_bit_exact(pkg, oracle, monkeypatch, store_kind, big):
     import torch
+    monkeypatch.setenv("HPS_BIG", big)
     dims, E, B, nnz, J, layers, nb = 10**7, 16, 16384, 100, 4, (8, 16, 1), 3
     off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=1)
     tier = pkg.Tier(width=E, layer_dims=layers, minibatches=J, key_space=dims,
@@ -70,12 +79,12 @@ def test_config2_full_size_bit_exact(pkg, oracle, store_kind):
     if store_kind == "device":
         torch.cuda.synchronize()
         store = dstore.cpu().numpy()
-    # the data makes ~16-chunk segments (fuse_chunk(16) = 256 occurrences)...
+    # the data makes segments of > 15 x 256 occurrences ...
     seg = max_segment(off, keys, B, J)
     assert seg > 15 * 256, seg
-    # ... and the device planned them
+    # ... and the device took them on the long-segment path, in chunks
     assert all(s.big_segments > 0 for s in stats)
-    assert max(s.max_segment_chunks for s in stats) >= 16
+    assert max(s.max_segment_chunks for s in stats) >= -(-(15 * 256 + 1) // big_chunk(E, big))
     wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, layers, J=J), B, off, keys, lab)
     assert np.array_equal(dense, wd), np.abs(dense - wd).max()
     got = store[wk.astype(np.int64)]
@@ -83,10 +92,12 @@ def test_config2_full_size_bit_exact(pkg, oracle, store_kind):
     assert bad.size == 0, f"{bad.size} rows differ, e.g. key {wk[bad[0]]}"
 
 
+@pytest.mark.parametrize("big", ["key", "fused"])
 @pytest.mark.parametrize("E,B,nnz,chunks", [(16, 4096, 20, 2), (8, 2048, 30, 1), (64, 1024, 20, 2)])
 def test_forced_certificate_failure_takes_exact_fallbacks(pkg, oracle, monkeypatch, E, B, nnz,
-                                                          chunks):
+                                                          chunks, big):
     monkeypatch.setenv("HPS_CERT_FORCE_FAIL", "1")
+    monkeypatch.setenv("HPS_BIG", big)
     monkeypatch.setenv("HPS_MID_SEG", "32")  # every long segment on the certified path
     dims, J, layers, nb = 20000, 4, (8, 16, 1), 3
     off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=17)
@@ -103,8 +114,10 @@ def test_forced_certificate_failure_takes_exact_fallbacks(pkg, oracle, monkeypat
     # took the exact chain
     assert all(s.exact_fallbacks >= s.big_segments * E for s in stats)
     assert all(s.big_segments > 0 for s in stats)
-    # chunks >= 2: the multi-CTA look-back path; 1: the single-CTA path
-    assert max(s.max_segment_chunks for s in stats) >= chunks
+    # fused: chunks >= 2 takes the multi-CTA look-back path, 1 the single-CTA
+    # path; key: one CTA per key (its chunks run in turn)
+    if big == "fused":
+        assert max(s.max_segment_chunks for s in stats) >= chunks
     wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, layers, J=J), B, off, keys, lab)
     assert np.array_equal(dense, wd), np.abs(dense - wd).max()
     assert np.array_equal(store[wk.astype(np.int64)], wr)
