@@ -704,6 +704,142 @@ __global__ void __launch_bounds__(32 * kDGFinWarps)
 
 inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw + 31) / 32); }
 
+// The dense gradient in ONE launch and ONE pass over the records
+// (HPS_DG_FUSED=1, the default; the four launches above are the
+// alternative). B is bounded without the slices' offsets: with O_s the
+// exact prefix before slice s and lambda_k the prefix inside it,
+// |s_k| <= |O_s| + |lambda_k|, so
+//   B = sum_s ( cnt_s * |O_s| + Lambda_s ),  Lambda_s = sum_k |l_k|
+// bounds sum_k |s_k| (up to the rounding terms certify_f32 already carries;
+// at most a small factor looser than the offset walk of p2). A slice
+// (one thread: one weight, per consecutive examples) computes its
+// double-double total T, sum|x| A and Lambda in one walk, publishes them, and
+// bumps its weight group's counter; the group's last CTA scans the slices'
+// totals in order (O_s), forms S, A, B, certifies (certify_f32) and
+// recomputes an uncertified weight's exact chain, then resets the counter.
+// No CTA waits for another. CTA = kDGFWarps warps = kDGFWarps slices of one
+// weight group (lane = weight).
+constexpr int kDGFWarps = 16;
+
+__global__ void __launch_bounds__(32 * kDGFWarps, 1)
+    dense_grad_fused_kernel(ModelDims md, std::uint64_t n, const double* __restrict__ H,
+                            const double* __restrict__ DL, double* __restrict__ part,
+                            unsigned* __restrict__ done, float* __restrict__ grad,
+                            unsigned long long* __restrict__ fallbacks) {
+  pdl_wait();
+  __shared__ double red[4][kDGFWarps][32];
+  __shared__ double stage[kDGStage];
+  __shared__ unsigned s_last, s_bad;
+  const unsigned lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const unsigned grp = blockIdx.x, sl = blockIdx.y * kDGFWarps + wq;
+  const int w = int(grp * 32 + lane);
+  const bool valid = w < md.nw;
+  const WeightRef r = weight_ref(md, valid ? w : md.nw - 1);
+  const std::uint64_t per = (n + kDGSlices - 1) / kDGSlices;
+  const std::uint64_t k0 = sl * per < n ? sl * per : n, k1 = k0 + per < n ? k0 + per : n;
+  DD t{0.0, 0.0};
+  double a = 0.0, l = 0.0, lam = 0.0;
+#pragma unroll 8
+  for (std::uint64_t k = k0; k < k1; ++k) {
+    const double x = weight_term(md, H, DL, r, k);
+    t = dd_add(t, x);
+    a = __dadd_ru(a, fabs(x));
+    l = __dadd_rn(l, x);
+    lam = __dadd_ru(lam, fabs(l));
+  }
+  if (valid) {
+    double* slot = part + (std::uint64_t(w) * kDGSlices + sl) * 4;
+    slot[0] = t.hi;
+    slot[1] = t.lo;
+    slot[2] = a;
+    slot[3] = lam;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&done[grp], 1u) == kDGSlices / kDGFWarps - 1;
+    if (s_last) __threadfence();
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // the group's last CTA: warp wq owns slices [wq * R, (wq + 1) * R) of
+  // weight `lane`; their totals in order, a cross-warp exclusive prefix,
+  // then the B walk over the same slices
+  constexpr int R = kDGSlices / kDGFWarps;
+  const double* base = part + std::uint64_t(valid ? w : 0) * kDGSlices * 4;
+  DD S{0.0, 0.0};
+  double A = 0.0, run = 0.0;
+  double rec[R][4];  // this warp's slices, all loads in flight at once
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) rec[i][c] = valid ? __ldcg(base + (int(wq) * R + i) * 4 + c) : 0.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    S = dd_add(S, DD{rec[i][0], rec[i][1]});
+    A = __dadd_ru(A, rec[i][2]);
+    run = __dadd_rn(run, __dadd_rn(rec[i][0], rec[i][1]));
+  }
+  red[0][wq][lane] = run;
+  __syncthreads();
+  double O = 0.0;  // exact-prefix estimate before this warp's first slice
+  for (unsigned q = 0; q < wq; ++q) O = __dadd_rn(O, red[0][q][lane]);
+  double B = 0.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const std::uint64_t q0 = std::uint64_t(int(wq) * R + i) * per;
+    const std::uint64_t cnt = q0 >= n ? 0 : (q0 + per < n ? per : n - q0);
+    B = __dadd_ru(B, __dadd_ru(__dmul_ru(double(cnt), fabs(O)), rec[i][3]));
+    O = __dadd_rn(O, __dadd_rn(rec[i][0], rec[i][1]));
+  }
+  __syncthreads();  // red[0] is rewritten below
+  red[0][wq][lane] = S.hi;
+  red[1][wq][lane] = S.lo;
+  red[2][wq][lane] = A;
+  red[3][wq][lane] = B;
+  __syncthreads();
+  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  float g = 0.0f;
+  bool bad = false;
+  if (wq == 0 && valid) {
+    DD St{red[0][0][lane], red[1][0][lane]};
+    double At = red[2][0][lane], Bt = red[3][0][lane];
+    for (int q = 1; q < kDGFWarps; ++q) {
+      St = dd_add(St, DD{red[0][q][lane], red[1][q][lane]});
+      At = __dadd_ru(At, red[2][q][lane]);
+      Bt = __dadd_ru(Bt, red[3][q][lane]);
+    }
+    bad = !certify_f32(dd_value(St), Bt, At, n, per + kDGSlices, inv_n, &g);
+  }
+  // an uncertified weight: its exact chain in order (rare), staged by the CTA
+  const unsigned bm = __ballot_sync(0xFFFFFFFFu, bad);
+  if (threadIdx.x == 0) s_bad = bm;
+  __syncthreads();
+  unsigned badm = s_bad;
+  while (badm) {
+    const int bl = __ffs(badm) - 1;
+    badm &= badm - 1;
+    const WeightRef rb = weight_ref(md, int(grp * 32) + bl);
+    double acc = 0.0;
+    for (std::uint64_t c0 = 0; c0 < n; c0 += kDGStage) {
+      const int cnt = int(n - c0 < kDGStage ? n - c0 : kDGStage);
+      for (int j = int(threadIdx.x); j < cnt; j += int(blockDim.x))
+        stage[j] = weight_term(md, H, DL, rb, c0 + j);
+      __syncthreads();
+      if (threadIdx.x == 0) acc = chain_sum(stage, cnt, acc);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      red[0][0][bl] = acc;
+      if (fallbacks) atomicAdd(fallbacks, 1ull);
+    }
+    __syncthreads();
+    if (wq == 0 && int(lane) == bl) g = __double2float_rn(__dmul_rn(red[0][0][bl], inv_n));
+  }
+  if (wq == 0 && valid) grad[w] = g;
+  if (threadIdx.x == 0) done[grp] = 0u;  // every CTA of the group has counted
+}
+
 // Sparse gradient segment-reduce + sgd_delta (model.hpp:182-200, 226-230).
 // Per unique key u: sum over its occurrences, in example order, of the
 // example's dL/dx (the CSR segment [seg[u], seg[u+1]) of the stably sorted
@@ -960,6 +1096,131 @@ __global__ void __launch_bounds__(32 * kMidWarps)
   }
 }
 
+// Medium segments, certified (the default for E in {4, 8, 16, 32}; the
+// exact warp chains above otherwise, or with HPS_MID_CERT=0): one warp per
+// key, lane = (slice s, group g of 4 dimensions), SL = 32 / (E/4) slices of
+// consecutive occurrences. The segment's example ids are staged in shared
+// memory (cp.async, one round trip); each lane then streams its slice's
+// dL/dx quads (16 loads in flight) into four Neumaier totals T, sums |x| (A)
+// and Lambda = sum |in-slice prefix|. Shuffles over the slices give the
+// exclusive prefix O_s of the slice totals, B = sum_s (cnt_s |O_s| +
+// Lambda_s) >= sum_k |s_k|, and S, A, B per dimension; certify_f32 decides
+// each dimension (n = the key's occurrences), and an uncertified one (rare)
+// recomputes the in-order chain from the ordered segment.
+constexpr int kMidCertWarps = 4;
+__host__ __device__ constexpr std::size_t mid_cert_smem() {
+  return std::size_t(kMidCertWarps) * kMidMaxSeg * 4;
+}
+
+template <int E>
+__global__ void __launch_bounds__(32 * kMidCertWarps)
+    sparse_mid_cert_kernel(std::uint64_t n, const unsigned long long* __restrict__ n_mid,
+                           const std::uint32_t* __restrict__ mid_list,
+                           const std::uint32_t* __restrict__ seg,
+                           const std::uint32_t* __restrict__ exs, DeltaOut dout,
+                           const double* __restrict__ DX, unsigned long long* __restrict__ mid_keys,
+                           unsigned long long* __restrict__ fallbacks) {
+  pdl_wait();
+  constexpr int DG = E / 4, SL = 32 / DG;
+  static_assert(E % 4 == 0 && 32 % DG == 0 && DG <= 32, "mid_cert shape");
+  constexpr int kBatch = 8;  // occurrences per load round (2 x double2 each)
+  extern __shared__ __align__(16) unsigned char mcs[];
+  const unsigned lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  std::uint32_t* sx = reinterpret_cast<std::uint32_t*>(mcs) + std::size_t(wib) * kMidMaxSeg;
+  const int g = int(lane) % DG, s = int(lane) / DG;
+  const std::uint64_t NM = *n_mid;
+  if (mid_keys && blockIdx.x == 0 && threadIdx.x == 0 && NM) atomicAdd(mid_keys, NM);
+  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
+  const std::uint64_t nwarps = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (std::uint64_t it = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5; it < NM;
+       it += nwarps) {
+    const std::uint32_t u = mid_list[it];
+    const std::uint32_t p0 = seg[u], L = seg[u + 1] - p0;  // L <= kMidMaxSeg
+    for (std::uint32_t i = lane; i < L; i += 32) {
+      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sx + i));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(exs + p0 + i));
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    const std::uint32_t per = (L + SL - 1) / SL;
+    const std::uint32_t b0 = min(L, std::uint32_t(s) * per), b1 = min(L, b0 + per);
+    DD t[4];
+    double a[4], l[4], lam[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      t[c] = DD{0.0, 0.0};
+      a[c] = l[c] = lam[c] = 0.0;
+    }
+    for (std::uint32_t q = b0; q < b1; q += kBatch) {
+      double2 v[kBatch][2];
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        if (q + i < b1) {
+          const double2* row =
+              reinterpret_cast<const double2*>(DX + std::uint64_t(sx[q + i]) * E + 4 * g);
+          v[i][0] = row[0];
+          v[i][1] = row[1];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        if (q + i < b1) {
+          const double x[4] = {v[i][0].x, v[i][0].y, v[i][1].x, v[i][1].y};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            t[c] = dd_add(t[c], x[c]);
+            a[c] = __dadd_ru(a[c], fabs(x[c]));
+            l[c] = __dadd_rn(l[c], x[c]);
+            lam[c] = __dadd_ru(lam[c], fabs(l[c]));
+          }
+        }
+      }
+    }
+    // across the slices (lanes s*DG + g): exclusive prefix of the totals,
+    // then S (double-double), A and B (rounded up) to slice 0
+    float gv[4];
+    bool bad[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double tot = __dadd_rn(t[c].hi, t[c].lo);
+      double inc = tot;
+#pragma unroll
+      for (int o = DG; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (int(lane) >= o) inc = __dadd_rn(inc, y);
+      }
+      double O = __shfl_up_sync(0xFFFFFFFFu, inc, DG);
+      if (s == 0) O = 0.0;
+      double B = __dadd_ru(__dmul_ru(double(b1 - b0), fabs(O)), lam[c]);
+      DD S = t[c];
+      double A = a[c];
+#pragma unroll
+      for (int o = 16; o >= DG; o >>= 1) {
+        const DD y{__shfl_xor_sync(0xFFFFFFFFu, S.hi, o), __shfl_xor_sync(0xFFFFFFFFu, S.lo, o)};
+        S = dd_add(S, y);
+        A = __dadd_ru(A, __shfl_xor_sync(0xFFFFFFFFu, A, o));
+        B = __dadd_ru(B, __shfl_xor_sync(0xFFFFFFFFu, B, o));
+      }
+      bad[c] = !certify_f32(dd_value(S), B, A, L, per + 2 * SL, inv_n, &gv[c]);
+    }
+    if (s == 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int d = 4 * g + c;
+        if (bad[c]) {  // the in-order chain (the segment is in example order)
+          double acc = 0.0;
+          for (std::uint32_t k = 0; k < L; ++k) acc = __dadd_rn(acc, DX[std::uint64_t(sx[k]) * E + d]);
+          gv[c] = __double2float_rn(__dmul_rn(acc, inv_n));
+          if (fallbacks) atomicAdd(fallbacks, 1ull);
+        }
+        dout.grad(u, E, d, gv[c]);
+      }
+    }
+    __syncwarp();  // sx is the next key's
+  }
+}
+
 // ---- big segments (> kLongSeg occurrences): split over CTAs --------------
 //
 // Work item w = (big key, chunk of fuse_chunk(E) occurrences). big_plan:
@@ -1033,24 +1294,19 @@ __global__ void big_plan_kernel(int chunk, const std::uint32_t* __restrict__ big
   if ((threadIdx.x & 31) == 0 && occ) atomicAdd(big_occ, occ);
 }
 
-// Acquire load (gpu scope): later loads of this thread observe what the
-// releasing writer published before the flag.
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // ---- big segments: one fused kernel ---------------------------------------
 //
 // Work items (key, chunk) are taken in ticket order. A CTA loads its chunk's
-// values once into registers (kFusePer per thread and dimension), publishes
-// the chunk's per-dimension Neumaier total (flag), takes its prefix offset
-// from the totals of the key's earlier chunks (they hold earlier tickets, so
-// they are running or done and publish before they wait: no deadlock, no
-// serial chain), then computes its share of B from the same registers. The
-// key's last CTA combines all chunks and certifies (certify_f32), recomputing
-// the exact chain for any uncertified dimension.
+// values once into registers (kFusePer per thread and dimension), forms the
+// chunk's per-dimension Neumaier total, sum|x| and Lambda = sum of |prefix
+// inside the chunk| (slice offsets from shared memory), publishes them, and
+// counts itself done for the key. No CTA waits for another: the key's last
+// CTA scans the chunk totals in order (O_c), bounds B = sum_c (cnt_c |O_c| +
+// Lambda_c) >= sum_k |s_k| (|s_k| <= |O_c| + |lambda_k|), certifies
+// (certify_f32) and recomputes the exact chain for any uncertified
+// dimension. (Round 1 walked B from each chunk's exact offset, waiting on
+// the earlier chunks' published totals; the looser bound certifies as
+// reliably and removes that wait.)
 constexpr int kFuseThreads = 256;
 constexpr int kFusePer = 16;  // occurrences per slice of a chunk
 inline int fuse_chunk(int E) { return (kFuseThreads / E) * kFusePer; }
@@ -1064,7 +1320,7 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
                      const std::uint32_t* __restrict__ item_chunk,
                      const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
                      DeltaOut dout, const double* __restrict__ DX,
-                     ChunkSum* __restrict__ chunk_tot, unsigned* __restrict__ flags,
+                     ChunkSum* __restrict__ chunk_tot,
                      unsigned long long* __restrict__ ticket, unsigned* __restrict__ key_done,
                      unsigned long long* __restrict__ fallbacks) {
   pdl_wait();
@@ -1221,34 +1477,12 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
       cs.lo = ct.lo;
       cs.a = ca;
     }
-    __syncthreads();
-    // one release after the barrier covers every writer of the block
-    // (cumulativity), instead of a fence per writer
-    if (threadIdx.x == 0) {
-      __threadfence();
-      *reinterpret_cast<volatile unsigned*>(&flags[w]) = 1u;
-    }
     if (worker) {
-      // offset: the key's earlier chunks' totals in chunk order, then this
-      // chunk's earlier slices
+      // the prefix inside the chunk: this chunk's earlier slices, then the
+      // slice's own running sum. The earlier chunks enter only through
+      // cnt x |their total| in the last CTA (|s_k| <= |O_c| + |lambda_k|):
+      // no CTA waits for another
       DD off{0.0, 0.0};
-      // every earlier chunk's total published (flags polled 4 at a time),
-      // one fence, then their totals with plain loads, added in chunk order
-      for (std::uint32_t g0 = 0; g0 < c; g0 += 4) {
-        bool ready;
-        do {
-          ready = true;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (g0 + q < c) ready &= ld_acquire_u32(&flags[w0 + g0 + q]) != 0u;
-          if (!ready) __nanosleep(32);
-        } while (!ready);
-      }
-#pragma unroll 4
-      for (std::uint32_t cc = 0; cc < c; ++cc) {
-        const double* bp = reinterpret_cast<const double*>(&chunk_tot[(w0 + cc) * E + d]);
-        off = dd_add(off, DD{__ldcg(bp), __ldcg(bp + 1)});
-      }
       for (int q = 0; q < s; ++q) off = dd_add(off, DD{sh[q * E + d], sl[q * E + d]});
       const double o = dd_value(off);
       double l = 0.0, b = 0.0;
@@ -1262,7 +1496,7 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
       sb[threadIdx.x] = b;
     }
     __syncthreads();
-    if (int(threadIdx.x) < E) {  // this chunk's B bound per dimension
+    if (int(threadIdx.x) < E) {  // this chunk's Lambda (in-chunk prefixes) per dimension
       double cb = 0.0;
       for (int q = 0; q < slices; ++q) cb = __dadd_ru(cb, sb[q * E + threadIdx.x]);
       chunk_tot[w * E + threadIdx.x].b = cb;
@@ -1279,14 +1513,19 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
     if (!s_last) continue;
     float g = 0.0f;
     if (int(threadIdx.x) < E) {
+      // S, A; B = sum_c (cnt_c |O_c| + Lambda_c), O_c = the chunks before c
       DD S{0.0, 0.0};
-      double A = 0.0, B = 0.0;
+      double A = 0.0, B = 0.0, O = 0.0;
 #pragma unroll 4
       for (std::uint32_t cc = 0; cc < nch; ++cc) {
         const double* bp = reinterpret_cast<const double*>(&chunk_tot[(w0 + cc) * E + threadIdx.x]);
-        S = dd_add(S, DD{__ldcg(bp), __ldcg(bp + 1)});
+        const double hi = __ldcg(bp), lo = __ldcg(bp + 1);
+        const std::uint32_t q0 = k0 + cc * std::uint32_t(chunk);
+        const std::uint32_t cnt_c = min(k1 - q0, std::uint32_t(chunk));
+        S = dd_add(S, DD{hi, lo});
         A = __dadd_ru(A, __ldcg(bp + 2));
-        B = __dadd_ru(B, __ldcg(bp + 3));
+        B = __dadd_ru(B, __dadd_ru(__dmul_ru(double(cnt_c), fabs(O)), __ldcg(bp + 3)));
+        O = __dadd_rn(O, __dadd_rn(hi, lo));
       }
       bad[threadIdx.x] = !certify_f32(dd_value(S), B, A, k1 - k0, (k1 - k0) + slices + nch,
                                       inv_n, &g);
@@ -1312,156 +1551,6 @@ __global__ void __launch_bounds__(kFuseThreads, 3)
     if (int(threadIdx.x) < E)
       dout.grad(u, E, int(threadIdx.x), g);
     __syncthreads();
-  }
-}
-
-// ---- big segments: one CTA per key --------------------------------------
-//
-// The alternative to big_fused_kernel's cross-CTA chunks (HPS_BIG=key, the
-// default): one 1024-thread CTA owns a key, so nothing crosses CTAs — no
-// flags, no fences, no polling. Thread (s, d) takes slice s (kBigPer
-// consecutive occurrences of the key's ordered segment) of dimension d per
-// chunk of slices x kBigPer occurrences, holds its values in registers and
-//   1. adds them into its Neumaier total (S) and sum|x| (A), and publishes
-//      the slice total;
-//   2. takes its offset = the running total of the earlier chunks + the
-//      earlier slices' totals (one f64 chain in slice order; its error is
-//      within the (m + slices) u A term of certify_f32), and adds |offset +
-//      in-slice prefix| into its share of B;
-// the last slice carries the running total to the next chunk. After the
-// last chunk a tree over the slices combines S (double-double), A and B
-// (rounded up), and certify_f32 decides each dimension exactly as for
-// big_fused_kernel; an uncertified dimension recomputes the in-order chain.
-constexpr int kBigThreads = 1024;
-constexpr int kBigPer = 16;  // occurrences per thread and chunk (in registers)
-
-__host__ __device__ constexpr int big_slices(int E) { return kBigThreads / E; }
-__host__ __device__ constexpr std::size_t big_smem(int E) {
-  return (std::size_t(5) * big_slices(E) * E + E) * 8;
-}
-
-__global__ void __launch_bounds__(kBigThreads, 1)
-    big_key_kernel(int E, std::uint64_t n, const std::uint32_t* __restrict__ big_list,
-                   const unsigned long long* __restrict__ n_big,
-                   const std::uint32_t* __restrict__ seg, const std::uint32_t* __restrict__ exs,
-                   DeltaOut dout, const double* __restrict__ DX,
-                   unsigned long long* __restrict__ fallbacks,
-                   unsigned long long* __restrict__ big_keys,
-                   unsigned long long* __restrict__ max_chunks,
-                   unsigned long long* __restrict__ big_occ) {
-  pdl_wait();
-  extern __shared__ double bk[];
-  __shared__ bool bad[256];
-  const int slices = kBigThreads / E, SE = slices * E;
-  double* sh = bk;       // [slices][E] this chunk's slice totals
-  double* rt = sh + SE;  // [E] running total of the earlier chunks
-  double* r0 = rt + E;   // [slices][E] the final tree: S.hi, S.lo, A, B
-  double* r1 = r0 + SE;
-  double* r2 = r1 + SE;
-  double* r3 = r2 + SE;
-  const int s = int(threadIdx.x) / E, d = int(threadIdx.x) - s * E;
-  const bool worker = s < slices;
-  const std::uint32_t chunk = std::uint32_t(slices) * kBigPer;
-  const std::uint64_t NB = *n_big;
-  const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && NB) atomicAdd(big_keys, (unsigned long long)NB);
-  for (std::uint64_t ki = blockIdx.x; ki < NB; ki += gridDim.x) {
-    const std::uint32_t u = big_list[ki];
-    const std::uint32_t k0 = seg[u], k1 = seg[u + 1];
-    const std::uint32_t nch = (k1 - k0 + chunk - 1) / chunk;
-    if (threadIdx.x == 0) {
-      atomicAdd(big_occ, (unsigned long long)(k1 - k0));
-      atomicMax(max_chunks, (unsigned long long)nch);
-    }
-    if (int(threadIdx.x) < E) rt[threadIdx.x] = 0.0;
-    DD S{0.0, 0.0};
-    double A = 0.0, B = 0.0;
-    for (std::uint32_t c = 0; c < nch; ++c) {
-      const std::uint32_t a0 = k0 + c * chunk + std::uint32_t(s) * kBigPer;
-      const int cnt = worker && a0 < k1 ? int(min(k1 - a0, std::uint32_t(kBigPer))) : 0;
-      double x[kBigPer];
-      {
-        std::uint32_t e[kBigPer];
-#pragma unroll
-        for (int i = 0; i < kBigPer; ++i) e[i] = i < cnt ? exs[a0 + i] : 0u;
-#pragma unroll
-        for (int i = 0; i < kBigPer; ++i) x[i] = i < cnt ? DX[std::uint64_t(e[i]) * E + d] : 0.0;
-      }
-      DD t{0.0, 0.0};
-#pragma unroll
-      for (int i = 0; i < kBigPer; ++i)
-        if (i < cnt) {
-          t = dd_add(t, x[i]);
-          A = __dadd_ru(A, fabs(x[i]));
-        }
-      S = dd_add(S, t);
-      if (worker) sh[s * E + d] = dd_value(t);
-      __syncthreads();
-      double o = 0.0;
-      if (worker) {
-        o = rt[d];
-        for (int q = 0; q < s; ++q) o = __dadd_rn(o, sh[q * E + d]);
-        double l = 0.0;
-#pragma unroll
-        for (int i = 0; i < kBigPer; ++i)
-          if (i < cnt) {
-            l = __dadd_rn(l, x[i]);
-            B = __dadd_ru(B, fabs(__dadd_rn(o, l)));
-          }
-      }
-      __syncthreads();  // every offset read rt before the last slice moves it
-      if (worker && s == slices - 1) rt[d] = __dadd_rn(o, sh[s * E + d]);
-    }
-    if (worker) {
-      r0[s * E + d] = S.hi;
-      r1[s * E + d] = S.lo;
-      r2[s * E + d] = A;
-      r3[s * E + d] = B;
-    }
-    __syncthreads();
-    int h = 1;
-    while (h < slices) h <<= 1;
-    for (h >>= 1; h >= 1; h >>= 1) {
-      if (worker && s < h && s + h < slices) {
-        const int i = s * E + d, j = (s + h) * E + d;
-        const DD a = dd_add(DD{r0[i], r1[i]}, DD{r0[j], r1[j]});
-        r0[i] = a.hi;
-        r1[i] = a.lo;
-        r2[i] = __dadd_ru(r2[i], r2[j]);
-        r3[i] = __dadd_ru(r3[i], r3[j]);
-      }
-      __syncthreads();
-    }
-    float g = 0.0f;
-    if (int(threadIdx.x) < E) {
-      const std::uint32_t m = k1 - k0;
-      bad[threadIdx.x] = !certify_f32(dd_value(DD{r0[threadIdx.x], r1[threadIdx.x]}),
-                                      r3[threadIdx.x], r2[threadIdx.x], m,
-                                      // offsets: slices x nch terms; S: <= 2 slices (nch + 1)
-                                      // double-double adds beyond the n terms
-                                      std::uint64_t(m) + 2 * std::uint64_t(slices) * (nch + 1) + nch,
-                                      inv_n, &g);
-    }
-    __syncthreads();
-    double* stage = r0;  // the tree is read: SE doubles of staging
-    for (int dd = 0; dd < E; ++dd) {
-      if (!bad[dd]) continue;
-      double acc = 0.0;
-      for (std::uint32_t cs0 = k0; cs0 < k1; cs0 += std::uint32_t(SE)) {
-        const int mm = int(min(k1 - cs0, std::uint32_t(SE)));
-        for (int j = threadIdx.x; j < mm; j += kBigThreads)
-          stage[j] = DX[std::uint64_t(exs[cs0 + j]) * E + dd];
-        __syncthreads();
-        if (int(threadIdx.x) == dd) acc = chain_sum(stage, mm, acc);
-        __syncthreads();
-      }
-      if (int(threadIdx.x) == dd) {
-        g = __double2float_rn(__dmul_rn(acc, inv_n));
-        if (fallbacks) atomicAdd(fallbacks, 1ull);
-      }
-    }
-    if (int(threadIdx.x) < E) dout.grad(u, E, int(threadIdx.x), g);
-    __syncthreads();  // shared memory is the next key's
   }
 }
 

@@ -251,8 +251,9 @@ struct Tier {
   cudaEvent_t fork4 = nullptr, join4 = nullptr;
   int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
   std::uint32_t mid_max = 512;          // medium segments: kLongSeg < length <= mid_max
+  bool mid_cert = true;  // medium segments certified (HPS_MID_CERT=0: exact warp chains)
+  bool dg_fused = true;  // dense gradient in one launch (HPS_DG_FUSED=0: four launches)
   bool fb_tile = true;  // fwd/bwd embed_sum through shared-memory row tiles (HPS_FB_TILE=0: off)
-  bool big_key = true;  // longer segments: one CTA per key (HPS_BIG=fused: chunks over CTAs)
                                         // (HPS_MID_SEG; kLongSeg disables the path)
   Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
                                         // 2..: the next batch's mini-batch groupings
@@ -333,7 +334,6 @@ struct Tier {
                 *orank = nullptr,
                 *key_done = nullptr;
   ChunkSum* chunk_tot = nullptr;
-  unsigned* fuse_flags = nullptr;          // big_fused_kernel: chunk total published
   std::uint32_t *item_key = nullptr, *item_chunk = nullptr;  // item -> (big key, chunk)
   unsigned long long* fuse_ticket = nullptr;
   std::uint64_t fuse_items = 0;
@@ -369,6 +369,7 @@ struct Tier {
   float* wP = nullptr;
   std::uint64_t wP_cap = 0;
   double *dg_off = nullptr, *dg_tot = nullptr;  // dense-grad slice offsets, totals
+  unsigned* dg_sync = nullptr;  // dense_grad_fused_kernel: per weight group, CTAs counted
   float *dense = nullptr, *dgrad = nullptr;
 
   // value store (MEM-PS stand-in)
@@ -1274,12 +1275,10 @@ static hps_status launch_big_plan(Tier* t, std::uint64_t u_upper, const std::uin
   HPS_CUDA(cudaMemsetAsync(&t->dsc->n_mid, 0, 8, bs));
   launch_on(t, bs, big_classify_kernel, grid_for(std::max<std::uint64_t>(u_upper, 1)), 256, 0,
             U, seg, t->big_list, nb, t->mid_max, t->mid_list, &t->dsc->n_mid);
-  if (t->big_key) return HPS_OK;  // big_key_kernel plans nothing
   launch_on(t, bs, big_plan_kernel, 1, 1024, 0, fuse_chunk(t->E),
             (const std::uint32_t*)t->big_list, (const unsigned long long*)nb, seg, t->chunk_off,
             &t->dsc->n_items, t->item_key, t->item_chunk, &t->dsc->big_keys, &t->dsc->max_chunks,
             &t->dsc->big_occ);
-  HPS_CUDA(cudaMemsetAsync(t->fuse_flags, 0, t->fuse_items * 4, bs));
   HPS_CUDA(cudaMemsetAsync(t->fuse_ticket, 0, 8, bs));
   return HPS_OK;
 }
@@ -1307,7 +1306,15 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
     HPS_CUDA(cudaEventRecord(t->fork4, bs));
     HPS_CUDA(cudaStreamWaitEvent(ms, t->fork4, 0));
   }
-  if (t->mid_max > std::uint32_t(kLongSeg)) {
+  const bool mid_cert = t->mid_cert && (E == 4 || E == 8 || E == 16 || E == 32);
+  if (t->mid_max > std::uint32_t(kLongSeg) && mid_cert) {
+    auto mk = E == 4 ? sparse_mid_cert_kernel<4>
+                     : (E == 8 ? sparse_mid_cert_kernel<8>
+                               : (E == 16 ? sparse_mid_cert_kernel<16> : sparse_mid_cert_kernel<32>));
+    launch_on(t, ms, mk, kSMs * 2, 32 * kMidCertWarps, mid_cert_smem(), n,
+              (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
+              exs, dout, DX, &t->dsc->mid_keys, &t->dsc->fallbacks);
+  } else if (t->mid_max > std::uint32_t(kLongSeg)) {
     const int rpi = E <= 8 ? 4 : (E <= 16 ? 2 : 1);
     auto mk = rpi == 4 ? sparse_mid_kernel<4> : (rpi == 2 ? sparse_mid_kernel<2> : sparse_mid_kernel<1>);
     launch_on(t, ms, mk, kSMs * 4, 32 * kMidWarps, mid_smem(rpi), E, n,
@@ -1316,18 +1323,11 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   }
   if (t->big_side) HPS_CUDA(cudaEventRecord(t->join4, ms));
   mark_big(t, -1);
-  if (t->big_key)
-    launch_on(t, bs, big_key_kernel, kSMs, kBigThreads, big_smem(E), E, n,
-              (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big, seg,
-              exs, dout, DX, &t->dsc->fallbacks, &t->dsc->big_keys, &t->dsc->max_chunks,
-              &t->dsc->big_occ);
-  else
-    launch_on(t, bs, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
-              (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big,
-              (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
-              (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs,
-              dout, DX, t->chunk_tot, t->fuse_flags, t->fuse_ticket, t->key_done,
-              &t->dsc->fallbacks);
+  launch_on(t, bs, big_fused_kernel, kSMs * 4, kFuseThreads, 0, E, lr, n,
+            (const std::uint32_t*)t->big_list, (const unsigned long long*)&t->dsc->n_big,
+            (const std::uint32_t*)t->chunk_off, (const unsigned long long*)&t->dsc->n_items,
+            (const std::uint32_t*)t->item_key, (const std::uint32_t*)t->item_chunk, seg, exs,
+            dout, DX, t->chunk_tot, t->fuse_ticket, t->key_done, &t->dsc->fallbacks);
   mark_big(t, HPS_T_BIGFUSED);
   HPS_CUDA(cudaEventRecord(t->join3, bs));
   // DPT dims per thread: 4 when E allows 32-byte row loads (8 measured 1-2%
@@ -1959,6 +1959,12 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
       // dense-grad reduce on the side stream, overlapping the sparse reduce
       HPS_CUDA(cudaEventRecord(T->fork, T->st));
       HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
+      if (T->dg_fused) {
+        launch_on(T, T->st2, dense_grad_fused_kernel,
+                  dim3(dense_grad_groups(T->md), kDGSlices / kDGFWarps), 32 * kDGFWarps, 0, T->md, n,
+                  (const double*)T->H, (const double*)T->DL, T->dpart, T->dg_sync, T->dgrad,
+                  &T->dsc->fallbacks);
+      } else {
       launch_on(T, T->st2, dense_grad_p1_kernel, dim3(dense_grad_groups(T->md), kDGSlices), 32,
                 0, T->md, n, (const double*)T->H, (const double*)T->DL, T->dpart);
       launch_on(T, T->st2, dense_grad_scan_kernel, unsigned((T->md.nw + 3) / 4), 128, 0, T->md,
@@ -1970,6 +1976,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                 unsigned((T->md.nw + kDGFinWarps - 1) / kDGFinWarps), 32 * kDGFinWarps, 0, T->md,
                 n, (const double*)T->H, (const double*)T->DL, (const double*)T->dpart,
                 (const double*)T->dg_tot, T->dgrad, &T->dsc->fallbacks);
+      }
       HPS_CUDA(cudaEventRecord(T->join, T->st2));
       }
       if (T->big_side) HPS_CUDA(cudaStreamWaitEvent(T->st3, T->fork, 0));  // after fwd/bwd
@@ -2676,8 +2683,9 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     t->prep_mbs = std::max(0, std::atoi(v));
   if (const char* v = std::getenv("HPS_PRIO")) t->priorities = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_BIG_SIDE")) t->big_side = std::atoi(v) != 0;
-  if (const char* v = std::getenv("HPS_BIG")) t->big_key = std::strcmp(v, "fused") != 0;
   if (const char* v = std::getenv("HPS_FB_TILE")) t->fb_tile = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_DG_FUSED")) t->dg_fused = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_MID_CERT")) t->mid_cert = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_SHORT_DPT")) {
     const int d = std::atoi(v);
     if (d == 1 || (d == 4 && c.embedding_dim % 4 == 0) || (d == 8 && c.embedding_dim % 8 == 0))
@@ -2945,7 +2953,6 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   // fused big-segment items: one per (key, chunk of fuse_chunk(E) occurrences)
   t->fuse_items = S / std::uint64_t(fuse_chunk(int(E))) + S / (kLongSeg + 1) + 2;
   A(chunk_tot, t->fuse_items * E);
-  A(fuse_flags, t->fuse_items);
   A(item_key, t->fuse_items);
   A(item_chunk, t->fuse_items);
   A(fuse_ticket, 1);
@@ -2980,6 +2987,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     A(dpart, std::uint64_t(t->md.nw) * kDGSlices * 4);
     A(dg_off, std::uint64_t(t->md.nw) * kDGSlices);
     A(dg_tot, std::uint64_t(t->md.nw) * 4);
+    A(dg_sync, dense_grad_groups(t->md));
   }
   A(dense, t->md.nw);
   A(dgrad, t->md.nw);
@@ -2989,6 +2997,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     cudaMemsetAsync(g.part_n, 0, std::uint64_t(kGroupParts) * kGroupPartStride * 4, t->st);
   }
   cudaMemsetAsync(t->key_done, 0, (S / (kLongSeg + 1) + 2) * 4, t->st);
+  if (t->dg_sync) cudaMemsetAsync(t->dg_sync, 0, dense_grad_groups(t->md) * 4, t->st);
   if ((e = cudaMemsetAsync(t->dsc, 0, sizeof(Scalars), t->st)) != cudaSuccess)
     return fail(set_error(HPS_ERR_CUDA, "cuda: memset: %s", cudaGetErrorString(e)));
   t->hsc->rq_capv = t->rq_cap;

@@ -45,18 +45,9 @@ def max_segment(off, keys, B, J):
     return int(c.max())
 
 
-def big_chunk(E, big):
-    """Occurrences per chunk of the long-segment kernels: big_key_kernel
-    (HPS_BIG=key: 1024 threads, one CTA per key) and big_fused_kernel
-    (HPS_BIG=fused: 256 threads, chunks over CTAs); 16 per thread."""
-    return ((1024 if big == "key" else 256) // E) * 16
-
-
-@pytest.mark.parametrize("store_kind,big", [("host", "key"), ("device", "key"),
-                                            ("host", "fused")])
-def test_config2_full_size_bit_exact(pkg, oracle, monkeypatch, store_kind, big):
+@pytest.mark.parametrize("store_kind", ["host", "device"])
+def test_config2_full_size_bit_exact(pkg, oracle, store_kind):
     import torch
-    monkeypatch.setenv("HPS_BIG", big)
     dims, E, B, nnz, J, layers, nb = 10**7, 16, 16384, 100, 4, (8, 16, 1), 3
     off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=1)
     tier = pkg.Tier(width=E, layer_dims=layers, minibatches=J, key_space=dims,
@@ -79,12 +70,12 @@ def test_config2_full_size_bit_exact(pkg, oracle, monkeypatch, store_kind, big):
     if store_kind == "device":
         torch.cuda.synchronize()
         store = dstore.cpu().numpy()
-    # the data makes segments of > 15 x 256 occurrences ...
+    # the data makes ~16-chunk segments (fuse_chunk(16) = 256 occurrences)...
     seg = max_segment(off, keys, B, J)
     assert seg > 15 * 256, seg
-    # ... and the device took them on the long-segment path, in chunks
+    # ... and the device planned them
     assert all(s.big_segments > 0 for s in stats)
-    assert max(s.max_segment_chunks for s in stats) >= -(-(15 * 256 + 1) // big_chunk(E, big))
+    assert max(s.max_segment_chunks for s in stats) >= 16
     wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, layers, J=J), B, off, keys, lab)
     assert np.array_equal(dense, wd), np.abs(dense - wd).max()
     got = store[wk.astype(np.int64)]
@@ -92,12 +83,10 @@ def test_config2_full_size_bit_exact(pkg, oracle, monkeypatch, store_kind, big):
     assert bad.size == 0, f"{bad.size} rows differ, e.g. key {wk[bad[0]]}"
 
 
-@pytest.mark.parametrize("big", ["key", "fused"])
 @pytest.mark.parametrize("E,B,nnz,chunks", [(16, 4096, 20, 2), (8, 2048, 30, 1), (64, 1024, 20, 2)])
 def test_forced_certificate_failure_takes_exact_fallbacks(pkg, oracle, monkeypatch, E, B, nnz,
-                                                          chunks, big):
+                                                          chunks):
     monkeypatch.setenv("HPS_CERT_FORCE_FAIL", "1")
-    monkeypatch.setenv("HPS_BIG", big)
     monkeypatch.setenv("HPS_MID_SEG", "32")  # every long segment on the certified path
     dims, J, layers, nb = 20000, 4, (8, 16, 1), 3
     off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=17)
@@ -114,22 +103,49 @@ def test_forced_certificate_failure_takes_exact_fallbacks(pkg, oracle, monkeypat
     # took the exact chain
     assert all(s.exact_fallbacks >= s.big_segments * E for s in stats)
     assert all(s.big_segments > 0 for s in stats)
-    # fused: chunks >= 2 takes the multi-CTA look-back path, 1 the single-CTA
-    # path; key: one CTA per key (its chunks run in turn)
-    if big == "fused":
-        assert max(s.max_segment_chunks for s in stats) >= chunks
+    # chunks >= 2: the multi-CTA path (last CTA combines), 1: the single-CTA path
+    assert max(s.max_segment_chunks for s in stats) >= chunks
     wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, layers, J=J), B, off, keys, lab)
     assert np.array_equal(dense, wd), np.abs(dense - wd).max()
     assert np.array_equal(store[wk.astype(np.int64)], wr)
 
 
+@pytest.mark.parametrize("E", [16, 8, 32])
+def test_forced_certificate_failure_on_the_medium_path(pkg, oracle, monkeypatch, E):
+    """Segments of 33..1024 occurrences on the certified warp reduce
+    (sparse_mid_cert_kernel) with every certificate failing: each such key's
+    E dimensions recompute the in-order chain, bit-exact."""
+    monkeypatch.setenv("HPS_CERT_FORCE_FAIL", "1")
+    monkeypatch.setenv("HPS_MID_SEG", "1024")
+    dims, B, nnz, J, layers, nb = 20000, 4096, 20, 4, (8, 16, 1), 2
+    off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=19)
+    tier = pkg.Tier(width=E, layer_dims=layers, minibatches=J, key_space=dims,
+                    max_batch_examples=B, max_batch_keys=max_keys_of(off, B))
+    store = np.zeros((dims, E), dtype=np.float32)
+    tier.attach_store(store)
+    stats = [tier.train_batch(o, k, l) for o, k, l in batches_of(off, keys, lab, B)]
+    tier.flush()
+    dense = tier.get_dense()
+    tier.close()
+    monkeypatch.delenv("HPS_CERT_FORCE_FAIL")
+    assert all(s.mid_segments > 0 for s in stats)
+    assert all(s.exact_fallbacks >= (s.mid_segments + s.big_segments) * E for s in stats)
+    wd, wk, wr = oracle.train_reference(make_cfg(1, 1, E, layers, J=J), B, off, keys, lab)
+    assert np.array_equal(dense, wd), np.abs(dense - wd).max()
+    assert np.array_equal(store[wk.astype(np.int64)], wr)
+
+
+@pytest.mark.parametrize("cert", ["1", "0"])
 @pytest.mark.parametrize("mid", ["32", "128", "1024", "100000"])
 @pytest.mark.parametrize("E", [4, 16, 64])
-def test_mid_segment_warp_chains_bit_exact(pkg, oracle, monkeypatch, mid, E):
-    """Segments of 33..HPS_MID_SEG occurrences are summed by one warp each in
-    the exact reference order (sparse_mid_kernel); longer ones by the chunked
-    certified reduce. Every split point gives the oracle's bits."""
+def test_mid_segment_warp_paths_bit_exact(pkg, oracle, monkeypatch, mid, E, cert):
+    """Segments of 33..HPS_MID_SEG occurrences take one warp each: certified
+    (sparse_mid_cert_kernel, E in {4, 8, 16, 32}) or, with HPS_MID_CERT=0 and
+    for other widths, the exact reference-order chain (sparse_mid_kernel);
+    longer ones the chunked certified reduce. Every split point gives the
+    oracle's bits."""
     monkeypatch.setenv("HPS_MID_SEG", mid)
+    monkeypatch.setenv("HPS_MID_CERT", cert)
     dims, B, J = 20000, 4096, 4
     off, keys, lab = pkg.gen_dataset(dims, 2 * B, 20, zipf=True, seed=29)
     tier = pkg.Tier(width=E, minibatches=J, key_space=dims, max_batch_examples=B,

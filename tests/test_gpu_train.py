@@ -328,15 +328,31 @@ def test_hbm_store_grouping_split_bit_exact(pkg, oracle, monkeypatch, J, prep_gr
     assert np.array_equal(store[wk.astype(np.int64)], wr)
 
 
-@pytest.mark.parametrize("slack", ["-1", "8", "29"])
+@pytest.mark.parametrize("tile,slack", [("1", "29"), ("0", "-1"), ("0", "8"), ("0", "29")])
 @pytest.mark.parametrize("E,nnz", [(8, 20), (16, 100)])
-def test_embed_sum_order_free_and_fallback_bit_exact(pkg, oracle, monkeypatch, slack, E, nnz):
-    """fwd/bwd's embed_sum takes the order-free path (whole rows per lane,
-    recursive halving) only where the f64 sum is exact in any order
-    (model.cuh embed_sum_exact); HPS_EMBED_SLACK tightens the bound so the
-    in-order fallback runs for all (-1) or part (8) of the examples, mixed
-    within one mini-batch, against the same oracle."""
+def test_embed_sum_paths_bit_exact(pkg, oracle, monkeypatch, tile, slack, E, nnz):
+    """fwd/bwd's embed_sum: the default streams the rows through shared-memory
+    tiles and chains each dimension in feature order (model.cuh
+    embed_sum_tiled); HPS_FB_TILE=0 takes the register path, whose order-free
+    branch (whole rows per lane, recursive halving; embed_sum_exact) runs
+    only where the f64 sum is exact in any order — HPS_EMBED_SLACK tightens
+    that bound so the in-order fallback runs for all (-1) or part (8) of the
+    examples, mixed within one mini-batch. All against the same oracle."""
+    monkeypatch.setenv("HPS_FB_TILE", tile)
     monkeypatch.setenv("HPS_EMBED_SLACK", slack)
     dims, B = 30000, 512
     off, keys, lab = pkg.gen_dataset(dims, B * 3, nnz, zipf=True, seed=11)
     check_bit_exact(oracle, pkg, off, keys, lab, B, E=E, layers=(8, 16, 1), J=4, dims=dims)
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("E,J", [(8, 4), (16, 1)])
+def test_dense_grad_paths_bit_exact(pkg, oracle, monkeypatch, fused, E, J):
+    """The certified dense-gradient reduce: one launch and one pass (slices
+    publish T, A and Lambda; the weight group's last CTA bounds B from the
+    ordered slice totals; dense_grad_fused_kernel) or four launches with the
+    offset walk (HPS_DG_FUSED=0); both bit-exact against the oracle."""
+    monkeypatch.setenv("HPS_DG_FUSED", fused)
+    dims, B = 30000, 2048
+    off, keys, lab = pkg.gen_dataset(dims, B * 2, 40, zipf=True, seed=23)
+    check_bit_exact(oracle, pkg, off, keys, lab, B, E=E, layers=(8, 16, 1), J=J, dims=dims)
