@@ -870,7 +870,8 @@ __device__ __forceinline__ void warp_append(bool pick, std::uint32_t u, std::uin
 __global__ void __launch_bounds__(256)
     big_classify_kernel(const std::uint64_t* __restrict__ u_ptr,
                         const std::uint32_t* __restrict__ seg, std::uint32_t* __restrict__ big_list,
-                        unsigned long long* __restrict__ n_big, std::uint32_t mid_max,
+                        unsigned long long* __restrict__ n_big, std::uint32_t short_max,
+                        std::uint32_t mid_max,
                         std::uint32_t* __restrict__ mid_list, unsigned long long* __restrict__ n_mid) {
   pdl_wait();
   const std::uint64_t U = *u_ptr;
@@ -882,7 +883,7 @@ __global__ void __launch_bounds__(256)
     const std::uint64_t u = b + lane;
     const std::uint32_t len = u < U ? seg[u + 1] - seg[u] : 0u;
     warp_append(len > mid_max, std::uint32_t(u), big_list, n_big, lane);
-    warp_append(len > std::uint32_t(kLongSeg) && len <= mid_max, std::uint32_t(u), mid_list, n_mid,
+    warp_append(len > short_max && len <= mid_max, std::uint32_t(u), mid_list, n_mid,
                 lane);
   }
 }
@@ -922,13 +923,13 @@ __device__ __forceinline__ void write_delta(const DeltaOut& o, std::uint64_t u, 
 // does not add two more dependent round trips after it.
 template <int DPT>
 __global__ void __launch_bounds__(256)
-    sparse_short_kernel(int E, float lr, std::uint64_t n, const std::uint64_t* __restrict__ u_ptr,
+    sparse_short_kernel(int E, std::uint32_t short_max, std::uint64_t n,
+                        const std::uint64_t* __restrict__ u_ptr,
                         const std::uint32_t* __restrict__ seg,
                         const std::uint32_t* __restrict__ exs, DeltaOut dout,
                         const double* __restrict__ DX,
                         unsigned long long* __restrict__ pulled) {
   pdl_wait();
-  (void)lr;
   const std::uint64_t U = *u_ptr;
   if (pulled && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(pulled, (unsigned long long)U);
   const double inv_n = n == 0 ? 0.0 : 1.0 / double(n);
@@ -945,7 +946,7 @@ __global__ void __launch_bounds__(256)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
     }
     const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
-    if (p1 - p0 > std::uint32_t(kLongSeg)) continue;
+    if (p1 - p0 > short_max) continue;
     double acc[DPT];
 #pragma unroll
     for (int i = 0; i < DPT; ++i) acc[i] = 0.0;

@@ -250,7 +250,8 @@ struct Tier {
   cudaStream_t st4 = nullptr;           // side stream: the medium segments (sparse_mid_kernel)
   cudaEvent_t fork4 = nullptr, join4 = nullptr;
   int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
-  std::uint32_t mid_max = 512;          // medium segments: kLongSeg < length <= mid_max
+  std::uint32_t mid_max = 512;          // medium segments: short_max < length <= mid_max
+  std::uint32_t short_max = 32;         // short segments (thread chains): length <= short_max
   bool mid_cert = true;  // medium segments certified (HPS_MID_CERT=0: exact warp chains)
   bool dg_fused = true;  // dense gradient in one launch (HPS_DG_FUSED=0: four launches)
   bool fb_tile = true;  // fwd/bwd embed_sum through shared-memory row tiles (HPS_FB_TILE=0: off)
@@ -1274,7 +1275,7 @@ static hps_status launch_big_plan(Tier* t, std::uint64_t u_upper, const std::uin
   HPS_CUDA(cudaMemsetAsync(nb, 0, 8, bs));
   HPS_CUDA(cudaMemsetAsync(&t->dsc->n_mid, 0, 8, bs));
   launch_on(t, bs, big_classify_kernel, grid_for(std::max<std::uint64_t>(u_upper, 1)), 256, 0,
-            U, seg, t->big_list, nb, t->mid_max, t->mid_list, &t->dsc->n_mid);
+            U, seg, t->big_list, nb, t->short_max, t->mid_max, t->mid_list, &t->dsc->n_mid);
   launch_on(t, bs, big_plan_kernel, 1, 1024, 0, fuse_chunk(t->E),
             (const std::uint32_t*)t->big_list, (const unsigned long long*)nb, seg, t->chunk_off,
             &t->dsc->n_items, t->item_key, t->item_chunk, &t->dsc->big_keys, &t->dsc->max_chunks,
@@ -1307,14 +1308,14 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
     HPS_CUDA(cudaStreamWaitEvent(ms, t->fork4, 0));
   }
   const bool mid_cert = t->mid_cert && (E == 4 || E == 8 || E == 16 || E == 32);
-  if (t->mid_max > std::uint32_t(kLongSeg) && mid_cert) {
+  if (t->mid_max > t->short_max && mid_cert) {
     auto mk = E == 4 ? sparse_mid_cert_kernel<4>
                      : (E == 8 ? sparse_mid_cert_kernel<8>
                                : (E == 16 ? sparse_mid_cert_kernel<16> : sparse_mid_cert_kernel<32>));
     launch_on(t, ms, mk, kSMs * 2, 32 * kMidCertWarps, mid_cert_smem(), n,
               (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
               exs, dout, DX, &t->dsc->mid_keys, &t->dsc->fallbacks);
-  } else if (t->mid_max > std::uint32_t(kLongSeg)) {
+  } else if (t->mid_max > t->short_max) {
     const int rpi = E <= 8 ? 4 : (E <= 16 ? 2 : 1);
     auto mk = rpi == 4 ? sparse_mid_kernel<4> : (rpi == 2 ? sparse_mid_kernel<2> : sparse_mid_kernel<1>);
     launch_on(t, ms, mk, kSMs * 4, 32 * kMidWarps, mid_smem(rpi), E, n,
@@ -1336,7 +1337,7 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   auto sk = dpt == 8 ? sparse_short_kernel<8>
                      : (dpt == 4 ? sparse_short_kernel<4> : sparse_short_kernel<1>);
   launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,
-         E, lr, n, U, seg, exs, dout, DX, &t->dsc->pulled);
+         E, t->short_max, n, U, seg, exs, dout, DX, &t->dsc->pulled);
   HPS_CUDA(cudaStreamWaitEvent(t->st, t->join3, 0));
   if (t->big_side) HPS_CUDA(cudaStreamWaitEvent(t->st, t->join4, 0));
   return HPS_OK;
@@ -2693,6 +2694,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   }
   if (const char* v = std::getenv("HPS_MID_SEG"))
     t->mid_max = std::uint32_t(std::min(kMidMaxSeg, std::max(kLongSeg, std::atoi(v))));
+  if (const char* v = std::getenv("HPS_SHORT_SEG"))
+    t->short_max = std::uint32_t(std::min(kLongSeg, std::max(1, std::atoi(v))));
   if (const char* v = std::getenv("HPS_FOLD_WAIT")) t->fold_wait = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_XFUSE")) t->xfuse = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_XPREP")) t->xprep = std::atoi(v) != 0;
@@ -2947,7 +2950,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   }
   A(otot, kMaxRanks);
   A(big_list, S / (kLongSeg + 1) + 2);
-  A(mid_list, S / (kLongSeg + 1) + 2);
+  A(mid_list, S / 2 + 2);  // keys longer than short_max >= 1
   A(chunk_off, S / (kLongSeg + 1) + 3);
   A(key_done, S / (kLongSeg + 1) + 2);
   // fused big-segment items: one per (key, chunk of fuse_chunk(E) occurrences)

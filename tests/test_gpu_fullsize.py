@@ -87,7 +87,8 @@ def test_config2_full_size_bit_exact(pkg, oracle, store_kind):
 def test_forced_certificate_failure_takes_exact_fallbacks(pkg, oracle, monkeypatch, E, B, nnz,
                                                           chunks):
     monkeypatch.setenv("HPS_CERT_FORCE_FAIL", "1")
-    monkeypatch.setenv("HPS_MID_SEG", "32")  # every long segment on the certified path
+    monkeypatch.setenv("HPS_SHORT_SEG", "32")  # every segment > 32 on the chunked path
+    monkeypatch.setenv("HPS_MID_SEG", "32")
     dims, J, layers, nb = 20000, 4, (8, 16, 1), 3
     off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=17)
     tier = pkg.Tier(width=E, layer_dims=layers, minibatches=J, key_space=dims,
@@ -139,13 +140,16 @@ def test_forced_certificate_failure_on_the_medium_path(pkg, oracle, monkeypatch,
 @pytest.mark.parametrize("mid", ["32", "128", "1024", "100000"])
 @pytest.mark.parametrize("E", [4, 16, 64])
 def test_mid_segment_warp_paths_bit_exact(pkg, oracle, monkeypatch, mid, E, cert):
-    """Segments of 33..HPS_MID_SEG occurrences take one warp each: certified
+    """Segments of HPS_SHORT_SEG+1..HPS_MID_SEG occurrences (default 33..512)
+    take one warp each: certified
     (sparse_mid_cert_kernel, E in {4, 8, 16, 32}) or, with HPS_MID_CERT=0 and
     for other widths, the exact reference-order chain (sparse_mid_kernel);
     longer ones the chunked certified reduce. Every split point gives the
     oracle's bits."""
     monkeypatch.setenv("HPS_MID_SEG", mid)
     monkeypatch.setenv("HPS_MID_CERT", cert)
+    if mid == "32":  # no medium path: thread chains up to 32, chunks beyond
+        monkeypatch.setenv("HPS_SHORT_SEG", "32")
     dims, B, J = 20000, 4096, 4
     off, keys, lab = pkg.gen_dataset(dims, 2 * B, 20, zipf=True, seed=29)
     tier = pkg.Tier(width=E, minibatches=J, key_space=dims, max_batch_examples=B,
