@@ -149,4 +149,49 @@ __device__ __forceinline__ std::uint32_t probe_slot(
   return kNoSlot;
 }
 
+// Lookup in a table with the ascending-insert layout (every batch table:
+// ordered linear probing, table_insert_ordered): when key k sits at slot p,
+// every slot of [home(k), p) held a smaller key when k was placed and still
+// does, so the first slot holding a key >= k decides — a miss stops at the
+// first larger key instead of the first empty slot (kEmptyKey is the
+// largest u64).
+__device__ __forceinline__ std::uint32_t probe_slot_ordered(
+    const std::uint64_t* __restrict__ keys, std::uint64_t cap, std::uint64_t key) {
+  std::uint64_t idx = mix64(key) & (cap - 1);
+  for (std::uint64_t n = 0; n < cap; ++n) {
+    const std::uint64_t k = __ldg(keys + idx);
+    if (k >= key) return k == key ? std::uint32_t(idx) : kNoSlot;
+    idx = (idx + 1) & (cap - 1);
+  }
+  return kNoSlot;
+}
+
+// The same lookup in up to three ordered tables at once (a null table or
+// cap 0 answers kNoSlot): the three home slots load together, and only the
+// runs that continue past their home slot walk on.
+__device__ __forceinline__ void probe3_ordered(std::uint64_t key, const std::uint64_t* t0,
+                                               std::uint64_t c0, const std::uint64_t* t1,
+                                               std::uint64_t c1, const std::uint64_t* t2,
+                                               std::uint64_t c2, std::uint32_t* s0,
+                                               std::uint32_t* s1, std::uint32_t* s2) {
+  const std::uint64_t h = mix64(key);
+  const std::uint64_t i0 = h & (c0 - 1), i1 = h & (c1 - 1), i2 = h & (c2 - 1);
+  const std::uint64_t k0 = c0 ? __ldg(t0 + i0) : kEmptyKey;
+  const std::uint64_t k1 = c1 ? __ldg(t1 + i1) : kEmptyKey;
+  const std::uint64_t k2 = c2 ? __ldg(t2 + i2) : kEmptyKey;
+  auto finish = [&](const std::uint64_t* t, std::uint64_t c, std::uint64_t i,
+                    std::uint64_t k) -> std::uint32_t {
+    if (!c) return kNoSlot;
+    for (std::uint64_t n = 0; n < c; ++n) {
+      if (k >= key) return k == key ? std::uint32_t(i) : kNoSlot;
+      i = (i + 1) & (c - 1);
+      k = __ldg(t + i);
+    }
+    return kNoSlot;
+  };
+  *s0 = finish(t0, c0, i0, k0);
+  *s1 = finish(t1, c1, i1, k1);
+  *s2 = finish(t2, c2, i2, k2);
+}
+
 }  // namespace hpsgpu

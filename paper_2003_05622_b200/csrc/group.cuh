@@ -93,7 +93,8 @@ __global__ void group_probe_kernel(ShardMap sm, const std::int64_t* __restrict__
                                    std::uint32_t* __restrict__ part_n,
                                    std::uint32_t* __restrict__ occ_slot,
                                    std::uint32_t* __restrict__ tick,
-                                   std::uint32_t* __restrict__ ex_of, DevError* err) {
+                                   std::uint32_t* __restrict__ ex_of, DevError* err,
+                                   bool ordered) {
   pdl_wait();
   const std::uint64_t cap = *cap_ptr;
   const unsigned lane = threadIdx.x & 31;
@@ -119,7 +120,8 @@ __global__ void group_probe_kernel(ShardMap sm, const std::int64_t* __restrict__
       const bool act = p < len;
       std::uint32_t slot = kNoSlot;
       if (act) {
-        slot = probe_slot(tkeys, cap, keys[b + p]);
+        slot = ordered ? probe_slot_ordered(tkeys, cap, keys[b + p])  // the batch table
+                       : probe_slot(tkeys, cap, keys[b + p]);         // G > 1: request table
         if (slot == kNoSlot) raise_error(err, 1, keys[b + p]);
       }
       const unsigned am = __ballot_sync(0xFFFFFFFFu, act && slot != kNoSlot);

@@ -261,7 +261,7 @@ __global__ void p2p_serve_rows_kernel(P2PCtx ctx, int G, int me, std::uint64_t s
     while (s + 1 < G && r >= base[s + 1]) ++s;
     const std::uint64_t i = r - base[s];
     const std::uint64_t key = my_keys[s * slot + i];
-    const std::uint32_t sl = probe_slot(tkeys, cap, key);
+    const std::uint32_t sl = probe_slot_ordered(tkeys, cap, key);
     if (sl == kNoSlot) {
       raise_error(err, 2, key);
       continue;

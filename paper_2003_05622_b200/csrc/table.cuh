@@ -261,20 +261,20 @@ __global__ void table_prefetch_probe_kernel(
     const bool live = i < n;
     const std::uint64_t key = live ? ws[i] : 0;
     const std::uint32_t slot = live ? wslot[i] : 0;
-    std::uint32_t ps = kNoSlot;
-    if (live && pcap) ps = probe_slot(prev_keys, pcap, key);
+    // the three resident tables probed at once (their home slots load
+    // together); ordered tables: a miss stops at the first larger key
+    std::uint32_t ps = kNoSlot, os = kNoSlot, o2 = kNoSlot;
+    if (live) probe3_ordered(key, prev_keys, pcap, old_keys, ocap, old2_keys, o2cap, &ps, &os, &o2);
     bool need = false;
     if (live && ps == kNoSlot) {
       // newest proxy first: its row is the key's latest. The copy itself is
       // table_carry_kernel's (in the body, when the source rows are final),
       // so this prep never waits for the batches still training.
       std::uint32_t src = kNoSlot;
-      const std::uint32_t os = ocap ? probe_slot(old_keys, ocap, key) : kNoSlot;
       if (os != kNoSlot) {
         src = kSrcProxy1 | os;
-      } else if (o2cap) {
-        const std::uint32_t o2 = probe_slot(old2_keys, o2cap, key);
-        if (o2 != kNoSlot) src = kSrcProxy2 | o2;
+      } else if (o2 != kNoSlot) {
+        src = kSrcProxy2 | o2;
       }
       csrc[i] = src;
       if (src != kNoSlot) {
@@ -448,9 +448,9 @@ __global__ void table_evict_filter_kernel(const std::uint64_t* __restrict__ ws,
     std::uint64_t key = 0;
     if (i < n) {
       key = ws[i];
-      keep = key < store_keys && (!cap1 || probe_slot(k1, cap1, key) == kNoSlot) &&
-             (!cap2 || probe_slot(k2, cap2, key) == kNoSlot) &&
-             (!cap3 || probe_slot(k3, cap3, key) == kNoSlot);
+      std::uint32_t s1 = kNoSlot, s2 = kNoSlot, s3 = kNoSlot;
+      if (key < store_keys) probe3_ordered(key, k1, cap1, k2, cap2, k3, cap3, &s1, &s2, &s3);
+      keep = key < store_keys && s1 == kNoSlot && s2 == kNoSlot && s3 == kNoSlot;
     }
     const unsigned m = __ballot_sync(0xFFFFFFFFu, keep);
     if (m) {
@@ -529,14 +529,14 @@ __global__ void table_fill_kernel(
     const std::uint64_t i = t / tpk;
     const int part = int(t - i * tpk);
     const std::uint64_t key = ws[i];
-    const std::uint32_t slot = probe_slot(keys, cap, key);
+    const std::uint32_t slot = probe_slot_ordered(keys, cap, key);
     if (slot == kNoSlot) {
       raise_error(err, 2, key);
       continue;
     }
     const float* src = nullptr;
     if (pcap) {
-      const std::uint32_t ps = probe_slot(prev_keys, pcap, key);
+      const std::uint32_t ps = probe_slot_ordered(prev_keys, pcap, key);
       if (ps != kNoSlot) src = prev_vals + std::uint64_t(ps) * E;
     }
     if (carried) {  // warp-aggregated count of carry-over rows
@@ -578,7 +578,7 @@ __global__ void table_gather_kernel(const std::uint64_t* __restrict__ qkeys,
     const std::uint64_t i = t / tpk;
     const int part = int(t - i * tpk);
     const std::uint64_t key = qkeys[i];
-    const std::uint32_t slot = probe_slot(keys, cap, key);
+    const std::uint32_t slot = probe_slot_ordered(keys, cap, key);
     if (slot == kNoSlot) {
       raise_error(err, 2, key);
       continue;
@@ -608,7 +608,7 @@ __global__ void table_lookup_kernel(const std::uint64_t* __restrict__ qkeys, std
   for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < n;
        i += std::uint64_t(gridDim.x) * blockDim.x) {
     const std::uint64_t key = qkeys[i];
-    const std::uint32_t slot = key == kEmptyKey ? kNoSlot : probe_slot(keys, cap, key);
+    const std::uint32_t slot = key == kEmptyKey ? kNoSlot : probe_slot_ordered(keys, cap, key);
     found[i] = slot != kNoSlot;
     if (rows)
       for (int d = 0; d < RW; ++d)
@@ -643,7 +643,7 @@ __global__ void table_apply_kernel(const std::uint32_t* __restrict__ slots,
     if (slots) {
       slot = slots[i];
     } else {
-      slot = probe_slot(tkeys, *cap_ptr, qkeys[i]);
+      slot = probe_slot_ordered(tkeys, *cap_ptr, qkeys[i]);
       if (slot == kNoSlot) {
         raise_error(err, 2, qkeys[i]);
         continue;
@@ -681,7 +681,7 @@ __global__ void table_dump_kernel(const std::uint64_t* __restrict__ ws,
     const std::uint64_t i = t / tpk;
     const int part = int(t - i * tpk);
     const std::uint64_t key = ws[i];
-    const std::uint32_t slot = probe_slot(keys, cap, key);
+    const std::uint32_t slot = probe_slot_ordered(keys, cap, key);
     if (slot == kNoSlot) {
       raise_error(err, 2, key);
       continue;

@@ -1492,7 +1492,7 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     const std::uint64_t* gc = G == 1 ? &T->dsc->cap[tb] : &T->dsc->rq_capv;
     launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys, gk, gc, g.gcnt,
            g.slot_uid, g.part_slot, pcap, g.part_n, T->g_occslot[tb], T->g_tick[tb], T->g_exof[tb],
-           err);
+           err, G == 1);
     launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)g.part_n,
            (const std::uint32_t*)g.part_slot, pcap, g.part_base, uids, U);
     const Count Uc{reinterpret_cast<const std::uint64_t*>(U), 0};
