@@ -228,6 +228,30 @@ struct BatchOut {
   DevError err, err_stage, err_prep;
 };
 
+// A batch's readback (loss, counters, error words) in ONE launch after its
+// body: one thread copies the fields into the slot's pinned BatchOut (mapped,
+// UVA) — nine small D2H copies serialised the body stream by ~30 us.
+__global__ void batch_out_kernel(const Scalars* __restrict__ d, int tb, int sp,
+                                 BatchOut* __restrict__ o) {
+  pdl_wait();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  o->loss = d->loss;
+  o->pulled = d->pulled;
+  o->fallbacks = d->fallbacks;
+  o->served = d->served;
+  o->big_keys = d->big_keys;
+  o->max_chunks = d->max_chunks;
+  o->big_occ = d->big_occ;
+  o->mid_keys = d->mid_keys;
+  o->carried = d->carried_tab[tb];
+  o->stored = d->stored_tab[tb];
+  o->n_ws = d->nws_tab[tb];
+  o->cap = d->cap[tb];
+  o->err = d->err;
+  o->err_stage = d->serr[sp];
+  o->err_prep = d->perr[tb];
+}
+
 // One sender's pushed (keys, deltas) awaiting hps_drain: a range of the
 // pending arena (Tier::pend_*), which grows by doubling and is reused.
 struct PendingChunk {
@@ -252,6 +276,7 @@ struct Tier {
   int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
   std::uint32_t mid_max = 512;          // medium segments: short_max < length <= mid_max
   std::uint32_t short_max = 32;         // short segments (thread chains): length <= short_max
+  unsigned prep_grid = 4 * kSMs;  // HPS_PREP_GRID: block cap of the prep-side kernels (0: none)
   bool mid_cert = true;  // medium segments certified (HPS_MID_CERT=0: exact warp chains)
   bool dg_fused = true;  // dense gradient in one launch (HPS_DG_FUSED=0: four launches)
   bool fb_tile = true;  // fwd/bwd embed_sum through shared-memory row tiles (HPS_FB_TILE=0: off)
@@ -529,6 +554,12 @@ static unsigned grid_for(std::uint64_t work, int threads = 256,
   return unsigned(std::max<std::uint64_t>(1, std::min<std::uint64_t>(b, cap)));
 }
 
+// Grid of a prep-side (off the critical path) grid-stride kernel: capped at
+// Tier::prep_grid blocks (HPS_PREP_GRID; 0 = uncapped) so that the batch
+// build never fills every SM while the body's kernels wait for slots.
+struct Tier;
+static unsigned prep_grid_of(const Tier* t, unsigned g);
+
 bool debug_sync_enabled();
 
 // HPS_DEBUG_SYNC=1 (diagnostics, graphs must be off): synchronise after every
@@ -631,6 +662,7 @@ static hps_status device_error_status(Tier* t, const DevError& e, const char* mi
 }
 
 // ------------------------------------------------------ small kernels ----
+
 
 __global__ void iota_kernel(std::uint32_t* v, std::uint64_t n) {
   pdl_wait();
@@ -1448,6 +1480,10 @@ inline std::uint64_t shape_bound(std::uint64_t x) {
   return p;
 }
 
+static unsigned prep_grid_of(const Tier* t, unsigned g) {
+  return t->prep_grid ? std::min(g, t->prep_grid) : g;
+}
+
 // Start of mini-batch j's region in the per-table grouping pools: the sum of
 // the earlier mini-batches' shape bounds (stable per shape, so captured
 // graphs hold across batches).
@@ -1490,18 +1526,18 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     // rank's request table (G > 1)
     const std::uint64_t* gk = G == 1 ? T->tkeys[tb] : T->rq_keys[tb];
     const std::uint64_t* gc = G == 1 ? &T->dsc->cap[tb] : &T->dsc->rq_capv;
-    launch(T, group_probe_kernel, grid_for(warps * 32), 256, 0, sm, doff, dkeys, gk, gc, g.gcnt,
+    launch(T, group_probe_kernel, prep_grid_of(T, grid_for(warps * 32)), 256, 0, sm, doff, dkeys, gk, gc, g.gcnt,
            g.slot_uid, g.part_slot, pcap, g.part_n, T->g_occslot[tb], T->g_tick[tb], T->g_exof[tb],
            err, G == 1);
-    launch(T, group_compact_kernel, grid_for(ob), 256, 0, (const std::uint32_t*)g.part_n,
+    launch(T, group_compact_kernel, prep_grid_of(T, grid_for(ob)), 256, 0, (const std::uint32_t*)g.part_n,
            (const std::uint32_t*)g.part_slot, pcap, g.part_base, uids, U);
     const Count Uc{reinterpret_cast<const std::uint64_t*>(U), 0};
     tile_scan(T, UidCount{uids, g.gcnt}, SegEmit{seg, Uc}, Uc, ob, &l.d->total);
-    launch(T, group_place_kernel, grid_for(n * 32), 256, 0, sm, doff,
+    launch(T, group_place_kernel, prep_grid_of(T, grid_for(n * 32)), 256, 0, sm, doff,
            (const std::uint32_t*)T->g_occslot[tb], (const std::uint32_t*)T->g_tick[tb],
            (const std::uint32_t*)g.slot_uid, pcap, (const std::uint32_t*)g.part_base,
            (const std::uint32_t*)seg, segocc, G == 1 ? nullptr : T->g_inv[tb]);
-    launch(T, group_order_kernel, grid_for(ob), 256, 0, (const unsigned long long*)U,
+    launch(T, group_order_kernel, prep_grid_of(T, grid_for(ob)), 256, 0, (const unsigned long long*)U,
            (const std::uint32_t*)seg, segocc, (const std::uint32_t*)T->g_exof[tb],
            (const std::uint32_t*)uids, g.gcnt, exs, g.g_long, &g.gn[0], g.g_huge,
            &g.gn[2], g.part_n);
@@ -1563,7 +1599,7 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   HPS_CUDA(cudaMemsetAsync(&T->dsc->carried_tab[tb], 0, 8, l.st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->stored_tab[tb], 0, 8, l.st));
   HPS_CUDA(cudaMemsetAsync(&T->dsc->spec_fail, 0, 4, l.st));
-  const unsigned gk = grid_for(sh.batch_bound, 256, kSMs * 8);
+  const unsigned gk = prep_grid_of(T, grid_for(sh.batch_bound, 256, kSMs * 8));
   const std::uint64_t cap_bound = table_capacity(sh.own_bound);
   // speculative build at the previous table's capacity (a steady workload
   // keeps it), counting the distinct keys; the check redoes the build at the
@@ -1637,7 +1673,7 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   const int tq2 = bp.tq2;
   const std::uint64_t* q2k = tq2 >= 0 ? T->tkeys[tq2] : nullptr;
   const std::uint64_t* q2c = tq2 >= 0 ? &T->dsc->cap[tq2] : nullptr;
-  launch(T, table_prefetch_probe_kernel, grid_for(sh.own_bound), 256, 0,
+  launch(T, table_prefetch_probe_kernel, prep_grid_of(T, grid_for(sh.own_bound)), 256, 0,
          (const std::uint64_t*)T->wsb[tb], (const std::uint32_t*)T->wsib[tb],
          (const std::uint64_t*)nws, T->tvals[tb], T->csrc[tb], pk, pc, qk, qc, q2k, q2c,
          T->store != nullptr, T->store_keys, T->RW, T->need_key[tb], T->need_slot[tb],
@@ -2042,7 +2078,7 @@ static hps_status enqueue_writeback(Tier* T, int t, const int* newer, int n_newe
     nc[i] = &T->dsc->cap[newer[i]];
   }
   HPS_CUDA(cudaMemsetAsync(&T->dsc->wb_n[t], 0, 8, T->st_wb));
-  launch_on(T, T->st_wb, table_evict_filter_kernel, grid_for(T->Wmax), 256, 0,
+  launch_on(T, T->st_wb, table_evict_filter_kernel, prep_grid_of(T, grid_for(T->Wmax)), 256, 0,
             (const std::uint64_t*)T->wsb[t], (const std::uint32_t*)T->wsib[t],
             (const std::uint64_t*)&T->dsc->nws_tab[t], nk[0], nc[0], nk[1], nc[1], nk[2], nc[2],
             T->store_keys, T->wb_key[t], T->wb_slot[t], &T->dsc->wb_n[t], &T->dsc->wb_total);
@@ -2533,17 +2569,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   }
   BatchOut* ho = &T->hout[sp];
   const int tb = bp.tb;
-  HPS_CUDA(cudaMemcpyAsync(&ho->loss, &T->dsc->loss, 16, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->fallbacks, &T->dsc->fallbacks, 48, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->carried, &T->dsc->carried_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->stored, &T->dsc->stored_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->n_ws, &T->dsc->nws_tab[tb], 8, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->cap, &T->dsc->cap[tb], 8, cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->err, &T->dsc->err, sizeof(DevError), cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->err_stage, &T->dsc->serr[sp], sizeof(DevError),
-                           cudaMemcpyDeviceToHost, T->st));
-  HPS_CUDA(cudaMemcpyAsync(&ho->err_prep, &T->dsc->perr[tb], sizeof(DevError),
-                           cudaMemcpyDeviceToHost, T->st));
+  launch(T, batch_out_kernel, 1, 32, 0, (const Scalars*)T->dsc, tb, sp, ho);
   if (T->trace) cudaEventRecord(T->tr[sp][5], T->st);
   HPS_CUDA(cudaEventRecord(T->ev_body_tab[tb], T->st));
   HPS_CUDA(cudaEventRecord(T->ev_body_sp[sp], T->st));
@@ -2687,6 +2713,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_FB_TILE")) t->fb_tile = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_DG_FUSED")) t->dg_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_MID_CERT")) t->mid_cert = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_PREP_GRID")) t->prep_grid = unsigned(std::max(0, std::atoi(v)));
   if (const char* v = std::getenv("HPS_SHORT_DPT")) {
     const int d = std::atoi(v);
     if (d == 1 || (d == 4 && c.embedding_dim % 4 == 0) || (d == 8 && c.embedding_dim % 8 == 0))
