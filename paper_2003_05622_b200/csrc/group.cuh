@@ -239,11 +239,20 @@ __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__
                                    const std::uint32_t* __restrict__ part_base,
                                    const std::uint32_t* __restrict__ seg,
                                    std::uint32_t* __restrict__ seg_occ,
-                                   std::uint32_t* __restrict__ inv) {
+                                   std::uint32_t* __restrict__ inv,
+                                   std::uint32_t* __restrict__ cnt,
+                                   std::uint32_t* __restrict__ part_n,
+                                   std::uint32_t* __restrict__ long_list,
+                                   unsigned long long* __restrict__ n_long,
+                                   std::uint32_t* __restrict__ huge_list,
+                                   unsigned long long* __restrict__ n_huge) {
   pdl_wait();
   __shared__ std::uint32_t pb[kGroupParts];
   if (threadIdx.x < kGroupParts) pb[threadIdx.x] = part_base[threadIdx.x];
   __syncthreads();
+  // the claim counters are read (group_compact) and free again
+  if (cnt && blockIdx.x == 0 && threadIdx.x < kGroupParts)
+    part_n[threadIdx.x * kGroupPartStride] = 0;
   const unsigned lane = threadIdx.x & 31;
   const std::uint64_t nw = (std::uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (std::uint64_t k = (blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -251,9 +260,17 @@ __global__ void group_place_kernel(ShardMap sm, const std::int64_t* __restrict__
     const std::uint64_t ex = sm.first + k * sm.stride;
     const std::int64_t b = off[ex], e = off[ex + 1];
     for (std::int64_t q = b + lane; q < e; q += 32) {
-      const std::uint32_t u = dense_uid(slot_uid[occ_slot[q]], part_cap, pb);
-      seg_occ[seg[u] + tick[q]] = std::uint32_t(q);
+      const std::uint32_t sl = occ_slot[q];
+      const std::uint32_t u = dense_uid(slot_uid[sl], part_cap, pb);
+      const std::uint32_t t = tick[q];
+      seg_occ[seg[u] + t] = std::uint32_t(q);
       if (inv) inv[q] = u;
+      if (cnt && t == 0) {  // one occurrence per key: its counter and its list
+        cnt[sl] = 0;        // (the segment scan has read it)
+        const std::uint32_t n = seg[u + 1] - seg[u];
+        if (n > std::uint32_t(kGroupWarpMax)) huge_list[atomicAdd(n_huge, 1ull)] = u;
+        else if (n > std::uint32_t(kGroupShort)) long_list[atomicAdd(n_long, 1ull)] = u;
+      }
     }
   }
 }
@@ -486,6 +503,180 @@ __global__ void __launch_bounds__(kGroupThreads)
       std::uint32_t r = 0;
       for (std::uint32_t i = p0; i < p1; ++i) r += seg_occ[i] < q;
       exs[p0 + r] = ex_of[q];
+    }
+  }
+}
+
+// The whole segment ordering in ONE launch (HPS_GROUP_FUSED=1, the
+// default; group_order + group_warp + group_cta + group_dup otherwise), after
+// group_place has listed the longer segments: every block first orders the
+// short segments (<= kGroupShort) of its share of the uids in registers, then
+// takes the huge segments (> kGroupWarpMax) one per block, then its warps take
+// the long ones one per warp — the same example-bitmap ranks as above. A
+// segment whose examples repeat its key (the input repeats a feature inside
+// an example) is ranked in place by counting smaller occurrence ids.
+__device__ __forceinline__ void rank_by_count(std::uint32_t p0, std::uint32_t p1,
+                                              const std::uint32_t* __restrict__ seg_occ,
+                                              const std::uint32_t* __restrict__ ex_of,
+                                              std::uint32_t* __restrict__ exs, unsigned t,
+                                              unsigned nt) {
+  for (std::uint32_t p = p0 + t; p < p1; p += nt) {
+    const std::uint32_t q = seg_occ[p];
+    std::uint32_t r = 0;
+    for (std::uint32_t i = p0; i < p1; ++i) r += seg_occ[i] < q;
+    exs[p0 + r] = ex_of[q];
+  }
+}
+
+__global__ void __launch_bounds__(kGroupWarpThreads)
+    group_sort_kernel(const unsigned long long* __restrict__ n_uid,
+                      const std::uint32_t* __restrict__ seg,
+                      const std::uint32_t* __restrict__ seg_occ,
+                      const std::uint32_t* __restrict__ ex_of, std::uint32_t words,
+                      std::uint32_t* __restrict__ exs,
+                      const unsigned long long* __restrict__ n_long,
+                      const std::uint32_t* __restrict__ long_list,
+                      const unsigned long long* __restrict__ n_huge,
+                      const std::uint32_t* __restrict__ huge_list) {
+  pdl_wait();
+  extern __shared__ std::uint32_t gsort_sm[];  // per warp: bitmap[words], prefix[words]
+  __shared__ std::uint32_t wsum[kGroupWarpThreads / 32];
+  __shared__ int s_dup;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr unsigned kWarps = kGroupWarpThreads / 32;
+  // ---- short segments: one thread each, in registers
+  const std::uint64_t U = *n_uid;
+  for (std::uint64_t u = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; u < U;
+       u += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint32_t p0 = seg[u];
+    const int n = int(seg[u + 1] - p0);
+    if (n > kGroupShort) continue;
+    std::uint32_t v[kGroupShort];
+#pragma unroll
+    for (int i = 0; i < kGroupShort; ++i) v[i] = i < n ? seg_occ[p0 + i] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = 1; i < kGroupShort; ++i)
+#pragma unroll
+      for (int j = i; j > 0; --j) {
+        const std::uint32_t a = v[j - 1], b = v[j];
+        v[j - 1] = min(a, b);
+        v[j] = max(a, b);
+      }
+#pragma unroll
+    for (int i = 0; i < kGroupShort; ++i)
+      if (i < n) exs[p0 + i] = ex_of[v[i]];
+  }
+  // ---- huge segments: one block each (bitmap over the block's smem)
+  {
+    std::uint32_t* cbm = gsort_sm;
+    std::uint32_t* pre = gsort_sm + words;
+    const std::uint64_t NH = *n_huge;
+    for (std::uint64_t li = blockIdx.x; li < NH; li += gridDim.x) {
+      const std::uint32_t u = huge_list[li];
+      const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
+      for (std::uint32_t i = threadIdx.x; i < words; i += blockDim.x) cbm[i] = 0;
+      if (threadIdx.x == 0) s_dup = 0;
+      __syncthreads();
+      constexpr int R = 4;
+      for (std::uint32_t b0 = p0 + warp * 32; b0 < p1; b0 += blockDim.x * R) {
+        std::uint32_t ev[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const std::uint32_t p = b0 + r * blockDim.x + lane;
+          ev[r] = p < p1 ? seg_occ[p] : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) ev[r] = ev[r] != 0xFFFFFFFFu ? ex_of[ev[r]] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (set_bits(cbm, ev[r], ev[r] != 0xFFFFFFFFu)) s_dup = 1;
+      }
+      __syncthreads();
+      if (s_dup) {
+        rank_by_count(p0, p1, seg_occ, ex_of, exs, threadIdx.x, blockDim.x);
+        __syncthreads();
+        continue;
+      }
+      const std::uint32_t per = (words + blockDim.x - 1) / blockDim.x;
+      const std::uint32_t w0 = threadIdx.x * per, w1 = min(words, w0 + per);
+      std::uint32_t mine = 0;
+      for (std::uint32_t i = w0; i < w1; ++i) mine += __popc(cbm[i]);
+      std::uint32_t x = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= unsigned(o)) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      std::uint32_t run = x - mine;
+      for (unsigned w = 0; w < warp; ++w) run += wsum[w];
+      for (std::uint32_t i = w0; i < w1; ++i) {
+        pre[i] = run;
+        run += __popc(cbm[i]);
+      }
+      __syncthreads();
+      for (std::uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const std::uint32_t e = ex_of[seg_occ[p]];
+        const std::uint32_t r = pre[e >> 5] + __popc(cbm[e >> 5] & ((1u << (e & 31)) - 1u));
+        exs[p0 + r] = e;
+      }
+      __syncthreads();
+    }
+  }
+  // ---- long segments: one warp each
+  {
+    constexpr int R = kGroupWarpMax / 32;
+    std::uint32_t* bm = gsort_sm + std::size_t(warp) * 2 * words;
+    std::uint32_t* pre = bm + words;
+    const std::uint64_t NL = *n_long;
+    const std::uint64_t nwarps = std::uint64_t(gridDim.x) * kWarps;
+    for (std::uint64_t li = std::uint64_t(blockIdx.x) * kWarps + warp; li < NL; li += nwarps) {
+      const std::uint32_t u = long_list[li];
+      const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
+      std::uint32_t ev[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const std::uint32_t p = p0 + r * 32 + lane;
+        ev[r] = p < p1 ? seg_occ[p] : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) ev[r] = ev[r] != 0xFFFFFFFFu ? ex_of[ev[r]] : 0xFFFFFFFFu;
+      for (std::uint32_t i = lane; i < words; i += 32) bm[i] = 0;
+      __syncwarp();
+      bool dup = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) dup |= set_bits(bm, ev[r], ev[r] != 0xFFFFFFFFu);
+      if (__any_sync(0xFFFFFFFFu, dup)) {
+        rank_by_count(p0, p1, seg_occ, ex_of, exs, lane, 32);
+        __syncwarp();
+        continue;
+      }
+      __syncwarp();
+      const std::uint32_t per = (words + 31) / 32;
+      const std::uint32_t w0 = lane * per, w1 = min(words, w0 + per);
+      std::uint32_t mine = 0;
+      for (std::uint32_t i = w0; i < w1; ++i) mine += __popc(bm[i]);
+      std::uint32_t x = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= unsigned(o)) x += y;
+      }
+      std::uint32_t run = x - mine;
+      for (std::uint32_t i = w0; i < w1; ++i) {
+        pre[i] = run;
+        run += __popc(bm[i]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const std::uint32_t e = ev[r];
+        if (e == 0xFFFFFFFFu) continue;
+        const std::uint32_t rk = pre[e >> 5] + __popc(bm[e >> 5] & ((1u << (e & 31)) - 1u));
+        exs[p0 + rk] = e;
+      }
+      __syncwarp();
     }
   }
 }

@@ -276,6 +276,8 @@ struct Tier {
   int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
   std::uint32_t mid_max = 512;          // medium segments: short_max < length <= mid_max
   std::uint32_t short_max = 32;         // short segments (thread chains): length <= short_max
+  bool group_fused = true;  // segment ordering in one launch (HPS_GROUP_FUSED=0: four)
+  bool group_prio = false;  // the body's own grouping lane at body priority (HPS_GROUP_PRIO=1)
   unsigned prep_grid = 4 * kSMs;  // HPS_PREP_GRID: block cap of the prep-side kernels (0: none)
   bool mid_cert = true;  // medium segments certified (HPS_MID_CERT=0: exact warp chains)
   bool dg_fused = true;  // dense gradient in one launch (HPS_DG_FUSED=0: four launches)
@@ -1533,16 +1535,32 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
            (const std::uint32_t*)g.part_slot, pcap, g.part_base, uids, U);
     const Count Uc{reinterpret_cast<const std::uint64_t*>(U), 0};
     tile_scan(T, UidCount{uids, g.gcnt}, SegEmit{seg, Uc}, Uc, ob, &l.d->total);
+    const std::uint32_t words = std::uint32_t((n + 31) / 32);
+    const std::size_t wsmem = std::size_t(kGroupWarpThreads / 32) * 2 * words * 4;
+    if (T->group_fused) {
+      // place also resets the slot counters and lists the longer segments;
+      // one launch then orders every segment
+      launch(T, group_place_kernel, prep_grid_of(T, grid_for(n * 32)), 256, 0, sm, doff,
+             (const std::uint32_t*)T->g_occslot[tb], (const std::uint32_t*)T->g_tick[tb],
+             (const std::uint32_t*)g.slot_uid, pcap, (const std::uint32_t*)g.part_base,
+             (const std::uint32_t*)seg, segocc, G == 1 ? nullptr : T->g_inv[tb], g.gcnt, g.part_n,
+             g.g_long, &g.gn[0], g.g_huge, &g.gn[2]);
+      launch(T, group_sort_kernel, kSMs * 4, kGroupWarpThreads, wsmem,
+             (const unsigned long long*)U, (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
+             (const std::uint32_t*)T->g_exof[tb], words, exs,
+             (const unsigned long long*)&g.gn[0], (const std::uint32_t*)g.g_long,
+             (const unsigned long long*)&g.gn[2], (const std::uint32_t*)g.g_huge);
+    } else {
     launch(T, group_place_kernel, prep_grid_of(T, grid_for(n * 32)), 256, 0, sm, doff,
            (const std::uint32_t*)T->g_occslot[tb], (const std::uint32_t*)T->g_tick[tb],
            (const std::uint32_t*)g.slot_uid, pcap, (const std::uint32_t*)g.part_base,
-           (const std::uint32_t*)seg, segocc, G == 1 ? nullptr : T->g_inv[tb]);
+           (const std::uint32_t*)seg, segocc, G == 1 ? nullptr : T->g_inv[tb],
+           (std::uint32_t*)nullptr, (std::uint32_t*)nullptr, (std::uint32_t*)nullptr,
+           (unsigned long long*)nullptr, (std::uint32_t*)nullptr, (unsigned long long*)nullptr);
     launch(T, group_order_kernel, prep_grid_of(T, grid_for(ob)), 256, 0, (const unsigned long long*)U,
            (const std::uint32_t*)seg, segocc, (const std::uint32_t*)T->g_exof[tb],
            (const std::uint32_t*)uids, g.gcnt, exs, g.g_long, &g.gn[0], g.g_huge,
            &g.gn[2], g.part_n);
-    const std::uint32_t words = std::uint32_t((n + 31) / 32);
-    const std::size_t wsmem = std::size_t(kGroupWarpThreads / 32) * 2 * words * 4;
     launch(T, group_warp_kernel, kSMs * 4, kGroupWarpThreads, wsmem,
            (const unsigned long long*)&g.gn[0], (const std::uint32_t*)g.g_long,
            (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
@@ -1555,6 +1573,7 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
            (const unsigned long long*)&g.gn[1], (const std::uint32_t*)g.g_dup,
            (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
            (const std::uint32_t*)T->g_exof[tb], exs);
+    }
     if (G > 1 && T->xfuse && T->xprep) {
       // the fused exchange's keys of this mini-batch, off the body's path:
       // unique keys in uid order and their owner ranks (no round opened here)
@@ -2714,6 +2733,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_DG_FUSED")) t->dg_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_MID_CERT")) t->mid_cert = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_PREP_GRID")) t->prep_grid = unsigned(std::max(0, std::atoi(v)));
+  if (const char* v = std::getenv("HPS_GROUP_PRIO")) t->group_prio = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_GROUP_FUSED")) t->group_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_SHORT_DPT")) {
     const int d = std::atoi(v);
     if (d == 1 || (d == 4 && c.embedding_dim % 4 == 0) || (d == 8 && c.embedding_dim % 8 == 0))
@@ -2803,7 +2824,12 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     str(&t->st3, hi);
     str(&t->st4, hi);
     str(&t->lane[1].st, lo);
-    for (int gl = 0; gl < kGroupLanes; ++gl) str(&t->lane[2 + gl].st, lo);
+    // lane 2 groups the next batch (prep, low); lane 3 groups this body's
+    // later mini-batches, which wait for it — at prep priority too: body
+    // priority (HPS_GROUP_PRIO=1) measured 28.9M vs 30.0M ex/s on c2 (its
+    // kernels then crowd the running mini-batch's reduce instead)
+    str(&t->lane[2].st, lo);
+    str(&t->lane[3].st, t->group_prio ? hi : lo);
     str(&t->st_stage, lo);
     str(&t->st_wb, lo);
     str(&t->st_pf, lo);
@@ -2874,6 +2900,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     cudaFuncSetAttribute(group_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kGroupSmemMax));
     cudaFuncSetAttribute(group_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kGroupSmemMax));
+    cudaFuncSetAttribute(group_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kGroupSmemMax));
   }
   const std::uint64_t O = t->Omax, W = t->Wmax, E = std::uint64_t(t->E);

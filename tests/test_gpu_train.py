@@ -266,16 +266,20 @@ def test_pipelined_submit_wait_bit_exact(pkg, oracle, store_kind):
     assert any(s.store_rows + s.carried_rows < s.working_set for s in stats[2:])
 
 
-@pytest.mark.parametrize("dedup", ["hash", "sort"])
-def test_duplicate_keys_within_examples(pkg, oracle, dedup, monkeypatch):
+@pytest.mark.parametrize("B", [512, 2048])
+@pytest.mark.parametrize("dedup", ["hash", "hash-unfused", "sort"])
+def test_duplicate_keys_within_examples(pkg, oracle, dedup, B, monkeypatch):
     """A key repeated inside one example is two occurrences (embed_sum adds
     its row twice, backward accumulates it twice, model.hpp:59-117,182-187).
-    Both mini-batch dedup paths (slot grouping, group.cuh; radix sort) must
-    keep the occurrence order and match the oracle bit for bit. Hot keys make
-    long segments (the bitmap-ranked path)."""
-    monkeypatch.setenv("HPS_DEDUP", dedup)
+    Both mini-batch dedup paths (slot grouping, group.cuh, with the segment
+    ordering in one launch or, "hash-unfused", in four; radix sort) must keep
+    the occurrence order and match the oracle bit for bit. Hot keys make long
+    segments (the bitmap-ranked paths; at B = 2048 over 256 occurrences, the
+    per-CTA path) that repeat inside examples (the counting fallback)."""
+    monkeypatch.setenv("HPS_DEDUP", "hash" if dedup.startswith("hash") else dedup)
+    monkeypatch.setenv("HPS_GROUP_FUSED", "0" if dedup == "hash-unfused" else "1")
     rng = np.random.default_rng(12)
-    dims, n = 3000, 1500
+    dims, n = 3000, 3 * B
     lens = rng.integers(1, 60, size=n)
     rows = []
     for l in lens:
@@ -286,7 +290,7 @@ def test_duplicate_keys_within_examples(pkg, oracle, dedup, monkeypatch):
     off[1:] = np.cumsum(lens)
     keys = np.concatenate(rows).astype(np.uint64)
     lab = rng.integers(0, 2, size=n).astype(np.uint8)
-    check_bit_exact(oracle, pkg, off, keys, lab, 512, E=8, layers=(8, 16, 1), J=4, dims=dims)
+    check_bit_exact(oracle, pkg, off, keys, lab, B, E=8, layers=(8, 16, 1), J=4, dims=dims)
 
 
 def test_sort_dedup_path_bit_exact(pkg, oracle, monkeypatch):
