@@ -169,7 +169,7 @@ __global__ void table_insert_dedup_kernel(const std::int64_t* __restrict__ off, 
       bool act = p < len;
       if (act) {
         cur = keys[b + p];
-        if (cur % G != g) {  // another rank's key
+        if (G > 1 && cur % G != g) {  // another rank's key (no 64-bit division at G == 1)
           act = false;
           cur = kEmptyKey;
         } else if (cur == kEmptyKey) {

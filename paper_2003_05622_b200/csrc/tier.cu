@@ -696,10 +696,18 @@ __global__ void batch_count_kernel(const std::int64_t* __restrict__ off,
   const std::uint64_t O = std::uint64_t(off[B]);
   if (tid == 0) counts[J + 1] = O;  // the batch's key occurrences
   unsigned long long own = 0;
-  for (std::uint64_t q = tid; q < O; q += nth) {
-    const std::uint64_t k = keys[q];
-    if (k >= key_space) raise_error(err, HPS_ERR_KEY_RANGE, k);
-    own += (k % std::uint64_t(G)) == std::uint64_t(g);
+  if (G == 1) {  // every key owned: the range check alone (no 64-bit division)
+    for (std::uint64_t q = tid; q < O; q += nth) {
+      const std::uint64_t k = keys[q];
+      if (k >= key_space) raise_error(err, HPS_ERR_KEY_RANGE, k);
+    }
+    own = tid == 0 ? O : 0;
+  } else {
+    for (std::uint64_t q = tid; q < O; q += nth) {
+      const std::uint64_t k = keys[q];
+      if (k >= key_space) raise_error(err, HPS_ERR_KEY_RANGE, k);
+      own += (k % std::uint64_t(G)) == std::uint64_t(g);
+    }
   }
   atomicAdd(&c[J], own);
   __syncthreads();
