@@ -276,6 +276,7 @@ struct Tier {
   int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
   std::uint32_t mid_max = 512;          // medium segments: short_max < length <= mid_max
   std::uint32_t short_max = 32;         // short segments (thread chains): length <= short_max
+  bool tail_prio = false;  // st3/st4 above st/st2 (HPS_TAIL_PRIO=1; measured no gain on c2)
   bool group_fused = true;  // segment ordering in one launch (HPS_GROUP_FUSED=0: four)
   bool group_prio = false;  // the body's own grouping lane at body priority (HPS_GROUP_PRIO=1)
   unsigned prep_grid = 4 * kSMs;  // HPS_PREP_GRID: block cap of the prep-side kernels (0: none)
@@ -1356,7 +1357,7 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
                                : (E == 16 ? sparse_mid_cert_kernel<16> : sparse_mid_cert_kernel<32>));
     launch_on(t, ms, mk, kSMs * 2, 32 * kMidCertWarps, mid_cert_smem(), n,
               (const unsigned long long*)&t->dsc->n_mid, (const std::uint32_t*)t->mid_list, seg,
-              exs, dout, DX, &t->dsc->mid_keys, &t->dsc->fallbacks);
+              exs, dout, DX, &t->dsc->mid_keys, &t->dsc->fallbacks, int(t->wide));
   } else if (t->mid_max > t->short_max) {
     const int rpi = E <= 8 ? 4 : (E <= 16 ? 2 : 1);
     auto mk = rpi == 4 ? sparse_mid_kernel<4> : (rpi == 2 ? sparse_mid_kernel<2> : sparse_mid_kernel<1>);
@@ -2743,6 +2744,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_PREP_GRID")) t->prep_grid = unsigned(std::max(0, std::atoi(v)));
   if (const char* v = std::getenv("HPS_GROUP_PRIO")) t->group_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_GROUP_FUSED")) t->group_fused = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_TAIL_PRIO")) t->tail_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_SHORT_DPT")) {
     const int d = std::atoi(v);
     if (d == 1 || (d == 4 && c.embedding_dim % 4 == 0) || (d == 8 && c.embedding_dim % 8 == 0))
@@ -2827,8 +2829,13 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     auto str = [&](cudaStream_t* x, int prio) {
       if (e == cudaSuccess) e = cudaStreamCreateWithPriority(x, cudaStreamNonBlocking, prio);
     };
-    str(&t->st, hi);
-    str(&t->st2, hi);
+    // within the body, the long-latency reductions (medium keys on st4, hot
+    // keys on st3) outrank the short-key pass and the dense gradient, whose
+    // many CTAs would otherwise take every slot first and start them late
+    // (HPS_TAIL_PRIO=0: all four equal)
+    const int body2 = (t->tail_prio && hi < lo) ? hi + 1 : hi;
+    str(&t->st, body2);
+    str(&t->st2, body2);
     str(&t->st3, hi);
     str(&t->st4, hi);
     str(&t->lane[1].st, lo);
