@@ -189,11 +189,51 @@ __device__ __forceinline__ void embed_sum_tiled(const std::uint32_t* __restrict_
   hrec[sub] = acc;
 }
 
+// One dense layer of the fixed {8, 16, 1} stack (fwd_bwd_kernel<LPE, true>):
+// compile-time widths, so every product is issued ahead of the in-order
+// bias-then-inputs DADD chain (model.hpp:65-71) — the same operations in the
+// same order as the generic loop, without its runtime trip counts.
+template <int OUT, int IN, int LPE>
+__device__ __forceinline__ void layer_fwd_fixed(const float* W, const double* h, double* z,
+                                                double* hnext, int sub, DevError* err) {
+#pragma unroll
+  for (int o0 = 0; o0 < OUT; o0 += LPE) {
+    const int o = o0 + sub;
+    if (OUT % LPE != 0 && o >= OUT) break;
+    double p[IN];
+#pragma unroll
+    for (int i = 0; i < IN; ++i) p[i] = __dmul_rn(double(W[o * IN + i]), h[i]);
+    double acc = double(W[IN * OUT + o]);
+#pragma unroll
+    for (int i = 0; i < IN; ++i) acc = __dadd_rn(acc, p[i]);
+    if (!isfinite(acc)) raise_error(err, 5, 0);
+    z[o] = acc;
+    if (hnext) hnext[o] = acc > 0.0 ? acc : 0.0;
+  }
+}
+// dprev[i] = sum over outputs in index order (model.hpp:167-172)
+template <int OUT, int IN, int LPE>
+__device__ __forceinline__ void layer_bwd_fixed(const float* W, const double* dl, double* dprev,
+                                                int sub) {
+#pragma unroll
+  for (int i0 = 0; i0 < IN; i0 += LPE) {
+    const int i = i0 + sub;
+    if (IN % LPE != 0 && i >= IN) break;
+    double p[OUT];
+#pragma unroll
+    for (int o = 0; o < OUT; ++o) p[o] = __dmul_rn(double(W[o * IN + i]), dl[o]);
+    double acc = 0.0;
+#pragma unroll
+    for (int o = 0; o < OUT; ++o) acc = __dadd_rn(acc, p[o]);
+    dprev[i] = acc;
+  }
+}
+
 // Forward + per-example backward. LPE lanes per example (power of two
 // <= 32); each example's scratch lives in shared memory. Writes the H and DL
 // records (for the dense-gradient reduction), DX = dL/dx (for the sparse
 // segment reduction) and accumulates the log loss (model.hpp:232-242).
-template <int LPE>
+template <int LPE, bool FIX = false>
 __global__ void __launch_bounds__(128)
     fwd_bwd_kernel(ModelDims md, ShardMap sm, const float* __restrict__ dense,
                    const std::uint32_t* __restrict__ occ_off,
@@ -346,6 +386,18 @@ __global__ void __launch_bounds__(128)
     __syncwarp();
     // --- run_stack
     double z_out = 0.0;
+    if constexpr (FIX) {  // layers {8, 16, 1} over E == LPE inputs
+      if (active) layer_fwd_fixed<8, LPE, LPE>(W + md.offs[0], hrec + md.hoff[0],
+                                               zrec + md.doff[0], hrec + md.hoff[1], sub, err);
+      __syncwarp();
+      if (active) layer_fwd_fixed<16, 8, LPE>(W + md.offs[1], hrec + md.hoff[1],
+                                              zrec + md.doff[1], hrec + md.hoff[2], sub, err);
+      __syncwarp();
+      if (active && sub == 0)
+        layer_fwd_fixed<1, 16, LPE>(W + md.offs[2], hrec + md.hoff[2], zrec + md.doff[2],
+                                    (double*)nullptr, 0, err);
+      __syncwarp();
+    } else
     for (int l = 0; l < md.L; ++l) {
       const int out = md.dims[l], in = md.ins[l], off = md.offs[l];
       const double* h = hrec + md.hoff[l];
@@ -385,11 +437,17 @@ __global__ void __launch_bounds__(128)
       const int out = md.dims[li], in = md.ins[li], off = md.offs[li];
       const double* dl = zrec + md.doff[li];  // deltas of layer li
       if (active) {
-        for (int i = sub; i < in; i += LPE) {
-          double acc = 0.0;
-          for (int o = 0; o < out; ++o)
-            acc = __dadd_rn(acc, __dmul_rn(double(W[off + o * in + i]), dl[o]));
-          dprev[i] = acc;
+        if constexpr (FIX) {
+          if (li == 2) layer_bwd_fixed<1, 16, LPE>(W + off, dl, dprev, sub);
+          else if (li == 1) layer_bwd_fixed<16, 8, LPE>(W + off, dl, dprev, sub);
+          else layer_bwd_fixed<8, LPE, LPE>(W + off, dl, dprev, sub);
+        } else {
+          for (int i = sub; i < in; i += LPE) {
+            double acc = 0.0;
+            for (int o = 0; o < out; ++o)
+              acc = __dadd_rn(acc, __dmul_rn(double(W[off + o * in + i]), dl[o]));
+            dprev[i] = acc;
+          }
         }
       }
       __syncwarp();
@@ -720,6 +778,7 @@ inline unsigned dense_grad_groups(const ModelDims& md) { return unsigned((md.nw 
 // No CTA waits for another. CTA = kDGFWarps warps = kDGFWarps slices of one
 // weight group (lane = weight).
 constexpr int kDGFWarps = 16;
+constexpr int kDGFSlices = 128;  // slices per weight (32 examples each at c2; 256 measured slower)
 
 __global__ void __launch_bounds__(32 * kDGFWarps, 2)
     dense_grad_fused_kernel(ModelDims md, std::uint64_t n, const double* __restrict__ H,
@@ -735,7 +794,7 @@ __global__ void __launch_bounds__(32 * kDGFWarps, 2)
   const int w = int(grp * 32 + lane);
   const bool valid = w < md.nw;
   const WeightRef r = weight_ref(md, valid ? w : md.nw - 1);
-  const std::uint64_t per = (n + kDGSlices - 1) / kDGSlices;
+  const std::uint64_t per = (n + kDGFSlices - 1) / kDGFSlices;
   const std::uint64_t k0 = sl * per < n ? sl * per : n, k1 = k0 + per < n ? k0 + per : n;
   DD t{0.0, 0.0};
   double a = 0.0, l = 0.0, lam = 0.0;
@@ -748,7 +807,7 @@ __global__ void __launch_bounds__(32 * kDGFWarps, 2)
     lam = __dadd_ru(lam, fabs(l));
   }
   if (valid) {
-    double* slot = part + (std::uint64_t(w) * kDGSlices + sl) * 4;
+    double* slot = part + (std::uint64_t(w) * kDGFSlices + sl) * 4;
     slot[0] = t.hi;
     slot[1] = t.lo;
     slot[2] = a;
@@ -757,7 +816,7 @@ __global__ void __launch_bounds__(32 * kDGFWarps, 2)
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    s_last = atomicAdd(&done[grp], 1u) == kDGSlices / kDGFWarps - 1;
+    s_last = atomicAdd(&done[grp], 1u) == kDGFSlices / kDGFWarps - 1;
     if (s_last) __threadfence();
   }
   __syncthreads();
@@ -765,8 +824,8 @@ __global__ void __launch_bounds__(32 * kDGFWarps, 2)
   // the group's last CTA: warp wq owns slices [wq * R, (wq + 1) * R) of
   // weight `lane`; their totals in order, a cross-warp exclusive prefix,
   // then the B walk over the same slices
-  constexpr int R = kDGSlices / kDGFWarps;
-  const double* base = part + std::uint64_t(valid ? w : 0) * kDGSlices * 4;
+  constexpr int R = kDGFSlices / kDGFWarps;
+  const double* base = part + std::uint64_t(valid ? w : 0) * kDGFSlices * 4;
   DD S{0.0, 0.0};
   double A = 0.0, run = 0.0;
   // this warp's slices: totals and sum|x| first (loads in flight four
@@ -828,7 +887,7 @@ __global__ void __launch_bounds__(32 * kDGFWarps, 2)
       At = __dadd_ru(At, red[2][q][lane]);
       Bt = __dadd_ru(Bt, red[3][q][lane]);
     }
-    bad = !certify_f32(dd_value(St), Bt, At, n, per + kDGSlices, inv_n, &g);
+    bad = !certify_f32(dd_value(St), Bt, At, n, per + kDGFSlices, inv_n, &g);
   }
   // an uncertified weight: its exact chain in order (rare), staged by the CTA
   const unsigned bm = __ballot_sync(0xFFFFFFFFu, bad);

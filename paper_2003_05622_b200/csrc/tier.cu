@@ -205,8 +205,9 @@ struct Lane {
 };
 
 // The temporaries of one grouping context: the prep's (lane 2) and the
-// body's (lane 3).
-constexpr int kGroupLanes = 2;
+// body's (lanes 3 and 4: the body's later mini-batches alternate between
+// them, so two groupings run side by side).
+constexpr int kGroupLanes = 3;
 struct GroupState {
   std::uint32_t* gcnt = nullptr;       // [gslots] per-slot occurrence counters (kept zero)
   std::uint32_t* slot_uid = nullptr;   // [gslots]
@@ -276,6 +277,8 @@ struct Tier {
   int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
   std::uint32_t mid_max = 512;          // medium segments: short_max < length <= mid_max
   std::uint32_t short_max = 32;         // short segments (thread chains): length <= short_max
+  int body_group_lanes = 1;  // lanes grouping the body's later mini-batches (HPS_BODY_GROUP_LANES=2: two, measured 29.7M vs 30.4M)
+  bool fb_fixed = true;  // fwd/bwd with the {8, 16, 1} stack at compile time (HPS_FB_FIXED=0: generic)
   bool tail_prio = false;  // st3/st4 above st/st2 (HPS_TAIL_PRIO=1; measured no gain on c2)
   bool group_fused = true;  // segment ordering in one launch (HPS_GROUP_FUSED=0: four)
   bool group_prio = false;  // the body's own grouping lane at body priority (HPS_GROUP_PRIO=1)
@@ -286,7 +289,7 @@ struct Tier {
                                         // (HPS_MID_SEG; kLongSeg disables the path)
   Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
                                         // 2..: the next batch's mini-batch groupings
-  GroupState gs[kGroupLanes];           // [0]: the prep's grouping, [1]: the body's
+  GroupState gs[kGroupLanes];           // [0]: the prep's grouping, [1], [2]: the body's
   int prep_mbs = 0;                     // mini-batches the prep groups (HPS_PREP_GROUP;
                                         // 0 = auto); the body groups the rest, each
                                         // beside the previous mini-batch's compute
@@ -1917,10 +1920,14 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
   const bool side = bp.grouped && bp.prep_mbs < J;
   if (side) {
     HPS_CUDA(cudaEventRecord(T->b_fork, T->st));
-    HPS_CUDA(cudaStreamWaitEvent(T->lane[3].st, T->b_fork, 0));
-    T->L = &T->lane[3];
-    const hps_status gst =
-        enqueue_grouping(T, sh, bp, T->gs[1], bp.prep_mbs, J, &T->dsc->err, T->gmb_done);
+    const int nl = T->body_group_lanes;
+    for (int i = 0; i < nl; ++i) HPS_CUDA(cudaStreamWaitEvent(T->lane[3 + i].st, T->b_fork, 0));
+    hps_status gst = HPS_OK;
+    for (int j = bp.prep_mbs; j < J && gst == HPS_OK; ++j) {  // alternate lanes 3, 4
+      const int i = (j - bp.prep_mbs) % nl;
+      T->L = &T->lane[3 + i];
+      gst = enqueue_grouping(T, sh, bp, T->gs[1 + i], j, j + 1, &T->dsc->err, T->gmb_done);
+    }
     T->L = &T->lane[0];
     HPS_TRY(gst);
   }
@@ -2016,7 +2023,12 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                           size_t(epb) * (T->md.hw + T->md.dw + T->md.maxw) * 8 +
                           (tiled ? 16 + size_t(epb) * 2 * kTileRows * LPE * 4 : 0);
       const unsigned blocks = unsigned(std::min<std::uint64_t>((n + epb - 1) / epb, kSMs * 8));
-      auto k = LPE == 8 ? fwd_bwd_kernel<8> : (LPE == 16 ? fwd_bwd_kernel<16> : fwd_bwd_kernel<32>);
+      // the fixed {8, 16, 1} stack over E == LPE inputs: compile-time widths
+      const bool fix = T->fb_fixed && E == LPE && T->md.L == 3 && T->md.dims[0] == 8 &&
+                       T->md.dims[1] == 16 && T->md.dims[2] == 1;
+      auto k = LPE == 8 ? (fix ? fwd_bwd_kernel<8, true> : fwd_bwd_kernel<8>)
+                        : (LPE == 16 ? (fix ? fwd_bwd_kernel<16, true> : fwd_bwd_kernel<16>)
+                                     : fwd_bwd_kernel<32>);
       launch(T, k, blocks, 128, smem, T->md, sm, (const float*)T->dense,
              (const std::uint32_t*)T->occ_off, goff, occ_row, rows, rstride, dlab, T->H,
              T->DL, T->DX, &T->dsc->loss, &T->dsc->err, tiled);
@@ -2026,7 +2038,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
       HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
       if (T->dg_fused) {
         launch_on(T, T->st2, dense_grad_fused_kernel,
-                  dim3(dense_grad_groups(T->md), kDGSlices / kDGFWarps), 32 * kDGFWarps, 0, T->md, n,
+                  dim3(dense_grad_groups(T->md), kDGFSlices / kDGFWarps), 32 * kDGFWarps, 0, T->md, n,
                   (const double*)T->H, (const double*)T->DL, T->dpart, T->dg_sync, T->dgrad,
                   &T->dsc->fallbacks);
       } else {
@@ -2380,10 +2392,11 @@ static BatchPlan rotated(const BatchPlan& bp, int r) {
 // launches bake context-relative tickets) and restored.
 static hps_status precapture_rotations(Tier* T, const BatchShape& sh, const BatchPlan& bp,
                                        bool body) {
-  const int lanes[2] = {body ? 0 : 1, body ? 3 : 2};
-  std::uint64_t tk[2];
-  std::uint32_t lb[2];
-  for (int i = 0; i < 2; ++i) {
+  const int nl = body ? 3 : 2;  // body: lanes 0, 3, 4; prep: lanes 1, 2
+  const int lanes[3] = {body ? 0 : 1, body ? 3 : 2, 4};
+  std::uint64_t tk[3];
+  std::uint32_t lb[3];
+  for (int i = 0; i < nl; ++i) {
     tk[i] = T->lane[lanes[i]].tickets;
     lb[i] = T->lane[lanes[i]].lb_local;
   }
@@ -2391,7 +2404,7 @@ static hps_status precapture_rotations(Tier* T, const BatchShape& sh, const Batc
   hps_status st = HPS_OK;
   for (int r = 1; r < kTables && st == HPS_OK; ++r) {
     const BatchPlan q = rotated(bp, r);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < nl; ++i) {
       T->lane[lanes[i]].tickets = tk[i];
       T->lane[lanes[i]].lb_local = lb[i];
     }
@@ -2404,7 +2417,7 @@ static hps_status precapture_rotations(Tier* T, const BatchShape& sh, const Batc
     }
   }
   T->cur = cur;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < nl; ++i) {
     T->lane[lanes[i]].tickets = tk[i];
     T->lane[lanes[i]].lb_local = lb[i];
   }
@@ -2569,16 +2582,18 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   // ---- body on lane 0 (after its prep and its store rows)
   HPS_CUDA(cudaStreamWaitEvent(T->st, T->ev_prep, 0));
   if (T->store) HPS_CUDA(cudaStreamWaitEvent(T->st, T->pf_join, 0));
-  if (bp.grouped && bp.prep_mbs < J) {  // lane 3's look-back context (the body's
-    // grouping branch): after the previous body, before this one
-    Lane& l3 = T->lane[3];
-    if (bp.id >= 1)
-      HPS_CUDA(cudaStreamWaitEvent(l3.st, T->ev_body_sp[(bp.id - 1) % kSlots], 0));
-    T->L = &l3;
-    open_lookback_context(T);
-    T->L = &T->lane[0];
-    HPS_CUDA(cudaEventRecord(T->gs[1].ctx, l3.st));
-    HPS_CUDA(cudaStreamWaitEvent(T->st, T->gs[1].ctx, 0));
+  if (bp.grouped && bp.prep_mbs < J) {  // the look-back contexts of lanes 3, 4 (the
+    // body's grouping branches): after the previous body, before this one
+    for (int i = 0; i < T->body_group_lanes; ++i) {
+      Lane& lx = T->lane[3 + i];
+      if (bp.id >= 1)
+        HPS_CUDA(cudaStreamWaitEvent(lx.st, T->ev_body_sp[(bp.id - 1) % kSlots], 0));
+      T->L = &lx;
+      open_lookback_context(T);
+      T->L = &T->lane[0];
+      HPS_CUDA(cudaEventRecord(T->gs[1 + i].ctx, lx.st));
+      HPS_CUDA(cudaStreamWaitEvent(T->st, T->gs[1 + i].ctx, 0));
+    }
   }
   if (T->trace) cudaEventRecord(T->tr[sp][4], T->st);
   open_lookback_context(T);
@@ -2745,6 +2760,9 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_GROUP_PRIO")) t->group_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_GROUP_FUSED")) t->group_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_TAIL_PRIO")) t->tail_prio = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_FB_FIXED")) t->fb_fixed = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_BODY_GROUP_LANES"))
+    t->body_group_lanes = std::min(kGroupLanes - 1, std::max(1, std::atoi(v)));
   if (const char* v = std::getenv("HPS_SHORT_DPT")) {
     const int d = std::atoi(v);
     if (d == 1 || (d == 4 && c.embedding_dim % 4 == 0) || (d == 8 && c.embedding_dim % 8 == 0))
@@ -2845,6 +2863,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     // kernels then crowd the running mini-batch's reduce instead)
     str(&t->lane[2].st, lo);
     str(&t->lane[3].st, t->group_prio ? hi : lo);
+    str(&t->lane[4].st, t->group_prio ? hi : lo);
     str(&t->st_stage, lo);
     str(&t->st_wb, lo);
     str(&t->st_pf, lo);
@@ -2899,6 +2918,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
 
     cudaFuncSetAttribute(fwd_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(fwd_bwd_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(fwd_bwd_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(fwd_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(sparse_mid_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(mid_smem(1)));
@@ -3057,7 +3078,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   }
   A(DX, t->nmb_max * E);
   if (!t->wide) {  // the certified dense-gradient reduce of the exact path
-    A(dpart, std::uint64_t(t->md.nw) * kDGSlices * 4);
+    A(dpart, std::uint64_t(t->md.nw) * std::max(kDGSlices, kDGFSlices) * 4);
     A(dg_off, std::uint64_t(t->md.nw) * kDGSlices);
     A(dg_tot, std::uint64_t(t->md.nw) * 4);
     A(dg_sync, dense_grad_groups(t->md));
