@@ -207,7 +207,7 @@ struct Lane {
 // The temporaries of one grouping context: the prep's (lane 2) and the
 // body's (lanes 3 and 4: the body's later mini-batches alternate between
 // them, so two groupings run side by side).
-constexpr int kGroupLanes = 3;
+constexpr int kGroupLanes = 4;
 struct GroupState {
   std::uint32_t* gcnt = nullptr;       // [gslots] per-slot occurrence counters (kept zero)
   std::uint32_t* slot_uid = nullptr;   // [gslots]
@@ -253,6 +253,23 @@ __global__ void batch_out_kernel(const Scalars* __restrict__ d, int tb, int sp,
   o->err_prep = d->perr[tb];
 }
 
+// Zeroes up to kZeroRegions small device regions (u32 words) in ONE launch:
+// inside the captured graphs a memset node breaks the programmatic-launch
+// chain and costs ~5 us of dependency latency each; the CUPTI timeline
+// showed chains of 2-5 of them at the head of every mini-batch's reduce,
+// grouping and build.
+constexpr int kZeroRegions = 6;
+struct ZeroList {
+  std::uint32_t* p[kZeroRegions];
+  std::uint32_t n[kZeroRegions];  // words
+};
+__global__ void zero_kernel(ZeroList z) {
+  pdl_wait();
+#pragma unroll
+  for (int r = 0; r < kZeroRegions; ++r)
+    for (std::uint32_t i = threadIdx.x; i < z.n[r]; i += blockDim.x) z.p[r][i] = 0u;
+}
+
 // One sender's pushed (keys, deltas) awaiting hps_drain: a range of the
 // pending arena (Tier::pend_*), which grows by doubling and is reused.
 struct PendingChunk {
@@ -277,7 +294,8 @@ struct Tier {
   int short_dpt = 0;                    // sparse_short dims per thread (HPS_SHORT_DPT; 0 = auto)
   std::uint32_t mid_max = 512;          // medium segments: short_max < length <= mid_max
   std::uint32_t short_max = 32;         // short segments (thread chains): length <= short_max
-  int body_group_lanes = 1;  // lanes grouping the body's later mini-batches (HPS_BODY_GROUP_LANES=2: two, measured 29.7M vs 30.4M)
+  int prep_group_lanes = 2;  // lanes grouping the prep's mini-batches (HPS_PREP_GROUP_LANES)
+  int body_group_lanes = 2;  // lanes grouping the body's later mini-batches (HPS_BODY_GROUP_LANES)
   bool fb_fixed = true;  // fwd/bwd with the {8, 16, 1} stack at compile time (HPS_FB_FIXED=0: generic)
   bool tail_prio = false;  // st3/st4 above st/st2 (HPS_TAIL_PRIO=1; measured no gain on c2)
   bool group_fused = true;  // segment ordering in one launch (HPS_GROUP_FUSED=0: four)
@@ -289,7 +307,7 @@ struct Tier {
                                         // (HPS_MID_SEG; kLongSeg disables the path)
   Lane lane[2 + kGroupLanes];           // 0: main (body), 1: prep (build of the next batch),
                                         // 2..: the next batch's mini-batch groupings
-  GroupState gs[kGroupLanes];           // [0]: the prep's grouping, [1], [2]: the body's
+  GroupState gs[kGroupLanes];           // the prep's groupings first, then the body's
   int prep_mbs = 0;                     // mini-batches the prep groups (HPS_PREP_GROUP;
                                         // 0 = auto); the body groups the rest, each
                                         // beside the previous mini-batch's compute
@@ -1314,19 +1332,36 @@ static hps_status enqueue_wide(Tier* t, const ShardMap& sm, std::uint64_t n,
 // The big-segment path's preparation, on st3 beside fwd/bwd: list the keys
 // with segments over kLongSeg (big_classify_kernel), plan their (key, chunk)
 // items, reset the fused kernel's flags and ticket.
+// zero_kernel over (pointer, bytes) regions (bytes a multiple of 4) on s.
+static void zero_on(Tier* t, cudaStream_t s,
+                    std::initializer_list<std::pair<void*, std::size_t>> regions) {
+  ZeroList z{};
+  int r = 0;
+  for (const auto& pr : regions) {
+    z.p[r] = reinterpret_cast<std::uint32_t*>(pr.first);
+    z.n[r] = std::uint32_t(pr.second / 4);
+    ++r;
+  }
+  for (; r < kZeroRegions; ++r) {
+    z.p[r] = nullptr;
+    z.n[r] = 0;
+  }
+  launch_on(t, s, zero_kernel, 1, 128, 0, z);
+}
+
 static hps_status launch_big_plan(Tier* t, std::uint64_t u_upper, const std::uint64_t* U,
                                   const std::uint32_t* seg) {
   unsigned long long* nb = &t->dsc->n_big;
   cudaStream_t bs = t->big_side ? t->st3 : t->st;
-  HPS_CUDA(cudaMemsetAsync(nb, 0, 8, bs));
-  HPS_CUDA(cudaMemsetAsync(&t->dsc->n_mid, 0, 8, bs));
+  // the counters and the fused kernel's ticket (its previous use, the last
+  // mini-batch's big_fused_kernel, ran earlier on this stream)
+  zero_on(t, bs, {{nb, 8}, {&t->dsc->n_mid, 8}, {t->fuse_ticket, 8}});
   launch_on(t, bs, big_classify_kernel, grid_for(std::max<std::uint64_t>(u_upper, 1)), 256, 0,
             U, seg, t->big_list, nb, t->short_max, t->mid_max, t->mid_list, &t->dsc->n_mid);
   launch_on(t, bs, big_plan_kernel, 1, 1024, 0, fuse_chunk(t->E),
             (const std::uint32_t*)t->big_list, (const unsigned long long*)nb, seg, t->chunk_off,
             &t->dsc->n_items, t->item_key, t->item_chunk, &t->dsc->big_keys, &t->dsc->max_chunks,
             &t->dsc->big_occ);
-  HPS_CUDA(cudaMemsetAsync(t->fuse_ticket, 0, 8, bs));
   return HPS_OK;
 }
 
@@ -1529,8 +1564,7 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
     std::uint32_t* uids = T->g_uidb[tb] + r0;
     std::uint32_t* segocc = T->g_segocc[tb] + r0;  // (positions are per mini-batch)
     unsigned long long* U = &T->dsc->Ug[tb][j];
-    HPS_CUDA(cudaMemsetAsync(U, 0, 8, l.st));
-    HPS_CUDA(cudaMemsetAsync(g.gn, 0, 4 * sizeof(unsigned long long), l.st));
+    zero_on(T, l.st, {{U, 8}, {g.gn, 4 * sizeof(unsigned long long)}});
     if (!n) {
       if (mb_done) HPS_CUDA(cudaEventRecord(mb_done[j], l.st));
       continue;
@@ -1625,11 +1659,8 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
   std::uint64_t* cap = &T->dsc->cap[tb];
   DevError* perr = &T->dsc->perr[tb];
   mark(T, -1);
-  HPS_CUDA(cudaMemsetAsync(perr, 0, sizeof(DevError), l.st));
-  HPS_CUDA(cudaMemsetAsync(nws, 0, 8, l.st));
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->carried_tab[tb], 0, 8, l.st));
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->stored_tab[tb], 0, 8, l.st));
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->spec_fail, 0, 4, l.st));
+  zero_on(T, l.st, {{perr, sizeof(DevError)}, {nws, 8}, {&T->dsc->carried_tab[tb], 8},
+                    {&T->dsc->stored_tab[tb], 8}, {&T->dsc->spec_fail, 4}});
   const unsigned gk = prep_grid_of(T, grid_for(sh.batch_bound, 256, kSMs * 8));
   const std::uint64_t cap_bound = table_capacity(sh.own_bound);
   // speculative build at the previous table's capacity (a steady workload
@@ -1667,14 +1698,18 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
              (const std::uint64_t*)&T->dsc->rq_capv);
     }
     HPS_CUDA(cudaEventRecord(T->g_fork, l.st));
-    Lane& ln = T->lane[2];
-    HPS_CUDA(cudaStreamWaitEvent(ln.st, T->g_fork, 0));
-    T->L = &ln;
-    const hps_status st = enqueue_grouping(T, sh, bp, T->gs[0], 0, bp.prep_mbs, perr);
+    const int np = T->prep_group_lanes;  // lanes 2 .. 2 + np - 1, mini-batches alternating
+    for (int i = 0; i < np; ++i) HPS_CUDA(cudaStreamWaitEvent(T->lane[2 + i].st, T->g_fork, 0));
+    hps_status st = HPS_OK;
+    for (int j = 0; j < bp.prep_mbs && st == HPS_OK; ++j) {
+      T->L = &T->lane[2 + j % np];
+      st = enqueue_grouping(T, sh, bp, T->gs[j % np], j, j + 1, perr);
+    }
+    T->L = &T->lane[2];
     if (st == HPS_OK) mark(T, HPS_T_DEDUP);
     T->L = &l;
     HPS_TRY(st);
-    HPS_CUDA(cudaEventRecord(T->gs[0].join, ln.st));
+    for (int i = 0; i < np; ++i) HPS_CUDA(cudaEventRecord(T->gs[i].join, T->lane[2 + i].st));
   }
   // the distinct keys with their slots: compact the live slots (slot order),
   // then sort them by key (n_ws items, ~3x fewer than the occurrences) when
@@ -1718,7 +1753,9 @@ static hps_status enqueue_prep(Tier* T, const BatchShape& sh, const BatchPlan& b
     HPS_CUDA(cudaEventRecordWithFlags(
         T->pf_fork, l.st, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
   }
-  if (bp.grouped) HPS_CUDA(cudaStreamWaitEvent(l.st, T->gs[0].join, 0));
+  if (bp.grouped)
+    for (int i = 0; i < T->prep_group_lanes; ++i)
+      HPS_CUDA(cudaStreamWaitEvent(l.st, T->gs[i].join, 0));
   mark(T, HPS_T_BUILD);
   return HPS_OK;
 }
@@ -1903,9 +1940,9 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
   mark(T, -1);
   // the body's error word is this batch's from here (bodies run in order on
   // T->st; the previous one's was copied to its BatchOut already)
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->err, 0, sizeof(DevError), T->st));
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->loss, 0, 16, T->st));       // loss, pulled
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->fallbacks, 0, 48, T->st));  // fallbacks .. mid_keys
+  zero_on(T, T->st, {{&T->dsc->err, sizeof(DevError)},
+                     {&T->dsc->loss, 16},         // loss, pulled
+                     {&T->dsc->fallbacks, 48}});  // fallbacks .. mid_keys
   if (bp.tp >= 0) {  // rows from the resident tables (carry-over, proxies)
     const int RW = T->RW, V = vec_of(RW);
     const unsigned gc = grid_for(sh.own_bound * std::uint64_t(RW / V));
@@ -1920,13 +1957,14 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
   const bool side = bp.grouped && bp.prep_mbs < J;
   if (side) {
     HPS_CUDA(cudaEventRecord(T->b_fork, T->st));
-    const int nl = T->body_group_lanes;
-    for (int i = 0; i < nl; ++i) HPS_CUDA(cudaStreamWaitEvent(T->lane[3 + i].st, T->b_fork, 0));
+    const int nl = T->body_group_lanes, b0 = T->prep_group_lanes;  // lanes after the prep's
+    for (int i = 0; i < nl; ++i)
+      HPS_CUDA(cudaStreamWaitEvent(T->lane[2 + b0 + i].st, T->b_fork, 0));
     hps_status gst = HPS_OK;
-    for (int j = bp.prep_mbs; j < J && gst == HPS_OK; ++j) {  // alternate lanes 3, 4
+    for (int j = bp.prep_mbs; j < J && gst == HPS_OK; ++j) {  // alternating lanes
       const int i = (j - bp.prep_mbs) % nl;
-      T->L = &T->lane[3 + i];
-      gst = enqueue_grouping(T, sh, bp, T->gs[1 + i], j, j + 1, &T->dsc->err, T->gmb_done);
+      T->L = &T->lane[2 + b0 + i];
+      gst = enqueue_grouping(T, sh, bp, T->gs[b0 + i], j, j + 1, &T->dsc->err, T->gmb_done);
     }
     T->L = &T->lane[0];
     HPS_TRY(gst);
@@ -2392,10 +2430,15 @@ static BatchPlan rotated(const BatchPlan& bp, int r) {
 // launches bake context-relative tickets) and restored.
 static hps_status precapture_rotations(Tier* T, const BatchShape& sh, const BatchPlan& bp,
                                        bool body) {
-  const int nl = body ? 3 : 2;  // body: lanes 0, 3, 4; prep: lanes 1, 2
-  const int lanes[3] = {body ? 0 : 1, body ? 3 : 2, 4};
-  std::uint64_t tk[3];
-  std::uint32_t lb[3];
+  // body: lane 0 + its grouping lanes; prep: lane 1 + its grouping lanes
+  int lanes[1 + kGroupLanes];
+  int nl = 0;
+  lanes[nl++] = body ? 0 : 1;
+  const int g0 = body ? 2 + T->prep_group_lanes : 2;
+  const int gn = body ? T->body_group_lanes : T->prep_group_lanes;
+  for (int i = 0; i < gn; ++i) lanes[nl++] = g0 + i;
+  std::uint64_t tk[1 + kGroupLanes];
+  std::uint32_t lb[1 + kGroupLanes];
   for (int i = 0; i < nl; ++i) {
     tk[i] = T->lane[lanes[i]].tickets;
     lb[i] = T->lane[lanes[i]].lb_local;
@@ -2476,8 +2519,8 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     HPS_CUDA(cudaMemcpyAsync(T->b_keys[sp], keys, O * 8, cudaMemcpyHostToDevice, ss));
     HPS_CUDA(cudaMemcpyAsync(T->b_lab[sp], labels, B, cudaMemcpyHostToDevice, ss));
   }
-  HPS_CUDA(cudaMemsetAsync(T->dsc->counts[sp], 0, sizeof(T->dsc->counts[sp]), ss));
-  HPS_CUDA(cudaMemsetAsync(&T->dsc->serr[sp], 0, sizeof(DevError), ss));
+  zero_on(T, ss, {{T->dsc->counts[sp], sizeof(T->dsc->counts[sp])},
+                  {&T->dsc->serr[sp], sizeof(DevError)}});
   launch_on(T, ss, batch_count_kernel, kSMs * 4, 256, 0, (const std::int64_t*)T->b_off[sp],
             (const std::uint64_t*)T->b_keys[sp], B, G, T->g, J,
             T->cfg.key_space ? T->cfg.key_space : ~std::uint64_t(0), T->dsc->counts[sp],
@@ -2546,14 +2589,16 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     if (T->body_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tb], 0));
     if (T->wb_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_wb[bp.tb], 0));
     if (T->trace) cudaEventRecord(T->tr[sp][2], ps);
-    if (bp.grouped) {  // lane 2's look-back context: after the previous prep (whose
-      // graph ran lane 2's last grouping), before this one
-      Lane& ln = T->lane[2];
-      HPS_CUDA(cudaStreamWaitEvent(ln.st, T->ev_prep, 0));
-      T->L = &ln;
-      open_lookback_context(T);
-      HPS_CUDA(cudaEventRecord(T->gs[0].ctx, ln.st));
-      HPS_CUDA(cudaStreamWaitEvent(ps, T->gs[0].ctx, 0));
+    if (bp.grouped) {  // the prep grouping lanes' look-back contexts: after the
+      // previous prep (whose graph ran their last groupings), before this one
+      for (int i = 0; i < T->prep_group_lanes; ++i) {
+        Lane& ln = T->lane[2 + i];
+        HPS_CUDA(cudaStreamWaitEvent(ln.st, T->ev_prep, 0));
+        T->L = &ln;
+        open_lookback_context(T);
+        HPS_CUDA(cudaEventRecord(T->gs[i].ctx, ln.st));
+        HPS_CUDA(cudaStreamWaitEvent(ps, T->gs[i].ctx, 0));
+      }
     }
     T->L = &T->lane[1];
     open_lookback_context(T);
@@ -2585,14 +2630,14 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
   if (bp.grouped && bp.prep_mbs < J) {  // the look-back contexts of lanes 3, 4 (the
     // body's grouping branches): after the previous body, before this one
     for (int i = 0; i < T->body_group_lanes; ++i) {
-      Lane& lx = T->lane[3 + i];
+      Lane& lx = T->lane[2 + T->prep_group_lanes + i];
       if (bp.id >= 1)
         HPS_CUDA(cudaStreamWaitEvent(lx.st, T->ev_body_sp[(bp.id - 1) % kSlots], 0));
       T->L = &lx;
       open_lookback_context(T);
       T->L = &T->lane[0];
-      HPS_CUDA(cudaEventRecord(T->gs[1 + i].ctx, lx.st));
-      HPS_CUDA(cudaStreamWaitEvent(T->st, T->gs[1 + i].ctx, 0));
+      HPS_CUDA(cudaEventRecord(T->gs[T->prep_group_lanes + i].ctx, lx.st));
+      HPS_CUDA(cudaStreamWaitEvent(T->st, T->gs[T->prep_group_lanes + i].ctx, 0));
     }
   }
   if (T->trace) cudaEventRecord(T->tr[sp][4], T->st);
@@ -2761,8 +2806,10 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_GROUP_FUSED")) t->group_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_TAIL_PRIO")) t->tail_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_FB_FIXED")) t->fb_fixed = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_PREP_GROUP_LANES"))
+    t->prep_group_lanes = std::min(kGroupLanes - 1, std::max(1, std::atoi(v)));
   if (const char* v = std::getenv("HPS_BODY_GROUP_LANES"))
-    t->body_group_lanes = std::min(kGroupLanes - 1, std::max(1, std::atoi(v)));
+    t->body_group_lanes = std::min(kGroupLanes - t->prep_group_lanes, std::max(1, std::atoi(v)));
   if (const char* v = std::getenv("HPS_SHORT_DPT")) {
     const int d = std::atoi(v);
     if (d == 1 || (d == 4 && c.embedding_dim % 4 == 0) || (d == 8 && c.embedding_dim % 8 == 0))
@@ -2861,9 +2908,8 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
     // later mini-batches, which wait for it — at prep priority too: body
     // priority (HPS_GROUP_PRIO=1) measured 28.9M vs 30.0M ex/s on c2 (its
     // kernels then crowd the running mini-batch's reduce instead)
-    str(&t->lane[2].st, lo);
-    str(&t->lane[3].st, t->group_prio ? hi : lo);
-    str(&t->lane[4].st, t->group_prio ? hi : lo);
+    for (int i = 0; i < kGroupLanes; ++i)
+      str(&t->lane[2 + i].st, (t->group_prio && i >= t->prep_group_lanes) ? hi : lo);
     str(&t->st_stage, lo);
     str(&t->st_wb, lo);
     str(&t->st_pf, lo);
