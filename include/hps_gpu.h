@@ -241,6 +241,24 @@ hps_status hps_set_dense(hps_tier_t h, const float* w);
 hps_status hps_attach_store(hps_tier_t h, float* rows, uint64_t num_keys,
                             int on_device);
 
+/* Where the attached value store is trained (hps_store_mode):
+ * HPS_STORE_HOST_MIRRORED — a host store (on_device = 0) that fits the HBM
+ * budget (HPS_STORE_MIRROR_GB, default 32 GB; 180 GB per B200) is copied to
+ * HBM once at attach, the builds and write-backs use that copy, and the host
+ * array is made exact whenever it is observed (every entry point that
+ * quiesces: hps_flush, hps_destroy, hps_attach_store, hps_get_dense, ...),
+ * so the per-batch PCIe traffic is the batch alone. A bigger host store is
+ * staged per batch: zero-copy SM gathers/scatters (HPS_STORE_HOST_ZEROCOPY)
+ * or host threads + cudaMemcpyAsync (HPS_STAGE=dma, HPS_STORE_HOST_DMA). */
+enum {
+  HPS_STORE_NONE = 0,
+  HPS_STORE_DEVICE = 1,
+  HPS_STORE_HOST_ZEROCOPY = 2,
+  HPS_STORE_HOST_DMA = 3,
+  HPS_STORE_HOST_MIRRORED = 4
+};
+hps_status hps_store_mode(hps_tier_t h, int* mode);
+
 /* Write-back (the reference's collect stage, pipeline.hpp:462-474) runs
  * asynchronously beside the next batches. The four most recent batch tables
  * stay resident in HBM; a row reaches the store when its table is recycled

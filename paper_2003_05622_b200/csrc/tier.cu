@@ -426,6 +426,15 @@ struct Tier {
   float* store = nullptr;
   std::uint64_t store_keys = 0;
   bool store_on_host = false;
+  // host value store mirrored in HBM (HPS_STORE_MIRROR_GB, default 32: a
+  // store that fits is copied to the device once at attach, trained there,
+  // and copied back whenever the host observes it, i.e. at every quiesce
+  // after a write-back; bigger stores are staged per batch over PCIe)
+  float* mirror = nullptr;
+  float* mirror_host = nullptr;
+  std::uint64_t mirror_bytes = 0;
+  bool mirror_dirty = false;
+  double mirror_gb = 32.0;
   // zero-copy kernels on a host store run on a few SMs only: a PCIe access
   // stalls the memory pipeline of the SM issuing it for everyone on that SM
   unsigned pf_ctas = 8, wb_ctas = 4;
@@ -2147,6 +2156,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
 // is all the next builds read from it; hps_flush makes it exact for all keys.
 static hps_status enqueue_writeback(Tier* T, int t, const int* newer, int n_newer) {
   const int E = T->RW, V = vec_of(E);  // whole rows (embedding + optimizer state)
+  T->mirror_dirty = T->mirror != nullptr;  // the host copy is stale until the next quiesce
   HPS_CUDA(cudaStreamWaitEvent(T->st_wb, T->ev_body_tab[t], 0));
   if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[t][0], T->st_wb));
   const std::uint64_t* nk[3] = {nullptr, nullptr, nullptr};
@@ -2381,7 +2391,15 @@ static hps_status quiesce(Tier* T) {
     T->retired.clear();
   }
   HPS_TRY(flush_all(T));
-  return wb_fence(T);
+  HPS_TRY(wb_fence(T));
+  if (T->mirror && T->mirror_dirty) {  // the host store is observed: make it exact
+    HPS_CUDA(cudaStreamSynchronize(T->st_wb));
+    HPS_CUDA(cudaMemcpyAsync(T->mirror_host, T->mirror, T->mirror_bytes, cudaMemcpyDeviceToHost,
+                             T->st_wb));
+    HPS_CUDA(cudaStreamSynchronize(T->st_wb));
+    T->mirror_dirty = false;
+  }
+  return HPS_OK;
 }
 
 // Graph keys of a batch's prep and body: the shape plus the table / staging
@@ -2806,6 +2824,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_GROUP_FUSED")) t->group_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_TAIL_PRIO")) t->tail_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_FB_FIXED")) t->fb_fixed = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_STORE_MIRROR_GB")) t->mirror_gb = std::atof(v);
   if (const char* v = std::getenv("HPS_PREP_GROUP_LANES"))
     t->prep_group_lanes = std::min(kGroupLanes - 1, std::max(1, std::atoi(v)));
   if (const char* v = std::getenv("HPS_BODY_GROUP_LANES"))
@@ -3173,6 +3192,7 @@ hps_status hps_destroy(hps_tier_t t) {
   for (int gl = 0; gl < kGroupLanes; ++gl)
     if (t->lane[2 + gl].st) cudaStreamSynchronize(t->lane[2 + gl].st);
   if (t->comm) nccl().CommDestroy(t->comm);
+  if (t->mirror) cudaFree(t->mirror);
   cudaFree(t->pend_keys);
   cudaFree(t->pend_deltas);
   for (auto& kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -3612,6 +3632,15 @@ hps_status hps_flush(hps_tier_t t) {
   return HPS_OK;
 }
 
+hps_status hps_store_mode(hps_tier_t t, int* mode) {
+  if (!t || !mode) return set_error(HPS_ERR_ARG, "null argument");
+  *mode = !t->store ? HPS_STORE_NONE
+          : t->mirror ? HPS_STORE_HOST_MIRRORED
+          : !t->store_on_host ? HPS_STORE_DEVICE
+          : t->dma ? HPS_STORE_HOST_DMA : HPS_STORE_HOST_ZEROCOPY;
+  return HPS_OK;
+}
+
 hps_status hps_store_traffic(hps_tier_t t, uint64_t* rows_read, uint64_t* rows_written) {
   HPS_ENTER(t);
   HPS_CUDA(cudaMemcpyAsync(&t->hsc->wb_total, &t->dsc->wb_total, 8, cudaMemcpyDeviceToHost,
@@ -3637,7 +3666,32 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
   t->store_keys = 0;
   t->store_hptr = nullptr;
   t->dma = false;
+  if (t->mirror) {  // (hps_flush above copied it back)
+    cudaFree(t->mirror);
+    t->mirror = nullptr;
+    t->mirror_host = nullptr;
+    t->mirror_bytes = 0;
+    t->mirror_dirty = false;
+  }
   if (!rows || !num_keys) return HPS_OK;
+  const std::uint64_t sbytes = num_keys * std::uint64_t(t->RW) * 4;
+  std::size_t freeb = 0, totalb = 0;
+  cudaMemGetInfo(&freeb, &totalb);
+  if (!on_device && t->stage_mode != 1 && t->mirror_gb > 0 &&
+      double(sbytes) <= t->mirror_gb * 1e9 && sbytes + (std::uint64_t(4) << 30) < freeb) {
+    // the store fits in HBM: trained there, the host array exact when observed
+    void* d = nullptr;
+    if (cudaMalloc(&d, sbytes) == cudaSuccess) {
+      HPS_CUDA(cudaMemcpy(d, rows, sbytes, cudaMemcpyHostToDevice));
+      t->mirror = static_cast<float*>(d);
+      t->mirror_host = rows;
+      t->mirror_bytes = sbytes;
+      t->store = t->mirror;
+      t->store_keys = num_keys;
+      return HPS_OK;
+    }
+    cudaGetLastError();
+  }
   if (on_device) {
     t->store = rows;
   } else {

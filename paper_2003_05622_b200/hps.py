@@ -113,6 +113,7 @@ _SIGS = {
     "hps_set_dense": ([_P, _P], ctypes.c_int),
     "hps_attach_store": ([_P, _P, _U64, ctypes.c_int], ctypes.c_int),
     "hps_flush": ([_P], ctypes.c_int),
+    "hps_store_mode": ([_P, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "hps_store_traffic": ([_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)],
                           ctypes.c_int),
     "hps_train_batch": ([_P, _U64, _P, _P, _P, ctypes.c_int,
@@ -434,6 +435,15 @@ class Tier:
                 raise Error(7, "hbm: value store row width mismatch")
             _check(lib().hps_attach_store(self._h, _ptr(rows), rows.shape[0], 0))
             self._store = rows
+
+    STORE_MODES = {0: "none", 1: "device", 2: "host-zerocopy", 3: "host-dma",
+                   4: "host-mirrored"}
+
+    def store_mode(self) -> str:
+        """Where the attached store is trained (hps_store_mode)."""
+        m = ctypes.c_int()
+        _check(lib().hps_store_mode(self._h, ctypes.byref(m)))
+        return self.STORE_MODES[m.value]
 
     def store_traffic(self):
         """(rows read from, rows written to) the value store since creation."""

@@ -45,14 +45,16 @@ def max_segment(off, keys, B, J):
     return int(c.max())
 
 
-@pytest.mark.parametrize("store_kind", ["host", "device"])
-def test_config2_full_size_bit_exact(pkg, oracle, store_kind):
+@pytest.mark.parametrize("store_kind", ["host", "host-zerocopy", "device"])
+def test_config2_full_size_bit_exact(pkg, oracle, monkeypatch, store_kind):
     import torch
+    if store_kind == "host-zerocopy":  # staged per batch, not mirrored in HBM
+        monkeypatch.setenv("HPS_STORE_MIRROR_GB", "0")
     dims, E, B, nnz, J, layers, nb = 10**7, 16, 16384, 100, 4, (8, 16, 1), 3
     off, keys, lab = pkg.gen_dataset(dims, nb * B, nnz, zipf=True, seed=1)
     tier = pkg.Tier(width=E, layer_dims=layers, minibatches=J, key_space=dims,
                     max_batch_examples=B, max_batch_keys=max_keys_of(off, B))
-    if store_kind == "host":
+    if store_kind.startswith("host"):
         store = np.zeros((dims, E), dtype=np.float32)
         tier.attach_store(store)
     else:

@@ -212,21 +212,26 @@ def test_export_trained_table_as_reference_parameter_files(pkg, oracle, tmp_path
     assert info["fsck_ok"] == 1 and info["files"] == nf and info["live_records"] == want.size
 
 
-@pytest.mark.parametrize("store_kind", ["host", "device", "none"])
-def test_pipelined_submit_wait_bit_exact(pkg, oracle, store_kind):
+@pytest.mark.parametrize("store_kind", ["host", "host-zerocopy", "device", "none"])
+def test_pipelined_submit_wait_bit_exact(pkg, oracle, monkeypatch, store_kind):
     """hps_submit_batch / hps_wait_batch keep two batches in flight: the next
     batch's table is built (rows prefetched, from the table two builds back
     or the store) beside the running body, write-backs are deferred. Results
     must equal the oracle bit for bit, and equal hps_train_batch's, for a host
-    (zero-copy) store, an HBM store and no store (zeros for new rows)."""
+    store (mirrored in HBM, the default for a store that fits, or staged
+    per batch with zero-copy kernels), an HBM store and no store (zeros for
+    new rows)."""
     import torch
+    if store_kind == "host-zerocopy":
+        monkeypatch.setenv("HPS_STORE_MIRROR_GB", "0")
     dims, B, nnz, nb = 20000, 512, 20, 8
     off, keys, lab = pkg.gen_dataset(dims, B * nb, nnz, zipf=True, seed=33)
     tier = pkg.Tier(width=8, layer_dims=(8, 16, 1), minibatches=4, key_space=dims,
                     max_batch_examples=B, max_batch_keys=B * nnz)
-    if store_kind == "host":
+    if store_kind.startswith("host"):
         store = np.zeros((dims, 8), dtype=np.float32)
         tier.attach_store(store)
+        assert tier.store_mode() == ("host-mirrored" if store_kind == "host" else "host-zerocopy")
     elif store_kind == "device":
         dstore = torch.zeros((dims, 8), dtype=torch.float32, device="cuda")
         tier.attach_store(dstore.data_ptr(), on_device=True, num_keys=dims)

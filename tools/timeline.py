@@ -32,6 +32,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=12)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "timeline.json"))
+    ap.add_argument("--host", action="store_true",
+                    help="the e2e path: pinned host batches and a pinned host value store")
     args = ap.parse_args()
     c = bench.CONFIGS[args.config]
     dims, E, B, J = c["dims"], c["E"], c["B"], c["J"]
@@ -45,14 +47,24 @@ def main() -> None:
     dev = torch.device("cuda:0")
     tier = pkg.Tier(width=E, layer_dims=c["layers"], minibatches=J, key_space=dims,
                     max_batch_examples=B, max_batch_keys=max_keys, optimizer=c.get("opt", "sgd"))
-    dbatches = [(torch.from_numpy(o).to(dev), torch.from_numpy(k.view(np.int64)).to(dev),
-                 torch.from_numpy(l).to(dev)) for o, k, l in batches]
-    dstore = torch.zeros((dims, tier.row_width), dtype=torch.float32, device=dev)
-    tier.attach_store(dstore.data_ptr(), on_device=True, num_keys=dims)
+    if args.host:
+        hstore_t = torch.zeros((dims, tier.row_width), dtype=torch.float32).pin_memory()
+        tier.attach_store(hstore_t.numpy())
+        hb = [tuple(torch.from_numpy(x).pin_memory().numpy() for x in (o, k.view(np.int64), l))
+              for o, k, l in batches]
 
-    def step(b):
-        o, k, l = dbatches[b % P]
-        tier.submit_batch((o.data_ptr(), B), k.data_ptr(), l.data_ptr(), on_device=True)
+        def step(b):
+            o, k, l = hb[b % P]
+            tier.submit_batch(o, k.view(np.uint64), l, on_device=False)
+    else:
+        dbatches = [(torch.from_numpy(o).to(dev), torch.from_numpy(k.view(np.int64)).to(dev),
+                     torch.from_numpy(l).to(dev)) for o, k, l in batches]
+        dstore = torch.zeros((dims, tier.row_width), dtype=torch.float32, device=dev)
+        tier.attach_store(dstore.data_ptr(), on_device=True, num_keys=dims)
+
+        def step(b):
+            o, k, l = dbatches[b % P]
+            tier.submit_batch((o.data_ptr(), B), k.data_ptr(), l.data_ptr(), on_device=True)
 
     lag = 3
     n = 0
