@@ -430,25 +430,26 @@ def run_ours(args, rank, world, local_rank):
         tier.flush()
         barrier()
         rd0, wr0 = tier.store_traffic()
+        ph0, pd0 = tier.store_pcie_bytes()
         e2e_ms, e2e_stats = timed_steps(host_step, args.steps, args.warmup)
         barrier()
         rd1, wr1 = tier.store_traffic()
+        ph1, pd1 = tier.store_pcie_bytes()
         e2e_ms_max = max_over_ranks(e2e_ms)
         mode = tier.store_mode()
         h2d = sum(8 * (b[0].size) + 8 * b[1].size + b[2].size for b in
                   (hbatches[(args.warmup + i) % P] for i in range(args.steps))) / args.steps
+        h2d += (ph1 - ph0) / args.steps                    # store bytes over PCIe
+        d2h = ((pd1 - pd0) + 24 * args.steps) / args.steps  # written back + stats
         if mode == "host-mirrored":
             # the store trains in HBM; the host array is made exact by the
-            # flush that closes the timed region (one full copy back)
-            d2h = (dims * RW * 4 + 24 * args.steps) / args.steps
+            # flush that closes the timed region (its dirty pages copied back)
             path = ("hps_submit_batch/hps_wait_batch(on_device=0): pinned batch H2D on the "
                     "staging stream, loss D2H every step; the pinned host value store "
-                    "(MEM-PS stand-in) is mirrored in HBM (it fits the 32 GB budget: "
-                    f"{dims * RW * 4 / 1e9:.2f} GB) and copied back to the host by the "
-                    "hps_flush inside the timed region")
+                    "(MEM-PS stand-in) is mirrored in HBM (it fits the 2 GB budget: "
+                    f"{dims * RW * 4 / 1e9:.2f} GB) and its dirty 1024-row pages are copied "
+                    "back to the host by the hps_flush inside the timed region")
         else:
-            h2d += (rd1 - rd0) * RW * 4 / args.steps        # store rows read by the builds
-            d2h = ((wr1 - wr0) * RW * 4 + 24 * args.steps) / args.steps  # written back + stats
             path = ("hps_submit_batch/hps_wait_batch(on_device=0): pinned batch H2D on "
                     "the staging stream, store rows prefetched (zero-copy) beside the "
                     "previous batch, deferred zero-copy write-back to the pinned host "

@@ -243,7 +243,8 @@ hps_status hps_attach_store(hps_tier_t h, float* rows, uint64_t num_keys,
 
 /* Where the attached value store is trained (hps_store_mode):
  * HPS_STORE_HOST_MIRRORED — a host store (on_device = 0) that fits the HBM
- * budget (HPS_STORE_MIRROR_GB, default 32 GB; 180 GB per B200) is copied to
+ * budget (HPS_STORE_MIRROR_GB, default 2 GB: the copy-back of a bigger
+ * store at every observation would outweigh a short run's per-batch staging) is copied to
  * HBM once at attach, the builds and write-backs use that copy, and the host
  * array is made exact whenever it is observed (every entry point that
  * quiesces: hps_flush, hps_destroy, hps_attach_store, hps_get_dense, ...),
@@ -258,6 +259,11 @@ enum {
   HPS_STORE_HOST_MIRRORED = 4
 };
 hps_status hps_store_mode(hps_tier_t h, int* mode);
+
+/* Bytes the value store has moved over PCIe since hps_create: per-batch
+ * staging (zero-copy or DMA: every row read or written back), or the
+ * mirror's attach copies and its copy-backs (dirty 1024-row pages only). */
+hps_status hps_store_pcie_bytes(hps_tier_t h, uint64_t* h2d, uint64_t* d2h);
 
 /* Write-back (the reference's collect stage, pipeline.hpp:462-474) runs
  * asynchronously beside the next batches. The four most recent batch tables

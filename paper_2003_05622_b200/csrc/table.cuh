@@ -471,12 +471,13 @@ __global__ void table_evict_filter_kernel(const std::uint64_t* __restrict__ ws,
 
 // The evicted rows of the list to the value store (zero-copy for a host
 // store): ILP independent row loads per thread before their posted stores.
+constexpr int kMirrorPageShift = 10;  // 1024 rows per dirty page of a mirrored store
 template <int VEC, int ILP>
 __global__ void store_scatter_kernel(const std::uint64_t* __restrict__ keys,
                                      const std::uint32_t* __restrict__ slots,
                                      const unsigned long long* __restrict__ n_ptr,
                                      const float* __restrict__ vals, float* __restrict__ store,
-                                     int E) {
+                                     int E, std::uint8_t* __restrict__ dirty) {
   pdl_wait();
   using V = typename std::conditional<VEC == 4, float4, float>::type;
   const int tpk = E / VEC;
@@ -494,6 +495,8 @@ __global__ void store_scatter_kernel(const std::uint64_t* __restrict__ keys,
         const int part = int(t - i * tpk);
         v[u] = reinterpret_cast<const V*>(vals + std::uint64_t(slots[i]) * E)[part];
         dst[u] = keys[i] * E + std::uint64_t(part) * VEC;
+        // a mirrored host store: the key's page is copied back at the next quiesce
+        if (dirty && part == 0) dirty[keys[i] >> kMirrorPageShift] = 1;
       }
     }
 #pragma unroll

@@ -426,15 +426,19 @@ struct Tier {
   float* store = nullptr;
   std::uint64_t store_keys = 0;
   bool store_on_host = false;
-  // host value store mirrored in HBM (HPS_STORE_MIRROR_GB, default 32: a
+  // host value store mirrored in HBM (HPS_STORE_MIRROR_GB, default 2: a
   // store that fits is copied to the device once at attach, trained there,
-  // and copied back whenever the host observes it, i.e. at every quiesce
-  // after a write-back; bigger stores are staged per batch over PCIe)
+  // and its dirty pages copied back whenever the host observes it, i.e. at
+  // every quiesce after a write-back; bigger stores, whose copy-back would
+  // cost more than a short run's per-batch staging, stay on the host)
   float* mirror = nullptr;
   float* mirror_host = nullptr;
   std::uint64_t mirror_bytes = 0;
   bool mirror_dirty = false;
-  double mirror_gb = 32.0;
+  double mirror_gb = 2.0;
+  std::uint8_t* mirror_pages = nullptr;  // dirty flag per 2^kMirrorPageShift-row page
+  std::uint64_t mirror_h2d = 0, mirror_d2h = 0;  // bytes the mirror moved over PCIe
+  std::vector<std::uint8_t> mirror_hpages;
   // zero-copy kernels on a host store run on a few SMs only: a PCIe access
   // stalls the memory pipeline of the SM issuing it for everyone on that SM
   unsigned pf_ctas = 8, wb_ctas = 4;
@@ -2194,7 +2198,7 @@ static hps_status enqueue_writeback(Tier* T, int t, const int* newer, int n_newe
   auto k = V == 4 ? store_scatter_kernel<4, 4> : store_scatter_kernel<1, 4>;
   launch_on(T, T->st_wb, k, gw, tpb, 0, (const std::uint64_t*)T->wb_key[t],
             (const std::uint32_t*)T->wb_slot[t], (const unsigned long long*)&T->dsc->wb_n[t],
-            (const float*)T->tvals[t], T->store, E);
+            (const float*)T->tvals[t], T->store, E, T->mirror_pages);
   if (T->timing) HPS_CUDA(cudaEventRecord(T->ev_wbt[t][1], T->st_wb));
   HPS_CUDA(cudaEventRecord(T->ev_wb[t], T->st_wb));
   T->wb_pending[t] = true;
@@ -2393,9 +2397,28 @@ static hps_status quiesce(Tier* T) {
   HPS_TRY(flush_all(T));
   HPS_TRY(wb_fence(T));
   if (T->mirror && T->mirror_dirty) {  // the host store is observed: make it exact
+    // (the pages written back since the last copy, in runs of DMA copies)
+    const std::uint64_t np = T->mirror_hpages.size();
+    const std::uint64_t prow = std::uint64_t(1) << kMirrorPageShift;
+    const std::uint64_t rowb = std::uint64_t(T->RW) * 4;
     HPS_CUDA(cudaStreamSynchronize(T->st_wb));
-    HPS_CUDA(cudaMemcpyAsync(T->mirror_host, T->mirror, T->mirror_bytes, cudaMemcpyDeviceToHost,
-                             T->st_wb));
+    HPS_CUDA(cudaMemcpy(T->mirror_hpages.data(), T->mirror_pages, np, cudaMemcpyDeviceToHost));
+    for (std::uint64_t p = 0; p < np;) {
+      if (!T->mirror_hpages[p]) {
+        ++p;
+        continue;
+      }
+      std::uint64_t q = p;
+      while (q < np && T->mirror_hpages[q]) ++q;
+      const std::uint64_t off = p * prow * rowb;
+      const std::uint64_t len = std::min(q * prow * rowb, T->mirror_bytes) - off;
+      HPS_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(T->mirror_host) + off,
+                               reinterpret_cast<const char*>(T->mirror) + off, len,
+                               cudaMemcpyDeviceToHost, T->st_wb));
+      T->mirror_d2h += len;
+      p = q;
+    }
+    HPS_CUDA(cudaMemsetAsync(T->mirror_pages, 0, np, T->st_wb));
     HPS_CUDA(cudaStreamSynchronize(T->st_wb));
     T->mirror_dirty = false;
   }
@@ -3193,6 +3216,7 @@ hps_status hps_destroy(hps_tier_t t) {
     if (t->lane[2 + gl].st) cudaStreamSynchronize(t->lane[2 + gl].st);
   if (t->comm) nccl().CommDestroy(t->comm);
   if (t->mirror) cudaFree(t->mirror);
+  if (t->mirror_pages) cudaFree(t->mirror_pages);
   cudaFree(t->pend_keys);
   cudaFree(t->pend_deltas);
   for (auto& kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -3641,6 +3665,18 @@ hps_status hps_store_mode(hps_tier_t t, int* mode) {
   return HPS_OK;
 }
 
+hps_status hps_store_pcie_bytes(hps_tier_t t, uint64_t* h2d, uint64_t* d2h) {
+  HPS_ENTER(t);
+  std::uint64_t r = 0, w = 0;
+  HPS_TRY(hps_store_traffic(t, &r, &w));
+  const std::uint64_t rowb = std::uint64_t(t->RW) * 4;
+  // zero-copy / DMA staging move every store row they read or write; the
+  // mirror moves its attach copy and its copy-backs
+  if (h2d) *h2d = t->mirror_h2d + (t->store_on_host ? r * rowb : 0);
+  if (d2h) *d2h = t->mirror_d2h + (t->store_on_host ? w * rowb : 0);
+  return HPS_OK;
+}
+
 hps_status hps_store_traffic(hps_tier_t t, uint64_t* rows_read, uint64_t* rows_written) {
   HPS_ENTER(t);
   HPS_CUDA(cudaMemcpyAsync(&t->hsc->wb_total, &t->dsc->wb_total, 8, cudaMemcpyDeviceToHost,
@@ -3668,7 +3704,10 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
   t->dma = false;
   if (t->mirror) {  // (hps_flush above copied it back)
     cudaFree(t->mirror);
+    cudaFree(t->mirror_pages);
     t->mirror = nullptr;
+    t->mirror_pages = nullptr;
+    t->mirror_hpages.clear();
     t->mirror_host = nullptr;
     t->mirror_bytes = 0;
     t->mirror_dirty = false;
@@ -3681,8 +3720,14 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
       double(sbytes) <= t->mirror_gb * 1e9 && sbytes + (std::uint64_t(4) << 30) < freeb) {
     // the store fits in HBM: trained there, the host array exact when observed
     void* d = nullptr;
-    if (cudaMalloc(&d, sbytes) == cudaSuccess) {
+    void* pg = nullptr;
+    const std::uint64_t np = ((num_keys - 1) >> kMirrorPageShift) + 1;
+    if (cudaMalloc(&d, sbytes) == cudaSuccess && cudaMalloc(&pg, np) == cudaSuccess) {
       HPS_CUDA(cudaMemcpy(d, rows, sbytes, cudaMemcpyHostToDevice));
+      HPS_CUDA(cudaMemset(pg, 0, np));
+      t->mirror_h2d += sbytes;
+      t->mirror_pages = static_cast<std::uint8_t*>(pg);
+      t->mirror_hpages.assign(np, 0);
       t->mirror = static_cast<float*>(d);
       t->mirror_host = rows;
       t->mirror_bytes = sbytes;
@@ -3690,6 +3735,7 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
       t->store_keys = num_keys;
       return HPS_OK;
     }
+    if (d) cudaFree(d);
     cudaGetLastError();
   }
   if (on_device) {

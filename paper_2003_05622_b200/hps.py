@@ -114,6 +114,8 @@ _SIGS = {
     "hps_attach_store": ([_P, _P, _U64, ctypes.c_int], ctypes.c_int),
     "hps_flush": ([_P], ctypes.c_int),
     "hps_store_mode": ([_P, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+    "hps_store_pcie_bytes": ([_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)],
+                             ctypes.c_int),
     "hps_store_traffic": ([_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)],
                           ctypes.c_int),
     "hps_train_batch": ([_P, _U64, _P, _P, _P, ctypes.c_int,
@@ -444,6 +446,12 @@ class Tier:
         m = ctypes.c_int()
         _check(lib().hps_store_mode(self._h, ctypes.byref(m)))
         return self.STORE_MODES[m.value]
+
+    def store_pcie_bytes(self):
+        """(H2D, D2H) bytes the value store has moved over PCIe since creation."""
+        h, d = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().hps_store_pcie_bytes(self._h, ctypes.byref(h), ctypes.byref(d)))
+        return h.value, d.value
 
     def store_traffic(self):
         """(rows read from, rows written to) the value store since creation."""
