@@ -41,6 +41,7 @@ constexpr int kGroupShort = 8;      // segments ordered in registers by one thre
 constexpr int kGroupThreads = 1024;
 constexpr int kGroupPosGroups = 64;  // warps sharing one 32-example group
 constexpr int kGroupWarpThreads = 256;  // group_warp_kernel: one warp per segment
+constexpr int kGroupSortThreads = 512;  // group_sort_kernel (a block per huge segment)
 constexpr int kGroupWarpMax = 256;      // longer segments: one CTA each (group_cta_kernel)
 constexpr int kGroupParts = 32;         // uid claim counters (contention / kGroupParts)
 constexpr int kGroupPartStride = 32;    // u32 words between counters (one 128-B line each)
@@ -528,7 +529,7 @@ __device__ __forceinline__ void rank_by_count(std::uint32_t p0, std::uint32_t p1
   }
 }
 
-__global__ void __launch_bounds__(kGroupWarpThreads)
+__global__ void __launch_bounds__(kGroupSortThreads)
     group_sort_kernel(const unsigned long long* __restrict__ n_uid,
                       const std::uint32_t* __restrict__ seg,
                       const std::uint32_t* __restrict__ seg_occ,
@@ -540,10 +541,10 @@ __global__ void __launch_bounds__(kGroupWarpThreads)
                       const std::uint32_t* __restrict__ huge_list) {
   pdl_wait();
   extern __shared__ std::uint32_t gsort_sm[];  // per warp: bitmap[words], prefix[words]
-  __shared__ std::uint32_t wsum[kGroupWarpThreads / 32];
+  __shared__ std::uint32_t wsum[kGroupSortThreads / 32];
   __shared__ int s_dup;
   const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr unsigned kWarps = kGroupWarpThreads / 32;
+  constexpr unsigned kWarps = kGroupSortThreads / 32;
   // ---- short segments: one thread each, in registers
   const std::uint64_t U = *n_uid;
   for (std::uint64_t u = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; u < U;
@@ -629,9 +630,15 @@ __global__ void __launch_bounds__(kGroupWarpThreads)
     constexpr int R = kGroupWarpMax / 32;
     std::uint32_t* bm = gsort_sm + std::size_t(warp) * 2 * words;
     std::uint32_t* pre = bm + words;
+    // the blocks that ordered a huge segment take no long ones (they are the
+    // grid's tail); the rest share them
     const std::uint64_t NL = *n_long;
-    const std::uint64_t nwarps = std::uint64_t(gridDim.x) * kWarps;
-    for (std::uint64_t li = std::uint64_t(blockIdx.x) * kWarps + warp; li < NL; li += nwarps) {
+    const std::uint64_t NH0 = *n_huge, gl = std::uint64_t(gridDim.x) - 1;
+    const std::uint64_t NHb = NH0 < gl ? NH0 : gl;
+    if (blockIdx.x < NHb) return;
+    const std::uint64_t nwarps = (std::uint64_t(gridDim.x) - NHb) * kWarps;
+    for (std::uint64_t li = (std::uint64_t(blockIdx.x) - NHb) * kWarps + warp; li < NL;
+         li += nwarps) {
       const std::uint32_t u = long_list[li];
       const std::uint32_t p0 = seg[u], p1 = seg[u + 1];
       std::uint32_t ev[R];

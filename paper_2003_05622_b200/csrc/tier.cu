@@ -1604,7 +1604,8 @@ static hps_status enqueue_grouping(Tier* T, const BatchShape& sh, const BatchPla
              (const std::uint32_t*)g.slot_uid, pcap, (const std::uint32_t*)g.part_base,
              (const std::uint32_t*)seg, segocc, G == 1 ? nullptr : T->g_inv[tb], g.gcnt, g.part_n,
              g.g_long, &g.gn[0], g.g_huge, &g.gn[2]);
-      launch(T, group_sort_kernel, kSMs * 4, kGroupWarpThreads, wsmem,
+      launch(T, group_sort_kernel, kSMs * 2, kGroupSortThreads,
+             std::size_t(kGroupSortThreads / 32) * 2 * words * 4,
              (const unsigned long long*)U, (const std::uint32_t*)seg, (const std::uint32_t*)segocc,
              (const std::uint32_t*)T->g_exof[tb], words, exs,
              (const unsigned long long*)&g.gn[0], (const std::uint32_t*)g.g_long,
@@ -2607,7 +2608,7 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
     const std::uint64_t nmax = (B + std::uint64_t(G) * J - 1) / (std::uint64_t(G) * J);
     const std::size_t words = std::size_t((nmax + 31) / 32);
     bp.grouped = T->hash_dedup &&
-                 std::size_t(kGroupWarpThreads / 32) * 8 * words <= kGroupSmemMax;
+                 std::size_t(kGroupSortThreads / 32) * 8 * words <= kGroupSmemMax;
     // who groups what: with a host store the prep is short next to the PCIe
     // traffic and takes every mini-batch; with an HBM store the body takes
     // the later half beside its compute (c2: 0.80 vs 0.85 ms/step; with a host
