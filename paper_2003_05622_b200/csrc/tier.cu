@@ -297,6 +297,7 @@ struct Tier {
   int prep_group_lanes = 2;  // lanes grouping the prep's mini-batches (HPS_PREP_GROUP_LANES)
   int body_group_lanes = 2;  // lanes grouping the body's later mini-batches (HPS_BODY_GROUP_LANES)
   bool fb_fixed = true;  // fwd/bwd with the {8, 16, 1} stack at compile time (HPS_FB_FIXED=0: generic)
+  unsigned short_grid = 8 * kSMs;  // block cap of sparse_short_kernel (HPS_SHORT_GRID; 0: kSMs * 32)
   bool tail_prio = false;  // st3/st4 above st/st2 (HPS_TAIL_PRIO=1; measured no gain on c2)
   bool group_fused = true;  // segment ordering in one launch (HPS_GROUP_FUSED=0: four)
   bool group_prio = false;  // the body's own grouping lane at body priority (HPS_GROUP_PRIO=1)
@@ -1430,8 +1431,13 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   const int dpt = t->short_dpt ? t->short_dpt : ((E % 4 == 0) ? 4 : 1);
   auto sk = dpt == 8 ? sparse_short_kernel<8>
                      : (dpt == 4 ? sparse_short_kernel<4> : sparse_short_kernel<1>);
-  launch(t, sk, grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256, kSMs * 32), 256, 0,
-         E, t->short_max, n, U, seg, exs, dout, DX, &t->dsc->pulled);
+  // grid-stride over the keys, capped (HPS_SHORT_GRID) so the medium / hot-key
+  // reduces and the dense gradient, forked at the same point, find SM slots
+  // at once instead of after this kernel's last wave
+  launch(t, sk,
+         grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256,
+                  t->short_grid ? t->short_grid : kSMs * 32),
+         256, 0, E, t->short_max, n, U, seg, exs, dout, DX, &t->dsc->pulled);
   HPS_CUDA(cudaStreamWaitEvent(t->st, t->join3, 0));
   if (t->big_side) HPS_CUDA(cudaStreamWaitEvent(t->st, t->join4, 0));
   return HPS_OK;
@@ -2847,6 +2853,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_GROUP_PRIO")) t->group_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_GROUP_FUSED")) t->group_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_TAIL_PRIO")) t->tail_prio = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_SHORT_GRID")) t->short_grid = unsigned(std::max(0, std::atoi(v)));
   if (const char* v = std::getenv("HPS_FB_FIXED")) t->fb_fixed = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_STORE_MIRROR_GB")) t->mirror_gb = std::atof(v);
   if (const char* v = std::getenv("HPS_PREP_GROUP_LANES"))
