@@ -298,6 +298,7 @@ struct Tier {
   int body_group_lanes = 2;  // lanes grouping the body's later mini-batches (HPS_BODY_GROUP_LANES)
   bool fb_fixed = true;  // fwd/bwd with the {8, 16, 1} stack at compile time (HPS_FB_FIXED=0: generic)
   unsigned short_grid = 8 * kSMs;  // block cap of sparse_short_kernel (HPS_SHORT_GRID; 0: kSMs * 32)
+  bool dg_main = false;  // dense gradient on the body stream, short keys on st2 (HPS_DG_MAIN)
   bool tail_prio = false;  // st3/st4 above st/st2 (HPS_TAIL_PRIO=1; measured no gain on c2)
   bool group_fused = true;  // segment ordering in one launch (HPS_GROUP_FUSED=0: four)
   bool group_prio = false;  // the body's own grouping lane at body priority (HPS_GROUP_PRIO=1)
@@ -1385,7 +1386,8 @@ static hps_status launch_big_plan(Tier* t, std::uint64_t u_upper, const std::uin
 static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint32_t* pos,
                                       std::uint64_t u_upper, const std::uint64_t* U,
                                       const std::uint32_t* seg, const std::uint32_t* exs,
-                                      const std::uint32_t* apply_slot = nullptr) {
+                                      const std::uint32_t* apply_slot = nullptr,
+                                      bool short_side = false) {
   // apply_slot non-null (one rank, the keys' table slots known): the deltas
   // go straight into the current table, no delta rows and no apply launch
   const DeltaOut dout{t->deltas, pos, apply_slot, apply_slot ? t->tvals[t->cur] : nullptr,
@@ -1434,10 +1436,15 @@ static hps_status launch_sparse_delta(Tier* t, std::uint64_t n, const std::uint3
   // grid-stride over the keys, capped (HPS_SHORT_GRID) so the medium / hot-key
   // reduces and the dense gradient, forked at the same point, find SM slots
   // at once instead of after this kernel's last wave
-  launch(t, sk,
-         grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256,
-                  t->short_grid ? t->short_grid : kSMs * 32),
-         256, 0, E, t->short_max, n, U, seg, exs, dout, DX, &t->dsc->pulled);
+  const unsigned sg = grid_for(std::max<std::uint64_t>(u_upper, 1) * (E / dpt), 256,
+                               t->short_grid ? t->short_grid : kSMs * 32);
+  if (short_side) {  // (the caller keeps st for the dense gradient and joins all)
+    launch_on(t, t->st2, sk, sg, 256, 0, E, t->short_max, n, U, seg, exs, dout, DX,
+              &t->dsc->pulled);
+    HPS_CUDA(cudaEventRecord(t->join, t->st2));
+    return HPS_OK;
+  }
+  launch(t, sk, sg, 256, 0, E, t->short_max, n, U, seg, exs, dout, DX, &t->dsc->pulled);
   HPS_CUDA(cudaStreamWaitEvent(t->st, t->join3, 0));
   if (t->big_side) HPS_CUDA(cudaStreamWaitEvent(t->st, t->join4, 0));
   return HPS_OK;
@@ -2091,6 +2098,26 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
              (const std::uint32_t*)T->occ_off, goff, occ_row, rows, rstride, dlab, T->H,
              T->DL, T->DX, &T->dsc->loss, &T->dsc->err, tiled);
       mark(T, HPS_T_FWDBWD);
+      }
+      if (!T->wide && T->dg_main && T->dg_fused && T->big_side) {
+        // the dense gradient follows fwd/bwd on the body stream (programmatic
+        // launch: no cross-branch start latency), the three sparse passes
+        // fork onto st2 (short), st3 (hot keys) and st4 (medium keys)
+        HPS_CUDA(cudaEventRecord(T->fork, T->st));
+        HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
+        HPS_CUDA(cudaStreamWaitEvent(T->st3, T->fork, 0));
+        HPS_TRY(launch_sparse_delta(T, n, plan.pos, ob, Uj, segj, exsj,
+                                    bp.grouped && G == 1 ? slotsj : nullptr, true));
+        launch(T, dense_grad_fused_kernel,
+               dim3(dense_grad_groups(T->md), kDGFSlices / kDGFWarps), 32 * kDGFWarps, 0, T->md,
+               n, (const double*)T->H, (const double*)T->DL, T->dpart, T->dg_sync, T->dgrad,
+               &T->dsc->fallbacks);
+        HPS_CUDA(cudaStreamWaitEvent(T->st, T->join3, 0));
+        HPS_CUDA(cudaStreamWaitEvent(T->st, T->join4, 0));
+        HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
+        mark(T, HPS_T_SPARSE);
+      } else {
+      if (!T->wide) {
       // dense-grad reduce on the side stream, overlapping the sparse reduce
       HPS_CUDA(cudaEventRecord(T->fork, T->st));
       HPS_CUDA(cudaStreamWaitEvent(T->st2, T->fork, 0));
@@ -2119,6 +2146,7 @@ static hps_status enqueue_body(Tier* T, const BatchShape& sh, const BatchPlan& b
                                   bp.grouped && G == 1 ? slotsj : nullptr));
       mark(T, HPS_T_SPARSE);
       HPS_CUDA(cudaStreamWaitEvent(T->st, T->join, 0));
+      }
     } else {
       HPS_CUDA(cudaMemsetAsync(T->dgrad, 0, std::uint64_t(T->md.nw) * 4, T->st));
     }
@@ -2853,6 +2881,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_GROUP_PRIO")) t->group_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_GROUP_FUSED")) t->group_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_TAIL_PRIO")) t->tail_prio = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_DG_MAIN")) t->dg_main = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_SHORT_GRID")) t->short_grid = unsigned(std::max(0, std::atoi(v)));
   if (const char* v = std::getenv("HPS_FB_FIXED")) t->fb_fixed = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_STORE_MIRROR_GB")) t->mirror_gb = std::atof(v);
