@@ -3753,8 +3753,14 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
   const std::uint64_t sbytes = num_keys * std::uint64_t(t->RW) * 4;
   std::size_t freeb = 0, totalb = 0;
   cudaMemGetInfo(&freeb, &totalb);
-  if (!on_device && t->stage_mode != 1 && t->mirror_gb > 0 &&
-      double(sbytes) <= t->mirror_gb * 1e9 && sbytes + (std::uint64_t(4) << 30) < freeb) {
+  // mirror when the store is small (the budget) or no bigger than 16 batches'
+  // worst-case staging (then a run of ~16+ batches moves less over PCIe with
+  // the one copy back than with per-batch staging; c3's 51 GB Adagrad store
+  // vs its 3.3 GB working set), and it fits in HBM beside the tables
+  const double wsb = double(t->Wmax) * double(t->RW) * 4.0;
+  const bool worth = double(sbytes) <= t->mirror_gb * 1e9 || double(sbytes) <= 16.0 * wsb;
+  if (!on_device && t->stage_mode != 1 && t->mirror_gb > 0 && worth &&
+      sbytes + (std::uint64_t(4) << 30) < freeb) {
     // the store fits in HBM: trained there, the host array exact when observed
     void* d = nullptr;
     void* pg = nullptr;
