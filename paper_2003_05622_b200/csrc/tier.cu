@@ -3759,7 +3759,9 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
   // vs its 3.3 GB working set), and it fits in HBM beside the tables
   const double wsb = double(t->Wmax) * double(t->RW) * 4.0;
   const bool worth = double(sbytes) <= t->mirror_gb * 1e9 || double(sbytes) <= 16.0 * wsb;
-  if (!on_device && t->stage_mode != 1 && t->mirror_gb > 0 && worth &&
+  // one rank only: at G > 1 the ranks may share one host array, each writing
+  // back the rows it owns, and a page copy-back would overwrite the others'
+  if (t->G == 1 && !on_device && t->stage_mode != 1 && t->mirror_gb > 0 && worth &&
       sbytes + (std::uint64_t(4) << 30) < freeb) {
     // the store fits in HBM: trained there, the host array exact when observed
     void* d = nullptr;
