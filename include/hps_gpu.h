@@ -243,14 +243,14 @@ hps_status hps_attach_store(hps_tier_t h, float* rows, uint64_t num_keys,
 
 /* Where the attached value store is trained (hps_store_mode):
  * HPS_STORE_HOST_MIRRORED — a host store (on_device = 0) that fits the HBM
- * budget at one rank (at N*D > 1 the ranks may share the host array and
- * each writes back only its own rows) (HPS_STORE_MIRROR_GB, default 2 GB, or
+ * budget (HPS_STORE_MIRROR_GB, default 2 GB, or
  * up to 16 batches of worst-case staging; the copy-back of a bigger
  * store at every observation would outweigh a short run's per-batch staging) is copied to
  * HBM once at attach, the builds and write-backs use that copy, and the host
  * array is made exact whenever it is observed (every entry point that
  * quiesces: hps_flush, hps_destroy, hps_attach_store, hps_get_dense, ...),
- * so the per-batch PCIe traffic is the batch alone. A bigger host store is
+ * so the per-batch PCIe traffic is the batch alone. At N*D > 1 (ranks may
+ * share one host array) the copy-back writes only the rows this rank owns. A bigger host store is
  * staged per batch: zero-copy SM gathers/scatters (HPS_STORE_HOST_ZEROCOPY)
  * or host threads + cudaMemcpyAsync (HPS_STAGE=dma, HPS_STORE_HOST_DMA). */
 enum {

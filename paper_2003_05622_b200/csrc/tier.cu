@@ -270,6 +270,24 @@ __global__ void zero_kernel(ZeroList z) {
     for (std::uint32_t i = threadIdx.x; i < z.n[r]; i += blockDim.x) z.p[r][i] = 0u;
 }
 
+// Copy-back of a mirrored store at G > 1: the rows this rank owns (key % G
+// == g) in the dirty pages, straight into the mapped host array (the ranks
+// may share it; each writes only its own rows, as the per-batch write-back
+// does).
+__global__ void mirror_owned_copyback_kernel(const float4* __restrict__ mirror,
+                                             float4* __restrict__ host,
+                                             const std::uint8_t* __restrict__ pages,
+                                             std::uint64_t num_keys, int rw4, int G, int g) {
+  pdl_wait();
+  const std::uint64_t total = num_keys * std::uint64_t(rw4);
+  for (std::uint64_t t = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint64_t key = t / std::uint64_t(rw4);
+    if (key % std::uint64_t(G) != std::uint64_t(g) || !pages[key >> 10]) continue;
+    host[t] = mirror[t];
+  }
+}
+
 // One sender's pushed (keys, deltas) awaiting hps_drain: a range of the
 // pending arena (Tier::pend_*), which grows by doubling and is reused.
 struct PendingChunk {
@@ -441,6 +459,8 @@ struct Tier {
   std::uint8_t* mirror_pages = nullptr;  // dirty flag per 2^kMirrorPageShift-row page
   std::uint64_t mirror_h2d = 0, mirror_d2h = 0;  // bytes the mirror moved over PCIe
   std::vector<std::uint8_t> mirror_hpages;
+  float* mirror_hmapped = nullptr;  // G > 1: the host array's device mapping (owned-row copy-back)
+  bool mirror_registered = false;
   // zero-copy kernels on a host store run on a few SMs only: a PCIe access
   // stalls the memory pipeline of the SM issuing it for everyone on that SM
   unsigned pf_ctas = 8, wb_ctas = 4;
@@ -2437,6 +2457,19 @@ static hps_status quiesce(Tier* T) {
     const std::uint64_t prow = std::uint64_t(1) << kMirrorPageShift;
     const std::uint64_t rowb = std::uint64_t(T->RW) * 4;
     HPS_CUDA(cudaStreamSynchronize(T->st_wb));
+    if (T->G > 1) {  // this rank's rows only, zero-copy writes (the array may be shared)
+      const int rw4 = T->RW / 4;
+      const std::uint64_t keys = T->mirror_bytes / rowb;
+      launch_on(T, T->st_wb, mirror_owned_copyback_kernel, kSMs * 4, 512, 0,
+                reinterpret_cast<const float4*>(T->mirror),
+                reinterpret_cast<float4*>(T->mirror_hmapped),
+                (const std::uint8_t*)T->mirror_pages, keys, rw4, T->G, T->g);
+      T->mirror_d2h += keys / std::uint64_t(T->G) * rowb;  // (at most)
+      HPS_CUDA(cudaMemsetAsync(T->mirror_pages, 0, np, T->st_wb));
+      HPS_CUDA(cudaStreamSynchronize(T->st_wb));
+      T->mirror_dirty = false;
+      return HPS_OK;
+    }
     HPS_CUDA(cudaMemcpy(T->mirror_hpages.data(), T->mirror_pages, np, cudaMemcpyDeviceToHost));
     for (std::uint64_t p = 0; p < np;) {
       if (!T->mirror_hpages[p]) {
@@ -3254,6 +3287,7 @@ hps_status hps_destroy(hps_tier_t t) {
   if (t->comm) nccl().CommDestroy(t->comm);
   if (t->mirror) cudaFree(t->mirror);
   if (t->mirror_pages) cudaFree(t->mirror_pages);
+  if (t->mirror_registered) cudaHostUnregister(t->mirror_host);
   cudaFree(t->pend_keys);
   cudaFree(t->pend_deltas);
   for (auto& kv : t->graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -3742,6 +3776,9 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
   if (t->mirror) {  // (hps_flush above copied it back)
     cudaFree(t->mirror);
     cudaFree(t->mirror_pages);
+    if (t->mirror_registered) cudaHostUnregister(t->mirror_host);
+    t->mirror_registered = false;
+    t->mirror_hmapped = nullptr;
     t->mirror = nullptr;
     t->mirror_pages = nullptr;
     t->mirror_hpages.clear();
@@ -3759,14 +3796,27 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
   // vs its 3.3 GB working set), and it fits in HBM beside the tables
   const double wsb = double(t->Wmax) * double(t->RW) * 4.0;
   const bool worth = double(sbytes) <= t->mirror_gb * 1e9 || double(sbytes) <= 16.0 * wsb;
-  // one rank only: at G > 1 the ranks may share one host array, each writing
-  // back the rows it owns, and a page copy-back would overwrite the others'
-  if (t->G == 1 && !on_device && t->stage_mode != 1 && t->mirror_gb > 0 && worth &&
-      sbytes + (std::uint64_t(4) << 30) < freeb) {
+  // at G > 1 the ranks may share one host array: the copy-back then writes
+  // only this rank's rows, through the array's device mapping (float4 rows)
+  if ((t->G == 1 || t->RW % 4 == 0) && !on_device && t->stage_mode != 1 && t->mirror_gb > 0 &&
+      worth && sbytes + (std::uint64_t(4) << 30) < freeb) {
     // the store fits in HBM: trained there, the host array exact when observed
     void* d = nullptr;
     void* pg = nullptr;
     const std::uint64_t np = ((num_keys - 1) >> kMirrorPageShift) + 1;
+    if (t->G > 1) {
+      cudaPointerAttributes at{};
+      const bool pinned = cudaPointerGetAttributes(&at, rows) == cudaSuccess &&
+                          at.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+      if (!pinned) {
+        HPS_CUDA(cudaHostRegister(rows, sbytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+        t->mirror_registered = true;
+      }
+      void* dp = nullptr;
+      HPS_CUDA(cudaHostGetDevicePointer(&dp, rows, 0));
+      t->mirror_hmapped = static_cast<float*>(dp);
+    }
     if (cudaMalloc(&d, sbytes) == cudaSuccess && cudaMalloc(&pg, np) == cudaSuccess) {
       HPS_CUDA(cudaMemcpy(d, rows, sbytes, cudaMemcpyHostToDevice));
       HPS_CUDA(cudaMemset(pg, 0, np));
@@ -3781,6 +3831,9 @@ hps_status hps_attach_store(hps_tier_t t, float* rows, uint64_t num_keys, int on
       return HPS_OK;
     }
     if (d) cudaFree(d);
+    if (t->mirror_registered) cudaHostUnregister(rows);
+    t->mirror_registered = false;
+    t->mirror_hmapped = nullptr;
     cudaGetLastError();
   }
   if (on_device) {

@@ -173,6 +173,11 @@ def main():
                                           1024, 9, 30)
     results["train_pipelined"] = case_train(world, rank, oracle, 16, (8, 16, 1), 4, True, 50000,
                                             1024, 9, 30, pipelined=True)
+    # the host store staged per batch (zero-copy) instead of mirrored in HBM
+    os.environ["HPS_STORE_MIRROR_GB"] = "0"
+    results["train_pipelined_zerocopy"] = case_train(world, rank, oracle, 16, (8, 16, 1), 4, True,
+                                                     50000, 1024, 5, 30, pipelined=True)
+    del os.environ["HPS_STORE_MIRROR_GB"]
     results["train_hbm_store"] = case_train(world, rank, oracle, 8, (8, 16, 1), 4, True, 30000,
                                             1024, 7, 24, pipelined=True, hbm_store=True)
     # Adagrad state in the rows: owners apply each sender's gradient in
