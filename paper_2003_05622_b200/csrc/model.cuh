@@ -133,9 +133,6 @@ __device__ __forceinline__ bool embed_sum_exact(const std::uint32_t* __restrict_
 // in-order f64 chain of dimension d from shared memory — one LDS, one
 // conversion and one DADD per feature instead of a shuffle, an address and a
 // predicated scalar load per (feature, lane).
-#ifndef HPS_FB_MINB
-#define HPS_FB_MINB 1
-#endif
 constexpr int kTileRows = 32;
 template <int LPE>
 __host__ __device__ constexpr int embed_tile_floats() { return 2 * kTileRows * LPE; }
@@ -236,11 +233,10 @@ __device__ __forceinline__ void layer_bwd_fixed(const float* W, const double* dl
 // <= 32); each example's scratch lives in shared memory. Writes the H and DL
 // records (for the dense-gradient reduction), DX = dL/dx (for the sparse
 // segment reduction) and accumulates the log loss (model.hpp:232-242).
-// (HPS_FB_MINB, compile time: a register cap through the minimum blocks per
-// SM; 5 blocks (96 registers, a little spill) measured 30.2M vs 35.3M ex/s
-// on c2, so no cap)
+// (No minimum-blocks register cap: 5 blocks per SM (96 registers, a little
+// spill) measured 30.2M vs 35.3M ex/s on c2.)
 template <int LPE, bool FIX = false>
-__global__ void __launch_bounds__(128, LPE == 32 ? 1 : HPS_FB_MINB)
+__global__ void __launch_bounds__(128)
     fwd_bwd_kernel(ModelDims md, ShardMap sm, const float* __restrict__ dense,
                    const std::uint32_t* __restrict__ occ_off,
                    const std::int64_t* __restrict__ goff,  // non-null: occurrence = batch index
