@@ -316,6 +316,7 @@ struct Tier {
   int body_group_lanes = 2;  // lanes grouping the body's later mini-batches (HPS_BODY_GROUP_LANES)
   bool fb_fixed = true;  // fwd/bwd with the {8, 16, 1} stack at compile time (HPS_FB_FIXED=0: generic)
   unsigned short_grid = 8 * kSMs;  // block cap of sparse_short_kernel (HPS_SHORT_GRID; 0: kSMs * 32)
+  bool prep_lag1 = false;  // the build waits for the previous body's carry (HPS_PREP_LAG=1)
   bool dg_main = false;  // dense gradient on the body stream, short keys on st2 (HPS_DG_MAIN)
   bool tail_prio = false;  // st3/st4 above st/st2 (HPS_TAIL_PRIO=1; measured no gain on c2)
   bool group_fused = true;  // segment ordering in one launch (HPS_GROUP_FUSED=0: four)
@@ -2695,6 +2696,10 @@ static hps_status submit_batch(Tier* T, std::uint64_t B, const std::int64_t* off
       const int sp2 = int((bp.id - 2) % kSlots);
       HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_carry_sp[sp2], 0));
     }
+    // HPS_PREP_LAG=1: the build also waits for the previous body's carry, so
+    // it does not crowd that body's start (the batch boundary)
+    if (T->prep_lag1 && bp.id >= 1)
+      HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_carry_sp[(bp.id - 1) % kSlots], 0));
     if (T->body_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_body_tab[bp.tb], 0));
     if (T->wb_pending[bp.tb]) HPS_CUDA(cudaStreamWaitEvent(ps, T->ev_wb[bp.tb], 0));
     if (T->trace) cudaEventRecord(T->tr[sp][2], ps);
@@ -2915,6 +2920,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_GROUP_FUSED")) t->group_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_TAIL_PRIO")) t->tail_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_DG_MAIN")) t->dg_main = std::atoi(v) != 0;
+  if (const char* v = std::getenv("HPS_PREP_LAG")) t->prep_lag1 = std::atoi(v) == 1;
   if (const char* v = std::getenv("HPS_SHORT_GRID")) t->short_grid = unsigned(std::max(0, std::atoi(v)));
   if (const char* v = std::getenv("HPS_FB_FIXED")) t->fb_fixed = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_STORE_MIRROR_GB")) t->mirror_gb = std::atof(v);
