@@ -314,6 +314,19 @@ class HbmTier {
     check(hps_store_traffic(h_, &r, &w));
     return {r, w};
   }
+  // where the attached store trains: HPS_STORE_HOST_MIRRORED (copied to
+  // HBM, exact on the host at every observation) or per-batch staging
+  int store_mode() const {
+    int m = 0;
+    check(hps_store_mode(h_, &m));
+    return m;
+  }
+  // (H2D, D2H) bytes the store has moved over PCIe
+  std::pair<std::uint64_t, std::uint64_t> store_pcie_bytes() const {
+    std::uint64_t h = 0, d = 0;
+    check(hps_store_pcie_bytes(h_, &h, &d));
+    return {h, d};
+  }
   std::vector<float> dense() const {
     std::uint64_t n = 0;
     check(hps_dense_count(h_, &n));
