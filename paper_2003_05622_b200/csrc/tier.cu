@@ -316,6 +316,7 @@ struct Tier {
   int body_group_lanes = 2;  // lanes grouping the body's later mini-batches (HPS_BODY_GROUP_LANES)
   bool fb_fixed = true;  // fwd/bwd with the {8, 16, 1} stack at compile time (HPS_FB_FIXED=0: generic)
   unsigned short_grid = 8 * kSMs;  // block cap of sparse_short_kernel (HPS_SHORT_GRID; 0: kSMs * 32)
+  int prog_edges = 1;  // programmatic graph edges: 1 fwd/bwd -> side reduces, 2 all kernel->kernel (HPS_PROG_EDGES)
   bool prep_lag1 = false;  // the build waits for the previous body's carry (HPS_PREP_LAG=1)
   bool dg_main = false;  // dense gradient on the body stream, short keys on st2 (HPS_DG_MAIN)
   bool tail_prio = false;  // st3/st4 above st/st2 (HPS_TAIL_PRIO=1; measured no gain on c2)
@@ -2312,6 +2313,59 @@ static hps_status wb_fence(Tier* T, int p = -1, cudaStream_t s = nullptr) {
 // a whole prep or body becomes one graph. The cache keeps the 256 most
 // recently used graphs; an evicted one may still be running (batches are in
 // flight), so it is destroyed only at the next quiesce.
+// HPS_PROG_EDGES=1: in a captured body graph, the edges from fwd/bwd to the
+// reduces that other streams run after it (dense gradient, medium and
+// hot-key segments) become programmatic edges, as the same-stream launches
+// already are: those kernels may launch as fwd/bwd's blocks retire and wait
+// for its results in griddepcontrol.wait (pdl_wait, their first statement),
+// instead of paying a cross-stream launch after its completion.
+static bool is_fwd_bwd(const void* f) {
+  return f == reinterpret_cast<const void*>(fwd_bwd_kernel<8>) ||
+         f == reinterpret_cast<const void*>(fwd_bwd_kernel<16>) ||
+         f == reinterpret_cast<const void*>(fwd_bwd_kernel<32>) ||
+         f == reinterpret_cast<const void*>(fwd_bwd_kernel<8, true>) ||
+         f == reinterpret_cast<const void*>(fwd_bwd_kernel<16, true>);
+}
+static bool is_side_reduce(const void* f) {
+  return f == reinterpret_cast<const void*>(dense_grad_fused_kernel) ||
+         f == reinterpret_cast<const void*>(big_fused_kernel) ||
+         f == reinterpret_cast<const void*>(sparse_mid_cert_kernel<4>) ||
+         f == reinterpret_cast<const void*>(sparse_mid_cert_kernel<8>) ||
+         f == reinterpret_cast<const void*>(sparse_mid_cert_kernel<16>) ||
+         f == reinterpret_cast<const void*>(sparse_mid_cert_kernel<32>);
+}
+static const void* kernel_of(cudaGraphNode_t n) {
+  cudaGraphNodeType ty;
+  if (cudaGraphNodeGetType(n, &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) return nullptr;
+  cudaKernelNodeParams p{};
+  if (cudaGraphKernelNodeGetParams(n, &p) != cudaSuccess) return nullptr;
+  return p.func;
+}
+static hps_status programmatic_side_edges(cudaGraph_t g, bool all) {
+  std::size_t ne = 0;
+  HPS_CUDA(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
+  if (!ne) return HPS_OK;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> ed(ne);
+  HPS_CUDA(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne));
+  for (std::size_t i = 0; i < ne; ++i) {
+    if (ed[i].type != cudaGraphDependencyTypeDefault) continue;
+    const void* kf = kernel_of(from[i]);
+    const void* kt = kernel_of(to[i]);
+    if (!kf || !kt) continue;  // memset / copy / event nodes keep full edges
+    // all: every kernel -> kernel edge (every kernel here opens with pdl_wait,
+    // and a programmatic port fires only once all of the upstream kernel's
+    // blocks have exited, so no early block can starve it of SMs)
+    if (!all && !(is_fwd_bwd(kf) && is_side_reduce(kt))) continue;
+    HPS_CUDA(cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &ed[i], 1));
+    cudaGraphEdgeData pe{};
+    pe.from_port = cudaGraphKernelNodePortProgrammatic;
+    pe.type = cudaGraphDependencyTypeProgrammatic;
+    HPS_CUDA(cudaGraphAddDependencies_v2(g, &from[i], &to[i], &pe, 1));
+  }
+  return HPS_OK;
+}
+
 template <class Fn>
 static hps_status capture_graph(Tier* T, const std::vector<std::uint64_t>& key, Fn&& enqueue,
                                 GraphEntry** out) {
@@ -2338,6 +2392,7 @@ static hps_status capture_graph(Tier* T, const std::vector<std::uint64_t>& key, 
     }
     if (ce != cudaSuccess)
       return set_error(HPS_ERR_CUDA, "cuda: graph capture: %s", cudaGetErrorString(ce));
+    if (T->prog_edges) HPS_TRY(programmatic_side_edges(g, T->prog_edges >= 2));
     // node priorities follow the capturing stream (body high, prep low)
     const cudaError_t ie =
         cudaGraphInstantiate(&ge.exec, g, cudaGraphInstantiateFlagUseNodePriority);
@@ -2921,6 +2976,7 @@ hps_status hps_create(const hps_config* cfg, const uint8_t* nccl_id, hps_tier_t*
   if (const char* v = std::getenv("HPS_TAIL_PRIO")) t->tail_prio = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_DG_MAIN")) t->dg_main = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_PREP_LAG")) t->prep_lag1 = std::atoi(v) == 1;
+  if (const char* v = std::getenv("HPS_PROG_EDGES")) t->prog_edges = std::atoi(v);
   if (const char* v = std::getenv("HPS_SHORT_GRID")) t->short_grid = unsigned(std::max(0, std::atoi(v)));
   if (const char* v = std::getenv("HPS_FB_FIXED")) t->fb_fixed = std::atoi(v) != 0;
   if (const char* v = std::getenv("HPS_STORE_MIRROR_GB")) t->mirror_gb = std::atof(v);
