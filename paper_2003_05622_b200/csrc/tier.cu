@@ -317,7 +317,8 @@ struct Tier {
   bool fb_fixed = true;  // fwd/bwd with the {8, 16, 1} stack at compile time (HPS_FB_FIXED=0: generic)
   unsigned short_grid = 8 * kSMs;  // block cap of sparse_short_kernel (HPS_SHORT_GRID; 0: kSMs * 32)
   int prog_edges = 1;  // programmatic graph edges: 1 fwd/bwd -> side reduces, 2 all kernel->kernel,
-                       // 3 also side reduces -> dense update (HPS_PROG_EDGES)
+                       // 3 also side reduces -> dense update, 4 every kernel edge into a side
+                       // reduce (HPS_PROG_EDGES)
   bool prep_lag1 = false;  // the build waits for the previous body's carry (HPS_PREP_LAG=1)
   bool dg_main = false;  // dense gradient on the body stream, short keys on st2 (HPS_DG_MAIN)
   bool tail_prio = false;  // st3/st4 above st/st2 (HPS_TAIL_PRIO=1; measured no gain on c2)
@@ -2342,7 +2343,8 @@ static const void* kernel_of(cudaGraphNode_t n) {
   if (cudaGraphKernelNodeGetParams(n, &p) != cudaSuccess) return nullptr;
   return p.func;
 }
-static hps_status programmatic_side_edges(cudaGraph_t g, bool all, bool join_edges) {
+static hps_status programmatic_side_edges(cudaGraph_t g, bool all, bool join_edges,
+                                          bool any_into_side) {
   std::size_t ne = 0;
   HPS_CUDA(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
   if (!ne) return HPS_OK;
@@ -2357,7 +2359,8 @@ static hps_status programmatic_side_edges(cudaGraph_t g, bool all, bool join_edg
     // all: every kernel -> kernel edge (every kernel here opens with pdl_wait,
     // and a programmatic port fires only once all of the upstream kernel's
     // blocks have exited, so no early block can starve it of SMs)
-    const bool side_in = is_fwd_bwd(kf) && is_side_reduce(kt);
+    // mode 4: every kernel edge into a side reduce (also big_plan -> medium keys)
+    const bool side_in = (is_fwd_bwd(kf) || any_into_side) && is_side_reduce(kt);
     // mode 3 adds the joins: the side reduces -> the dense update after them
     const bool side_out = join_edges && is_side_reduce(kf) &&
                           kt == reinterpret_cast<const void*>(dense_update_kernel);
@@ -2398,7 +2401,8 @@ static hps_status capture_graph(Tier* T, const std::vector<std::uint64_t>& key, 
     if (ce != cudaSuccess)
       return set_error(HPS_ERR_CUDA, "cuda: graph capture: %s", cudaGetErrorString(ce));
     if (T->prog_edges)
-      HPS_TRY(programmatic_side_edges(g, T->prog_edges == 2, T->prog_edges == 3));
+      HPS_TRY(programmatic_side_edges(g, T->prog_edges == 2, T->prog_edges == 3,
+                                      T->prog_edges == 4));
     // node priorities follow the capturing stream (body high, prep low)
     const cudaError_t ie =
         cudaGraphInstantiate(&ge.exec, g, cudaGraphInstantiateFlagUseNodePriority);
